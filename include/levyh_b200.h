@@ -1,0 +1,146 @@
+/*
+ * levyh_b200.h -- C ABI of the B200-native Crank-Nicolson H-matrix hot path.
+ *
+ * Drop-in boundary for the reference package `levyh` (arxiv 1812.08324,
+ * /root/reference/pkg/src/levyh).  Each entry point names the reference
+ * function it replaces (file:line).  Plain pointers and sizes only: `*_dev`
+ * arguments are CUDA device pointers (fp64 unless noted), `*_host` arguments
+ * are host pointers.  Every call is ordered on the context's CUDA stream.
+ *
+ * Status codes map onto the reference's exception types:
+ *   LH_EINVAL    -> ValueError            (hops.py:68-69, hmatrix.py:315-318, ...)
+ *   LH_ESINGULAR -> numpy.linalg.LinAlgError, message carries the block path
+ *                   ("zero pivot in dense diagonal leaf at root.11.22", hops.py:395-396)
+ *   LH_ETYPE     -> TypeError             (hops.py:62, :401)
+ * The message of the last failure is returned by lh_ctx_last_error().
+ */
+#ifndef LEVYH_B200_H
+#define LEVYH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    LH_OK = 0,
+    LH_EINVAL = 1,
+    LH_ESINGULAR = 2,
+    LH_ETYPE = 3,
+    LH_ECUDA = 4,
+    LH_ENOMEM = 5,
+    LH_ERANK = 6,     /* rank capacity / ACA max-rank exceeded */
+    LH_EINTERNAL = 7
+};
+
+typedef struct lh_ctx lh_ctx;
+typedef struct lh_tree lh_tree;
+typedef struct lh_hmat lh_hmat;
+
+/* ---- context --------------------------------------------------------- */
+int lh_ctx_create(int device, void *cuda_stream, lh_ctx **out);
+void lh_ctx_destroy(lh_ctx *ctx);
+const char *lh_ctx_last_error(const lh_ctx *ctx);
+int lh_ctx_synchronize(lh_ctx *ctx);
+int lh_version(void);
+
+/* ---- cluster tree: geometry.py:191-243 build_cluster_tree (bisection) -- */
+int lh_tree_build(lh_ctx *ctx, const double *pts_host, int64_t n, int dim, int leaf_size,
+                  lh_tree **out);
+void lh_tree_destroy(lh_tree *t);
+int64_t lh_tree_num_nodes(const lh_tree *t);
+/* lohi[2*i], lohi[2*i+1] = start, end; bbox[(2*i)*dim ...] lo then hi; kids[2*i..] (-1 = leaf) */
+int lh_tree_nodes(const lh_tree *t, int64_t *lohi_host, double *bbox_host, int32_t *kids_host);
+/* order[i_tree] = i_orig  (Permutation.inverse, geometry.py:239) */
+int lh_tree_order(const lh_tree *t, int64_t *order_host);
+
+/* Block partition only (host, no GPU): the decision order of hmatrix.py:319-337 with every
+ * admissible block of min(m,n) > n_min reported as low-rank (kind 1, rank -1).  Call with
+ * recs_host = NULL to get the counts; recs_host[5*b..] = row0,row1,col0,col1,kind. */
+int lh_partition(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
+                 int64_t *recs_host, int64_t *nblocks, int64_t *nhier);
+
+/* ---- H-matrix construction: hmatrix.py:121-137 HConfig, :306-340 build_from_dense */
+typedef struct {
+    int32_t n_min;        /* HConfig.n_min                                   */
+    int32_t n_block;      /* HConfig.n_block                                 */
+    double eta;           /* HConfig.eta                                     */
+    double eps1;          /* HConfig.eps1: keep sigma_k > eps1*sigma_1        */
+    int32_t kcap;         /* low-rank column capacity (>= rank; slack for H-LU) */
+    int32_t max_aca_rank; /* ACA iteration cap before recompression          */
+    double aca_tol;       /* ACA stop: |u_k||v_k| <= aca_tol*|S_k|_F          */
+} lh_hconfig;
+
+/* Partition + ACA/QR/SVD compression of a Toeplitz operator A[i,j] = t[j - i + nrows - 1]
+ * (t has nrows + ncols - 1 entries, device).  Matrix-free analogue of
+ * build_from_dense(toeplitz(t), rt, ct, cfg) (hmatrix.py:306-340). */
+int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,
+                           const lh_hconfig *cfg, lh_hmat **out);
+/* build_from_dense(A, rt, ct, cfg) with A on the device (tree order), element (i,j) at
+ * A[i*lda + j] (row_major=1, numpy C order) or A[i + j*lda] (row_major=0). */
+int lh_hmat_build_dense(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *A_dev,
+                        int64_t lda, int row_major, const lh_hconfig *cfg, lh_hmat **out);
+/* Same partition and ranks as `src`; low-rank blocks (lr_scale*U, V); dense blocks refilled
+ * from the Toeplitz symbol t_dev.  Used for A- from A+ (hard part 4). kcap<=0: tight. */
+int lh_hmat_derive_toeplitz(lh_ctx *ctx, const lh_hmat *src, const double *t_dev, double lr_scale,
+                            int32_t kcap, lh_hmat **out);
+int lh_hmat_clone(lh_ctx *ctx, const lh_hmat *src, int32_t kcap, lh_hmat **out);
+void lh_hmat_destroy(lh_hmat *h);
+
+/* ---- introspection: hmatrix.py:343-433 -------------------------------- */
+int64_t lh_hmat_num_blocks(const lh_hmat *h);
+/* recs[6*b ..] = row0,row1,col0,col1,kind(0 dense,1 lowrank,2 dense_lu),rank  (walk order) */
+int lh_hmat_structure(lh_ctx *ctx, const lh_hmat *h, int64_t *recs_host);
+/* stats[0..3] = dense_blocks, lowrank_blocks, stored_scalars, hier_nodes  (memory_report) */
+int lh_hmat_memory(lh_ctx *ctx, const lh_hmat *h, int64_t *stats_host);
+/* dense/dense_lu: a = m*n col-major (+ perm int64[m] into b for dense_lu as doubles);
+ * lowrank: a = U (m*rank col-major), b = V (n*rank col-major). */
+int lh_hmat_export_block(lh_ctx *ctx, const lh_hmat *h, int64_t block, double *a_host,
+                         double *b_host);
+
+/* ---- H-arithmetic ------------------------------------------------------ */
+/* hops.py:65-70 matvec / :73-85 mul_dense:  Y = H X, X is ncols x nrhs (col-major, ldx) */
+int lh_hmat_matvec(lh_ctx *ctx, const lh_hmat *h, const double *x_dev, int64_t ldx, double *y_dev,
+                   int64_t ldy, int32_t nrhs);
+/* hops.py:411-421 hlu: in-place recursive H-LU with eps2 recompression.
+ * On LH_ESINGULAR the message names the block path. */
+int lh_hlu(lh_ctx *ctx, lh_hmat *h, double eps2);
+/* hops.py:424-432 solve: forward (unit L, leaf pivots) + backward (U) substitution,
+ * in place on B (n x nrhs, col-major, ldb). method 0 = substitution DAG, 1 = inverse factors. */
+int lh_solve(lh_ctx *ctx, lh_hmat *factor, double *b_dev, int64_t ldb, int32_t nrhs,
+             int32_t method);
+/* Precompute the triangular-inverse factors used by method 1. */
+int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *factor, double eps2);
+/* levy.py:309-330 run_cn loop: U <- solve(F, Hm U), nsteps times, in place. */
+int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev, int64_t ldu,
+                int32_t nrhs, int32_t nsteps, int32_t method);
+
+/* ---- entry generation: fractional.py:285-405 + levy.py:169-206 -------- */
+typedef struct {
+    int32_t kind;   /* 0: power c|y|^(-1-2s); 1: CGMY; 2: tabulated nu(j*h), j=-M..M */
+    double c, s;    /* power measure */
+    double C, G, M, Y; /* CGMY */
+    const double *table_dev; /* kind 2 */
+} lh_measure;
+
+typedef struct {
+    double h;       /* grid spacing                       */
+    int64_t N;      /* interior unknowns                   */
+    int64_t M;      /* window offsets |j| <= M (L_W/h)     */
+    double rho_r;   /* window radius                       */
+    double tail;    /* tail mass beyond L_W                */
+    double m2;      /* windowed second moment (host quad)  */
+    double a, b, c; /* local coefficients (b = b_eff)      */
+    double dt;      /* CN time step                        */
+} lh_cn_params;
+
+/* Writes the Toeplitz symbols tA, tPlus, tMinus (2N-1 each, device) of A and
+ * A+- = I +- dt/2 A, and sums_host[0..2] = S0, Sg, Sd (GPU reduction). */
+int lh_cn_symbol(lh_ctx *ctx, const lh_measure *nu, const lh_cn_params *p, double *tA_dev,
+                 double *tPlus_dev, double *tMinus_dev, double *sums_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

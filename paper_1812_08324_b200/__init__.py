@@ -1,0 +1,20 @@
+"""B200-native Crank-Nicolson H-matrix solver for 1D Levy-generator equations.
+
+Drop-in for the hot path of the reference package `levyh` (arxiv 1812.08324):
+operator assembly (entry generation), compression, H-LU and time stepping,
+with the reference's public Python names.  All arithmetic runs in
+hand-written sm_100a CUDA kernels behind the C ABI in include/levyh_b200.h;
+there is no CPU fallback.
+"""
+from . import _lib  # noqa: F401
+from .fractional import (FracConfig, LevyMeasure, assemble_fractional_poisson_1d, cgmy_measure,  # noqa: F401
+                         frac_kernel_constant, frac_stencil_1d, frac_symbol_1d, power_measure,
+                         quartic_window, tail_mass_power_1d, windowed_second_moment)
+from .geometry import (ClusterNode, ClusterTree, Permutation, PointSet, admissible,  # noqa: F401
+                       build_cluster_tree)
+from .hmatrix import (HConfig, HMatrix, build_from_dense, build_toeplitz, dump_structure,  # noqa: F401
+                      export_blocks, h_entry, memory_report, structure_summary, to_dense)
+from .hops import HFactorization, hlu, matvec, mul_dense, solve  # noqa: F401
+from .levy import FracCNSystem, run_cn, step_cn  # noqa: F401
+
+__version__ = "0.1.0"

@@ -1,0 +1,146 @@
+"""ctypes binding of liblevyh_b200.so (include/levyh_b200.h).
+
+The native library is the only compute path: importing the package on a
+machine without it raises, and every GPU operation raises when no CUDA device
+is present.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblevyh_b200.so")
+
+LH_OK, LH_EINVAL, LH_ESINGULAR, LH_ETYPE, LH_ECUDA, LH_ENOMEM, LH_ERANK, LH_EINTERNAL = range(8)
+
+
+class HConfigC(C.Structure):
+    _fields_ = [("n_min", C.c_int32), ("n_block", C.c_int32), ("eta", C.c_double),
+                ("eps1", C.c_double), ("kcap", C.c_int32), ("max_aca_rank", C.c_int32),
+                ("aca_tol", C.c_double)]
+
+
+class MeasureC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("c", C.c_double), ("s", C.c_double), ("C", C.c_double),
+                ("G", C.c_double), ("M", C.c_double), ("Y", C.c_double),
+                ("table_dev", C.c_void_p)]
+
+
+class CNParamsC(C.Structure):
+    _fields_ = [("h", C.c_double), ("N", C.c_int64), ("M", C.c_int64), ("rho_r", C.c_double),
+                ("tail", C.c_double), ("m2", C.c_double), ("a", C.c_double), ("b", C.c_double),
+                ("c", C.c_double), ("dt", C.c_double)]
+
+
+# (name, restype, argtypes) for every symbol declared in include/levyh_b200.h
+P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+SIGNATURES = [
+    ("lh_ctx_create", C.c_int, [C.c_int, P, C.POINTER(P)]),
+    ("lh_ctx_destroy", None, [P]),
+    ("lh_ctx_last_error", C.c_char_p, [P]),
+    ("lh_ctx_synchronize", C.c_int, [P]),
+    ("lh_version", C.c_int, []),
+    ("lh_tree_build", C.c_int, [P, P, I64, C.c_int, C.c_int, C.POINTER(P)]),
+    ("lh_tree_destroy", None, [P]),
+    ("lh_tree_num_nodes", I64, [P]),
+    ("lh_tree_nodes", C.c_int, [P, P, P, P]),
+    ("lh_tree_order", C.c_int, [P, P]),
+    ("lh_partition", C.c_int, [P, P, C.c_int, C.c_int, D, P, P, P]),
+    ("lh_hmat_build_toeplitz", C.c_int, [P, P, P, P, C.POINTER(HConfigC), C.POINTER(P)]),
+    ("lh_hmat_build_dense", C.c_int, [P, P, P, P, I64, C.c_int, C.POINTER(HConfigC), C.POINTER(P)]),
+    ("lh_hmat_derive_toeplitz", C.c_int, [P, P, P, D, I32, C.POINTER(P)]),
+    ("lh_hmat_clone", C.c_int, [P, P, I32, C.POINTER(P)]),
+    ("lh_hmat_destroy", None, [P]),
+    ("lh_hmat_num_blocks", I64, [P]),
+    ("lh_hmat_structure", C.c_int, [P, P, P]),
+    ("lh_hmat_memory", C.c_int, [P, P, P]),
+    ("lh_hmat_export_block", C.c_int, [P, P, I64, P, P]),
+    ("lh_hmat_matvec", C.c_int, [P, P, P, I64, P, I64, I32]),
+    ("lh_hlu", C.c_int, [P, P, D]),
+    ("lh_solve", C.c_int, [P, P, P, I64, I32, I32]),
+    ("lh_prepare_inverse", C.c_int, [P, P, D]),
+    ("lh_cn_steps", C.c_int, [P, P, P, P, I64, I32, I32, I32]),
+    ("lh_cn_symbol", C.c_int, [P, C.POINTER(MeasureC), C.POINTER(CNParamsC), P, P, P, P]),
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load the native library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError(
+                        f"{LIB_PATH} is missing: build it with "
+                        "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback)")
+                L = C.CDLL(LIB_PATH)
+                for name, res, args in SIGNATURES:
+                    f = getattr(L, name)
+                    f.restype = res
+                    f.argtypes = args
+                _lib = L
+    return _lib
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def check(rc, ctx=None):
+    """Map an lh status code onto the reference's exception types."""
+    if rc == LH_OK:
+        return
+    msg = lib().lh_ctx_last_error(ctx).decode() if ctx else f"native error {rc}"
+    if rc == LH_EINVAL:
+        raise ValueError(msg)
+    if rc == LH_ESINGULAR:
+        raise np.linalg.LinAlgError(msg)
+    if rc == LH_ETYPE:
+        raise TypeError(msg)
+    if rc == LH_ENOMEM:
+        raise MemoryError(msg)
+    raise NativeError(f"[{rc}] {msg}")
+
+
+class Context:
+    """One native context per CUDA device, on torch's current stream at creation."""
+
+    _per_device: dict = {}
+
+    def __init__(self, device):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1812_08324_b200 needs a CUDA device (B200); none is visible")
+        self.device = device
+        with torch.cuda.device(device):
+            self.stream = torch.cuda.current_stream(device)
+        h = C.c_void_p()
+        rc = lib().lh_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        self.h = h
+        check(rc, h)
+
+    @classmethod
+    def get(cls, device=None):
+        import torch
+
+        if device is None:
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        if device not in cls._per_device:
+            cls._per_device[device] = Context(device)
+        return cls._per_device[device]
+
+    def sync(self):
+        check(lib().lh_ctx_synchronize(self.h), self.h)
+
+
+def host_ptr(a):
+    return C.c_void_p(a.ctypes.data)

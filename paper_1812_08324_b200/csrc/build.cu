@@ -1,0 +1,627 @@
+// Entry generation (Toeplitz symbol of the singular CN operator) and H-matrix
+// construction: partition + batched ACA + QR/SVD recompression with the
+// reference truncation rule, dense-leaf fill.
+//
+// Reference: fractional.py:78-86 (window), :108-127 (power density),
+// :285-301 (_window_sums_1d), :362-405 (frac_stencil_1d / Poisson assembly),
+// levy.py:169-206 (local band, A+-), hmatrix.py:294-340 (build_from_dense).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "core.h"
+#include "dev.cuh"
+
+namespace lh {
+
+using dev::KA_MAX;
+using dev::KC_MAX;
+using dev::NT;
+
+// ===========================================================================
+// entry generation
+// ===========================================================================
+struct MeasureDev {
+    int kind;
+    double c, expo;           // power: c * |y|^expo, expo = -1 - 2s
+    double C, G, M, Yexpo;    // CGMY: C e^{-rate|y|} |y|^Yexpo, Yexpo = -1 - Y
+    const double *table;      // tabulated nu(j h), j = -Mw..Mw
+    i64 Mw;
+};
+
+__device__ __forceinline__ double nu_eval(const MeasureDev &nu, i64 j, double y) {
+    if (nu.kind == 0) return nu.c * pow(fabs(y), nu.expo);
+    if (nu.kind == 1) {
+        double rate = y < 0.0 ? nu.G : nu.M;
+        double ay = fabs(y);
+        return nu.C * exp(-rate * ay) * pow(ay, nu.Yexpo);
+    }
+    return nu.table[j + nu.Mw];
+}
+
+// kern_j = nu(j h) * w_j, w = h (h/2 at |j| = M), kern_0 = 0  (fractional.py:285-296)
+__device__ __forceinline__ double kern_eval(const MeasureDev &nu, i64 j, double h, i64 M) {
+    if (j == 0) return 0.0;
+    double y = (double)j * h;
+    double w = (j == M || j == -M) ? h / 2.0 : h;
+    return nu_eval(nu, j, y) * w;
+}
+
+__device__ __forceinline__ double window_eval(double y, double r) {
+    double t = fabs(y) / r;
+    if (!(t < 1.0)) return 0.0;
+    double p = pow(fmin(t, 1.0), 4.0);
+    double q = 1.0 - p;
+    return q * q;
+}
+
+constexpr int SUM_CHUNK = 4096;
+
+// per-CTA partial sums of kern, rho*y*kern, rho*y*y*kern over a fixed chunk of j
+__global__ void window_sums_kernel(MeasureDev nu, double h, i64 M, double rho_r, double *partials) {
+    __shared__ double red[dev::NW];
+    i64 j0 = -M + (i64)blockIdx.x * SUM_CHUNK;
+    i64 j1 = min(j0 + SUM_CHUNK, M + 1);
+    double s0 = 0.0, sg = 0.0, sd = 0.0;
+    for (i64 j = j0 + threadIdx.x; j < j1; j += NT) {
+        double kern = kern_eval(nu, j, h, M);
+        double y = (double)j * h;
+        double rho = window_eval(y, rho_r);
+        s0 += kern;
+        sg += (rho * y) * kern;
+        sd += ((rho * y) * y) * kern;
+    }
+    s0 = dev::block_sum(s0, red);
+    sg = dev::block_sum(sg, red);
+    sd = dev::block_sum(sd, red);
+    if (threadIdx.x == 0) {
+        partials[3 * blockIdx.x + 0] = s0;
+        partials[3 * blockIdx.x + 1] = sg;
+        partials[3 * blockIdx.x + 2] = sd;
+    }
+}
+
+__global__ void reduce_partials_kernel(const double *partials, int nparts, double *sums) {
+    __shared__ double red[dev::NW];
+    for (int q = 0; q < 3; ++q) {
+        double s = 0.0;
+        for (int k = threadIdx.x; k < nparts; k += NT) s += partials[3 * k + q];
+        s = dev::block_sum(s, red);
+        if (threadIdx.x == 0) sums[q] = s;
+    }
+}
+
+struct SymbolArgs {
+    double h, tail, m2, a, b, c, dt;
+    i64 N, M;
+};
+
+// tA[k + N - 1] = A[i, i + k]; tP/tM for A+- (fractional.py:375-387, levy.py:173-176, :201-205)
+__global__ void symbol_fill_kernel(MeasureDev nu, SymbolArgs p, const double *sums, double *tA,
+                                   double *tP, double *tM) {
+    const double S0 = sums[0], Sg = sums[1], Sd = sums[2];
+    const double h = p.h;
+    const double h2 = h * h;
+    const i64 N = p.N;
+    const i64 kmax = min(N - 1, p.M);
+    const double hd = 0.5 * p.dt;
+    for (i64 idx = (i64)blockIdx.x * NT + threadIdx.x; idx < 2 * N - 1; idx += (i64)gridDim.x * NT) {
+        i64 k = idx - (N - 1);
+        double W = 0.0;
+        if (k != 0 && (k <= kmax && k >= -kmax)) W = kern_eval(nu, k, h, p.M);
+        if (k == 0) W = 0.0 + ((-S0 - p.tail) - (p.m2 - Sd) / h2);
+        double cside = (p.m2 - Sd) / (2 * h2);
+        if (k == 1) W += cside - Sg / (2 * h);
+        if (k == -1) W += cside + Sg / (2 * h);
+        double t = -W;
+        if (k == 0) t += 2 * p.a / h2 - p.c;
+        if (k == 1) t += -p.a / h2 - p.b / (2 * h);
+        if (k == -1) t += -p.a / h2 + p.b / (2 * h);
+        tA[idx] = t;
+        if (tP) tP[idx] = (k == 0 ? 1.0 : 0.0) + hd * t;
+        if (tM) tM[idx] = (k == 0 ? 1.0 : 0.0) - hd * t;
+    }
+}
+
+void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA, double *tP,
+               double *tM, double *sums_host) {
+    LH_REQUIRE(p.N >= 1 && p.M >= 1, LH_EINVAL, "need N >= 1 and M >= 1");
+    LH_REQUIRE(p.h > 0 && p.rho_r > 0, LH_EINVAL, "need h > 0 and rho_r > 0");
+    MeasureDev nu{};
+    nu.kind = m.kind;
+    nu.c = m.c;
+    nu.expo = -1 - 2 * m.s;
+    nu.C = m.C;
+    nu.G = m.G;
+    nu.M = m.M;
+    nu.Yexpo = -1.0 - m.Y;
+    nu.table = m.table_dev;
+    nu.Mw = p.M;
+    LH_REQUIRE(m.kind >= 0 && m.kind <= 2, LH_EINVAL, "unknown measure kind");
+    LH_REQUIRE(m.kind != 2 || m.table_dev, LH_EINVAL, "tabulated measure needs a table");
+    i64 cnt = 2 * p.M + 1;
+    int nparts = (int)((cnt + SUM_CHUNK - 1) / SUM_CHUNK);
+    double *buf = (double *)ctx.ensure_scratch(sizeof(double) * (3 * (size_t)nparts + 4));
+    double *sums = buf + 3 * (size_t)nparts;
+    window_sums_kernel<<<nparts, NT, 0, ctx.stream>>>(nu, p.h, p.M, p.rho_r, buf);
+    reduce_partials_kernel<<<1, NT, 0, ctx.stream>>>(buf, nparts, sums);
+    SymbolArgs a{p.h, p.tail, p.m2, p.a, p.b, p.c, p.dt, p.N, p.M};
+    int grid = (int)std::min<i64>((2 * p.N - 1 + NT - 1) / NT, 148 * 16);
+    symbol_fill_kernel<<<grid, NT, 0, ctx.stream>>>(nu, a, sums, tA, tP, tM);
+    LH_CUDA(cudaGetLastError());
+    if (sums_host) {
+        LH_CUDA(cudaMemcpyAsync(sums_host, sums, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+}
+
+// ===========================================================================
+// entry sources
+// ===========================================================================
+struct ToepSrc {  // A[i, j] = t[(nrows - 1) + j - i]
+    const double *t;
+    i64 nrows;
+    __device__ __forceinline__ double operator()(i64 i, i64 j) const { return t[nrows - 1 + j - i]; }
+};
+struct DenseSrc {  // row-major (numpy C order) or column-major
+    const double *A;
+    i64 lda;
+    int row_major;
+    __device__ __forceinline__ double operator()(i64 i, i64 j) const {
+        return row_major ? A[i * lda + j] : A[i + j * lda];
+    }
+};
+
+// ===========================================================================
+// dense fill
+// ===========================================================================
+struct FillJob {
+    i64 r0, c0, m, n, off;
+};
+
+template <class Src>
+__global__ void dense_fill_kernel(Src src, const FillJob *jobs, int njobs, double *arena) {
+    for (int b = blockIdx.x; b < njobs; b += gridDim.x) {
+        FillJob J = jobs[b];
+        double *D = arena + J.off;
+        i64 tot = J.m * J.n;
+        for (i64 e = threadIdx.x; e < tot; e += NT) {
+            i64 i = e % J.m, j = e / J.m;
+            D[e] = src(J.r0 + i, J.c0 + j);
+        }
+    }
+}
+
+// ===========================================================================
+// ACA + recompression, one low-rank block per CTA (persistent, size-sorted)
+// ===========================================================================
+struct AcaJob {
+    i64 r0, c0, m, n;
+    i64 wu, wv;      // workspace offsets: U (m x KA), V (n x KA), column-major
+    i64 fu, fv;      // final offsets in the arena (ld m / n)
+    int32_t kcap;    // final capacity
+    int32_t slot;    // rank slot
+};
+
+struct AcaSmem {
+    dev::RecompSmem R;
+    double ui[KA_MAX];
+    double vj[KA_MAX];
+    double hu[KA_MAX];
+    double hv[KA_MAX];
+    long long used[KA_MAX + 16];
+    double redv[dev::NW];
+    long long redi[dev::NW];
+    double red[dev::NW];
+    int nused;
+};
+
+// Adaptive cross approximation with partial pivoting on block (r0, c0, m, n).
+// Returns the number of terms K; U[:, :K], V[:, :K] hold A ~= U V^T.
+template <class Src>
+__device__ int aca_block(const Src &src, i64 r0, i64 c0, i64 m, i64 n, double *U, double *V,
+                         int KA, double tol, AcaSmem &S, int &converged) {
+    int k = 0, fails = 0, conv = 0;
+    double nS2 = 0.0;
+    long long i = 0;
+    if (threadIdx.x == 0) S.nused = 0;
+    converged = 0;
+    __syncthreads();
+    while (k < KA) {
+        for (int l = threadIdx.x; l < k; l += NT) S.ui[l] = U[i + (i64)l * m];
+        __syncthreads();
+        // residual row i -> V[:, k]
+        double *vk = V + (i64)k * n;
+        double best = -1.0;
+        long long bj = 0;
+        for (i64 j = threadIdx.x; j < n; j += NT) {
+            double r = src(r0 + i, c0 + j);
+            for (int l = 0; l < k; ++l) r -= S.ui[l] * V[j + (i64)l * n];
+            vk[j] = r;
+            double a = fabs(r);
+            if (a > best) {
+                best = a;
+                bj = j;
+            }
+        }
+        double amax;
+        long long jstar;
+        dev::block_argmax(best, bj, S.redv, S.redi, amax, jstar);
+        if (threadIdx.x == 0 && S.nused < KA_MAX + 16) S.used[S.nused++] = i;
+        __syncthreads();
+        if (!(amax > 0.0)) {
+            // row already represented exactly: try the next unused row
+            if (++fails > 8 || S.nused >= m || S.nused >= KA_MAX + 16) {
+                converged = 1;
+                break;
+            }
+            long long cand = i;
+            bool ok = false;
+            for (int tries = 0; tries < KA_MAX + 16 && !ok; ++tries) {
+                cand = (cand + 1) % m;
+                ok = true;
+                for (int q = 0; q < S.nused; ++q) ok = ok && (S.used[q] != cand);
+            }
+            i = cand;
+            continue;
+        }
+        fails = 0;
+        double delta = vk[jstar];
+        double inv = 1.0 / delta;
+        for (int l = threadIdx.x; l < k; l += NT) S.vj[l] = V[jstar + (i64)l * n];
+        __syncthreads();
+        for (i64 j = threadIdx.x; j < n; j += NT) vk[j] *= inv;
+        // residual column jstar -> U[:, k]
+        double *uk = U + (i64)k * m;
+        for (i64 ii = threadIdx.x; ii < m; ii += NT) {
+            double c = src(r0 + ii, c0 + jstar);
+            for (int l = 0; l < k; ++l) c -= U[ii + (i64)l * m] * S.vj[l];
+            uk[ii] = c;
+        }
+        __syncthreads();
+        // |S_k|_F^2 update
+        dev::col_dots(U, m, m, k, uk, S.hu);
+        dev::col_dots(V, n, n, k, vk, S.hv);
+        double su = 0.0, sv = 0.0;
+        for (i64 ii = threadIdx.x; ii < m; ii += NT) su += uk[ii] * uk[ii];
+        for (i64 j = threadIdx.x; j < n; j += NT) sv += vk[j] * vk[j];
+        su = dev::block_sum(su, S.red);
+        sv = dev::block_sum(sv, S.red);
+        double cross = 0.0;
+        for (int l = 0; l < k; ++l) cross += S.hu[l] * S.hv[l];
+        nS2 += 2.0 * cross + su * sv;
+        ++k;
+        if (sqrt(su * sv) <= tol * sqrt(fabs(nS2))) {
+            if (++conv >= 2) {
+                converged = 1;
+                break;
+            }
+        } else {
+            conv = 0;
+        }
+        // next pivot row: argmax |U[:, k-1]| over unused rows
+        best = -1.0;
+        long long bi = 0;
+        for (i64 ii = threadIdx.x; ii < m; ii += NT) {
+            double a = fabs(uk[ii]);
+            if (a > best) {
+                bool fresh = true;
+                for (int q = 0; q < S.nused; ++q) fresh = fresh && (S.used[q] != ii);
+                if (fresh) {
+                    best = a;
+                    bi = ii;
+                }
+            }
+        }
+        double bmax;
+        long long inext;
+        dev::block_argmax(best, bi, S.redv, S.redi, bmax, inext);
+        if (bmax < 0.0) {  // every row used
+            converged = 1;
+            break;
+        }
+        i = inext;
+        __syncthreads();
+    }
+    __syncthreads();
+    return k;
+}
+
+// flags: 0 ok (low rank), 2 -> store dense (rank > min//2), 3 -> rank > kcap,
+//        4 -> ACA hit max rank without converging
+template <class Src>
+__global__ void __launch_bounds__(NT) aca_kernel(Src src, const AcaJob *jobs, int njobs,
+                                                 int *counter, double *work, double *arena,
+                                                 int *ranks, int *flags, int KA, double tol,
+                                                 double eps1) {
+    extern __shared__ double4 smem_raw[];
+    AcaSmem &S = *reinterpret_cast<AcaSmem *>(smem_raw);
+    __shared__ int s_job;
+    while (true) {
+        if (threadIdx.x == 0) s_job = atomicAdd(counter, 1);
+        __syncthreads();
+        int jb = s_job;
+        __syncthreads();
+        if (jb >= njobs) break;
+        AcaJob J = jobs[jb];
+        double *U = work + J.wu;
+        double *V = work + J.wv;
+        int conv = 0;
+        int K = aca_block(src, J.r0, J.c0, J.m, J.n, U, V, KA, tol, S, conv);
+        i64 half = min(J.m, J.n) / 2;
+        int rmax = (int)min((i64)min(J.kcap, KC_MAX), half);
+        int r = dev::recompress(U, J.m, J.m, V, J.n, J.n, K, 0, eps1, arena + J.fu, J.m,
+                                arena + J.fv, J.n, rmax, S.R);
+        if (threadIdx.x == 0) {
+            int f = 0;
+            if (r > half) f = 2;
+            else if (r > rmax) f = 3;
+            else if (!conv) f = 4;
+            ranks[J.slot] = (f == 0 || f == 4) ? r : 0;
+            flags[jb] = f;
+        }
+        __syncthreads();
+    }
+}
+
+// ===========================================================================
+// host: build
+// ===========================================================================
+static void set_smem(const void *fn, size_t bytes) {
+    LH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+template <class Src>
+static void run_build(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg) {
+    const int KA = std::min(std::max(cfg.max_aca_rank, 1), KA_MAX);
+    const int kcap = std::min(std::max(cfg.kcap, 1), KC_MAX);
+    // --- storage layout: dense region then low-rank region -------------------
+    i64 off = 0;
+    int nslots = 0;
+    std::vector<int32_t> lr;
+    for (int32_t b : H.leafblocks) {
+        Node &nd = H.nodes[b];
+        if (nd.kind == K_DENSE) {
+            nd.doff = off;
+            off += nd.m * nd.n;
+        }
+    }
+    for (int32_t b : H.leafblocks) {
+        Node &nd = H.nodes[b];
+        if (nd.kind == K_LR) {
+            nd.kcap = kcap;
+            nd.rslot = nslots++;
+            nd.uoff = off;
+            off += nd.m * kcap;
+            nd.voff = off;
+            off += nd.n * kcap;
+            lr.push_back(b);
+        }
+    }
+    H.arena_len = off;
+    H.d_arena = dalloc<double>(off);
+    H.nslots = nslots;
+    H.d_ranks = dalloc<int32_t>(std::max(nslots, 1));
+    LH_CUDA(cudaMemsetAsync(H.d_ranks, 0, sizeof(int32_t) * std::max(nslots, 1), ctx.stream));
+    // --- ACA in size-sorted batches bounded by a workspace budget -------------
+    std::sort(lr.begin(), lr.end(), [&](int32_t a, int32_t b) {
+        i64 sa = H.nodes[a].m + H.nodes[a].n, sb = H.nodes[b].m + H.nodes[b].n;
+        return sa != sb ? sa > sb : a < b;
+    });
+    const i64 budget = (i64)1 << 30;  // doubles (8 GiB)
+    std::vector<int32_t> to_dense;
+    size_t smem = sizeof(AcaSmem);
+    set_smem((const void *)aca_kernel<Src>, smem);
+    size_t p = 0;
+    double *work = nullptr;
+    i64 work_len = 0;
+    while (p < lr.size()) {
+        std::vector<AcaJob> jobs;
+        i64 w = 0;
+        size_t q = p;
+        while (q < lr.size()) {
+            const Node &nd = H.nodes[lr[q]];
+            i64 need = (nd.m + nd.n) * KA;
+            if (!jobs.empty() && w + need > budget) break;
+            AcaJob J{nd.r0, nd.c0, nd.m, nd.n, w, w + nd.m * KA, nd.uoff, nd.voff, nd.kcap, nd.rslot};
+            jobs.push_back(J);
+            w += need;
+            ++q;
+        }
+        if (w > work_len) {
+            if (work) cudaFree(work);
+            work = dalloc<double>(w);
+            work_len = w;
+        }
+        AcaJob *djobs = dupload(jobs, ctx.stream);
+        int *dcnt = dalloc<int>(1 + (i64)jobs.size());
+        int *dflags = dcnt + 1;
+        LH_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * (1 + jobs.size()), ctx.stream));
+        int grid = std::min<int>((int)jobs.size(), ctx.num_sms * 2);
+        aca_kernel<Src><<<grid, NT, smem, ctx.stream>>>(src, djobs, (int)jobs.size(), dcnt, work,
+                                                        H.d_arena, H.d_ranks, dflags, KA,
+                                                        cfg.aca_tol, cfg.eps1);
+        LH_CUDA(cudaGetLastError());
+        std::vector<int> flags(jobs.size());
+        LH_CUDA(cudaMemcpyAsync(flags.data(), dflags, sizeof(int) * jobs.size(),
+                                cudaMemcpyDeviceToHost, ctx.stream));
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(djobs);
+        cudaFree(dcnt);
+        for (size_t k = 0; k < jobs.size(); ++k) {
+            const Node &nd = H.nodes[lr[p + k]];
+            if (flags[k] == 2) to_dense.push_back(lr[p + k]);
+            else if (flags[k] == 3)
+                throw Error(LH_ERANK, "recompressed rank exceeds kcap=" + std::to_string(kcap) +
+                                          " for block (" + std::to_string(nd.r0) + "," +
+                                          std::to_string(nd.c0) + "," + std::to_string(nd.m) + "x" +
+                                          std::to_string(nd.n) + ")");
+            else if (flags[k] == 4)
+                throw Error(LH_ERANK, "ACA did not converge within max_aca_rank=" +
+                                          std::to_string(KA) + " for block (" +
+                                          std::to_string(nd.r0) + "," + std::to_string(nd.c0) +
+                                          "," + std::to_string(nd.m) + "x" + std::to_string(nd.n) +
+                                          ")");
+        }
+        p = q;
+    }
+    if (work) cudaFree(work);
+    // --- blocks whose rank exceeds min(m,n)//2 are stored dense (hmatrix.py:301-302,331)
+    if (!to_dense.empty()) {
+        i64 extra = 0;
+        for (int32_t b : to_dense) extra += H.nodes[b].m * H.nodes[b].n;
+        double *na = dalloc<double>(H.arena_len + extra);
+        LH_CUDA(cudaMemcpyAsync(na, H.d_arena, sizeof(double) * H.arena_len, cudaMemcpyDeviceToDevice,
+                                ctx.stream));
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(H.d_arena);
+        H.d_arena = na;
+        i64 o = H.arena_len;
+        for (int32_t b : to_dense) {
+            Node &nd = H.nodes[b];
+            nd.kind = K_DENSE;
+            nd.doff = o;
+            o += nd.m * nd.n;
+            nd.uoff = nd.voff = -1;
+        }
+        H.arena_len += extra;
+    }
+    // --- dense fill ----------------------------------------------------------
+    std::vector<FillJob> fj;
+    for (int32_t b : H.leafblocks) {
+        const Node &nd = H.nodes[b];
+        if (nd.kind == K_DENSE) fj.push_back({nd.r0, nd.c0, nd.m, nd.n, nd.doff});
+    }
+    if (!fj.empty()) {
+        FillJob *d = dupload(fj, ctx.stream);
+        int grid = (int)std::min<size_t>(fj.size(), (size_t)ctx.num_sms * 16);
+        dense_fill_kernel<Src><<<grid, NT, 0, ctx.stream>>>(src, d, (int)fj.size(), H.d_arena);
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(d);
+    }
+    H.sync_ranks(ctx.stream);
+}
+
+void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg) {
+    ToepSrc s{t, H.nrows};
+    run_build(ctx, H, s, cfg);
+}
+
+void build_dense(Ctx &ctx, HMat &H, const double *A, i64 lda, int row_major, const lh_hconfig &cfg) {
+    DenseSrc s{A, lda, row_major};
+    run_build(ctx, H, s, cfg);
+}
+
+// ===========================================================================
+// derive: same partition/ranks, U scaled, dense refilled from a symbol
+// ===========================================================================
+struct CopyLrJob {
+    i64 su, sv, du, dv, m, n;
+    int32_t slot;
+};
+
+__global__ void copy_lr_kernel(const CopyLrJob *jobs, int njobs, const double *src, double *dst,
+                               const int *ranks, double scale) {
+    for (int b = blockIdx.x; b < njobs; b += gridDim.x) {
+        CopyLrJob J = jobs[b];
+        int r = ranks[J.slot];
+        for (i64 e = threadIdx.x; e < J.m * r; e += NT) {
+            i64 i = e % J.m, c = e / J.m;
+            dst[J.du + i + c * J.m] = scale * src[J.su + i + c * J.m];
+        }
+        for (i64 e = threadIdx.x; e < J.n * r; e += NT) {
+            i64 i = e % J.n, c = e / J.n;
+            dst[J.dv + i + c * J.n] = src[J.sv + i + c * J.n];
+        }
+    }
+}
+
+__global__ void copy_dense_kernel(const FillJob *jobs, int njobs, const double *src, double *dst,
+                                  const i64 *src_off) {
+    for (int b = blockIdx.x; b < njobs; b += gridDim.x) {
+        FillJob J = jobs[b];
+        for (i64 e = threadIdx.x; e < J.m * J.n; e += NT) dst[J.off + e] = src[src_off[b] + e];
+    }
+}
+
+// Copy of `S` with LR capacity kcap (<= 0: tight = rank), LR U scaled by `scale`.
+// If t != nullptr dense blocks are refilled from the Toeplitz symbol, else copied.
+void derive(Ctx &ctx, const HMat &S, HMat &D, const double *t, double scale, int kcap) {
+    LH_REQUIRE(!S.factored, LH_EINVAL, "cannot derive from a factored H-matrix");
+    D.rt = S.rt;
+    D.ct = S.ct;
+    D.rt_hold = S.rt_hold;
+    D.ct_hold = S.ct_hold;
+    D.nrows = S.nrows;
+    D.ncols = S.ncols;
+    D.root = S.root;
+    D.nodes = S.nodes;
+    D.leafblocks = S.leafblocks;
+    D.nslots = S.nslots;
+    D.h_ranks = S.h_ranks;
+    i64 off = 0;
+    for (int32_t b : D.leafblocks) {
+        Node &nd = D.nodes[b];
+        if (nd.kind == K_DENSE) {
+            nd.doff = off;
+            off += nd.m * nd.n;
+        }
+    }
+    std::vector<CopyLrJob> lj;
+    for (int32_t b : D.leafblocks) {
+        Node &nd = D.nodes[b];
+        if (nd.kind == K_LR) {
+            int r = S.h_ranks[nd.rslot];
+            nd.kcap = kcap > 0 ? std::max(kcap, r) : r;
+            LH_REQUIRE(nd.kcap <= KC_MAX, LH_ERANK, "kcap exceeds the compile-time maximum");
+            nd.uoff = off;
+            off += nd.m * nd.kcap;
+            nd.voff = off;
+            off += nd.n * nd.kcap;
+            const Node &sn = S.nodes[b];
+            lj.push_back({sn.uoff, sn.voff, nd.uoff, nd.voff, nd.m, nd.n, nd.rslot});
+        }
+    }
+    D.arena_len = off;
+    D.d_arena = dalloc<double>(off);
+    D.d_ranks = dalloc<int32_t>(std::max(D.nslots, 1));
+    LH_CUDA(cudaMemcpyAsync(D.d_ranks, S.d_ranks, sizeof(int32_t) * std::max(D.nslots, 1),
+                            cudaMemcpyDeviceToDevice, ctx.stream));
+    if (!lj.empty()) {
+        CopyLrJob *d = dupload(lj, ctx.stream);
+        int grid = (int)std::min<size_t>(lj.size(), (size_t)ctx.num_sms * 16);
+        copy_lr_kernel<<<grid, NT, 0, ctx.stream>>>(d, (int)lj.size(), S.d_arena, D.d_arena,
+                                                    D.d_ranks, scale);
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(d);
+    }
+    std::vector<FillJob> fj;
+    std::vector<i64> so;
+    for (int32_t b : D.leafblocks) {
+        const Node &nd = D.nodes[b];
+        if (nd.kind == K_DENSE) {
+            fj.push_back({nd.r0, nd.c0, nd.m, nd.n, nd.doff});
+            so.push_back(S.nodes[b].doff);
+        }
+    }
+    if (!fj.empty()) {
+        FillJob *d = dupload(fj, ctx.stream);
+        int grid = (int)std::min<size_t>(fj.size(), (size_t)ctx.num_sms * 16);
+        if (t) {
+            ToepSrc s{t, D.nrows};
+            dense_fill_kernel<ToepSrc><<<grid, NT, 0, ctx.stream>>>(s, d, (int)fj.size(), D.d_arena);
+        } else {
+            i64 *dso = dupload(so, ctx.stream);
+            copy_dense_kernel<<<grid, NT, 0, ctx.stream>>>(d, (int)fj.size(), S.d_arena, D.d_arena, dso);
+            LH_CUDA(cudaStreamSynchronize(ctx.stream));
+            cudaFree(dso);
+        }
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(d);
+    }
+}
+
+}  // namespace lh

@@ -1,0 +1,351 @@
+// C-ABI of the B200 H-matrix engine (include/levyh_b200.h).
+#include <cstring>
+
+#include "core.h"
+#include "matvec.h"
+
+struct lh_ctx {
+    lh::Ctx c;
+};
+struct lh_tree {
+    std::shared_ptr<lh::Tree> t;
+};
+struct lh_hmat {
+    lh::HMat h;
+};
+
+namespace lh {
+void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA, double *tP,
+               double *tM, double *sums_host);
+void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg);
+void build_dense(Ctx &ctx, HMat &H, const double *A, i64 lda, int row_major, const lh_hconfig &cfg);
+void derive(Ctx &ctx, const HMat &S, HMat &D, const double *t, double scale, int kcap);
+void hlu(Ctx &ctx, HMat &H, double eps2);
+void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method);
+void prepare_inverse(Ctx &ctx, HMat &F, double eps2);
+void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method);
+
+void *Ctx::ensure_scratch(size_t bytes) {
+    if (bytes > scratch_bytes) {
+        if (scratch) {
+            cudaStreamSynchronize(stream);
+            cudaFree(scratch);
+        }
+        scratch = nullptr;
+        LH_CUDA(cudaMalloc(&scratch, bytes));
+        scratch_bytes = bytes;
+    }
+    return scratch;
+}
+Ctx::~Ctx() {
+    if (scratch) cudaFree(scratch);
+}
+HMat::~HMat() {
+    mv_plan.reset();
+    solve_plan.reset();
+    inv_plan.reset();
+    if (d_arena) cudaFree(d_arena);
+    if (d_ranks) cudaFree(d_ranks);
+    if (d_perm) cudaFree(d_perm);
+}
+void HMat::sync_ranks(cudaStream_t s) {
+    h_ranks.assign(std::max(nslots, 0), 0);
+    if (nslots > 0) {
+        LH_CUDA(cudaMemcpyAsync(h_ranks.data(), d_ranks, sizeof(int32_t) * nslots,
+                                cudaMemcpyDeviceToHost, s));
+        LH_CUDA(cudaStreamSynchronize(s));
+    }
+}
+}  // namespace lh
+
+using namespace lh;
+
+template <class F>
+static int guard(lh_ctx *ctx, F &&f) {
+    try {
+        f();
+        return LH_OK;
+    } catch (const lh::Error &e) {
+        if (ctx) ctx->c.last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        if (ctx) ctx->c.last_error = "host allocation failed";
+        return LH_ENOMEM;
+    } catch (const std::exception &e) {
+        if (ctx) ctx->c.last_error = e.what();
+        return LH_EINTERNAL;
+    }
+}
+
+static void check_cfg(const lh_hconfig *cfg) {
+    LH_REQUIRE(cfg != nullptr, LH_EINVAL, "null HConfig");
+    LH_REQUIRE(cfg->n_block >= 2, LH_EINVAL, "n_block must be >= 2");
+    LH_REQUIRE(cfg->n_min >= 1, LH_EINVAL, "n_min must be >= 1");
+    LH_REQUIRE(cfg->eta > 0, LH_EINVAL, "eta must be positive");
+}
+
+extern "C" {
+
+int lh_version(void) { return 1; }
+
+int lh_ctx_create(int device, void *stream, lh_ctx **out) {
+    lh_ctx *c = new lh_ctx();
+    int rc = guard(c, [&] {
+        LH_CUDA(cudaSetDevice(device));
+        c->c.device = device;
+        c->c.stream = (cudaStream_t)stream;
+        int sms = 0;
+        LH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        c->c.num_sms = sms;
+    });
+    if (rc != LH_OK) {
+        // keep the context so the caller can read the message
+    }
+    *out = c;
+    return rc;
+}
+
+void lh_ctx_destroy(lh_ctx *ctx) { delete ctx; }
+
+const char *lh_ctx_last_error(const lh_ctx *ctx) { return ctx ? ctx->c.last_error.c_str() : ""; }
+
+int lh_ctx_synchronize(lh_ctx *ctx) {
+    return guard(ctx, [&] { LH_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+}
+
+int lh_tree_build(lh_ctx *ctx, const double *pts, int64_t n, int dim, int leaf_size, lh_tree **out) {
+    return guard(ctx, [&] {
+        std::shared_ptr<Tree> t(build_tree(pts, n, dim, leaf_size));
+        lh_tree *o = new lh_tree();
+        o->t = t;
+        *out = o;
+    });
+}
+
+void lh_tree_destroy(lh_tree *t) { delete t; }
+
+int64_t lh_tree_num_nodes(const lh_tree *t) { return (int64_t)t->t->nodes.size(); }
+
+int lh_tree_nodes(const lh_tree *t, int64_t *lohi, double *bbox, int32_t *kids) {
+    const Tree &T = *t->t;
+    for (size_t i = 0; i < T.nodes.size(); ++i) {
+        const Cluster &c = T.nodes[i];
+        if (lohi) {
+            lohi[2 * i] = c.lo;
+            lohi[2 * i + 1] = c.hi;
+        }
+        if (bbox)
+            for (int d = 0; d < T.dim; ++d) {
+                bbox[(2 * i) * T.dim + d] = c.blo[d];
+                bbox[(2 * i + 1) * T.dim + d] = c.bhi[d];
+            }
+        if (kids) {
+            kids[2 * i] = c.kid[0];
+            kids[2 * i + 1] = c.kid[1];
+        }
+    }
+    return LH_OK;
+}
+
+int lh_tree_order(const lh_tree *t, int64_t *order) {
+    std::memcpy(order, t->t->order.data(), sizeof(int64_t) * t->t->order.size());
+    return LH_OK;
+}
+
+int lh_partition(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
+                 int64_t *recs, int64_t *nblocks, int64_t *nhier) {
+    return guard(nullptr, [&] {
+        HMat H;
+        partition(H, *rt->t, *ct->t, n_min, n_block, eta);
+        int64_t nh = 0;
+        for (const Node &nd : H.nodes) nh += nd.kind == K_HIER;
+        if (nblocks) *nblocks = (int64_t)H.leafblocks.size();
+        if (nhier) *nhier = nh;
+        if (recs)
+            for (size_t k = 0; k < H.leafblocks.size(); ++k) {
+                const Node &nd = H.nodes[H.leafblocks[k]];
+                int64_t *r = recs + 5 * k;
+                r[0] = nd.r0;
+                r[1] = nd.r0 + nd.m;
+                r[2] = nd.c0;
+                r[3] = nd.c0 + nd.n;
+                r[4] = nd.kind == K_LR ? 1 : 0;
+            }
+    });
+}
+
+static lh_hmat *new_hmat(const lh_tree *rt, const lh_tree *ct) {
+    lh_hmat *o = new lh_hmat();
+    o->h.rt_hold = rt->t;
+    o->h.ct_hold = ct->t;
+    return o;
+}
+
+int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,
+                           const lh_hconfig *cfg, lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        check_cfg(cfg);
+        o = new_hmat(rt, ct);
+        partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
+        build_toeplitz(ctx->c, o->h, t_dev, *cfg);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+int lh_hmat_build_dense(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *A_dev,
+                        int64_t lda, int row_major, const lh_hconfig *cfg, lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        check_cfg(cfg);
+        o = new_hmat(rt, ct);
+        partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
+        build_dense(ctx->c, o->h, A_dev, lda, row_major, *cfg);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+int lh_hmat_derive_toeplitz(lh_ctx *ctx, const lh_hmat *src, const double *t_dev, double lr_scale,
+                            int32_t kcap, lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        o = new lh_hmat();
+        derive(ctx->c, src->h, o->h, t_dev, lr_scale, kcap);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+int lh_hmat_clone(lh_ctx *ctx, const lh_hmat *src, int32_t kcap, lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        o = new lh_hmat();
+        derive(ctx->c, src->h, o->h, nullptr, 1.0, kcap);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+void lh_hmat_destroy(lh_hmat *h) { delete h; }
+
+int64_t lh_hmat_num_blocks(const lh_hmat *h) { return (int64_t)h->h.leafblocks.size(); }
+
+int lh_hmat_structure(lh_ctx *ctx, const lh_hmat *h, int64_t *recs) {
+    return guard(ctx, [&] {
+        const HMat &H = h->h;
+        const_cast<HMat &>(H).sync_ranks(ctx->c.stream);
+        for (size_t k = 0; k < H.leafblocks.size(); ++k) {
+            const Node &nd = H.nodes[H.leafblocks[k]];
+            int64_t *r = recs + 6 * k;
+            r[0] = nd.r0;
+            r[1] = nd.r0 + nd.m;
+            r[2] = nd.c0;
+            r[3] = nd.c0 + nd.n;
+            r[4] = nd.kind == K_LR ? 1 : (nd.kind == K_FDENSE ? 2 : 0);
+            r[5] = nd.kind == K_LR ? H.h_ranks[nd.rslot] : -1;
+        }
+    });
+}
+
+int lh_hmat_memory(lh_ctx *ctx, const lh_hmat *h, int64_t *stats) {
+    return guard(ctx, [&] {
+        const HMat &H = h->h;
+        const_cast<HMat &>(H).sync_ranks(ctx->c.stream);
+        int64_t nd_ = 0, nl = 0, sc = 0, nh = 0;
+        for (const Node &nd : H.nodes) {
+            if (nd.kind == K_HIER) {
+                ++nh;
+            } else if (nd.kind == K_LR) {
+                ++nl;
+                sc += (int64_t)H.h_ranks[nd.rslot] * (nd.m + nd.n);
+            } else {
+                ++nd_;
+                sc += nd.m * nd.n;
+            }
+        }
+        stats[0] = nd_;
+        stats[1] = nl;
+        stats[2] = sc;
+        stats[3] = nh;
+    });
+}
+
+int lh_hmat_export_block(lh_ctx *ctx, const lh_hmat *h, int64_t block, double *a, double *b) {
+    return guard(ctx, [&] {
+        const HMat &H = h->h;
+        LH_REQUIRE(block >= 0 && block < (int64_t)H.leafblocks.size(), LH_EINVAL, "block index");
+        const Node &nd = H.nodes[H.leafblocks[block]];
+        cudaStream_t s = ctx->c.stream;
+        if (nd.kind == K_LR) {
+            const_cast<HMat &>(H).sync_ranks(s);
+            int r = H.h_ranks[nd.rslot];
+            if (a && r)
+                LH_CUDA(cudaMemcpyAsync(a, H.d_arena + nd.uoff, sizeof(double) * nd.m * r,
+                                        cudaMemcpyDeviceToHost, s));
+            if (b && r)
+                LH_CUDA(cudaMemcpyAsync(b, H.d_arena + nd.voff, sizeof(double) * nd.n * r,
+                                        cudaMemcpyDeviceToHost, s));
+        } else {
+            if (a)
+                LH_CUDA(cudaMemcpyAsync(a, H.d_arena + nd.doff, sizeof(double) * nd.m * nd.n,
+                                        cudaMemcpyDeviceToHost, s));
+            if (b && nd.kind == K_FDENSE) {
+                std::vector<int32_t> p(nd.m);
+                LH_CUDA(cudaMemcpyAsync(p.data(), H.d_perm + nd.poff, sizeof(int32_t) * nd.m,
+                                        cudaMemcpyDeviceToHost, s));
+                LH_CUDA(cudaStreamSynchronize(s));
+                for (i64 i = 0; i < nd.m; ++i) b[i] = (double)p[i];
+            }
+        }
+        LH_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int lh_hmat_matvec(lh_ctx *ctx, const lh_hmat *h, const double *x, int64_t ldx, double *y,
+                   int64_t ldy, int32_t nrhs) {
+    return guard(ctx, [&] { matvec(ctx->c, const_cast<HMat &>(h->h), x, ldx, y, ldy, nrhs); });
+}
+
+int lh_hlu(lh_ctx *ctx, lh_hmat *h, double eps2) {
+    return guard(ctx, [&] { hlu(ctx->c, h->h, eps2); });
+}
+
+int lh_solve(lh_ctx *ctx, lh_hmat *f, double *b, int64_t ldb, int32_t nrhs, int32_t method) {
+    return guard(ctx, [&] { solve(ctx->c, f->h, b, ldb, nrhs, method); });
+}
+
+int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *f, double eps2) {
+    return guard(ctx, [&] { prepare_inverse(ctx->c, f->h, eps2); });
+}
+
+int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t ldu, int32_t nrhs,
+                int32_t nsteps, int32_t method) {
+    return guard(ctx, [&] {
+        cn_steps(ctx->c, const_cast<HMat &>(hm->h), f->h, u, ldu, nrhs, nsteps, method);
+    });
+}
+
+int lh_cn_symbol(lh_ctx *ctx, const lh_measure *nu, const lh_cn_params *p, double *tA, double *tP,
+                 double *tM, double *sums_host) {
+    return guard(ctx, [&] { cn_symbol(ctx->c, *nu, *p, tA, tP, tM, sums_host); });
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// Internal structures of the B200 H-matrix engine (host side).
+// Public ABI: include/levyh_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/levyh_b200.h"
+
+namespace lh {
+
+typedef int64_t i64;
+
+// Error carrying an lh status code; converted to a return code at the C-ABI.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define LH_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            throw ::lh::Error(LH_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LH_REQUIRE(cond, code, msg)                   \
+    do {                                              \
+        if (!(cond)) throw ::lh::Error((code), (msg)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// cluster tree (geometry.py:66-243)
+// ---------------------------------------------------------------------------
+struct Cluster {
+    i64 lo, hi;          // tree-order range [lo, hi)
+    double blo[2], bhi[2];
+    int32_t kid[2];      // -1: leaf
+    int32_t depth;
+    i64 size() const { return hi - lo; }
+    bool leaf() const { return kid[0] < 0; }
+};
+
+struct Tree {
+    int dim = 1;
+    i64 n = 0;
+    int leaf_size = 64;
+    std::vector<Cluster> nodes;  // nodes[0] is the root
+    std::vector<i64> order;      // order[i_tree] = i_orig
+    std::vector<int32_t> leaves; // leaf cluster ids in tree order
+};
+
+Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size);
+bool admissible(const Cluster &a, const Cluster &b, int dim, double eta);
+double diameter(const Cluster &a, int dim);
+
+// ---------------------------------------------------------------------------
+// block tree (hmatrix.py:51-118)
+// ---------------------------------------------------------------------------
+enum Kind : int32_t { K_HIER = 0, K_DENSE = 1, K_LR = 2, K_FDENSE = 3 };
+
+struct Node {
+    int32_t kind;
+    int32_t rcl, ccl;     // row / column cluster ids
+    i64 r0, c0, m, n;     // absolute tree-order position and shape
+    int32_t kid[4];       // HIER: 11, 12, 21, 22
+    i64 rs, cs;           // HIER: row_split, col_split
+    i64 doff;             // DENSE/FDENSE: arena offset, column-major, ld = m
+    i64 uoff, voff;       // LR: U (m x kcap), V (n x kcap), column-major
+    int32_t kcap;         // LR: column capacity
+    int32_t rslot;        // LR: index into the rank array
+    i64 poff;             // FDENSE: offset of the int32 net row permutation
+    int32_t depth;        // block-tree depth
+};
+
+struct Ctx;
+
+struct HMat {
+    const Tree *rt = nullptr, *ct = nullptr;
+    std::shared_ptr<const Tree> rt_hold, ct_hold;  // keep trees alive
+    i64 nrows = 0, ncols = 0;
+    int32_t root = 0;
+    std::vector<Node> nodes;
+    std::vector<int32_t> leafblocks;  // non-HIER nodes in walk order (11,12,21,22)
+    double *d_arena = nullptr;
+    i64 arena_len = 0;
+    int32_t *d_ranks = nullptr;
+    std::vector<int32_t> h_ranks;     // host mirror (valid after sync_ranks)
+    int32_t nslots = 0;
+    int32_t *d_perm = nullptr;        // FDENSE permutations
+    i64 perm_len = 0;
+    bool factored = false;
+    // lazily built plans (opaque; see matvec.cu / plan.cpp)
+    std::shared_ptr<void> mv_plan;
+    std::shared_ptr<void> solve_plan;
+    std::shared_ptr<void> inv_plan;
+    ~HMat();
+    void sync_ranks(cudaStream_t s);
+};
+
+// Partition exactly as build_from_dense decides it (hmatrix.py:319-337), with every
+// admissible block with min(m,n) > n_min marked K_LR (compression decides later).
+void partition(HMat &H, const Tree &rt, const Tree &ct, int n_min, int n_block, double eta);
+void walk_leaves(HMat &H);
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string last_error;
+    int num_sms = 148;
+    // reusable device scratch
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void *ensure_scratch(size_t bytes);
+    ~Ctx();
+};
+
+// device memory helpers
+template <class T>
+T *dalloc(i64 count) {
+    void *p = nullptr;
+    if (count <= 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * (size_t)count);
+    if (e != cudaSuccess)
+        throw Error(LH_ENOMEM, std::string("cudaMalloc(") + std::to_string(sizeof(T) * count) +
+                                   " bytes): " + cudaGetErrorString(e));
+    return (T *)p;
+}
+template <class T>
+void upload(T *dst, const std::vector<T> &src, cudaStream_t s) {
+    if (!src.empty())
+        LH_CUDA(cudaMemcpyAsync(dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
+}
+template <class T>
+T *dupload(const std::vector<T> &src, cudaStream_t s) {
+    T *p = dalloc<T>((i64)src.size());
+    upload(p, src, s);
+    return p;
+}
+
+}  // namespace lh

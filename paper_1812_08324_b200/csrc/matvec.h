@@ -1,0 +1,48 @@
+// H-matvec plan (see matvec.cu).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "core.h"
+
+namespace lh {
+
+struct SegDesc {
+    i64 y0;
+    int32_t rows;
+    int32_t dbeg, dend;
+    int32_t lbeg, lend;
+};
+struct DPiece {  // element (i, j) of the piece = arena[off + i + j * ld], multiplies x[xc0 + j]
+    i64 off, ld, xc0;
+    int32_t ncols;
+};
+struct LPiece {  // U rows of the piece at arena[off + i + c * ld]; t_b from chunk partials [cbeg, cend)
+    i64 off, ld;
+    int32_t slot, cbeg, cend;
+};
+struct VChunk {  // V rows at arena[voff + i + c * ld], i < len, multiplies x[xc0 + i]
+    i64 voff, ld, xc0;
+    int32_t len, slot;
+};
+
+struct MvPlan {
+    int nseg = 0, nch = 0;
+    i64 n_dpieces = 0, n_lpieces = 0;
+    SegDesc *segs = nullptr;
+    DPiece *dp = nullptr;
+    LPiece *lp = nullptr;
+    VChunk *chunks = nullptr;
+    double *part = nullptr;
+    ~MvPlan();
+};
+
+std::shared_ptr<MvPlan> build_mv_plan(const HMat &H, const std::vector<int32_t> &blocks,
+                                      cudaStream_t s);
+void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
+            cudaStream_t s, int num_sms);
+MvPlan &get_mv_plan(HMat &H, cudaStream_t s);
+void matvec(Ctx &ctx, HMat &H, const double *x, i64 ldx, double *y, i64 ldy, int nrhs);
+
+}  // namespace lh

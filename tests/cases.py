@@ -1,0 +1,45 @@
+"""Shared parity-case definitions (parameters of tests/golden/*.npz)."""
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+CASES = {
+    # name: (measure spec, L, n, L_W, tail or None)
+    "cfg1": (("power", 0.5), 1.0, 512, 2.0),
+    "cfg2_s025": (("power", 0.25), 1.0, 1024, 2.0),
+    "cfg2_s075": (("power", 0.75), 1.0, 1024, 2.0),
+    "cfg3_cgmy": (("cgmy", 1.0, 5.0, 10.0, 0.5), 4.0, 512, 8.0),
+    "cfg5_s08": (("power", 0.8), 1.0, 512, 2.0),
+}
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+
+
+def make_system(name, g=None):
+    """FracCNSystem with exactly the golden case's parameters."""
+    import paper_1812_08324_b200 as P
+
+    g = g if g is not None else load(name)
+    spec, L, n, L_W = CASES[name]
+    if spec[0] == "power":
+        nu = P.power_measure(1, spec[1])
+        tail = None
+        b = float(g["b_eff"])
+        drift = False
+    else:
+        nu = P.cgmy_measure(*spec[1:])
+        sc = load("cfg3_scalars")
+        tail = float(sc["tail"])
+        b = float(g["b_eff"]) - float(sc["beta"])
+        drift = True
+    sys_ = P.FracCNSystem(nu, float(g["a"]), b, float(g["c"]), n, float(g["dt"]), L=L, L_W=L_W,
+                          tail_mass=tail, drift_compensation=drift)
+    return sys_
+
+
+def struct_from_golden(arr):
+    return arr.copy()

@@ -1,0 +1,104 @@
+"""CPU-only checks of the native library: it loads, exports every symbol the
+public header declares, and its host logic (cluster tree, block partition)
+is bit-identical to the oracle / the reference golden pins."""
+import hashlib
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import levyh_oracle as O
+from paper_1812_08324_b200 import _lib
+from paper_1812_08324_b200.geometry import build_cluster_tree
+from paper_1812_08324_b200.hmatrix import HConfig, partition_array
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "levyh_b200.h")).read()
+    declared = set(re.findall(r"\b(lh_[a-z0-9_]+)\s*\(", hdr))
+    assert len(declared) >= 20
+    L = _lib.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    bound = {s[0] for s in _lib.SIGNATURES}
+    assert declared == bound
+
+
+def _oracle_nodes(root):
+    out = []
+    st = [root]
+    while st:
+        c = st.pop()
+        out.append((c.lo, c.hi, tuple(c.blo), tuple(c.bhi)))
+        if c.kids:
+            st.extend(reversed(c.kids))
+    return out
+
+
+def _native_nodes(ct):
+    out = []
+    st = [ct.root]
+    while st:
+        c = st.pop()
+        out.append((c.start, c.end, tuple(c.bbox_lo), tuple(c.bbox_hi)))
+        st.extend(reversed(c.children))
+    return out
+
+
+@pytest.mark.parametrize("dim,n,leaf", [(1, 1023, 32), (1, 777, 16), (2, 500, 20), (1, 1, 4)])
+def test_tree_matches_oracle_unsorted(dim, n, leaf):
+    rng = np.random.default_rng(n)
+    pts = rng.standard_normal((n, dim))
+    if n > 3:
+        pts[::7] = pts[3]  # ties exercise the stable argsort
+    ct = build_cluster_tree(pts, leaf_size=leaf)
+    root, order = O.cluster_tree(pts, leaf)
+    assert np.array_equal(ct.perm.inverse, order)
+    assert _native_nodes(ct) == _oracle_nodes(root)
+    v = rng.standard_normal(n)
+    assert np.array_equal(ct.perm.from_tree(ct.perm.to_tree(v)), v)
+
+
+def test_tree_errors():
+    with pytest.raises(ValueError):
+        build_cluster_tree(np.zeros((0, 1)))
+    with pytest.raises(ValueError):
+        build_cluster_tree(np.array([0.0, np.nan]))
+    with pytest.raises(ValueError):
+        build_cluster_tree(np.zeros(4), leaf_size=0)
+    with pytest.raises(ValueError):
+        build_cluster_tree(np.zeros(4), strategy="nope")
+
+
+def test_partition_matches_oracle_small():
+    N = 1023
+    x = (2.0 / (N + 1)) * np.arange(-(N // 2), N // 2 + 1)
+    ct = build_cluster_tree(x[:, None], leaf_size=32)
+    recs, nh = partition_array(ct, ct, HConfig(n_min=32, eps1=1e-10))
+    root, _ = O.cluster_tree(x, 32)
+    H = O.compress_dense(np.eye(N), root, 1e-10, 32)
+    st = O.structure(H)
+    assert np.array_equal(recs, st[:, :5])
+    assert nh == 83
+
+
+@pytest.mark.parametrize("tag", ["cfg1", "cfg2", "cfg4", "cfg3", "cfg5"])
+def test_partition_matches_reference_pins(tag, golden_dir):
+    p = json.load(open(os.path.join(golden_dir, "partitions.json")))[tag]
+    N, leaf = p["N"], p["leaf"]
+    lo = -4.0 if tag == "cfg3" else -1.0
+    hh = (-2 * lo) / (N + 1)
+    x = hh * np.arange(-(N // 2), N // 2 + 1)
+    ct = build_cluster_tree(x[:, None], leaf_size=leaf)
+    assert np.array_equal(ct.perm.inverse, np.arange(N)) == p["identity_perm"]
+    recs, nh = partition_array(ct, ct, HConfig(n_min=leaf))
+    assert int((recs[:, 4] == 0).sum()) == p["dense"]
+    assert int((recs[:, 4] == 1).sum()) == p["lowrank"]
+    assert nh == p["hier"]
+    lr = recs[recs[:, 4] == 1]
+    assert int(((lr[:, 1] - lr[:, 0]) + (lr[:, 3] - lr[:, 2])).sum()) == p["sum_mn_lowrank"]
+    assert hashlib.sha256(np.ascontiguousarray(recs).tobytes()).hexdigest() == p["sha256"]
