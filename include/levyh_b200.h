@@ -61,6 +61,12 @@ int lh_tree_order(const lh_tree *t, int64_t *order_host);
 int lh_partition(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
                  int64_t *recs_host, int64_t *nblocks, int64_t *nhier);
 
+/* Host-only planning statistics of the H-LU / solve task DAGs for the partition of
+ * (rt, ct) (no GPU): stats[0..7] = lu tasks, lu deps, lu temp doubles, lu plan seconds,
+ * solve tasks, solve deps, solve critical-path tasks, lu critical-path tasks. */
+int lh_plan_stats(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
+                  int kcap, double *stats_host);
+
 /* ---- H-matrix construction: hmatrix.py:121-137 HConfig, :306-340 build_from_dense */
 typedef struct {
     int32_t n_min;        /* HConfig.n_min                                   */

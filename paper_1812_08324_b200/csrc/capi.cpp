@@ -3,6 +3,7 @@
 
 #include "core.h"
 #include "matvec.h"
+#include "plan_impl.h"
 
 struct lh_ctx {
     lh::Ctx c;
@@ -171,6 +172,43 @@ int lh_partition(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, d
                 r[3] = nd.c0 + nd.n;
                 r[4] = nd.kind == K_LR ? 1 : 0;
             }
+    });
+}
+
+int lh_plan_stats(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
+                  int kcap, double *stats) {
+    return guard(nullptr, [&] {
+        HMat H;
+        partition(H, *rt->t, *ct->t, n_min, n_block, eta);
+        i64 off = 0;
+        int32_t slots = 0;
+        for (int32_t b : H.leafblocks) {
+            Node &nd = H.nodes[b];
+            if (nd.kind == K_DENSE) {
+                nd.doff = off;
+                off += nd.m * nd.n;
+            } else if (nd.kind == K_LR) {
+                nd.kcap = kcap;
+                nd.rslot = slots++;
+                nd.uoff = off;
+                off += nd.m * kcap;
+                nd.voff = off;
+                off += nd.n * kcap;
+            }
+        }
+        H.nslots = slots;
+        i64 pl = 0;
+        auto P = plan_hlu(H, 1e-10, pl);
+        stats[0] = (double)P->tasks.size();
+        stats[1] = (double)P->deps.size();
+        stats[2] = (double)P->temp_len;
+        stats[3] = P->build_seconds;
+        stats[7] = (double)critical_path(*P);
+        H.factored = true;
+        auto S = plan_solve(H, H.nrows, 1);
+        stats[4] = (double)S->tasks.size();
+        stats[5] = (double)S->deps.size();
+        stats[6] = (double)critical_path(*S);
     });
 }
 

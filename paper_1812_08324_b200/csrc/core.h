@@ -96,6 +96,7 @@ struct HMat {
     int32_t *d_perm = nullptr;        // FDENSE permutations
     i64 perm_len = 0;
     bool factored = false;
+    double lu_stats[4] = {0, 0, 0, 0};  // tasks, plan seconds, temp bytes, -
     // lazily built plans (opaque; see matvec.cu / plan.cpp)
     std::shared_ptr<void> mv_plan;
     std::shared_ptr<void> solve_plan;

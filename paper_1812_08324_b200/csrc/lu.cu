@@ -1,0 +1,714 @@
+// Persistent dataflow executor for the static H-arithmetic DAG (plan.cpp) and
+// the host drivers of H-LU (hops.py:392-421), solve (hops.py:424-432), the
+// triangular-inverse factors of the fast solve, and the CN stepping loop
+// (levy.py:309-330).
+//
+// One 256-thread CTA per SM claims tasks in the planner's (critical-path
+// ordered, topological) order from a global counter, spins until every
+// predecessor has published its completion flag, runs the task, then
+// publishes its own flag with release semantics.  All CTAs are co-resident
+// (cooperative launch), so the claim order guarantees progress.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "core.h"
+#include "dev.cuh"
+#include "matvec.h"
+#include "plan_impl.h"
+
+namespace lh {
+
+using dev::KA_MAX;
+using dev::KC_MAX;
+using dev::NT;
+
+struct ExecArgs {
+    const DTask *tasks;
+    int32_t ntasks;
+    const int32_t *deps;
+    const DPiece *pieces;
+    int32_t *done;
+    int32_t *counter;
+    int32_t *err;  // [0] code, [1] task, [2] path
+    double *base[4];
+    int32_t *ranks;
+    int32_t *perm;
+};
+
+constexpr int SMEM_BYTES = 168 * 1024;
+
+__device__ __forceinline__ double *vp(const ExecArgs &A, const DView &v) { return A.base[v.base] + v.off; }
+__device__ __forceinline__ i64 vi(const DView &v, i64 i, i64 j) {
+    return v.trans ? j + i * (i64)v.ld : i + j * (i64)v.ld;
+}
+__device__ __forceinline__ int vcols(const ExecArgs &A, const DView &v) {
+    return v.wslot >= 0 ? A.ranks[v.wslot] : v.cols;
+}
+__device__ __forceinline__ void set_err(const ExecArgs &A, int code, int task, int path) {
+    if (atomicCAS(&A.err[0], 0, code) == 0) {
+        A.err[1] = task;
+        A.err[2] = path;
+    }
+}
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int32_t *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// GETRF: partial pivoting LU of a dense m x m leaf (sla.lu_factor, hops.py:394)
+// ---------------------------------------------------------------------------
+__device__ void task_getrf(const ExecArgs &A, const DTask &T, int tid, double *sm) {
+    const DView &v = T.v[0];
+    const int m = v.rows;
+    double *G = vp(A, v);
+    double *S = sm;                       // m x m, column-major
+    int *piv = (int *)(sm + m * m);
+    __shared__ int s_p;
+    for (int e = threadIdx.x; e < m * m; e += NT) S[e] = G[vi(v, e % m, e / m)];
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = 0; j < m; ++j) {
+        // pivot: first index of max |A[i, j]|, i >= j (idamax)
+        if (w == 0) {
+            double best = -1.0;
+            int bi = j;
+            for (int i = j + lane; i < m; i += 32) {
+                double a = fabs(S[i + j * m]);
+                if (a > best) {
+                    best = a;
+                    bi = i;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                s_p = bi;
+                piv[j] = bi;
+            }
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (p != j)
+            for (int c = threadIdx.x; c < m; c += NT) {
+                double t = S[j + c * m];
+                S[j + c * m] = S[p + c * m];
+                S[p + c * m] = t;
+            }
+        __syncthreads();
+        const double d = S[j + j * m];
+        if (d != 0.0)
+            for (int i = j + 1 + threadIdx.x; i < m; i += NT) S[i + j * m] /= d;
+        __syncthreads();
+        const int rem = m - j - 1;
+        for (int e = threadIdx.x; e < rem * rem; e += NT) {
+            int i = j + 1 + e % rem, c = j + 1 + e / rem;
+            S[i + c * m] -= S[i + j * m] * S[j + c * m];
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < m * m; e += NT) G[vi(v, e % m, e / m)] = S[e];
+    if (threadIdx.x == 0) {
+        // net permutation P^T b == b[perm] (hops.py:171-177)
+        int32_t *pp = A.perm + T.aux;
+        for (int i = 0; i < m; ++i) pp[i] = i;
+        for (int i = 0; i < m; ++i) {
+            int q = piv[i];
+            if (q != i) {
+                int t = pp[i];
+                pp[i] = pp[q];
+                pp[q] = t;
+            }
+        }
+        for (int i = 0; i < m; ++i)
+            if (S[i + i * m] == 0.0) {
+                set_err(A, LH_ESINGULAR, tid, T.path);
+                break;
+            }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TRSM with a factored leaf: mode 0 unit-L with the leaf permutation, 1 U, 2 U^T
+// (dtrsm in _leaf_solve, hops.py:185-208)
+// ---------------------------------------------------------------------------
+__device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
+    const DView &tv = T.v[0];
+    const DView &bv = T.v[1];
+    const int m = tv.rows;
+    const int mode = T.flags & 15;
+    const double *Tg = vp(A, tv);
+    double *Bg = vp(A, bv);
+    const int k = vcols(A, bv);
+    if (k <= 0) return;
+    double *Ts = sm;
+    double *Bs = sm + m * m;
+    const int32_t *perm = A.perm + T.aux;
+    for (int e = threadIdx.x; e < m * m; e += NT) Ts[e] = Tg[vi(tv, e % m, e / m)];
+    const int CW = 32;
+    for (int c0 = 0; c0 < k; c0 += CW) {
+        const int kc = min(CW, k - c0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < m * kc; e += NT) {
+            int i = e % m, c = e / m;
+            int src = (mode == 0) ? perm[i] : i;
+            Bs[e] = Bg[vi(bv, src, c0 + c)];
+        }
+        __syncthreads();
+        if (mode == 0) {
+            for (int l = 0; l < m - 1; ++l) {
+                const int rem = m - l - 1;
+                for (int e = threadIdx.x; e < rem * kc; e += NT) {
+                    int i = l + 1 + e % rem, c = e / rem;
+                    Bs[i + c * m] -= Ts[i + l * m] * Bs[l + c * m];
+                }
+                __syncthreads();
+            }
+        } else if (mode == 1) {
+            for (int l = m - 1; l >= 0; --l) {
+                for (int c = threadIdx.x; c < kc; c += NT) Bs[l + c * m] /= Ts[l + l * m];
+                __syncthreads();
+                for (int e = threadIdx.x; e < l * kc; e += NT) {
+                    int i = e % l, c = e / l;
+                    Bs[i + c * m] -= Ts[i + l * m] * Bs[l + c * m];
+                }
+                __syncthreads();
+            }
+        } else {
+            for (int l = 0; l < m; ++l) {
+                for (int c = threadIdx.x; c < kc; c += NT) Bs[l + c * m] /= Ts[l + l * m];
+                __syncthreads();
+                const int rem = m - l - 1;
+                for (int e = threadIdx.x; e < rem * kc; e += NT) {
+                    int i = l + 1 + e % rem, c = e / rem;
+                    Bs[i + c * m] -= Ts[l + i * m] * Bs[l + c * m];
+                }
+                __syncthreads();
+            }
+        }
+        for (int e = threadIdx.x; e < m * kc; e += NT) Bg[vi(bv, e % m, c0 + e / m)] = Bs[e];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SEGMUL: Y_seg = beta Y_seg + alpha * sum of pieces (mul_dense/tmul_dense rows)
+// ---------------------------------------------------------------------------
+__device__ void task_segmul(const ExecArgs &A, const DTask &T, double *sm) {
+    const DView &yv = T.v[0];
+    const int s = yv.rows;
+    const int k = vcols(A, yv);
+    double *Yg = vp(A, yv);
+    const bool overwrite = T.flags & 1;
+    const int RP = s <= 64 ? 64 : (s <= 128 ? 128 : 256);
+    const int G = NT / RP;            // thread groups over columns
+    const int i = threadIdx.x % RP, g = threadIdx.x / RP;
+    constexpr int NA = 16;
+    const int CW = NA * G;            // columns per chunk
+    for (int c0 = 0; c0 < k; c0 += CW) {
+        double acc[NA];
+#pragma unroll
+        for (int q = 0; q < NA; ++q) acc[q] = 0.0;
+        for (int p = T.pc_beg; p < T.pc_end; ++p) {
+            const DPiece pc = A.pieces[p];
+            const double *M = vp(A, pc.mat);
+            const double *X = vp(A, pc.x);
+            const int inner = pc.kind == 0 ? pc.mat.cols : vcols(A, pc.mat);
+            if (i < s) {
+                for (int j = 0; j < inner; ++j) {
+                    const double a = M[vi(pc.mat, i, j)];
+#pragma unroll
+                    for (int q = 0; q < NA; ++q) {
+                        int c = c0 + g + q * G;
+                        if (c < k) acc[q] += a * X[vi(pc.x, j, c)];
+                    }
+                }
+            }
+        }
+        if (i < s) {
+#pragma unroll
+            for (int q = 0; q < NA; ++q) {
+                int c = c0 + g + q * G;
+                if (c < k) {
+                    double &y = Yg[vi(yv, i, c)];
+                    y = (overwrite ? 0.0 : y) + T.alpha * acc[q];
+                }
+            }
+        }
+    }
+    (void)sm;
+}
+
+// ---------------------------------------------------------------------------
+// VTX: W (r x k, ld KC) = F^T X, F (n x r), X (n x k)
+// ---------------------------------------------------------------------------
+__device__ void task_vtx(const ExecArgs &A, const DTask &T, double *sm) {
+    const DView &fv = T.v[0], &xv = T.v[1], &wv = T.v[2];
+    const int n = fv.rows;
+    const int r = vcols(A, fv);
+    const int k = vcols(A, xv);
+    const double *F = vp(A, fv);
+    const double *X = vp(A, xv);
+    double *W = vp(A, wv);
+    if (r == 0 || k == 0) return;
+    constexpr int CH = 64;
+    double *Fs = sm;                 // CH x r
+    double *Xs = sm + CH * KC_MAX;   // CH x k (k <= 128)
+    constexpr int NP = 16;
+    const int npair = r * k;
+    double acc[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) acc[q] = 0.0;
+    for (int j0 = 0; j0 < n; j0 += CH) {
+        const int len = min(CH, n - j0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < len * r; e += NT) Fs[e] = F[vi(fv, j0 + e % len, e / len)];
+        for (int e = threadIdx.x; e < len * k; e += NT) Xs[e] = X[vi(xv, j0 + e % len, e / len)];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            int p = threadIdx.x + q * NT;
+            if (p < npair) {
+                int l = p % r, c = p / r;
+                double s = 0.0;
+                for (int j = 0; j < len; ++j) s += Fs[j + l * len] * Xs[j + c * len];
+                acc[q] += s;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        int p = threadIdx.x + q * NT;
+        if (p < npair) {
+            int l = p % r, c = p / r;
+            W[l + c * (i64)wv.ld] = acc[q];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// LRADD: C = C + alpha U2 V2^T recompressed at eps2 (_add_lr, hops.py:134-144)
+// ---------------------------------------------------------------------------
+__device__ void task_lradd(const ExecArgs &A, const DTask &T, int tid, double *sm) {
+    const DView &cu = T.v[0], &cv = T.v[1], &u2 = T.v[2], &v2 = T.v[3];
+    const int r2 = vcols(A, u2);
+    if (r2 == 0) return;
+    const int slot = cu.wslot;
+    const int r1 = A.ranks[slot];
+    const int K = r1 + r2;
+    const int kcap = cu.cols;
+    if (K > kcap || K > KA_MAX) {
+        if (threadIdx.x == 0) set_err(A, LH_ERANK, tid, -1);
+        return;
+    }
+    const i64 m = cu.rows, n = cv.rows;
+    double *U = vp(A, cu);
+    double *V = vp(A, cv);
+    const double *U2 = vp(A, u2);
+    const double *V2 = vp(A, v2);
+    for (i64 e = threadIdx.x; e < m * r2; e += NT) {
+        i64 i = e % m, c = e / m;
+        U[i + (r1 + c) * (i64)cu.ld] = T.alpha * U2[vi(u2, i, c)];
+    }
+    for (i64 e = threadIdx.x; e < n * r2; e += NT) {
+        i64 i = e % n, c = e / n;
+        V[i + (r1 + c) * (i64)cv.ld] = V2[vi(v2, i, c)];
+    }
+    __syncthreads();
+    dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(sm);
+    int r = dev::recompress(U, cu.ld, m, V, cv.ld, n, K, 1, T.alpha2, U, cu.ld, V, cv.ld,
+                            min(kcap, KC_MAX), S);
+    if (threadIdx.x == 0) {
+        if (r > min(kcap, KC_MAX)) set_err(A, LH_ERANK, tid, -1);
+        else A.ranks[slot] = r;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// small dense kernels
+// ---------------------------------------------------------------------------
+__device__ void task_dgemm(const ExecArgs &A, const DTask &T) {
+    const DView &cv = T.v[0], &av = T.v[1], &bv = T.v[2];
+    const bool transB = T.flags & 1, overwrite = T.flags & 2;
+    const int m = cv.rows, n = cv.cols;
+    const int inner = vcols(A, av);
+    double *C = vp(A, cv);
+    const double *Am = vp(A, av);
+    const double *Bm = vp(A, bv);
+    for (int e = threadIdx.x; e < m * n; e += NT) {
+        int i = e % m, j = e / m;
+        double s = 0.0;
+        for (int l = 0; l < inner; ++l)
+            s += Am[vi(av, i, l)] * (transB ? Bm[vi(bv, j, l)] : Bm[vi(bv, l, j)]);
+        double &c = C[vi(cv, i, j)];
+        c = (overwrite ? 0.0 : c) + T.alpha * s;
+    }
+}
+
+__device__ void task_dadd(const ExecArgs &A, const DTask &T) {
+    const DView &cv = T.v[0], &dv = T.v[1];
+    double *C = vp(A, cv);
+    const double *D = vp(A, dv);
+    for (int e = threadIdx.x; e < cv.rows * cv.cols; e += NT) {
+        int i = e % cv.rows, j = e / cv.rows;
+        C[vi(cv, i, j)] += T.alpha * D[vi(dv, i, j)];
+    }
+}
+
+__device__ void task_densify(const ExecArgs &A, const DTask &T) {
+    const DView &dv = T.v[0], &sv = T.v[1], &v2 = T.v[2];
+    double *D = vp(A, dv);
+    const double *S = vp(A, sv);
+    if (T.flags & 1) {
+        const int r = vcols(A, sv);
+        const double *V = vp(A, v2);
+        for (int e = threadIdx.x; e < dv.rows * dv.cols; e += NT) {
+            int i = e % dv.rows, j = e / dv.rows;
+            double s = 0.0;
+            for (int l = 0; l < r; ++l) s += S[vi(sv, i, l)] * V[vi(v2, j, l)];
+            D[vi(dv, i, j)] = s;
+        }
+    } else {
+        for (int e = threadIdx.x; e < dv.rows * dv.cols; e += NT) {
+            int i = e % dv.rows, j = e / dv.rows;
+            D[vi(dv, i, j)] = S[vi(sv, i, j)];
+        }
+    }
+}
+
+__device__ void task_ident(const ExecArgs &A, const DTask &T) {
+    const DView &dv = T.v[0];
+    double *D = vp(A, dv);
+    const bool zero = T.flags & 1;
+    const int k = vcols(A, dv);
+    for (int e = threadIdx.x; e < dv.rows * k; e += NT) {
+        int i = e % dv.rows, j = e / dv.rows;
+        D[vi(dv, i, j)] = (!zero && i == j) ? 1.0 : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the persistent executor
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
+    extern __shared__ double4 smem_raw[];
+    double *sm = reinterpret_cast<double *>(smem_raw);
+    __shared__ int s_t;
+    __shared__ DTask s_task;
+    while (true) {
+        if (threadIdx.x == 0) s_t = atomicAdd(A.counter, 1);
+        __syncthreads();
+        const int t = s_t;
+        if (t >= A.ntasks) return;
+        if (threadIdx.x == 0) s_task = A.tasks[t];
+        __syncthreads();
+        const DTask &T = s_task;
+        if (threadIdx.x < 32) {
+            for (int q = threadIdx.x; q < T.dep_cnt; q += 32) {
+                const int p = A.deps[T.dep_beg + q];
+                long long spins = 0;
+                while (ld_acquire(A.done + p) == 0) {
+                    __nanosleep(100);
+                    if (++spins > (1ll << 27)) {  // watchdog (~>10 s): never hang the GPU
+                        set_err(A, LH_EINTERNAL, t, -2);
+                        break;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        __threadfence();  // acquire side: drop stale L1 lines before reading operands
+        switch (T.type) {
+            case T_GETRF: task_getrf(A, T, t, sm); break;
+            case T_TRSM: task_trsm(A, T, sm); break;
+            case T_SEGMUL: task_segmul(A, T, sm); break;
+            case T_VTX: task_vtx(A, T, sm); break;
+            case T_LRADD: task_lradd(A, T, t, sm); break;
+            case T_DGEMM: task_dgemm(A, T); break;
+            case T_DADD: task_dadd(A, T); break;
+            case T_DENSIFY: task_densify(A, T); break;
+            case T_IDENT: task_ident(A, T); break;
+            default: break;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release(A.done + t, 1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+Plan::~Plan() {
+    cudaFree(d_tasks);
+    cudaFree(d_deps);
+    cudaFree(d_pieces);
+    cudaFree(d_done);
+    cudaFree(d_temp);
+    cudaFree(d_ranks);
+    cudaFree(d_err);
+}
+
+void Plan::upload(cudaStream_t s) {
+    d_tasks = dupload(tasks, s);
+    d_deps = dupload(deps, s);
+    d_pieces = dupload(pieces, s);
+    d_done = dalloc<int32_t>((i64)tasks.size() + 1);
+    d_temp = dalloc<double>(std::max<i64>(temp_len, 1));
+    d_ranks = dalloc<int32_t>(std::max(nslots_total + 1, 1));
+    d_err = dalloc<int32_t>(4);
+    LH_CUDA(cudaStreamSynchronize(s));
+}
+
+static int exec_grid(Ctx &ctx) {
+    static bool attr = false;
+    if (!attr) {
+        LH_CUDA(cudaFuncSetAttribute((const void *)exec_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr = true;
+    }
+    int per_sm = 0;
+    LH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, exec_kernel, NT, SMEM_BYTES));
+    LH_REQUIRE(per_sm >= 1, LH_EINTERNAL, "executor kernel cannot be resident");
+    return ctx.num_sms * per_sm;
+}
+
+// Run a plan; F / X / RHS bases.  Ranks of F (and X) are copied in and back out.
+static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val) {
+    cudaStream_t s = ctx.stream;
+    LH_CUDA(cudaMemsetAsync(P.d_done, 0, sizeof(int32_t) * (P.tasks.size() + 1), s));
+    LH_CUDA(cudaMemsetAsync(P.d_err, 0, sizeof(int32_t) * 4, s));
+    if (F.nslots)
+        LH_CUDA(cudaMemcpyAsync(P.d_ranks, F.d_ranks, sizeof(int32_t) * F.nslots,
+                                cudaMemcpyDeviceToDevice, s));
+    if (X && X->nslots)
+        LH_CUDA(cudaMemcpyAsync(P.d_ranks + P.slot_off_x, X->d_ranks, sizeof(int32_t) * X->nslots,
+                                cudaMemcpyDeviceToDevice, s));
+    if (rhs_slot_val >= 0)
+        LH_CUDA(cudaMemcpyAsync(P.d_ranks + P.rhs_slot, &rhs_slot_val, sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+    ExecArgs A;
+    A.tasks = P.d_tasks;
+    A.ntasks = (int32_t)P.tasks.size();
+    A.deps = P.d_deps;
+    A.pieces = P.d_pieces;
+    A.done = P.d_done;
+    A.counter = P.d_done + P.tasks.size();
+    A.err = P.d_err;
+    A.base[B_F] = F.d_arena;
+    A.base[B_TMP] = P.d_temp;
+    A.base[B_RHS] = rhs;
+    A.base[B_X] = X ? X->d_arena : nullptr;
+    A.ranks = P.d_ranks;
+    A.perm = F.d_perm;
+    if (A.ntasks > 0) {
+        int grid = exec_grid(ctx);
+        void *args[] = {&A};
+        LH_CUDA(cudaLaunchCooperativeKernel((const void *)exec_kernel, grid, NT, args, SMEM_BYTES, s));
+    }
+    int err[4];
+    LH_CUDA(cudaMemcpyAsync(err, P.d_err, sizeof(err), cudaMemcpyDeviceToHost, s));
+    LH_CUDA(cudaStreamSynchronize(s));
+    if (F.nslots)
+        LH_CUDA(cudaMemcpyAsync(F.d_ranks, P.d_ranks, sizeof(int32_t) * F.nslots,
+                                cudaMemcpyDeviceToDevice, s));
+    if (X && X->nslots)
+        LH_CUDA(cudaMemcpyAsync(X->d_ranks, P.d_ranks + P.slot_off_x, sizeof(int32_t) * X->nslots,
+                                cudaMemcpyDeviceToDevice, s));
+    LH_CUDA(cudaStreamSynchronize(s));
+    if (err[0] == LH_ESINGULAR) {
+        std::string msg = err[2] >= 0 && err[2] < (int)P.paths.size() ? P.paths[err[2]]
+                                                                      : "singular diagonal block";
+        throw Error(LH_ESINGULAR, msg);
+    }
+    if (err[0] == LH_ERANK)
+        throw Error(LH_ERANK, "low-rank capacity exceeded during H-arithmetic (increase kcap)");
+    if (err[0] != 0) throw Error(err[0], "executor failure (task " + std::to_string(err[1]) + ")");
+}
+
+void hlu(Ctx &ctx, HMat &F, double eps2) {
+    LH_REQUIRE(F.nrows == F.ncols, LH_EINVAL, "LU requires a square matrix");
+    LH_REQUIRE(!F.factored, LH_EINVAL, "matrix is already factored");
+    i64 perm_len = 0;
+    auto P = plan_hlu(F, eps2, perm_len);  // marks diagonal leaves K_FDENSE
+    F.d_perm = dalloc<int32_t>(std::max<i64>(perm_len, 1));
+    F.perm_len = perm_len;
+    P->upload(ctx.stream);
+    F.factored = true;
+    F.mv_plan.reset();
+    run_plan(ctx, *P, F, nullptr, nullptr, -1);
+    F.sync_ranks(ctx.stream);
+    F.lu_stats[0] = (double)P->tasks.size();
+    F.lu_stats[1] = P->build_seconds;
+    F.lu_stats[2] = (double)P->temp_len * 8.0;
+}
+
+struct SolvePlans {
+    std::shared_ptr<Plan> sub;  // substitution DAG
+    int cap = 0;
+    std::shared_ptr<HMat> XL, XU;   // triangular inverses
+    std::shared_ptr<MvPlan> mvL, mvU;
+    double *tmp = nullptr;          // scratch vector(s)
+    i64 tmp_len = 0;
+    ~SolvePlans() {
+        if (tmp) cudaFree(tmp);
+    }
+};
+
+static SolvePlans &plans_of(HMat &F) {
+    if (!F.solve_plan) F.solve_plan = std::make_shared<SolvePlans>();
+    return *static_cast<SolvePlans *>(F.solve_plan.get());
+}
+
+static void solve_substitution(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
+    LH_REQUIRE(ldb == F.nrows, LH_EINVAL, "solve expects a packed right-hand side (ldb == n)");
+    SolvePlans &S = plans_of(F);
+    const int CAP = 64;
+    if (!S.sub) {
+        S.sub = plan_solve(F, F.nrows, CAP);
+        S.sub->upload(ctx.stream);
+    }
+    for (int c0 = 0; c0 < nrhs; c0 += CAP) {
+        int kc = std::min(CAP, nrhs - c0);
+        run_plan(ctx, *S.sub, F, nullptr, b + (i64)c0 * ldb, kc);
+    }
+}
+
+// X: same block tree as F restricted to one triangle; other-triangle leaves are K_ZERO.
+static std::shared_ptr<HMat> make_triangle(const HMat &F, bool lower, int kcap) {
+    auto X = std::make_shared<HMat>();
+    X->rt = F.rt;
+    X->ct = F.ct;
+    X->rt_hold = F.rt_hold;
+    X->ct_hold = F.ct_hold;
+    X->nrows = F.nrows;
+    X->ncols = F.ncols;
+    X->root = F.root;
+    X->nodes = F.nodes;
+    X->leafblocks = F.leafblocks;
+    i64 off = 0;
+    int32_t slots = 0;
+    for (int32_t b : X->leafblocks) {
+        Node &nd = X->nodes[b];
+        bool diag = (nd.r0 == nd.c0 && nd.m == nd.n);
+        bool other = lower ? (nd.c0 >= nd.r0 + nd.m) : (nd.r0 >= nd.c0 + nd.n);
+        if (other && !diag) {
+            nd.kind = K_ZERO;
+            continue;
+        }
+        if (nd.kind == K_FDENSE || nd.kind == K_DENSE) {
+            nd.kind = K_DENSE;
+            nd.doff = off;
+            off += nd.m * nd.n;
+        } else if (nd.kind == K_LR) {
+            nd.kcap = kcap;
+            nd.rslot = slots++;
+            nd.uoff = off;
+            off += nd.m * kcap;
+            nd.voff = off;
+            off += nd.n * kcap;
+        }
+    }
+    X->arena_len = off;
+    X->d_arena = dalloc<double>(std::max<i64>(off, 1));
+    X->nslots = slots;
+    X->d_ranks = dalloc<int32_t>(std::max(slots, 1));
+    LH_CUDA(cudaMemset(X->d_ranks, 0, sizeof(int32_t) * std::max(slots, 1)));
+    return X;
+}
+
+void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
+    LH_REQUIRE(F.factored, LH_EINVAL, "prepare_inverse needs an H-LU factorization");
+    SolvePlans &S = plans_of(F);
+    if (S.XL) return;
+    int kcap = KC_MAX;
+    for (int mode = 0; mode < 2; ++mode) {
+        auto X = make_triangle(F, mode == 0, kcap);
+        walk_leaves(*X);
+        auto P = plan_inverse(F, *X, mode, eps2);
+        P->upload(ctx.stream);
+        run_plan(ctx, *P, F, X.get(), nullptr, -1);
+        X->sync_ranks(ctx.stream);
+        std::vector<int32_t> blocks;
+        for (int32_t b : X->leafblocks)
+            if (X->nodes[b].kind != K_ZERO) blocks.push_back(b);
+        auto mv = build_mv_plan(*X, blocks, ctx.stream);
+        if (mode == 0) {
+            S.XL = X;
+            S.mvL = mv;
+        } else {
+            S.XU = X;
+            S.mvU = mv;
+        }
+    }
+    S.tmp_len = F.nrows;
+    S.tmp = dalloc<double>(S.tmp_len);
+}
+
+static void solve_inverse(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
+    SolvePlans &S = plans_of(F);
+    LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
+    for (int q = 0; q < nrhs; ++q) {
+        double *bq = b + (i64)q * ldb;
+        mv_run(*S.mvL, *S.XL, bq, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
+        mv_run(*S.mvU, *S.XU, S.tmp, bq, 1.0, 0.0, ctx.stream, ctx.num_sms);
+    }
+}
+
+void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method) {
+    LH_REQUIRE(F.factored, LH_EINVAL, "solve needs an H-LU factorization");
+    if (nrhs <= 0) return;
+    if (method == 0) solve_substitution(ctx, F, b, ldb, nrhs);
+    else solve_inverse(ctx, F, b, ldb, nrhs);
+}
+
+void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method) {
+    LH_REQUIRE(F.factored, LH_EINVAL, "cn_steps needs an H-LU factorization of A+");
+    LH_REQUIRE(Hm.nrows == F.nrows, LH_EINVAL, "operator sizes differ");
+    MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
+    double *y = (double *)ctx.ensure_scratch(sizeof(double) * (size_t)Hm.nrows);
+    if (method == 1) {
+        SolvePlans &S = plans_of(F);
+        LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
+        // one step = 3 H-matvecs (6 kernels), captured once as a CUDA graph
+        for (int q = 0; q < nrhs; ++q) {
+            double *uq = u + (i64)q * ldu;
+            cudaGraph_t g;
+            cudaGraphExec_t ge;
+            LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+            mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+            mv_run(*S.mvL, *S.XL, y, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
+            mv_run(*S.mvU, *S.XU, S.tmp, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
+            LH_CUDA(cudaStreamEndCapture(ctx.stream, &g));
+            LH_CUDA(cudaGraphInstantiate(&ge, g, 0));
+            for (int k = 0; k < nsteps; ++k) LH_CUDA(cudaGraphLaunch(ge, ctx.stream));
+            LH_CUDA(cudaStreamSynchronize(ctx.stream));
+            cudaGraphExecDestroy(ge);
+            cudaGraphDestroy(g);
+        }
+        return;
+    }
+    for (int q = 0; q < nrhs; ++q) {
+        double *uq = u + (i64)q * ldu;
+        for (int k = 0; k < nsteps; ++k) {
+            mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+            LH_CUDA(cudaMemcpyAsync(uq, y, sizeof(double) * Hm.nrows, cudaMemcpyDeviceToDevice,
+                                    ctx.stream));
+            solve_substitution(ctx, F, uq, Hm.nrows, 1);
+        }
+    }
+}
+
+}  // namespace lh

@@ -47,8 +47,8 @@ __global__ void __launch_bounds__(NT) vtx_kernel(const VChunk *chunks, int nch, 
     }
 }
 
-__global__ void __launch_bounds__(NT) seg_kernel(const SegDesc *segs, int nseg, const DPiece *dp,
-                                                 const LPiece *lp, const double *arena,
+__global__ void __launch_bounds__(NT) seg_kernel(const SegDesc *segs, int nseg, const MvDense *dp,
+                                                 const MvLr *lp, const double *arena,
                                                  const int *ranks, const double *part,
                                                  const double *x, double *y, double alpha,
                                                  double beta) {
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(NT) seg_kernel(const SegDesc *segs, int nseg, 
         double acc = 0.0;
         // dense pieces: D[row, j] x[j], columns split over the GRP groups
         for (int p = S.dbeg; p < S.dend; ++p) {
-            DPiece P = dp[p];
+            MvDense P = dp[p];
             if (row < S.rows) {
                 const double *D = arena + P.off + row;
                 const double *xx = x + P.xc0;
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(NT) seg_kernel(const SegDesc *segs, int nseg, 
         }
         // low-rank pieces: U[row, :] t_b with t_b = sum of the block's chunk partials
         for (int p = S.lbeg; p < S.lend; ++p) {
-            LPiece P = lp[p];
+            MvLr P = lp[p];
             int r = ranks[P.slot];
             __syncthreads();
             if (threadIdx.x < r) {
@@ -122,8 +122,8 @@ std::shared_ptr<MvPlan> build_mv_plan(const HMat &H, const std::vector<int32_t> 
     auto seg_of = [&](i64 row) {
         return (int)(std::upper_bound(seg_start.begin(), seg_start.end(), row) - seg_start.begin()) - 1;
     };
-    std::vector<std::vector<DPiece>> dps(nseg);
-    std::vector<std::vector<LPiece>> lps(nseg);
+    std::vector<std::vector<MvDense>> dps(nseg);
+    std::vector<std::vector<MvLr>> lps(nseg);
     std::vector<VChunk> chunks;
     for (int32_t b : blocks) {
         const Node &nd = H.nodes[b];
@@ -150,8 +150,8 @@ std::shared_ptr<MvPlan> build_mv_plan(const HMat &H, const std::vector<int32_t> 
         }
     }
     std::vector<SegDesc> segs(nseg);
-    std::vector<DPiece> dall;
-    std::vector<LPiece> lall;
+    std::vector<MvDense> dall;
+    std::vector<MvLr> lall;
     for (int sg = 0; sg < nseg; ++sg) {
         SegDesc &S = segs[sg];
         S.y0 = seg_start[sg];

@@ -14,11 +14,11 @@ struct SegDesc {
     int32_t dbeg, dend;
     int32_t lbeg, lend;
 };
-struct DPiece {  // element (i, j) of the piece = arena[off + i + j * ld], multiplies x[xc0 + j]
+struct MvDense {  // element (i, j) of the piece = arena[off + i + j * ld], multiplies x[xc0 + j]
     i64 off, ld, xc0;
     int32_t ncols;
 };
-struct LPiece {  // U rows of the piece at arena[off + i + c * ld]; t_b from chunk partials [cbeg, cend)
+struct MvLr {  // U rows of the piece at arena[off + i + c * ld]; t_b from chunk partials [cbeg, cend)
     i64 off, ld;
     int32_t slot, cbeg, cend;
 };
@@ -31,8 +31,8 @@ struct MvPlan {
     int nseg = 0, nch = 0;
     i64 n_dpieces = 0, n_lpieces = 0;
     SegDesc *segs = nullptr;
-    DPiece *dp = nullptr;
-    LPiece *lp = nullptr;
+    MvDense *dp = nullptr;
+    MvLr *lp = nullptr;
     VChunk *chunks = nullptr;
     double *part = nullptr;
     ~MvPlan();

@@ -1,0 +1,753 @@
+// Host replay of the reference H-arithmetic recursion into a static task DAG.
+//
+// Mirrors, case by case:
+//   hops.py:392-408 _lu_block          -> Planner::lu_block
+//   hops.py:232-258 _trisolve_block    -> Planner::trisolve_left
+//   hops.py:261-279 _trisolve_right_upper -> Planner::trisolve_right_upper
+//   hops.py:211-229 _solve_dense_rhs   -> Planner::solve_dense
+//   hops.py:348-369 _schur             -> Planner::schur
+//   hops.py:318-345 _sub_lowrank/_sub_dense -> Planner::sub_lowrank / sub_dense
+//   hops.py:73-100  mul_dense/tmul_dense -> Planner::segmul (per-row-segment tasks)
+// Ranks are never read on the host: every width that depends on a rank is a
+// run-time rank slot, so one plan serves every matrix with this block structure.
+#include "plan_impl.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+namespace lh {
+
+// ---------------------------------------------------------------------------
+// views
+// ---------------------------------------------------------------------------
+PView PView::rows_(i64 a, i64 cnt) const {
+    PView r = *this;
+    if (!d.trans) {
+        r.d.off += a;
+        r.r0 += a;
+    } else {
+        r.d.off += a * d.ld;
+    }
+    r.d.rows = (int32_t)cnt;
+    return r;
+}
+PView PView::cols_(i64 a, i64 cnt) const {
+    PView r = *this;
+    if (!d.trans) r.d.off += a * d.ld;
+    else r.d.off += a;
+    r.d.cols = (int32_t)cnt;
+    return r;
+}
+PView PView::T() const {
+    PView r = *this;
+    std::swap(r.d.rows, r.d.cols);
+    r.d.trans = !d.trans;
+    r.whole = true;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// dependency tracking: per object, disjoint row intervals with last writer + readers
+// ---------------------------------------------------------------------------
+void DepTracker::access(int32_t task, u64 obj, i64 a, i64 b, bool write, std::vector<int32_t> &out) {
+    auto &m = objs[obj];
+    if (m.empty()) m[0] = Seg{INT64_MAX, -1, {}};
+    // split at a and b
+    auto split = [&](i64 x) {
+        auto it = m.upper_bound(x);
+        --it;
+        if (it->first == x) return;
+        Seg s = it->second;
+        i64 end = s.end;
+        it->second.end = x;
+        m[x] = Seg{end, s.writer, s.readers};
+    };
+    split(a);
+    if (b < INT64_MAX) split(b);
+    for (auto it = m.find(a); it != m.end() && it->first < b; ++it) {
+        Seg &s = it->second;
+        if (s.writer >= 0 && s.writer != task) out.push_back(s.writer);
+        if (write) {
+            for (int32_t r : s.readers)
+                if (r != task) out.push_back(r);
+            s.writer = task;
+            s.readers.clear();
+        } else {
+            if (s.readers.empty() || s.readers.back() != task) s.readers.push_back(task);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Planner
+// ---------------------------------------------------------------------------
+Planner::Planner(HMat &F, HMat *X) : F(F), X(X) {
+    P = std::make_shared<Plan>();
+    P->slot_off_x = F.nslots;
+    P->slot_off_tmp = F.nslots + (X ? X->nslots : 0);
+    next_slot = P->slot_off_tmp;
+}
+
+u64 Planner::key(int base, i64 id, int which) const {
+    return ((u64)base << 56) | ((u64)id << 2) | (u64)which;
+}
+
+PView Planner::dense_view(const Mref &M, int32_t b) const {
+    const Node &nd = M.H->nodes[b];
+    PView v{};
+    v.d = DView{nd.doff, (int32_t)nd.m, (int32_t)nd.n, (int32_t)nd.m, -1, (int8_t)M.base, 0, 0};
+    v.obj = key(M.base, b, 0);
+    v.r0 = 0;
+    v.whole = false;
+    return v;
+}
+PView Planner::u_view(const Mref &M, int32_t b) const {
+    const Node &nd = M.H->nodes[b];
+    PView v{};
+    v.d = DView{nd.uoff, (int32_t)nd.m, nd.kcap, (int32_t)nd.m, M.slot_off + nd.rslot,
+                (int8_t)M.base, 0, 0};
+    v.obj = key(M.base, b, 1);
+    return v;
+}
+PView Planner::v_view(const Mref &M, int32_t b) const {
+    const Node &nd = M.H->nodes[b];
+    PView v{};
+    v.d = DView{nd.voff, (int32_t)nd.n, nd.kcap, (int32_t)nd.n, M.slot_off + nd.rslot,
+                (int8_t)M.base, 0, 0};
+    v.obj = key(M.base, b, 2);
+    return v;
+}
+
+// temporaries: size-class pools with delayed FIFO reuse; reuse adds WAR edges
+// on every task that touched the previous occupant.
+PView Planner::temp(i64 rows, i64 cols, int32_t wslot) {
+    i64 need = std::max<i64>(rows * cols, 1);
+    int cls = 0;
+    while (((i64)1 << cls) < need) ++cls;
+    auto &fl = freelist[cls];
+    i64 off;
+    std::vector<int32_t> prev;
+    const size_t MIN_AGE = 512;
+    if (fl.size() > MIN_AGE) {
+        off = fl.front().off;
+        prev = std::move(fl.front().users);
+        fl.pop_front();
+    } else {
+        off = P->temp_len;
+        P->temp_len += (i64)1 << cls;
+    }
+    int32_t id = next_temp++;
+    TempRec tr;
+    tr.off = off;
+    tr.cls = cls;
+    tr.barrier = -1;
+    if (!prev.empty()) {
+        // every task touching the new occupant waits for every user of the old one
+        DTask nop;
+        std::memset(&nop, 0, sizeof(nop));
+        nop.type = T_NOP;
+        nop.path = -1;
+        for (auto &vv : nop.v) vv.wslot = -1;
+        std::sort(prev.begin(), prev.end());
+        prev.erase(std::unique(prev.begin(), prev.end()), prev.end());
+        nop.dep_beg = (int32_t)P->deps.size();
+        nop.dep_cnt = (int32_t)prev.size();
+        P->deps.insert(P->deps.end(), prev.begin(), prev.end());
+        tr.barrier = (int32_t)P->tasks.size();
+        P->tasks.push_back(nop);
+    }
+    temps[id] = std::move(tr);
+    PView v{};
+    v.d = DView{off, (int32_t)rows, (int32_t)cols, (int32_t)rows, wslot, B_TMP, 0, 0};
+    v.obj = key(B_TMP, id, 0);
+    v.tmp = id;
+    return v;
+}
+
+void Planner::release(const PView &v) {
+    auto it = temps.find(v.tmp);
+    if (it == temps.end()) return;
+    FreeBlock fb{it->second.off, std::move(it->second.users)};
+    freelist[it->second.cls].push_back(std::move(fb));
+    temps.erase(it);
+}
+
+int32_t Planner::new_slot() { return next_slot++; }
+
+int32_t Planner::emit(DTask t, std::initializer_list<std::pair<const PView *, bool>> acc,
+                      const std::vector<std::pair<PView, bool>> *more) {
+    int32_t id = (int32_t)P->tasks.size();
+    std::vector<int32_t> d;
+    auto touch = [&](const PView &v, bool w) {
+        i64 a = v.whole ? 0 : v.r0;
+        i64 b = v.whole ? INT64_MAX : v.r0 + v.d.rows;
+        deps.access(id, v.obj, a, b, w, d);
+        if (v.tmp >= 0) {
+            auto it = temps.find(v.tmp);
+            if (it != temps.end()) {
+                if (it->second.barrier >= 0) d.push_back(it->second.barrier);
+                it->second.users.push_back(id);
+            }
+        }
+    };
+    for (auto &p : acc) touch(*p.first, p.second);
+    if (more)
+        for (auto &p : *more) touch(p.first, p.second);
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    t.dep_beg = (int32_t)P->deps.size();
+    t.dep_cnt = (int32_t)d.size();
+    P->deps.insert(P->deps.end(), d.begin(), d.end());
+    P->tasks.push_back(t);
+    return id;
+}
+
+static DTask mk(int32_t type) {
+    DTask t;
+    std::memset(&t, 0, sizeof(t));
+    t.type = type;
+    t.path = -1;
+    for (auto &v : t.v) v.wslot = -1;
+    return t;
+}
+
+// leaf blocks of a subtree with offsets relative to the subtree root
+void Planner::leaves_of(const Mref &M, int32_t b, i64 r, i64 c, std::vector<LeafRef> &out) const {
+    const Node &nd = M.H->nodes[b];
+    if (nd.kind == K_HIER) {
+        leaves_of(M, nd.kid[0], r, c, out);
+        leaves_of(M, nd.kid[1], r, c + nd.cs, out);
+        leaves_of(M, nd.kid[2], r + nd.rs, c, out);
+        leaves_of(M, nd.kid[3], r + nd.rs, c + nd.cs, out);
+    } else {
+        out.push_back({b, r, c});
+    }
+}
+
+// row segments (leaf clusters) of a cluster subtree, relative to its start
+void Planner::segments_of(const Tree &T, int32_t cl, std::vector<std::pair<i64, i64>> &out) const {
+    const Cluster &c = T.nodes[cl];
+    if (c.leaf()) {
+        out.push_back({0, c.size()});
+        return;
+    }
+    std::vector<int32_t> st{cl};
+    while (!st.empty()) {
+        int32_t k = st.back();
+        st.pop_back();
+        const Cluster &q = T.nodes[k];
+        if (q.leaf()) out.push_back({q.lo - c.lo, q.size()});
+        else {
+            st.push_back(q.kid[1]);
+            st.push_back(q.kid[0]);
+        }
+    }
+}
+
+// Y (rows of op(A)) = beta*Y + alpha * op(A) * X    (mul_dense / tmul_dense, hops.py:73-100)
+// A is a block subtree of M; X has rows = columns of op(A).
+void Planner::segmul(const PView &Y, const Mref &M, int32_t a, const PView &X, bool trans,
+                     double alpha, bool overwrite) {
+    const Node &A = M.H->nodes[a];
+    if (A.kind == K_ZERO) {
+        if (overwrite) {
+            DTask t = mk(T_IDENT);
+            t.flags = 1;
+            t.v[0] = Y.d;
+            emit(t, {{&Y, true}});
+        }
+        return;
+    }
+    std::vector<LeafRef> lv;
+    leaves_of(M, a, 0, 0, lv);
+    // phase 1: W_b = F^T X for every low-rank leaf (F = V, or U when transposed)
+    struct LRW {
+        PView w;
+        bool used;
+    };
+    std::vector<PView> W(lv.size());
+    std::vector<bool> hasW(lv.size(), false);
+    for (size_t q = 0; q < lv.size(); ++q) {
+        const Node &nd = M.H->nodes[lv[q].b];
+        if (nd.kind != K_LR) continue;
+        PView F = trans ? u_view(M, lv[q].b) : v_view(M, lv[q].b);
+        i64 xr = trans ? lv[q].r : lv[q].c;
+        i64 n = trans ? nd.m : nd.n;
+        PView Xs = X.rows_(xr, n);
+        // W is (rank of F) x (columns of X); both widths are read at run time from
+        // the operands, so W itself carries no rank slot.
+        PView w = temp(KC, std::max<i64>(X.d.cols, 1), -1);
+        w.d.ld = KC;
+        DTask t = mk(T_VTX);
+        t.v[0] = F.d;
+        t.v[1] = Xs.d;
+        t.v[2] = w.d;
+        emit(t, {{&F, false}, {&Xs, false}, {&w, true}});
+        W[q] = w;
+        hasW[q] = true;
+    }
+    // phase 2: one task per output row segment
+    std::vector<std::pair<i64, i64>> segs;
+    segments_of(trans ? *M.H->ct : *M.H->rt, trans ? A.ccl : A.rcl, segs);
+    for (auto &sg : segs) {
+        i64 s0 = sg.first, s1 = sg.first + sg.second;
+        PView Ys = Y.rows_(s0, s1 - s0);
+        DTask t = mk(T_SEGMUL);
+        t.alpha = alpha;
+        t.flags = overwrite ? 1 : 0;
+        t.v[0] = Ys.d;
+        t.pc_beg = (int32_t)P->pieces.size();
+        std::vector<std::pair<PView, bool>> more;
+        for (size_t q = 0; q < lv.size(); ++q) {
+            const Node &nd = M.H->nodes[lv[q].b];
+            if (nd.kind == K_ZERO) continue;
+            i64 o0 = trans ? lv[q].c : lv[q].r;   // output-row range of this leaf
+            i64 on = trans ? nd.n : nd.m;
+            i64 a0 = std::max(o0, s0), a1 = std::min(o0 + on, s1);
+            if (a0 >= a1) continue;
+            LH_REQUIRE(a0 == s0 && a1 == s1, LH_EINTERNAL, "leaf block not aligned with segments");
+            DPiece pc;
+            std::memset(&pc, 0, sizeof(pc));
+            if (nd.kind == K_LR) {
+                PView F = trans ? v_view(M, lv[q].b) : u_view(M, lv[q].b);
+                PView Fs = F.rows_(a0 - o0, a1 - a0);
+                pc.kind = 1;
+                pc.mat = Fs.d;
+                pc.x = W[q].d;
+                more.push_back({Fs, false});
+                more.push_back({W[q], false});
+            } else {
+                PView D = dense_view(M, lv[q].b);
+                PView Ds = trans ? D.T().rows_(a0 - o0, a1 - a0) : D.rows_(a0 - o0, a1 - a0);
+                i64 xr = trans ? lv[q].r : lv[q].c;
+                i64 n = trans ? nd.m : nd.n;
+                PView Xs = X.rows_(xr, n);
+                pc.kind = 0;
+                pc.mat = Ds.d;
+                pc.x = Xs.d;
+                more.push_back({Ds, false});
+                more.push_back({Xs, false});
+            }
+            P->pieces.push_back(pc);
+        }
+        t.pc_end = (int32_t)P->pieces.size();
+        more.push_back({Ys, true});
+        emit(t, {}, &more);
+    }
+    for (size_t q = 0; q < lv.size(); ++q)
+        if (hasW[q]) release(W[q]);
+}
+
+// T X = B for a dense right-hand side view B (hops.py:211-229); mode 0 L, 1 U, 2 Ut
+void Planner::solve_dense(const Mref &T, int32_t t, const PView &B, int mode, bool unit,
+                          const std::string &path) {
+    const Node &nd = T.H->nodes[t];
+    if (nd.kind != K_HIER) {
+        LH_REQUIRE(nd.kind == K_FDENSE, LH_ETYPE,
+                   "triangular solve needs an LU-factored diagonal leaf at " + path);
+        PView Tv = dense_view(T, t);
+        DTask k = mk(T_TRSM);
+        k.flags = mode | (unit ? 16 : 0) | 32;
+        k.aux = (int32_t)nd.poff;
+        k.v[0] = Tv.d;
+        k.v[1] = B.d;
+        k.path = add_path(path);
+        emit(k, {{&Tv, false}, {&B, true}});
+        return;
+    }
+    i64 s = nd.rs;
+    PView B1 = B.rows_(0, s), B2 = B.rows_(s, nd.m - s);
+    if (mode == 0) {
+        solve_dense(T, nd.kid[0], B1, mode, unit, path + ".11");
+        segmul(B2, T, nd.kid[2], B1, false, -1.0, false);
+        solve_dense(T, nd.kid[3], B2, mode, unit, path + ".22");
+    } else if (mode == 1) {
+        solve_dense(T, nd.kid[3], B2, mode, unit, path + ".22");
+        segmul(B1, T, nd.kid[1], B2, false, -1.0, false);
+        solve_dense(T, nd.kid[0], B1, mode, unit, path + ".11");
+    } else {
+        solve_dense(T, nd.kid[0], B1, mode, unit, path + ".11");
+        segmul(B2, T, nd.kid[1], B1, true, -1.0, false);
+        solve_dense(T, nd.kid[3], B2, mode, unit, path + ".22");
+    }
+}
+
+// hops.py:232-258: T X = B in place on block b of matrix Bm (mode 0 L, 1 U)
+void Planner::trisolve_left(const Mref &T, int32_t t, const Mref &Bm, int32_t b, int mode,
+                            bool unit, const std::string &path) {
+    const Node &B = Bm.H->nodes[b];
+    if (B.kind == K_ZERO) return;
+    if (B.kind == K_LR) {
+        solve_dense(T, t, u_view(Bm, b), mode, unit, path);
+        return;
+    }
+    if (B.kind == K_DENSE) {
+        solve_dense(T, t, dense_view(Bm, b), mode, unit, path);
+        return;
+    }
+    const Node &Tn = T.H->nodes[t];
+    LH_REQUIRE(Tn.kind == K_HIER, LH_ETYPE,
+               "hierarchical right-hand side against a leaf triangle at " + path);
+    const int32_t c00 = Tn.kid[0], c01 = Tn.kid[1], c10 = Tn.kid[2], c11 = Tn.kid[3];
+    const int32_t b00 = B.kid[0], b01 = B.kid[1], b10 = B.kid[2], b11 = B.kid[3];
+    if (mode == 0) {
+        trisolve_left(T, c00, Bm, b00, mode, unit, path + ".11");
+        trisolve_left(T, c00, Bm, b01, mode, unit, path + ".11");
+        schur(Bm, b10, T, c10, Bm, b00);
+        schur(Bm, b11, T, c10, Bm, b01);
+        trisolve_left(T, c11, Bm, b10, mode, unit, path + ".22");
+        trisolve_left(T, c11, Bm, b11, mode, unit, path + ".22");
+    } else {
+        trisolve_left(T, c11, Bm, b10, mode, unit, path + ".22");
+        trisolve_left(T, c11, Bm, b11, mode, unit, path + ".22");
+        schur(Bm, b00, T, c01, Bm, b10);
+        schur(Bm, b01, T, c01, Bm, b11);
+        trisolve_left(T, c00, Bm, b00, mode, unit, path + ".11");
+        trisolve_left(T, c00, Bm, b01, mode, unit, path + ".11");
+    }
+}
+
+// hops.py:261-279: X U = B in place on block b
+void Planner::trisolve_right_upper(const Mref &T, int32_t t, const Mref &Bm, int32_t b,
+                                   const std::string &path) {
+    const Node &B = Bm.H->nodes[b];
+    if (B.kind == K_ZERO) return;
+    if (B.kind == K_LR) {
+        solve_dense(T, t, v_view(Bm, b), 2, true, path);
+        return;
+    }
+    if (B.kind == K_DENSE) {
+        solve_dense(T, t, dense_view(Bm, b).T(), 2, true, path);
+        return;
+    }
+    const Node &Tn = T.H->nodes[t];
+    LH_REQUIRE(Tn.kind == K_HIER, LH_ETYPE,
+               "hierarchical right-hand side against a leaf triangle at " + path);
+    const int32_t c00 = Tn.kid[0], c01 = Tn.kid[1], c11 = Tn.kid[3];
+    const int32_t b00 = B.kid[0], b01 = B.kid[1], b10 = B.kid[2], b11 = B.kid[3];
+    trisolve_right_upper(T, c00, Bm, b00, path + ".11");
+    trisolve_right_upper(T, c00, Bm, b10, path + ".11");
+    schur(Bm, b01, Bm, b00, T, c01);
+    schur(Bm, b11, Bm, b10, T, c01);
+    trisolve_right_upper(T, c11, Bm, b01, path + ".22");
+    trisolve_right_upper(T, c11, Bm, b11, path + ".22");
+}
+
+// hops.py:318-331: C -= U V^T
+void Planner::sub_lowrank(const Mref &Cm, int32_t c, const PView &U, const PView &V) {
+    const Node &C = Cm.H->nodes[c];
+    if (C.kind == K_ZERO) throw Error(LH_EINTERNAL, "update into a structurally zero block");
+    if (C.kind == K_DENSE) {
+        PView Cv = dense_view(Cm, c);
+        DTask t = mk(T_DGEMM);
+        t.alpha = -1.0;
+        t.flags = 1;  // C += alpha * U * V^T
+        t.v[0] = Cv.d;
+        t.v[1] = U.d;
+        t.v[2] = V.d;
+        emit(t, {{&U, false}, {&V, false}, {&Cv, true}});
+    } else if (C.kind == K_LR) {
+        PView Cu = u_view(Cm, c), Cv = v_view(Cm, c);
+        DTask t = mk(T_LRADD);
+        t.alpha = -1.0;
+        t.alpha2 = eps2;
+        t.v[0] = Cu.d;
+        t.v[1] = Cv.d;
+        t.v[2] = U.d;
+        t.v[3] = V.d;
+        Cu.whole = Cv.whole = true;
+        emit(t, {{&U, false}, {&V, false}, {&Cu, true}, {&Cv, true}});
+    } else {
+        i64 rs = C.rs, cs = C.cs;
+        sub_lowrank(Cm, C.kid[0], U.rows_(0, rs), V.rows_(0, cs));
+        sub_lowrank(Cm, C.kid[1], U.rows_(0, rs), V.rows_(cs, C.n - cs));
+        sub_lowrank(Cm, C.kid[2], U.rows_(rs, C.m - rs), V.rows_(0, cs));
+        sub_lowrank(Cm, C.kid[3], U.rows_(rs, C.m - rs), V.rows_(cs, C.n - cs));
+    }
+}
+
+// hops.py:334-345: C -= D
+void Planner::sub_dense(const Mref &Cm, int32_t c, const PView &D) {
+    const Node &C = Cm.H->nodes[c];
+    if (C.kind == K_DENSE) {
+        PView Cv = dense_view(Cm, c);
+        DTask t = mk(T_DADD);
+        t.alpha = -1.0;
+        t.v[0] = Cv.d;
+        t.v[1] = D.d;
+        emit(t, {{&D, false}, {&Cv, true}});
+    } else if (C.kind == K_LR) {
+        throw Error(LH_EINTERNAL,
+                    "dense update into a low-rank target (hops.py:339 _svd_lowrank) is not "
+                    "supported by the B200 planner");
+    } else if (C.kind == K_ZERO) {
+        throw Error(LH_EINTERNAL, "update into a structurally zero block");
+    } else {
+        i64 rs = C.rs, cs = C.cs;
+        sub_dense(Cm, C.kid[0], D.rows_(0, rs).cols_(0, cs));
+        sub_dense(Cm, C.kid[1], D.rows_(0, rs).cols_(cs, C.n - cs));
+        sub_dense(Cm, C.kid[2], D.rows_(rs, C.m - rs).cols_(0, cs));
+        sub_dense(Cm, C.kid[3], D.rows_(rs, C.m - rs).cols_(cs, C.n - cs));
+    }
+}
+
+// dense temp copy of a block subtree (hmatrix.py:402-413 to_dense)
+PView Planner::densify(const Mref &M, int32_t b) {
+    const Node &nd = M.H->nodes[b];
+    PView D = temp(nd.m, nd.n, -1);
+    std::vector<LeafRef> lv;
+    leaves_of(M, b, 0, 0, lv);
+    for (auto &l : lv) {
+        const Node &q = M.H->nodes[l.b];
+        PView Ds = D.rows_(l.r, q.m).cols_(l.c, q.n);
+        DTask t = mk(T_DENSIFY);
+        if (q.kind == K_ZERO) {
+            t.type = T_IDENT;
+            t.flags = 1;
+            t.v[0] = Ds.d;
+            emit(t, {{&Ds, true}});
+        } else if (q.kind == K_LR) {
+            PView U = u_view(M, l.b), V = v_view(M, l.b);
+            t.v[0] = Ds.d;
+            t.v[1] = U.d;
+            t.v[2] = V.d;
+            t.flags = 1;
+            emit(t, {{&U, false}, {&V, false}, {&Ds, true}});
+        } else {
+            PView S = dense_view(M, l.b);
+            t.v[0] = Ds.d;
+            t.v[1] = S.d;
+            emit(t, {{&S, false}, {&Ds, true}});
+        }
+    }
+    return D;
+}
+
+static bool is_zero(const Node &n) { return n.kind == K_ZERO; }
+
+// hops.py:348-369: C -= A B
+void Planner::schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const Mref &Bm, int32_t b) {
+    const Node &A = Am.H->nodes[a];
+    const Node &B = Bm.H->nodes[b];
+    const Node &C = Cm.H->nodes[c];
+    if (is_zero(A) || is_zero(B)) return;  // structurally zero operand: no update
+    if (A.kind == K_LR) {
+        PView Av = v_view(Am, a);
+        PView W = temp(B.n, Av.d.cols, Av.d.wslot);  // tmul_dense(B, A.v): B^T A.v
+        segmul(W, Bm, b, Av, true, 1.0, true);
+        sub_lowrank(Cm, c, u_view(Am, a), W);
+        release(W);
+    } else if (B.kind == K_LR) {
+        PView Bu = u_view(Bm, b);
+        PView W = temp(A.m, Bu.d.cols, Bu.d.wslot);  // mul_dense(A, B.u)
+        segmul(W, Am, a, Bu, false, 1.0, true);
+        sub_lowrank(Cm, c, W, v_view(Bm, b));
+        release(W);
+    } else if (A.kind == K_DENSE && B.kind == K_DENSE) {
+        PView Ad = dense_view(Am, a), Bd = dense_view(Bm, b);
+        if (C.kind == K_DENSE) {
+            PView Cv = dense_view(Cm, c);
+            DTask t = mk(T_DGEMM);
+            t.alpha = -1.0;
+            t.v[0] = Cv.d;
+            t.v[1] = Ad.d;
+            t.v[2] = Bd.d;
+            emit(t, {{&Ad, false}, {&Bd, false}, {&Cv, true}});
+        } else {
+            PView D = temp(A.m, B.n, -1);
+            DTask t = mk(T_DGEMM);
+            t.alpha = 1.0;
+            t.flags = 2;
+            t.v[0] = D.d;
+            t.v[1] = Ad.d;
+            t.v[2] = Bd.d;
+            emit(t, {{&Ad, false}, {&Bd, false}, {&D, true}});
+            sub_dense(Cm, c, D);
+            release(D);
+        }
+    } else if (A.kind == K_DENSE) {
+        // tmul_dense(B, A.d^T)^T
+        PView Ad = dense_view(Am, a);
+        PView D = temp(B.n, A.m, -1);
+        segmul(D, Bm, b, Ad.T(), true, 1.0, true);
+        sub_dense(Cm, c, D.T());
+        release(D);
+    } else if (B.kind == K_DENSE) {
+        PView Bd = dense_view(Bm, b);
+        PView D = temp(A.m, B.n, -1);
+        segmul(D, Am, a, Bd, false, 1.0, true);
+        sub_dense(Cm, c, D);
+        release(D);
+    } else if (C.kind == K_HIER && A.kind == K_HIER && B.kind == K_HIER) {
+        if (A.cs != B.rs || C.rs != A.rs || C.cs != B.cs) {
+            PView Bd = densify(Bm, b);
+            PView D = temp(A.m, B.n, -1);
+            segmul(D, Am, a, Bd, false, 1.0, true);
+            sub_dense(Cm, c, D);
+            release(D);
+            release(Bd);
+            return;
+        }
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j)
+                for (int k = 0; k < 2; ++k)
+                    schur(Cm, C.kid[2 * i + j], Am, A.kid[2 * i + k], Bm, B.kid[2 * k + j]);
+    } else {
+        PView Bd = densify(Bm, b);
+        PView D = temp(A.m, B.n, -1);
+        segmul(D, Am, a, Bd, false, 1.0, true);
+        sub_dense(Cm, c, D);
+        release(D);
+        release(Bd);
+    }
+}
+
+// hops.py:392-408
+void Planner::lu_block(int32_t b, const std::string &path) {
+    Node &nd = F.nodes[b];
+    Mref Fm{&F, B_F, 0};
+    if (nd.kind == K_DENSE) {
+        LH_REQUIRE(nd.m == nd.n, LH_EINTERNAL, "non-square diagonal leaf");
+        PView D = dense_view(Fm, b);
+        DTask t = mk(T_GETRF);
+        t.aux = (int32_t)perm_len;
+        nd.poff = perm_len;
+        perm_len += nd.m;
+        t.v[0] = D.d;
+        t.path = add_path("zero pivot in dense diagonal leaf at " + path);
+        emit(t, {{&D, true}});
+        nd.kind = K_FDENSE;
+        return;
+    }
+    LH_REQUIRE(nd.kind == K_HIER, LH_ETYPE,
+               std::string("cannot LU-factorize diagonal block of type ") +
+                   (nd.kind == K_LR ? "LowRank" : "Dense") + " at " + path);
+    lu_block(nd.kid[0], path + ".11");
+    trisolve_left(Fm, nd.kid[0], Fm, nd.kid[1], 0, true, path + ".12");
+    trisolve_right_upper(Fm, nd.kid[0], Fm, nd.kid[2], path + ".21");
+    schur(Fm, nd.kid[3], Fm, nd.kid[2], Fm, nd.kid[1]);
+    lu_block(nd.kid[3], path + ".22");
+}
+
+int32_t Planner::add_path(const std::string &s) {
+    P->paths.push_back(s);
+    return (int32_t)P->paths.size() - 1;
+}
+
+// order tasks by weighted ASAP level (critical-path friendly, topological)
+void Planner::finalize() {
+    auto &T = P->tasks;
+    const int32_t n = (int32_t)T.size();
+    std::vector<double> lvl(n, 0.0);
+    auto cost = [&](const DTask &t) -> double {
+        switch (t.type) {
+            case T_GETRF: return 8.0;
+            case T_TRSM: return 3.0;
+            case T_SEGMUL: return 1.0 + 0.3 * (t.pc_end - t.pc_beg);
+            case T_VTX: return 1.0 + t.v[0].rows / 4096.0;
+            case T_LRADD: return 4.0 + (t.v[0].rows + t.v[1].rows) / 1024.0;
+            case T_NOP: return 0.0;
+            default: return 1.0;
+        }
+    };
+    for (int32_t i = 0; i < n; ++i) {
+        double l = 0.0;
+        for (int32_t k = 0; k < T[i].dep_cnt; ++k) {
+            int32_t p = P->deps[T[i].dep_beg + k];
+            l = std::max(l, lvl[p] + cost(T[p]));
+        }
+        lvl[i] = l;
+    }
+    std::vector<int32_t> ord(n);
+    for (int32_t i = 0; i < n; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return lvl[a] < lvl[b]; });
+    std::vector<int32_t> pos(n);
+    for (int32_t i = 0; i < n; ++i) pos[ord[i]] = i;
+    std::vector<DTask> nt(n);
+    std::vector<int32_t> nd;
+    nd.reserve(P->deps.size());
+    for (int32_t i = 0; i < n; ++i) {
+        DTask t = T[ord[i]];
+        int32_t b = (int32_t)nd.size();
+        for (int32_t k = 0; k < t.dep_cnt; ++k) nd.push_back(pos[P->deps[t.dep_beg + k]]);
+        t.dep_beg = b;
+        nt[i] = t;
+    }
+    T.swap(nt);
+    P->deps.swap(nd);
+    P->nslots_total = next_slot;
+}
+
+// longest dependency chain (in tasks, NOPs excluded); tasks are topologically ordered
+int64_t critical_path(const Plan &P) {
+    std::vector<int64_t> d(P.tasks.size(), 0);
+    int64_t best = 0;
+    for (size_t i = 0; i < P.tasks.size(); ++i) {
+        int64_t l = 0;
+        const DTask &t = P.tasks[i];
+        for (int32_t k = 0; k < t.dep_cnt; ++k) l = std::max(l, d[P.deps[t.dep_beg + k]]);
+        d[i] = l + (t.type == T_NOP ? 0 : 1);
+        best = std::max(best, d[i]);
+    }
+    return best;
+}
+
+// ---------------------------------------------------------------------------
+// entry points
+// ---------------------------------------------------------------------------
+std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out) {
+    auto t0 = std::chrono::steady_clock::now();
+    Planner pl(F, nullptr);
+    pl.eps2 = eps2;
+    pl.lu_block(F.root, "root");
+    pl.finalize();
+    perm_len_out = pl.perm_len;
+    pl.P->build_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return pl.P;
+}
+
+// forward (unit L with leaf pivots) + backward (U) substitution on a dense RHS (hops.py:424-432)
+std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap) {
+    auto t0 = std::chrono::steady_clock::now();
+    Planner pl(F, nullptr);
+    Mref Fm{&F, B_F, 0};
+    PView B{};
+    pl.P->rhs_slot = pl.new_slot();
+    B.d = DView{0, (int32_t)n, nrhs_cap, (int32_t)n, pl.P->rhs_slot, B_RHS, 0, 0};
+    B.obj = pl.key(B_RHS, 0, 0);
+    pl.solve_dense(Fm, F.root, B, 0, true, "root");
+    pl.solve_dense(Fm, F.root, B, 1, false, "root");
+    pl.finalize();
+    pl.P->build_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return pl.P;
+}
+
+// X <- T^{-1} X with X initialised to the identity (lower: mode 0 unit L with pivots; upper: mode 1)
+std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2) {
+    auto t0 = std::chrono::steady_clock::now();
+    Planner pl(F, &X);
+    pl.eps2 = eps2;
+    Mref Fm{&F, B_F, 0};
+    Mref Xm{&X, B_X, F.nslots};
+    // identity initialisation of every stored leaf
+    for (int32_t b : X.leafblocks) {
+        const Node &nd = X.nodes[b];
+        if (nd.kind == K_DENSE) {
+            PView D = pl.dense_view(Xm, b);
+            DTask t = mk(T_IDENT);
+            t.flags = (nd.r0 == nd.c0 && nd.m == nd.n) ? 0 : 1;
+            t.v[0] = D.d;
+            pl.emit(t, {{&D, true}});
+        }
+    }
+    pl.trisolve_left(Fm, F.root, Xm, X.root, mode, mode == 0, "root");
+    pl.finalize();
+    pl.P->build_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return pl.P;
+}
+
+}  // namespace lh

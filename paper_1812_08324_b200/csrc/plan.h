@@ -1,0 +1,78 @@
+// Static task DAG for H-arithmetic (H-LU, triangular solves, triangular inverses).
+//
+// The host replays the reference recursion (hops.py:211-421) symbolically and
+// records primitive tasks with their operand views; data dependencies come from
+// row-interval tracking of every operand; ranks stay on the device, so the
+// schedule is independent of the numerical values and can be cached per
+// block structure.  csrc/lu.cu executes the DAG in one persistent kernel.
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "core.h"
+
+namespace lh {
+
+enum Base : int8_t { B_F = 0, B_TMP = 1, B_RHS = 2, B_X = 3 };
+
+struct DView {     // element (i, j) = base[off + (trans ? j + i*ld : i + j*ld)]
+    i64 off;
+    int32_t rows, cols, ld;
+    int32_t wslot;  // >= 0: the number of COLUMNS is ranks[wslot] at run time (cols = capacity)
+    int8_t base, trans;
+    int16_t pad;
+};
+
+enum TaskType : int32_t {
+    T_GETRF = 1,   // v0 dense leaf (m x m), aux = perm offset
+    T_TRSM = 2,    // v0 triangle (factored leaf), v1 rhs (in place); flags: mode|unit<<4|perm<<5
+    T_SEGMUL = 3,  // v0 = Y segment; pieces; alpha; flags&1: overwrite (beta = 0)
+    T_VTX = 4,     // v2 = W (r x k) <- v0^T (n x r) v1 (n x k); W rank slot = r
+    T_LRADD = 5,   // LR target U = v0, V = v1 ; += alpha * v2 v3^T ; recompress (eps in alpha2)
+    T_DGEMM = 6,   // v0 (m x n) = beta*v0 + alpha * v1 * op(v2); flags&1: transB, flags&2: overwrite
+    T_DADD = 7,    // v0 += alpha * v1
+    T_DENSIFY = 8, // v0 (m x n) <- v1 v2^T (low rank) or copy v1 (dense, v2 unused)
+    T_IDENT = 9,   // v0 <- identity (or zero if flags&1)
+    T_NOP = 10,    // dependency barrier (temp-buffer reuse)
+};
+
+struct DTask {
+    int32_t type, flags, path, aux;
+    double alpha, alpha2;
+    DView v[4];
+    int32_t dep_beg, dep_cnt;
+    int32_t pc_beg, pc_end;
+};
+
+struct DPiece {     // SEGMUL piece: Y += alpha * mat * (X rows or W)
+    int32_t kind;   // 0 dense: mat (seg x n) times X[xrow : xrow+n, :]; 1 low-rank: mat (seg x r) times w
+    int32_t pad;
+    DView mat;
+    DView x;        // dense: X rows slice; low-rank: W (r x k)
+};
+
+struct Plan {
+    std::vector<DTask> tasks;
+    std::vector<int32_t> deps;
+    std::vector<DPiece> pieces;
+    std::vector<std::string> paths;
+    i64 temp_len = 0;
+    int32_t nslots_total = 0;  // rank slots: F, X, temps
+    int32_t slot_off_x = 0, slot_off_tmp = 0;
+    int32_t rhs_slot = -1;       // slot holding the run-time RHS width (solve plans)
+    // device copies
+    DTask *d_tasks = nullptr;
+    int32_t *d_deps = nullptr;
+    DPiece *d_pieces = nullptr;
+    int32_t *d_done = nullptr;  // one flag per task + counters
+    double *d_temp = nullptr;
+    int32_t *d_ranks = nullptr;
+    int32_t *d_err = nullptr;
+    double build_seconds = 0.0;
+    ~Plan();
+    void upload(cudaStream_t s);
+};
+
+}  // namespace lh

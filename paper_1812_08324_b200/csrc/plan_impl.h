@@ -1,0 +1,109 @@
+// Planner internals (host only).
+#pragma once
+
+#include <deque>
+#include <initializer_list>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "plan.h"
+
+namespace lh {
+
+typedef uint64_t u64;
+constexpr int K_ZERO = 4;   // structurally zero block (triangular-inverse storage)
+constexpr int KC = 32;      // rows of a W = F^T X temp (>= any rank)
+
+struct PView {
+    DView d;
+    u64 obj;
+    i64 r0;       // first row of this view inside its object
+    bool whole;   // transposed: dependency on the whole object
+    int32_t tmp = -1;
+    PView rows_(i64 a, i64 cnt) const;
+    PView cols_(i64 a, i64 cnt) const;
+    PView T() const;
+};
+
+struct DepTracker {
+    struct Seg {
+        i64 end;
+        int32_t writer;
+        std::vector<int32_t> readers;
+    };
+    std::unordered_map<u64, std::map<i64, Seg>> objs;
+    void access(int32_t task, u64 obj, i64 a, i64 b, bool write, std::vector<int32_t> &out);
+};
+
+struct Mref {
+    HMat *H;
+    int base;
+    int32_t slot_off;
+};
+
+struct LeafRef {
+    int32_t b;
+    i64 r, c;
+};
+
+struct Planner {
+    HMat &F;
+    HMat *X;
+    std::shared_ptr<Plan> P;
+    DepTracker deps;
+    double eps2 = 1e-10;
+    i64 perm_len = 0;
+    int32_t next_slot = 0;
+    int32_t next_temp = 0;
+    struct TempRec {
+        i64 off;
+        int cls;
+        int32_t barrier;
+        std::vector<int32_t> users;
+    };
+    struct FreeBlock {
+        i64 off;
+        std::vector<int32_t> users;
+    };
+    std::unordered_map<int32_t, TempRec> temps;
+    std::map<int, std::deque<FreeBlock>> freelist;
+
+    Planner(HMat &F, HMat *X);
+    u64 key(int base, i64 id, int which) const;
+    PView dense_view(const Mref &M, int32_t b) const;
+    PView u_view(const Mref &M, int32_t b) const;
+    PView v_view(const Mref &M, int32_t b) const;
+    PView temp(i64 rows, i64 cols, int32_t wslot);
+    void release(const PView &v);
+    int32_t new_slot();
+    int32_t emit(DTask t, std::initializer_list<std::pair<const PView *, bool>> acc,
+                 const std::vector<std::pair<PView, bool>> *more = nullptr);
+    int32_t add_path(const std::string &s);
+    void leaves_of(const Mref &M, int32_t b, i64 r, i64 c, std::vector<LeafRef> &out) const;
+    void segments_of(const Tree &T, int32_t cl, std::vector<std::pair<i64, i64>> &out) const;
+    void segmul(const PView &Y, const Mref &M, int32_t a, const PView &X, bool trans, double alpha,
+                bool overwrite);
+    void solve_dense(const Mref &T, int32_t t, const PView &B, int mode, bool unit,
+                     const std::string &path);
+    void trisolve_left(const Mref &T, int32_t t, const Mref &Bm, int32_t b, int mode, bool unit,
+                       const std::string &path);
+    void trisolve_right_upper(const Mref &T, int32_t t, const Mref &Bm, int32_t b,
+                              const std::string &path);
+    void sub_lowrank(const Mref &Cm, int32_t c, const PView &U, const PView &V);
+    void sub_dense(const Mref &Cm, int32_t c, const PView &D);
+    PView densify(const Mref &M, int32_t b);
+    void schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const Mref &Bm, int32_t b);
+    void lu_block(int32_t b, const std::string &path);
+    void finalize();
+};
+
+std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out);
+std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap);
+std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2);
+int64_t critical_path(const Plan &P);
+
+}  // namespace lh
