@@ -67,6 +67,11 @@ int lh_partition(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, d
 int lh_plan_stats(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
                   int kcap, double *stats_host);
 
+/* Host-only: write the block layouts and the H-LU / solve / inverse task DAGs of this
+ * partition to `path` (binary, see tests/plan_emulator.py) for CPU verification. */
+int lh_debug_dump_plans(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
+                        int kcap_f, int kcap_x, const char *path);
+
 /* ---- H-matrix construction: hmatrix.py:121-137 HConfig, :306-340 build_from_dense */
 typedef struct {
     int32_t n_min;        /* HConfig.n_min                                   */
@@ -121,6 +126,15 @@ int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *factor, double eps2);
 /* levy.py:309-330 run_cn loop: U <- solve(F, Hm U), nsteps times, in place. */
 int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev, int64_t ldu,
                 int32_t nrhs, int32_t nsteps, int32_t method);
+
+/* Measurement: CUDA-event timing of each kernel of one CN step (inverse-factor method),
+ * averaged over `iters` steps applied to u_dev in place.  out[0..5] mean ms of
+ * vtx(H-), seg(H-), vtx(L^-1), seg(L^-1), vtx(U^-1), seg(U^-1); out[6..11] their algorithmic
+ * bytes; out[12..15] stored scalars of H-, L^-1, U^-1 and of the H-LU factor. */
+int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev,
+                    int32_t iters, double *out_host);
+/* out[0..3] = H-LU task count, planning seconds, temp bytes, executor seconds */
+int lh_hlu_stats(const lh_hmat *factor, double *out_host);
 
 /* ---- entry generation: fractional.py:285-405 + levy.py:169-206 -------- */
 typedef struct {

@@ -51,6 +51,7 @@ SIGNATURES = [
     ("lh_tree_order", C.c_int, [P, P]),
     ("lh_partition", C.c_int, [P, P, C.c_int, C.c_int, D, P, P, P]),
     ("lh_plan_stats", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, P]),
+    ("lh_debug_dump_plans", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, C.c_int, C.c_char_p]),
     ("lh_hmat_build_toeplitz", C.c_int, [P, P, P, P, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_build_dense", C.c_int, [P, P, P, P, I64, C.c_int, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_derive_toeplitz", C.c_int, [P, P, P, D, I32, C.POINTER(P)]),
@@ -65,6 +66,8 @@ SIGNATURES = [
     ("lh_solve", C.c_int, [P, P, P, I64, I32, I32]),
     ("lh_prepare_inverse", C.c_int, [P, P, D]),
     ("lh_cn_steps", C.c_int, [P, P, P, P, I64, I32, I32, I32]),
+    ("lh_step_profile", C.c_int, [P, P, P, P, I32, P]),
+    ("lh_hlu_stats", C.c_int, [P, P]),
     ("lh_cn_symbol", C.c_int, [P, C.POINTER(MeasureC), C.POINTER(CNParamsC), P, P, P, P]),
 ]
 

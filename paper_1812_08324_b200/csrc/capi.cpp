@@ -25,6 +25,7 @@ void hlu(Ctx &ctx, HMat &H, double eps2);
 void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method);
 void prepare_inverse(Ctx &ctx, HMat &F, double eps2);
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method);
+void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out);
 
 void *Ctx::ensure_scratch(size_t bytes) {
     if (bytes > scratch_bytes) {
@@ -40,6 +41,7 @@ void *Ctx::ensure_scratch(size_t bytes) {
 }
 Ctx::~Ctx() {
     if (scratch) cudaFree(scratch);
+    if (owns_stream) cudaStreamDestroy(stream);
 }
 HMat::~HMat() {
     mv_plan.reset();
@@ -95,6 +97,12 @@ int lh_ctx_create(int device, void *stream, lh_ctx **out) {
         LH_CUDA(cudaSetDevice(device));
         c->c.device = device;
         c->c.stream = (cudaStream_t)stream;
+        if (c->c.stream == nullptr) {
+            // the legacy default stream cannot be graph-captured; a blocking stream still
+            // orders implicitly with work that callers put on the legacy default stream
+            LH_CUDA(cudaStreamCreate(&c->c.stream));
+            c->c.owns_stream = true;
+        }
         int sms = 0;
         LH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         c->c.num_sms = sms;
@@ -379,6 +387,16 @@ int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t l
     return guard(ctx, [&] {
         cn_steps(ctx->c, const_cast<HMat &>(hm->h), f->h, u, ldu, nrhs, nsteps, method);
     });
+}
+
+int lh_step_profile(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int32_t iters,
+                    double *out) {
+    return guard(ctx, [&] { step_profile(ctx->c, const_cast<HMat &>(hm->h), f->h, u, iters, out); });
+}
+
+int lh_hlu_stats(const lh_hmat *f, double *out) {
+    for (int k = 0; k < 4; ++k) out[k] = f->h.lu_stats[k];
+    return LH_OK;
 }
 
 int lh_cn_symbol(lh_ctx *ctx, const lh_measure *nu, const lh_cn_params *p, double *tA, double *tP,

@@ -113,6 +113,7 @@ void walk_leaves(HMat &H);
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    bool owns_stream = false;
     std::string last_error;
     int num_sms = 148;
     // reusable device scratch

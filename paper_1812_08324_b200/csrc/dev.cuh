@@ -87,6 +87,9 @@ __device__ __noinline__ static void cgs2(double *Q, i64 ldq, i64 m, int K, doubl
     for (int k = 0; k < K; ++k) {
         double *u = Q + (i64)k * ldq;
         for (int l = threadIdx.x; l < KA_MAX; l += NT) R[l + k * KA_MAX] = 0.0;
+        double s0 = 0.0;
+        for (i64 i = threadIdx.x; i < m; i += NT) s0 += u[i] * u[i];
+        const double n0 = sqrt(block_sum(s0, red));
         for (int pass = 0; pass < 2; ++pass) {
             __syncthreads();
             col_dots(Q, ldq, m, k, u, h);
@@ -102,6 +105,10 @@ __device__ __noinline__ static void cgs2(double *Q, i64 ldq, i64 m, int K, doubl
         double s = 0.0;
         for (i64 i = threadIdx.x; i < m; i += NT) s += u[i] * u[i];
         double nrm = sqrt(block_sum(s, red));
+        // a residual at rounding level after reorthogonalisation means the column is
+        // numerically inside span(q_0..q_{k-1}): drop it (q_k = 0, R_kk = 0) so Q keeps
+        // orthonormal columns (normalising noise would not be orthogonal to the span)
+        if (!(nrm > 1e-13 * n0)) nrm = 0.0;
         double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
         for (i64 i = threadIdx.x; i < m; i += NT) u[i] *= inv;
         if (threadIdx.x == 0) R[k + k * KA_MAX] = nrm;

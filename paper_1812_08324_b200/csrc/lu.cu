@@ -386,6 +386,34 @@ __device__ void task_densify(const ExecArgs &A, const DTask &T) {
     }
 }
 
+__device__ __forceinline__ double hash_normal(uint32_t seed, uint64_t i) {
+    // splitmix64 -> two uniforms -> Box-Muller
+    uint64_t z = (uint64_t)seed * 0x9E3779B97F4A7C15ull + i * 0xBF58476D1CE4E5B9ull + 0x94D049BB133111EBull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    double u1 = ((z >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    uint64_t y = z * 0x2545F4914F6CDD1Dull + 0x9E3779B97F4A7C15ull;
+    y ^= y >> 29;
+    double u2 = ((y >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+__device__ void task_rand(const ExecArgs &A, const DTask &T) {
+    const DView &dv = T.v[0];
+    double *D = vp(A, dv);
+    for (int e = threadIdx.x; e < dv.rows * dv.cols; e += NT) {
+        int i = e % dv.rows, j = e / dv.rows;
+        D[vi(dv, i, j)] = hash_normal((uint32_t)T.aux, (uint64_t)e);
+    }
+}
+
+__device__ void task_orth(const ExecArgs &A, const DTask &T, double *sm) {
+    const DView &dv = T.v[0];
+    dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(sm);
+    dev::cgs2(vp(A, dv), dv.ld, dv.rows, dv.cols, S.Ru, S.h, S.red);
+}
+
 __device__ void task_ident(const ExecArgs &A, const DTask &T) {
     const DView &dv = T.v[0];
     double *D = vp(A, dv);
@@ -438,6 +466,8 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
             case T_DADD: task_dadd(A, T); break;
             case T_DENSIFY: task_densify(A, T); break;
             case T_IDENT: task_ident(A, T); break;
+            case T_RAND: task_rand(A, T); break;
+            case T_ORTH: task_orth(A, T, sm); break;
             default: break;
         }
         __syncthreads();
@@ -548,7 +578,10 @@ void hlu(Ctx &ctx, HMat &F, double eps2) {
     P->upload(ctx.stream);
     F.factored = true;
     F.mv_plan.reset();
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    auto t0 = std::chrono::steady_clock::now();
     run_plan(ctx, *P, F, nullptr, nullptr, -1);
+    F.lu_stats[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     F.sync_ranks(ctx.stream);
     F.lu_stats[0] = (double)P->tasks.size();
     F.lu_stats[1] = P->build_seconds;
@@ -587,21 +620,20 @@ static void solve_substitution(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) 
 }
 
 // X: same block tree as F restricted to one triangle; other-triangle leaves are K_ZERO.
-static std::shared_ptr<HMat> make_triangle(const HMat &F, bool lower, int kcap) {
-    auto X = std::make_shared<HMat>();
-    X->rt = F.rt;
-    X->ct = F.ct;
-    X->rt_hold = F.rt_hold;
-    X->ct_hold = F.ct_hold;
-    X->nrows = F.nrows;
-    X->ncols = F.ncols;
-    X->root = F.root;
-    X->nodes = F.nodes;
-    X->leafblocks = F.leafblocks;
+void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap) {
+    X.rt = F.rt;
+    X.ct = F.ct;
+    X.rt_hold = F.rt_hold;
+    X.ct_hold = F.ct_hold;
+    X.nrows = F.nrows;
+    X.ncols = F.ncols;
+    X.root = F.root;
+    X.nodes = F.nodes;
     i64 off = 0;
     int32_t slots = 0;
-    for (int32_t b : X->leafblocks) {
-        Node &nd = X->nodes[b];
+    walk_leaves(X);
+    for (int32_t b : X.leafblocks) {
+        Node &nd = X.nodes[b];
         bool diag = (nd.r0 == nd.c0 && nd.m == nd.n);
         bool other = lower ? (nd.c0 >= nd.r0 + nd.m) : (nd.r0 >= nd.c0 + nd.n);
         if (other && !diag) {
@@ -621,22 +653,21 @@ static std::shared_ptr<HMat> make_triangle(const HMat &F, bool lower, int kcap) 
             off += nd.n * kcap;
         }
     }
-    X->arena_len = off;
-    X->d_arena = dalloc<double>(std::max<i64>(off, 1));
-    X->nslots = slots;
-    X->d_ranks = dalloc<int32_t>(std::max(slots, 1));
-    LH_CUDA(cudaMemset(X->d_ranks, 0, sizeof(int32_t) * std::max(slots, 1)));
-    return X;
+    X.arena_len = off;
+    X.nslots = slots;
 }
 
 void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.factored, LH_EINVAL, "prepare_inverse needs an H-LU factorization");
     SolvePlans &S = plans_of(F);
     if (S.XL) return;
-    int kcap = KC_MAX;
+    int kcap = KA_MAX;  // room for rank + sketch width before recompression
     for (int mode = 0; mode < 2; ++mode) {
-        auto X = make_triangle(F, mode == 0, kcap);
-        walk_leaves(*X);
+        auto X = std::make_shared<HMat>();
+        triangle_layout(*X, F, mode == 0, kcap);
+        X->d_arena = dalloc<double>(std::max<i64>(X->arena_len, 1));
+        X->d_ranks = dalloc<int32_t>(std::max(X->nslots, 1));
+        LH_CUDA(cudaMemsetAsync(X->d_ranks, 0, sizeof(int32_t) * std::max(X->nslots, 1), ctx.stream));
         auto P = plan_inverse(F, *X, mode, eps2);
         P->upload(ctx.stream);
         run_plan(ctx, *P, F, X.get(), nullptr, -1);
@@ -672,6 +703,87 @@ void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method) {
     if (nrhs <= 0) return;
     if (method == 0) solve_substitution(ctx, F, b, ldb, nrhs);
     else solve_inverse(ctx, F, b, ldb, nrhs);
+}
+
+// algorithmic bytes of the two matvec phases over `blocks` (fp64): phase 1 reads V,
+// phase 2 reads the dense leaves and U, reads x once and writes y once.
+static void mv_bytes(const HMat &H, const std::vector<int32_t> &blocks, double &b1, double &b2) {
+    b1 = b2 = 0.0;
+    for (int32_t b : blocks) {
+        const Node &nd = H.nodes[b];
+        if (nd.kind == K_LR) {
+            double r = H.h_ranks[nd.rslot];
+            b1 += 8.0 * r * nd.n;
+            b2 += 8.0 * r * nd.m;
+        } else if (nd.kind == K_DENSE || nd.kind == K_FDENSE) {
+            b2 += 8.0 * nd.m * nd.n;
+        }
+    }
+    b2 += 16.0 * H.nrows;
+}
+
+// Per-kernel CUDA-event timing of one CN step (method 1): out[0..5] = mean ms of
+// vtx(H-), seg(H-), vtx(XL), seg(XL), vtx(XU), seg(XU); out[6..11] their algorithmic
+// bytes; out[12..14] stored scalars of H-, XL, XU; out[15] stored scalars of F.
+void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out) {
+    SolvePlans &S = plans_of(F);
+    LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
+    MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
+    double *y = (double *)ctx.ensure_scratch(sizeof(double) * (size_t)Hm.nrows);
+    Hm.sync_ranks(ctx.stream);
+    S.XL->sync_ranks(ctx.stream);
+    S.XU->sync_ranks(ctx.stream);
+    const MvPlan *plans[3] = {&Pm, S.mvL.get(), S.mvU.get()};
+    HMat *mats[3] = {&Hm, S.XL.get(), S.XU.get()};
+    double *xin[3] = {u, y, S.tmp};
+    double *yout[3] = {y, S.tmp, u};
+    cudaEvent_t ev[7];
+    for (auto &e : ev) LH_CUDA(cudaEventCreate(&e));
+    std::vector<double> acc(6, 0.0);
+    for (int it = 0; it < iters; ++it) {
+        for (int q = 0; q < 3; ++q) {
+            const MvPlan &P = *plans[q];
+            LH_CUDA(cudaEventRecord(ev[2 * q], ctx.stream));
+            if (P.nch > 0) {
+                int g1 = std::min(P.nch, ctx.num_sms * 16);
+                mv_vtx_launch(P, *mats[q], xin[q], g1, ctx.stream);
+            }
+            LH_CUDA(cudaEventRecord(ev[2 * q + 1], ctx.stream));
+            mv_seg_launch(P, *mats[q], xin[q], yout[q], 1.0, 0.0, ctx.stream, ctx.num_sms);
+        }
+        LH_CUDA(cudaEventRecord(ev[6], ctx.stream));
+        LH_CUDA(cudaEventSynchronize(ev[6]));
+        for (int k = 0; k < 6; ++k) {
+            float ms = 0.f;
+            LH_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+            acc[k] += ms;
+        }
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < 6; ++k) out[k] = acc[k] / std::max(iters, 1);
+    std::vector<int32_t> all_m = Hm.leafblocks;
+    std::vector<int32_t> bl, bu;
+    for (int32_t b : S.XL->leafblocks)
+        if (S.XL->nodes[b].kind != K_ZERO) bl.push_back(b);
+    for (int32_t b : S.XU->leafblocks)
+        if (S.XU->nodes[b].kind != K_ZERO) bu.push_back(b);
+    mv_bytes(Hm, all_m, out[6], out[7]);
+    mv_bytes(*S.XL, bl, out[8], out[9]);
+    mv_bytes(*S.XU, bu, out[10], out[11]);
+    auto stored = [](const HMat &H, const std::vector<int32_t> &blocks) {
+        double s = 0.0;
+        for (int32_t b : blocks) {
+            const Node &nd = H.nodes[b];
+            if (nd.kind == K_LR) s += (double)H.h_ranks[nd.rslot] * (nd.m + nd.n);
+            else if (nd.kind != K_ZERO && nd.kind != K_HIER) s += (double)nd.m * nd.n;
+        }
+        return s;
+    };
+    F.sync_ranks(ctx.stream);
+    out[12] = stored(Hm, all_m);
+    out[13] = stored(*S.XL, bl);
+    out[14] = stored(*S.XU, bu);
+    out[15] = stored(F, F.leafblocks);
 }
 
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method) {

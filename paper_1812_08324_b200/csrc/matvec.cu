@@ -184,6 +184,17 @@ MvPlan::~MvPlan() {
     cudaFree(part);
 }
 
+void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int grid, cudaStream_t s) {
+    vtx_kernel<<<grid, NT, 0, s>>>(P.chunks, P.nch, H.d_arena, H.d_ranks, x, P.part, 0.0);
+}
+
+void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
+                   double beta, cudaStream_t s, int num_sms) {
+    int g2 = std::min(P.nseg, num_sms * 32);
+    seg_kernel<<<g2, NT, 0, s>>>(P.segs, P.nseg, P.dp, P.lp, H.d_arena, H.d_ranks, P.part, x, y,
+                                 alpha, beta);
+}
+
 // y = alpha * H x + beta * y  for one right-hand side
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
             cudaStream_t s, int num_sms) {

@@ -478,9 +478,7 @@ void Planner::sub_dense(const Mref &Cm, int32_t c, const PView &D) {
         t.v[1] = D.d;
         emit(t, {{&D, false}, {&Cv, true}});
     } else if (C.kind == K_LR) {
-        throw Error(LH_EINTERNAL,
-                    "dense update into a low-rank target (hops.py:339 _svd_lowrank) is not "
-                    "supported by the B200 planner");
+        lr_sketch_update(Cm, c, nullptr, -1, nullptr, -1, &D);
     } else if (C.kind == K_ZERO) {
         throw Error(LH_EINTERNAL, "update into a structurally zero block");
     } else {
@@ -490,6 +488,67 @@ void Planner::sub_dense(const Mref &Cm, int32_t c, const PView &D) {
         sub_dense(Cm, C.kid[2], D.rows_(rs, C.m - rs).cols_(0, cs));
         sub_dense(Cm, C.kid[3], D.rows_(rs, C.m - rs).cols_(cs, C.n - cs));
     }
+}
+
+// C (low-rank) -= M with M = A B (implicit, both block subtrees) or M = D (explicit dense).
+// The reference converts such updates through a dense SVD (_sub_dense -> _svd_lowrank,
+// hops.py:334-345, :159-163), which would materialise whole admissible blocks.  Here M
+// is sketched: Y = M Omega (p Gaussian columns), Q = orth(Y), Z = M^T Q, and C -= Q Z^T
+// goes through the same eps2 Frobenius recompression (_add_lr).
+constexpr int P_SKETCH = 20;
+void Planner::lr_sketch_update(const Mref &Cm, int32_t c, const Mref *Am, int32_t a,
+                               const Mref *Bm, int32_t b, const PView *D) {
+    const Node &C = Cm.H->nodes[c];
+    const int p = P_SKETCH;
+    PView Om = temp(C.n, p, -1);
+    {
+        DTask t = mk(T_RAND);
+        t.aux = rand_seed++;
+        t.v[0] = Om.d;
+        emit(t, {{&Om, true}});
+    }
+    PView Y = temp(C.m, p, -1);
+    if (D) {
+        DTask t = mk(T_DGEMM);
+        t.alpha = 1.0;
+        t.flags = 2;
+        t.v[0] = Y.d;
+        t.v[1] = D->d;
+        t.v[2] = Om.d;
+        emit(t, {{D, false}, {&Om, false}, {&Y, true}});
+    } else {
+        const Node &B = Bm->H->nodes[b];
+        PView T1 = temp(B.m, p, -1);
+        segmul(T1, *Bm, b, Om, false, 1.0, true);
+        segmul(Y, *Am, a, T1, false, 1.0, true);
+        release(T1);
+    }
+    release(Om);
+    {
+        DTask t = mk(T_ORTH);
+        t.v[0] = Y.d;
+        emit(t, {{&Y, true}});
+    }
+    PView Z = temp(C.n, p, -1);
+    if (D) {
+        DTask t = mk(T_DGEMM);
+        t.alpha = 1.0;
+        t.flags = 2;
+        t.v[0] = Z.d;
+        t.v[1] = D->T().d;
+        t.v[2] = Y.d;
+        PView Dt = D->T();
+        emit(t, {{&Dt, false}, {&Y, false}, {&Z, true}});
+    } else {
+        const Node &A = Am->H->nodes[a];
+        PView T2 = temp(A.n, p, -1);
+        segmul(T2, *Am, a, Y, true, 1.0, true);
+        segmul(Z, *Bm, b, T2, true, 1.0, true);
+        release(T2);
+    }
+    sub_lowrank(Cm, c, Y, Z);
+    release(Y);
+    release(Z);
 }
 
 // dense temp copy of a block subtree (hmatrix.py:402-413 to_dense)
@@ -544,6 +603,9 @@ void Planner::schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const 
         segmul(W, Am, a, Bu, false, 1.0, true);
         sub_lowrank(Cm, c, W, v_view(Bm, b));
         release(W);
+    } else if (C.kind == K_LR) {
+        // dense product into an admissible target: sketched instead of a dense SVD
+        lr_sketch_update(Cm, c, &Am, a, &Bm, b, nullptr);
     } else if (A.kind == K_DENSE && B.kind == K_DENSE) {
         PView Ad = dense_view(Am, a), Bd = dense_view(Bm, b);
         if (C.kind == K_DENSE) {

@@ -36,6 +36,8 @@ enum TaskType : int32_t {
     T_DENSIFY = 8, // v0 (m x n) <- v1 v2^T (low rank) or copy v1 (dense, v2 unused)
     T_IDENT = 9,   // v0 <- identity (or zero if flags&1)
     T_NOP = 10,    // dependency barrier (temp-buffer reuse)
+    T_RAND = 11,   // v0 <- N(0,1) samples, seed aux
+    T_ORTH = 12,   // v0 (m x p) <- Q of its CGS2 QR, in place
 };
 
 struct DTask {

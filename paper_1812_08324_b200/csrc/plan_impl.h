@@ -95,6 +95,9 @@ struct Planner {
                               const std::string &path);
     void sub_lowrank(const Mref &Cm, int32_t c, const PView &U, const PView &V);
     void sub_dense(const Mref &Cm, int32_t c, const PView &D);
+    void lr_sketch_update(const Mref &Cm, int32_t c, const Mref *Am, int32_t a, const Mref *Bm,
+                          int32_t b, const PView *D);
+    int32_t rand_seed = 1;
     PView densify(const Mref &M, int32_t b);
     void schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const Mref &Bm, int32_t b);
     void lu_block(int32_t b, const std::string &path);
