@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: Crank-Nicolson steps/s at N = 2^20 (BASELINE.json configs[2], the
+tempered-stable CGMY case), with assembly + H-LU time and the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One "step" is one CN step u <- A+^{-1} A- u on the resident vector: the H-matvec
+with A- followed by the solve with the H-LU factors, applied as the two
+triangular-inverse factors.  Under torchrun (N > 1) every rank runs
+an independent replica (single-RHS stepping does not shard);
+``value`` is the sum over ranks, timing is the max over ranks.
+
+``--impl reference`` times the reference algorithm (the oracle restatement of
+levyh hops.matvec + hops.solve, oracle/levyh_oracle.py) on the host cores, on the
+same N = 2^20 operator (factors built on the GPU and exported, because the
+reference cannot assemble or compress at this size: SURVEY G7).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Crank-Nicolson steps/s at N=2^20 (cfg3 CGMY); assembly+H-LU time; % of HBM roofline"
+
+# configs[2] of BASELINE.json
+CFG3 = dict(workload="cfg3: CGMY C=1 G=5 M=10 Y=0.5 on [-4,4], N=2^20-1, a=0.05 b=0.1 c=-0.05, "
+                     "dt=2^-13, leaf 64, eta 1, ACA tol 1e-9, fp64, u0=max(e^x-1,0)",
+            n=2 ** 19, L=4.0, L_W=8.0, a=0.05, b=0.1, c=-0.05, dt=8.0 / 2 ** 20 * 16, leaf=64,
+            eps1=1e-9, eps2=1e-10)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def build_system(P, cfg=CFG3, n=None):
+    """Operator assembly (GPU symbol + ACA compression) and factorisation, timed."""
+    import torch
+
+    n = n or cfg["n"]
+    t0 = time.perf_counter()
+    nu = P.cgmy_measure(1.0, 5.0, 10.0, 0.5)
+    s = P.FracCNSystem(nu, cfg["a"], cfg["b"], cfg["c"], n, cfg["dt"], L=cfg["L"], L_W=cfg["L_W"],
+                       drift_compensation=True)
+    torch.cuda.synchronize()
+    t_symbol = time.perf_counter() - t0
+    hc = P.HConfig(n_min=cfg["leaf"], eps1=cfg["eps1"])
+    t1 = time.perf_counter()
+    Hp, Hm = s.build_pair(hc)
+    torch.cuda.synchronize()
+    t_aca = time.perf_counter() - t1
+    s.h_minus = Hm
+    mem_p = P.memory_report(Hp)
+    t2 = time.perf_counter()
+    F = P.hlu(Hp, cfg["eps2"])
+    torch.cuda.synchronize()
+    t_lu = time.perf_counter() - t2
+    st = np.zeros(4)
+    P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st))
+    t3 = time.perf_counter()
+    F.prepare_inverse()
+    torch.cuda.synchronize()
+    t_inv = time.perf_counter() - t3
+    s.factor = F
+    s.method = "inverse"
+    times = dict(symbol_s=t_symbol, aca_s=t_aca, assembly_s=t_symbol + t_aca, hlu_s=t_lu,
+                 hlu_plan_s=float(st[1]), hlu_exec_s=float(st[3]), hlu_tasks=int(st[0]),
+                 inverse_factors_s=t_inv, stored_scalars_plus=mem_p["stored_scalars"])
+    return s, F, Hm, times
+
+
+def cpu_reference_steps(P, s, F, Hm, u0, n_steps, max_seconds=None):
+    """The reference algorithm (oracle restatement of hops.matvec + hops.solve) on host cores."""
+    from oracle import export_bridge as EB
+    from oracle import levyh_oracle as O
+
+    leaf = CFG3["leaf"]
+    t0 = time.perf_counter()
+    Fr = EB.tree_from_export(s.x, leaf, *P.hmatrix.export_layout(F.h))
+    Hr = EB.tree_from_export(s.x, leaf, *P.hmatrix.export_layout(Hm))
+    t_export = time.perf_counter() - t0
+    u = np.asarray(u0, dtype=float).copy()
+    times = []
+    for k in range(n_steps):
+        t = time.perf_counter()
+        u = O.lu_solve(Fr, O.hmatvec(Hr, u))
+        times.append(time.perf_counter() - t)
+        if max_seconds and sum(times) > max_seconds:
+            break
+    return u, times, t_export
+
+
+def cpu_info():
+    info = {"cores": os.cpu_count()}
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["blas_threads"] = max((d.get("num_threads", 0) for d in threadpool_info()), default=None)
+    except Exception:
+        info["blas_threads"] = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return info
+
+
+def run_b200(args, world, rank, local):
+    import torch
+
+    import paper_1812_08324_b200 as P
+
+    s, F, Hm, times = build_system(P, n=args.n)
+    ctx = Hm.ctx
+    L = P._lib.lib()
+    N = s.N
+    u0 = np.maximum(np.exp(s.x) - 1.0, 0.0)
+    u = torch.from_numpy(u0.copy()).cuda()
+
+    def steps(k, vec):
+        P._lib.check(L.lh_cn_steps(ctx.h, Hm.handle, F.h.handle, vec.data_ptr(), N, 1, int(k), 1), ctx.h)
+
+    # warm-up (also captures the CUDA graph of one step)
+    steps(args.warmup, u)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        time.sleep(0.3)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        # events on the stream the library launches on
+        lib_stream = ctx.torch_stream()
+        start.record(lib_stream)
+        steps(args.steps, u)
+        end.record(lib_stream)
+        torch.cuda.synchronize()
+        ms = start.elapsed_time(end)
+        # keep the GPU busy for the clock sampler (extra untimed steps)
+        t_load = time.perf_counter()
+        while time.perf_counter() - t_load < 1.5:
+            steps(50, u)
+        torch.cuda.synchronize()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1000.0)
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), one step per call
+    u_host = torch.from_numpy(u0.copy()).pin_memory()
+    u_dev = torch.empty_like(u)
+    e2e_steps = max(1, min(args.steps, 50))
+    steps_e2e_dev = u_dev
+    # warm (graph for this vector)
+    u_dev.copy_(u_host, non_blocking=True)
+    steps(1, steps_e2e_dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        u_dev.copy_(u_host, non_blocking=True)
+        steps(1, steps_e2e_dev)
+        u_host.copy_(u_dev, non_blocking=True)
+        torch.cuda.synchronize()
+    t_e2e = time.perf_counter() - t0
+    e2e = {"value": world * e2e_steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * N,
+           "d2h_bytes_per_step": 8 * N, "path": "lh_cn_steps (C ABI) with pinned host u per step"}
+
+    # ---- per-kernel roofline (CUDA events on the library stream)
+    prof = np.zeros(16)
+    uprof = torch.from_numpy(u0.copy()).cuda()
+    P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, uprof.data_ptr(), 5, P._lib.host_ptr(prof)),
+                 ctx.h)
+    names = ["vtx(A-)", "seg(A-)", "vtx(L^-1)", "seg(L^-1)", "vtx(U^-1)", "seg(U^-1)"]
+    kms = prof[:6]
+    kbytes = prof[6:12]
+    dom = int(np.argmax(kms))
+    peak, peak_src = measured_peaks()
+    achieved = kbytes[dom] / (kms[dom] / 1000.0) / 1e9
+    step_bytes = float(kbytes.sum())
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(names[dom])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": float(kbytes[dom]),
+                "kernel_ms": float(kms[dom]),
+                "per_kernel": {nm: {"ms": round(float(kms[i]), 4), "GBps": round(kbytes[i] / (kms[i] / 1e3) / 1e9, 1)}
+                               for i, nm in enumerate(names)},
+                "step_bytes": step_bytes,
+                "step_GBps_sum_of_kernels": round(step_bytes / (kms.sum() / 1e3) / 1e9, 1),
+                "step_GBps_timed": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1),
+                "stored_scalars": {"A-": int(prof[12]), "L^-1": int(prof[13]), "U^-1": int(prof[14]),
+                                   "LU factor": int(prof[15])},
+                "reference_algorithm_bytes_per_step": 8.0 * (prof[12] + prof[15] + 6 * N)}
+
+    out = {"metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (BASELINE.json configs[2]; seeded/closed-form inputs, no dataset)",
+           "config": {"workload": CFG3["workload"] if args.n is None else f"cfg3 operator at n={args.n}",
+                      "N": N, "leaf": CFG3["leaf"], "eps1": CFG3["eps1"], "eps2": CFG3["eps2"],
+                      "solve": "triangular-inverse H-factors of the H-LU (DESIGN.md)",
+                      "parallelism": f"replicas x{world}",
+                      "l2": "inputs larger than L2 (>= 14 GB streamed per step vs 126 MB L2)"},
+           "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": 6 * args.steps,
+           "roofline": roofline, "phases": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in times.items()}}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ucpu, ts, t_exp = cpu_reference_steps(P, s, F, Hm, u0, args.cpu_steps, max_seconds=30)
+        ci = cpu_info()
+        out["cpu_baseline"] = {"value": round(len(ts) / sum(ts), 5), "unit": "steps/s",
+                               "cores": ci["cores"], "blas_threads": ci.get("blas_threads"),
+                               "cpu_model": ci.get("cpu_model"), "kind": "port",
+                               "sample": f"{len(ts)} CN steps (matvec + substitution solve) of the cfg3 operator "
+                                         f"at N=2^20 with oracle/levyh_oracle.py on GPU-built factors exported "
+                                         f"to host ({t_exp:.1f}s export, untimed)"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_reference(args, world, rank, local):
+    """--impl reference: the reference algorithm on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import torch
+
+    import paper_1812_08324_b200 as P
+
+    s, F, Hm, times = build_system(P, n=args.n)
+    u0 = np.maximum(np.exp(s.x) - 1.0, 0.0)
+    warm = min(args.warmup, 1)
+    k = max(1, min(args.steps, args.ref_steps))
+    u, ts, t_exp = cpu_reference_steps(P, s, F, Hm, u0, warm + k)
+    ts = ts[warm:]
+    ci = cpu_info()
+    value = len(ts) / sum(ts)
+    out = {"metric": METRIC, "value": round(value, 5), "unit": "steps/s", "n_gpus": world,
+           "steps": len(ts), "warmup": warm, "ms_per_step": round(1000 * sum(ts) / len(ts), 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (BASELINE.json configs[2])", "impl": "reference",
+           "config": {"workload": CFG3["workload"], "N": s.N, "leaf": CFG3["leaf"], "eps1": CFG3["eps1"],
+                      "parallelism": "host cores (OpenBLAS threads)"},
+           "cpu_baseline": {"value": round(value, 5), "unit": "steps/s", "cores": ci["cores"],
+                            "blas_threads": ci.get("blas_threads"), "cpu_model": ci.get("cpu_model"),
+                            "kind": "port",
+                            "sample": f"{len(ts)} timed CN steps (+{warm} warm-up) of oracle hmatvec + lu_solve "
+                                      f"(restated levyh hops.matvec/hops.solve) on GPU-built cfg3 factors "
+                                      f"exported to host ({t_exp:.1f}s export, untimed); the reference "
+                                      f"cannot assemble at N=2^20 (SURVEY G7)"},
+           "e2e": {"value": round(value, 5), "unit": "steps/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override half-grid n (N = 2n-1); default 2^19")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--ref-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: fewer than 3 warm-up steps")
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_b200(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -43,6 +43,8 @@ int lh_ctx_create(int device, void *cuda_stream, lh_ctx **out);
 void lh_ctx_destroy(lh_ctx *ctx);
 const char *lh_ctx_last_error(const lh_ctx *ctx);
 int lh_ctx_synchronize(lh_ctx *ctx);
+/* the cudaStream_t every call of this context is ordered on (for caller-side events) */
+void *lh_ctx_stream(const lh_ctx *ctx);
 int lh_version(void);
 
 /* ---- cluster tree: geometry.py:191-243 build_cluster_tree (bisection) -- */
@@ -109,6 +111,14 @@ int lh_hmat_memory(lh_ctx *ctx, const lh_hmat *h, int64_t *stats_host);
  * lowrank: a = U (m*rank col-major), b = V (n*rank col-major). */
 int lh_hmat_export_block(lh_ctx *ctx, const lh_hmat *h, int64_t block, double *a_host,
                          double *b_host);
+
+/* Bulk export (host copies) for checkpointing and for timing the reference CPU path on
+ * GPU-built factors.  sizes[0..2] = arena length (doubles), rank slots, permutation length.
+ * recs[11*b ..] per leaf block (walk order): row0,row1,col0,col1,kind(1 dense,2 lowrank,
+ * 3 dense_lu),dense_off,u_off,v_off,kcap,rank_slot,perm_off. */
+int lh_hmat_layout(const lh_hmat *h, int64_t *recs_host, int64_t *sizes_host);
+int lh_hmat_export_arena(lh_ctx *ctx, const lh_hmat *h, double *arena_host, int32_t *ranks_host,
+                         int32_t *perm_host);
 
 /* ---- H-arithmetic ------------------------------------------------------ */
 /* hops.py:65-70 matvec / :73-85 mul_dense:  Y = H X, X is ncols x nrhs (col-major, ldx) */

@@ -43,6 +43,7 @@ SIGNATURES = [
     ("lh_ctx_destroy", None, [P]),
     ("lh_ctx_last_error", C.c_char_p, [P]),
     ("lh_ctx_synchronize", C.c_int, [P]),
+    ("lh_ctx_stream", C.c_void_p, [P]),
     ("lh_version", C.c_int, []),
     ("lh_tree_build", C.c_int, [P, P, I64, C.c_int, C.c_int, C.POINTER(P)]),
     ("lh_tree_destroy", None, [P]),
@@ -61,6 +62,8 @@ SIGNATURES = [
     ("lh_hmat_structure", C.c_int, [P, P, P]),
     ("lh_hmat_memory", C.c_int, [P, P, P]),
     ("lh_hmat_export_block", C.c_int, [P, P, I64, P, P]),
+    ("lh_hmat_layout", C.c_int, [P, P, P]),
+    ("lh_hmat_export_arena", C.c_int, [P, P, P, P, P]),
     ("lh_hmat_matvec", C.c_int, [P, P, P, I64, P, I64, I32]),
     ("lh_hlu", C.c_int, [P, P, D]),
     ("lh_solve", C.c_int, [P, P, P, I64, I32, I32]),
@@ -144,6 +147,12 @@ class Context:
 
     def sync(self):
         check(lib().lh_ctx_synchronize(self.h), self.h)
+
+    def torch_stream(self):
+        """The library's CUDA stream as a torch stream (for CUDA-event timing)."""
+        import torch
+
+        return torch.cuda.ExternalStream(lib().lh_ctx_stream(self.h) or 0, device=self.device)
 
 
 def host_ptr(a):

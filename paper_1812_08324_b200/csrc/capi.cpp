@@ -118,6 +118,8 @@ void lh_ctx_destroy(lh_ctx *ctx) { delete ctx; }
 
 const char *lh_ctx_last_error(const lh_ctx *ctx) { return ctx ? ctx->c.last_error.c_str() : ""; }
 
+void *lh_ctx_stream(const lh_ctx *ctx) { return ctx ? (void *)ctx->c.stream : nullptr; }
+
 int lh_ctx_synchronize(lh_ctx *ctx) {
     return guard(ctx, [&] { LH_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
 }
@@ -361,6 +363,50 @@ int lh_hmat_export_block(lh_ctx *ctx, const lh_hmat *h, int64_t block, double *a
                 for (i64 i = 0; i < nd.m; ++i) b[i] = (double)p[i];
             }
         }
+        LH_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int lh_hmat_layout(const lh_hmat *h, int64_t *recs, int64_t *sizes) {
+    const HMat &H = h->h;
+    if (sizes) {
+        sizes[0] = H.arena_len;
+        sizes[1] = H.nslots;
+        sizes[2] = H.perm_len;
+    }
+    if (recs)
+        for (size_t k = 0; k < H.leafblocks.size(); ++k) {
+            const Node &n = H.nodes[H.leafblocks[k]];
+            int64_t *r = recs + 11 * k;
+            r[0] = n.r0;
+            r[1] = n.r0 + n.m;
+            r[2] = n.c0;
+            r[3] = n.c0 + n.n;
+            r[4] = n.kind;
+            r[5] = n.doff;
+            r[6] = n.uoff;
+            r[7] = n.voff;
+            r[8] = n.kcap;
+            r[9] = n.rslot;
+            r[10] = n.poff;
+        }
+    return LH_OK;
+}
+
+int lh_hmat_export_arena(lh_ctx *ctx, const lh_hmat *h, double *arena, int32_t *ranks,
+                         int32_t *perm) {
+    return guard(ctx, [&] {
+        const HMat &H = h->h;
+        cudaStream_t s = ctx->c.stream;
+        if (arena && H.arena_len)
+            LH_CUDA(cudaMemcpyAsync(arena, H.d_arena, sizeof(double) * H.arena_len,
+                                    cudaMemcpyDeviceToHost, s));
+        if (ranks && H.nslots)
+            LH_CUDA(cudaMemcpyAsync(ranks, H.d_ranks, sizeof(int32_t) * H.nslots,
+                                    cudaMemcpyDeviceToHost, s));
+        if (perm && H.perm_len)
+            LH_CUDA(cudaMemcpyAsync(perm, H.d_perm, sizeof(int32_t) * H.perm_len,
+                                    cudaMemcpyDeviceToHost, s));
         LH_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -595,7 +595,11 @@ struct SolvePlans {
     std::shared_ptr<MvPlan> mvL, mvU;
     double *tmp = nullptr;          // scratch vector(s)
     i64 tmp_len = 0;
+    cudaGraphExec_t graph = nullptr;  // cached CN step
+    const double *g_u = nullptr, *g_y = nullptr;
+    const HMat *g_hm = nullptr;
     ~SolvePlans() {
+        if (graph) cudaGraphExecDestroy(graph);
         if (tmp) cudaFree(tmp);
     }
 };
@@ -794,22 +798,35 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
     if (method == 1) {
         SolvePlans &S = plans_of(F);
         LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
-        // one step = 3 H-matvecs (6 kernels), captured once as a CUDA graph
+        // one step = 3 H-matvecs (6 kernels), captured once as a CUDA graph and cached
+        // per (operator, vector, scratch) so repeated single-step calls do not re-capture
         for (int q = 0; q < nrhs; ++q) {
             double *uq = u + (i64)q * ldu;
-            cudaGraph_t g;
-            cudaGraphExec_t ge;
-            LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
-            mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
-            mv_run(*S.mvL, *S.XL, y, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
-            mv_run(*S.mvU, *S.XU, S.tmp, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
-            LH_CUDA(cudaStreamEndCapture(ctx.stream, &g));
-            LH_CUDA(cudaGraphInstantiate(&ge, g, 0));
-            for (int k = 0; k < nsteps; ++k) LH_CUDA(cudaGraphLaunch(ge, ctx.stream));
-            LH_CUDA(cudaStreamSynchronize(ctx.stream));
-            cudaGraphExecDestroy(ge);
-            cudaGraphDestroy(g);
+            if (!(S.graph && S.g_u == uq && S.g_hm == &Hm && S.g_y == y)) {
+                if (S.graph) {
+                    cudaGraphExecDestroy(S.graph);
+                    S.graph = nullptr;
+                }
+                cudaGraph_t g;
+                LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                    mv_run(*S.mvL, *S.XL, y, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                    mv_run(*S.mvU, *S.XU, S.tmp, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                } catch (...) {
+                    cudaStreamEndCapture(ctx.stream, &g);
+                    throw;
+                }
+                LH_CUDA(cudaStreamEndCapture(ctx.stream, &g));
+                LH_CUDA(cudaGraphInstantiate(&S.graph, g, 0));
+                cudaGraphDestroy(g);
+                S.g_u = uq;
+                S.g_hm = &Hm;
+                S.g_y = y;
+            }
+            for (int k = 0; k < nsteps; ++k) LH_CUDA(cudaGraphLaunch(S.graph, ctx.stream));
         }
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
         return;
     }
     for (int q = 0; q < nrhs; ++q) {

@@ -264,6 +264,24 @@ def export_blocks(H):
     return out
 
 
+def export_layout(H):
+    """Host copy of the whole device storage: (recs, arena, ranks, perm), recs[b] =
+    (row0,row1,col0,col1,kind 1 dense/2 lowrank/3 dense_lu, dense_off, u_off, v_off, kcap,
+    rank_slot, perm_off) in walk order."""
+    L = _lib.lib()
+    sizes = np.zeros(3, dtype=np.int64)
+    L.lh_hmat_layout(H.handle, None, _lib.host_ptr(sizes))
+    nb = H.num_blocks()
+    recs = np.empty((nb, 11), dtype=np.int64)
+    L.lh_hmat_layout(H.handle, _lib.host_ptr(recs), _lib.host_ptr(sizes))
+    arena = np.empty(max(int(sizes[0]), 1), dtype=np.float64)
+    ranks = np.zeros(max(int(sizes[1]), 1), dtype=np.int32)
+    perm = np.zeros(max(int(sizes[2]), 1), dtype=np.int32)
+    _lib.check(L.lh_hmat_export_arena(H.ctx.h, H.handle, _lib.host_ptr(arena), _lib.host_ptr(ranks),
+                                      _lib.host_ptr(perm)), H.ctx.h)
+    return recs, arena, ranks, perm
+
+
 def to_dense(H):
     """hmatrix.py:402-413 (host copy; small matrices only)."""
     if H.factored:
