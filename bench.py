@@ -298,7 +298,7 @@ def run_b200(args, world, rank, local):
                       "solve": "triangular-inverse H-factors of the H-LU (DESIGN.md)",
                       "parallelism": f"replicas x{world}",
                       "l2": "inputs larger than L2 (>= 14 GB streamed per step vs 126 MB L2)"},
-           "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": 6 * args.steps,
+           "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": 9 * args.steps,
            "roofline": roofline, "phases": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in times.items()}}
 
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -50,6 +50,7 @@ HMat::~HMat() {
     if (d_arena) cudaFree(d_arena);
     if (d_ranks) cudaFree(d_ranks);
     if (d_perm) cudaFree(d_perm);
+    if (d_inv) cudaFree(d_inv);
 }
 void HMat::sync_ranks(cudaStream_t s) {
     h_ranks.assign(std::max(nslots, 0), 0);

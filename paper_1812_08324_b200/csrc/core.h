@@ -76,6 +76,7 @@ struct Node {
     int32_t kcap;         // LR: column capacity
     int32_t rslot;        // LR: index into the rank array
     i64 poff;             // FDENSE: offset of the int32 net row permutation
+    i64 ioff = -1;        // FDENSE: offset of the packed leaf inverse (L^-1 strict lower, U^-1 upper)
     int32_t depth;        // block-tree depth
 };
 
@@ -95,6 +96,8 @@ struct HMat {
     int32_t nslots = 0;
     int32_t *d_perm = nullptr;        // FDENSE permutations
     i64 perm_len = 0;
+    double *d_inv = nullptr;          // FDENSE packed leaf inverses
+    i64 inv_len = 0;
     bool factored = false;
     double lu_stats[4] = {0, 0, 0, 0};  // tasks, plan seconds, temp bytes, -
     // lazily built plans (opaque; see matvec.cu / plan.cpp)

@@ -31,10 +31,17 @@ struct ExecArgs {
     int32_t *done;
     int32_t *counter;
     int32_t *err;  // [0] code, [1] task, [2] path
-    double *base[4];
+    double *base[NBASE];
     int32_t *ranks;
     int32_t *perm;
+    unsigned long long *times;  // optional: [2*t] start (deps met), [2*t+1] end (globaltimer ns)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int SMEM_BYTES = 168 * 1024;
 
@@ -61,11 +68,190 @@ __device__ __forceinline__ void st_release(int32_t *p, int v) {
 }
 
 // ---------------------------------------------------------------------------
+// GETRF fast path (m <= 64): right-looking LU with partial pivoting, thread (row
+// i = t % 64, column group t / 64), 2 barriers per column; then the packed leaf
+// inverse P = strict_lower(L^-1) + upper(U^-1) by one fused forward/backward sweep.
+// ---------------------------------------------------------------------------
+constexpr int LD65 = 65;  // odd leading dimension: conflict-free column and row walks
+
+__device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double *sm) {
+    const DView &v = T.v[0];
+    const int m = v.rows;
+    double *G = vp(A, v);
+    double *S = sm;                       // m x m, ld 65
+    double *Li = sm + 64 * LD65;          // L^-1 (unit lower)
+    double *Ui = sm + 2 * 64 * LD65;      // U^-1 (upper, unscaled rows until the end)
+    int *piv = (int *)(sm + 3 * 64 * LD65);
+    __shared__ int s_p;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    for (int e = threadIdx.x; e < m * m; e += NT) S[(e % m) + (e / m) * LD65] = G[e % m + (e / m) * (i64)v.ld];
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = 0; j < m; ++j) {
+        if (w == 0) {
+            double best = -1.0;
+            int bi = j;
+            for (int i = j + lane; i < m; i += 32) {
+                double a = fabs(S[i + j * LD65]);
+                if (a > best) {
+                    best = a;
+                    bi = i;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                s_p = bi;
+                piv[j] = bi;
+            }
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (p != j) {
+            if (threadIdx.x < m) {
+                const int c = threadIdx.x;
+                double t = S[j + c * LD65];
+                S[j + c * LD65] = S[p + c * LD65];
+                S[p + c * LD65] = t;
+            }
+            __syncthreads();
+        }
+        const double d = S[j + j * LD65];
+        double l = 0.0;
+        if (tx > j && tx < m) {
+            l = d != 0.0 ? S[tx + j * LD65] / d : S[tx + j * LD65];
+            for (int c = j + 1 + ty; c < m; c += 4) S[tx + c * LD65] -= l * S[j + c * LD65];
+        }
+        __syncthreads();
+        if (ty == 0 && tx > j && tx < m) S[tx + j * LD65] = l;  // column j is not read again
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * m; e += NT) G[e % m + (e / m) * (i64)v.ld] = S[(e % m) + (e / m) * LD65];
+    if (threadIdx.x == 0) {
+        int32_t *pp = A.perm + T.aux;
+        for (int i = 0; i < m; ++i) pp[i] = i;
+        for (int i = 0; i < m; ++i) {
+            int q = piv[i];
+            if (q != i) {
+                int t = pp[i];
+                pp[i] = pp[q];
+                pp[q] = t;
+            }
+        }
+        for (int i = 0; i < m; ++i)
+            if (S[i + i * LD65] == 0.0) {
+                set_err(A, LH_ESINGULAR, tid, T.path);
+                break;
+            }
+    }
+    if (!(T.flags & 1)) return;
+    // identity start
+    for (int e = threadIdx.x; e < m * m; e += NT) {
+        int i = e % m, c = e / m;
+        Li[i + c * LD65] = (i == c) ? 1.0 : 0.0;
+        Ui[i + c * LD65] = (i == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    // step k: forward column k of L X = I, backward column l = m-1-k of U X = I
+    for (int k = 0; k < m; ++k) {
+        const int l = m - 1 - k;
+        if (tx > k && tx < m) {
+            const double a = S[tx + k * LD65];
+            for (int c = ty; c <= k; c += 4) Li[tx + c * LD65] -= a * Li[k + c * LD65];
+        }
+        if (tx < l) {
+            const double a = S[tx + l * LD65] / S[l + l * LD65];
+            for (int c = l + ty; c < m; c += 4) Ui[tx + c * LD65] -= a * Ui[l + c * LD65];
+        }
+        __syncthreads();
+    }
+    // rows of U^-1 are divided by the pivots; pack strict lower of L^-1 with upper of U^-1
+    double *Pg = A.base[T.v[1].base] + T.v[1].off;
+    for (int e = threadIdx.x; e < m * m; e += NT) {
+        int i = e % m, c = e / m;
+        Pg[e] = (i > c) ? Li[i + c * LD65] : Ui[i + c * LD65] / S[i + i * LD65];
+    }
+}
+
+// TRSM through the packed leaf inverse: B <- op(T^-1) P B as a small GEMM
+// (mode 0: L^-1 with the leaf permutation; 1: U^-1; 2: U^-T).
+__device__ void task_trsm_inv(const ExecArgs &A, const DTask &T, double *sm) {
+    const DView &bv = T.v[1];
+    const DView &iv = T.v[2];
+    const int m = iv.rows;
+    const int mode = T.flags & 15;
+    const double *Pg = A.base[iv.base] + iv.off;
+    double *Bg = vp(A, bv);
+    const int k = vcols(A, bv);
+    if (k <= 0) return;
+    double *Ps = sm;                 // m x m, ld 65
+    double *Bs = sm + 64 * LD65;     // m x 64, ld 65
+    const int32_t *perm = A.perm + T.aux;
+    for (int e = threadIdx.x; e < m * m; e += NT) Ps[(e % m) + (e / m) * LD65] = Pg[e];
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    for (int c0 = 0; c0 < k; c0 += 64) {
+        const int kc = min(64, k - c0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < m * kc; e += NT) {
+            int i = e % m, c = e / m;
+            int src = (mode == 0) ? perm[i] : i;
+            Bs[i + c * LD65] = Bg[vi(bv, src, c0 + c)];
+        }
+        __syncthreads();
+        double acc[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+        if (tx < m) {
+            if (mode == 0) {
+                for (int l = 0; l < tx; ++l) {
+                    const double a = Ps[tx + l * LD65];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) acc[q] += a * Bs[l + (ty + 4 * q) * LD65];
+                }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) acc[q] += Bs[tx + (ty + 4 * q) * LD65];
+            } else if (mode == 1) {
+                for (int l = tx; l < m; ++l) {
+                    const double a = Ps[tx + l * LD65];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) acc[q] += a * Bs[l + (ty + 4 * q) * LD65];
+                }
+            } else {
+                for (int l = 0; l <= tx; ++l) {
+                    const double a = Ps[l + tx * LD65];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) acc[q] += a * Bs[l + (ty + 4 * q) * LD65];
+                }
+            }
+        }
+        __syncthreads();
+        if (tx < m) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int c = ty + 4 * q;
+                if (c < kc) Bg[vi(bv, tx, c0 + c)] = acc[q];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // GETRF: partial pivoting LU of a dense m x m leaf (sla.lu_factor, hops.py:394)
 // ---------------------------------------------------------------------------
 __device__ void task_getrf(const ExecArgs &A, const DTask &T, int tid, double *sm) {
     const DView &v = T.v[0];
     const int m = v.rows;
+    if (m <= 64 && !v.trans) {
+        task_getrf64(A, T, tid, sm);
+        return;
+    }
     double *G = vp(A, v);
     double *S = sm;                       // m x m, column-major
     int *piv = (int *)(sm + m * m);
@@ -144,6 +330,10 @@ __device__ void task_getrf(const ExecArgs &A, const DTask &T, int tid, double *s
 // (dtrsm in _leaf_solve, hops.py:185-208)
 // ---------------------------------------------------------------------------
 __device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
+    if (T.flags & 64) {
+        task_trsm_inv(A, T, sm);
+        return;
+    }
     const DView &tv = T.v[0];
     const DView &bv = T.v[1];
     const int m = tv.rows;
@@ -204,12 +394,75 @@ __device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
 // ---------------------------------------------------------------------------
 // SEGMUL: Y_seg = beta Y_seg + alpha * sum of pieces (mul_dense/tmul_dense rows)
 // ---------------------------------------------------------------------------
+// fast path: Y segment of <= 64 rows, no transposed operands; each piece's X rows (or
+// W) staged in shared memory, the piece's rows streamed from global (coalesced), 16
+// accumulators per thread (row t % 64, columns t / 64 + 4q).
+__device__ void task_segmul_fast(const ExecArgs &A, const DTask &T, double *sm) {
+    const DView &yv = T.v[0];
+    const int s = yv.rows;
+    const int k = vcols(A, yv);
+    double *Yg = vp(A, yv);
+    const bool overwrite = T.flags & 1;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    double *Xs = sm;
+    for (int c0 = 0; c0 < k; c0 += 64) {
+        const int kc = min(64, k - c0);
+        double acc[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+        for (int p = T.pc_beg; p < T.pc_end; ++p) {
+            const DPiece pc = A.pieces[p];
+            const double *M = vp(A, pc.mat);
+            const double *X = vp(A, pc.x);
+            const int inner = pc.kind == 0 ? pc.mat.cols : vcols(A, pc.mat);
+            if (inner == 0) continue;
+            __syncthreads();
+            for (int e = threadIdx.x; e < inner * kc; e += NT) {
+                int j = e % inner, c = e / inner;
+                Xs[e] = X[j + (i64)(c0 + c) * pc.x.ld];
+            }
+            __syncthreads();
+            if (tx < s) {
+                const double *Mr = M + tx;
+                const i64 ldm = pc.mat.ld;
+                for (int j = 0; j < inner; ++j) {
+                    const double a = Mr[j * ldm];
+                    const double *xr = Xs + j;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) acc[q] += a * xr[(ty + 4 * q) * inner];
+                }
+            }
+        }
+        if (tx < s) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int c = ty + 4 * q;
+                if (c < kc) {
+                    double &y = Yg[tx + (i64)(c0 + c) * yv.ld];
+                    y = (overwrite ? 0.0 : y) + T.alpha * acc[q];
+                }
+            }
+        }
+    }
+}
+
 __device__ void task_segmul(const ExecArgs &A, const DTask &T, double *sm) {
     const DView &yv = T.v[0];
     const int s = yv.rows;
     const int k = vcols(A, yv);
     double *Yg = vp(A, yv);
     const bool overwrite = T.flags & 1;
+    {
+        bool fast = s <= 64 && !yv.trans;
+        for (int p = T.pc_beg; p < T.pc_end && fast; ++p) {
+            const DPiece &pc = A.pieces[p];
+            fast = !pc.mat.trans && !pc.x.trans && (pc.kind == 1 || pc.mat.cols <= 128);
+        }
+        if (fast) {
+            task_segmul_fast(A, T, sm);
+            return;
+        }
+    }
     const int RP = s <= 64 ? 64 : (s <= 128 ? 128 : 256);
     const int G = NT / RP;            // thread groups over columns
     const int i = threadIdx.x % RP, g = threadIdx.x / RP;
@@ -262,8 +515,9 @@ __device__ void task_vtx(const ExecArgs &A, const DTask &T, double *sm) {
     double *W = vp(A, wv);
     if (r == 0 || k == 0) return;
     constexpr int CH = 64;
-    double *Fs = sm;                 // CH x r
-    double *Xs = sm + CH * KC_MAX;   // CH x k (k <= 128)
+    constexpr int CL = CH + 1;       // odd stride: column walks hit distinct banks
+    double *Fs = sm;                 // CH x r, ld CL
+    double *Xs = sm + CL * KC_MAX;   // CH x k (k <= 128), ld CL
     constexpr int NP = 16;
     const int npair = r * k;
     double acc[NP];
@@ -272,8 +526,14 @@ __device__ void task_vtx(const ExecArgs &A, const DTask &T, double *sm) {
     for (int j0 = 0; j0 < n; j0 += CH) {
         const int len = min(CH, n - j0);
         __syncthreads();
-        for (int e = threadIdx.x; e < len * r; e += NT) Fs[e] = F[vi(fv, j0 + e % len, e / len)];
-        for (int e = threadIdx.x; e < len * k; e += NT) Xs[e] = X[vi(xv, j0 + e % len, e / len)];
+        for (int e = threadIdx.x; e < len * r; e += NT) {
+            int j = e % len, c = e / len;
+            Fs[j + c * CL] = F[vi(fv, j0 + j, c)];
+        }
+        for (int e = threadIdx.x; e < len * k; e += NT) {
+            int j = e % len, c = e / len;
+            Xs[j + c * CL] = X[vi(xv, j0 + j, c)];
+        }
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
@@ -281,7 +541,8 @@ __device__ void task_vtx(const ExecArgs &A, const DTask &T, double *sm) {
             if (p < npair) {
                 int l = p % r, c = p / r;
                 double s = 0.0;
-                for (int j = 0; j < len; ++j) s += Fs[j + l * len] * Xs[j + c * len];
+                const double *fa = Fs + l * CL, *xa = Xs + c * CL;
+                for (int j = 0; j < len; ++j) s += fa[j] * xa[j];
                 acc[q] += s;
             }
         }
@@ -456,6 +717,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
         }
         __syncthreads();
         __threadfence();  // acquire side: drop stale L1 lines before reading operands
+        if (A.times && threadIdx.x == 0) A.times[2 * t] = gtimer();
         switch (T.type) {
             case T_GETRF: task_getrf(A, T, t, sm); break;
             case T_TRSM: task_trsm(A, T, sm); break;
@@ -473,6 +735,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
+            if (A.times) A.times[2 * t + 1] = gtimer();
             st_release(A.done + t, 1);
         }
     }
@@ -515,8 +778,61 @@ static int exec_grid(Ctx &ctx) {
     return ctx.num_sms * per_sm;
 }
 
+// Task-level profile (LEVYH_TASK_PROFILE=<file>): per-type busy time and the measured
+// critical path (latest-finishing predecessor chain) with its per-type composition.
+static void report_profile(const Plan &P, const std::vector<unsigned long long> &tm, const char *label) {
+    const char *path = getenv("LEVYH_TASK_PROFILE");
+    if (!path) return;
+    FILE *f = fopen(path, "a");
+    if (!f) return;
+    const int n = (int)P.tasks.size();
+    const char *names[] = {"?", "GETRF", "TRSM", "SEGMUL", "VTX", "LRADD", "DGEMM", "DADD",
+                           "DENSIFY", "IDENT", "NOP", "RAND", "ORTH"};
+    double busy[13] = {0}, cnt[13] = {0}, cp_busy[13] = {0}, cp_cnt[13] = {0};
+    unsigned long long t0 = ~0ull, t1 = 0;
+    int last = 0;
+    for (int i = 0; i < n; ++i) {
+        int ty = std::min(std::max(P.tasks[i].type, 0), 12);
+        busy[ty] += (tm[2 * i + 1] - tm[2 * i]) * 1e-9;
+        cnt[ty] += 1;
+        t0 = std::min(t0, tm[2 * i]);
+        if (tm[2 * i + 1] > t1) {
+            t1 = tm[2 * i + 1];
+            last = i;
+        }
+    }
+    double wait = 0.0;
+    int len = 0;
+    for (int t = last; t >= 0;) {
+        const DTask &T = P.tasks[t];
+        int ty = std::min(std::max(T.type, 0), 12);
+        cp_busy[ty] += (tm[2 * t + 1] - tm[2 * t]) * 1e-9;
+        cp_cnt[ty] += 1;
+        ++len;
+        int best = -1;
+        unsigned long long be = 0;
+        for (int k = 0; k < T.dep_cnt; ++k) {
+            int p = P.deps[T.dep_beg + k];
+            if (best < 0 || tm[2 * p + 1] > be) {
+                be = tm[2 * p + 1];
+                best = p;
+            }
+        }
+        if (best >= 0 && tm[2 * t] > be) wait += (tm[2 * t] - be) * 1e-9;
+        t = best;
+    }
+    fprintf(f, "== %s: %d tasks, span %.4f s, critical path %d tasks, waits on path %.4f s\n", label, n,
+            (t1 - t0) * 1e-9, len, wait);
+    for (int ty = 1; ty <= 12; ++ty)
+        if (cnt[ty] > 0)
+            fprintf(f, "  %-8s count %9.0f busy %9.4f s mean %8.2f us | on path %7.0f tasks %8.4f s\n",
+                    names[ty], cnt[ty], busy[ty], 1e6 * busy[ty] / cnt[ty], cp_cnt[ty], cp_busy[ty]);
+    fclose(f);
+}
+
 // Run a plan; F / X / RHS bases.  Ranks of F (and X) are copied in and back out.
-static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val) {
+static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val,
+                     const char *label = "plan") {
     cudaStream_t s = ctx.stream;
     LH_CUDA(cudaMemsetAsync(P.d_done, 0, sizeof(int32_t) * (P.tasks.size() + 1), s));
     LH_CUDA(cudaMemsetAsync(P.d_err, 0, sizeof(int32_t) * 4, s));
@@ -541,8 +857,12 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     A.base[B_TMP] = P.d_temp;
     A.base[B_RHS] = rhs;
     A.base[B_X] = X ? X->d_arena : nullptr;
+    A.base[B_INV] = F.d_inv;
     A.ranks = P.d_ranks;
     A.perm = F.d_perm;
+    A.times = nullptr;
+    const bool prof = getenv("LEVYH_TASK_PROFILE") != nullptr && A.ntasks > 0;
+    if (prof) A.times = dalloc<unsigned long long>(2 * (i64)A.ntasks);
     if (A.ntasks > 0) {
         int grid = exec_grid(ctx);
         void *args[] = {&A};
@@ -551,6 +871,13 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     int err[4];
     LH_CUDA(cudaMemcpyAsync(err, P.d_err, sizeof(err), cudaMemcpyDeviceToHost, s));
     LH_CUDA(cudaStreamSynchronize(s));
+    if (prof) {
+        std::vector<unsigned long long> tm(2 * (size_t)A.ntasks);
+        LH_CUDA(cudaMemcpy(tm.data(), A.times, sizeof(unsigned long long) * tm.size(),
+                           cudaMemcpyDeviceToHost));
+        cudaFree(A.times);
+        report_profile(P, tm, label);
+    }
     if (F.nslots)
         LH_CUDA(cudaMemcpyAsync(F.d_ranks, P.d_ranks, sizeof(int32_t) * F.nslots,
                                 cudaMemcpyDeviceToDevice, s));
@@ -575,12 +902,13 @@ void hlu(Ctx &ctx, HMat &F, double eps2) {
     auto P = plan_hlu(F, eps2, perm_len);  // marks diagonal leaves K_FDENSE
     F.d_perm = dalloc<int32_t>(std::max<i64>(perm_len, 1));
     F.perm_len = perm_len;
+    F.d_inv = dalloc<double>(std::max<i64>(F.inv_len, 1));
     P->upload(ctx.stream);
     F.factored = true;
     F.mv_plan.reset();
     LH_CUDA(cudaStreamSynchronize(ctx.stream));
     auto t0 = std::chrono::steady_clock::now();
-    run_plan(ctx, *P, F, nullptr, nullptr, -1);
+    run_plan(ctx, *P, F, nullptr, nullptr, -1, "hlu");
     F.lu_stats[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     F.sync_ranks(ctx.stream);
     F.lu_stats[0] = (double)P->tasks.size();
@@ -619,7 +947,7 @@ static void solve_substitution(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) 
     }
     for (int c0 = 0; c0 < nrhs; c0 += CAP) {
         int kc = std::min(CAP, nrhs - c0);
-        run_plan(ctx, *S.sub, F, nullptr, b + (i64)c0 * ldb, kc);
+        run_plan(ctx, *S.sub, F, nullptr, b + (i64)c0 * ldb, kc, "solve");
     }
 }
 
@@ -674,7 +1002,7 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
         LH_CUDA(cudaMemsetAsync(X->d_ranks, 0, sizeof(int32_t) * std::max(X->nslots, 1), ctx.stream));
         auto P = plan_inverse(F, *X, mode, eps2);
         P->upload(ctx.stream);
-        run_plan(ctx, *P, F, X.get(), nullptr, -1);
+        run_plan(ctx, *P, F, X.get(), nullptr, -1, mode == 0 ? "inverse L" : "inverse U");
         X->sync_ranks(ctx.stream);
         std::vector<int32_t> blocks;
         for (int32_t b : X->leafblocks)
@@ -748,10 +1076,7 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out
         for (int q = 0; q < 3; ++q) {
             const MvPlan &P = *plans[q];
             LH_CUDA(cudaEventRecord(ev[2 * q], ctx.stream));
-            if (P.nch > 0) {
-                int g1 = std::min(P.nch, ctx.num_sms * 16);
-                mv_vtx_launch(P, *mats[q], xin[q], g1, ctx.stream);
-            }
+            mv_vtx_launch(P, *mats[q], xin[q], ctx.num_sms * 16, ctx.stream);
             LH_CUDA(cudaEventRecord(ev[2 * q + 1], ctx.stream));
             mv_seg_launch(P, *mats[q], xin[q], yout[q], 1.0, 0.0, ctx.stream, ctx.num_sms);
         }

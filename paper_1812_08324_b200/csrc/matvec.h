@@ -25,10 +25,20 @@ struct MvLr {  // U rows of the piece at arena[off + i + c * ld]; t_b from chunk
 struct VChunk {  // V rows at arena[voff + i + c * ld], i < len, multiplies x[xc0 + i]
     i64 voff, ld, xc0;
     int32_t len, slot;
+    i64 tout;      // >= 0: whole block in this chunk, write t_b at tvec[tout]
+    int32_t pidx;  // else: partial row index
+    int32_t pad;
+};
+
+struct TJob {  // t_b = sum of the partials of chunks [cbeg, cend) of the block in rank slot `slot`
+    int32_t slot, cbeg, cend;
 };
 
 struct MvPlan {
-    int nseg = 0, nch = 0;
+    int nseg = 0, nch = 0, nch16 = 0, ntj = 0;
+    VChunk *chunks16 = nullptr;  // chunks whose block rank exceeded 8 at plan time
+    TJob *tjobs = nullptr;
+    double *tvec = nullptr;  // KC_MAX per rank slot
     i64 n_dpieces = 0, n_lpieces = 0;
     SegDesc *segs = nullptr;
     MvDense *dp = nullptr;

@@ -352,7 +352,10 @@ void Planner::solve_dense(const Mref &T, int32_t t, const PView &B, int mode, bo
         k.aux = (int32_t)nd.poff;
         k.v[0] = Tv.d;
         k.v[1] = B.d;
-        k.path = add_path(path);
+        if (nd.ioff >= 0) {  // apply the packed leaf inverse written by the leaf's GETRF
+            k.flags |= 64;
+            k.v[2] = DView{nd.ioff, (int32_t)nd.m, (int32_t)nd.m, (int32_t)nd.m, -1, B_INV, 0, 0};
+        }
         emit(k, {{&Tv, false}, {&B, true}});
         return;
     }
@@ -677,6 +680,12 @@ void Planner::lu_block(int32_t b, const std::string &path) {
         nd.poff = perm_len;
         perm_len += nd.m;
         t.v[0] = D.d;
+        if (nd.m <= LEAF_INV_MAX) {  // also write the packed leaf inverse (L^-1 | U^-1)
+            nd.ioff = inv_len;
+            inv_len += nd.m * nd.m;
+            t.v[1] = DView{nd.ioff, (int32_t)nd.m, (int32_t)nd.m, (int32_t)nd.m, -1, B_INV, 0, 0};
+            t.flags = 1;
+        }
         t.path = add_path("zero pivot in dense diagonal leaf at " + path);
         emit(t, {{&D, true}});
         nd.kind = K_FDENSE;
@@ -765,6 +774,7 @@ std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out) {
     pl.lu_block(F.root, "root");
     pl.finalize();
     perm_len_out = pl.perm_len;
+    F.inv_len = pl.inv_len;
     pl.P->build_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return pl.P;

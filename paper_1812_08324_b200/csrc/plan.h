@@ -15,7 +15,9 @@
 
 namespace lh {
 
-enum Base : int8_t { B_F = 0, B_TMP = 1, B_RHS = 2, B_X = 3 };
+enum Base : int8_t { B_F = 0, B_TMP = 1, B_RHS = 2, B_X = 3, B_INV = 4 };
+constexpr int NBASE = 5;
+constexpr int LEAF_INV_MAX = 64;  // diagonal leaves up to this size also store packed inverses
 
 struct DView {     // element (i, j) = base[off + (trans ? j + i*ld : i + j*ld)]
     i64 off;

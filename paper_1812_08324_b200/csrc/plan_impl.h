@@ -57,6 +57,7 @@ struct Planner {
     DepTracker deps;
     double eps2 = 1e-10;
     i64 perm_len = 0;
+    i64 inv_len = 0;
     int32_t next_slot = 0;
     int32_t next_temp = 0;
     struct TempRec {
