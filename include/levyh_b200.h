@@ -145,6 +145,11 @@ int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double 
                     int32_t iters, double *out_host);
 /* out[0..3] = H-LU task count, planning seconds, temp bytes, executor seconds */
 int lh_hlu_stats(const lh_hmat *factor, double *out_host);
+/* Executor micro-benchmark: R synthetic tasks of one kind (0 GETRF 64x64 + leaf inverse,
+ * 1 TRSM via leaf inverse, 2 SEGMUL with one dense 64x64 piece), k right-hand columns,
+ * chained (each depends on the previous) or independent.  out[0] = wall us per task,
+ * out[1] = mean task body us (device timestamps). */
+int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out_host);
 
 /* ---- entry generation: fractional.py:285-405 + levy.py:169-206 -------- */
 typedef struct {

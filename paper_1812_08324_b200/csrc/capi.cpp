@@ -26,6 +26,7 @@ void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method);
 void prepare_inverse(Ctx &ctx, HMat &F, double eps2);
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method);
 void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out);
+void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
 
 void *Ctx::ensure_scratch(size_t bytes) {
     if (bytes > scratch_bytes) {
@@ -439,6 +440,10 @@ int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t l
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int32_t iters,
                     double *out) {
     return guard(ctx, [&] { step_profile(ctx->c, const_cast<HMat &>(hm->h), f->h, u, iters, out); });
+}
+
+int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out) {
+    return guard(ctx, [&] { task_bench(ctx->c, kind, R, k, chain != 0, out); });
 }
 
 int lh_hlu_stats(const lh_hmat *f, double *out) {

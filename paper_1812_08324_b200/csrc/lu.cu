@@ -29,7 +29,11 @@ struct ExecArgs {
     const int32_t *deps;
     const DPiece *pieces;
     int32_t *done;
-    int32_t *counter;
+    int32_t *counter;    // next FIFO slot to take
+    int32_t *tail;       // next FIFO slot to fill
+    int32_t *queue;      // ready FIFO (task ids, -1 = not yet filled)
+    int32_t *remaining;  // unfinished predecessors per task
+    const int32_t *succ_beg, *succ;  // successor CSR
     int32_t *err;  // [0] code, [1] task, [2] path
     double *base[NBASE];
     int32_t *ranks;
@@ -44,6 +48,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 constexpr int SMEM_BYTES = 168 * 1024;
+constexpr unsigned POLL_NS_MAX = 128;
 
 __device__ __forceinline__ double *vp(const ExecArgs &A, const DView &v) { return A.base[v.base] + v.off; }
 __device__ __forceinline__ i64 vi(const DView &v, i64 i, i64 j) {
@@ -178,6 +183,189 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
         int i = e % m, c = e / m;
         Pg[e] = (i > c) ? Li[i + c * LD65] : Ui[i + c * LD65] / S[i + i * LD65];
     }
+}
+
+// ---------------------------------------------------------------------------
+// Register-tiled small GEMM helpers: thread (row tx = t % 64, column group ty = t / 64)
+// owns columns c0 + ty + 4q, q < NQ.  Operands stream through L1 (row-coalesced), no
+// shared-memory staging and no barriers; NQ is picked from the column count.
+// ---------------------------------------------------------------------------
+struct Strided {  // element (i, j) at p[i * si + j * sj]
+    const double *p;
+    i64 si, sj;
+};
+__device__ __forceinline__ Strided strided(const ExecArgs &A, const DView &v) {
+    Strided s;
+    s.p = A.base[v.base] + v.off;
+    s.si = v.trans ? v.ld : 1;
+    s.sj = v.trans ? 1 : v.ld;
+    return s;
+}
+
+// acc[q] += sum_{j in [j0, j1)} M(tx, j) * X(xrow(j), c0 + ty + 4q)
+template <int NQ>
+__device__ __forceinline__ void tile_fma(double (&acc)[NQ], const Strided &M, int tx, int j0, int j1,
+                                         const Strided &X, const int32_t *xperm, int c0, int ty,
+                                         int kc) {
+    const double *mrow = M.p + tx * M.si;
+    int cidx[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) cidx[q] = min(c0 + ty + 4 * q, c0 + kc - 1);  // clamp: always valid
+    int j = j0;
+    for (; j + 2 <= j1; j += 2) {
+        const double a0 = mrow[j * M.sj], a1 = mrow[(j + 1) * M.sj];
+        const i64 r0 = xperm ? xperm[j] : j, r1 = xperm ? xperm[j + 1] : j + 1;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const double x0 = X.p[r0 * X.si + cidx[q] * X.sj];
+            const double x1 = X.p[r1 * X.si + cidx[q] * X.sj];
+            acc[q] += a0 * x0 + a1 * x1;
+        }
+    }
+    if (j < j1) {
+        const double a0 = mrow[j * M.sj];
+        const i64 r0 = xperm ? xperm[j] : j;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] += a0 * X.p[r0 * X.si + cidx[q] * X.sj];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cp.async staging: copies carry no register result, so every copy of a tile issues
+// back to back and the tile costs one memory round trip (a load->store loop would
+// serialise one round trip per element).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp8(double *smem, const double *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// stage a (rows x cols) view into smem at dst[i + j * lds] (optionally row-permuted source)
+__device__ __forceinline__ void stage_view(double *dst, int lds, const Strided &S, int rows, int cols,
+                                           int col0, const int32_t *rperm) {
+    for (int e = threadIdx.x; e < rows * cols; e += NT) {
+        const int i = e % rows, j = e / rows;
+        const i64 ri = rperm ? rperm[i] : i;
+        cp8(dst + i + j * lds, S.p + ri * S.si + (i64)(col0 + j) * S.sj);
+    }
+}
+
+// TRSM via the packed leaf inverse (m <= 64): P and B staged with cp.async, product from
+// shared memory, written back in place (all reads of B precede the writes).
+template <int NQ>
+__device__ void trsm_inv_staged(const ExecArgs &A, const DTask &T, int k, double *sm) {
+    const DView &bv = T.v[1];
+    const DView &iv = T.v[2];
+    const int m = iv.rows;
+    const int mode = T.flags & 15;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    double *Ps = sm;               // m x m, ld 65
+    double *Bs = sm + 64 * LD65;   // m x 64, ld 65
+    const Strided Pg = strided(A, iv);
+    const Strided Bg = strided(A, bv);
+    const int32_t *perm = mode == 0 ? A.perm + T.aux : nullptr;
+    double *Bw = vp(A, bv);
+    stage_view(Ps, LD65, Pg, m, m, 0, nullptr);
+    for (int c0 = 0; c0 < k; c0 += 4 * NQ) {
+        const int kc = min(4 * NQ, k - c0);
+        stage_view(Bs, LD65, Bg, m, kc, c0, perm);
+        cp_commit();
+        cp_wait<0>();
+        __syncthreads();
+        double acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+        int cq[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) cq[q] = min(ty + 4 * q, kc - 1) * LD65;
+        if (tx < m) {
+            if (mode == 0) {
+                for (int l = 0; l < tx; ++l) {
+                    const double a = Ps[tx + l * LD65];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) acc[q] += a * Bs[l + cq[q]];
+                }
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) acc[q] += Bs[tx + cq[q]];
+            } else if (mode == 1) {
+                for (int l = tx; l < m; ++l) {
+                    const double a = Ps[tx + l * LD65];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) acc[q] += a * Bs[l + cq[q]];
+                }
+            } else {
+                for (int l = 0; l <= tx; ++l) {
+                    const double a = Ps[l + tx * LD65];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) acc[q] += a * Bs[l + cq[q]];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int c = ty + 4 * q;
+                if (c < kc) Bw[vi(bv, tx, c0 + c)] = acc[q];
+            }
+        }
+        __syncthreads();  // Bs reused by the next column chunk
+    }
+}
+
+// TRSM via the packed leaf inverse, register-tiled: out = op(T^-1) P B (in place on B)
+template <int NQ>
+__device__ void trsm_inv_tiled(const ExecArgs &A, const DTask &T, int k) {
+    const DView &bv = T.v[1];
+    const DView &iv = T.v[2];
+    const int m = iv.rows;
+    const int mode = T.flags & 15;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    Strided Pm = strided(A, iv);
+    if (mode == 2) {  // U^-T: M(i, l) = P(l, i)
+        Pm.si = iv.ld;
+        Pm.sj = 1;
+    }
+    const Strided B = strided(A, bv);
+    const int32_t *perm = mode == 0 ? A.perm + T.aux : nullptr;
+    double *Bw = vp(A, bv);
+    for (int c0 = 0; c0 < k; c0 += 4 * NQ) {
+        const int kc = min(4 * NQ, k - c0);
+        double acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+        if (tx < m) {
+            if (mode == 0) {
+                tile_fma<NQ>(acc, Pm, tx, 0, tx, B, perm, c0, ty, kc);   // strict lower of L^-1
+                const i64 rp = perm[tx];                                    // unit diagonal
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    acc[q] += B.p[rp * B.si + min(c0 + ty + 4 * q, c0 + kc - 1) * B.sj];
+            } else if (mode == 1) {
+                tile_fma<NQ>(acc, Pm, tx, tx, m, B, nullptr, c0, ty, kc);
+            } else {
+                tile_fma<NQ>(acc, Pm, tx, 0, tx + 1, B, nullptr, c0, ty, kc);
+            }
+        }
+        __syncthreads();  // every read of this column chunk of B precedes the in-place write
+        if (tx < m) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int c = ty + 4 * q;
+                if (c < kc) Bw[vi(bv, tx, c0 + c)] = acc[q];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__device__ void task_trsm_fast(const ExecArgs &A, const DTask &T, double *sm) {
+    const int k = vcols(A, T.v[1]);
+    if (k <= 0) return;
+    if (k <= 8) trsm_inv_staged<2>(A, T, k, sm);
+    else if (k <= 16) trsm_inv_staged<4>(A, T, k, sm);
+    else if (k <= 32) trsm_inv_staged<8>(A, T, k, sm);
+    else trsm_inv_staged<16>(A, T, k, sm);
 }
 
 // TRSM through the packed leaf inverse: B <- op(T^-1) P B as a small GEMM
@@ -331,7 +519,7 @@ __device__ void task_getrf(const ExecArgs &A, const DTask &T, int tid, double *s
 // ---------------------------------------------------------------------------
 __device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
     if (T.flags & 64) {
-        task_trsm_inv(A, T, sm);
+        task_trsm_fast(A, T, sm);
         return;
     }
     const DView &tv = T.v[0];
@@ -446,12 +634,128 @@ __device__ void task_segmul_fast(const ExecArgs &A, const DTask &T, double *sm) 
     }
 }
 
+// SEGMUL for segments of <= 64 rows whose pieces have inner dimension <= 64: each piece's
+// matrix rows and X rows are staged with cp.async, double-buffered so the copies of piece
+// p+1 overlap the products of piece p.
+template <int NQ>
+__device__ void segmul_staged(const ExecArgs &A, const DTask &T, int k, double *sm) {
+    const DView &yv = T.v[0];
+    const int s = yv.rows;
+    const bool overwrite = T.flags & 1;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    double *Yw = vp(A, yv);
+    constexpr int BUF = 2 * 64 * LD65;  // M tile + X tile
+    for (int c0 = 0; c0 < k; c0 += 4 * NQ) {
+        const int kc = min(4 * NQ, k - c0);
+        double acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+        int cq[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) cq[q] = min(ty + 4 * q, kc - 1) * LD65;
+        auto stage = [&](int p, int buf) {
+            const DPiece pc = A.pieces[p];
+            const int inner = pc.kind == 0 ? pc.mat.cols : vcols(A, pc.mat);
+            double *Ms = sm + buf * BUF;
+            stage_view(Ms, LD65, strided(A, pc.mat), s, inner, 0, nullptr);
+            stage_view(Ms + 64 * LD65, LD65, strided(A, pc.x), inner, kc, c0, nullptr);
+            cp_commit();
+        };
+        if (T.pc_beg < T.pc_end) stage(T.pc_beg, 0);
+        for (int p = T.pc_beg; p < T.pc_end; ++p) {
+            const int buf = (p - T.pc_beg) & 1;
+            if (p + 1 < T.pc_end) {
+                stage(p + 1, buf ^ 1);
+                cp_wait<1>();
+            } else {
+                cp_wait<0>();
+            }
+            __syncthreads();
+            const DPiece &pc = A.pieces[p];
+            const int inner = pc.kind == 0 ? pc.mat.cols : vcols(A, pc.mat);
+            const double *Ms = sm + buf * BUF;
+            const double *Xs = Ms + 64 * LD65;
+            if (tx < s) {
+                for (int j = 0; j < inner; ++j) {
+                    const double a = Ms[tx + j * LD65];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) acc[q] += a * Xs[j + cq[q]];
+                }
+            }
+            __syncthreads();  // this buffer is refilled by the stage after next
+        }
+        if (tx < s) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int c = ty + 4 * q;
+                if (c < kc) {
+                    double &y = Yw[vi(yv, tx, c0 + c)];
+                    y = (overwrite ? 0.0 : y) + T.alpha * acc[q];
+                }
+            }
+        }
+    }
+}
+
+// register-tiled SEGMUL for segments of <= 64 rows: every piece (dense, transposed dense or
+// low-rank U[seg] W) streamed through L1 with no staging and no barriers
+template <int NQ>
+__device__ void segmul_tiled(const ExecArgs &A, const DTask &T, int k) {
+    const DView &yv = T.v[0];
+    const int s = yv.rows;
+    const bool overwrite = T.flags & 1;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    double *Yw = vp(A, yv);
+    for (int c0 = 0; c0 < k; c0 += 4 * NQ) {
+        const int kc = min(4 * NQ, k - c0);
+        double acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+        if (tx < s) {
+            for (int p = T.pc_beg; p < T.pc_end; ++p) {
+                const DPiece &pc = A.pieces[p];
+                const int inner = pc.kind == 0 ? pc.mat.cols : vcols(A, pc.mat);
+                tile_fma<NQ>(acc, strided(A, pc.mat), tx, 0, inner, strided(A, pc.x), nullptr, c0,
+                             ty, kc);
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int c = ty + 4 * q;
+                if (c < kc) {
+                    double &y = Yw[vi(yv, tx, c0 + c)];
+                    y = (overwrite ? 0.0 : y) + T.alpha * acc[q];
+                }
+            }
+        }
+    }
+}
+
 __device__ void task_segmul(const ExecArgs &A, const DTask &T, double *sm) {
     const DView &yv = T.v[0];
     const int s = yv.rows;
     const int k = vcols(A, yv);
     double *Yg = vp(A, yv);
     const bool overwrite = T.flags & 1;
+    if (s <= 64) {
+        if (k <= 0) return;
+        bool small_inner = true;
+        for (int p = T.pc_beg; p < T.pc_end && small_inner; ++p) {
+            const DPiece &pc = A.pieces[p];
+            small_inner = pc.kind == 1 || pc.mat.cols <= 64;
+        }
+        if (small_inner) {
+            if (k <= 8) segmul_staged<2>(A, T, k, sm);
+            else if (k <= 16) segmul_staged<4>(A, T, k, sm);
+            else if (k <= 32) segmul_staged<8>(A, T, k, sm);
+            else segmul_staged<16>(A, T, k, sm);
+        } else {
+            if (k <= 8) segmul_tiled<2>(A, T, k);
+            else if (k <= 16) segmul_tiled<4>(A, T, k);
+            else if (k <= 32) segmul_tiled<8>(A, T, k);
+            else segmul_tiled<16>(A, T, k);
+        }
+        return;
+    }
     {
         bool fast = s <= 64 && !yv.trans;
         for (int p = T.pc_beg; p < T.pc_end && fast; ++p) {
@@ -695,28 +999,33 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
     __shared__ int s_t;
     __shared__ DTask s_task;
     while (true) {
-        if (threadIdx.x == 0) s_t = atomicAdd(A.counter, 1);
-        __syncthreads();
-        const int t = s_t;
-        if (t >= A.ntasks) return;
-        if (threadIdx.x == 0) s_task = A.tasks[t];
-        __syncthreads();
-        const DTask &T = s_task;
-        if (threadIdx.x < 32) {
-            for (int q = threadIdx.x; q < T.dep_cnt; q += 32) {
-                const int p = A.deps[T.dep_beg + q];
+        // take the next slot of the ready FIFO; a slot is filled once its task's last
+        // predecessor has finished (exactly ntasks tasks are ever pushed)
+        if (threadIdx.x == 0) {
+            const int slot = atomicAdd(A.counter, 1);
+            int t = -1;
+            if (slot < A.ntasks) {
                 long long spins = 0;
-                while (ld_acquire(A.done + p) == 0) {
-                    __nanosleep(100);
-                    if (++spins > (1ll << 27)) {  // watchdog (~>10 s): never hang the GPU
-                        set_err(A, LH_EINTERNAL, t, -2);
+                unsigned ns = 32;
+                while ((t = *(volatile const int32_t *)(A.queue + slot)) < 0) {
+                    __nanosleep(ns);
+                    ns = ns < POLL_NS_MAX ? ns * 2 : POLL_NS_MAX;
+                    if (++spins > (1ll << 26)) {  // watchdog (tens of seconds): never hang
+                        set_err(A, LH_EINTERNAL, slot, -2);
+                        t = -2;
                         break;
                     }
                 }
+                // acquire: pairs with the pusher's release and invalidates this SM's L1
+                if (t >= 0) t = ld_acquire(A.queue + slot);
             }
+            s_t = t;
+            if (t >= 0) s_task = A.tasks[t];
         }
         __syncthreads();
-        __threadfence();  // acquire side: drop stale L1 lines before reading operands
+        const int t = s_t;
+        if (t < 0) return;
+        const DTask &T = s_task;
         if (A.times && threadIdx.x == 0) A.times[2 * t] = gtimer();
         switch (T.type) {
             case T_GETRF: task_getrf(A, T, t, sm); break;
@@ -733,10 +1042,21 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
             default: break;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            if (A.times) A.times[2 * t + 1] = gtimer();
-            st_release(A.done + t, 1);
+        if (threadIdx.x < 32) {
+            // release side: the barrier made the CTA's writes visible to warp 0; its
+            // gpu-scope acq_rel fences publish them before the counter decrements
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            if (A.times && threadIdx.x == 0) A.times[2 * t + 1] = gtimer();
+            const int sb = A.succ_beg[t], se = A.succ_beg[t + 1];
+            for (int q = sb + threadIdx.x; q < se; q += 32) {
+                const int s = A.succ[q];
+                if (atomicSub(A.remaining + s, 1) == 1) {
+                    // last predecessor: acquire the other predecessors' releases, then push
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    const int pos = atomicAdd(A.tail, 1);
+                    st_release(A.queue + pos, s);
+                }
+            }
         }
     }
 }
@@ -752,13 +1072,39 @@ Plan::~Plan() {
     cudaFree(d_temp);
     cudaFree(d_ranks);
     cudaFree(d_err);
+    cudaFree(d_succ_beg);
+    cudaFree(d_succ);
+    cudaFree(d_rem_init);
+    cudaFree(d_rem);
+    cudaFree(d_queue_init);
+    cudaFree(d_queue);
 }
 
 void Plan::upload(cudaStream_t s) {
+    const int32_t n = (int32_t)tasks.size();
+    // successor CSR, initial dependency counts, initial ready FIFO (tasks without deps)
+    std::vector<int32_t> sb(n + 1, 0), sc(deps.size()), rem(n), q0(std::max(n, 1), -1);
+    for (int32_t t = 0; t < n; ++t)
+        for (int32_t k = 0; k < tasks[t].dep_cnt; ++k) ++sb[deps[tasks[t].dep_beg + k] + 1];
+    for (int32_t t = 0; t < n; ++t) sb[t + 1] += sb[t];
+    std::vector<int32_t> fill(sb.begin(), sb.end() - 1);
+    int32_t n0 = 0;
+    for (int32_t t = 0; t < n; ++t) {
+        rem[t] = tasks[t].dep_cnt;
+        for (int32_t k = 0; k < tasks[t].dep_cnt; ++k) sc[fill[deps[tasks[t].dep_beg + k]]++] = t;
+        if (rem[t] == 0) q0[n0++] = t;
+    }
+    n_ready0 = n0;
+    d_succ_beg = dupload(sb, s);
+    d_succ = dupload(sc, s);
+    d_rem_init = dupload(rem, s);
+    d_queue_init = dupload(q0, s);
+    d_rem = dalloc<int32_t>(std::max(n, 1));
+    d_queue = dalloc<int32_t>(std::max(n, 1));
     d_tasks = dupload(tasks, s);
     d_deps = dupload(deps, s);
     d_pieces = dupload(pieces, s);
-    d_done = dalloc<int32_t>((i64)tasks.size() + 1);
+    d_done = dalloc<int32_t>((i64)tasks.size() + 2);
     d_temp = dalloc<double>(std::max<i64>(temp_len, 1));
     d_ranks = dalloc<int32_t>(std::max(nslots_total + 1, 1));
     d_err = dalloc<int32_t>(4);
@@ -777,6 +1123,8 @@ static int exec_grid(Ctx &ctx) {
     LH_REQUIRE(per_sm >= 1, LH_EINTERNAL, "executor kernel cannot be resident");
     return ctx.num_sms * per_sm;
 }
+
+static double g_last_mean_task_us = 0.0;
 
 // Task-level profile (LEVYH_TASK_PROFILE=<file>): per-type busy time and the measured
 // critical path (latest-finishing predecessor chain) with its per-type composition.
@@ -834,8 +1182,17 @@ static void report_profile(const Plan &P, const std::vector<unsigned long long> 
 static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val,
                      const char *label = "plan") {
     cudaStream_t s = ctx.stream;
-    LH_CUDA(cudaMemsetAsync(P.d_done, 0, sizeof(int32_t) * (P.tasks.size() + 1), s));
+    LH_CUDA(cudaMemsetAsync(P.d_done, 0, sizeof(int32_t) * (P.tasks.size() + 2), s));
     LH_CUDA(cudaMemsetAsync(P.d_err, 0, sizeof(int32_t) * 4, s));
+    if (!P.tasks.empty()) {
+        LH_CUDA(cudaMemcpyAsync(P.d_rem, P.d_rem_init, sizeof(int32_t) * P.tasks.size(),
+                                cudaMemcpyDeviceToDevice, s));
+        LH_CUDA(cudaMemcpyAsync(P.d_queue, P.d_queue_init, sizeof(int32_t) * P.tasks.size(),
+                                cudaMemcpyDeviceToDevice, s));
+        const int32_t n0 = P.n_ready0;
+        LH_CUDA(cudaMemcpyAsync(P.d_done + P.tasks.size() + 1, &n0, sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+    }
     if (F.nslots)
         LH_CUDA(cudaMemcpyAsync(P.d_ranks, F.d_ranks, sizeof(int32_t) * F.nslots,
                                 cudaMemcpyDeviceToDevice, s));
@@ -852,6 +1209,11 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     A.pieces = P.d_pieces;
     A.done = P.d_done;
     A.counter = P.d_done + P.tasks.size();
+    A.tail = P.d_done + P.tasks.size() + 1;
+    A.queue = P.d_queue;
+    A.remaining = P.d_rem;
+    A.succ_beg = P.d_succ_beg;
+    A.succ = P.d_succ;
     A.err = P.d_err;
     A.base[B_F] = F.d_arena;
     A.base[B_TMP] = P.d_temp;
@@ -861,7 +1223,8 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     A.ranks = P.d_ranks;
     A.perm = F.d_perm;
     A.times = nullptr;
-    const bool prof = getenv("LEVYH_TASK_PROFILE") != nullptr && A.ntasks > 0;
+    const bool prof = (getenv("LEVYH_TASK_PROFILE") != nullptr ||
+                       getenv("LEVYH_TASK_PROFILE_STATS") != nullptr) && A.ntasks > 0;
     if (prof) A.times = dalloc<unsigned long long>(2 * (i64)A.ntasks);
     if (A.ntasks > 0) {
         int grid = exec_grid(ctx);
@@ -876,6 +1239,9 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
         LH_CUDA(cudaMemcpy(tm.data(), A.times, sizeof(unsigned long long) * tm.size(),
                            cudaMemcpyDeviceToHost));
         cudaFree(A.times);
+        double s = 0.0;
+        for (int i = 0; i < A.ntasks; ++i) s += (tm[2 * i + 1] - tm[2 * i]) * 1e-3;
+        g_last_mean_task_us = s / A.ntasks;
         report_profile(P, tm, label);
     }
     if (F.nslots)
@@ -1035,6 +1401,91 @@ void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method) {
     if (nrhs <= 0) return;
     if (method == 0) solve_substitution(ctx, F, b, ldb, nrhs);
     else solve_inverse(ctx, F, b, ldb, nrhs);
+}
+
+// ---------------------------------------------------------------------------
+// micro-benchmark: chains of R identical tasks through the real executor
+// kind 0: GETRF 64x64 (independent blocks, chained); 1: TRSM (inverse GEMM) with k
+// columns; 2: SEGMUL with one dense 64x64 piece and k columns.  out[0] = executor
+// wall time per task (us, includes hand-off), out[1] = mean task body (us).
+// ---------------------------------------------------------------------------
+__global__ void fill_random_kernel(double *p, i64 n, double diag_boost, int m) {
+    for (i64 e = (i64)blockIdx.x * NT + threadIdx.x; e < n; e += (i64)gridDim.x * NT) {
+        uint64_t z = e * 0x9E3779B97F4A7C15ull + 12345;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z ^= z >> 31;
+        double v = ((z >> 11) * (1.0 / 9007199254740992.0)) - 0.5;
+        i64 w = e % ((i64)m * m);
+        if (w % m == w / m) v += diag_boost;
+        p[e] = v;
+    }
+}
+
+void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out) {
+    const int m = 64;
+    HMat F;  // synthetic storage owner
+    F.arena_len = (i64)R * m * m + (i64)R * m * 64;
+    F.d_arena = dalloc<double>(F.arena_len);
+    F.d_perm = dalloc<int32_t>((i64)R * m);
+    F.inv_len = (i64)R * m * m;
+    F.d_inv = dalloc<double>(F.inv_len);
+    fill_random_kernel<<<1024, NT, 0, ctx.stream>>>(F.d_arena, F.arena_len, 8.0, m);
+    fill_random_kernel<<<1024, NT, 0, ctx.stream>>>(F.d_inv, F.inv_len, 1.0, m);
+    LH_CUDA(cudaMemsetAsync(F.d_perm, 0, sizeof(int32_t) * R * m, ctx.stream));
+    std::vector<int32_t> permh((size_t)R * m);
+    for (int r = 0; r < R; ++r)
+        for (int i = 0; i < m; ++i) permh[(size_t)r * m + i] = i;
+    upload(F.d_perm, permh, ctx.stream);
+    Plan P;
+    for (int r = 0; r < R; ++r) {
+        DTask t;
+        std::memset(&t, 0, sizeof(t));
+        for (auto &v : t.v) v.wslot = -1;
+        t.path = -1;
+        const i64 dense_off = (i64)r * m * m, rhs_off = (i64)R * m * m + (i64)r * m * 64;
+        DView D{dense_off, m, m, m, -1, B_F, 0, 0};
+        DView Bv{rhs_off, m, k, m, -1, B_F, 0, 0};
+        DView Iv{(i64)r * m * m, m, m, m, -1, B_INV, 0, 0};
+        if (kind == 0) {
+            t.type = T_GETRF;
+            t.aux = r * m;
+            t.v[0] = D;
+            t.v[1] = Iv;
+            t.flags = 1;
+        } else if (kind == 1) {
+            t.type = T_TRSM;
+            t.flags = 0 | 32 | 64;
+            t.aux = r * m;
+            t.v[0] = D;
+            t.v[1] = Bv;
+            t.v[2] = Iv;
+        } else {
+            t.type = T_SEGMUL;
+            t.alpha = -1.0;
+            t.v[0] = Bv;
+            t.pc_beg = (int32_t)P.pieces.size();
+            DPiece pc;
+            std::memset(&pc, 0, sizeof(pc));
+            pc.kind = 0;
+            pc.mat = D;
+            pc.x = DView{(i64)R * m * m + (i64)((r + 1) % R) * m * 64, m, k, m, -1, B_F, 0, 0};
+            P.pieces.push_back(pc);
+            t.pc_end = (int32_t)P.pieces.size();
+        }
+        t.dep_beg = (int32_t)P.deps.size();
+        t.dep_cnt = (chain && r > 0) ? 1 : 0;
+        if (t.dep_cnt) P.deps.push_back(r - 1);
+        P.tasks.push_back(t);
+    }
+    P.nslots_total = 0;
+    P.upload(ctx.stream);
+    setenv("LEVYH_TASK_PROFILE_STATS", "1", 1);
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    auto t0 = std::chrono::steady_clock::now();
+    run_plan(ctx, P, F, nullptr, nullptr, -1, "bench");
+    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    out[0] = 1e6 * wall / R;
+    out[1] = g_last_mean_task_us;
 }
 
 // algorithmic bytes of the two matvec phases over `blocks` (fp64): phase 1 reads V,

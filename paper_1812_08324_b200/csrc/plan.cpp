@@ -51,7 +51,14 @@ PView PView::T() const {
 // dependency tracking: per object, disjoint row intervals with last writer + readers
 // ---------------------------------------------------------------------------
 void DepTracker::access(int32_t task, u64 obj, i64 a, i64 b, bool write, std::vector<int32_t> &out) {
-    auto &m = objs[obj];
+    std::map<i64, Seg> *mp;
+    if (obj < dense_limit) {
+        if (obj >= dense.size()) dense.resize(std::max<size_t>(obj + 1, dense.size() * 2));
+        mp = &dense[obj];
+    } else {
+        mp = &objs[obj];
+    }
+    auto &m = *mp;
     if (m.empty()) m[0] = Seg{INT64_MAX, -1, {}};
     // split at a and b
     auto split = [&](i64 x) {
@@ -87,10 +94,18 @@ Planner::Planner(HMat &F, HMat *X) : F(F), X(X) {
     P->slot_off_x = F.nslots;
     P->slot_off_tmp = F.nslots + (X ? X->nslots : 0);
     next_slot = P->slot_off_tmp;
+    nF = (i64)F.nodes.size();
+    nX = X ? (i64)X->nodes.size() : 0;
+    deps.dense_limit = (u64)(3 * (nF + nX));
+    deps.dense.reserve(deps.dense_limit);
 }
 
+// object ids: block storage of F and X get dense ids (vector-indexed dependency maps);
+// temporaries and the right-hand side live in a hash map
 u64 Planner::key(int base, i64 id, int which) const {
-    return ((u64)base << 56) | ((u64)id << 2) | (u64)which;
+    if (base == B_F) return (u64)(3 * id + which);
+    if (base == B_X) return (u64)(3 * nF + 3 * id + which);
+    return (1ull << 62) | ((u64)base << 56) | ((u64)id << 2) | (u64)which;
 }
 
 PView Planner::dense_view(const Mref &M, int32_t b) const {
@@ -287,10 +302,21 @@ void Planner::segmul(const PView &Y, const Mref &M, int32_t a, const PView &X, b
         W[q] = w;
         hasW[q] = true;
     }
-    // phase 2: one task per output row segment
+    // phase 2: one task per output row segment; leaves bucketed by the segments they cover
     std::vector<std::pair<i64, i64>> segs;
     segments_of(trans ? *M.H->ct : *M.H->rt, trans ? A.ccl : A.rcl, segs);
-    for (auto &sg : segs) {
+    std::vector<i64> starts(segs.size());
+    for (size_t k = 0; k < segs.size(); ++k) starts[k] = segs[k].first;
+    std::vector<std::vector<int32_t>> bucket(segs.size());
+    for (size_t q = 0; q < lv.size(); ++q) {
+        const Node &nd = M.H->nodes[lv[q].b];
+        if (nd.kind == K_ZERO) continue;
+        const i64 o0 = trans ? lv[q].c : lv[q].r, on = trans ? nd.n : nd.m;
+        size_t k = std::upper_bound(starts.begin(), starts.end(), o0) - starts.begin() - 1;
+        for (; k < segs.size() && segs[k].first < o0 + on; ++k) bucket[k].push_back((int32_t)q);
+    }
+    for (size_t sk = 0; sk < segs.size(); ++sk) {
+        const auto &sg = segs[sk];
         i64 s0 = sg.first, s1 = sg.first + sg.second;
         PView Ys = Y.rows_(s0, s1 - s0);
         DTask t = mk(T_SEGMUL);
@@ -299,13 +325,12 @@ void Planner::segmul(const PView &Y, const Mref &M, int32_t a, const PView &X, b
         t.v[0] = Ys.d;
         t.pc_beg = (int32_t)P->pieces.size();
         std::vector<std::pair<PView, bool>> more;
-        for (size_t q = 0; q < lv.size(); ++q) {
+        more.reserve(2 * bucket[sk].size() + 1);
+        for (int32_t q : bucket[sk]) {
             const Node &nd = M.H->nodes[lv[q].b];
-            if (nd.kind == K_ZERO) continue;
             i64 o0 = trans ? lv[q].c : lv[q].r;   // output-row range of this leaf
             i64 on = trans ? nd.n : nd.m;
             i64 a0 = std::max(o0, s0), a1 = std::min(o0 + on, s1);
-            if (a0 >= a1) continue;
             LH_REQUIRE(a0 == s0 && a1 == s1, LH_EINTERNAL, "leaf block not aligned with segments");
             DPiece pc;
             std::memset(&pc, 0, sizeof(pc));
@@ -722,17 +747,19 @@ void Planner::finalize() {
             default: return 1.0;
         }
     };
+    std::vector<double> cst(n);
+    for (int32_t i = 0; i < n; ++i) cst[i] = cost(T[i]);
     for (int32_t i = 0; i < n; ++i) {
         double l = 0.0;
-        for (int32_t k = 0; k < T[i].dep_cnt; ++k) {
-            int32_t p = P->deps[T[i].dep_beg + k];
-            l = std::max(l, lvl[p] + cost(T[p]));
-        }
+        const int32_t *dp = P->deps.data() + T[i].dep_beg;
+        for (int32_t k = 0; k < T[i].dep_cnt; ++k) l = std::max(l, lvl[dp[k]] + cst[dp[k]]);
         lvl[i] = l;
     }
+    std::vector<std::pair<double, int32_t>> key(n);
+    for (int32_t i = 0; i < n; ++i) key[i] = {lvl[i], i};
+    std::sort(key.begin(), key.end());  // (level, program order): topological
     std::vector<int32_t> ord(n);
-    for (int32_t i = 0; i < n; ++i) ord[i] = i;
-    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return lvl[a] < lvl[b]; });
+    for (int32_t i = 0; i < n; ++i) ord[i] = key[i].second;
     std::vector<int32_t> pos(n);
     for (int32_t i = 0; i < n; ++i) pos[ord[i]] = i;
     std::vector<DTask> nt(n);

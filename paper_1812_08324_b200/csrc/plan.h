@@ -71,6 +71,10 @@ struct Plan {
     int32_t *d_deps = nullptr;
     DPiece *d_pieces = nullptr;
     int32_t *d_done = nullptr;  // one flag per task + counters
+    int32_t *d_succ_beg = nullptr, *d_succ = nullptr;  // successor CSR
+    int32_t *d_rem_init = nullptr, *d_rem = nullptr;   // dependency counters
+    int32_t *d_queue_init = nullptr, *d_queue = nullptr;  // ready FIFO
+    int32_t n_ready0 = 0;
     double *d_temp = nullptr;
     int32_t *d_ranks = nullptr;
     int32_t *d_err = nullptr;

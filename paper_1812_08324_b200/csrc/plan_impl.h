@@ -36,6 +36,8 @@ struct DepTracker {
         std::vector<int32_t> readers;
     };
     std::unordered_map<u64, std::map<i64, Seg>> objs;
+    std::vector<std::map<i64, Seg>> dense;
+    u64 dense_limit = 0;
     void access(int32_t task, u64 obj, i64 a, i64 b, bool write, std::vector<int32_t> &out);
 };
 
@@ -56,6 +58,7 @@ struct Planner {
     std::shared_ptr<Plan> P;
     DepTracker deps;
     double eps2 = 1e-10;
+    i64 nF = 0, nX = 0;
     i64 perm_len = 0;
     i64 inv_len = 0;
     int32_t next_slot = 0;
