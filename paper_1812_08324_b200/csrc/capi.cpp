@@ -27,6 +27,7 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2);
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method);
 void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out);
 void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
+void start_background_plans(HMat &H);
 
 void *Ctx::ensure_scratch(size_t bytes) {
     if (bytes > scratch_bytes) {
@@ -239,6 +240,7 @@ int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, co
         o = new_hmat(rt, ct);
         partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
         build_toeplitz(ctx->c, o->h, t_dev, *cfg);
+        start_background_plans(o->h);
     });
     if (rc != LH_OK) {
         delete o;
@@ -256,6 +258,7 @@ int lh_hmat_build_dense(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const
         o = new_hmat(rt, ct);
         partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
         build_dense(ctx->c, o->h, A_dev, lda, row_major, *cfg);
+        start_background_plans(o->h);
     });
     if (rc != LH_OK) {
         delete o;

@@ -104,6 +104,7 @@ struct HMat {
     std::shared_ptr<void> mv_plan;
     std::shared_ptr<void> solve_plan;
     std::shared_ptr<void> inv_plan;
+    std::shared_ptr<void> bg_plan;  // background H-LU + inverse planning (lu.cu: PlanJob)
     ~HMat();
     void sync_ranks(cudaStream_t s);
 };

@@ -68,16 +68,37 @@ __device__ __forceinline__ void col_dots(const double *Q, i64 ldq, i64 m, int k,
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int l = w; l < k; l += NW) {
         const double *q = Q + (i64)l * ldq;
-        double s0 = 0.0, s1 = 0.0;
+        // 8 independent loads per lane per iteration: in-order issue would otherwise pay
+        // one memory round trip per iteration on long columns
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         i64 i = lane;
-        for (; i + 32 < m; i += 64) {
-            s0 += q[i] * u[i];
-            s1 += q[i + 32] * u[i + 32];
+        for (; i + 96 < m; i += 128) {
+            const double q0 = q[i], q1 = q[i + 32], q2 = q[i + 64], q3 = q[i + 96];
+            const double u0 = u[i], u1 = u[i + 32], u2 = u[i + 64], u3 = u[i + 96];
+            s0 += q0 * u0;
+            s1 += q1 * u1;
+            s2 += q2 * u2;
+            s3 += q3 * u3;
         }
-        if (i < m) s0 += q[i] * u[i];
-        s0 = warp_sum(s0 + s1);
+        for (; i < m; i += 32) s0 += q[i] * u[i];
+        s0 = warp_sum((s0 + s1) + (s2 + s3));
         if (lane == 0) h[l] = s0;
     }
+}
+
+// per-thread partial sum of squares over a strided column (4 independent loads in flight)
+__device__ __forceinline__ double sumsq(const double *u, i64 m) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    i64 i = threadIdx.x;
+    for (; i + 3 * NT < m; i += 4 * NT) {
+        const double a = u[i], b = u[i + NT], c = u[i + 2 * NT], d = u[i + 3 * NT];
+        s0 += a * a;
+        s1 += b * b;
+        s2 += c * c;
+        s3 += d * d;
+    }
+    for (; i < m; i += NT) s0 += u[i] * u[i];
+    return (s0 + s1) + (s2 + s3);
 }
 
 // Classical Gram-Schmidt with one reorthogonalisation (CGS2), in place:
@@ -87,14 +108,50 @@ __device__ __noinline__ static void cgs2(double *Q, i64 ldq, i64 m, int K, doubl
     for (int k = 0; k < K; ++k) {
         double *u = Q + (i64)k * ldq;
         for (int l = threadIdx.x; l < KA_MAX; l += NT) R[l + k * KA_MAX] = 0.0;
-        double s0 = 0.0;
-        for (i64 i = threadIdx.x; i < m; i += NT) s0 += u[i] * u[i];
-        const double n0 = sqrt(block_sum(s0, red));
+        const double n0 = sqrt(block_sum(sumsq(u, m), red));
         for (int pass = 0; pass < 2; ++pass) {
             __syncthreads();
             col_dots(Q, ldq, m, k, u, h);
             __syncthreads();
-            for (i64 i = threadIdx.x; i < m; i += NT) {
+            // four rows per iteration: 4k independent loads before the first use
+            i64 i = threadIdx.x;
+            for (; i + 3 * NT < m; i += 4 * NT) {
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int l = 0;
+                for (; l + 4 <= k; l += 4) {  // 16 independent loads per batch
+                    double a[4][4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double *ql = Q + (i64)(l + j) * ldq + i;
+                        a[j][0] = ql[0];
+                        a[j][1] = ql[NT];
+                        a[j][2] = ql[2 * NT];
+                        a[j][3] = ql[3 * NT];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double hl = h[l + j];
+                        s0 += a[j][0] * hl;
+                        s1 += a[j][1] * hl;
+                        s2 += a[j][2] * hl;
+                        s3 += a[j][3] * hl;
+                    }
+                }
+                for (; l < k; ++l) {
+                    const double *ql = Q + (i64)l * ldq + i;
+                    const double hl = h[l];
+                    s0 += ql[0] * hl;
+                    s1 += ql[NT] * hl;
+                    s2 += ql[2 * NT] * hl;
+                    s3 += ql[3 * NT] * hl;
+                }
+                const double a0 = u[i], a1 = u[i + NT], a2 = u[i + 2 * NT], a3 = u[i + 3 * NT];
+                u[i] = a0 - s0;
+                u[i + NT] = a1 - s1;
+                u[i + 2 * NT] = a2 - s2;
+                u[i + 3 * NT] = a3 - s3;
+            }
+            for (; i < m; i += NT) {
                 double s = 0.0;
                 for (int l = 0; l < k; ++l) s += Q[i + (i64)l * ldq] * h[l];
                 u[i] -= s;
@@ -102,15 +159,23 @@ __device__ __noinline__ static void cgs2(double *Q, i64 ldq, i64 m, int K, doubl
             for (int l = threadIdx.x; l < k; l += NT) R[l + k * KA_MAX] += h[l];
         }
         __syncthreads();
-        double s = 0.0;
-        for (i64 i = threadIdx.x; i < m; i += NT) s += u[i] * u[i];
-        double nrm = sqrt(block_sum(s, red));
+        double nrm = sqrt(block_sum(sumsq(u, m), red));
         // a residual at rounding level after reorthogonalisation means the column is
         // numerically inside span(q_0..q_{k-1}): drop it (q_k = 0, R_kk = 0) so Q keeps
         // orthonormal columns (normalising noise would not be orthogonal to the span)
         if (!(nrm > 1e-13 * n0)) nrm = 0.0;
         double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-        for (i64 i = threadIdx.x; i < m; i += NT) u[i] *= inv;
+        {
+            i64 i = threadIdx.x;
+            for (; i + 3 * NT < m; i += 4 * NT) {
+                const double a = u[i], b = u[i + NT], c = u[i + 2 * NT], d = u[i + 3 * NT];
+                u[i] = a * inv;
+                u[i + NT] = b * inv;
+                u[i + 2 * NT] = c * inv;
+                u[i + 3 * NT] = d * inv;
+            }
+            for (; i < m; i += NT) u[i] *= inv;
+        }
         if (threadIdx.x == 0) R[k + k * KA_MAX] = nrm;
         __syncthreads();
     }
@@ -230,11 +295,18 @@ __device__ static void apply_coeffs(const double *Q, i64 ldq, i64 m, int K, cons
         double acc[KC_MAX];
 #pragma unroll
         for (int c = 0; c < KC_MAX; ++c) acc[c] = 0.0;
-        for (int l = 0; l < K; ++l) {
-            double q = Q[i + (i64)l * ldq];
+        for (int l0 = 0; l0 < K; l0 += 8) {
+            // 8 independent loads of the row before they are consumed
+            double q[8];
 #pragma unroll
-            for (int c = 0; c < KC_MAX; ++c)
-                if (c < r) acc[c] += q * Cm[l + c * ldc];
+            for (int j = 0; j < 8; ++j) q[j] = l0 + j < K ? Q[i + (i64)(l0 + j) * ldq] : 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (l0 + j >= K) break;
+#pragma unroll
+                for (int c = 0; c < KC_MAX; ++c)
+                    if (c < r) acc[c] += q[j] * Cm[l0 + j + c * ldc];
+            }
         }
 #pragma unroll
         for (int c = 0; c < KC_MAX; ++c)

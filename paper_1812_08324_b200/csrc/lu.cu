@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <future>
 
 #include "core.h"
 #include "dev.cuh"
@@ -29,11 +30,13 @@ struct ExecArgs {
     const int32_t *deps;
     const DPiece *pieces;
     int32_t *done;
-    int32_t *counter;    // next FIFO slot to take
-    int32_t *tail;       // next FIFO slot to fill
-    int32_t *queue;      // ready FIFO (task ids, -1 = not yet filled)
+    int32_t *heads;      // per bucket: next FIFO slot to take
+    int32_t *tails;      // per bucket: next FIFO slot to fill
+    int32_t *done_count; // finished tasks
+    const int32_t *qoff; // per bucket: offset of its FIFO in `queue`
+    int32_t *queue;      // ready FIFOs (task ids, -1 = not yet filled)
     int32_t *remaining;  // unfinished predecessors per task
-    const int32_t *succ_beg, *succ;  // successor CSR
+    const int32_t *succ_beg, *succ;  // successor CSR, entries = task | bucket << SUCC_SHIFT
     int32_t *err;  // [0] code, [1] task, [2] path
     double *base[NBASE];
     int32_t *ranks;
@@ -49,6 +52,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 constexpr int SMEM_BYTES = 168 * 1024;
 constexpr unsigned POLL_NS_MAX = 128;
+constexpr int SUCC_SHIFT = 28;
+constexpr int SUCC_MASK = (1 << SUCC_SHIFT) - 1;
 
 __device__ __forceinline__ double *vp(const ExecArgs &A, const DView &v) { return A.base[v.base] + v.off; }
 __device__ __forceinline__ i64 vi(const DView &v, i64 i, i64 j) {
@@ -89,7 +94,12 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
     int *piv = (int *)(sm + 3 * 64 * LD65);
     __shared__ int s_p;
     const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-    for (int e = threadIdx.x; e < m * m; e += NT) S[(e % m) + (e / m) * LD65] = G[e % m + (e / m) * (i64)v.ld];
+    for (int e = threadIdx.x; e < m * m; e += NT) {
+        const unsigned s = (unsigned)__cvta_generic_to_shared(S + (e % m) + (e / m) * LD65);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s),
+                     "l"(G + e % m + (e / m) * (i64)v.ld) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = 0; j < m; ++j) {
@@ -131,7 +141,8 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
         const double d = S[j + j * LD65];
         double l = 0.0;
         if (tx > j && tx < m) {
-            l = d != 0.0 ? S[tx + j * LD65] / d : S[tx + j * LD65];
+            // scale by the reciprocal pivot (as LAPACK dgetf2 does for |pivot| >= sfmin)
+            l = d != 0.0 ? S[tx + j * LD65] * (1.0 / d) : S[tx + j * LD65];
             for (int c = j + 1 + ty; c < m; c += 4) S[tx + c * LD65] -= l * S[j + c * LD65];
         }
         __syncthreads();
@@ -157,7 +168,9 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
             }
     }
     if (!(T.flags & 1)) return;
-    // identity start
+    // identity start; reciprocal pivots
+    __shared__ double rdiag[64];
+    if (threadIdx.x < m) rdiag[threadIdx.x] = 1.0 / S[threadIdx.x + threadIdx.x * LD65];
     for (int e = threadIdx.x; e < m * m; e += NT) {
         int i = e % m, c = e / m;
         Li[i + c * LD65] = (i == c) ? 1.0 : 0.0;
@@ -172,7 +185,7 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
             for (int c = ty; c <= k; c += 4) Li[tx + c * LD65] -= a * Li[k + c * LD65];
         }
         if (tx < l) {
-            const double a = S[tx + l * LD65] / S[l + l * LD65];
+            const double a = S[tx + l * LD65] * rdiag[l];
             for (int c = l + ty; c < m; c += 4) Ui[tx + c * LD65] -= a * Ui[l + c * LD65];
         }
         __syncthreads();
@@ -181,7 +194,7 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
     double *Pg = A.base[T.v[1].base] + T.v[1].off;
     for (int e = threadIdx.x; e < m * m; e += NT) {
         int i = e % m, c = e / m;
-        Pg[e] = (i > c) ? Li[i + c * LD65] : Ui[i + c * LD65] / S[i + i * LD65];
+        Pg[e] = (i > c) ? Li[i + c * LD65] : Ui[i + c * LD65] * rdiag[i];
     }
 }
 
@@ -881,16 +894,57 @@ __device__ void task_lradd(const ExecArgs &A, const DTask &T, int tid, double *s
     double *V = vp(A, cv);
     const double *U2 = vp(A, u2);
     const double *V2 = vp(A, v2);
-    for (i64 e = threadIdx.x; e < m * r2; e += NT) {
-        i64 i = e % m, c = e / m;
-        U[i + (r1 + c) * (i64)cu.ld] = T.alpha * U2[vi(u2, i, c)];
-    }
-    for (i64 e = threadIdx.x; e < n * r2; e += NT) {
-        i64 i = e % n, c = e / n;
-        V[i + (r1 + c) * (i64)cv.ld] = V2[vi(v2, i, c)];
-    }
-    __syncthreads();
     dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(sm);
+    constexpr int RS = (int)((sizeof(dev::RecompSmem) + 15) / 8) & ~1;
+    constexpr i64 ROOM = SMEM_BYTES / 8 - RS;
+    if ((m + n) * K <= ROOM) {
+        // staged: [U1 alpha*U2] and [V1 V2] in shared memory (one cp.async round trip),
+        // recompressed there, written back once
+        double *Us = sm + RS, *Vs = Us + m * K;
+        const Strided U1g{U, 1, cu.ld}, V1g{V, 1, cv.ld};
+        stage_view(Us, (int)m, U1g, (int)m, r1, 0, nullptr);
+        stage_view(Us + m * r1, (int)m, strided(A, u2), (int)m, r2, 0, nullptr);
+        stage_view(Vs, (int)n, V1g, (int)n, r1, 0, nullptr);
+        stage_view(Vs + n * r1, (int)n, strided(A, v2), (int)n, r2, 0, nullptr);
+        cp_commit();
+        cp_wait<0>();
+        __syncthreads();
+        for (i64 e = threadIdx.x; e < m * r2; e += NT) Us[m * r1 + e] *= T.alpha;
+        __syncthreads();
+        const int rmax = min(kcap, KC_MAX);
+        int r = dev::recompress(Us, m, m, Vs, n, n, K, 1, T.alpha2, Us, m, Vs, n, rmax, S);
+        if (r <= rmax) {
+            for (i64 e = threadIdx.x; e < m * r; e += NT) U[e % m + (e / m) * (i64)cu.ld] = Us[e];
+            for (i64 e = threadIdx.x; e < n * r; e += NT) V[e % n + (e / n) * (i64)cv.ld] = Vs[e];
+        }
+        if (threadIdx.x == 0) {
+            if (r > rmax) set_err(A, LH_ERANK, tid, -1);
+            else A.ranks[slot] = r;
+        }
+        return;
+    }
+    // copies with 8 independent loads in flight per thread (a load->store loop would pay one
+    // memory round trip per element)
+    auto copy_cols = [&](double *dst, i64 ldd, const DView &src, i64 rows, double scale) {
+        const Strided S2 = strided(A, src);
+        const i64 tot = rows * r2;
+        for (i64 e0 = threadIdx.x; e0 < tot; e0 += 8 * NT) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const i64 e = e0 + (i64)q * NT;
+                v[q] = e < tot ? S2.p[(e % rows) * S2.si + (e / rows) * S2.sj] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const i64 e = e0 + (i64)q * NT;
+                if (e < tot) dst[e % rows + (r1 + e / rows) * ldd] = scale * v[q];
+            }
+        }
+    };
+    copy_cols(U, cu.ld, u2, m, T.alpha);
+    copy_cols(V, cv.ld, v2, n, 1.0);
+    __syncthreads();
     int r = dev::recompress(U, cu.ld, m, V, cv.ld, n, K, 1, T.alpha2, U, cu.ld, V, cv.ld,
                             min(kcap, KC_MAX), S);
     if (threadIdx.x == 0) {
@@ -976,7 +1030,21 @@ __device__ void task_rand(const ExecArgs &A, const DTask &T) {
 __device__ void task_orth(const ExecArgs &A, const DTask &T, double *sm) {
     const DView &dv = T.v[0];
     dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(sm);
-    dev::cgs2(vp(A, dv), dv.ld, dv.rows, dv.cols, S.Ru, S.h, S.red);
+    constexpr int RS = (int)((sizeof(dev::RecompSmem) + 15) / 8) & ~1;
+    const i64 m = dv.rows;
+    const int k = dv.cols;
+    double *G = vp(A, dv);
+    if (!dv.trans && m * k <= SMEM_BYTES / 8 - RS) {
+        double *Ys = sm + RS;
+        stage_view(Ys, (int)m, strided(A, dv), (int)m, k, 0, nullptr);
+        cp_commit();
+        cp_wait<0>();
+        __syncthreads();
+        dev::cgs2(Ys, m, m, k, S.Ru, S.h, S.red);
+        for (i64 e = threadIdx.x; e < m * k; e += NT) G[e % m + (e / m) * (i64)dv.ld] = Ys[e];
+        return;
+    }
+    dev::cgs2(G, dv.ld, m, k, S.Ru, S.h, S.red);
 }
 
 __device__ void task_ident(const ExecArgs &A, const DTask &T) {
@@ -999,25 +1067,37 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
     __shared__ int s_t;
     __shared__ DTask s_task;
     while (true) {
-        // take the next slot of the ready FIFO; a slot is filled once its task's last
-        // predecessor has finished (exactly ntasks tasks are ever pushed)
+        // pop the most urgent ready task: buckets by b-level class, highest first; a slot
+        // below `tail` is reserved by a pusher and filled momentarily
         if (threadIdx.x == 0) {
-            const int slot = atomicAdd(A.counter, 1);
             int t = -1;
-            if (slot < A.ntasks) {
-                long long spins = 0;
-                unsigned ns = 32;
-                while ((t = *(volatile const int32_t *)(A.queue + slot)) < 0) {
-                    __nanosleep(ns);
-                    ns = ns < POLL_NS_MAX ? ns * 2 : POLL_NS_MAX;
-                    if (++spins > (1ll << 26)) {  // watchdog (tens of seconds): never hang
-                        set_err(A, LH_EINTERNAL, slot, -2);
-                        t = -2;
-                        break;
+            long long spins = 0;
+            unsigned ns = 32;
+            while (true) {
+                int slot = -1;
+                for (int b = NPRIO - 1; b >= 0 && slot < 0; --b) {
+                    while (true) {
+                        const int h = *(volatile const int32_t *)(A.heads + b);
+                        const int tl = *(volatile const int32_t *)(A.tails + b);
+                        if (h >= tl) break;
+                        if (atomicCAS(A.heads + b, h, h + 1) == h) {
+                            slot = A.qoff[b] + h;
+                            break;
+                        }
                     }
                 }
-                // acquire: pairs with the pusher's release and invalidates this SM's L1
-                if (t >= 0) t = ld_acquire(A.queue + slot);
+                if (slot >= 0) {
+                    // acquire: pairs with the pusher's release and invalidates this SM's L1
+                    while ((t = ld_acquire(A.queue + slot)) < 0) __nanosleep(32);
+                    break;
+                }
+                if (*(volatile const int32_t *)A.done_count >= A.ntasks) break;  // all done
+                __nanosleep(ns);
+                ns = ns < POLL_NS_MAX ? ns * 2 : POLL_NS_MAX;
+                if (++spins > (1ll << 26)) {  // watchdog (tens of seconds): never hang
+                    set_err(A, LH_EINTERNAL, -1, -2);
+                    break;
+                }
             }
             s_t = t;
             if (t >= 0) s_task = A.tasks[t];
@@ -1049,14 +1129,17 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
             if (A.times && threadIdx.x == 0) A.times[2 * t + 1] = gtimer();
             const int sb = A.succ_beg[t], se = A.succ_beg[t + 1];
             for (int q = sb + threadIdx.x; q < se; q += 32) {
-                const int s = A.succ[q];
+                const int e = A.succ[q];
+                const int s = e & SUCC_MASK, b = (int)((unsigned)e >> SUCC_SHIFT);
                 if (atomicSub(A.remaining + s, 1) == 1) {
                     // last predecessor: acquire the other predecessors' releases, then push
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    const int pos = atomicAdd(A.tail, 1);
-                    st_release(A.queue + pos, s);
+                    const int pos = atomicAdd(A.tails + b, 1);
+                    st_release(A.queue + A.qoff[b] + pos, s);
                 }
             }
+            __syncwarp();
+            if (threadIdx.x == 0) atomicAdd(A.done_count, 1);
         }
     }
 }
@@ -1078,6 +1161,8 @@ Plan::~Plan() {
     cudaFree(d_rem);
     cudaFree(d_queue_init);
     cudaFree(d_queue);
+    cudaFree(d_qoff);
+    cudaFree(d_ctr);
 }
 
 void Plan::upload(cudaStream_t s) {
@@ -1088,13 +1173,23 @@ void Plan::upload(cudaStream_t s) {
         for (int32_t k = 0; k < tasks[t].dep_cnt; ++k) ++sb[deps[tasks[t].dep_beg + k] + 1];
     for (int32_t t = 0; t < n; ++t) sb[t + 1] += sb[t];
     std::vector<int32_t> fill(sb.begin(), sb.end() - 1);
-    int32_t n0 = 0;
+    LH_REQUIRE(n < (1 << 28), LH_EINTERNAL, "task count exceeds the successor encoding");
+    std::vector<int32_t> cnt(NPRIO, 0), qoff(NPRIO, 0), pos(NPRIO, 0);
+    for (int32_t t = 0; t < n; ++t) ++cnt[tasks[t].prio];
+    for (int b = 1; b < NPRIO; ++b) qoff[b] = qoff[b - 1] + cnt[b - 1];
     for (int32_t t = 0; t < n; ++t) {
         rem[t] = tasks[t].dep_cnt;
-        for (int32_t k = 0; k < tasks[t].dep_cnt; ++k) sc[fill[deps[tasks[t].dep_beg + k]]++] = t;
-        if (rem[t] == 0) q0[n0++] = t;
+        const int32_t code = t | (tasks[t].prio << 28);
+        for (int32_t k = 0; k < tasks[t].dep_cnt; ++k) sc[fill[deps[tasks[t].dep_beg + k]]++] = code;
+        if (rem[t] == 0) {
+            const int b = tasks[t].prio;
+            q0[qoff[b] + pos[b]++] = t;
+        }
     }
-    n_ready0 = n0;
+    ctr_init.assign(2 * NPRIO + 2, 0);
+    for (int b = 0; b < NPRIO; ++b) ctr_init[NPRIO + b] = pos[b];  // tails
+    d_qoff = dupload(qoff, s);
+    d_ctr = dalloc<int32_t>(2 * NPRIO + 2);
     d_succ_beg = dupload(sb, s);
     d_succ = dupload(sc, s);
     d_rem_init = dupload(rem, s);
@@ -1189,8 +1284,7 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
                                 cudaMemcpyDeviceToDevice, s));
         LH_CUDA(cudaMemcpyAsync(P.d_queue, P.d_queue_init, sizeof(int32_t) * P.tasks.size(),
                                 cudaMemcpyDeviceToDevice, s));
-        const int32_t n0 = P.n_ready0;
-        LH_CUDA(cudaMemcpyAsync(P.d_done + P.tasks.size() + 1, &n0, sizeof(int32_t),
+        LH_CUDA(cudaMemcpyAsync(P.d_ctr, P.ctr_init.data(), sizeof(int32_t) * P.ctr_init.size(),
                                 cudaMemcpyHostToDevice, s));
     }
     if (F.nslots)
@@ -1208,8 +1302,10 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     A.deps = P.d_deps;
     A.pieces = P.d_pieces;
     A.done = P.d_done;
-    A.counter = P.d_done + P.tasks.size();
-    A.tail = P.d_done + P.tasks.size() + 1;
+    A.heads = P.d_ctr;
+    A.tails = P.d_ctr + NPRIO;
+    A.done_count = P.d_ctr + 2 * NPRIO;
+    A.qoff = P.d_qoff;
     A.queue = P.d_queue;
     A.remaining = P.d_rem;
     A.succ_beg = P.d_succ_beg;
@@ -1261,11 +1357,89 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     if (err[0] != 0) throw Error(err[0], "executor failure (task " + std::to_string(err[1]) + ")");
 }
 
+// ---------------------------------------------------------------------------
+// background planning: plans depend only on the block structure, so the H-LU plan is
+// built on a host thread as soon as a square H-matrix is assembled, and the two
+// triangular-inverse plans right after it (overlapping the GPU execution of the LU)
+// ---------------------------------------------------------------------------
+void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap);
+
+struct PlanJob {
+    HMat shadow;  // structure-only copy the planner mutates (no device memory)
+    std::shared_ptr<Plan> lu;
+    i64 perm_len = 0;
+    HMat X[2];
+    std::shared_ptr<Plan> inv[2];
+    std::future<void> f_lu, f_inv;
+    std::string error;
+};
+
+static void copy_structure(HMat &D, const HMat &S) {
+    D.rt = S.rt;
+    D.ct = S.ct;
+    D.rt_hold = S.rt_hold;
+    D.ct_hold = S.ct_hold;
+    D.nrows = S.nrows;
+    D.ncols = S.ncols;
+    D.root = S.root;
+    D.nodes = S.nodes;
+    D.leafblocks = S.leafblocks;
+    D.nslots = S.nslots;
+    D.arena_len = S.arena_len;
+}
+
+static void patch_eps(Plan &P, double eps2) {
+    for (DTask &t : P.tasks)
+        if (t.type == T_LRADD) t.alpha2 = eps2;
+}
+
+void start_background_plans(HMat &H) {
+    if (H.nrows != H.ncols || H.factored || getenv("LEVYH_NO_BG_PLAN")) return;
+    auto job = std::make_shared<PlanJob>();
+    copy_structure(job->shadow, H);
+    PlanJob *j = job.get();
+    job->f_lu = std::async(std::launch::async, [j] {
+        try {
+            j->lu = plan_hlu(j->shadow, 1e-10, j->perm_len);
+        } catch (const std::exception &e) {
+            j->error = e.what();
+        }
+    });
+    job->f_inv = std::async(std::launch::async, [j] {
+        j->f_lu.wait();
+        if (!j->error.empty()) return;
+        try {
+            j->shadow.factored = true;
+            for (int mode = 0; mode < 2; ++mode) triangle_layout(j->X[mode], j->shadow, mode == 0, KA_MAX);
+            auto f0 = std::async(std::launch::async,
+                                 [j] { j->inv[0] = plan_inverse(j->shadow, j->X[0], 0, 1e-10); });
+            j->inv[1] = plan_inverse(j->shadow, j->X[1], 1, 1e-10);
+            f0.get();
+        } catch (const std::exception &e) {
+            j->error = e.what();
+        }
+    });
+    H.bg_plan = job;
+}
+
 void hlu(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.nrows == F.ncols, LH_EINVAL, "LU requires a square matrix");
     LH_REQUIRE(!F.factored, LH_EINVAL, "matrix is already factored");
     i64 perm_len = 0;
-    auto P = plan_hlu(F, eps2, perm_len);  // marks diagonal leaves K_FDENSE
+    std::shared_ptr<Plan> P;
+    PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
+    if (job) {
+        job->f_lu.wait();
+        if (job->error.empty() && job->lu) {
+            P = job->lu;
+            F.nodes = job->shadow.nodes;  // diagonal leaves K_FDENSE with pivot/inverse offsets
+            F.inv_len = job->shadow.inv_len;
+            perm_len = job->perm_len;
+            if (eps2 != 1e-10) patch_eps(*P, eps2);
+            P->build_seconds = job->lu->build_seconds;
+        }
+    }
+    if (!P) P = plan_hlu(F, eps2, perm_len);  // marks diagonal leaves K_FDENSE
     F.d_perm = dalloc<int32_t>(std::max<i64>(perm_len, 1));
     F.perm_len = perm_len;
     F.d_inv = dalloc<double>(std::max<i64>(F.inv_len, 1));
@@ -1360,13 +1534,28 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
     SolvePlans &S = plans_of(F);
     if (S.XL) return;
     int kcap = KA_MAX;  // room for rank + sketch width before recompression
+    PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
+    bool use_bg = false;
+    if (job) {
+        job->f_inv.wait();
+        use_bg = job->error.empty() && job->inv[0] && job->inv[1];
+    }
     for (int mode = 0; mode < 2; ++mode) {
         auto X = std::make_shared<HMat>();
-        triangle_layout(*X, F, mode == 0, kcap);
+        std::shared_ptr<Plan> P;
+        if (use_bg) {
+            copy_structure(*X, job->X[mode]);
+            X->nslots = job->X[mode].nslots;
+            X->arena_len = job->X[mode].arena_len;
+            P = job->inv[mode];
+            if (eps2 != 1e-10) patch_eps(*P, eps2);
+        } else {
+            triangle_layout(*X, F, mode == 0, kcap);
+        }
         X->d_arena = dalloc<double>(std::max<i64>(X->arena_len, 1));
         X->d_ranks = dalloc<int32_t>(std::max(X->nslots, 1));
         LH_CUDA(cudaMemsetAsync(X->d_ranks, 0, sizeof(int32_t) * std::max(X->nslots, 1), ctx.stream));
-        auto P = plan_inverse(F, *X, mode, eps2);
+        if (!P) P = plan_inverse(F, *X, mode, eps2);
         P->upload(ctx.stream);
         run_plan(ctx, *P, F, X.get(), nullptr, -1, mode == 0 ? "inverse L" : "inverse U");
         X->sync_ranks(ctx.stream);
@@ -1384,6 +1573,7 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
     }
     S.tmp_len = F.nrows;
     S.tmp = dalloc<double>(S.tmp_len);
+    F.bg_plan.reset();
 }
 
 static void solve_inverse(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {

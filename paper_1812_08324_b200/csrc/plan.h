@@ -48,7 +48,9 @@ struct DTask {
     DView v[4];
     int32_t dep_beg, dep_cnt;
     int32_t pc_beg, pc_end;
+    int32_t prio, pad;  // ready-queue bucket (b-level class; higher = more urgent)
 };
+constexpr int NPRIO = 8;
 
 struct DPiece {     // SEGMUL piece: Y += alpha * mat * (X rows or W)
     int32_t kind;   // 0 dense: mat (seg x n) times X[xrow : xrow+n, :]; 1 low-rank: mat (seg x r) times w
@@ -74,7 +76,8 @@ struct Plan {
     int32_t *d_succ_beg = nullptr, *d_succ = nullptr;  // successor CSR
     int32_t *d_rem_init = nullptr, *d_rem = nullptr;   // dependency counters
     int32_t *d_queue_init = nullptr, *d_queue = nullptr;  // ready FIFO
-    int32_t n_ready0 = 0;
+    int32_t *d_qoff = nullptr, *d_ctr = nullptr;  // bucket offsets; heads, tails, done count
+    std::vector<int32_t> ctr_init;
     double *d_temp = nullptr;
     int32_t *d_ranks = nullptr;
     int32_t *d_err = nullptr;
