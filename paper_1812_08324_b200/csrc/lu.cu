@@ -1636,12 +1636,12 @@ void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out) {
         DView D{dense_off, m, m, m, -1, B_F, 0, 0};
         DView Bv{rhs_off, m, k, m, -1, B_F, 0, 0};
         DView Iv{(i64)r * m * m, m, m, m, -1, B_INV, 0, 0};
-        if (kind == 0) {
+        if (kind == 0 || kind == 3) {
             t.type = T_GETRF;
             t.aux = r * m;
             t.v[0] = D;
             t.v[1] = Iv;
-            t.flags = 1;
+            t.flags = kind == 0 ? 1 : 0;  // kind 3: LU without the packed leaf inverse
         } else if (kind == 1) {
             t.type = T_TRSM;
             t.flags = 0 | 32 | 64;
