@@ -103,6 +103,17 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def max_over_ranks(value, world, device):
+    """Timing contract: the job's time is the slowest rank's (all_reduce MAX)."""
+    if world <= 1:
+        return float(value)
+    import torch
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_setup():
     import torch
 
@@ -235,10 +246,7 @@ def run_b200(args, world, rank, local):
         while time.perf_counter() - t_load < 1.5:
             steps(50, u)
         torch.cuda.synchronize()
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, "cuda")
     ms_per_step = ms / args.steps
     value = world * args.steps / (ms / 1000.0)
 
