@@ -22,6 +22,9 @@ using dev::NT;
 constexpr int SEG = 64;         // rows per segment
 constexpr int GRP = NT / SEG;   // thread groups per segment
 constexpr i64 VCHUNK = 1024;    // rows of V per phase-1 chunk (one warp)
+#ifndef SEG_MIN_BLOCKS
+#define SEG_MIN_BLOCKS 4        // CTAs per SM for the segment kernel (5-6 spill and lose ~10%)
+#endif
 
 // Phase 1: each CTA owns one chunk of rows of one V_b; every thread accumulates all
 // r columns for its rows (x[i] read once, r independent coalesced loads per row),
@@ -34,12 +37,24 @@ __device__ __forceinline__ void vtx_warp(const VChunk &C, int r, const double *a
     double acc[RB];
 #pragma unroll
     for (int c = 0; c < RB; ++c) acc[c] = 0.0;
-    for (int i = lane; i < C.len; i += 32) {
+    int i = lane;
+    // two rows per iteration: 2 (r + 1) independent loads in flight before the FMAs
+    for (; i + 32 < C.len; i += 64) {
+        const double x0 = xx[i], x1 = xx[i + 32];
+        double v0[RB], v1[RB];
+#pragma unroll
+        for (int c = 0; c < RB; ++c) {
+            v0[c] = c < r ? V[i + (i64)c * C.ld] : 0.0;
+            v1[c] = c < r ? V[i + 32 + (i64)c * C.ld] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < RB; ++c) acc[c] += v0[c] * x0 + v1[c] * x1;
+    }
+    if (i < C.len) {
         const double xi = xx[i];
-        const double *vi = V + i;
 #pragma unroll
         for (int c = 0; c < RB; ++c)
-            if (c < r) acc[c] += vi[(i64)c * C.ld] * xi;
+            if (c < r) acc[c] += V[i + (i64)c * C.ld] * xi;
     }
 #pragma unroll
     for (int c = 0; c < RB; ++c)
@@ -93,7 +108,7 @@ __global__ void treduce_kernel(const TJob *jobs, int njobs, const int *ranks, co
     }
 }
 
-__global__ void __launch_bounds__(NT) seg_kernel(const SegDesc *segs, int nseg, const MvDense *dp,
+__global__ void __launch_bounds__(NT, SEG_MIN_BLOCKS) seg_kernel(const SegDesc *segs, int nseg, const MvDense *dp,
                                                  const MvLr *lp, const double *arena,
                                                  const int *ranks, const double *tvec,
                                                  const double *x, double *y, double alpha,
