@@ -128,21 +128,30 @@ int lh_hmat_matvec(lh_ctx *ctx, const lh_hmat *h, const double *x_dev, int64_t l
  * On LH_ESINGULAR the message names the block path. */
 int lh_hlu(lh_ctx *ctx, lh_hmat *h, double eps2);
 /* hops.py:424-432 solve: forward (unit L, leaf pivots) + backward (U) substitution,
- * in place on B (n x nrhs, col-major, ldb). method 0 = substitution DAG, 1 = inverse factors. */
+ * in place on B (n x nrhs, col-major, ldb). method 0 = substitution DAG, 1 = inverse factors,
+ * 2 = propagator (one H-matvec of Z = (LU)^-1). */
 int lh_solve(lh_ctx *ctx, lh_hmat *factor, double *b_dev, int64_t ldb, int32_t nrhs,
              int32_t method);
 /* Precompute the triangular-inverse factors used by method 1. */
 int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *factor, double eps2);
-/* levy.py:309-330 run_cn loop: U <- solve(F, Hm U), nsteps times, in place. */
+/* Precompute the propagator Z = (LU)^-1 as an H-matrix on the factor's block tree
+ * (L- then U-solve of the identity, eps2 recompression), used by method 2. */
+int lh_prepare_propagator(lh_ctx *ctx, lh_hmat *factor, double eps2);
+/* out[0..3] = propagator task count, planning seconds, temp bytes, executor seconds */
+int lh_propagator_stats(lh_hmat *factor, double *out_host);
+/* levy.py:309-330 run_cn loop: U <- solve(F, Hm U), nsteps times, in place.
+ * method 2 with Hm = 2I - A+ (the CN pair; checked once with a probe vector) runs
+ * U <- 2 Z U - U, one H-matvec per step; any other Hm runs U <- Z (Hm U). */
 int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev, int64_t ldu,
                 int32_t nrhs, int32_t nsteps, int32_t method);
 
-/* Measurement: CUDA-event timing of each kernel of one CN step (inverse-factor method),
- * averaged over `iters` steps applied to u_dev in place.  out[0..5] mean ms of
- * vtx(H-), seg(H-), vtx(L^-1), seg(L^-1), vtx(U^-1), seg(U^-1); out[6..11] their algorithmic
- * bytes; out[12..15] stored scalars of H-, L^-1, U^-1 and of the H-LU factor. */
+/* Measurement: CUDA-event timing of each kernel of one CN step, averaged over `iters`
+ * steps applied to u_dev in place.  method 1: out[0..5] mean ms of vtx(H-), seg(H-),
+ * vtx(L^-1), seg(L^-1), vtx(U^-1), seg(U^-1); out[6..11] their algorithmic bytes;
+ * out[12..14] stored scalars of H-, L^-1, U^-1.  method 2: out[0..1], out[6..7] for
+ * vtx(Z), seg(Z) (others 0); out[12] H-, out[13] Z.  out[15] stored scalars of the factor. */
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev,
-                    int32_t iters, double *out_host);
+                    int32_t iters, int32_t method, double *out_host);
 /* out[0..3] = H-LU task count, planning seconds, temp bytes, executor seconds */
 int lh_hlu_stats(const lh_hmat *factor, double *out_host);
 /* Executor micro-benchmark: R synthetic tasks of one kind (0 GETRF 64x64 + leaf inverse,

@@ -68,8 +68,10 @@ SIGNATURES = [
     ("lh_hlu", C.c_int, [P, P, D]),
     ("lh_solve", C.c_int, [P, P, P, I64, I32, I32]),
     ("lh_prepare_inverse", C.c_int, [P, P, D]),
+    ("lh_prepare_propagator", C.c_int, [P, P, D]),
+    ("lh_propagator_stats", C.c_int, [P, P]),
     ("lh_cn_steps", C.c_int, [P, P, P, P, I64, I32, I32, I32]),
-    ("lh_step_profile", C.c_int, [P, P, P, P, I32, P]),
+    ("lh_step_profile", C.c_int, [P, P, P, P, I32, I32, P]),
     ("lh_hlu_stats", C.c_int, [P, P]),
     ("lh_debug_task_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
     ("lh_cn_symbol", C.c_int, [P, C.POINTER(MeasureC), C.POINTER(CNParamsC), P, P, P, P]),

@@ -25,7 +25,9 @@ void hlu(Ctx &ctx, HMat &H, double eps2);
 void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method);
 void prepare_inverse(Ctx &ctx, HMat &F, double eps2);
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method);
-void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out);
+void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method, double *out);
+void prepare_propagator(Ctx &ctx, HMat &F, double eps2);
+void propagator_stats(HMat &F, double *out);
 void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
 void start_background_plans(HMat &H);
 
@@ -433,6 +435,14 @@ int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *f, double eps2) {
     return guard(ctx, [&] { prepare_inverse(ctx->c, f->h, eps2); });
 }
 
+int lh_prepare_propagator(lh_ctx *ctx, lh_hmat *f, double eps2) {
+    return guard(ctx, [&] { prepare_propagator(ctx->c, f->h, eps2); });
+}
+
+int lh_propagator_stats(lh_hmat *f, double *out) {
+    return guard(nullptr, [&] { propagator_stats(f->h, out); });
+}
+
 int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t ldu, int32_t nrhs,
                 int32_t nsteps, int32_t method) {
     return guard(ctx, [&] {
@@ -441,8 +451,10 @@ int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t l
 }
 
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int32_t iters,
-                    double *out) {
-    return guard(ctx, [&] { step_profile(ctx->c, const_cast<HMat &>(hm->h), f->h, u, iters, out); });
+                    int32_t method, double *out) {
+    return guard(ctx, [&] {
+        step_profile(ctx->c, const_cast<HMat &>(hm->h), f->h, u, iters, method, out);
+    });
 }
 
 int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out) {

@@ -7,6 +7,7 @@
 
 namespace lh {
 void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap);
+void block_layout(HMat &X, const HMat &F, int part, int kcap);
 }
 
 using namespace lh;
@@ -122,6 +123,13 @@ extern "C" int lh_debug_dump_plans(const lh_tree *rt, const lh_tree *ct, int n_m
             dump_nodes(f, X);
             auto Pi = plan_inverse(F, X, mode, 1e-10);
             dump_plan(f, *Pi);
+        }
+        {
+            HMat Z;
+            block_layout(Z, F, 2, kcap_x);
+            dump_nodes(f, Z);
+            auto Pz = plan_propagator(F, Z, 1e-10);
+            dump_plan(f, *Pz);
         }
         fclose(f);
         return LH_OK;

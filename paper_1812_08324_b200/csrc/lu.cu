@@ -1360,9 +1360,11 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
 // ---------------------------------------------------------------------------
 // background planning: plans depend only on the block structure, so the H-LU plan is
 // built on a host thread as soon as a square H-matrix is assembled, and the two
-// triangular-inverse plans right after it (overlapping the GPU execution of the LU)
+// triangular-inverse plans and the propagator plan right after it (overlapping the GPU
+// execution of the LU)
 // ---------------------------------------------------------------------------
 void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap);
+void block_layout(HMat &X, const HMat &F, int part, int kcap);
 
 struct PlanJob {
     HMat shadow;  // structure-only copy the planner mutates (no device memory)
@@ -1370,8 +1372,10 @@ struct PlanJob {
     i64 perm_len = 0;
     HMat X[2];
     std::shared_ptr<Plan> inv[2];
-    std::future<void> f_lu, f_inv;
-    std::string error;
+    HMat Z;
+    std::shared_ptr<Plan> prop;
+    std::future<void> f_lu, f_inv, f_prop;
+    std::string error, inv_error, prop_error;
 };
 
 static void copy_structure(HMat &D, const HMat &S) {
@@ -1401,22 +1405,33 @@ void start_background_plans(HMat &H) {
     job->f_lu = std::async(std::launch::async, [j] {
         try {
             j->lu = plan_hlu(j->shadow, 1e-10, j->perm_len);
+            j->shadow.factored = true;
         } catch (const std::exception &e) {
             j->error = e.what();
         }
     });
+    // the shadow is read-only from here on; each follow-up plan owns its target layout
     job->f_inv = std::async(std::launch::async, [j] {
         j->f_lu.wait();
         if (!j->error.empty()) return;
         try {
-            j->shadow.factored = true;
             for (int mode = 0; mode < 2; ++mode) triangle_layout(j->X[mode], j->shadow, mode == 0, KA_MAX);
             auto f0 = std::async(std::launch::async,
                                  [j] { j->inv[0] = plan_inverse(j->shadow, j->X[0], 0, 1e-10); });
             j->inv[1] = plan_inverse(j->shadow, j->X[1], 1, 1e-10);
             f0.get();
         } catch (const std::exception &e) {
-            j->error = e.what();
+            j->inv_error = e.what();
+        }
+    });
+    job->f_prop = std::async(std::launch::async, [j] {
+        j->f_lu.wait();
+        if (!j->error.empty()) return;
+        try {
+            block_layout(j->Z, j->shadow, 2, KA_MAX);
+            j->prop = plan_propagator(j->shadow, j->Z, 1e-10);
+        } catch (const std::exception &e) {
+            j->prop_error = e.what();
         }
     });
     H.bg_plan = job;
@@ -1461,6 +1476,11 @@ struct SolvePlans {
     int cap = 0;
     std::shared_ptr<HMat> XL, XU;   // triangular inverses
     std::shared_ptr<MvPlan> mvL, mvU;
+    std::shared_ptr<HMat> Z;        // propagator (A+)^{-1} = (L U)^{-1} on the full block tree
+    std::shared_ptr<MvPlan> mvZ;
+    const HMat *pair_hm = nullptr;  // hminus last checked against 2I - A+
+    bool pair_ok = false;
+    int g_method = -1;
     double *tmp = nullptr;          // scratch vector(s)
     i64 tmp_len = 0;
     cudaGraphExec_t graph = nullptr;  // cached CN step
@@ -1491,8 +1511,13 @@ static void solve_substitution(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) 
     }
 }
 
-// X: same block tree as F restricted to one triangle; other-triangle leaves are K_ZERO.
+// X: same block tree as F; part 0 / 1 keep the lower / upper triangle (leaves of the other
+// triangle are K_ZERO), part 2 keeps every block.  Low-rank leaves get kcap columns.
 void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap) {
+    block_layout(X, F, lower ? 0 : 1, kcap);
+}
+
+void block_layout(HMat &X, const HMat &F, int part, int kcap) {
     X.rt = F.rt;
     X.ct = F.ct;
     X.rt_hold = F.rt_hold;
@@ -1507,7 +1532,9 @@ void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap) {
     for (int32_t b : X.leafblocks) {
         Node &nd = X.nodes[b];
         bool diag = (nd.r0 == nd.c0 && nd.m == nd.n);
-        bool other = lower ? (nd.c0 >= nd.r0 + nd.m) : (nd.r0 >= nd.c0 + nd.n);
+        bool other = part == 0 ? (nd.c0 >= nd.r0 + nd.m)
+                   : part == 1 ? (nd.r0 >= nd.c0 + nd.n)
+                               : false;
         if (other && !diag) {
             nd.kind = K_ZERO;
             continue;
@@ -1538,7 +1565,7 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
     bool use_bg = false;
     if (job) {
         job->f_inv.wait();
-        use_bg = job->error.empty() && job->inv[0] && job->inv[1];
+        use_bg = job->error.empty() && job->inv_error.empty() && job->inv[0] && job->inv[1];
     }
     for (int mode = 0; mode < 2; ++mode) {
         auto X = std::make_shared<HMat>();
@@ -1547,7 +1574,7 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
             copy_structure(*X, job->X[mode]);
             X->nslots = job->X[mode].nslots;
             X->arena_len = job->X[mode].arena_len;
-            P = job->inv[mode];
+            P = std::move(job->inv[mode]);  // the job lets go: the plan dies after its run
             if (eps2 != 1e-10) patch_eps(*P, eps2);
         } else {
             triangle_layout(*X, F, mode == 0, kcap);
@@ -1571,9 +1598,104 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
             S.mvU = mv;
         }
     }
-    S.tmp_len = F.nrows;
-    S.tmp = dalloc<double>(S.tmp_len);
-    F.bg_plan.reset();
+    if (!S.tmp) {
+        S.tmp_len = F.nrows;
+        S.tmp = dalloc<double>(S.tmp_len);
+    }
+}
+
+void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
+    LH_REQUIRE(F.factored, LH_EINVAL, "prepare_propagator needs an H-LU factorization");
+    SolvePlans &S = plans_of(F);
+    if (S.Z) return;
+    PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
+    auto Z = std::make_shared<HMat>();
+    std::shared_ptr<Plan> P;
+    if (job) {
+        job->f_prop.wait();
+        if (job->error.empty() && job->prop_error.empty() && job->prop) {
+            copy_structure(*Z, job->Z);
+            Z->nslots = job->Z.nslots;
+            Z->arena_len = job->Z.arena_len;
+            P = std::move(job->prop);
+            if (eps2 != 1e-10) patch_eps(*P, eps2);
+        }
+    }
+    if (!P) {
+        block_layout(*Z, F, 2, KA_MAX);
+        P = plan_propagator(F, *Z, eps2);
+    }
+    Z->d_arena = dalloc<double>(std::max<i64>(Z->arena_len, 1));
+    Z->d_ranks = dalloc<int32_t>(std::max(Z->nslots, 1));
+    LH_CUDA(cudaMemsetAsync(Z->d_ranks, 0, sizeof(int32_t) * std::max(Z->nslots, 1), ctx.stream));
+    P->upload(ctx.stream);
+    auto t0 = std::chrono::steady_clock::now();
+    run_plan(ctx, *P, F, Z.get(), nullptr, -1, "propagator");
+    Z->sync_ranks(ctx.stream);
+    Z->lu_stats[0] = (double)P->tasks.size();
+    Z->lu_stats[1] = P->build_seconds;
+    Z->lu_stats[2] = (double)P->temp_len * 8.0;
+    Z->lu_stats[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    P.reset();
+    S.mvZ = build_mv_plan(*Z, Z->leafblocks, ctx.stream);
+    S.Z = Z;
+    if (!S.tmp) {
+        S.tmp_len = F.nrows;
+        S.tmp = dalloc<double>(S.tmp_len);
+    }
+}
+
+void propagator_stats(HMat &F, double *out) {
+    SolvePlans &S = plans_of(F);
+    LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
+    for (int k = 0; k < 4; ++k) out[k] = S.Z->lu_stats[k];
+}
+
+static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
+    SolvePlans &S = plans_of(F);
+    LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
+    for (int q = 0; q < nrhs; ++q) {
+        double *bq = b + (i64)q * ldb;
+        mv_run(*S.mvZ, *S.Z, bq, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
+        LH_CUDA(cudaMemcpyAsync(bq, S.tmp, sizeof(double) * F.nrows, cudaMemcpyDeviceToDevice,
+                                ctx.stream));
+    }
+}
+
+__global__ void probe_fill_kernel(double *p, i64 n) {
+    for (i64 e = (i64)blockIdx.x * NT + threadIdx.x; e < n; e += (i64)gridDim.x * NT) {
+        uint64_t z = (uint64_t)e * 0x9E3779B97F4A7C15ull + 777;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z ^= z >> 31;
+        p[e] = ((z >> 11) * (1.0 / 9007199254740992.0)) - 0.5;
+    }
+}
+
+// One probe per (hminus, factor) pair: the one-matvec CN step u <- 2 Z u - u is exact only
+// for hminus = 2I - A+ (the CN pair derive_toeplitz builds).  Compare Z (hminus x) with
+// 2 Z x - x on a pseudo-random x; a mismatch selects the general two-matvec step.
+static bool cn_pair_ok(Ctx &ctx, SolvePlans &S, HMat &Hm, MvPlan &Pm) {
+    if (S.pair_hm == &Hm) return S.pair_ok;
+    const i64 n = Hm.nrows;
+    double *w = dalloc<double>(4 * n);
+    probe_fill_kernel<<<1024, NT, 0, ctx.stream>>>(w, n);
+    mv_run(Pm, Hm, w, w + n, 1.0, 0.0, ctx.stream, ctx.num_sms);                  // A- x
+    mv_run(*S.mvZ, *S.Z, w + n, w + 2 * n, 1.0, 0.0, ctx.stream, ctx.num_sms);     // Z A- x
+    mv_run(*S.mvZ, *S.Z, w, w + 3 * n, 2.0, -1.0, ctx.stream, ctx.num_sms, w);     // 2 Z x - x
+    std::vector<double> h((size_t)2 * n);
+    LH_CUDA(cudaMemcpyAsync(h.data(), w + 2 * n, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost,
+                            ctx.stream));
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaFree(w);
+    double num = 0.0, den = 0.0;
+    for (i64 i = 0; i < n; ++i) {
+        const double d = h[i] - h[n + i];
+        num += d * d;
+        den += h[n + i] * h[n + i];
+    }
+    S.pair_hm = &Hm;
+    S.pair_ok = num <= 1e-12 * den;  // relative 1e-6: an unrelated hminus differs at O(1)
+    return S.pair_ok;
 }
 
 static void solve_inverse(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
@@ -1590,7 +1712,9 @@ void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method) {
     LH_REQUIRE(F.factored, LH_EINVAL, "solve needs an H-LU factorization");
     if (nrhs <= 0) return;
     if (method == 0) solve_substitution(ctx, F, b, ldb, nrhs);
-    else solve_inverse(ctx, F, b, ldb, nrhs);
+    else if (method == 1) solve_inverse(ctx, F, b, ldb, nrhs);
+    else if (method == 2) solve_propagator(ctx, F, b, ldb, nrhs);
+    else throw Error(LH_EINVAL, "solve method must be 0 (substitution), 1 (inverse factors) or 2 (propagator)");
 }
 
 // ---------------------------------------------------------------------------
@@ -1695,51 +1819,68 @@ static void mv_bytes(const HMat &H, const std::vector<int32_t> &blocks, double &
     b2 += 16.0 * H.nrows;
 }
 
-// Per-kernel CUDA-event timing of one CN step (method 1): out[0..5] = mean ms of
-// vtx(H-), seg(H-), vtx(XL), seg(XL), vtx(XU), seg(XU); out[6..11] their algorithmic
-// bytes; out[12..14] stored scalars of H-, XL, XU; out[15] stored scalars of F.
-void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out) {
+// Per-kernel CUDA-event timing of one CN step.  method 1: out[0..5] = mean ms of vtx(H-),
+// seg(H-), vtx(XL), seg(XL), vtx(XU), seg(XU); out[6..11] their algorithmic bytes;
+// out[12..14] stored scalars of H-, XL, XU.  method 2: out[0..1] / out[6..7] = vtx(Z), seg(Z)
+// of the step u <- 2 Z u - u (rest 0); out[12] H-, out[13] Z.  out[15] stored scalars of F.
+void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method, double *out) {
     SolvePlans &S = plans_of(F);
-    LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
+    if (method == 2) LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
+    else LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
     MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
     double *y = (double *)ctx.ensure_scratch(sizeof(double) * (size_t)Hm.nrows);
     Hm.sync_ranks(ctx.stream);
-    S.XL->sync_ranks(ctx.stream);
-    S.XU->sync_ranks(ctx.stream);
-    const MvPlan *plans[3] = {&Pm, S.mvL.get(), S.mvU.get()};
-    HMat *mats[3] = {&Hm, S.XL.get(), S.XU.get()};
-    double *xin[3] = {u, y, S.tmp};
-    double *yout[3] = {y, S.tmp, u};
+    struct Mv {
+        const MvPlan *P;
+        HMat *H;
+        double *x, *y;
+        double alpha, beta;
+        const double *z;
+    };
+    std::vector<Mv> mv;
+    if (method == 2) {
+        S.Z->sync_ranks(ctx.stream);
+        mv.push_back({S.mvZ.get(), S.Z.get(), u, y, 2.0, -1.0, u});
+    } else {
+        S.XL->sync_ranks(ctx.stream);
+        S.XU->sync_ranks(ctx.stream);
+        mv.push_back({&Pm, &Hm, u, y, 1.0, 0.0, nullptr});
+        mv.push_back({S.mvL.get(), S.XL.get(), y, S.tmp, 1.0, 0.0, nullptr});
+        mv.push_back({S.mvU.get(), S.XU.get(), S.tmp, u, 1.0, 0.0, nullptr});
+    }
+    const int nk = 2 * (int)mv.size();
     cudaEvent_t ev[7];
     for (auto &e : ev) LH_CUDA(cudaEventCreate(&e));
     std::vector<double> acc(6, 0.0);
     for (int it = 0; it < iters; ++it) {
-        for (int q = 0; q < 3; ++q) {
-            const MvPlan &P = *plans[q];
+        for (size_t q = 0; q < mv.size(); ++q) {
+            const Mv &m = mv[q];
             LH_CUDA(cudaEventRecord(ev[2 * q], ctx.stream));
-            mv_vtx_launch(P, *mats[q], xin[q], ctx.num_sms * 16, ctx.stream);
+            mv_vtx_launch(*m.P, *m.H, m.x, ctx.num_sms * 16, ctx.stream);
             LH_CUDA(cudaEventRecord(ev[2 * q + 1], ctx.stream));
-            mv_seg_launch(P, *mats[q], xin[q], yout[q], 1.0, 0.0, ctx.stream, ctx.num_sms);
+            mv_seg_launch(*m.P, *m.H, m.x, m.y, m.alpha, m.beta, ctx.stream, ctx.num_sms, m.z);
         }
-        LH_CUDA(cudaEventRecord(ev[6], ctx.stream));
-        LH_CUDA(cudaEventSynchronize(ev[6]));
-        for (int k = 0; k < 6; ++k) {
+        LH_CUDA(cudaEventRecord(ev[nk], ctx.stream));
+        if (method == 2)
+            LH_CUDA(cudaMemcpyAsync(u, y, sizeof(double) * Hm.nrows, cudaMemcpyDeviceToDevice,
+                                    ctx.stream));
+        LH_CUDA(cudaEventSynchronize(ev[nk]));
+        for (int k = 0; k < nk; ++k) {
             float ms = 0.f;
             LH_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
             acc[k] += ms;
         }
     }
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
     for (auto &e : ev) cudaEventDestroy(e);
-    for (int k = 0; k < 6; ++k) out[k] = acc[k] / std::max(iters, 1);
-    std::vector<int32_t> all_m = Hm.leafblocks;
-    std::vector<int32_t> bl, bu;
-    for (int32_t b : S.XL->leafblocks)
-        if (S.XL->nodes[b].kind != K_ZERO) bl.push_back(b);
-    for (int32_t b : S.XU->leafblocks)
-        if (S.XU->nodes[b].kind != K_ZERO) bu.push_back(b);
-    mv_bytes(Hm, all_m, out[6], out[7]);
-    mv_bytes(*S.XL, bl, out[8], out[9]);
-    mv_bytes(*S.XU, bu, out[10], out[11]);
+    for (int k = 0; k < 16; ++k) out[k] = 0.0;
+    for (int k = 0; k < nk; ++k) out[k] = acc[k] / std::max(iters, 1);
+    auto nonzero = [](const HMat &H) {
+        std::vector<int32_t> bl;
+        for (int32_t b : H.leafblocks)
+            if (H.nodes[b].kind != K_ZERO) bl.push_back(b);
+        return bl;
+    };
     auto stored = [](const HMat &H, const std::vector<int32_t> &blocks) {
         double s = 0.0;
         for (int32_t b : blocks) {
@@ -1749,10 +1890,19 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, double *out
         }
         return s;
     };
+    for (size_t q = 0; q < mv.size(); ++q) {
+        const auto bl = nonzero(*mv[q].H);
+        mv_bytes(*mv[q].H, bl, out[6 + 2 * q], out[7 + 2 * q]);
+        if (mv[q].z && mv[q].z != mv[q].y) out[7 + 2 * q] += 8.0 * mv[q].H->nrows;  // reads z
+    }
+    out[12] = stored(Hm, Hm.leafblocks);
+    if (method == 2) {
+        out[13] = stored(*S.Z, S.Z->leafblocks);
+    } else {
+        out[13] = stored(*S.XL, nonzero(*S.XL));
+        out[14] = stored(*S.XU, nonzero(*S.XU));
+    }
     F.sync_ranks(ctx.stream);
-    out[12] = stored(Hm, all_m);
-    out[13] = stored(*S.XL, bl);
-    out[14] = stored(*S.XU, bu);
     out[15] = stored(F, F.leafblocks);
 }
 
@@ -1761,14 +1911,17 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
     LH_REQUIRE(Hm.nrows == F.nrows, LH_EINVAL, "operator sizes differ");
     MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
     double *y = (double *)ctx.ensure_scratch(sizeof(double) * (size_t)Hm.nrows);
-    if (method == 1) {
+    if (method == 1 || method == 2) {
         SolvePlans &S = plans_of(F);
-        LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
-        // one step = 3 H-matvecs (6 kernels), captured once as a CUDA graph and cached
-        // per (operator, vector, scratch) so repeated single-step calls do not re-capture
+        if (method == 1) LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
+        else LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
+        // method 1: one step = 3 H-matvecs (A-, L^-1, U^-1); method 2: u <- 2 Z u - u, one
+        // H-matvec of the propagator (Z A- u with two when hminus is not 2I - A+).  The step
+        // is captured once as a CUDA graph, cached per (operator, vector, scratch, method).
+        const int shape = method == 2 ? (cn_pair_ok(ctx, S, Hm, Pm) ? 2 : 3) : 1;
         for (int q = 0; q < nrhs; ++q) {
             double *uq = u + (i64)q * ldu;
-            if (!(S.graph && S.g_u == uq && S.g_hm == &Hm && S.g_y == y)) {
+            if (!(S.graph && S.g_u == uq && S.g_hm == &Hm && S.g_y == y && S.g_method == shape)) {
                 if (S.graph) {
                     cudaGraphExecDestroy(S.graph);
                     S.graph = nullptr;
@@ -1776,9 +1929,18 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                 cudaGraph_t g;
                 LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
                 try {
-                    mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
-                    mv_run(*S.mvL, *S.XL, y, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
-                    mv_run(*S.mvU, *S.XU, S.tmp, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                    if (shape == 1) {
+                        mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                        mv_run(*S.mvL, *S.XL, y, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                        mv_run(*S.mvU, *S.XU, S.tmp, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                    } else if (shape == 2) {
+                        mv_run(*S.mvZ, *S.Z, uq, y, 2.0, -1.0, ctx.stream, ctx.num_sms, uq);
+                        LH_CUDA(cudaMemcpyAsync(uq, y, sizeof(double) * Hm.nrows,
+                                                cudaMemcpyDeviceToDevice, ctx.stream));
+                    } else {
+                        mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                        mv_run(*S.mvZ, *S.Z, y, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                    }
                 } catch (...) {
                     cudaStreamEndCapture(ctx.stream, &g);
                     throw;
@@ -1789,12 +1951,14 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                 S.g_u = uq;
                 S.g_hm = &Hm;
                 S.g_y = y;
+                S.g_method = shape;
             }
             for (int k = 0; k < nsteps; ++k) LH_CUDA(cudaGraphLaunch(S.graph, ctx.stream));
         }
         LH_CUDA(cudaStreamSynchronize(ctx.stream));
         return;
     }
+    LH_REQUIRE(method == 0, LH_EINVAL, "cn_steps method must be 0, 1 or 2");
     for (int q = 0; q < nrhs; ++q) {
         double *uq = u + (i64)q * ldu;
         for (int k = 0; k < nsteps; ++k) {

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NT, SEG_MIN_BLOCKS) seg_kernel(const SegDesc *
                                                  const MvLr *lp, const double *arena,
                                                  const int *ranks, const double *tvec,
                                                  const double *x, double *y, double alpha,
-                                                 double beta) {
+                                                 double beta, const double *z) {
     __shared__ double acc_s[GRP][SEG];
     const int row = threadIdx.x % SEG, g = threadIdx.x / SEG;
     for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
@@ -192,86 +192,10 @@ __global__ void __launch_bounds__(NT, SEG_MIN_BLOCKS) seg_kernel(const SegDesc *
         if (g == 0 && row < S.rows) {
             double v = acc_s[0][row];
             for (int k = 1; k < GRP; ++k) v += acc_s[k][row];
-            double *yy = y + S.y0 + row;
-            *yy = (beta == 0.0 ? 0.0 : beta * *yy) + alpha * v;
+            const i64 i = S.y0 + row;
+            y[i] = (beta == 0.0 ? 0.0 : beta * z[i]) + alpha * v;
         }
         __syncthreads();
-    }
-}
-
-// Phase 2, warp form: one warp per 32-row half segment, one row per lane; every piece of
-// the segment is streamed by the warp alone (no shared memory, no barriers), dense pieces
-// in batches of 16 independent loads with x broadcast by shuffles.
-__global__ void __launch_bounds__(NT) seg_warp_kernel(const SegDesc *segs, int nseg,
-                                                      const MvDense *dp, const MvLr *lp,
-                                                      const double *arena, const int *ranks,
-                                                      const double *tvec, const double *x,
-                                                      double *y, double alpha, double beta) {
-    const int lane = threadIdx.x & 31;
-    const int nwork = 2 * nseg;
-    for (int wk = blockIdx.x * dev::NW + (threadIdx.x >> 5); wk < nwork; wk += gridDim.x * dev::NW) {
-        const SegDesc S = segs[wk >> 1];
-        const int base = (wk & 1) * 32;
-        if (base >= S.rows) continue;  // warp-uniform
-        const int row = base + lane;
-        const bool active = row < S.rows;
-        const int rr = active ? row : base;  // idle lanes read a valid row, discard it
-        double acc0 = 0.0, acc1 = 0.0;
-        for (int p = S.dbeg; p < S.dend; ++p) {
-            const MvDense P = dp[p];
-            const double *D = arena + P.off + rr;
-            const double *xx = x + P.xc0;
-            for (int j0 = 0; j0 < P.ncols; j0 += 32) {
-                const int jn = min(32, P.ncols - j0);
-                const double xl = lane < jn ? xx[j0 + lane] : 0.0;
-#pragma unroll
-                for (int h = 0; h < 32; h += 16) {
-                    double d[16];
-#pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        d[q] = h + q < jn ? D[(i64)(j0 + h + q) * P.ld] : 0.0;
-#pragma unroll
-                    for (int q = 0; q < 16; q += 2) {
-                        acc0 += d[q] * __shfl_sync(0xffffffffu, xl, h + q);
-                        acc1 += d[q + 1] * __shfl_sync(0xffffffffu, xl, h + q + 1);
-                    }
-                }
-            }
-        }
-        int p = S.lbeg;
-        for (; p + 2 <= S.lend; p += 2) {
-            const MvLr Q0 = lp[p], Q1 = lp[p + 1];
-            const int r0 = ranks[Q0.slot], r1 = ranks[Q1.slot];
-            const double *U0 = arena + Q0.off + rr, *U1 = arena + Q1.off + rr;
-            const double *t0 = tvec + (i64)Q0.slot * KC_MAX, *t1 = tvec + (i64)Q1.slot * KC_MAX;
-            double u0[8], u1[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                u0[c] = c < r0 ? U0[(i64)c * Q0.ld] : 0.0;
-                u1[c] = c < r1 ? U1[(i64)c * Q1.ld] : 0.0;
-            }
-            // t_b is warp-uniform: one lane-indexed load, broadcast by shuffles
-            const double tl0 = lane < min(r0, 8) ? t0[lane] : 0.0;
-            const double tl1 = lane < min(r1, 8) ? t1[lane] : 0.0;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                acc0 += u0[c] * __shfl_sync(0xffffffffu, tl0, c);
-                acc1 += u1[c] * __shfl_sync(0xffffffffu, tl1, c);
-            }
-            for (int c = 8; c < r0; ++c) acc0 += U0[(i64)c * Q0.ld] * t0[c];
-            for (int c = 8; c < r1; ++c) acc1 += U1[(i64)c * Q1.ld] * t1[c];
-        }
-        for (; p < S.lend; ++p) {
-            const MvLr Q0 = lp[p];
-            const int r0 = ranks[Q0.slot];
-            const double *U0 = arena + Q0.off + rr;
-            const double *t0 = tvec + (i64)Q0.slot * KC_MAX;
-            for (int c = 0; c < r0; ++c) acc0 += U0[(i64)c * Q0.ld] * t0[c];
-        }
-        if (active) {
-            double *yy = y + S.y0 + row;
-            *yy = (beta == 0.0 ? 0.0 : beta * *yy) + alpha * (acc0 + acc1);
-        }
     }
 }
 
@@ -393,27 +317,19 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int grid, cu
 }
 
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
-                   double beta, cudaStream_t s, int num_sms) {
-    // The warp form measured slower on B200 (370 vs 384 steps/s at 128 regs; 331 capped at 64
-    // regs with spills), so the CTA form is the default and the warp form is opt-in.
-    static const bool warp_form = getenv("LEVYH_SEG_WARP") != nullptr;
-    if (warp_form) {
-        const int warps = 2 * P.nseg;
-        int g2 = std::min((warps + dev::NW - 1) / dev::NW, num_sms * 16);
-        seg_warp_kernel<<<std::max(g2, 1), NT, 0, s>>>(P.segs, P.nseg, P.dp, P.lp, H.d_arena,
-                                                       H.d_ranks, P.tvec, x, y, alpha, beta);
-        return;
-    }
+                   double beta, cudaStream_t s, int num_sms, const double *z) {
+    // (A one-warp-per-32-rows variant without shared memory measured slower on B200:
+    // 370 vs 384 steps/s at 128 registers, 331 when capped to 64 with spills.)
     int g2 = std::min(P.nseg, num_sms * 32);
     seg_kernel<<<g2, NT, 0, s>>>(P.segs, P.nseg, P.dp, P.lp, H.d_arena, H.d_ranks, P.tvec, x, y,
-                                 alpha, beta);
+                                 alpha, beta, z ? z : y);
 }
 
-// y = alpha * H x + beta * y  for one right-hand side
+// y = alpha * H x + beta * z (z = y when null) for one right-hand side
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
-            cudaStream_t s, int num_sms) {
+            cudaStream_t s, int num_sms, const double *z) {
     mv_vtx_launch(P, H, x, num_sms * 16, s);
-    mv_seg_launch(P, H, x, y, alpha, beta, s, num_sms);
+    mv_seg_launch(P, H, x, y, alpha, beta, s, num_sms, z);
     LH_CUDA(cudaGetLastError());
 }
 

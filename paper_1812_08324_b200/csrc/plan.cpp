@@ -841,4 +841,50 @@ std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2) {
     return pl.P;
 }
 
+// Z <- (L U)^{-1} on the full block structure of F: Z = I, then Z <- L^{-1} Z (unit L with
+// leaf pivots) while the strict upper triangle of Z is still structurally zero, then
+// Z <- U^{-1} Z on every block.  Same task vocabulary as plan_inverse; the CN step
+// (A+)^{-1} A- = 2 (A+)^{-1} - I then costs one H-matvec of Z.
+std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2) {
+    auto t0 = std::chrono::steady_clock::now();
+    Planner pl(F, &Z);
+    pl.eps2 = eps2;
+    Mref Fm{&F, B_F, 0};
+    Mref Zm{&Z, B_X, F.nslots};
+    std::vector<std::pair<int32_t, int32_t>> upper;  // (block, stored kind) of strict-upper leaves
+    for (int32_t b : Z.leafblocks) {
+        Node &nd = Z.nodes[b];
+        const bool diag = (nd.r0 == nd.c0 && nd.m == nd.n);
+        if (!diag && nd.c0 >= nd.r0 + nd.m) {
+            upper.push_back({b, nd.kind});
+            nd.kind = K_ZERO;
+            continue;
+        }
+        if (nd.kind == K_DENSE) {
+            PView D = pl.dense_view(Zm, b);
+            DTask t = mk(T_IDENT);
+            t.flags = diag ? 0 : 1;
+            t.v[0] = D.d;
+            pl.emit(t, {{&D, true}});
+        }
+    }
+    pl.trisolve_left(Fm, F.root, Zm, Z.root, 0, true, "root");
+    for (auto &u : upper) {  // the upper triangle becomes live storage: zero dense, rank 0
+        Node &nd = Z.nodes[u.first];
+        nd.kind = u.second;
+        if (nd.kind == K_DENSE) {
+            PView D = pl.dense_view(Zm, u.first);
+            DTask t = mk(T_IDENT);
+            t.flags = 1;
+            t.v[0] = D.d;
+            pl.emit(t, {{&D, true}});
+        }
+    }
+    pl.trisolve_left(Fm, F.root, Zm, Z.root, 1, false, "root");
+    pl.finalize();
+    pl.P->build_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return pl.P;
+}
+
 }  // namespace lh

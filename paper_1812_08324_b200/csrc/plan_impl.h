@@ -111,6 +111,7 @@ struct Planner {
 std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out);
 std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap);
 std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2);
+std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2);
 int64_t critical_path(const Plan &P);
 
 }  // namespace lh

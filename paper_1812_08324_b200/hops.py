@@ -4,8 +4,9 @@
 ``matvec``/``mul_dense`` run the two-phase streaming kernel (csrc/matvec.cu);
 ``hlu`` runs the recursive H-LU as a static task DAG on a persistent
 dataflow kernel (csrc/lu.cu); ``solve`` applies forward/backward substitution
-(method "substitution") or the precomputed triangular-inverse factors
-(method "inverse", the per-step fast path).
+(method "substitution"), the precomputed triangular-inverse factors
+(method "inverse") or one H-matvec of the propagator Z = (LU)^{-1}
+(method "propagator", the per-step fast path).
 """
 from __future__ import annotations
 
@@ -18,7 +19,7 @@ from .hmatrix import HMatrix
 
 __all__ = ["matvec", "mul_dense", "hlu", "HFactorization", "solve"]
 
-SOLVE_METHODS = {"substitution": 0, "inverse": 1}
+SOLVE_METHODS = {"substitution": 0, "inverse": 1, "propagator": 2}
 
 
 def _to_device(x, ctx):
@@ -77,6 +78,7 @@ class HFactorization:
     h: HMatrix
     eps2: float
     inverse_ready: bool = False
+    propagator_ready: bool = False
 
     def solve(self, b, method="substitution"):
         return solve(self, b, method)
@@ -86,6 +88,19 @@ class HFactorization:
             _lib.check(_lib.lib().lh_prepare_inverse(self.h.ctx.h, self.h.handle, float(self.eps2)),
                        self.h.ctx.h)
             self.inverse_ready = True
+
+    def prepare_propagator(self):
+        """Z = (LU)^{-1} as an H-matrix on the factor's block tree (method "propagator")."""
+        if not self.propagator_ready:
+            _lib.check(_lib.lib().lh_prepare_propagator(self.h.ctx.h, self.h.handle,
+                                                        float(self.eps2)), self.h.ctx.h)
+            self.propagator_ready = True
+
+    def propagator_stats(self):
+        """(task count, planning s, temp bytes, executor s) of the propagator build."""
+        out = np.zeros(4)
+        _lib.check(_lib.lib().lh_propagator_stats(self.h.handle, _lib.host_ptr(out)))
+        return out
 
 
 def hlu(H: HMatrix, eps2=1e-10):
@@ -106,6 +121,8 @@ def solve(F: HFactorization, b, method="substitution"):
     m = SOLVE_METHODS[method]
     if m == 1:
         F.prepare_inverse()
+    elif m == 2:
+        F.prepare_propagator()
     shape = bt.shape
     bc, k = _colmajor(bt.reshape(shape[0], -1))
     bc = bc.clone()

@@ -15,7 +15,7 @@ import numpy as np
 from . import fractional as frac
 from .geometry import build_cluster_tree
 from .hmatrix import HConfig, build_toeplitz, derive_toeplitz
-from .hops import hlu, matvec, solve
+from .hops import SOLVE_METHODS, hlu, matvec, solve
 
 __all__ = ["FracCNSystem", "step_cn", "run_cn"]
 
@@ -98,6 +98,8 @@ class FracCNSystem:
         self.factor = hlu(Hp, eps2)
         if method == "inverse":
             self.factor.prepare_inverse()
+        elif method == "propagator":
+            self.factor.prepare_propagator()
         self.method = method
         return self.factor
 
@@ -125,7 +127,11 @@ def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method="inverse"):
     u = torch.as_tensor(perm.to_tree(np.asarray(u0, dtype=float))).to(f"cuda:{ctx.device}")
     uc = u.reshape(1, -1).contiguous() if u.ndim == 1 else u.t().contiguous()
     k = 1 if u.ndim == 1 else u.shape[1]
-    m = {"substitution": 0, "inverse": 1}[sys.method if method is None else method]
+    m = SOLVE_METHODS[sys.method if method is None else method]
+    if m == 2:
+        sys.factor.prepare_propagator()
+    elif m == 1:
+        sys.factor.prepare_inverse()
     _lib.check(_lib.lib().lh_cn_steps(ctx.h, sys.h_minus.handle, sys.factor.h.handle, uc.data_ptr(),
                                       sys.N, k, int(n_steps), m), ctx.h)
     out = uc.reshape(-1) if k == 1 else uc.t()

@@ -66,6 +66,8 @@ def load(path):
     out["invL"] = r.plan()
     out["XU"] = r.nodes()
     out["invU"] = r.plan()
+    out["Z"] = r.nodes()
+    out["prop"] = r.plan()
     return out
 
 

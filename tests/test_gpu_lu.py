@@ -1,4 +1,4 @@
-"""GPU parity: H-LU factorisation, substitution and inverse-factor solves, and
+"""GPU parity: H-LU factorisation, substitution / inverse-factor / propagator solves, and
 the CN stepping loop against the reference golden fixtures (rel. L2 1e-8,
 the BASELINE.json contract) and the oracle."""
 import numpy as np
@@ -55,13 +55,42 @@ def test_inverse_solve_matches_substitution(P, name):
 
 
 @pytest.mark.parametrize("name", NAMES)
-@pytest.mark.parametrize("method", ["inverse", "substitution"])
+def test_propagator_solve(P, name):
+    g = cases.load(name)
+    s, F, Hm = _factor(P, name, g)
+    a = P.solve(F, g["probe"], method="substitution")
+    b = P.solve(F, g["probe"], method="propagator")
+    assert _rel(b, a) <= 1e-9
+    assert _rel(b, g["solve_probe"]) <= 1e-9
+    st = F.propagator_stats()
+    assert st[0] > 0 and st[3] > 0  # tasks, executor seconds
+
+
+def test_propagator_general_hminus(P):
+    """cn_steps method 2 with an hminus that is NOT 2I - A+ must run Z (Hm u), not 2Zu - u."""
+    g = cases.load("cfg1")
+    s, F, Hm = _factor(P, "cfg1", g)
+    t = s.tMinus.clone().zero_()
+    t[s.N - 1] = 0.5
+    Hq = P.derive_toeplitz(Hm, t, lr_scale=0.5, kcap=0)  # 0.5 I + 0.5 (admissible blocks of A-)
+    u0 = np.asarray(g["u0"], dtype=float)
+    perm = s.tree.perm
+    s.h_minus, s.factor, s.method = Hq, F, "propagator"
+    u = P.run_cn(s, u0, 3)
+    want = u0
+    for _ in range(3):
+        want = perm.from_tree(P.solve(F, P.matvec(Hq, perm.to_tree(want)), method="substitution"))
+    assert _rel(u, want) <= 1e-9
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("method", ["propagator", "inverse", "substitution"])
 def test_cn_end_to_end(P, name, method):
     g = cases.load(name)
     s = cases.make_system(name, g)
     cfg = P.HConfig(n_min=int(g["leaf"]), eps1=float(g["eps1"]))
     s.prepare(cfg, float(g["eps2"]), method=method)
-    n_steps = int(g["n_steps"]) if method == "inverse" or name != "cfg1" else 64
+    n_steps = int(g["n_steps"]) if method != "substitution" or name != "cfg1" else 64
     u = P.run_cn(s, g["u0"], n_steps, method=method)
     if n_steps == int(g["n_steps"]):
         assert _rel(u, g["uT"]) <= 1e-8, "solution differs from the reference beyond 1e-8"
@@ -74,10 +103,11 @@ def test_cn_end_to_end(P, name, method):
         assert _rel(u, uo) <= 1e-8
 
 
-def test_cfg1_golden_pins(P):
+@pytest.mark.parametrize("method", ["propagator", "inverse"])
+def test_cfg1_golden_pins(P, method):
     g = cases.load("cfg1")
     s = cases.make_system("cfg1", g)
-    s.prepare(P.HConfig(n_min=32, eps1=1e-10), 1e-10, method="inverse")
+    s.prepare(P.HConfig(n_min=32, eps1=1e-10), 1e-10, method=method)
     u = P.run_cn(s, g["u0"], 512)
     assert abs(np.linalg.norm(u) - 6.179677103303214) <= 1e-8 * 6.18
     assert abs(u[511] - 0.25498164269386925) <= 1e-8

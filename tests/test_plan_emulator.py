@@ -1,5 +1,6 @@
 """CPU check of the H-arithmetic planner: the task DAGs exported by the native
-library (H-LU, substitution solve, lower/upper triangular inverses) are executed
+library (H-LU, substitution solve, lower/upper triangular inverses, propagator
+Z = (LU)^{-1}) are executed
 by a numpy emulator of the device task semantics (tests/plan_emulator.py) on the
 oracle's compressed operator, and compared with the oracle's hlu / solve."""
 import numpy as np
@@ -45,8 +46,8 @@ def test_planned_dags_match_oracle(name, tmp_path):
     M2.run(sp, np.random.default_rng(0))
     x = rhs[:2 * N].reshape(2, N).T
     assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
-    # --- triangular inverses: X b == forward / backward substitution
-    for key, pk, mode in (("XL", "invL", "L"), ("XU", "invU", "U")):
+    # --- triangular inverses: X b == forward / backward substitution; propagator Z b == solve
+    for key, pk, mode in (("XL", "invL", "L"), ("XU", "invU", "U"), ("Z", "prop", "LU")):
         lay, ip = D[key], D[pk]
         ar = np.zeros(max(lay["arena"], 1))
         rk3 = np.zeros(ip["nslots_total"] + 1, dtype=np.int64)
@@ -66,5 +67,8 @@ def test_planned_dags_match_oracle(name, tmp_path):
                 y[R0:R1] += U @ (V.T @ b[C0:C1])
             else:
                 y[R0:R1] += ar[doff + np.arange(m)[:, None] + np.arange(n)[None, :] * m] @ b[C0:C1]
-        want = O.solve_dense(Fo, b.copy(), mode, mode == "L", "root")
+        if mode == "LU":
+            want = ref
+        else:
+            want = O.solve_dense(Fo, b.copy(), mode, mode == "L", "root")
         assert np.linalg.norm(y - want) <= 1e-11 * np.linalg.norm(want), key
