@@ -130,7 +130,14 @@ def dist_setup():
     return world, rank, local
 
 
-def build_system(P, cfg=CFG3, n=None):
+SOLVE_DESC = {
+    "propagator": "u <- 2 Z u - u with Z = (A+)^-1 = (LU)^-1 precomputed as an H-matrix from the H-LU "
+                  "(one H-matvec per step, DESIGN.md)",
+    "inverse": "A- matvec + triangular-inverse H-factors L^-1, U^-1 of the H-LU (DESIGN.md)",
+}
+
+
+def build_system(P, cfg=CFG3, n=None, method="propagator"):
     """Operator assembly (GPU symbol + ACA compression) and factorisation, timed."""
     import torch
 
@@ -155,18 +162,26 @@ def build_system(P, cfg=CFG3, n=None):
     st = np.zeros(4)
     P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st))
     t3 = time.perf_counter()
-    F.prepare_inverse()
+    if method == "propagator":
+        F.prepare_propagator()
+    elif method == "inverse":
+        F.prepare_inverse()
     torch.cuda.synchronize()
-    t_inv = time.perf_counter() - t3
+    t_prep = time.perf_counter() - t3
     s.factor = F
-    s.method = "inverse"
+    s.method = method
     times = dict(symbol_s=t_symbol, aca_s=t_aca, assembly_s=t_symbol + t_aca, hlu_s=t_lu,
-                 hlu_plan_s=float(st[1]), hlu_exec_s=float(st[3]), hlu_tasks=int(st[0]),
-                 inverse_factors_s=t_inv, stored_scalars_plus=mem_p["stored_scalars"],
-                 setup_total_s=time.perf_counter() - t0,
-                 note="hlu_plan_s is host planning on a background thread started at the end of "
+                 hlu_plan_s=float(st[1]), hlu_exec_s=float(st[3]), hlu_tasks=int(st[0]))
+    if method == "propagator":
+        ps = F.propagator_stats()
+        times.update(propagator_s=t_prep, propagator_plan_s=float(ps[1]),
+                     propagator_exec_s=float(ps[3]), propagator_tasks=int(ps[0]))
+    elif method == "inverse":
+        times.update(inverse_factors_s=t_prep)
+    times.update(stored_scalars_plus=mem_p["stored_scalars"], setup_total_s=time.perf_counter() - t0,
+                 note="*_plan_s is host planning on background threads started at the end of "
                       "assembly (overlaps ACA/LU execution); setup_total_s = symbol + ACA + H-LU + "
-                      "triangular inverses, wall clock")
+                      f"{method} preparation, wall clock")
     return s, F, Hm, times
 
 
@@ -214,15 +229,17 @@ def run_b200(args, world, rank, local):
 
     import paper_1812_08324_b200 as P
 
-    s, F, Hm, times = build_system(P, n=args.n)
+    s, F, Hm, times = build_system(P, n=args.n, method=args.method)
     ctx = Hm.ctx
     L = P._lib.lib()
     N = s.N
     u0 = np.maximum(np.exp(s.x) - 1.0, 0.0)
     u = torch.from_numpy(u0.copy()).cuda()
+    mcode = P.SOLVE_METHODS[args.method]
 
     def steps(k, vec):
-        P._lib.check(L.lh_cn_steps(ctx.h, Hm.handle, F.h.handle, vec.data_ptr(), N, 1, int(k), 1), ctx.h)
+        P._lib.check(L.lh_cn_steps(ctx.h, Hm.handle, F.h.handle, vec.data_ptr(), N, 1, int(k), mcode),
+                     ctx.h)
 
     # warm-up (also captures the CUDA graph of one step)
     steps(args.warmup, u)
@@ -241,6 +258,7 @@ def run_b200(args, world, rank, local):
         end.record(lib_stream)
         torch.cuda.synchronize()
         ms = start.elapsed_time(end)
+        launches_per_step = int(L.lh_step_graph_kernels(F.h.handle))
         # keep the GPU busy for the clock sampler (extra untimed steps)
         t_load = time.perf_counter()
         while time.perf_counter() - t_load < 1.5:
@@ -272,11 +290,18 @@ def run_b200(args, world, rank, local):
     # ---- per-kernel roofline (CUDA events on the library stream)
     prof = np.zeros(16)
     uprof = torch.from_numpy(u0.copy()).cuda()
-    P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, uprof.data_ptr(), 5, P._lib.host_ptr(prof)),
-                 ctx.h)
-    names = ["vtx(A-)", "seg(A-)", "vtx(L^-1)", "seg(L^-1)", "vtx(U^-1)", "seg(U^-1)"]
-    kms = prof[:6]
-    kbytes = prof[6:12]
+    P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, uprof.data_ptr(), 5, mcode,
+                                   P._lib.host_ptr(prof)), ctx.h)
+    if args.method == "propagator":
+        names = ["vtx(Z)", "seg(Z)"]
+        stored = {"A-": int(prof[12]), "Z=(A+)^-1": int(prof[13]), "LU factor": int(prof[15])}
+    else:
+        names = ["vtx(A-)", "seg(A-)", "vtx(L^-1)", "seg(L^-1)", "vtx(U^-1)", "seg(U^-1)"]
+        stored = {"A-": int(prof[12]), "L^-1": int(prof[13]), "U^-1": int(prof[14]),
+                  "LU factor": int(prof[15])}
+    nk = len(names)
+    kms = prof[:nk]
+    kbytes = prof[6:6 + nk]
     dom = int(np.argmax(kms))
     peak, peak_src = measured_peaks()
     achieved = kbytes[dom] / (kms[dom] / 1000.0) / 1e9
@@ -297,8 +322,7 @@ def run_b200(args, world, rank, local):
                 "step_bytes": step_bytes,
                 "step_GBps_sum_of_kernels": round(step_bytes / (kms.sum() / 1e3) / 1e9, 1),
                 "step_GBps_timed": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1),
-                "stored_scalars": {"A-": int(prof[12]), "L^-1": int(prof[13]), "U^-1": int(prof[14]),
-                                   "LU factor": int(prof[15])},
+                "stored_scalars": stored,
                 "reference_algorithm_bytes_per_step": 8.0 * (prof[12] + prof[15] + 6 * N)}
 
     out = {"metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
@@ -307,10 +331,11 @@ def run_b200(args, world, rank, local):
            "data": "synthetic (BASELINE.json configs[2]; seeded/closed-form inputs, no dataset)",
            "config": {"workload": CFG3["workload"] if args.n is None else f"cfg3 operator at n={args.n}",
                       "N": N, "leaf": CFG3["leaf"], "eps1": CFG3["eps1"], "eps2": CFG3["eps2"],
-                      "solve": "triangular-inverse H-factors of the H-LU (DESIGN.md)",
+                      "solve": SOLVE_DESC[args.method],
                       "parallelism": f"replicas x{world}",
-                      "l2": "inputs larger than L2 (>= 14 GB streamed per step vs 126 MB L2)"},
-           "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": 9 * args.steps,
+                      "l2": f"inputs larger than L2 ({step_bytes / 1e9:.1f} GB streamed per step vs 126 MB L2)"},
+           "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+           "gpu_launches_per_step": launches_per_step,
            "roofline": roofline, "phases": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in times.items()}}
 
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -334,7 +359,7 @@ def run_reference(args, world, rank, local):
 
     import paper_1812_08324_b200 as P
 
-    s, F, Hm, times = build_system(P, n=args.n)
+    s, F, Hm, times = build_system(P, n=args.n, method="none")  # factors only
     u0 = np.maximum(np.exp(s.x) - 1.0, 0.0)
     warm = min(args.warmup, 1)
     k = max(1, min(args.steps, args.ref_steps))
@@ -370,6 +395,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--ref-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--method", default="propagator", choices=["propagator", "inverse"],
+                    help="per-step solve: one H-matvec of Z=(A+)^-1 (default) or A- + L^-1 + U^-1")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")

@@ -139,6 +139,9 @@ int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *factor, double eps2);
 int lh_prepare_propagator(lh_ctx *ctx, lh_hmat *factor, double eps2);
 /* out[0..3] = propagator task count, planning seconds, temp bytes, executor seconds */
 int lh_propagator_stats(lh_hmat *factor, double *out_host);
+/* Kernel launches per CN step: kernel nodes of the step graph lh_cn_steps last captured
+ * (methods 1 and 2), 0 before the first call. */
+int32_t lh_step_graph_kernels(lh_hmat *factor);
 /* levy.py:309-330 run_cn loop: U <- solve(F, Hm U), nsteps times, in place.
  * method 2 with Hm = 2I - A+ (the CN pair; checked once with a probe vector) runs
  * U <- 2 Z U - U, one H-matvec per step; any other Hm runs U <- Z (Hm U). */

@@ -12,9 +12,10 @@ from .fractional import (FracConfig, LevyMeasure, assemble_fractional_poisson_1d
                          quartic_window, tail_mass_power_1d, windowed_second_moment)
 from .geometry import (ClusterNode, ClusterTree, Permutation, PointSet, admissible,  # noqa: F401
                        build_cluster_tree)
-from .hmatrix import (HConfig, HMatrix, build_from_dense, build_toeplitz, dump_structure,  # noqa: F401
-                      export_blocks, h_entry, memory_report, structure_summary, to_dense)
-from .hops import HFactorization, hlu, matvec, mul_dense, solve  # noqa: F401
+from .hmatrix import (HConfig, HMatrix, build_from_dense, build_toeplitz, derive_toeplitz,  # noqa: F401
+                      dump_structure, export_blocks, h_entry, memory_report, structure_summary,
+                      to_dense)
+from .hops import SOLVE_METHODS, HFactorization, hlu, matvec, mul_dense, solve  # noqa: F401
 from .levy import FracCNSystem, run_cn, step_cn  # noqa: F401
 
 __version__ = "0.1.0"

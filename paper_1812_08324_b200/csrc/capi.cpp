@@ -28,6 +28,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
 void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method, double *out);
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2);
 void propagator_stats(HMat &F, double *out);
+int step_graph_kernels(HMat &F);
 void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
 void start_background_plans(HMat &H);
 
@@ -442,6 +443,8 @@ int lh_prepare_propagator(lh_ctx *ctx, lh_hmat *f, double eps2) {
 int lh_propagator_stats(lh_hmat *f, double *out) {
     return guard(nullptr, [&] { propagator_stats(f->h, out); });
 }
+
+int32_t lh_step_graph_kernels(lh_hmat *f) { return step_graph_kernels(f->h); }
 
 int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t ldu, int32_t nrhs,
                 int32_t nsteps, int32_t method) {

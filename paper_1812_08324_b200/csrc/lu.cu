@@ -1481,6 +1481,7 @@ struct SolvePlans {
     const HMat *pair_hm = nullptr;  // hminus last checked against 2I - A+
     bool pair_ok = false;
     int g_method = -1;
+    int g_kernels = 0;  // kernel nodes in the cached step graph
     double *tmp = nullptr;          // scratch vector(s)
     i64 tmp_len = 0;
     cudaGraphExec_t graph = nullptr;  // cached CN step
@@ -1644,6 +1645,8 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
         S.tmp = dalloc<double>(S.tmp_len);
     }
 }
+
+int step_graph_kernels(HMat &F) { return plans_of(F).g_kernels; }
 
 void propagator_stats(HMat &F, double *out) {
     SolvePlans &S = plans_of(F);
@@ -1946,6 +1949,16 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                     throw;
                 }
                 LH_CUDA(cudaStreamEndCapture(ctx.stream, &g));
+                size_t nn = 0;
+                LH_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+                std::vector<cudaGraphNode_t> nodes(nn);
+                LH_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+                S.g_kernels = 0;
+                for (auto nd : nodes) {
+                    cudaGraphNodeType ty;
+                    LH_CUDA(cudaGraphNodeGetType(nd, &ty));
+                    S.g_kernels += ty == cudaGraphNodeTypeKernel;
+                }
                 LH_CUDA(cudaGraphInstantiate(&S.graph, g, 0));
                 cudaGraphDestroy(g);
                 S.g_u = uq;
