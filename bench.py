@@ -159,7 +159,7 @@ def build_system(P, cfg=CFG3, n=None, method="propagator"):
     F = P.hlu(Hp, cfg["eps2"])
     torch.cuda.synchronize()
     t_lu = time.perf_counter() - t2
-    st = np.zeros(4)
+    st = np.zeros(5)
     P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st))
     t3 = time.perf_counter()
     if method == "propagator":
@@ -171,14 +171,17 @@ def build_system(P, cfg=CFG3, n=None, method="propagator"):
     s.factor = F
     s.method = method
     times = dict(symbol_s=t_symbol, aca_s=t_aca, assembly_s=t_symbol + t_aca, hlu_s=t_lu,
-                 hlu_plan_s=float(st[1]), hlu_exec_s=float(st[3]), hlu_tasks=int(st[0]))
+                 hlu_plan_s=float(st[1]), hlu_exec_s=float(st[3]), hlu_tasks=int(st[0]),
+                 hlu_plan_chunks=int(st[4]))
     if method == "propagator":
         ps = F.propagator_stats()
         times.update(propagator_s=t_prep, propagator_plan_s=float(ps[1]),
                      propagator_exec_s=float(ps[3]), propagator_tasks=int(ps[0]))
     elif method == "inverse":
         times.update(inverse_factors_s=t_prep)
+    free_b, total_b = torch.cuda.mem_get_info()
     times.update(stored_scalars_plus=mem_p["stored_scalars"], setup_total_s=time.perf_counter() - t0,
+                 device_mem_used_gb=round((total_b - free_b) / 1e9, 2),
                  note="*_plan_s is host planning on background threads started at the end of "
                       "assembly (overlaps ACA/LU execution); setup_total_s = symbol + ACA + H-LU + "
                       f"{method} preparation, wall clock")

@@ -155,7 +155,8 @@ int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_d
  * vtx(Z), seg(Z) (others 0); out[12] H-, out[13] Z.  out[15] stored scalars of the factor. */
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev,
                     int32_t iters, int32_t method, double *out_host);
-/* out[0..3] = H-LU task count, planning seconds, temp bytes, executor seconds */
+/* out[0..4] = H-LU task count, planning seconds, temp bytes, executor seconds, number of
+ * plan chunks executed (> 1 when the LU ran while its plan was still being built) */
 int lh_hlu_stats(const lh_hmat *factor, double *out_host);
 /* Executor micro-benchmark: R synthetic tasks of one kind (0 GETRF 64x64 + leaf inverse,
  * 1 TRSM via leaf inverse, 2 SEGMUL with one dense 64x64 piece), k right-hand columns,

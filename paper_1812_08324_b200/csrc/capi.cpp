@@ -465,7 +465,7 @@ int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *
 }
 
 int lh_hlu_stats(const lh_hmat *f, double *out) {
-    for (int k = 0; k < 4; ++k) out[k] = f->h.lu_stats[k];
+    for (int k = 0; k < 5; ++k) out[k] = f->h.lu_stats[k];
     return LH_OK;
 }
 

@@ -99,7 +99,7 @@ struct HMat {
     double *d_inv = nullptr;          // FDENSE packed leaf inverses
     i64 inv_len = 0;
     bool factored = false;
-    double lu_stats[4] = {0, 0, 0, 0};  // tasks, plan seconds, temp bytes, -
+    double lu_stats[5] = {0, 0, 0, 0, 0};  // tasks, plan s, temp bytes, exec s, chunks
     // lazily built plans (opaque; see matvec.cu / plan.cpp)
     std::shared_ptr<void> mv_plan;
     std::shared_ptr<void> solve_plan;

@@ -1152,7 +1152,7 @@ Plan::~Plan() {
     cudaFree(d_deps);
     cudaFree(d_pieces);
     cudaFree(d_done);
-    cudaFree(d_temp);
+    if (own_temp) cudaFree(d_temp);
     cudaFree(d_ranks);
     cudaFree(d_err);
     cudaFree(d_succ_beg);
@@ -1200,7 +1200,7 @@ void Plan::upload(cudaStream_t s) {
     d_deps = dupload(deps, s);
     d_pieces = dupload(pieces, s);
     d_done = dalloc<int32_t>((i64)tasks.size() + 2);
-    d_temp = dalloc<double>(std::max<i64>(temp_len, 1));
+    if (own_temp) d_temp = dalloc<double>(std::max<i64>(temp_len, 1));
     d_ranks = dalloc<int32_t>(std::max(nslots_total + 1, 1));
     d_err = dalloc<int32_t>(4);
     LH_CUDA(cudaStreamSynchronize(s));
@@ -1367,13 +1367,15 @@ void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap);
 void block_layout(HMat &X, const HMat &F, int part, int kcap);
 
 struct PlanJob {
-    HMat shadow;  // structure-only copy the planner mutates (no device memory)
+    HMat shadow;   // structure-only copy the H-LU planner mutates (no device memory)
+    HMat fshadow;  // the factor's structure as the H-LU leaves it (mark_lu_leaves), read-only
     std::shared_ptr<Plan> lu;
     i64 perm_len = 0;
     HMat X[2];
     std::shared_ptr<Plan> inv[2];
     HMat Z;
     std::shared_ptr<Plan> prop;
+    PlanStream lu_stream;  // the H-LU plan in chunks, when hlu() arrives before planning ends
     std::future<void> f_lu, f_inv, f_prop;
     std::string error, inv_error, prop_error;
 };
@@ -1397,44 +1399,119 @@ static void patch_eps(Plan &P, double eps2) {
         if (t.type == T_LRADD) t.alpha2 = eps2;
 }
 
+// Plans depend only on the block structure, so they are built on host threads as soon as
+// a square H-matrix is assembled: the H-LU plan, and concurrently the propagator plan
+// (itself split over column blocks) against the factor's structure from mark_lu_leaves.
+// The triangular-inverse plans are added when LEVYH_BG_INVERSE is set.
 void start_background_plans(HMat &H) {
     if (H.nrows != H.ncols || H.factored || getenv("LEVYH_NO_BG_PLAN")) return;
     auto job = std::make_shared<PlanJob>();
     copy_structure(job->shadow, H);
+    copy_structure(job->fshadow, H);
     PlanJob *j = job.get();
+    if (const char *e = getenv("LEVYH_STREAM_MIN_CHUNK")) j->lu_stream.min_chunk = std::max(1, atoi(e));
+    try {
+        i64 pl = 0, il = 0;
+        mark_lu_leaves(j->fshadow, pl, il);
+        j->fshadow.factored = true;
+    } catch (const std::exception &e) {
+        return;  // not LU-factorizable: hlu reports it
+    }
     job->f_lu = std::async(std::launch::async, [j] {
         try {
-            j->lu = plan_hlu(j->shadow, 1e-10, j->perm_len);
-            j->shadow.factored = true;
+            j->lu = plan_hlu(j->shadow, 1e-10, j->perm_len, &j->lu_stream);
         } catch (const std::exception &e) {
             j->error = e.what();
-        }
-    });
-    // the shadow is read-only from here on; each follow-up plan owns its target layout
-    job->f_inv = std::async(std::launch::async, [j] {
-        j->f_lu.wait();
-        if (!j->error.empty()) return;
-        try {
-            for (int mode = 0; mode < 2; ++mode) triangle_layout(j->X[mode], j->shadow, mode == 0, KA_MAX);
-            auto f0 = std::async(std::launch::async,
-                                 [j] { j->inv[0] = plan_inverse(j->shadow, j->X[0], 0, 1e-10); });
-            j->inv[1] = plan_inverse(j->shadow, j->X[1], 1, 1e-10);
-            f0.get();
-        } catch (const std::exception &e) {
-            j->inv_error = e.what();
+            std::lock_guard<std::mutex> lk(j->lu_stream.mu);  // release a waiting consumer
+            j->lu_stream.done = true;
+            j->lu_stream.cv.notify_all();
         }
     });
     job->f_prop = std::async(std::launch::async, [j] {
-        j->f_lu.wait();
-        if (!j->error.empty()) return;
         try {
-            block_layout(j->Z, j->shadow, 2, KA_MAX);
-            j->prop = plan_propagator(j->shadow, j->Z, 1e-10);
+            block_layout(j->Z, j->fshadow, 2, KA_MAX);
+            j->prop = plan_propagator(j->fshadow, j->Z, 1e-10);
         } catch (const std::exception &e) {
             j->prop_error = e.what();
         }
     });
+    if (getenv("LEVYH_BG_INVERSE")) {
+        job->f_inv = std::async(std::launch::async, [j] {
+            try {
+                for (int mode = 0; mode < 2; ++mode)
+                    triangle_layout(j->X[mode], j->fshadow, mode == 0, KA_MAX);
+                auto f0 = std::async(std::launch::async,
+                                     [j] { j->inv[0] = plan_inverse(j->fshadow, j->X[0], 0, 1e-10); });
+                j->inv[1] = plan_inverse(j->fshadow, j->X[1], 1, 1e-10);
+                f0.get();
+            } catch (const std::exception &e) {
+                j->inv_error = e.what();
+            }
+        });
+    }
     H.bg_plan = job;
+}
+
+static void check_leaf_layout(const HMat &F, const PlanJob &job) {
+    LH_REQUIRE(F.inv_len == job.fshadow.inv_len && job.perm_len == job.fshadow.perm_len,
+               LH_EINTERNAL, "background plans disagree on the diagonal-leaf layout");
+    for (size_t b = 0; b < F.nodes.size(); ++b) {
+        const Node &x = F.nodes[b], &y = job.fshadow.nodes[b];
+        LH_REQUIRE(x.kind == y.kind && x.poff == y.poff && x.ioff == y.ioff, LH_EINTERNAL,
+                   "background plans disagree on the diagonal-leaf layout");
+    }
+}
+
+// Run the H-LU as chunks of the plan still being built on the background thread; the
+// chunks share one temp pool (grown by copy when a later chunk needs more).
+static void hlu_streamed(Ctx &ctx, HMat &F, double eps2, PlanJob &job) {
+    PlanStream &st = job.lu_stream;
+    double *temp = nullptr;
+    i64 temp_cap = 0;
+    double exec_s = 0.0;
+    int nchunks = 0;
+    i64 ntasks = 0;
+    std::unique_lock<std::mutex> lk(st.mu);
+    for (;;) {
+        st.want.store(true);
+        st.cv.wait(lk, [&] { return !st.chunks.empty() || st.done; });
+        if (st.chunks.empty()) break;
+        std::shared_ptr<Plan> C = st.chunks.front();
+        st.chunks.pop_front();
+        lk.unlock();
+        if (eps2 != 1e-10) patch_eps(*C, eps2);
+        if (C->temp_len > temp_cap) {
+            double *nt = dalloc<double>(std::max<i64>(C->temp_len, 1));
+            if (temp) {
+                LH_CUDA(cudaMemcpyAsync(nt, temp, sizeof(double) * temp_cap, cudaMemcpyDeviceToDevice,
+                                        ctx.stream));
+                LH_CUDA(cudaStreamSynchronize(ctx.stream));
+                cudaFree(temp);
+            }
+            temp = nt;
+            temp_cap = C->temp_len;
+        }
+        C->upload(ctx.stream);
+        C->d_temp = temp;
+        auto t0 = std::chrono::steady_clock::now();
+        try {
+            run_plan(ctx, *C, F, nullptr, nullptr, -1, "hlu");
+        } catch (...) {
+            cudaFree(temp);
+            throw;
+        }
+        exec_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        ++nchunks;
+        ntasks += (i64)C->tasks.size();
+        lk.lock();
+    }
+    lk.unlock();
+    cudaFree(temp);
+    job.f_lu.wait();
+    LH_REQUIRE(job.error.empty(), LH_EINTERNAL, "H-LU planning failed: " + job.error);
+    LH_REQUIRE(ntasks == (i64)job.lu->tasks.size(), LH_EINTERNAL, "streamed H-LU plan incomplete");
+    F.lu_stats[3] = exec_s;
+    F.lu_stats[4] = nchunks;
 }
 
 void hlu(Ctx &ctx, HMat &F, double eps2) {
@@ -1443,15 +1520,41 @@ void hlu(Ctx &ctx, HMat &F, double eps2) {
     i64 perm_len = 0;
     std::shared_ptr<Plan> P;
     PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
-    if (job) {
+    if (job && job->f_lu.valid()) {
+        bool streamed = false;
+        {
+            std::lock_guard<std::mutex> lk(job->lu_stream.mu);
+            if (!job->lu_stream.done && !getenv("LEVYH_NO_STREAM_LU")) {
+                job->lu_stream.engaged = true;
+                streamed = true;
+            }
+        }
+        if (streamed) {
+            // the factor's storage layout is known up front (mark_lu_leaves)
+            F.d_perm = dalloc<int32_t>(std::max<i64>(job->fshadow.perm_len, 1));
+            F.perm_len = job->fshadow.perm_len;
+            F.inv_len = job->fshadow.inv_len;
+            F.d_inv = dalloc<double>(std::max<i64>(F.inv_len, 1));
+            F.factored = true;
+            F.mv_plan.reset();
+            hlu_streamed(ctx, F, eps2, *job);
+            F.nodes = job->shadow.nodes;
+            check_leaf_layout(F, *job);
+            F.sync_ranks(ctx.stream);
+            F.lu_stats[0] = (double)job->lu->tasks.size();
+            F.lu_stats[1] = job->lu->build_seconds;
+            F.lu_stats[2] = (double)job->lu->temp_len * 8.0;
+            job->lu.reset();
+            return;
+        }
         job->f_lu.wait();
         if (job->error.empty() && job->lu) {
-            P = job->lu;
+            P = std::move(job->lu);
             F.nodes = job->shadow.nodes;  // diagonal leaves K_FDENSE with pivot/inverse offsets
             F.inv_len = job->shadow.inv_len;
             perm_len = job->perm_len;
+            check_leaf_layout(F, *job);
             if (eps2 != 1e-10) patch_eps(*P, eps2);
-            P->build_seconds = job->lu->build_seconds;
         }
     }
     if (!P) P = plan_hlu(F, eps2, perm_len);  // marks diagonal leaves K_FDENSE
@@ -1465,6 +1568,7 @@ void hlu(Ctx &ctx, HMat &F, double eps2) {
     auto t0 = std::chrono::steady_clock::now();
     run_plan(ctx, *P, F, nullptr, nullptr, -1, "hlu");
     F.lu_stats[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    F.lu_stats[4] = 1;
     F.sync_ranks(ctx.stream);
     F.lu_stats[0] = (double)P->tasks.size();
     F.lu_stats[1] = P->build_seconds;
@@ -1564,9 +1668,9 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
     int kcap = KA_MAX;  // room for rank + sketch width before recompression
     PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
     bool use_bg = false;
-    if (job) {
+    if (job && job->f_inv.valid()) {
         job->f_inv.wait();
-        use_bg = job->error.empty() && job->inv_error.empty() && job->inv[0] && job->inv[1];
+        use_bg = job->inv_error.empty() && job->inv[0] && job->inv[1];
     }
     for (int mode = 0; mode < 2; ++mode) {
         auto X = std::make_shared<HMat>();
@@ -1612,9 +1716,9 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
     auto Z = std::make_shared<HMat>();
     std::shared_ptr<Plan> P;
-    if (job) {
+    if (job && job->f_prop.valid()) {
         job->f_prop.wait();
-        if (job->error.empty() && job->prop_error.empty() && job->prop) {
+        if (job->prop_error.empty() && job->prop) {
             copy_structure(*Z, job->Z);
             Z->nslots = job->Z.nslots;
             Z->arena_len = job->Z.arena_len;

@@ -15,6 +15,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
+#include <future>
 
 namespace lh {
 
@@ -215,7 +218,45 @@ int32_t Planner::emit(DTask t, std::initializer_list<std::pair<const PView *, bo
     t.dep_cnt = (int32_t)d.size();
     P->deps.insert(P->deps.end(), d.begin(), d.end());
     P->tasks.push_back(t);
+    if (stream && stream->want.load(std::memory_order_relaxed) &&
+        P->tasks.size() - cut_task >= stream->min_chunk)
+        cut_chunk();
     return id;
+}
+
+// tasks [cut_task, end) as a self-contained plan: dependencies on earlier chunks are dropped
+// (those chunks have run), indices are rebased; temp offsets stay global (shared pool)
+void Planner::cut_chunk() {
+    auto C = std::make_shared<Plan>();
+    const int32_t t0 = (int32_t)cut_task, p0 = (int32_t)cut_piece;
+    const int32_t n = (int32_t)P->tasks.size();
+    C->tasks.reserve(n - t0);
+    for (int32_t i = t0; i < n; ++i) {
+        DTask t = P->tasks[i];
+        const int32_t *dp = P->deps.data() + t.dep_beg;
+        const int32_t beg = (int32_t)C->deps.size();
+        for (int32_t k = 0; k < t.dep_cnt; ++k)
+            if (dp[k] >= t0) C->deps.push_back(dp[k] - t0);
+        t.dep_beg = beg;
+        t.dep_cnt = (int32_t)C->deps.size() - beg;
+        t.pc_beg -= p0;
+        t.pc_end -= p0;
+        C->tasks.push_back(t);
+    }
+    C->pieces.assign(P->pieces.begin() + p0, P->pieces.end());
+    C->paths = P->paths;
+    C->temp_len = P->temp_len;
+    C->nslots_total = next_slot;
+    C->slot_off_x = P->slot_off_x;
+    C->slot_off_tmp = P->slot_off_tmp;
+    C->own_temp = false;
+    assign_priorities(*C);
+    cut_task = P->tasks.size();
+    cut_piece = P->pieces.size();
+    std::lock_guard<std::mutex> lk(stream->mu);
+    stream->chunks.push_back(C);
+    stream->want.store(false);
+    stream->cv.notify_all();
 }
 
 static DTask mk(int32_t type) {
@@ -402,10 +443,21 @@ void Planner::solve_dense(const Mref &T, int32_t t, const PView &B, int mode, bo
 }
 
 // hops.py:232-258: T X = B in place on block b of matrix Bm (mode 0 L, 1 U)
+int Planner::colpart(const Mref &M, int32_t b) const {
+    if (!filt || M.base != B_X) return 1;
+    const Node &nd = M.H->nodes[b];
+    const i64 a = nd.c0, e = nd.c0 + nd.n;
+    if (e <= flo || a >= fhi) return 0;
+    return (a >= flo && e <= fhi) ? 1 : 2;
+}
+
 void Planner::trisolve_left(const Mref &T, int32_t t, const Mref &Bm, int32_t b, int mode,
                             bool unit, const std::string &path) {
     const Node &B = Bm.H->nodes[b];
     if (B.kind == K_ZERO) return;
+    const int cp = colpart(Bm, b);
+    if (cp == 0) return;
+    if (cp == 2 && B.kind != K_HIER) throw Error(LH_EINTERNAL, "column split straddles a leaf");
     if (B.kind == K_LR) {
         solve_dense(T, t, u_view(Bm, b), mode, unit, path);
         return;
@@ -619,6 +671,13 @@ void Planner::schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const 
     const Node &B = Bm.H->nodes[b];
     const Node &C = Cm.H->nodes[c];
     if (is_zero(A) || is_zero(B)) return;  // structurally zero operand: no update
+    const int cp = colpart(Cm, c);
+    if (cp == 0) return;
+    if (cp == 2) {  // only the block recursion may cross a column split
+        if (!(C.kind == K_HIER && A.kind == K_HIER && B.kind == K_HIER && A.cs == B.rs &&
+              C.rs == A.rs && C.cs == B.cs))
+            throw Error(LH_EINTERNAL, "column split straddles a product update");
+    }
     if (A.kind == K_LR) {
         PView Av = v_view(Am, a);
         PView W = temp(B.n, Av.d.cols, Av.d.wslot);  // tmul_dense(B, A.v): B^T A.v
@@ -731,9 +790,10 @@ int32_t Planner::add_path(const std::string &s) {
     return (int32_t)P->paths.size() - 1;
 }
 
-// order tasks by weighted ASAP level (critical-path friendly, topological)
-void Planner::finalize() {
-    auto &T = P->tasks;
+// b-level priority classes (critical-path friendly); tasks stay in program order
+// (topological) and the ready-queue executor takes them in readiness order
+void assign_priorities(Plan &P) {
+    auto &T = P.tasks;
     const int32_t n = (int32_t)T.size();
     // estimated microseconds per task incl. ~3 us hand-off (measured on B200, r01)
     auto cost = [&](const DTask &t) -> double {
@@ -750,14 +810,11 @@ void Planner::finalize() {
             default: return 8.0;
         }
     };
-    // Tasks stay in program order (topological); the ready-queue executor takes them in
-    // readiness order, so only the priority classes are computed here.
-    P->nslots_total = next_slot;
     // b-level (cost of the longest path from the task to the end) -> NPRIO buckets
     std::vector<double> bl(n);
     for (int32_t i = 0; i < n; ++i) bl[i] = cost(T[i]);
     for (int32_t i = n - 1; i >= 0; --i) {
-        const int32_t *dp = P->deps.data() + T[i].dep_beg;
+        const int32_t *dp = P.deps.data() + T[i].dep_beg;
         for (int32_t k = 0; k < T[i].dep_cnt; ++k) {
             const int32_t p = dp[k];
             bl[p] = std::max(bl[p], cost(T[p]) + bl[i]);
@@ -765,8 +822,23 @@ void Planner::finalize() {
     }
     double mx = 1e-30;
     for (int32_t i = 0; i < n; ++i) mx = std::max(mx, bl[i]);
-    for (int32_t i = 0; i < n; ++i)
-        T[i].prio = std::min(NPRIO - 1, (int)(NPRIO * bl[i] / mx));
+    for (int32_t i = 0; i < n; ++i) T[i].prio = std::min(NPRIO - 1, (int)(NPRIO * bl[i] / mx));
+}
+
+void Planner::finalize() {
+    P->nslots_total = next_slot;
+    assign_priorities(*P);
+    if (stream) {  // hand the tail to an engaged consumer, then signal completion
+        bool engaged;
+        {
+            std::lock_guard<std::mutex> lk(stream->mu);
+            engaged = stream->engaged;
+        }
+        if (engaged && P->tasks.size() > cut_task) cut_chunk();
+        std::lock_guard<std::mutex> lk(stream->mu);
+        stream->done = true;
+        stream->cv.notify_all();
+    }
 }
 
 // longest dependency chain (in tasks, NOPs excluded); tasks are topologically ordered
@@ -786,10 +858,11 @@ int64_t critical_path(const Plan &P) {
 // ---------------------------------------------------------------------------
 // entry points
 // ---------------------------------------------------------------------------
-std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out) {
+std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out, PlanStream *stream) {
     auto t0 = std::chrono::steady_clock::now();
     Planner pl(F, nullptr);
     pl.eps2 = eps2;
+    pl.stream = stream;
     pl.lu_block(F.root, "root");
     pl.finalize();
     perm_len_out = pl.perm_len;
@@ -845,12 +918,19 @@ std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2) {
 // leaf pivots) while the strict upper triangle of Z is still structurally zero, then
 // Z <- U^{-1} Z on every block.  Same task vocabulary as plan_inverse; the CN step
 // (A+)^{-1} A- = 2 (A+)^{-1} - I then costs one H-matvec of Z.
-std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2) {
-    auto t0 = std::chrono::steady_clock::now();
+// With filt, only the columns [lo, hi) of Z are planned: column blocks of a left solve are
+// independent, so they are planned on separate threads and merged into one DAG.
+static std::shared_ptr<Plan> plan_propagator_part(HMat &F, HMat &Z, double eps2, bool filt,
+                                                  i64 lo, i64 hi, int32_t seed0) {
     Planner pl(F, &Z);
     pl.eps2 = eps2;
+    pl.filt = filt;
+    pl.flo = lo;
+    pl.fhi = hi;
+    pl.rand_seed = seed0;
     Mref Fm{&F, B_F, 0};
     Mref Zm{&Z, B_X, F.nslots};
+    auto in_range = [&](const Node &nd) { return !filt || (nd.c0 >= lo && nd.c0 + nd.n <= hi); };
     std::vector<std::pair<int32_t, int32_t>> upper;  // (block, stored kind) of strict-upper leaves
     for (int32_t b : Z.leafblocks) {
         Node &nd = Z.nodes[b];
@@ -860,7 +940,7 @@ std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2) {
             nd.kind = K_ZERO;
             continue;
         }
-        if (nd.kind == K_DENSE) {
+        if (nd.kind == K_DENSE && in_range(nd)) {
             PView D = pl.dense_view(Zm, b);
             DTask t = mk(T_IDENT);
             t.flags = diag ? 0 : 1;
@@ -872,7 +952,7 @@ std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2) {
     for (auto &u : upper) {  // the upper triangle becomes live storage: zero dense, rank 0
         Node &nd = Z.nodes[u.first];
         nd.kind = u.second;
-        if (nd.kind == K_DENSE) {
+        if (nd.kind == K_DENSE && in_range(nd)) {
             PView D = pl.dense_view(Zm, u.first);
             DTask t = mk(T_IDENT);
             t.flags = 1;
@@ -882,9 +962,171 @@ std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2) {
     }
     pl.trisolve_left(Fm, F.root, Zm, Z.root, 1, false, "root");
     pl.finalize();
-    pl.P->build_seconds =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return pl.P;
+}
+
+static void structure_copy(HMat &D, const HMat &S) {
+    D.rt = S.rt;
+    D.ct = S.ct;
+    D.rt_hold = S.rt_hold;
+    D.ct_hold = S.ct_hold;
+    D.nrows = S.nrows;
+    D.ncols = S.ncols;
+    D.root = S.root;
+    D.nodes = S.nodes;
+    D.leafblocks = S.leafblocks;
+    D.nslots = S.nslots;
+    D.arena_len = S.arena_len;
+}
+
+// concatenation of independent DAGs: task, dependency, piece and path indices and the
+// temp-pool offsets of each part are shifted past the previous parts
+std::shared_ptr<Plan> merge_plans(const std::vector<std::shared_ptr<Plan>> &parts) {
+    auto M = std::make_shared<Plan>();
+    size_t nt = 0, nd = 0, np = 0;
+    for (auto &p : parts) {
+        nt += p->tasks.size();
+        nd += p->deps.size();
+        np += p->pieces.size();
+    }
+    M->tasks.reserve(nt);
+    M->deps.reserve(nd);
+    M->pieces.reserve(np);
+    M->slot_off_x = parts[0]->slot_off_x;
+    M->slot_off_tmp = parts[0]->slot_off_tmp;
+    for (auto &p : parts) {
+        const i64 toff = M->temp_len;
+        const int32_t t0 = (int32_t)M->tasks.size(), d0 = (int32_t)M->deps.size(),
+                      p0 = (int32_t)M->pieces.size(), s0 = (int32_t)M->paths.size();
+        auto fix = [&](DView &v) {
+            if (v.base == B_TMP) v.off += toff;
+        };
+        for (DTask t : p->tasks) {
+            t.dep_beg += d0;
+            t.pc_beg += p0;
+            t.pc_end += p0;
+            if (t.path >= 0) t.path += s0;
+            for (auto &v : t.v) fix(v);
+            M->tasks.push_back(t);
+        }
+        for (int32_t d : p->deps) M->deps.push_back(d + t0);
+        for (DPiece pc : p->pieces) {
+            fix(pc.mat);
+            fix(pc.x);
+            M->pieces.push_back(pc);
+        }
+        M->paths.insert(M->paths.end(), p->paths.begin(), p->paths.end());
+        M->temp_len += p->temp_len;
+        M->nslots_total = std::max(M->nslots_total, p->nslots_total);
+    }
+    return M;
+}
+
+// column ranges of the column clusters `depth` levels below the root (fewer when a leaf
+// cluster is reached first)
+static std::vector<std::pair<i64, i64>> column_blocks(const Tree &T, int depth) {
+    std::vector<int32_t> cur{0};
+    for (int d = 0; d < depth; ++d) {
+        std::vector<int32_t> nxt;
+        for (int32_t c : cur) {
+            if (T.nodes[c].leaf()) return {};
+            nxt.push_back(T.nodes[c].kid[0]);
+            nxt.push_back(T.nodes[c].kid[1]);
+        }
+        cur.swap(nxt);
+    }
+    std::vector<std::pair<i64, i64>> out;
+    for (int32_t c : cur) out.push_back({T.nodes[c].lo, T.nodes[c].lo + T.nodes[c].size()});
+    return out;
+}
+
+std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_parts) {
+    auto t0 = std::chrono::steady_clock::now();
+    std::shared_ptr<Plan> P;
+    if (const char *e = getenv("LEVYH_PROP_PARTS")) max_parts = atoi(e);
+    int depth = 0, parts = 1;
+    while ((2 << depth) <= max_parts) ++depth;
+    // a split `depth` levels down is clean iff no leaf block sits above that depth: then
+    // every leaf, and every product update of a leaf, lies inside one column block
+    std::vector<std::pair<int32_t, int>> st{{Z.root, 0}};
+    while (!st.empty() && depth > 0) {
+        auto [b, d] = st.back();
+        st.pop_back();
+        const Node &nd = Z.nodes[b];
+        if (nd.kind != K_HIER) {
+            depth = std::min(depth, d);
+            continue;
+        }
+        if (d + 1 >= depth) continue;
+        for (int q = 0; q < 4; ++q) st.push_back({nd.kid[q], d + 1});
+    }
+    auto cols = depth > 0 ? column_blocks(*Z.ct, depth) : std::vector<std::pair<i64, i64>>{};
+    if (cols.size() >= 2) {
+        std::vector<HMat> Zs(cols.size());
+        std::vector<std::future<std::shared_ptr<Plan>>> fut;
+        for (size_t k = 0; k < cols.size(); ++k) {
+            structure_copy(Zs[k], Z);
+            fut.push_back(std::async(std::launch::async, [&, k] {
+                auto ts = std::chrono::steady_clock::now();
+                auto r = plan_propagator_part(F, Zs[k], eps2, true, cols[k].first, cols[k].second,
+                                              1 + (int32_t)k * (1 << 24));
+                if (getenv("LEVYH_PLAN_VERBOSE"))
+                    fprintf(stderr, "[levyh]   part %zu: %zu tasks %.3f s\n", k, r->tasks.size(),
+                            std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count());
+                return r;
+            }));
+        }
+        std::vector<std::shared_ptr<Plan>> parts_v;
+        bool ok = true;
+        for (auto &f : fut) {
+            try {
+                parts_v.push_back(f.get());
+            } catch (const std::exception &) {
+                ok = false;  // defensive: the split check above should make this unreachable
+            }
+        }
+        if (ok) {
+            auto tm = std::chrono::steady_clock::now();
+            P = merge_plans(parts_v);
+            parts = (int)parts_v.size();
+            if (getenv("LEVYH_PLAN_VERBOSE"))
+                fprintf(stderr, "[levyh]   merge %.3f s\n",
+                        std::chrono::duration<double>(std::chrono::steady_clock::now() - tm).count());
+        }
+    }
+    if (!P) P = plan_propagator_part(F, Z, eps2, false, 0, 0, 1);
+    P->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (getenv("LEVYH_PLAN_VERBOSE"))
+        fprintf(stderr, "[levyh] propagator plan: %zu tasks, %d column parts, %.3f s\n",
+                P->tasks.size(), parts, P->build_seconds);
+    return P;
+}
+
+// the diagonal-leaf bookkeeping lu_block does while planning (pivot and packed-inverse
+// offsets in recursion order, kind K_FDENSE), without planning: lets every plan that
+// reads the factor start before the H-LU plan exists
+static void mark_rec(HMat &F, int32_t b, i64 &perm_len, i64 &inv_len) {
+    Node &nd = F.nodes[b];
+    if (nd.kind == K_DENSE) {
+        nd.poff = perm_len;
+        perm_len += nd.m;
+        if (nd.m <= LEAF_INV_MAX) {
+            nd.ioff = inv_len;
+            inv_len += nd.m * nd.m;
+        }
+        nd.kind = K_FDENSE;
+        return;
+    }
+    LH_REQUIRE(nd.kind == K_HIER, LH_ETYPE, "cannot LU-factorize a low-rank diagonal block");
+    mark_rec(F, nd.kid[0], perm_len, inv_len);
+    mark_rec(F, nd.kid[3], perm_len, inv_len);
+}
+
+void mark_lu_leaves(HMat &F, i64 &perm_len, i64 &inv_len) {
+    perm_len = inv_len = 0;
+    mark_rec(F, F.root, perm_len, inv_len);
+    F.inv_len = inv_len;
+    F.perm_len = perm_len;
 }
 
 }  // namespace lh

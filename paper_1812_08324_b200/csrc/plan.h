@@ -68,6 +68,7 @@ struct Plan {
     int32_t nslots_total = 0;  // rank slots: F, X, temps
     int32_t slot_off_x = 0, slot_off_tmp = 0;
     int32_t rhs_slot = -1;       // slot holding the run-time RHS width (solve plans)
+    bool own_temp = true;        // false: d_temp is lent by the caller (streamed chunks)
     // device copies
     DTask *d_tasks = nullptr;
     int32_t *d_deps = nullptr;

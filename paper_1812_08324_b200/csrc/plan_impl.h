@@ -1,8 +1,11 @@
 // Planner internals (host only).
 #pragma once
 
+#include <atomic>
+#include <condition_variable>
 #include <deque>
 #include <initializer_list>
+#include <mutex>
 #include <map>
 #include <memory>
 #include <string>
@@ -50,6 +53,19 @@ struct Mref {
 struct LeafRef {
     int32_t b;
     i64 r, c;
+};
+
+// A plan handed over in program-order chunks while the planner is still running: each
+// chunk only depends on itself and on earlier chunks, which have run by the time it starts.
+// Chunks are cut on demand (the consumer sets `want` when it is idle).
+struct PlanStream {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::shared_ptr<Plan>> chunks;
+    bool engaged = false;  // a consumer is taking chunks (set under mu)
+    bool done = false;     // planning finished (set under mu)
+    std::atomic<bool> want{false};
+    size_t min_chunk = 50000;
 };
 
 struct Planner {
@@ -102,16 +118,28 @@ struct Planner {
     void lr_sketch_update(const Mref &Cm, int32_t c, const Mref *Am, int32_t a, const Mref *Bm,
                           int32_t b, const PView *D);
     int32_t rand_seed = 1;
+    // column filter on the target (B_X) matrix: only its blocks with columns in [flo, fhi)
+    // are planned (independent column blocks of a left solve, planned on separate threads)
+    bool filt = false;
+    i64 flo = 0, fhi = 0;
+    int colpart(const Mref &M, int32_t b) const;  // 0 outside, 1 inside, 2 straddles
     PView densify(const Mref &M, int32_t b);
     void schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const Mref &Bm, int32_t b);
     void lu_block(int32_t b, const std::string &path);
     void finalize();
+    PlanStream *stream = nullptr;
+    size_t cut_task = 0, cut_piece = 0;
+    void cut_chunk();
 };
+void assign_priorities(Plan &P);
 
-std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out);
+std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out,
+                               PlanStream *stream = nullptr);
 std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap);
 std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2);
-std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2);
+std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_parts = 8);
+std::shared_ptr<Plan> merge_plans(const std::vector<std::shared_ptr<Plan>> &parts);
+void mark_lu_leaves(HMat &F, i64 &perm_len, i64 &inv_len);
 int64_t critical_path(const Plan &P);
 
 }  // namespace lh

@@ -54,6 +54,39 @@ def test_inverse_solve_matches_substitution(P, name):
     assert _rel(b, g["solve_probe"]) <= 1e-9
 
 
+def test_hlu_streamed_chunks(P, monkeypatch):
+    """H-LU executed in plan chunks while the background planner is still running
+    (N = 2^17 - 1, where planning outlasts assembly) gives the same factor as the
+    one-DAG run, and solves A+ x = b to the eps2-level residual."""
+    n = 1 << 16
+    h = 1.0 / n
+    x = np.random.default_rng(3).standard_normal(2 * n - 1)
+
+    def factor(stream):
+        if stream:
+            monkeypatch.setenv("LEVYH_STREAM_MIN_CHUNK", "2000")
+            monkeypatch.delenv("LEVYH_NO_STREAM_LU", raising=False)
+        else:
+            monkeypatch.setenv("LEVYH_NO_STREAM_LU", "1")
+        s = P.FracCNSystem(P.power_measure(1, 0.5), 0.0, 0.0, 0.0, n, h)
+        cfg = P.HConfig(n_min=64, eps1=1e-10)
+        Hp, _ = s.build_pair(cfg)
+        F = P.hlu(Hp, 1e-10)
+        st = np.zeros(5)
+        P._lib.check(P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st)))
+        return s, cfg, F, st
+
+    s, cfg, F1, st1 = factor(True)
+    assert st1[4] >= 2, st1  # ran as more than one chunk
+    _, _, F0, st0 = factor(False)
+    assert st0[4] == 1
+    x1 = P.solve(F1, x, method="substitution")
+    x0 = P.solve(F0, x, method="substitution")
+    assert _rel(x1, x0) <= 1e-12
+    Ap = s.hmatrix("plus", cfg)
+    assert _rel(P.matvec(Ap, x1), x) <= 1e-8
+
+
 @pytest.mark.parametrize("name", NAMES)
 def test_propagator_solve(P, name):
     g = cases.load(name)
