@@ -1,12 +1,18 @@
-// H-matvec y = H x (hops.py:50-70) as a two-phase HBM-streaming kernel pair.
+// H-matvec y = alpha H x + beta z (hops.py:50-70) as a two-phase HBM-streaming kernel pair.
 //
-// Phase 1: for every low-rank block b, partial products t_b = V_b^T x over
-//          fixed column chunks (deterministic; no atomics).
-// Phase 2: one CTA per row segment (<= 64 rows of a leaf cluster) accumulates
-//          every dense piece D x and every low-rank piece U_b[seg,:] t_b that
-//          covers the segment, and writes y[seg] once.
-// The same plan type serves the CN operator H-, and the triangular-inverse
-// factors of the fast solve.
+// Phase 1 (vtx_kernel): for every low-rank block b, t_b = V_b^T x, one warp per <= 1024-row
+//          chunk of V_b (chunk partials reduced by treduce_kernel; deterministic, no atomics);
+//          tscatter_kernel then copies t_b once per row segment the block covers,
+//          segment-ordered (tseg), so a segment's t values are contiguous.
+// Phase 2: every row segment (<= 64 rows of a leaf cluster) accumulates its dense pieces D x
+//          and its low-rank pieces U_b[seg, :] t_b and writes y[seg] once.
+//          seg_tma_kernel: persistent, one CTA per SM over a byte-balanced contiguous range
+//          of segments; a producer lane streams piece-aligned batches (<= 32 KB) of the
+//          packed operands with cp.async.bulk into a 5-stage shared-memory ring (full/empty
+//          mbarriers), together with each batch's piece descriptors, t_b span and x slice;
+//          eight consumer warps compute from shared memory.
+//          seg_kernel: the same per-segment work with direct loads (LEVYH_SEG_DIRECT=1).
+// The operands are gathered once per plan into a packed buffer in streaming order.
 #include <algorithm>
 #include <map>
 
@@ -23,29 +29,40 @@ constexpr int SEG = 64;         // rows per segment
 constexpr int GRP = NT / SEG;   // thread groups per segment
 constexpr i64 VCHUNK = 1024;    // rows of V per phase-1 chunk (one warp)
 #ifndef SEG_MIN_BLOCKS
-#define SEG_MIN_BLOCKS 4        // CTAs per SM for the segment kernel (5-6 spill and lose ~10%)
+#define SEG_MIN_BLOCKS 4        // CTAs per SM for the direct-load segment kernel
 #endif
+constexpr int TMA_STAGES = 5;
+constexpr int SLOT_D = 4096;    // doubles of operand data per ring slot (32 KB)
+constexpr int SLOT_A = 1024;    // doubles of aux (descriptors, t_b span, x slice) per slot
+constexpr int DESC_D = 64;      // aux doubles reserved for piece descriptors (32 x 16 B)
+constexpr int MAX_PIECES = 32;  // pieces per batch
+constexpr int TMA_CONS = 512;             // consumer threads: 64 rows x 8 column groups
+constexpr int TGRP = TMA_CONS / SEG;
+constexpr int TMA_THREADS = TMA_CONS + 32;  // one producer warp + 16 consumer warps
 
-// Phase 1: each CTA owns one chunk of rows of one V_b; every thread accumulates all
-// r columns for its rows (x[i] read once, r independent coalesced loads per row),
-// then a CTA reduction writes the chunk's r partial sums.
+// ---------------------------------------------------------------------------
+// phase 1
+// ---------------------------------------------------------------------------
+// one warp per chunk: each lane accumulates all r columns for its rows (x[i] read once,
+// r independent coalesced loads per row, two rows in flight), then warp shuffles reduce
 template <int RB>
-__device__ __forceinline__ void vtx_warp(const VChunk &C, int r, const double *arena, const double *x,
+__device__ __forceinline__ void vtx_warp(const VChunk &C, const double *pbuf, const double *x,
                                          double *out, int lane) {
-    const double *V = arena + C.voff;
+    const int r = C.r;
+    const double *V = pbuf + C.voff;
     const double *xx = x + C.xc0;
+    const i64 ld = C.len;
     double acc[RB];
 #pragma unroll
     for (int c = 0; c < RB; ++c) acc[c] = 0.0;
     int i = lane;
-    // two rows per iteration: 2 (r + 1) independent loads in flight before the FMAs
     for (; i + 32 < C.len; i += 64) {
         const double x0 = xx[i], x1 = xx[i + 32];
         double v0[RB], v1[RB];
 #pragma unroll
         for (int c = 0; c < RB; ++c) {
-            v0[c] = c < r ? V[i + (i64)c * C.ld] : 0.0;
-            v1[c] = c < r ? V[i + 32 + (i64)c * C.ld] : 0.0;
+            v0[c] = c < r ? V[i + c * ld] : 0.0;
+            v1[c] = c < r ? V[i + 32 + c * ld] : 0.0;
         }
 #pragma unroll
         for (int c = 0; c < RB; ++c) acc[c] += v0[c] * x0 + v1[c] * x1;
@@ -54,7 +71,7 @@ __device__ __forceinline__ void vtx_warp(const VChunk &C, int r, const double *a
         const double xi = xx[i];
 #pragma unroll
         for (int c = 0; c < RB; ++c)
-            if (c < r) acc[c] += V[i + (i64)c * C.ld] * xi;
+            if (c < r) acc[c] += V[i + c * ld] * xi;
     }
 #pragma unroll
     for (int c = 0; c < RB; ++c)
@@ -62,74 +79,84 @@ __device__ __forceinline__ void vtx_warp(const VChunk &C, int r, const double *a
             const double v = dev::warp_sum(acc[c]);
             if (lane == 0) out[c] = v;
         }
-    // ranks above RB (stale plan or rare large ranks): remaining columns one at a time
+    // ranks above RB: remaining columns one at a time
     for (int c = RB; c < r; ++c) {
-        const double *v = V + (i64)c * C.ld;
+        const double *v = V + c * ld;
         double s = 0.0;
-        for (int i = lane; i < C.len; i += 32) s += v[i] * xx[i];
+        for (int q = lane; q < C.len; q += 32) s += v[q] * xx[q];
         s = dev::warp_sum(s);
         if (lane == 0) out[c] = s;
     }
 }
 
-// Phase 1: one warp per chunk (<= VCHUNK rows of one V_b); each lane accumulates all r
-// columns for its rows (x[i] read once, r independent coalesced loads per row), then
-// warp shuffles reduce: no block barriers, so small blocks cost little.
-// The plan splits chunks by the rank seen at plan time: RB = 8 (32-register kernel, 8 CTAs
-// per SM) or RB = 16.  A chunk that covers its whole block writes t_b directly (C.out >= 0);
-// chunks of multi-chunk blocks write partials, reduced by treduce_kernel.
 template <int RB>
 __global__ void __launch_bounds__(NT, (RB <= 8 ? 6 : 4))
-    vtx_kernel(const VChunk *chunks, int nch, const double *arena, const int *ranks,
-               const double *x, double *part, double *tvec) {
+    vtx_kernel(const VChunk *chunks, int nch, const double *pbuf, const double *x, double *part,
+               double *tvec) {
     const int lane = threadIdx.x & 31;
     for (int q = blockIdx.x * dev::NW + (threadIdx.x >> 5); q < nch; q += gridDim.x * dev::NW) {
         const VChunk C = chunks[q];
-        const int r = ranks[C.slot];
-        double *out = C.tout >= 0 ? tvec + C.tout : part + (i64)C.pidx * KC_MAX;
-        vtx_warp<RB>(C, r, arena, x, out, lane);
+        double *out = C.pidx >= 0 ? part + (i64)C.pidx * KC_MAX : tvec + (i64)C.blk * KC_MAX;
+        vtx_warp<RB>(C, pbuf, x, out, lane);
     }
 }
 
-// t_b[c] = sum of the chunk partials of a multi-chunk block b (one warp per block,
-// fixed order: deterministic)
-__global__ void treduce_kernel(const TJob *jobs, int njobs, const int *ranks, const double *part,
-                               double *tvec) {
+// t_b[c] = sum of the chunk partials of a multi-chunk block (one warp per block, fixed order)
+__global__ void treduce_kernel(const TJob *jobs, int njobs, const double *part, double *tvec) {
     const int lane = threadIdx.x & 31;
     for (int j = blockIdx.x * dev::NW + (threadIdx.x >> 5); j < njobs; j += gridDim.x * dev::NW) {
         const TJob J = jobs[j];
-        const int r = ranks[J.slot];
-        for (int c = 0; c < r; ++c) {
+        double mine = 0.0;
+        for (int c = 0; c < J.r; ++c) {
             double t = 0.0;
             for (int k = J.cbeg + lane; k < J.cend; k += 32) t += part[(i64)k * KC_MAX + c];
             t = dev::warp_sum(t);
-            if (lane == 0) tvec[(i64)J.slot * KC_MAX + c] = t;
+            if (lane == c) mine = t;
+        }
+        if (lane < J.r) tvec[(i64)J.blk * KC_MAX + lane] = mine;
+    }
+}
+
+// TMA kernel inputs: batch-ordered low-rank coefficients tcol[e] = tvec[tmap[e]], and x
+// copied into an aligned buffer with two doubles of zero padding (16-byte bulk copies)
+__global__ void tgather_kernel(const int32_t *tmap, i64 n, const double *tvec, double *tcol,
+                               const double *x, i64 nx, double *xpad) {
+    for (i64 e = (i64)blockIdx.x * NT + threadIdx.x; e < n + nx + 2; e += (i64)gridDim.x * NT) {
+        if (e < n) {
+            const int32_t m = tmap[e];
+            tcol[e] = m >= 0 ? tvec[m] : 0.0;
+        } else {
+            const i64 i = e - n;
+            xpad[i] = i < nx ? x[i] : 0.0;
         }
     }
 }
 
-__global__ void __launch_bounds__(NT, SEG_MIN_BLOCKS) seg_kernel(const SegDesc *segs, int nseg, const MvDense *dp,
-                                                 const MvLr *lp, const double *arena,
-                                                 const int *ranks, const double *tvec,
-                                                 const double *x, double *y, double alpha,
-                                                 double beta, const double *z) {
+// ---------------------------------------------------------------------------
+// phase 2, direct loads
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT, SEG_MIN_BLOCKS)
+    seg_kernel(const SegDesc *segs, int nseg, const MvDense *dp, const MvLr *lp, const double *pbuf,
+               const double *tvec, const double *x, double *y, double alpha, double beta,
+               const double *z) {
     __shared__ double acc_s[GRP][SEG];
     const int row = threadIdx.x % SEG, g = threadIdx.x / SEG;
     for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
         const SegDesc S = segs[s];
+        const i64 ld = S.ld;
         double acc = 0.0;
         if (row < S.rows) {
-            // dense pieces: D[row, j] x[j], columns split over the GRP groups; a full
-            // 64-column piece issues its 16 loads per thread before any FMA
+            // dense pieces: columns split over the GRP groups; a full 64-column piece issues
+            // its 16 loads per thread before any FMA
             for (int p = S.dbeg; p < S.dend; ++p) {
                 const MvDense P = dp[p];
-                const double *D = arena + P.off + row;
+                const double *D = pbuf + P.off + row;
                 const double *xx = x + P.xc0;
                 if (P.ncols == 64) {
                     double d[16], xv[16];
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
-                        d[q] = D[(i64)(g + GRP * q) * P.ld];
+                        d[q] = D[(g + GRP * q) * ld];
                         xv[q] = xx[g + GRP * q];
                     }
                     double a0 = 0.0, a1 = 0.0;
@@ -143,48 +170,43 @@ __global__ void __launch_bounds__(NT, SEG_MIN_BLOCKS) seg_kernel(const SegDesc *
                     double a0 = 0.0, a1 = 0.0;
                     int j = g;
                     for (; j + GRP < P.ncols; j += 2 * GRP) {
-                        a0 += D[(i64)j * P.ld] * xx[j];
-                        a1 += D[(i64)(j + GRP) * P.ld] * xx[j + GRP];
+                        a0 += D[j * ld] * xx[j];
+                        a1 += D[(j + GRP) * ld] * xx[j + GRP];
                     }
-                    if (j < P.ncols) a0 += D[(i64)j * P.ld] * xx[j];
+                    if (j < P.ncols) a0 += D[j * ld] * xx[j];
                     acc += a0 + a1;
                 }
             }
-            // low-rank pieces: U[row, :] t_b (t_b precomputed, read through L1); four
-            // pieces at a time so their descriptor -> rank -> U load chains overlap
+            // low-rank pieces, four at a time so their descriptor -> U load chains overlap
             int p = S.lbeg;
             for (; p + 4 <= S.lend; p += 4) {
                 MvLr Q[4];
-                int r[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) Q[k] = lp[p + k];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) r[k] = ranks[Q[k].slot];
                 double u0[4], u1[4], t0[4], t1[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const double *U = arena + Q[k].off + row;
-                    const double *tb = tvec + (i64)Q[k].slot * KC_MAX;
-                    u0[k] = g < r[k] ? U[(i64)g * Q[k].ld] : 0.0;
-                    t0[k] = g < r[k] ? tb[g] : 0.0;
-                    u1[k] = g + GRP < r[k] ? U[(i64)(g + GRP) * Q[k].ld] : 0.0;
-                    t1[k] = g + GRP < r[k] ? tb[g + GRP] : 0.0;
+                    const double *U = pbuf + Q[k].off + row;
+                    const double *tb = tvec + (i64)Q[k].blk * KC_MAX;
+                    u0[k] = g < Q[k].r ? U[g * ld] : 0.0;
+                    t0[k] = g < Q[k].r ? tb[g] : 0.0;
+                    u1[k] = g + GRP < Q[k].r ? U[(g + GRP) * ld] : 0.0;
+                    t1[k] = g + GRP < Q[k].r ? tb[g + GRP] : 0.0;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc += u0[k] * t0[k] + u1[k] * t1[k];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const double *U = arena + Q[k].off + row;
-                    const double *tb = tvec + (i64)Q[k].slot * KC_MAX;
-                    for (int c = g + 2 * GRP; c < r[k]; c += GRP) acc += U[(i64)c * Q[k].ld] * tb[c];
+                    const double *U = pbuf + Q[k].off + row;
+                    const double *tb = tvec + (i64)Q[k].blk * KC_MAX;
+                    for (int c = g + 2 * GRP; c < Q[k].r; c += GRP) acc += U[c * ld] * tb[c];
                 }
             }
             for (; p < S.lend; ++p) {
                 const MvLr P = lp[p];
-                const int r = ranks[P.slot];
-                const double *U = arena + P.off + row;
-                const double *tb = tvec + (i64)P.slot * KC_MAX;
-                for (int c = g; c < r; c += GRP) acc += U[(i64)c * P.ld] * tb[c];
+                const double *U = pbuf + P.off + row;
+                const double *tb = tvec + (i64)P.blk * KC_MAX;
+                for (int c = g; c < P.r; c += GRP) acc += U[c * ld] * tb[c];
             }
         }
         acc_s[g][row] = acc;
@@ -200,31 +222,218 @@ __global__ void __launch_bounds__(NT, SEG_MIN_BLOCKS) seg_kernel(const SegDesc *
 }
 
 // ---------------------------------------------------------------------------
+// phase 2, bulk-copy (TMA) pipeline
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {  // the consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(TMA_CONS) : "memory");
+}
+
+constexpr int XOFF = 0;    // aux: x slice (<= 66 doubles)
+constexpr int TOFF = 128;  // aux: low-rank coefficients (<= SLOT_D / 2 columns)
+static_assert(TOFF + SLOT_D / 2 <= SLOT_A + SLOT_D, "aux layout");
+
+struct TmaSmem {
+    double data[TMA_STAGES][SLOT_D];
+    double aux[TMA_STAGES][TOFF + 64];
+    double red[TGRP][SEG];
+    uint64_t full[TMA_STAGES], empty[TMA_STAGES];
+    int32_t hdr[TMA_STAGES][4];  // K, kd, xadj
+};
+constexpr size_t TMA_SMEM = sizeof(TmaSmem) + 128;
+
+__global__ void __launch_bounds__(TMA_THREADS, 1)
+    seg_tma_kernel(const SegDesc *segs, const int32_t *cta_seg, const SBatch *batches,
+                   const double *pbuf, const double *tcol, const double *x, double *y,
+                   double alpha, double beta, const double *z) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TmaSmem &S = *reinterpret_cast<TmaSmem *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < TMA_STAGES; ++i) {
+            mbar_init(&S.full[i], 1);
+            mbar_init(&S.empty[i], TMA_CONS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int s0 = cta_seg[blockIdx.x], s1 = cta_seg[blockIdx.x + 1];
+    if (warp == 0) {
+        // producer: lane 0 walks this CTA's batches with a 4-deep register queue of
+        // descriptors (loads in flight ahead of use) and issues the bulk copies,
+        // TMA_STAGES slots ahead of the consumers
+        if (lane == 0 && s0 < s1) {
+            const int b0 = segs[s0].bbeg, b1 = segs[s1 - 1].bend;
+            int stage = 0;
+            uint32_t phase = 0;
+            SBatch q0 = batches[b0];
+            SBatch q1 = b0 + 1 < b1 ? batches[b0 + 1] : q0;
+            SBatch q2 = b0 + 2 < b1 ? batches[b0 + 2] : q0;
+            SBatch q3 = b0 + 3 < b1 ? batches[b0 + 3] : q0;
+            for (int b = b0; b < b1; ++b) {
+                const SBatch B = q0;
+                q0 = q1;
+                q1 = q2;
+                q2 = q3;
+                if (b + 4 < b1) q3 = batches[b + 4];
+                mbar_wait(&S.empty[stage], phase ^ 1);
+                S.hdr[stage][0] = B.K;
+                S.hdr[stage][1] = B.kd;
+                S.hdr[stage][2] = B.xadj;
+                mbar_expect_tx(&S.full[stage], (uint32_t)B.total);
+                const uint32_t tb = (uint32_t)(8 * ((B.K - B.kd + 1) & ~1));
+                const uint32_t xb = B.kd ? (uint32_t)(8 * ((B.xadj + B.kd + 1) & ~1)) : 0u;
+                bulk_g2s(S.data[stage], pbuf + B.src, (uint32_t)B.total - tb - xb, &S.full[stage]);
+                if (tb) bulk_g2s(S.aux[stage] + TOFF, tcol + B.tsrc, tb, &S.full[stage]);
+                if (xb) bulk_g2s(S.aux[stage] + XOFF, x + B.xsrc, xb, &S.full[stage]);
+                if (++stage == TMA_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        return;
+    }
+    // consumers: 64 rows x 8 column groups; group g takes columns g, g + 8, ... of each batch
+    const int tid = threadIdx.x - 32, row = tid % SEG, g = tid / SEG;
+    int stage = 0;
+    uint32_t phase = 0;
+    SegDesc sd = s0 < s1 ? segs[s0] : SegDesc{};
+    for (int s = s0; s < s1; ++s) {
+        const SegDesc cur = sd;
+        if (s + 1 < s1) sd = segs[s + 1];  // prefetch
+        const int ld = cur.ld;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int b = cur.bbeg; b < cur.bend; ++b) {
+            mbar_wait(&S.full[stage], phase);
+            const int K = S.hdr[stage][0], kd = S.hdr[stage][1], xadj = S.hdr[stage][2];
+            const double *col = S.data[stage] + row;
+            // dense columns [0, kd) against the x slice, low-rank columns [kd, K) against t
+            {
+                const double *cf = S.aux[stage] + XOFF + xadj;
+                int k = g;
+                for (; k + 3 * TGRP < kd; k += 4 * TGRP) {
+                    const double c0 = cf[k], c1 = cf[k + TGRP], c2 = cf[k + 2 * TGRP], c3 = cf[k + 3 * TGRP];
+                    const double m0 = col[k * ld], m1 = col[(k + TGRP) * ld];
+                    const double m2 = col[(k + 2 * TGRP) * ld], m3 = col[(k + 3 * TGRP) * ld];
+                    a0 += m0 * c0;
+                    a1 += m1 * c1;
+                    a2 += m2 * c2;
+                    a3 += m3 * c3;
+                }
+                for (; k < kd; k += TGRP) a0 += col[k * ld] * cf[k];
+            }
+            {
+                const double *cf = S.aux[stage] + TOFF - kd;
+                int k = kd + g;
+                for (; k + 3 * TGRP < K; k += 4 * TGRP) {
+                    const double c0 = cf[k], c1 = cf[k + TGRP], c2 = cf[k + 2 * TGRP], c3 = cf[k + 3 * TGRP];
+                    const double m0 = col[k * ld], m1 = col[(k + TGRP) * ld];
+                    const double m2 = col[(k + 2 * TGRP) * ld], m3 = col[(k + 3 * TGRP) * ld];
+                    a0 += m0 * c0;
+                    a1 += m1 * c1;
+                    a2 += m2 * c2;
+                    a3 += m3 * c3;
+                }
+                for (; k < K; k += TGRP) a1 += col[k * ld] * cf[k];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[stage]);
+            if (++stage == TMA_STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        S.red[g][row] = (a0 + a1) + (a2 + a3);
+        consumer_sync();
+        if (g == 0 && row < cur.rows) {
+            double v = S.red[0][row];
+            for (int q = 1; q < TGRP; ++q) v += S.red[q][row];
+            const i64 i = cur.y0 + row;
+            y[i] = (beta == 0.0 ? 0.0 : beta * z[i]) + alpha * v;
+        }
+        consumer_sync();
+    }
+}
+
+// gather the operands into the packed buffer (once per plan)
+__global__ void pack_kernel(const PackJob *jobs, int njobs, const double *arena, double *pbuf) {
+    for (int j = blockIdx.x; j < njobs; j += gridDim.x) {
+        const PackJob J = jobs[j];
+        const i64 n = (i64)J.rows * J.cols;
+        for (i64 e = threadIdx.x; e < n; e += NT) {
+            const i64 c = e / J.rows, i = e - c * J.rows;
+            pbuf[J.dst + i + c * J.ld] = arena[J.src + i + c * J.src_ld];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // plan construction
 // ---------------------------------------------------------------------------
-// Builds a plan over the given leaf blocks (default: all of H).  Row segments are
-// the leaf clusters of the row tree split into <= SEG rows.
-std::shared_ptr<MvPlan> build_mv_plan(const HMat &H, const std::vector<int32_t> &blocks,
-                                      cudaStream_t s) {
+static i64 even(i64 v) { return (v + 1) & ~i64(1); }
+
+// Builds a plan over the given leaf blocks (default: all of H).  Row segments are the leaf
+// clusters of the row tree split into <= SEG rows.
+std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &blocks, cudaStream_t s) {
     auto P = std::make_shared<MvPlan>();
+    H.sync_ranks(s);  // the packed layout is sized by the current ranks
     const Tree &rt = *H.rt;
-    // segments
     std::vector<i64> seg_start;
     for (int32_t lc : rt.leaves) {
         const Cluster &c = rt.nodes[lc];
         for (i64 a = c.lo; a < c.hi; a += SEG) seg_start.push_back(a);
     }
     seg_start.push_back(rt.n);
-    int nseg = (int)seg_start.size() - 1;
+    const int nseg = (int)seg_start.size() - 1;
     auto seg_of = [&](i64 row) {
         return (int)(std::upper_bound(seg_start.begin(), seg_start.end(), row) - seg_start.begin()) - 1;
     };
-    std::vector<std::vector<MvDense>> dps(nseg);
-    std::vector<std::vector<MvLr>> lps(nseg);
+    struct DRef {
+        i64 src, ld, xc0;
+        int32_t ncols;
+    };
+    struct LRef {
+        i64 src, ld;
+        int32_t r, blk;
+    };
+    std::vector<std::vector<DRef>> dps(nseg);
+    std::vector<std::vector<LRef>> lps(nseg);
     std::vector<VChunk> chunks, chunks16;
+    std::vector<i64> vld, vld16;  // source ld (block row count of V) per chunk
     std::vector<TJob> tjobs;
-    int32_t max_slot = -1;
-    int npart = 0;
+    int nblk = 0, npart = 0;
     for (int32_t b : blocks) {
         const Node &nd = H.nodes[b];
         if (nd.kind == K_DENSE || nd.kind == K_FDENSE) {
@@ -232,97 +441,240 @@ std::shared_ptr<MvPlan> build_mv_plan(const HMat &H, const std::vector<int32_t> 
                 i64 a = std::max(seg_start[sg], nd.r0), e = std::min(seg_start[sg + 1], nd.r0 + nd.m);
                 LH_REQUIRE(a == seg_start[sg] && e == seg_start[sg + 1], LH_EINTERNAL,
                            "dense block not aligned with row segments");
+                LH_REQUIRE(nd.n <= 64, LH_EINTERNAL, "dense matvec pieces are at most 64 columns");
                 dps[sg].push_back({nd.doff + (a - nd.r0), nd.m, nd.c0, (int32_t)nd.n});
             }
         } else if (nd.kind == K_LR) {
-            const bool big_rank = nd.rslot < (int32_t)H.h_ranks.size() ? H.h_ranks[nd.rslot] > 8 : true;
-            std::vector<VChunk> &dst = big_rank ? chunks16 : chunks;
+            const int r = H.h_ranks[nd.rslot];
+            LH_REQUIRE(r <= KC_MAX, LH_EINTERNAL, "rank above the matvec capacity");
+            if (r == 0) continue;
+            const int blk = nblk++;
+            std::vector<VChunk> &dst = r > 8 ? chunks16 : chunks;
+            std::vector<i64> &dld = r > 8 ? vld16 : vld;
             if (nd.n <= VCHUNK) {
-                dst.push_back({nd.voff, nd.n, nd.c0, (int32_t)nd.n, nd.rslot,
-                               (i64)nd.rslot * KC_MAX, -1, 0});
+                dst.push_back({nd.voff, nd.c0, (int32_t)nd.n, r, blk, -1});
+                dld.push_back(nd.n);
             } else {
                 int cb = npart;
                 for (i64 a = 0; a < nd.n; a += VCHUNK) {
                     int len = (int)std::min(VCHUNK, nd.n - a);
-                    dst.push_back({nd.voff + a, nd.n, nd.c0 + a, len, nd.rslot, -1, npart++, 0});
+                    dst.push_back({nd.voff + a, nd.c0 + a, len, r, blk, npart++});
+                    dld.push_back(nd.n);
                 }
-                tjobs.push_back({nd.rslot, cb, npart});
+                tjobs.push_back({blk, r, cb, npart});
             }
-            max_slot = std::max(max_slot, nd.rslot);
             for (int sg = seg_of(nd.r0); sg < nseg && seg_start[sg] < nd.r0 + nd.m; ++sg) {
                 i64 a = std::max(seg_start[sg], nd.r0), e = std::min(seg_start[sg + 1], nd.r0 + nd.m);
                 LH_REQUIRE(a == seg_start[sg] && e == seg_start[sg + 1], LH_EINTERNAL,
                            "low-rank block not aligned with row segments");
-                lps[sg].push_back({nd.uoff + (a - nd.r0), nd.m, nd.rslot, 0, 0});
+                lps[sg].push_back({nd.uoff + (a - nd.r0), nd.m, r, blk});
             }
         }
     }
+    // packed layout (columns of ld = even(rows)) + bulk-copy batches of <= SLOT_D doubles,
+    // at most one dense piece per batch and only as its first columns
+    std::vector<PackJob> jobs;
     std::vector<SegDesc> segs(nseg);
     std::vector<MvDense> dall;
     std::vector<MvLr> lall;
+    std::vector<SBatch> batches;
+    std::vector<int32_t> tmap;
+    std::vector<i64> seg_bytes(nseg, 0);
+    i64 poff = 0;
     for (int sg = 0; sg < nseg; ++sg) {
         SegDesc &S = segs[sg];
         S.y0 = seg_start[sg];
         S.rows = (int32_t)(seg_start[sg + 1] - seg_start[sg]);
+        S.ld = (int32_t)even(S.rows);
+        const i64 ld = S.ld;
+        const int kmax = (int)(SLOT_D / ld);
         S.dbeg = (int32_t)dall.size();
-        dall.insert(dall.end(), dps[sg].begin(), dps[sg].end());
-        S.dend = (int32_t)dall.size();
         S.lbeg = (int32_t)lall.size();
-        lall.insert(lall.end(), lps[sg].begin(), lps[sg].end());
+        S.bbeg = (int32_t)batches.size();
+        SBatch B{};
+        auto close = [&]() {
+            if (B.K == 0) return;
+            const i64 tb = 8 * even(B.K - B.kd), xb = B.kd ? 8 * even(B.xadj + B.kd) : 0;
+            B.total = (int32_t)(8 * B.K * ld + tb + xb);
+            batches.push_back(B);
+            seg_bytes[sg] += B.total;
+            B = SBatch{};
+        };
+        auto open = [&]() {
+            B = SBatch{};
+            B.src = poff;
+            B.tsrc = (i64)tmap.size();
+        };
+        open();
+        for (const DRef &d : dps[sg]) {
+            if (B.K > 0) {  // a dense piece always starts a batch
+                close();
+                open();
+            }
+            jobs.push_back({d.src, d.ld, poff, S.rows, d.ncols, S.ld, 0});
+            dall.push_back({poff, d.xc0, d.ncols, 0});
+            B.K = B.kd = d.ncols;
+            B.xsrc = d.xc0 & ~i64(1);
+            B.xadj = (int32_t)(d.xc0 - B.xsrc);
+            poff += (i64)d.ncols * ld;
+        }
+        for (const LRef &l : lps[sg]) {
+            if (B.K + l.r > kmax) {
+                close();
+                open();
+            }
+            jobs.push_back({l.src, l.ld, poff, S.rows, l.r, S.ld, 0});
+            lall.push_back({poff, l.r, l.blk});
+            for (int c = 0; c < l.r; ++c) tmap.push_back(l.blk * KC_MAX + c);
+            B.K += l.r;
+            poff += (i64)l.r * ld;
+        }
+        close();
+        // every batch's coefficient span starts 16-byte aligned in tcol
+        if (tmap.size() & 1) tmap.push_back(-1);
+        S.dend = (int32_t)dall.size();
         S.lend = (int32_t)lall.size();
+        S.bend = (int32_t)batches.size();
+    }
+    // batches opened mid-segment took tsrc before alignment padding of the previous segment
+    // only at segment starts; within a segment they are contiguous: re-derive aligned spans
+    {
+        std::vector<int32_t> tm2;
+        for (int sg = 0; sg < nseg; ++sg)
+            for (int b = segs[sg].bbeg; b < segs[sg].bend; ++b) {
+                SBatch &B = batches[b];
+                const i64 nlr = B.K - B.kd;
+                const i64 from = B.tsrc;
+                B.tsrc = (i64)tm2.size();
+                for (i64 e = 0; e < nlr; ++e) tm2.push_back(tmap[from + e]);
+                if (tm2.size() & 1) tm2.push_back(-1);
+            }
+        tmap.swap(tm2);
+    }
+    for (int k = 0; k < 2; ++k) {
+        std::vector<VChunk> &cv = k ? chunks16 : chunks;
+        const std::vector<i64> &ld = k ? vld16 : vld;
+        for (size_t q = 0; q < cv.size(); ++q) {
+            VChunk &c = cv[q];
+            jobs.push_back({c.voff, ld[q], poff, c.len, c.r, c.len, 0});
+            c.voff = poff;
+            poff += even((i64)c.len * c.r);
+        }
+    }
+    // TMA kernel: contiguous, byte-balanced segment ranges, one CTA per SM
+    int dev_id = 0, num_sms = 148;
+    cudaGetDevice(&dev_id);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev_id);
+    const int G = std::max(1, std::min(num_sms, nseg));
+    std::vector<int32_t> cta_seg(G + 1, nseg);
+    {
+        i64 total = 0;
+        for (i64 v : seg_bytes) total += v;
+        cta_seg[0] = 0;
+        i64 accb = 0;
+        int c = 1;
+        for (int sg = 0; sg < nseg && c < G; ++sg) {
+            accb += seg_bytes[sg];
+            while (c < G && accb * G >= total * c) cta_seg[c++] = sg + 1;
+        }
+        for (; c < G; ++c) cta_seg[c] = nseg;
+        cta_seg[G] = nseg;
     }
     P->nseg = nseg;
     P->nch = (int)chunks.size();
     P->nch16 = (int)chunks16.size();
+    P->ntj = (int)tjobs.size();
+    P->nbatch = (int)batches.size();
+    P->tma_grid = G;
+    P->pbuf_len = poff;
+    P->pbuf = dalloc<double>(std::max<i64>(poff, 2));
+    LH_CUDA(cudaMemsetAsync(P->pbuf, 0, sizeof(double) * std::max<i64>(poff, 2), s));  // pad rows
+    P->tcol_len = (i64)tmap.size();
+    P->tcol = dalloc<double>(std::max<i64>(P->tcol_len, 2));
+    P->tmap = dupload(tmap, s);
+    P->tvec = dalloc<double>((i64)std::max(nblk, 1) * KC_MAX);
+    P->nx = H.ncols;
+    P->xpad = dalloc<double>(H.ncols + 2);
     P->segs = dupload(segs, s);
     P->dp = dupload(dall, s);
     P->lp = dupload(lall, s);
     P->chunks = dupload(chunks, s);
     P->chunks16 = dupload(chunks16, s);
-    P->part = dalloc<double>((i64)std::max(npart, 1) * KC_MAX);
-    P->ntj = (int)tjobs.size();
     P->tjobs = dupload(tjobs, s);
-    P->tvec = dalloc<double>((i64)(max_slot + 1 > 0 ? max_slot + 1 : 1) * KC_MAX);
+    P->part = dalloc<double>((i64)std::max(npart, 1) * KC_MAX);
+    P->batches = dupload(batches, s);
+    P->cta_seg = dupload(cta_seg, s);
     P->n_dpieces = (i64)dall.size();
     P->n_lpieces = (i64)lall.size();
+    if (!jobs.empty()) {
+        PackJob *dj = dupload(jobs, s);
+        pack_kernel<<<std::min<int>((int)jobs.size(), 148 * 16), NT, 0, s>>>(dj, (int)jobs.size(),
+                                                                            H.d_arena, P->pbuf);
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(s));
+        cudaFree(dj);
+    }
     LH_CUDA(cudaStreamSynchronize(s));
     return P;
 }
 
 MvPlan::~MvPlan() {
+    cudaFree(pbuf);
+    cudaFree(tcol);
+    cudaFree(tmap);
+    cudaFree(xpad);
     cudaFree(segs);
     cudaFree(dp);
     cudaFree(lp);
     cudaFree(chunks);
     cudaFree(chunks16);
-    cudaFree(part);
     cudaFree(tjobs);
+    cudaFree(part);
     cudaFree(tvec);
+    cudaFree(batches);
+    cudaFree(cta_seg);
 }
 
-// phase 1 (V^T x partials) + t_b reduction
+// phase 1 (V^T x per chunk) + t_b reduction of multi-chunk blocks
 void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int grid, cudaStream_t s) {
+    (void)H;
     if (P.nch > 0) {
         int g = std::max(1, std::min(grid, (P.nch + dev::NW - 1) / dev::NW));
-        vtx_kernel<8><<<g, NT, 0, s>>>(P.chunks, P.nch, H.d_arena, H.d_ranks, x, P.part, P.tvec);
+        vtx_kernel<8><<<g, NT, 0, s>>>(P.chunks, P.nch, P.pbuf, x, P.part, P.tvec);
     }
     if (P.nch16 > 0) {
         int g = std::max(1, std::min(grid, (P.nch16 + dev::NW - 1) / dev::NW));
-        vtx_kernel<16><<<g, NT, 0, s>>>(P.chunks16, P.nch16, H.d_arena, H.d_ranks, x, P.part, P.tvec);
+        vtx_kernel<16><<<g, NT, 0, s>>>(P.chunks16, P.nch16, P.pbuf, x, P.part, P.tvec);
     }
     if (P.ntj > 0) {
         int g = std::max(1, std::min(148 * 8, (P.ntj + dev::NW - 1) / dev::NW));
-        treduce_kernel<<<g, NT, 0, s>>>(P.tjobs, P.ntj, H.d_ranks, P.part, P.tvec);
+        treduce_kernel<<<g, NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
     }
 }
 
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
                    double beta, cudaStream_t s, int num_sms, const double *z) {
-    // (A one-warp-per-32-rows variant without shared memory measured slower on B200:
-    // 370 vs 384 steps/s at 128 registers, 331 when capped to 64 with spills.)
+    (void)H;
+    static const bool direct = getenv("LEVYH_SEG_DIRECT") != nullptr;
+    if (!direct && P.nbatch > 0) {
+        static bool attr = false;
+        if (!attr) {
+            LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
+            attr = true;
+        }
+        const i64 n = P.tcol_len + P.nx + 2;
+        int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
+        tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x, P.nx, P.xpad);
+        seg_tma_kernel<<<P.tma_grid, TMA_THREADS, TMA_SMEM, s>>>(P.segs, P.cta_seg, P.batches, P.pbuf,
+                                                                P.tcol, P.xpad, y, alpha, beta,
+                                                                z ? z : y);
+        return;
+    }
+    // (A one-warp-per-32-rows variant without shared memory measured slower on B200.)
     int g2 = std::min(P.nseg, num_sms * 32);
-    seg_kernel<<<g2, NT, 0, s>>>(P.segs, P.nseg, P.dp, P.lp, H.d_arena, H.d_ranks, P.tvec, x, y,
-                                 alpha, beta, z ? z : y);
+    seg_kernel<<<g2, NT, 0, s>>>(P.segs, P.nseg, P.dp, P.lp, P.pbuf, P.tvec, x, y, alpha, beta,
+                                 z ? z : y);
 }
 
 // y = alpha * H x + beta * z (z = y when null) for one right-hand side

@@ -8,47 +8,74 @@
 
 namespace lh {
 
+// All operand offsets below index the plan's packed buffer (MvPlan::pbuf), which holds the
+// operands in the order the kernels stream them: per segment its dense pieces then the U
+// rows of its low-rank pieces, as COLUMNS of ld = even(rows) doubles (pad rows zero), then
+// every V chunk.  A segment is therefore a sequence of columns, each with one coefficient:
+// x[xc0 + j] for column j of a dense piece, t_b[c] for column c of a low-rank piece.
 struct SegDesc {
     i64 y0;
-    int32_t rows;
-    int32_t dbeg, dend;
-    int32_t lbeg, lend;
+    int32_t rows, ld;
+    int32_t dbeg, dend;  // dense pieces (MvDense)
+    int32_t lbeg, lend;  // low-rank pieces (MvLr)
+    int32_t bbeg, bend;  // bulk-copy batches (SBatch)
 };
-struct MvDense {  // element (i, j) of the piece = arena[off + i + j * ld], multiplies x[xc0 + j]
-    i64 off, ld, xc0;
-    int32_t ncols;
+struct MvDense {  // element (i, j) = pbuf[off + i + j * ld], multiplies x[xc0 + j]
+    i64 off, xc0;
+    int32_t ncols, pad;
 };
-struct MvLr {  // U rows of the piece at arena[off + i + c * ld]; t_b from chunk partials [cbeg, cend)
-    i64 off, ld;
-    int32_t slot, cbeg, cend;
+struct MvLr {  // U rows at pbuf[off + i + c * ld], c < r; t_b = tvec[blk * KC_MAX + c]
+    i64 off;
+    int32_t r, blk;
 };
-struct VChunk {  // V rows at arena[voff + i + c * ld], i < len, multiplies x[xc0 + i]
-    i64 voff, ld, xc0;
-    int32_t len, slot;
-    i64 tout;      // >= 0: whole block in this chunk, write t_b at tvec[tout]
-    int32_t pidx;  // else: partial row index
-    int32_t pad;
+struct VChunk {  // V rows at pbuf[voff + i + c * len], i < len, c < r, multiplies x[xc0 + i]
+    i64 voff, xc0;
+    int32_t len, r;
+    int32_t blk;   // the block's row of tvec (t_b = tvec[blk * KC_MAX + c])
+    int32_t pidx;  // < 0: the chunk is the whole block (write t_b); else partial row index
 };
-
-struct TJob {  // t_b = sum of the partials of chunks [cbeg, cend) of the block in rank slot `slot`
-    int32_t slot, cbeg, cend;
+struct TJob {  // t_b = sum of the partials of chunks [cbeg, cend), written to tvec row blk
+    int32_t blk, r, cbeg, cend;
+};
+// TMA segment kernel: a batch is K consecutive columns of one segment (K * ld <= one ring
+// slot); the first kd of them belong to a dense piece (coefficients = an x slice), the rest to
+// low-rank pieces (coefficients = tcol[tsrc .. tsrc + K - kd), gathered from tvec per step).
+struct SBatch {
+    i64 src;     // pbuf offset (doubles, even) of the batch's columns
+    i64 tsrc;    // tcol offset (even) of the low-rank coefficients
+    i64 xsrc;    // x element offset (even) of the x slice (kd > 0)
+    int32_t K, kd, xadj, total;  // columns, dense columns, x[xc0] at slice[xadj], bytes in flight
+};
+struct PackJob {  // pbuf[dst + i + j * ld] = arena[src + i + j * src_ld], i < rows
+    i64 src, src_ld, dst;
+    int32_t rows, cols;
+    int32_t ld, pad;
 };
 
 struct MvPlan {
-    int nseg = 0, nch = 0, nch16 = 0, ntj = 0;
-    VChunk *chunks16 = nullptr;  // chunks whose block rank exceeded 8 at plan time
-    TJob *tjobs = nullptr;
-    double *tvec = nullptr;  // KC_MAX per rank slot
-    i64 n_dpieces = 0, n_lpieces = 0;
+    int nseg = 0, nch = 0, nch16 = 0, ntj = 0, nbatch = 0, tma_grid = 0;
+    double *pbuf = nullptr;  // packed operands
+    i64 pbuf_len = 0;
+    double *tvec = nullptr;  // t_b per low-rank block, KC_MAX per block
+    double *tcol = nullptr;  // batch-ordered low-rank column coefficients (TMA kernel)
+    int32_t *tmap = nullptr; // tcol[e] = tvec[tmap[e]] (-1: padding)
+    i64 tcol_len = 0;
+    double *xpad = nullptr;  // aligned, zero-padded copy of x (TMA kernel)
+    i64 nx = 0;
     SegDesc *segs = nullptr;
     MvDense *dp = nullptr;
     MvLr *lp = nullptr;
     VChunk *chunks = nullptr;
+    VChunk *chunks16 = nullptr;  // chunks of blocks with rank > 8
+    TJob *tjobs = nullptr;
     double *part = nullptr;
+    SBatch *batches = nullptr;
+    int32_t *cta_seg = nullptr;  // TMA kernel: segments [cta_seg[c], cta_seg[c+1]) per CTA
+    i64 n_dpieces = 0, n_lpieces = 0;
     ~MvPlan();
 };
 
-std::shared_ptr<MvPlan> build_mv_plan(const HMat &H, const std::vector<int32_t> &blocks,
+std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &blocks,
                                       cudaStream_t s);
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
             cudaStream_t s, int num_sms, const double *z = nullptr);
