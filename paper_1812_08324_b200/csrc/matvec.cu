@@ -441,8 +441,10 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
                 i64 a = std::max(seg_start[sg], nd.r0), e = std::min(seg_start[sg + 1], nd.r0 + nd.m);
                 LH_REQUIRE(a == seg_start[sg] && e == seg_start[sg + 1], LH_EINTERNAL,
                            "dense block not aligned with row segments");
-                LH_REQUIRE(nd.n <= 64, LH_EINTERNAL, "dense matvec pieces are at most 64 columns");
-                dps[sg].push_back({nd.doff + (a - nd.r0), nd.m, nd.c0, (int32_t)nd.n});
+                // pieces of at most 64 columns (one ring slot with ld <= 64)
+                for (i64 j0 = 0; j0 < nd.n; j0 += 64)
+                    dps[sg].push_back({nd.doff + (a - nd.r0) + j0 * nd.m, nd.m, nd.c0 + j0,
+                                       (int32_t)std::min<i64>(64, nd.n - j0)});
             }
         } else if (nd.kind == K_LR) {
             const int r = H.h_ranks[nd.rslot];

@@ -12,6 +12,7 @@ CASES = {
     "cfg2_s075": (("power", 0.75), 1.0, 1024, 2.0),
     "cfg3_cgmy": (("cgmy", 1.0, 5.0, 10.0, 0.5), 4.0, 512, 8.0),
     "cfg5_s08": (("power", 0.8), 1.0, 512, 2.0),
+    "cfg5_leaf128": (("power", 0.8), 1.0, 1024, 2.0),  # cfg5's leaf size (128)
 }
 
 

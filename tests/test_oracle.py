@@ -8,7 +8,7 @@ import pytest
 
 from oracle import levyh_oracle as O
 
-CASES = ["cfg1", "cfg2_s025", "cfg2_s075", "cfg3_cgmy", "cfg5_s08"]
+CASES = ["cfg1", "cfg2_s025", "cfg2_s075", "cfg3_cgmy", "cfg5_s08", "cfg5_leaf128"]
 
 
 def _load(golden_dir, name):
@@ -24,7 +24,8 @@ def _case_symbol(name, g, golden_dir):
         tail = float(sc["tail"])
         L_W = 8.0
     else:
-        s = {"cfg1": 0.5, "cfg2_s025": 0.25, "cfg2_s075": 0.75, "cfg5_s08": 0.8}[name]
+        s = {"cfg1": 0.5, "cfg2_s025": 0.25, "cfg2_s075": 0.75, "cfg5_s08": 0.8,
+             "cfg5_leaf128": 0.8}[name]
         nu = O.nu_power(s)
         L_W = 2.0
         tail = O.tail_power(s, L_W)

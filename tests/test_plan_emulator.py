@@ -11,7 +11,7 @@ from tests import cases
 from tests import plan_emulator as E
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg3_cgmy"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg3_cgmy", "cfg5_leaf128"])
 def test_planned_dags_match_oracle(name, tmp_path):
     import paper_1812_08324_b200 as P
     from paper_1812_08324_b200 import _lib
