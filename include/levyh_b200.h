@@ -132,6 +132,20 @@ int lh_hlu(lh_ctx *ctx, lh_hmat *h, double eps2);
  * 2 = propagator (one H-matvec of Z = (LU)^-1). */
 int lh_solve(lh_ctx *ctx, lh_hmat *factor, double *b_dev, int64_t ldb, int32_t nrhs,
              int32_t method);
+/* hops.py:282-310 trisolve_lower / trisolve_upper_right with a dense right-hand side:
+ * T X = B in place on B (n x nrhs, col-major, ldb == n) using one triangle of T:
+ * mode 0 lower (unit_diagonal = unit), 1 upper, 2 upper transposed (X U = B^T is solved as
+ * U^T X^T = B^T by the caller).  LU-factored leaves use their LU (unit L with pivots);
+ * a plain dense leaf with a zero diagonal entry fails with LH_ESINGULAR and the message
+ * "singular triangular diagonal block at L.11..." (hops.py:179-182). */
+int lh_trisolve_dense(lh_ctx *ctx, lh_hmat *t, int32_t mode, int32_t unit, double *b_dev,
+                      int64_t ldb, int32_t nrhs);
+/* hops.py:147-156 lowrank_add_recompress: (u_out, v_out) = recompressed u1 v1^T + u2 v2^T,
+ * smallest rank r with ||tail||_F <= eps2 ||sum||_F (QR, QR, SVD).  Device, column-major,
+ * ld = m (u) / n (v); outputs hold r1 + r2 <= 48 columns; *r_out = r. */
+int lh_lowrank_add_recompress(lh_ctx *ctx, int64_t m, int64_t n, const double *u1, const double *v1,
+                              int32_t r1, const double *u2, const double *v2, int32_t r2,
+                              double eps2, double *u_out, double *v_out, int32_t *r_out);
 /* Precompute the triangular-inverse factors used by method 1. */
 int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *factor, double eps2);
 /* Precompute the propagator Z = (LU)^-1 as an H-matrix on the factor's block tree

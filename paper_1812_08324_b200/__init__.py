@@ -15,7 +15,8 @@ from .geometry import (ClusterNode, ClusterTree, Permutation, PointSet, admissib
 from .hmatrix import (HConfig, HMatrix, build_from_dense, build_toeplitz, derive_toeplitz,  # noqa: F401
                       dump_structure, export_blocks, h_entry, memory_report, structure_summary,
                       to_dense)
-from .hops import SOLVE_METHODS, HFactorization, hlu, matvec, mul_dense, solve  # noqa: F401
+from .hops import (SOLVE_METHODS, HFactorization, hlu, lowrank_add_recompress, matvec,  # noqa: F401
+                   mul_dense, solve, trisolve_lower, trisolve_upper_right)
 from .levy import FracCNSystem, run_cn, step_cn  # noqa: F401
 
 __version__ = "0.1.0"

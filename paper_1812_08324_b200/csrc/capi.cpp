@@ -29,6 +29,10 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2);
 void propagator_stats(HMat &F, double *out);
 int step_graph_kernels(HMat &F);
+void trisolve_dense(Ctx &ctx, HMat &T, int mode, bool unit, double *b, i64 ldb, int nrhs);
+int lowrank_add_recompress(Ctx &ctx, i64 m, i64 n, const double *u1, const double *v1, int r1,
+                           const double *u2, const double *v2, int r2, double eps2, double *uo,
+                           double *vo);
 void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
 void start_background_plans(HMat &H);
 
@@ -445,6 +449,19 @@ int lh_propagator_stats(lh_hmat *f, double *out) {
 }
 
 int32_t lh_step_graph_kernels(lh_hmat *f) { return step_graph_kernels(f->h); }
+
+int lh_trisolve_dense(lh_ctx *ctx, lh_hmat *t, int32_t mode, int32_t unit, double *b, int64_t ldb,
+                      int32_t nrhs) {
+    return guard(ctx, [&] { trisolve_dense(ctx->c, t->h, mode, unit != 0, b, ldb, nrhs); });
+}
+
+int lh_lowrank_add_recompress(lh_ctx *ctx, int64_t m, int64_t n, const double *u1, const double *v1,
+                              int32_t r1, const double *u2, const double *v2, int32_t r2,
+                              double eps2, double *u_out, double *v_out, int32_t *r_out) {
+    return guard(ctx, [&] {
+        *r_out = lowrank_add_recompress(ctx->c, m, n, u1, v1, r1, u2, v2, r2, eps2, u_out, v_out);
+    });
+}
 
 int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t ldu, int32_t nrhs,
                 int32_t nsteps, int32_t method) {

@@ -530,7 +530,11 @@ __device__ void task_getrf(const ExecArgs &A, const DTask &T, int tid, double *s
 // TRSM with a factored leaf: mode 0 unit-L with the leaf permutation, 1 U, 2 U^T
 // (dtrsm in _leaf_solve, hops.py:185-208)
 // ---------------------------------------------------------------------------
-__device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
+// generic TRSM (any m whose triangle fits shared memory): flags = mode | unit << 4 |
+// pivots << 5 | packed-inverse << 6 | check-diagonal << 7.  Mode 0 solves with the lower
+// triangle (unit or not, leaf pivots applied to B for LU-factored leaves), 1 with the upper
+// triangle, 2 with its transpose (_leaf_solve, hops.py:191-208).
+__device__ void task_trsm(const ExecArgs &A, const DTask &T, int tid, double *sm) {
     if (T.flags & 64) {
         task_trsm_fast(A, T, sm);
         return;
@@ -545,20 +549,37 @@ __device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
     if (k <= 0) return;
     double *Ts = sm;
     double *Bs = sm + m * m;
+    const bool unit = T.flags & 16, pivots = T.flags & 32;
     const int32_t *perm = A.perm + T.aux;
     for (int e = threadIdx.x; e < m * m; e += NT) Ts[e] = Tg[vi(tv, e % m, e / m)];
+    if (T.flags & 128) {  // _check_triangular_leaf (hops.py:179-182): zero on the diagonal
+        __shared__ int s_zero;
+        if (threadIdx.x == 0) s_zero = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += NT)
+            if (Ts[i + i * m] == 0.0) s_zero = 1;
+        __syncthreads();
+        if (s_zero) {
+            if (threadIdx.x == 0) set_err(A, LH_ESINGULAR, tid, T.path);
+            return;
+        }
+    }
     const int CW = 32;
     for (int c0 = 0; c0 < k; c0 += CW) {
         const int kc = min(CW, k - c0);
         __syncthreads();
         for (int e = threadIdx.x; e < m * kc; e += NT) {
             int i = e % m, c = e / m;
-            int src = (mode == 0) ? perm[i] : i;
+            int src = (mode == 0 && pivots) ? perm[i] : i;
             Bs[e] = Bg[vi(bv, src, c0 + c)];
         }
         __syncthreads();
         if (mode == 0) {
-            for (int l = 0; l < m - 1; ++l) {
+            for (int l = 0; l < m - 1 + (unit ? 0 : 1); ++l) {
+                if (!unit) {
+                    for (int c = threadIdx.x; c < kc; c += NT) Bs[l + c * m] /= Ts[l + l * m];
+                    __syncthreads();
+                }
                 const int rem = m - l - 1;
                 for (int e = threadIdx.x; e < rem * kc; e += NT) {
                     int i = l + 1 + e % rem, c = e / rem;
@@ -568,8 +589,10 @@ __device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
             }
         } else if (mode == 1) {
             for (int l = m - 1; l >= 0; --l) {
-                for (int c = threadIdx.x; c < kc; c += NT) Bs[l + c * m] /= Ts[l + l * m];
-                __syncthreads();
+                if (!unit) {
+                    for (int c = threadIdx.x; c < kc; c += NT) Bs[l + c * m] /= Ts[l + l * m];
+                    __syncthreads();
+                }
                 for (int e = threadIdx.x; e < l * kc; e += NT) {
                     int i = e % l, c = e / l;
                     Bs[i + c * m] -= Ts[i + l * m] * Bs[l + c * m];
@@ -578,8 +601,10 @@ __device__ void task_trsm(const ExecArgs &A, const DTask &T, double *sm) {
             }
         } else {
             for (int l = 0; l < m; ++l) {
-                for (int c = threadIdx.x; c < kc; c += NT) Bs[l + c * m] /= Ts[l + l * m];
-                __syncthreads();
+                if (!unit) {
+                    for (int c = threadIdx.x; c < kc; c += NT) Bs[l + c * m] /= Ts[l + l * m];
+                    __syncthreads();
+                }
                 const int rem = m - l - 1;
                 for (int e = threadIdx.x; e < rem * kc; e += NT) {
                     int i = l + 1 + e % rem, c = e / rem;
@@ -1109,7 +1134,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
         if (A.times && threadIdx.x == 0) A.times[2 * t] = gtimer();
         switch (T.type) {
             case T_GETRF: task_getrf(A, T, t, sm); break;
-            case T_TRSM: task_trsm(A, T, sm); break;
+            case T_TRSM: task_trsm(A, T, t, sm); break;
             case T_SEGMUL: task_segmul(A, T, sm); break;
             case T_VTX: task_vtx(A, T, sm); break;
             case T_LRADD: task_lradd(A, T, t, sm); break;
@@ -1586,6 +1611,7 @@ struct SolvePlans {
     bool pair_ok = false;
     int g_method = -1;
     int g_kernels = 0;  // kernel nodes in the cached step graph
+    std::shared_ptr<Plan> tri[3][2];  // dense-RHS triangular solves by (mode, unit)
     double *tmp = nullptr;          // scratch vector(s)
     i64 tmp_len = 0;
     cudaGraphExec_t graph = nullptr;  // cached CN step
@@ -1813,6 +1839,83 @@ static void solve_inverse(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
         mv_run(*S.mvL, *S.XL, bq, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
         mv_run(*S.mvU, *S.XU, S.tmp, bq, 1.0, 0.0, ctx.stream, ctx.num_sms);
     }
+}
+
+// trisolve_lower / trisolve_upper_right with a dense right-hand side (hops.py:282-310):
+// T X = B with one triangle of T (mode 0 lower, 1 upper, 2 upper transposed), in place
+void trisolve_dense(Ctx &ctx, HMat &T, int mode, bool unit, double *b, i64 ldb, int nrhs) {
+    LH_REQUIRE(T.nrows == T.ncols, LH_EINVAL, "triangular solve needs a square H-matrix");
+    LH_REQUIRE(mode >= 0 && mode <= 2, LH_EINVAL, "mode must be 0 (L), 1 (U) or 2 (U^T)");
+    LH_REQUIRE(ldb == T.nrows, LH_EINVAL, "solve expects a packed right-hand side (ldb == n)");
+    if (nrhs <= 0) return;
+    SolvePlans &S = plans_of(T);
+    const int CAP = 64;
+    auto &P = S.tri[mode][unit ? 1 : 0];
+    if (!P) {
+        P = plan_trisolve_dense(T, T.nrows, CAP, mode, unit, mode == 0 ? "L" : "U");
+        P->upload(ctx.stream);
+    }
+    for (int c0 = 0; c0 < nrhs; c0 += CAP) {
+        const int kc = std::min(CAP, nrhs - c0);
+        run_plan(ctx, *P, T, nullptr, b + (i64)c0 * ldb, kc, "trisolve");
+    }
+}
+
+// lowrank_add_recompress (hops.py:147-156): (u, v) <- recompressed u1 v1^T + u2 v2^T with the
+// Frobenius-tail rule at eps2, as one LRADD task on the executor.  Device, column-major
+// factors (ld = m resp. n); outputs need r1 + r2 columns; the new rank is returned.
+int lowrank_add_recompress(Ctx &ctx, i64 m, i64 n, const double *u1, const double *v1, int r1,
+                           const double *u2, const double *v2, int r2, double eps2, double *uo,
+                           double *vo) {
+    LH_REQUIRE(m > 0 && n > 0 && r1 >= 0 && r2 >= 0, LH_EINVAL, "invalid low-rank shapes");
+    LH_REQUIRE(r1 + r2 <= KA_MAX, LH_ERANK, "r1 + r2 exceeds the recompression width");
+    if (r2 == 0) {  // the task recompresses the target plus a non-empty addend
+        std::swap(u1, u2);
+        std::swap(v1, v2);
+        std::swap(r1, r2);
+    }
+    if (r2 == 0) return 0;
+    const int kcap = r1 + r2;
+    HMat W;
+    const i64 uo_off = 0, vo_off = m * kcap, u2_off = vo_off + n * kcap, v2_off = u2_off + m * r2;
+    W.arena_len = v2_off + n * r2;
+    W.d_arena = dalloc<double>(W.arena_len);
+    W.nslots = 1;
+    W.d_ranks = dalloc<int32_t>(1);
+    cudaStream_t s = ctx.stream;
+    if (r1 > 0) {
+        LH_CUDA(cudaMemcpyAsync(W.d_arena + uo_off, u1, sizeof(double) * m * r1, cudaMemcpyDeviceToDevice, s));
+        LH_CUDA(cudaMemcpyAsync(W.d_arena + vo_off, v1, sizeof(double) * n * r1, cudaMemcpyDeviceToDevice, s));
+    }
+    LH_CUDA(cudaMemcpyAsync(W.d_arena + u2_off, u2, sizeof(double) * m * r2, cudaMemcpyDeviceToDevice, s));
+    LH_CUDA(cudaMemcpyAsync(W.d_arena + v2_off, v2, sizeof(double) * n * r2, cudaMemcpyDeviceToDevice, s));
+    LH_CUDA(cudaMemcpyAsync(W.d_ranks, &r1, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    Plan P;
+    DTask t;
+    std::memset(&t, 0, sizeof(t));
+    for (auto &v : t.v) v.wslot = -1;
+    t.type = T_LRADD;
+    t.path = -1;
+    t.alpha = 1.0;
+    t.alpha2 = eps2;
+    t.v[0] = DView{uo_off, (int32_t)m, kcap, (int32_t)m, 0, B_F, 0, 0};
+    t.v[1] = DView{vo_off, (int32_t)n, kcap, (int32_t)n, 0, B_F, 0, 0};
+    t.v[2] = DView{u2_off, (int32_t)m, r2, (int32_t)m, -1, B_F, 0, 0};
+    t.v[3] = DView{v2_off, (int32_t)n, r2, (int32_t)n, -1, B_F, 0, 0};
+    P.tasks.push_back(t);
+    P.nslots_total = 1;
+    P.slot_off_x = 1;
+    P.slot_off_tmp = 1;
+    P.upload(s);
+    run_plan(ctx, P, W, nullptr, nullptr, -1, "lowrank_add_recompress");
+    W.sync_ranks(s);
+    const int r = W.h_ranks[0];
+    if (r > 0) {
+        LH_CUDA(cudaMemcpyAsync(uo, W.d_arena + uo_off, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, s));
+        LH_CUDA(cudaMemcpyAsync(vo, W.d_arena + vo_off, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, s));
+    }
+    LH_CUDA(cudaStreamSynchronize(s));
+    return r;
 }
 
 void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method) {

@@ -410,17 +410,25 @@ void Planner::solve_dense(const Mref &T, int32_t t, const PView &B, int mode, bo
                           const std::string &path) {
     const Node &nd = T.H->nodes[t];
     if (nd.kind != K_HIER) {
-        LH_REQUIRE(nd.kind == K_FDENSE, LH_ETYPE,
-                   "triangular solve needs an LU-factored diagonal leaf at " + path);
+        LH_REQUIRE(nd.kind == K_FDENSE || nd.kind == K_DENSE, LH_ETYPE,
+                   "triangular solve needs a dense diagonal leaf at " + path);
         PView Tv = dense_view(T, t);
         DTask k = mk(T_TRSM);
-        k.flags = mode | (unit ? 16 : 0) | 32;
-        k.aux = (int32_t)nd.poff;
         k.v[0] = Tv.d;
         k.v[1] = B.d;
-        if (nd.ioff >= 0) {  // apply the packed leaf inverse written by the leaf's GETRF
-            k.flags |= 64;
-            k.v[2] = DView{nd.ioff, (int32_t)nd.m, (int32_t)nd.m, (int32_t)nd.m, -1, B_INV, 0, 0};
+        if (nd.kind == K_FDENSE) {
+            // _leaf_solve on a FactoredDense leaf: unit L with the leaf pivots, non-unit U
+            k.flags = mode | (mode == 0 ? 16 : 0) | 32;
+            k.aux = (int32_t)nd.poff;
+            if (nd.ioff >= 0) {  // apply the packed leaf inverse written by the leaf's GETRF
+                k.flags |= 64;
+                k.v[2] = DView{nd.ioff, (int32_t)nd.m, (int32_t)nd.m, (int32_t)nd.m, -1, B_INV, 0, 0};
+            }
+        } else {
+            // plain dense triangle (trisolve_lower / trisolve_upper_right on an unfactored
+            // H-matrix): zero diagonal raises with the block path (hops.py:179-182)
+            k.flags = mode | (unit ? 16 : 0) | 128;
+            k.path = add_path("singular triangular diagonal block at " + path);
         }
         emit(k, {{&Tv, false}, {&B, true}});
         return;
@@ -883,6 +891,24 @@ std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap) {
     B.obj = pl.key(B_RHS, 0, 0);
     pl.solve_dense(Fm, F.root, B, 0, true, "root");
     pl.solve_dense(Fm, F.root, B, 1, false, "root");
+    pl.finalize();
+    pl.P->build_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return pl.P;
+}
+
+// T X = B for a dense right-hand side, one triangle of T (hops.py:282-310 trisolve_lower /
+// trisolve_upper_right on dense B): mode 0 lower, 1 upper, 2 upper transposed
+std::shared_ptr<Plan> plan_trisolve_dense(HMat &T, i64 n, int nrhs_cap, int mode, bool unit,
+                                          const std::string &root) {
+    auto t0 = std::chrono::steady_clock::now();
+    Planner pl(T, nullptr);
+    Mref Tm{&T, B_F, 0};
+    PView B{};
+    pl.P->rhs_slot = pl.new_slot();
+    B.d = DView{0, (int32_t)n, nrhs_cap, (int32_t)n, pl.P->rhs_slot, B_RHS, 0, 0};
+    B.obj = pl.key(B_RHS, 0, 0);
+    pl.solve_dense(Tm, T.root, B, mode, unit, root);
     pl.finalize();
     pl.P->build_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -10,6 +10,7 @@ dataflow kernel (csrc/lu.cu); ``solve`` applies forward/backward substitution
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -17,7 +18,8 @@ import numpy as np
 from . import _lib
 from .hmatrix import HMatrix
 
-__all__ = ["matvec", "mul_dense", "hlu", "HFactorization", "solve"]
+__all__ = ["matvec", "mul_dense", "hlu", "HFactorization", "solve", "trisolve_lower",
+           "trisolve_upper_right", "lowrank_add_recompress"]
 
 SOLVE_METHODS = {"substitution": 0, "inverse": 1, "propagator": 2}
 
@@ -129,3 +131,91 @@ def solve(F: HFactorization, b, method="substitution"):
     _lib.check(_lib.lib().lh_solve(ctx.h, F.h.handle, bc.data_ptr(), F.h.n_rows, k, m), ctx.h)
     out = bc.t().reshape(shape)
     return out if was_torch else out.cpu().numpy()
+
+
+def _tri_solve(T, B, mode, unit):
+    Th = T.h if isinstance(T, HFactorization) else T
+    if not isinstance(Th, HMatrix):
+        raise TypeError("triangular operand must be an HMatrix or HFactorization")
+    if not (isinstance(B, np.ndarray) or _is_torch(B)):
+        raise NotImplementedError("block (HMatrix) right-hand sides are not supported; "
+                                  "pass a dense array")
+    ctx = Th.ctx
+    bt, was_torch = _to_device(B, ctx)
+    return Th, ctx, bt, was_torch
+
+
+def _is_torch(x):
+    try:
+        import torch
+        return isinstance(x, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def trisolve_lower(L, B, unit_diagonal=False):
+    """hops.py:282-295: solve L X = B with the lower triangle of L (dense B, (n,) or (n, k)).
+
+    LU-factored diagonal leaves use their unit-L factor and pivots; plain dense leaves use
+    their lower triangle (unit diagonal if requested) and raise LinAlgError("singular
+    triangular diagonal block at L...") on a zero diagonal entry.  B is not modified."""
+    Th, ctx, bt, was_torch = _tri_solve(L, B, 0, unit_diagonal)
+    if bt.shape[0] != Th.n_rows:
+        raise ValueError("right-hand side length mismatch")
+    shape = bt.shape
+    bc, k = _colmajor(bt.reshape(shape[0], -1))
+    bc = bc.clone()
+    _lib.check(_lib.lib().lh_trisolve_dense(ctx.h, Th.handle, 0, int(bool(unit_diagonal)),
+                                            bc.data_ptr(), Th.n_rows, k), ctx.h)
+    out = bc.t().reshape(shape)
+    return out if was_torch else out.cpu().numpy()
+
+
+def trisolve_upper_right(U, B, unit_diagonal=False):
+    """hops.py:298-310: solve X U = B with the upper triangle of U, as U^T X^T = B^T
+    (dense B of shape (m, n), or (n,) for one row)."""
+    Th, ctx, bt, was_torch = _tri_solve(U, B, 2, unit_diagonal)
+    n = Th.n_rows
+    rows = bt.reshape(1, -1) if bt.ndim == 1 else bt.reshape(bt.shape[0], -1)
+    if rows.shape[1] != n:
+        raise ValueError("right-hand side width mismatch")
+    bc = rows.contiguous().clone()  # (m, n) row-major == n x m column-major (B^T)
+    k = rows.shape[0]
+    _lib.check(_lib.lib().lh_trisolve_dense(ctx.h, Th.handle, 2, int(bool(unit_diagonal)),
+                                            bc.data_ptr(), n, k), ctx.h)
+    out = bc.reshape(bt.shape)
+    return out if was_torch else out.cpu().numpy()
+
+
+def lowrank_add_recompress(A, B, eps2):
+    """hops.py:147-156: A + B recompressed (QR of [u1 u2], QR of [v1 v2], SVD of R_u R_v^T;
+    smallest rank with Frobenius tail <= eps2 * ||A + B||_F), on the GPU.  A and B are
+    LowRank (u: m x r, v: n x r); returns a LowRank of the same array type."""
+    import torch
+
+    from .hmatrix import LowRank
+
+    if tuple(A.shape) != tuple(B.shape):
+        raise ValueError("shape mismatch in low-rank addition")
+    ctx = _lib.Context.get()
+    m, n = A.shape
+    was_torch = _is_torch(A.u)
+
+    def dev(a):
+        t, _ = _to_device(a, ctx)
+        return t.reshape(t.shape[0], -1).t().contiguous()  # column-major storage
+
+    u1, v1, u2, v2 = dev(A.u), dev(A.v), dev(B.u), dev(B.v)
+    r1, r2 = u1.shape[0], u2.shape[0]
+    cap = max(r1 + r2, 1)
+    uo = torch.zeros((cap, m), dtype=torch.float64, device=u1.device)
+    vo = torch.zeros((cap, n), dtype=torch.float64, device=u1.device)
+    r = C.c_int32(0)
+    _lib.check(_lib.lib().lh_lowrank_add_recompress(ctx.h, m, n, u1.data_ptr(), v1.data_ptr(), r1,
+                                                    u2.data_ptr(), v2.data_ptr(), r2, float(eps2),
+                                                    uo.data_ptr(), vo.data_ptr(), C.byref(r)), ctx.h)
+    rr = r.value
+    u, v = uo[:rr].t(), vo[:rr].t()
+    if not was_torch:
+        u, v = u.cpu().numpy(), v.cpu().numpy()
+    return LowRank(u, v)
