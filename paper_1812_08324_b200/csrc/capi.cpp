@@ -36,6 +36,20 @@ int lowrank_add_recompress(Ctx &ctx, i64 m, i64 n, const double *u1, const doubl
 void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
 void start_background_plans(HMat &H);
 
+double *DevBuf::ensure(i64 n) {
+    if (n > cap) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        p = dalloc<double>(n);
+        cap = n;
+    }
+    return p;
+}
+DevBuf::~DevBuf() {
+    if (p) cudaFree(p);
+}
+
 void *Ctx::ensure_scratch(size_t bytes) {
     if (bytes > scratch_bytes) {
         if (scratch) {

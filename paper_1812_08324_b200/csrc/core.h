@@ -114,6 +114,16 @@ struct HMat {
 void partition(HMat &H, const Tree &rt, const Tree &ct, int n_min, int n_block, double eta);
 void walk_leaves(HMat &H);
 
+struct DevBuf {  // grow-only device buffer
+    double *p = nullptr;
+    i64 cap = 0;
+    double *ensure(i64 n);
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf();
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -124,6 +134,7 @@ struct Ctx {
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
     void *ensure_scratch(size_t bytes);
+    DevBuf mm[4];  // multi-RHS: X, Y (row-major), T = V^T X, chunk partials
     ~Ctx();
 };
 

@@ -1787,6 +1787,16 @@ void propagator_stats(HMat &F, double *out) {
 static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
     SolvePlans &S = plans_of(F);
     LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
+    if (nrhs >= mm_min_rhs()) {  // B <- Z B as one DMMA matmat
+        const i64 n = F.nrows, ldk = mm_pad(nrhs);
+        double *Xr = ctx.mm[0].ensure(n * ldk), *Yr = ctx.mm[1].ensure(n * ldk);
+        MmBufs bb = mm_bufs(ctx, *S.mvZ, ldk);
+        mm_transpose(b, ldb, Xr, ldk, n, nrhs, true, ctx.stream);
+        mm_run(*S.mvZ, Xr, Yr, ldk, 1.0, 0.0, nullptr, bb.T, bb.part, ctx.stream);
+        mm_transpose(Yr, ldk, b, ldb, n, nrhs, false, ctx.stream);
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        return;
+    }
     for (int q = 0; q < nrhs; ++q) {
         double *bq = b + (i64)q * ldb;
         mv_run(*S.mvZ, *S.Z, bq, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
@@ -2129,6 +2139,28 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
         // H-matvec of the propagator (Z A- u with two when hminus is not 2I - A+).  The step
         // is captured once as a CUDA graph, cached per (operator, vector, scratch, method).
         const int shape = method == 2 ? (cn_pair_ok(ctx, S, Hm, Pm) ? 2 : 3) : 1;
+        if (method == 2 && nrhs >= mm_min_rhs()) {
+            // K right-hand sides: U row-major on the device for the whole run, each step one
+            // (or two) DMMA matmats: U <- 2 Z U - U, or U <- Z (A- U)
+            const i64 n = Hm.nrows, ldk = mm_pad(nrhs);
+            double *Xr = ctx.mm[0].ensure(n * ldk), *Yr = ctx.mm[1].ensure(n * ldk);
+            MmBufs bz = mm_bufs(ctx, *S.mvZ, ldk);
+            MmBufs bm = mm_bufs(ctx, Pm, ldk);
+            mm_transpose(u, ldu, Xr, ldk, n, nrhs, true, ctx.stream);
+            for (int k = 0; k < nsteps; ++k) {
+                if (shape == 2) {
+                    mm_run(*S.mvZ, Xr, Yr, ldk, 2.0, -1.0, Xr, bz.T, bz.part, ctx.stream);
+                } else {
+                    mm_run(Pm, Xr, Yr, ldk, 1.0, 0.0, nullptr, bm.T, bm.part, ctx.stream);
+                    std::swap(Xr, Yr);
+                    mm_run(*S.mvZ, Xr, Yr, ldk, 1.0, 0.0, nullptr, bz.T, bz.part, ctx.stream);
+                }
+                std::swap(Xr, Yr);
+            }
+            mm_transpose(Xr, ldk, u, ldu, n, nrhs, false, ctx.stream);
+            LH_CUDA(cudaStreamSynchronize(ctx.stream));
+            return;
+        }
         for (int q = 0; q < nrhs; ++q) {
             double *uq = u + (i64)q * ldu;
             if (!(S.graph && S.g_u == uq && S.g_hm == &Hm && S.g_y == y && S.g_method == shape)) {

@@ -483,11 +483,14 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
     std::vector<int32_t> tmap;
     std::vector<i64> seg_bytes(nseg, 0);
     i64 poff = 0;
+    std::vector<int32_t> colmap;
     for (int sg = 0; sg < nseg; ++sg) {
         SegDesc &S = segs[sg];
         S.y0 = seg_start[sg];
         S.rows = (int32_t)(seg_start[sg + 1] - seg_start[sg]);
         S.ld = (int32_t)even(S.rows);
+        S.poff = poff;
+        S.cmoff = (int32_t)colmap.size();
         const i64 ld = S.ld;
         const int kmax = (int)(SLOT_D / ld);
         S.dbeg = (int32_t)dall.size();
@@ -516,6 +519,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
             jobs.push_back({d.src, d.ld, poff, S.rows, d.ncols, S.ld, 0});
             dall.push_back({poff, d.xc0, d.ncols, 0});
             B.K = B.kd = d.ncols;
+            for (int j = 0; j < d.ncols; ++j) colmap.push_back((int32_t)(d.xc0 + j));
             B.xsrc = d.xc0 & ~i64(1);
             B.xadj = (int32_t)(d.xc0 - B.xsrc);
             poff += (i64)d.ncols * ld;
@@ -527,11 +531,15 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
             }
             jobs.push_back({l.src, l.ld, poff, S.rows, l.r, S.ld, 0});
             lall.push_back({poff, l.r, l.blk});
-            for (int c = 0; c < l.r; ++c) tmap.push_back(l.blk * KC_MAX + c);
+            for (int c = 0; c < l.r; ++c) {
+                tmap.push_back(l.blk * KC_MAX + c);
+                colmap.push_back(-(1 + l.blk * KC_MAX + c));
+            }
             B.K += l.r;
             poff += (i64)l.r * ld;
         }
         close();
+        S.ncol = (int32_t)(colmap.size() - S.cmoff);
         // every batch's coefficient span starts 16-byte aligned in tcol
         if (tmap.size() & 1) tmap.push_back(-1);
         S.dend = (int32_t)dall.size();
@@ -608,6 +616,10 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
     P->cta_seg = dupload(cta_seg, s);
     P->n_dpieces = (i64)dall.size();
     P->n_lpieces = (i64)lall.size();
+    P->colmap = dupload(colmap, s);
+    P->ncolmap = (i64)colmap.size();
+    P->nblk = nblk;
+    P->npart = npart;
     if (!jobs.empty()) {
         PackJob *dj = dupload(jobs, s);
         pack_kernel<<<std::min<int>((int)jobs.size(), 148 * 16), NT, 0, s>>>(dj, (int)jobs.size(),
@@ -625,6 +637,7 @@ MvPlan::~MvPlan() {
     cudaFree(tcol);
     cudaFree(tmap);
     cudaFree(xpad);
+    cudaFree(colmap);
     cudaFree(segs);
     cudaFree(dp);
     cudaFree(lp);
@@ -698,6 +711,16 @@ MvPlan &get_mv_plan(HMat &H, cudaStream_t s) {
 void matvec(Ctx &ctx, HMat &H, const double *x, i64 ldx, double *y, i64 ldy, int nrhs) {
     LH_REQUIRE(!H.factored, LH_EINVAL, "matvec of an LU-factored H-matrix is not defined");
     MvPlan &P = get_mv_plan(H, ctx.stream);
+    if (nrhs >= mm_min_rhs()) {  // one pass over the operator on the FP64 tensor cores
+        const i64 ldk = mm_pad(nrhs);
+        double *Xr = ctx.mm[0].ensure(H.ncols * ldk);
+        double *Yr = ctx.mm[1].ensure(H.nrows * ldk);
+        MmBufs b = mm_bufs(ctx, P, ldk);
+        mm_transpose(x, ldx, Xr, ldk, H.ncols, nrhs, true, ctx.stream);
+        mm_run(P, Xr, Yr, ldk, 1.0, 0.0, nullptr, b.T, b.part, ctx.stream);
+        mm_transpose(Yr, ldk, y, ldy, H.nrows, nrhs, false, ctx.stream);
+        return;
+    }
     for (int q = 0; q < nrhs; ++q)
         mv_run(P, H, x + (i64)q * ldx, y + (i64)q * ldy, 1.0, 0.0, ctx.stream, ctx.num_sms);
 }

@@ -19,6 +19,8 @@ struct SegDesc {
     int32_t dbeg, dend;  // dense pieces (MvDense)
     int32_t lbeg, lend;  // low-rank pieces (MvLr)
     int32_t bbeg, bend;  // bulk-copy batches (SBatch)
+    i64 poff;            // the segment's column stream: pbuf[poff + i + q * ld], q < ncol
+    int32_t ncol, cmoff; // colmap[cmoff + q]: source row of column q's coefficient
 };
 struct MvDense {  // element (i, j) = pbuf[off + i + j * ld], multiplies x[xc0 + j]
     i64 off, xc0;
@@ -62,6 +64,11 @@ struct MvPlan {
     i64 tcol_len = 0;
     double *xpad = nullptr;  // aligned, zero-padded copy of x (TMA kernel)
     i64 nx = 0;
+    // multi-RHS (matmat.cu): coefficient row of every segment column, >= 0 a row of X
+    // (dense piece), < 0 a row -(1 + blk * KC_MAX + c) of T = V^T X (low-rank piece)
+    int32_t *colmap = nullptr;
+    i64 ncolmap = 0;
+    int nblk = 0, npart = 0;
     SegDesc *segs = nullptr;
     MvDense *dp = nullptr;
     MvLr *lp = nullptr;
@@ -84,5 +91,17 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int grid, cu
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
                    double beta, cudaStream_t s, int num_sms, const double *z = nullptr);
 void matvec(Ctx &ctx, HMat &H, const double *x, i64 ldx, double *y, i64 ldy, int nrhs);
+
+// multi-RHS (matmat.cu); row-major X, Y, Z with ldk = mm_pad(K)
+i64 mm_pad(int k);
+int mm_min_rhs();
+void mm_transpose(const double *src, i64 lds, double *dst, i64 ldd, i64 n, int k, bool to_rowmajor,
+                  cudaStream_t s);
+void mm_run(const MvPlan &P, const double *X, double *Y, i64 ldk, double alpha, double beta,
+            const double *Z, double *T, double *part, cudaStream_t s);
+struct MmBufs {  // the context's multi-RHS scratch sized for plan P and K right-hand sides
+    double *T, *part;
+};
+MmBufs mm_bufs(Ctx &ctx, const MvPlan &P, i64 ldk);
 
 }  // namespace lh
