@@ -4,11 +4,16 @@ tempered-stable CGMY case), with assembly + H-LU time and the HBM roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-One "step" is one CN step u <- A+^{-1} A- u on the resident vector: the H-matvec
-with A- followed by the solve with the H-LU factors, applied as the two
-triangular-inverse factors.  Under torchrun (N > 1) every rank runs
-an independent replica (single-RHS stepping does not shard, SURVEY 8(e));
-``value`` is the sum over ranks, timing is the max over ranks.
+One "step" is one CN step u <- A+^{-1} A- u on the resident vector, applied as one
+H-matvec of the propagator Z = (A+)^{-1} built from the H-LU factors
+(u <- 2 Z u - u; ``--method inverse`` uses A- and the two
+triangular-inverse factors instead).  Under torchrun (N > 1) every rank runs an
+independent replica (single-RHS stepping does not shard); ``value``
+is the sum over ranks, timing is the max over ranks.
+
+``--workload cfg4`` runs BASELINE.json configs[3] instead: N = 2^18 - 1, 256
+right-hand sides stepped together on the FP64 tensor cores (DMMA), columns sharded
+256/G across ranks (strong scaling), roofline against the measured DMMA peak.
 
 ``--impl reference`` times the reference algorithm (the oracle restatement of
 levyh hops.matvec + hops.solve, oracle/levyh_oracle.py) on the host cores, on the
@@ -39,6 +44,13 @@ CFG3 = dict(workload="cfg3: CGMY C=1 G=5 M=10 Y=0.5 on [-4,4], N=2^20-1, a=0.05 
                      "dt=2^-13, leaf 64, eta 1, ACA tol 1e-9, fp64, u0=max(e^x-1,0)",
             n=2 ** 19, L=4.0, L_W=8.0, a=0.05, b=0.1, c=-0.05, dt=8.0 / 2 ** 20 * 16, leaf=64,
             eps1=1e-9, eps2=1e-10)
+
+
+CFG4 = dict(workload="cfg4: fractional Laplacian s=0.5 on [-1,1], N=2^18-1, a=b=c=0, dt=h, 256 RHS "
+                     "(seed 0, 8 Gaussian bumps each: centres U(-0.8,0.8), widths U(0.02,0.2), "
+                     "amplitudes N(0,1)), leaf 64, eta 1, ACA tol 1e-10, fp64",
+            n=2 ** 17, K=256, leaf=64, eps1=1e-10, eps2=1e-10)
+METRIC4 = "Crank-Nicolson steps/s of the 256-RHS batch at N=2^18 (cfg4); FP64 tensor (DMMA) roofline"
 
 
 def log(*a):
@@ -354,6 +366,102 @@ def run_b200(args, world, rank, local):
         print(json.dumps(out), flush=True)
 
 
+def cfg4_bumps(x, K, seed=0):
+    """cfg4 initial conditions: per column a sum of 8 Gaussian bumps exp(-((x-c)/w)^2)."""
+    rng = np.random.default_rng(seed)
+    U = np.zeros((x.shape[0], K))
+    for k in range(K):
+        c = rng.uniform(-0.8, 0.8, 8)
+        w = rng.uniform(0.02, 0.2, 8)
+        a = rng.normal(0.0, 1.0, 8)
+        U[:, k] = (a[None, :] * np.exp(-((x[:, None] - c[None, :]) / w[None, :]) ** 2)).sum(1)
+    return U
+
+
+def run_cfg4(args, world, rank, local):
+    import torch
+
+    import paper_1812_08324_b200 as P
+
+    cfg = CFG4
+    t0 = time.perf_counter()
+    s = P.FracCNSystem(P.power_measure(1, 0.5), 0.0, 0.0, 0.0, cfg["n"], 1.0 / cfg["n"])
+    s.prepare(P.HConfig(n_min=cfg["leaf"], eps1=cfg["eps1"]), cfg["eps2"], method="propagator")
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    F, Hm = s.factor, s.h_minus
+    ctx, L, N = Hm.ctx, P._lib.lib(), s.N
+    K = cfg["K"]
+    lo, hi = rank * K // world, (rank + 1) * K // world  # this rank's columns
+    Kr = hi - lo
+    U0 = cfg4_bumps(s.x, K)[:, lo:hi]
+    u = torch.from_numpy(np.asfortranarray(U0).T.copy()).cuda()  # (Kr, N): column-major N x Kr
+
+    def steps(k, vec):
+        P._lib.check(L.lh_cn_steps(ctx.h, Hm.handle, F.h.handle, vec.data_ptr(), N, Kr, int(k), 2), ctx.h)
+
+    steps(args.warmup, u)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        time.sleep(0.3)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        lib_stream = ctx.torch_stream()
+        start.record(lib_stream)
+        steps(args.steps, u)
+        end.record(lib_stream)
+        torch.cuda.synchronize()
+        ms = start.elapsed_time(end)
+    ms = max_over_ranks(ms, world, "cuda")
+    ms_per_step = ms / args.steps
+    # e2e: each step through the C ABI with the rank's columns in pinned host memory
+    u_host = torch.from_numpy(np.asfortranarray(U0).T.copy()).pin_memory()
+    u_dev = torch.empty_like(u)
+    e2e_steps = max(1, min(args.steps, 10))
+    t1 = time.perf_counter()
+    for _ in range(e2e_steps):
+        u_dev.copy_(u_host, non_blocking=True)
+        steps(1, u_dev)
+        u_host.copy_(u_dev, non_blocking=True)
+        torch.cuda.synchronize()
+    t_e2e = max_over_ranks(time.perf_counter() - t1, world, "cuda")
+    # DMMA roofline: 2 K S_Z flops per step (phase 1 V^T X + phase 2 segment GEMMs)
+    prof = np.zeros(16)
+    P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, torch.zeros(N, dtype=torch.float64,
+                 device="cuda").data_ptr(), 1, 2, P._lib.host_ptr(prof)), ctx.h)
+    S_Z = float(prof[13])
+    flops = 2.0 * K * S_Z
+    try:
+        pk = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_dmma_peak.json")))
+        peak, peak_src = float(pk["tflops"]), "measured (profiles/r01_fp64_dmma_peak.json, tools/ubench_dmma.cu)"
+    except Exception:
+        peak, peak_src = 45.0, "nominal"
+    achieved = flops / (ms_per_step / 1e3) / 1e12
+    out = {"metric": METRIC4, "value": round(1000.0 / ms_per_step, 3), "unit": "steps/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (BASELINE.json configs[3]; seeded bumps, no dataset)",
+           "config": {"workload": cfg["workload"], "N": N, "rhs": K, "rhs_per_rank": Kr,
+                      "parallelism": f"columns sharded {K}/{world}",
+                      "solve": SOLVE_DESC["propagator"] + "; K right-hand sides as one DMMA matmat per step",
+                      "l2": "operator and state larger than L2"},
+           "rhs_steps_per_s": round(K * 1000.0 / ms_per_step, 1),
+           "clocks": sampler.summary(),
+           "e2e": {"value": round(world * e2e_steps / t_e2e / world, 3), "unit": "steps/s",
+                   "h2d_bytes_per_step": 8 * N * Kr, "d2h_bytes_per_step": 8 * N * Kr,
+                   "path": "lh_cn_steps (C ABI) with pinned host columns per step"},
+           "gpu_launches": None,
+           "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                        "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                        "flops_per_step": flops, "stored_scalars_Z": S_Z},
+           "phases": {"setup_total_s": round(t_setup, 3)}}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def run_reference(args, world, rank, local):
     """--impl reference: the reference algorithm on host cores (rank 0 only)."""
     if rank != 0:
@@ -398,6 +506,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--ref-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4"])
     ap.add_argument("--method", default="propagator", choices=["propagator", "inverse"],
                     help="per-step solve: one H-matvec of Z=(A+)^-1 (default) or A- + L^-1 + U^-1")
     args = ap.parse_args()
@@ -406,6 +515,8 @@ def main():
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank, local)
+    elif args.workload == "cfg4":
+        run_cfg4(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
     if world > 1:
