@@ -90,6 +90,21 @@ typedef struct {
  * build_from_dense(toeplitz(t), rt, ct, cfg) (hmatrix.py:306-340). */
 int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,
                            const lh_hconfig *cfg, lh_hmat **out);
+/* Sharded assembly: rank `rank` of `world` compresses its share of the
+ * admissible blocks (longest-processing-time assignment by m + n, identical on every
+ * rank).  The result is pending until every other rank's share has been unpacked:
+ *   lh_hmat_shard_pack(buf = NULL) -> length; pack -> device buffer (doubles);
+ *   exchange the buffers (e.g. NCCL all-gather); lh_hmat_shard_unpack for every source
+ *   rank; lh_hmat_shard_finalize (dense conversions + local dense fill).
+ * The finalized matrix equals the unsharded lh_hmat_build_toeplitz result bit for bit.
+ * t_dev must stay valid until finalize. */
+int lh_hmat_build_toeplitz_shard(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct,
+                                 const double *t_dev, const lh_hconfig *cfg, int32_t rank,
+                                 int32_t world, lh_hmat **out);
+int lh_hmat_shard_pack(lh_ctx *ctx, lh_hmat *h, double *buf_dev, int64_t cap, int64_t *len);
+int lh_hmat_shard_unpack(lh_ctx *ctx, lh_hmat *h, int32_t src_rank, const double *buf_dev,
+                         int64_t len);
+int lh_hmat_shard_finalize(lh_ctx *ctx, lh_hmat *h);
 /* build_from_dense(A, rt, ct, cfg) with A on the device (tree order), element (i,j) at
  * A[i*lda + j] (row_major=1, numpy C order) or A[i + j*lda] (row_major=0). */
 int lh_hmat_build_dense(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *A_dev,

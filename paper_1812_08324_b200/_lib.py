@@ -70,6 +70,10 @@ SIGNATURES = [
     ("lh_prepare_inverse", C.c_int, [P, P, D]),
     ("lh_prepare_propagator", C.c_int, [P, P, D]),
     ("lh_propagator_stats", C.c_int, [P, P]),
+    ("lh_hmat_build_toeplitz_shard", C.c_int, [P, P, P, P, P, I32, I32, P]),
+    ("lh_hmat_shard_pack", C.c_int, [P, P, P, I64, P]),
+    ("lh_hmat_shard_unpack", C.c_int, [P, P, I32, P, I64]),
+    ("lh_hmat_shard_finalize", C.c_int, [P, P]),
     ("lh_step_graph_kernels", I32, [P]),
     ("lh_trisolve_dense", C.c_int, [P, P, I32, I32, P, I64, I32]),
     ("lh_lowrank_add_recompress", C.c_int, [P, I64, I64, P, P, I32, P, P, I32, D, P, P, P]),

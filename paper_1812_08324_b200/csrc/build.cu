@@ -371,11 +371,10 @@ static void set_smem(const void *fn, size_t bytes) {
     LH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-template <class Src>
-static void run_build(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg) {
-    const int KA = std::min(std::max(cfg.max_aca_rank, 1), KA_MAX);
+// storage layout: dense region then low-rank region; returns the low-rank leaves in ACA
+// order (size-sorted, largest first)
+static std::vector<int32_t> build_layout(Ctx &ctx, HMat &H, const lh_hconfig &cfg) {
     const int kcap = std::min(std::max(cfg.kcap, 1), KC_MAX);
-    // --- storage layout: dense region then low-rank region -------------------
     i64 off = 0;
     int nslots = 0;
     std::vector<int32_t> lr;
@@ -403,11 +402,20 @@ static void run_build(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg) {
     H.nslots = nslots;
     H.d_ranks = dalloc<int32_t>(std::max(nslots, 1));
     LH_CUDA(cudaMemsetAsync(H.d_ranks, 0, sizeof(int32_t) * std::max(nslots, 1), ctx.stream));
-    // --- ACA in size-sorted batches bounded by a workspace budget -------------
     std::sort(lr.begin(), lr.end(), [&](int32_t a, int32_t b) {
         i64 sa = H.nodes[a].m + H.nodes[a].n, sb = H.nodes[b].m + H.nodes[b].n;
         return sa != sb ? sa > sb : a < b;
     });
+    return lr;
+}
+
+// ACA + recompression of the given low-rank leaves in size-sorted batches bounded by a
+// workspace budget; returns the blocks whose rank exceeds min(m,n)//2 (to be stored dense)
+template <class Src>
+static std::vector<int32_t> run_aca(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg,
+                                    const std::vector<int32_t> &lr) {
+    const int KA = std::min(std::max(cfg.max_aca_rank, 1), KA_MAX);
+    const int kcap = std::min(std::max(cfg.kcap, 1), KC_MAX);
     const i64 budget = (i64)1 << 30;  // doubles (8 GiB)
     std::vector<int32_t> to_dense;
     size_t smem = sizeof(AcaSmem);
@@ -466,7 +474,14 @@ static void run_build(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg) {
         p = q;
     }
     if (work) cudaFree(work);
-    // --- blocks whose rank exceeds min(m,n)//2 are stored dense (hmatrix.py:301-302,331)
+    return to_dense;
+}
+
+// blocks whose rank exceeds min(m,n)//2 are stored dense (hmatrix.py:301-302,331), appended
+// in block order; then every dense leaf is filled from the entry source
+template <class Src>
+static void build_finalize(Ctx &ctx, HMat &H, Src src, std::vector<int32_t> to_dense) {
+    std::sort(to_dense.begin(), to_dense.end());
     if (!to_dense.empty()) {
         i64 extra = 0;
         for (int32_t b : to_dense) extra += H.nodes[b].m * H.nodes[b].n;
@@ -486,7 +501,6 @@ static void run_build(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg) {
         }
         H.arena_len += extra;
     }
-    // --- dense fill ----------------------------------------------------------
     std::vector<FillJob> fj;
     for (int32_t b : H.leafblocks) {
         const Node &nd = H.nodes[b];
@@ -501,6 +515,165 @@ static void run_build(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg) {
         cudaFree(d);
     }
     H.sync_ranks(ctx.stream);
+}
+
+template <class Src>
+static void run_build(Ctx &ctx, HMat &H, Src src, const lh_hconfig &cfg) {
+    std::vector<int32_t> lr = build_layout(ctx, H, cfg);
+    std::vector<int32_t> to_dense = run_aca(ctx, H, src, cfg, lr);
+    build_finalize(ctx, H, src, to_dense);
+}
+
+// ---------------------------------------------------------------------------
+// sharded assembly: admissible blocks are independent, so rank q of W
+// compresses its share (longest-processing-time assignment by m + n over the size-sorted
+// list, identical on every rank), packs its factors, and after an all-gather every rank
+// unpacks the others' blocks and finalizes (dense conversions + local dense fill).
+// ---------------------------------------------------------------------------
+struct ShardState {
+    int rank = 0, world = 1;
+    std::vector<std::vector<int32_t>> owned;  // per rank, its blocks in ACA order
+    std::vector<int32_t> to_dense;            // dense conversions seen so far
+    const double *t = nullptr;                // Toeplitz symbol (kept alive by the caller)
+    std::vector<double> pack_meta;            // this rank's packed metadata (host)
+};
+
+static std::vector<std::vector<int32_t>> lpt_assign(const HMat &H, const std::vector<int32_t> &lr,
+                                                    int world) {
+    std::vector<std::vector<int32_t>> own(world);
+    std::vector<i64> load(world, 0);
+    for (int32_t b : lr) {  // lr is size-sorted, largest first
+        int q = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        own[q].push_back(b);
+        load[q] += H.nodes[b].m + H.nodes[b].n;
+    }
+    return own;
+}
+
+void build_toeplitz_shard(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg, int rank,
+                          int world) {
+    LH_REQUIRE(world >= 1 && rank >= 0 && rank < world, LH_EINVAL, "invalid shard rank/world");
+    std::vector<int32_t> lr = build_layout(ctx, H, cfg);
+    auto st = std::make_shared<ShardState>();
+    st->rank = rank;
+    st->world = world;
+    st->t = t;
+    st->owned = lpt_assign(H, lr, world);
+    ToepSrc s{t, H.nrows};
+    st->to_dense = run_aca(ctx, H, s, cfg, st->owned[rank]);
+    H.sync_ranks(ctx.stream);
+    H.shard = st;
+}
+
+static ShardState &shard_of(HMat &H) {
+    LH_REQUIRE(H.shard != nullptr, LH_EINVAL, "H-matrix is not a pending sharded build");
+    return *static_cast<ShardState *>(H.shard.get());
+}
+
+struct GatherJob {
+    i64 a, b;  // arena offset, packed offset
+    i64 rows;
+    int32_t cols, dir;  // dir 0: arena -> packed, 1: packed -> arena (ld = rows both sides)
+};
+
+__global__ void shard_copy_kernel(const GatherJob *jobs, int njobs, double *arena, double *packed) {
+    for (int j = blockIdx.x; j < njobs; j += gridDim.x) {
+        const GatherJob J = jobs[j];
+        const i64 n = J.rows * J.cols;
+        for (i64 e = threadIdx.x; e < n; e += NT) {
+            if (J.dir == 0) packed[J.b + e] = arena[J.a + e];
+            else arena[J.a + e] = packed[J.b + e];
+        }
+    }
+}
+
+static void run_jobs(Ctx &ctx, const std::vector<GatherJob> &jobs, double *arena, double *packed) {
+    if (jobs.empty()) return;
+    GatherJob *d = dupload(jobs, ctx.stream);
+    int grid = (int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 16);
+    shard_copy_kernel<<<grid, NT, 0, ctx.stream>>>(d, (int)jobs.size(), arena, packed);
+    LH_CUDA(cudaGetLastError());
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaFree(d);
+}
+
+// packed layout of rank q's share: [count][per block: rank, or -1 if stored dense] then
+// U (m x r) and V (n x r) of every low-rank block, in the owner's ACA order
+i64 shard_pack(Ctx &ctx, HMat &H, double *buf, i64 cap) {
+    ShardState &st = shard_of(H);
+    const auto &own = st.owned[st.rank];
+    std::vector<char> dense(H.nodes.size(), 0);
+    for (int32_t b : st.to_dense) dense[b] = 1;
+    const i64 nmeta = 1 + (i64)own.size();
+    i64 len = nmeta;
+    for (int32_t b : own) {
+        const Node &nd = H.nodes[b];
+        if (!dense[b]) len += (nd.m + nd.n) * H.h_ranks[nd.rslot];
+    }
+    if (!buf) return len;
+    LH_REQUIRE(cap >= len, LH_EINVAL, "shard pack buffer too small");
+    std::vector<double> meta(nmeta);
+    meta[0] = (double)own.size();
+    std::vector<GatherJob> jobs;
+    i64 o = nmeta;
+    for (size_t k = 0; k < own.size(); ++k) {
+        const Node &nd = H.nodes[own[k]];
+        if (dense[own[k]]) {
+            meta[1 + k] = -1.0;
+            continue;
+        }
+        const int r = H.h_ranks[nd.rslot];
+        meta[1 + k] = (double)r;
+        jobs.push_back({nd.uoff, o, nd.m, r, 0});
+        o += nd.m * r;
+        jobs.push_back({nd.voff, o, nd.n, r, 0});
+        o += nd.n * r;
+    }
+    LH_CUDA(cudaMemcpyAsync(buf, meta.data(), sizeof(double) * nmeta, cudaMemcpyHostToDevice, ctx.stream));
+    run_jobs(ctx, jobs, H.d_arena, buf);
+    return len;
+}
+
+void shard_unpack(Ctx &ctx, HMat &H, int src_rank, const double *buf, i64 len) {
+    ShardState &st = shard_of(H);
+    LH_REQUIRE(src_rank >= 0 && src_rank < st.world, LH_EINVAL, "invalid source rank");
+    if (src_rank == st.rank) return;
+    const auto &own = st.owned[src_rank];
+    const i64 nmeta = 1 + (i64)own.size();
+    LH_REQUIRE(len >= nmeta, LH_EINVAL, "shard buffer shorter than its metadata");
+    std::vector<double> meta(nmeta);
+    LH_CUDA(cudaMemcpyAsync(meta.data(), buf, sizeof(double) * nmeta, cudaMemcpyDeviceToHost, ctx.stream));
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    LH_REQUIRE((i64)meta[0] == (i64)own.size(), LH_EINVAL, "shard buffer from a different partition");
+    std::vector<GatherJob> jobs;
+    std::vector<int32_t> rk_slot, rk_val;
+    i64 o = nmeta;
+    for (size_t k = 0; k < own.size(); ++k) {
+        const Node &nd = H.nodes[own[k]];
+        const int r = (int)meta[1 + k];
+        if (r < 0) {
+            st.to_dense.push_back(own[k]);
+            continue;
+        }
+        H.h_ranks[nd.rslot] = r;
+        jobs.push_back({nd.uoff, o, nd.m, r, 1});
+        o += nd.m * r;
+        jobs.push_back({nd.voff, o, nd.n, r, 1});
+        o += nd.n * r;
+    }
+    LH_REQUIRE(o <= len, LH_EINVAL, "shard buffer shorter than its factors");
+    run_jobs(ctx, jobs, H.d_arena, const_cast<double *>(buf));
+    LH_CUDA(cudaMemcpyAsync(H.d_ranks, H.h_ranks.data(), sizeof(int32_t) * H.nslots,
+                            cudaMemcpyHostToDevice, ctx.stream));
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+void shard_finalize(Ctx &ctx, HMat &H) {
+    ShardState &st = shard_of(H);
+    ToepSrc s{st.t, H.nrows};
+    std::vector<int32_t> td = st.to_dense;
+    H.shard.reset();
+    build_finalize(ctx, H, s, td);
 }
 
 void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg) {

@@ -30,6 +30,11 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2);
 void propagator_stats(HMat &F, double *out);
 int step_graph_kernels(HMat &F);
 void trisolve_dense(Ctx &ctx, HMat &T, int mode, bool unit, double *b, i64 ldb, int nrhs);
+void build_toeplitz_shard(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg, int rank,
+                          int world);
+i64 shard_pack(Ctx &ctx, HMat &H, double *buf, i64 cap);
+void shard_unpack(Ctx &ctx, HMat &H, int src_rank, const double *buf, i64 len);
+void shard_finalize(Ctx &ctx, HMat &H);
 int lowrank_add_recompress(Ctx &ctx, i64 m, i64 n, const double *u1, const double *v1, int r1,
                            const double *u2, const double *v2, int r2, double eps2, double *uo,
                            double *vo);
@@ -251,6 +256,38 @@ static lh_hmat *new_hmat(const lh_tree *rt, const lh_tree *ct) {
     o->h.rt_hold = rt->t;
     o->h.ct_hold = ct->t;
     return o;
+}
+
+int lh_hmat_build_toeplitz_shard(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct,
+                                 const double *t_dev, const lh_hconfig *cfg, int32_t rank,
+                                 int32_t world, lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        check_cfg(cfg);
+        o = new_hmat(rt, ct);
+        partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
+        build_toeplitz_shard(ctx->c, o->h, t_dev, *cfg, rank, world);
+        start_background_plans(o->h);  // plans depend on the partition only
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+int lh_hmat_shard_pack(lh_ctx *ctx, lh_hmat *h, double *buf_dev, int64_t cap, int64_t *len) {
+    return guard(ctx, [&] { *len = shard_pack(ctx->c, h->h, buf_dev, cap); });
+}
+
+int lh_hmat_shard_unpack(lh_ctx *ctx, lh_hmat *h, int32_t src_rank, const double *buf_dev,
+                         int64_t len) {
+    return guard(ctx, [&] { shard_unpack(ctx->c, h->h, src_rank, buf_dev, len); });
+}
+
+int lh_hmat_shard_finalize(lh_ctx *ctx, lh_hmat *h) {
+    return guard(ctx, [&] { shard_finalize(ctx->c, h->h); });
 }
 
 int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,

@@ -105,6 +105,7 @@ struct HMat {
     std::shared_ptr<void> solve_plan;
     std::shared_ptr<void> inv_plan;
     std::shared_ptr<void> bg_plan;  // background H-LU + inverse planning (lu.cu: PlanJob)
+    std::shared_ptr<void> shard;    // pending sharded assembly (build.cu: ShardState)
     ~HMat();
     void sync_ranks(cudaStream_t s);
 };

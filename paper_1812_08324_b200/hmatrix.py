@@ -172,8 +172,13 @@ def build_from_dense(A, row_ct, col_ct, cfg=None):
     return HMatrix(h, row_ct, col_ct, cfg.eta, ctx, cfg)
 
 
-def build_toeplitz(t, row_ct, col_ct, cfg=None):
-    """Matrix-free build_from_dense of A[i, j] = t[j - i + n_rows - 1] (t on device, torch)."""
+def build_toeplitz(t, row_ct, col_ct, cfg=None, distributed=False):
+    """Matrix-free build_from_dense of A[i, j] = t[j - i + n_rows - 1] (t on device, torch).
+
+    distributed: False (default) builds on this GPU alone.  True (or a torch.distributed
+    process group) shards the ACA compression of the admissible blocks across the ranks
+    of the group and all-gathers the factors; every rank must call it with
+    the same symbol and configuration, and every rank receives the full matrix."""
     import torch
 
     cfg = cfg or HConfig()
@@ -182,12 +187,88 @@ def build_toeplitz(t, row_ct, col_ct, cfg=None):
         t = torch.as_tensor(np.asarray(t, dtype=np.float64)).to(f"cuda:{ctx.device}")
     if t.numel() != len(row_ct) + len(col_ct) - 1:
         raise ValueError("symbol length must be n_rows + n_cols - 1")
+    t = t.contiguous()
+    group = None
+    world = 1
+    if distributed is not False and distributed is not None:
+        import torch.distributed as dist
+
+        group = None if distributed is True else distributed
+        if dist.is_available() and dist.is_initialized():
+            world = dist.get_world_size(group)
+    if world > 1:
+        import torch.distributed as dist
+
+        rank = dist.get_rank(group)
+        return build_toeplitz_sharded(t, row_ct, col_ct, cfg, rank, world,
+                                      lambda buf: allgather_varlen(buf, group))
     h = C.c_void_p()
     nc = cfg.native()
     rc = _lib.lib().lh_hmat_build_toeplitz(ctx.h, row_ct.handle, col_ct.handle,
-                                           C.c_void_p(t.contiguous().data_ptr()), C.byref(nc), C.byref(h))
+                                           C.c_void_p(t.data_ptr()), C.byref(nc), C.byref(h))
     _lib.check(rc, ctx.h)
     return HMatrix(h, row_ct, col_ct, cfg.eta, ctx, cfg)
+
+
+def allgather_varlen(buf, group=None):
+    """All-gather of one 1-D tensor per rank with rank-dependent lengths: lengths first,
+    then one padded all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n = torch.tensor([buf.numel()], dtype=torch.int64, device=buf.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    lens = [int(v.item()) for v in ns]
+    mx = max(lens)
+    pad = torch.zeros(mx, dtype=buf.dtype, device=buf.device)
+    pad[:buf.numel()] = buf
+    out = torch.empty(world * mx, dtype=buf.dtype, device=buf.device)
+    if hasattr(dist, "all_gather_into_tensor") and buf.is_cuda:
+        dist.all_gather_into_tensor(out, pad, group=group)
+    else:
+        dist.all_gather(list(out.view(world, mx)), pad, group=group)
+    return [out[q * mx:q * mx + lens[q]] for q in range(world)]
+
+
+def build_toeplitz_sharded(t, row_ct, col_ct, cfg, rank, world, exchange):
+    """Sharded assembly: compress this rank's share of the admissible blocks, pack it,
+    `exchange(buf) -> [buf_0, ..., buf_{world-1}]` (device tensors), unpack the others,
+    finalize.  The result equals the unsharded build bit for bit."""
+    import time
+
+    import torch
+
+    ctx = _lib.Context.get()
+    L = _lib.lib()
+    h = C.c_void_p()
+    nc = cfg.native()
+    t0 = time.perf_counter()
+    _lib.check(L.lh_hmat_build_toeplitz_shard(ctx.h, row_ct.handle, col_ct.handle,
+                                              C.c_void_p(t.data_ptr()), C.byref(nc), int(rank),
+                                              int(world), C.byref(h)), ctx.h)
+    H = HMatrix(h, row_ct, col_ct, cfg.eta, ctx, cfg)
+    n = C.c_int64(0)
+    _lib.check(L.lh_hmat_shard_pack(ctx.h, H.handle, None, 0, C.byref(n)), ctx.h)
+    buf = torch.empty(max(n.value, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    _lib.check(L.lh_hmat_shard_pack(ctx.h, H.handle, C.c_void_p(buf.data_ptr()), buf.numel(),
+                                    C.byref(n)), ctx.h)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    bufs = exchange(buf[:n.value])
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    for q, b in enumerate(bufs):
+        b = b.contiguous()
+        _lib.check(L.lh_hmat_shard_unpack(ctx.h, H.handle, q, C.c_void_p(b.data_ptr()), b.numel()),
+                   ctx.h)
+    _lib.check(L.lh_hmat_shard_finalize(ctx.h, H.handle), ctx.h)
+    torch.cuda.synchronize()
+    H.shard_stats = dict(rank=rank, world=world, compress_s=t1 - t0, exchange_s=t2 - t1,
+                         finalize_s=time.perf_counter() - t2, bytes_sent=8 * n.value,
+                         bytes_received=8 * sum(int(b.numel()) for b in bufs))
+    return H
 
 
 def derive_toeplitz(H, t, lr_scale=1.0, kcap=0):

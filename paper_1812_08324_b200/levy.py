@@ -31,7 +31,7 @@ class FracCNSystem:
     """
 
     def __init__(self, nu, a, b, c, n, dt, L=1.0, L_W=None, rho_r=0.2, tail_mass=None,
-                 drift_compensation=True, s=None):
+                 drift_compensation=True, s=None, distributed=False):
         if a < 0 or c > 0:
             raise ValueError("stability requires a >= 0 and c <= 0")
         self.nu, self.a, self.b, self.c, self.dt, self.L = nu, a, b, c, dt, L
@@ -64,6 +64,8 @@ class FracCNSystem:
         self.factor = None
         self.h_minus = None
         self.h_plus = None
+        # True / a process group: shard the ACA compression across the ranks
+        self.distributed = distributed
 
     @property
     def size(self):
@@ -80,7 +82,7 @@ class FracCNSystem:
         cfg = cfg or HConfig()
         ct = self.cluster_tree(cfg.n_min)
         t = {"A": self.tA, "plus": self.tPlus, "minus": self.tMinus}[which]
-        return build_toeplitz(t, ct, ct, cfg)
+        return build_toeplitz(t, ct, ct, cfg, distributed=self.distributed)
 
     def build_pair(self, cfg=None):
         """H+ (capacity cfg.kcap, for H-LU) and H- derived from it: A-'s off-diagonal
