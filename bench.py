@@ -149,7 +149,7 @@ SOLVE_DESC = {
 }
 
 
-def build_system(P, cfg=CFG3, n=None, method="propagator"):
+def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
     """Operator assembly (GPU symbol + ACA compression) and factorisation, timed."""
     import torch
 
@@ -157,7 +157,7 @@ def build_system(P, cfg=CFG3, n=None, method="propagator"):
     t0 = time.perf_counter()
     nu = P.cgmy_measure(1.0, 5.0, 10.0, 0.5)
     s = P.FracCNSystem(nu, cfg["a"], cfg["b"], cfg["c"], n, cfg["dt"], L=cfg["L"], L_W=cfg["L_W"],
-                       drift_compensation=True)
+                       drift_compensation=True, distributed=world > 1)
     torch.cuda.synchronize()
     t_symbol = time.perf_counter() - t0
     hc = P.HConfig(n_min=cfg["leaf"], eps1=cfg["eps1"])
@@ -183,6 +183,9 @@ def build_system(P, cfg=CFG3, n=None, method="propagator"):
     s.factor = F
     s.method = method
     times = dict(symbol_s=t_symbol, aca_s=t_aca, assembly_s=t_symbol + t_aca, hlu_s=t_lu,
+                 assembly_sharding=(dict((k, round(v, 4) if isinstance(v, float) else v)
+                                         for k, v in Hp.shard_stats.items())
+                                    if getattr(Hp, "shard_stats", None) else "unsharded (1 rank)"),
                  hlu_plan_s=float(st[1]), hlu_exec_s=float(st[3]), hlu_tasks=int(st[0]),
                  hlu_plan_chunks=int(st[4]))
     if method == "propagator":
@@ -244,7 +247,7 @@ def run_b200(args, world, rank, local):
 
     import paper_1812_08324_b200 as P
 
-    s, F, Hm, times = build_system(P, n=args.n, method=args.method)
+    s, F, Hm, times = build_system(P, n=args.n, method=args.method, world=world)
     ctx = Hm.ctx
     L = P._lib.lib()
     N = s.N
@@ -347,7 +350,9 @@ def run_b200(args, world, rank, local):
            "config": {"workload": CFG3["workload"] if args.n is None else f"cfg3 operator at n={args.n}",
                       "N": N, "leaf": CFG3["leaf"], "eps1": CFG3["eps1"], "eps2": CFG3["eps2"],
                       "solve": SOLVE_DESC[args.method],
-                      "parallelism": f"replicas x{world}",
+                      "parallelism": (f"stepping: replicas x{world}; assembly (ACA): admissible blocks "
+                                      f"sharded over {world} ranks + NCCL all-gather of the factors"
+                                      if world > 1 else "replicas x1"),
                       "l2": f"inputs larger than L2 ({step_bytes / 1e9:.1f} GB streamed per step vs 126 MB L2)"},
            "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
            "gpu_launches_per_step": launches_per_step,
