@@ -261,12 +261,12 @@ __device__ __forceinline__ void consumer_sync() {  // the consumer warps only
 }
 
 constexpr int XOFF = 0;    // aux: x slice (<= 66 doubles)
-constexpr int TOFF = 128;  // aux: low-rank coefficients (<= SLOT_D / 2 columns)
-static_assert(TOFF + SLOT_D / 2 <= SLOT_A + SLOT_D, "aux layout");
+constexpr int TOFF = 128;  // aux: low-rank coefficients (<= MAXK)
+constexpr int MAXK = 128;  // columns per batch (segments of < 32 rows would allow more)
 
 struct TmaSmem {
     double data[TMA_STAGES][SLOT_D];
-    double aux[TMA_STAGES][TOFF + 64];
+    double aux[TMA_STAGES][TOFF + MAXK];
     double red[TGRP][SEG];
     uint64_t full[TMA_STAGES], empty[TMA_STAGES];
     int32_t hdr[TMA_STAGES][4];  // K, kd, xadj
@@ -492,7 +492,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
         S.poff = poff;
         S.cmoff = (int32_t)colmap.size();
         const i64 ld = S.ld;
-        const int kmax = (int)(SLOT_D / ld);
+        const int kmax = (int)std::min<i64>(MAXK, SLOT_D / ld);
         S.dbeg = (int32_t)dall.size();
         S.lbeg = (int32_t)lall.size();
         S.bbeg = (int32_t)batches.size();
