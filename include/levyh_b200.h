@@ -73,6 +73,10 @@ int lh_plan_stats(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, 
  * partition to `path` (binary, see tests/plan_emulator.py) for CPU verification. */
 int lh_debug_dump_plans(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
                         int kcap_f, int kcap_x, const char *path);
+/* Host-only planner timing on the partition of (rt, ct): which & 1 plans the H-LU, which & 2
+ * the propagator; out[0..3] = H-LU plan seconds, tasks, propagator plan seconds, tasks. */
+int lh_debug_plan_timing(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
+                         int kcap_f, int kcap_x, int which, double *out);
 
 /* ---- H-matrix construction: hmatrix.py:121-137 HConfig, :306-340 build_from_dense */
 typedef struct {

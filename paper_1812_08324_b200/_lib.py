@@ -53,6 +53,7 @@ SIGNATURES = [
     ("lh_partition", C.c_int, [P, P, C.c_int, C.c_int, D, P, P, P]),
     ("lh_plan_stats", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, P]),
     ("lh_debug_dump_plans", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, C.c_int, C.c_char_p]),
+    ("lh_debug_plan_timing", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, C.c_int, C.c_int, P]),
     ("lh_hmat_build_toeplitz", C.c_int, [P, P, P, P, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_build_dense", C.c_int, [P, P, P, P, I64, C.c_int, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_derive_toeplitz", C.c_int, [P, P, P, D, I32, C.POINTER(P)]),

@@ -150,13 +150,13 @@ T *dalloc(i64 count) {
                                    " bytes): " + cudaGetErrorString(e));
     return (T *)p;
 }
-template <class T>
-void upload(T *dst, const std::vector<T> &src, cudaStream_t s) {
+template <class T, class A>
+void upload(T *dst, const std::vector<T, A> &src, cudaStream_t s) {
     if (!src.empty())
         LH_CUDA(cudaMemcpyAsync(dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
 }
-template <class T>
-T *dupload(const std::vector<T> &src, cudaStream_t s) {
+template <class T, class A>
+T *dupload(const std::vector<T, A> &src, cudaStream_t s) {
     T *p = dalloc<T>((i64)src.size());
     upload(p, src, s);
     return p;

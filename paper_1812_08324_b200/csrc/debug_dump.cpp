@@ -138,3 +138,60 @@ extern "C" int lh_debug_dump_plans(const lh_tree *rt, const lh_tree *ct, int n_m
         return LH_EINTERNAL;
     }
 }
+
+// Host-only planner timing on a partition: out[0] H-LU plan seconds, out[1] its tasks,
+// out[2] propagator plan seconds (column-split, from mark_lu_leaves), out[3] its tasks.
+extern "C" int lh_debug_plan_timing(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block,
+                                    double eta, int kcap_f, int kcap_x, int which, double *out) {
+    try {
+        HMat F;
+        partition(F, *rt->t, *ct->t, n_min, n_block, eta);
+        i64 off = 0;
+        int32_t slots = 0;
+        for (int32_t b : F.leafblocks) {
+            Node &nd = F.nodes[b];
+            if (nd.kind == K_DENSE) {
+                nd.doff = off;
+                off += nd.m * nd.n;
+            }
+        }
+        for (int32_t b : F.leafblocks) {
+            Node &nd = F.nodes[b];
+            if (nd.kind == K_LR) {
+                nd.kcap = kcap_f;
+                nd.rslot = slots++;
+                nd.uoff = off;
+                off += nd.m * kcap_f;
+                nd.voff = off;
+                off += nd.n * kcap_f;
+            }
+        }
+        F.arena_len = off;
+        F.nslots = slots;
+        out[0] = out[1] = out[2] = out[3] = 0.0;
+        HMat G = F;  // structure copies for the two planners
+        G.d_arena = nullptr;
+        G.d_ranks = nullptr;
+        if (which & 1) {
+            i64 pl = 0;
+            auto P = plan_hlu(F, 1e-10, pl);
+            out[0] = P->build_seconds;
+            out[1] = (double)P->tasks.size();
+        }
+        if (which & 2) {
+            i64 pl = 0, il = 0;
+            mark_lu_leaves(G, pl, il);
+            G.factored = true;
+            HMat Z;
+            block_layout(Z, G, 2, kcap_x);
+            auto Pz = plan_propagator(G, Z, 1e-10);
+            out[2] = Pz->build_seconds;
+            out[3] = (double)Pz->tasks.size();
+        }
+        F.d_arena = nullptr;
+        return LH_OK;
+    } catch (const std::exception &e) {
+        fprintf(stderr, "lh_debug_plan_timing: %s\n", e.what());
+        return LH_EINTERNAL;
+    }
+}

@@ -53,40 +53,66 @@ PView PView::T() const {
 // ---------------------------------------------------------------------------
 // dependency tracking: per object, disjoint row intervals with last writer + readers
 // ---------------------------------------------------------------------------
-void DepTracker::access(int32_t task, u64 obj, i64 a, i64 b, bool write, std::vector<int32_t> &out) {
-    std::map<i64, Seg> *mp;
-    if (obj < dense_limit) {
-        if (obj >= dense.size()) dense.resize(std::max<size_t>(obj + 1, dense.size() * 2));
-        mp = &dense[obj];
-    } else {
-        mp = &objs[obj];
+static void add_reader(DepTracker::Seg &s, int32_t task) {
+    if (s.nr > 0) {  // the same task touching twice in a row
+        const int32_t last = s.nr <= 4 ? s.rd[s.nr - 1] : s.more->back();
+        if (last == task) return;
     }
-    auto &m = *mp;
-    if (m.empty()) m[0] = Seg{INT64_MAX, -1, {}};
-    // split at a and b
-    auto split = [&](i64 x) {
-        auto it = m.upper_bound(x);
-        --it;
-        if (it->first == x) return;
-        Seg s = it->second;
-        i64 end = s.end;
-        it->second.end = x;
-        m[x] = Seg{end, s.writer, s.readers};
+    if (s.nr < 4) s.rd[s.nr] = task;
+    else {
+        if (!s.more) s.more = new std::vector<int32_t>();
+        s.more->push_back(task);
+    }
+    ++s.nr;
+}
+
+void DepTracker::access(int32_t task, u64 obj, i64 a, i64 b, bool write, std::vector<int32_t> &out) {
+    if (obj >= objs.size()) objs.resize(std::max<size_t>(obj + 1, objs.size() + objs.size() / 2 + 16));
+    std::vector<Seg> &v = objs[obj];
+    if (v.empty()) v.push_back(Seg{0, INT64_MAX, -1, 0, {0, 0, 0, 0}, nullptr});
+    // first segment containing row a (segments are sorted and cover [0, inf))
+    size_t i = std::upper_bound(v.begin(), v.end(), a, [](i64 x, const Seg &s) { return x < s.a; }) -
+               v.begin() - 1;
+    auto split = [&](size_t k, i64 at) {  // split segment k at row `at` (a < at < b)
+        Seg t = v[k];
+        if (t.more) t.more = new std::vector<int32_t>(*t.more);
+        v[k].b = at;
+        t.a = at;
+        v.insert(v.begin() + k + 1, t);
     };
-    split(a);
-    if (b < INT64_MAX) split(b);
-    for (auto it = m.find(a); it != m.end() && it->first < b; ++it) {
-        Seg &s = it->second;
+    if (v[i].a < a) {
+        split(i, a);
+        ++i;
+    }
+    const size_t first = i;
+    for (; i < v.size() && v[i].a < b; ++i) {
+        if (v[i].b > b) split(i, b);
+        Seg &s = v[i];
         if (s.writer >= 0 && s.writer != task) out.push_back(s.writer);
         if (write) {
-            for (int32_t r : s.readers)
-                if (r != task) out.push_back(r);
+            for (int k = 0; k < std::min(s.nr, 4); ++k)
+                if (s.rd[k] != task) out.push_back(s.rd[k]);
+            if (s.more) {
+                for (int32_t r : *s.more)
+                    if (r != task) out.push_back(r);
+                delete s.more;
+                s.more = nullptr;
+            }
             s.writer = task;
-            s.readers.clear();
+            s.nr = 0;
         } else {
-            if (s.readers.empty() || s.readers.back() != task) s.readers.push_back(task);
+            add_reader(s, task);
         }
     }
+    if (write && i - first > 1) {  // the written rows now share one state: merge them
+        v[first].b = v[i - 1].b;
+        v.erase(v.begin() + first + 1, v.begin() + i);
+    }
+}
+
+DepTracker::~DepTracker() {
+    for (auto &v : objs)
+        for (auto &s : v) delete s.more;
 }
 
 // ---------------------------------------------------------------------------
@@ -99,16 +125,23 @@ Planner::Planner(HMat &F, HMat *X) : F(F), X(X) {
     next_slot = P->slot_off_tmp;
     nF = (i64)F.nodes.size();
     nX = X ? (i64)X->nodes.size() : 0;
-    deps.dense_limit = (u64)(3 * (nF + nX));
-    deps.dense.reserve(deps.dense_limit);
+    deps.objs.reserve((size_t)(3 * (nF + nX) + 1024));
+    // measured on the 1D operators: ~29 (H-LU) to ~38 (propagator) tasks per block-tree node
+    // and ~6 dependencies per task; reserving (virtual memory, touched only as used) avoids
+    // regrowth copies of the multi-100-MB arrays
+    const size_t est = (size_t)(nF + nX) * 40;
+    P->tasks.reserve(est);
+    P->deps.reserve(est * 7);
+    P->pieces.reserve(est * 2);
 }
 
-// object ids: block storage of F and X get dense ids (vector-indexed dependency maps);
-// temporaries and the right-hand side live in a hash map
+// dense object ids: block storage of F (U, V, dense) and X, then the right-hand side, then
+// the temporaries in creation order
 u64 Planner::key(int base, i64 id, int which) const {
     if (base == B_F) return (u64)(3 * id + which);
     if (base == B_X) return (u64)(3 * nF + 3 * id + which);
-    return (1ull << 62) | ((u64)base << 56) | ((u64)id << 2) | (u64)which;
+    if (base == B_RHS) return (u64)(3 * (nF + nX));
+    return (u64)(3 * (nF + nX) + 1 + id);  // B_TMP
 }
 
 PView Planner::dense_view(const Mref &M, int32_t b) const {
@@ -196,7 +229,8 @@ int32_t Planner::new_slot() { return next_slot++; }
 int32_t Planner::emit(DTask t, std::initializer_list<std::pair<const PView *, bool>> acc,
                       const std::vector<std::pair<PView, bool>> *more) {
     int32_t id = (int32_t)P->tasks.size();
-    std::vector<int32_t> d;
+    std::vector<int32_t> &d = dbuf;
+    d.clear();
     auto touch = [&](const PView &v, bool w) {
         i64 a = v.whole ? 0 : v.r0;
         i64 b = v.whole ? INT64_MAX : v.r0 + v.d.rows;
@@ -1006,45 +1040,57 @@ static void structure_copy(HMat &D, const HMat &S) {
 }
 
 // concatenation of independent DAGs: task, dependency, piece and path indices and the
-// temp-pool offsets of each part are shifted past the previous parts
+// temp-pool offsets of each part are shifted past the previous parts (parts copied in
+// parallel, each into its own slice)
 std::shared_ptr<Plan> merge_plans(const std::vector<std::shared_ptr<Plan>> &parts) {
     auto M = std::make_shared<Plan>();
-    size_t nt = 0, nd = 0, np = 0;
-    for (auto &p : parts) {
-        nt += p->tasks.size();
-        nd += p->deps.size();
-        np += p->pieces.size();
+    const size_t np = parts.size();
+    std::vector<size_t> t0(np + 1, 0), d0(np + 1, 0), p0(np + 1, 0), s0(np + 1, 0);
+    std::vector<i64> toff(np + 1, 0);
+    for (size_t k = 0; k < np; ++k) {
+        t0[k + 1] = t0[k] + parts[k]->tasks.size();
+        d0[k + 1] = d0[k] + parts[k]->deps.size();
+        p0[k + 1] = p0[k] + parts[k]->pieces.size();
+        s0[k + 1] = s0[k] + parts[k]->paths.size();
+        toff[k + 1] = toff[k] + parts[k]->temp_len;
+        M->nslots_total = std::max(M->nslots_total, parts[k]->nslots_total);
     }
-    M->tasks.reserve(nt);
-    M->deps.reserve(nd);
-    M->pieces.reserve(np);
+    M->tasks.resize(t0[np]);
+    M->deps.resize(d0[np]);
+    M->pieces.resize(p0[np]);
     M->slot_off_x = parts[0]->slot_off_x;
     M->slot_off_tmp = parts[0]->slot_off_tmp;
-    for (auto &p : parts) {
-        const i64 toff = M->temp_len;
-        const int32_t t0 = (int32_t)M->tasks.size(), d0 = (int32_t)M->deps.size(),
-                      p0 = (int32_t)M->pieces.size(), s0 = (int32_t)M->paths.size();
-        auto fix = [&](DView &v) {
-            if (v.base == B_TMP) v.off += toff;
-        };
-        for (DTask t : p->tasks) {
-            t.dep_beg += d0;
-            t.pc_beg += p0;
-            t.pc_end += p0;
-            if (t.path >= 0) t.path += s0;
-            for (auto &v : t.v) fix(v);
-            M->tasks.push_back(t);
-        }
-        for (int32_t d : p->deps) M->deps.push_back(d + t0);
-        for (DPiece pc : p->pieces) {
-            fix(pc.mat);
-            fix(pc.x);
-            M->pieces.push_back(pc);
-        }
-        M->paths.insert(M->paths.end(), p->paths.begin(), p->paths.end());
-        M->temp_len += p->temp_len;
-        M->nslots_total = std::max(M->nslots_total, p->nslots_total);
-    }
+    M->temp_len = toff[np];
+    std::vector<std::future<void>> fut;
+    for (size_t k = 0; k < np; ++k)
+        fut.push_back(std::async(std::launch::async, [&, k] {
+            const Plan &p = *parts[k];
+            const i64 to = toff[k];
+            auto fix = [&](DView &v) {
+                if (v.base == B_TMP) v.off += to;
+            };
+            DTask *T = M->tasks.data() + t0[k];
+            for (size_t i = 0; i < p.tasks.size(); ++i) {
+                DTask t = p.tasks[i];
+                t.dep_beg += (int32_t)d0[k];
+                t.pc_beg += (int32_t)p0[k];
+                t.pc_end += (int32_t)p0[k];
+                if (t.path >= 0) t.path += (int32_t)s0[k];
+                for (auto &v : t.v) fix(v);
+                T[i] = t;
+            }
+            int32_t *D = M->deps.data() + d0[k];
+            for (size_t i = 0; i < p.deps.size(); ++i) D[i] = p.deps[i] + (int32_t)t0[k];
+            DPiece *Pc = M->pieces.data() + p0[k];
+            for (size_t i = 0; i < p.pieces.size(); ++i) {
+                DPiece pc = p.pieces[i];
+                fix(pc.mat);
+                fix(pc.x);
+                Pc[i] = pc;
+            }
+        }));
+    for (auto &p : parts) M->paths.insert(M->paths.end(), p->paths.begin(), p->paths.end());
+    for (auto &f : fut) f.get();
     return M;
 }
 

@@ -7,6 +7,9 @@
 // block structure.  csrc/lu.cu executes the DAG in one persistent kernel.
 #pragma once
 
+#include <sys/mman.h>
+
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -14,6 +17,45 @@
 #include "core.h"
 
 namespace lh {
+
+// Allocator for the planner's large arrays (tens of millions of tasks): 2 MB-aligned blocks
+// advised for transparent huge pages (far fewer first-touch faults when several planner
+// threads fill them), and default-initialising construct (resize does not zero-fill).
+template <class T>
+struct HugeAlloc {
+    using value_type = T;
+    HugeAlloc() = default;
+    template <class U>
+    HugeAlloc(const HugeAlloc<U> &) {}
+    T *allocate(size_t n) {
+        const size_t bytes = n * sizeof(T), huge = (size_t)1 << 21;
+        if (bytes >= huge) {
+            const size_t sz = (bytes + huge - 1) / huge * huge;
+            void *p = std::aligned_alloc(huge, sz);
+            if (!p) throw std::bad_alloc();
+            madvise(p, sz, MADV_HUGEPAGE);
+            return static_cast<T *>(p);
+        }
+        void *p = std::malloc(bytes ? bytes : 1);
+        if (!p) throw std::bad_alloc();
+        return static_cast<T *>(p);
+    }
+    void deallocate(T *p, size_t) { std::free(p); }
+    template <class U>
+    void construct(U *p) {
+        ::new (static_cast<void *>(p)) U;
+    }
+    template <class U, class... Args>
+    void construct(U *p, Args &&...args) {
+        ::new (static_cast<void *>(p)) U(std::forward<Args>(args)...);
+    }
+    template <class U>
+    bool operator==(const HugeAlloc<U> &) const { return true; }
+    template <class U>
+    bool operator!=(const HugeAlloc<U> &) const { return false; }
+};
+template <class T>
+using hvec = std::vector<T, HugeAlloc<T>>;
 
 enum Base : int8_t { B_F = 0, B_TMP = 1, B_RHS = 2, B_X = 3, B_INV = 4 };
 constexpr int NBASE = 5;
@@ -60,9 +102,9 @@ struct DPiece {     // SEGMUL piece: Y += alpha * mat * (X rows or W)
 };
 
 struct Plan {
-    std::vector<DTask> tasks;
-    std::vector<int32_t> deps;
-    std::vector<DPiece> pieces;
+    hvec<DTask> tasks;
+    hvec<int32_t> deps;
+    hvec<DPiece> pieces;
     std::vector<std::string> paths;
     i64 temp_len = 0;
     int32_t nslots_total = 0;  // rank slots: F, X, temps

@@ -32,16 +32,21 @@ struct PView {
     PView T() const;
 };
 
+// Per-object row-interval state for dependency tracking: the object's rows are covered by
+// contiguous segments, each with its last writer and the readers since that write (up to
+// four inline).  Objects are indexed densely (F / X block storage, the right-hand side,
+// temporaries).
 struct DepTracker {
     struct Seg {
-        i64 end;
+        i64 a, b;
         int32_t writer;
-        std::vector<int32_t> readers;
+        int32_t nr;
+        int32_t rd[4];
+        std::vector<int32_t> *more;  // readers beyond four (rare)
     };
-    std::unordered_map<u64, std::map<i64, Seg>> objs;
-    std::vector<std::map<i64, Seg>> dense;
-    u64 dense_limit = 0;
+    std::vector<std::vector<Seg>> objs;
     void access(int32_t task, u64 obj, i64 a, i64 b, bool write, std::vector<int32_t> &out);
+    ~DepTracker();
 };
 
 struct Mref {
@@ -129,6 +134,7 @@ struct Planner {
     void finalize();
     PlanStream *stream = nullptr;
     size_t cut_task = 0, cut_piece = 0;
+    std::vector<int32_t> dbuf;  // emit's dependency scratch
     void cut_chunk();
 };
 void assign_priorities(Plan &P);
