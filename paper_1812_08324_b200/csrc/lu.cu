@@ -1400,6 +1400,8 @@ struct PlanJob {
     std::shared_ptr<Plan> inv[2];
     HMat Z;
     std::shared_ptr<Plan> prop;
+    bool prop_uploaded = false;  // device copies made by the planning thread (own stream)
+    int device = -1;             // device of the thread that assembled the matrix
     PlanStream lu_stream;  // the H-LU plan in chunks, when hlu() arrives before planning ends
     std::future<void> f_lu, f_inv, f_prop;
     std::string error, inv_error, prop_error;
@@ -1452,10 +1454,23 @@ void start_background_plans(HMat &H) {
             j->lu_stream.cv.notify_all();
         }
     });
+    cudaGetDevice(&j->device);
     job->f_prop = std::async(std::launch::async, [j] {
         try {
             block_layout(j->Z, j->fshadow, 2, KA_MAX);
             j->prop = plan_propagator(j->fshadow, j->Z, 1e-10);
+            // upload on a stream of this thread once the H-LU planning (and with it the
+            // streamed H-LU chunk uploads) is done: the copies overlap the H-LU's last chunks
+            if (j->device >= 0 && !getenv("LEVYH_NO_BG_UPLOAD")) {
+                j->f_lu.wait();
+                LH_CUDA(cudaSetDevice(j->device));
+                cudaStream_t st;
+                LH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+                j->prop->upload(st);
+                LH_CUDA(cudaStreamSynchronize(st));
+                LH_CUDA(cudaStreamDestroy(st));
+                j->prop_uploaded = true;
+            }
         } catch (const std::exception &e) {
             j->prop_error = e.what();
         }
@@ -1742,6 +1757,7 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
     auto Z = std::make_shared<HMat>();
     std::shared_ptr<Plan> P;
+    bool uploaded = false;
     if (job && job->f_prop.valid()) {
         job->f_prop.wait();
         if (job->prop_error.empty() && job->prop) {
@@ -1749,26 +1765,40 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
             Z->nslots = job->Z.nslots;
             Z->arena_len = job->Z.arena_len;
             P = std::move(job->prop);
-            if (eps2 != 1e-10) patch_eps(*P, eps2);
+            uploaded = job->prop_uploaded;
+            if (eps2 != 1e-10) {
+                patch_eps(*P, eps2);
+                if (uploaded)  // refresh the device task array
+                    LH_CUDA(cudaMemcpyAsync(P->d_tasks, P->tasks.data(), sizeof(DTask) * P->tasks.size(),
+                                            cudaMemcpyHostToDevice, ctx.stream));
+            }
         }
     }
     if (!P) {
         block_layout(*Z, F, 2, KA_MAX);
         P = plan_propagator(F, *Z, eps2);
     }
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    auto ta = now();
     Z->d_arena = dalloc<double>(std::max<i64>(Z->arena_len, 1));
     Z->d_ranks = dalloc<int32_t>(std::max(Z->nslots, 1));
     LH_CUDA(cudaMemsetAsync(Z->d_ranks, 0, sizeof(int32_t) * std::max(Z->nslots, 1), ctx.stream));
-    P->upload(ctx.stream);
-    auto t0 = std::chrono::steady_clock::now();
+    if (!uploaded) P->upload(ctx.stream);
+    auto t0 = now();
     run_plan(ctx, *P, F, Z.get(), nullptr, -1, "propagator");
     Z->sync_ranks(ctx.stream);
+    auto t1 = now();
     Z->lu_stats[0] = (double)P->tasks.size();
     Z->lu_stats[1] = P->build_seconds;
     Z->lu_stats[2] = (double)P->temp_len * 8.0;
-    Z->lu_stats[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    Z->lu_stats[3] = sec(t0, t1);
     P.reset();
+    auto t2 = now();
     S.mvZ = build_mv_plan(*Z, Z->leafblocks, ctx.stream);
+    if (getenv("LEVYH_PLAN_VERBOSE"))
+        fprintf(stderr, "[levyh] propagator: alloc+upload %.3f s, exec %.3f s, free plan %.3f s, "
+                        "matvec plan %.3f s\n", sec(ta, t0), sec(t0, t1), sec(t1, t2), sec(t2, now()));
     S.Z = Z;
     if (!S.tmp) {
         S.tmp_len = F.nrows;
