@@ -1391,6 +1391,15 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
 void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap);
 void block_layout(HMat &X, const HMat &F, int part, int kcap);
 
+// column capacity of the propagator's low-rank blocks: rank + sketch width (14) before each
+// recompression; the eps2 ranks of Z stay <= ~10 on these operators (LEVYH_PROP_KCAP overrides)
+static int prop_kcap() {
+    static const int v = getenv("LEVYH_PROP_KCAP") ? std::min(std::max(atoi(getenv("LEVYH_PROP_KCAP")), 16),
+                                                              (int)KA_MAX)
+                                                   : 32;
+    return v;
+}
+
 struct PlanJob {
     HMat shadow;   // structure-only copy the H-LU planner mutates (no device memory)
     HMat fshadow;  // the factor's structure as the H-LU leaves it (mark_lu_leaves), read-only
@@ -1457,7 +1466,7 @@ void start_background_plans(HMat &H) {
     cudaGetDevice(&j->device);
     job->f_prop = std::async(std::launch::async, [j] {
         try {
-            block_layout(j->Z, j->fshadow, 2, KA_MAX);
+            block_layout(j->Z, j->fshadow, 2, prop_kcap());
             j->prop = plan_propagator(j->fshadow, j->Z, 1e-10);
             // upload on a stream of this thread once the H-LU planning (and with it the
             // streamed H-LU chunk uploads) is done: the copies overlap the H-LU's last chunks
@@ -1775,7 +1784,7 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
         }
     }
     if (!P) {
-        block_layout(*Z, F, 2, KA_MAX);
+        block_layout(*Z, F, 2, prop_kcap());
         P = plan_propagator(F, *Z, eps2);
     }
     auto now = [] { return std::chrono::steady_clock::now(); };
