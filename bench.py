@@ -51,6 +51,11 @@ CFG4 = dict(workload="cfg4: fractional Laplacian s=0.5 on [-1,1], N=2^18-1, a=b=
                      "amplitudes N(0,1)), leaf 64, eta 1, ACA tol 1e-10, fp64",
             n=2 ** 17, K=256, leaf=64, eps1=1e-10, eps2=1e-10)
 METRIC4 = "Crank-Nicolson steps/s of the 256-RHS batch at N=2^18 (cfg4); FP64 tensor (DMMA) roofline"
+CFG5 = dict(workload="cfg5: fractional Laplacian s=0.8 on [-1,1], N=2^22-1, a=0.1 b=c=0, dt=h, leaf 128, "
+                     "eta 1, ACA tol 1e-10, fp64, u0=(1-x^2)_+^3; phases: assembly (sharded across ranks), "
+                     "H-LU, 50 CN steps",
+            n=2 ** 21, leaf=128, eps1=1e-10, eps2=1e-10, steps=50)
+METRIC5 = "cfg5 (N=2^22): assembly + H-LU time, CN steps/s"
 
 
 def log(*a):
@@ -467,6 +472,87 @@ def run_cfg4(args, world, rank, local):
         print(json.dumps(out), flush=True)
 
 
+def run_cfg5(args, world, rank, local):
+    """BASELINE configs[4]: the large-N phases.  Assembly (symbol + ACA) is sharded across the
+    ranks with an NCCL all-gather of the factors; H-LU and the 50 steps run on every rank.
+    The step uses the reference algorithm (matvec + substitution solve) unless --method says
+    otherwise: at N = 2^22 a propagator next to A+ and A- exceeds one GPU's memory."""
+    import torch
+
+    import paper_1812_08324_b200 as P
+
+    cfg = CFG5
+    method = args.method if args.method_set else "substitution"
+    t0 = time.perf_counter()
+    s = P.FracCNSystem(P.power_measure(1, 0.8), 0.1, 0.0, 0.0, cfg["n"], 1.0 / cfg["n"],
+                       distributed=world > 1)
+    torch.cuda.synchronize()
+    t_symbol = time.perf_counter() - t0
+    # low-rank capacity 24 (H-LU updates add two ranks of ~7): the factor, A-, and A-'s packed
+    # matvec copy then fit one GPU at N = 2^22
+    hc = P.HConfig(n_min=cfg["leaf"], eps1=cfg["eps1"], kcap=int(os.environ.get("LEVYH_CFG5_KCAP", "24")))
+    t1 = time.perf_counter()
+    Hp, Hm = s.build_pair(hc)
+    torch.cuda.synchronize()
+    t_aca = time.perf_counter() - t1
+    mem_p = P.memory_report(Hp)
+    t2 = time.perf_counter()
+    F = P.hlu(Hp, cfg["eps2"])
+    torch.cuda.synchronize()
+    t_lu = time.perf_counter() - t2
+    st = np.zeros(5)
+    P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st))
+    t3 = time.perf_counter()
+    if method == "propagator":
+        F.prepare_propagator()
+    elif method == "inverse":
+        F.prepare_inverse()
+    torch.cuda.synchronize()
+    t_prep = time.perf_counter() - t3
+    ctx, L, N = Hm.ctx, P._lib.lib(), s.N
+    u0 = np.maximum(1.0 - s.x ** 2, 0.0) ** 3
+    u = torch.from_numpy(u0.copy()).cuda()
+    mcode = P.SOLVE_METHODS[method]
+    k = min(args.steps, cfg["steps"])
+
+    def steps(kk):
+        P._lib.check(L.lh_cn_steps(ctx.h, Hm.handle, F.h.handle, u.data_ptr(), N, 1, int(kk), mcode), ctx.h)
+
+    steps(1)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        lib_stream = ctx.torch_stream()
+        start.record(lib_stream)
+        steps(k)
+        end.record(lib_stream)
+        torch.cuda.synchronize()
+        ms = start.elapsed_time(end)
+    ms = max_over_ranks(ms, world, "cuda")
+    free_b, total_b = torch.cuda.mem_get_info()
+    out = {"metric": METRIC5, "value": round(world * k / (ms / 1000.0), 3), "unit": "steps/s",
+           "n_gpus": world, "steps": k, "warmup": 1, "ms_per_step": round(ms / k, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (BASELINE.json configs[4]; closed-form inputs, no dataset)",
+           "config": {"workload": cfg["workload"], "N": N, "leaf": cfg["leaf"], "solve": method,
+                      "parallelism": f"assembly sharded over {world} rank(s); H-LU and steps replicated"},
+           "clocks": sampler.summary(),
+           "phases": {"symbol_s": round(t_symbol, 3), "aca_s": round(t_aca, 3),
+                      "assembly_s": round(t_symbol + t_aca, 3), "hlu_s": round(t_lu, 3),
+                      "hlu_plan_s": round(float(st[1]), 3), "hlu_exec_s": round(float(st[3]), 3),
+                      "hlu_tasks": int(st[0]), "prepare_s": round(t_prep, 3),
+                      "assembly_sharding": (Hp.shard_stats if getattr(Hp, "shard_stats", None)
+                                            else "unsharded (1 rank)"),
+                      "stored_scalars_plus": mem_p["stored_scalars"],
+                      "device_mem_used_gb": round((total_b - free_b) / 1e9, 2)}}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def run_reference(args, world, rank, local):
     """--impl reference: the reference algorithm on host cores (rank 0 only)."""
     if rank != 0:
@@ -511,10 +597,13 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--ref-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4"])
-    ap.add_argument("--method", default="propagator", choices=["propagator", "inverse"],
-                    help="per-step solve: one H-matvec of Z=(A+)^-1 (default) or A- + L^-1 + U^-1")
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--method", default=None, choices=["propagator", "inverse", "substitution"],
+                    help="per-step solve: one H-matvec of Z=(A+)^-1 (default; cfg5: substitution)")
     args = ap.parse_args()
+    args.method_set = args.method is not None
+    if args.method is None:
+        args.method = "propagator"
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
     world, rank, local = dist_setup()
@@ -522,6 +611,8 @@ def main():
         run_reference(args, world, rank, local)
     elif args.workload == "cfg4":
         run_cfg4(args, world, rank, local)
+    elif args.workload == "cfg5":
+        run_cfg5(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
     if world > 1:

@@ -382,6 +382,7 @@ int lh_hmat_memory(lh_ctx *ctx, const lh_hmat *h, int64_t *stats) {
         const_cast<HMat &>(H).sync_ranks(ctx->c.stream);
         int64_t nd_ = 0, nl = 0, sc = 0, nh = 0;
         for (const Node &nd : H.nodes) {
+            if (nd.vpar >= 0) continue;  // virtual children of refined leaves
             if (nd.kind == K_HIER) {
                 ++nh;
             } else if (nd.kind == K_LR) {
@@ -471,6 +472,25 @@ int lh_hmat_export_arena(lh_ctx *ctx, const lh_hmat *h, double *arena, int32_t *
             LH_CUDA(cudaMemcpyAsync(perm, H.d_perm, sizeof(int32_t) * H.perm_len,
                                     cudaMemcpyDeviceToHost, s));
         LH_CUDA(cudaStreamSynchronize(s));
+        if (perm && H.perm_len) {
+            // a refined leaf factored as 64-row halves: its net permutation is the halves'
+            // permutations, each offset by the half's first row in the leaf
+            for (int32_t b : H.leafblocks) {
+                const Node &nd = H.nodes[b];
+                if (nd.kind != K_FDENSE || nd.kid[0] < 0) continue;
+                std::vector<int32_t> st{b};
+                while (!st.empty()) {
+                    const Node &q = H.nodes[st.back()];
+                    st.pop_back();
+                    if (q.kid[0] >= 0) {
+                        st.push_back(q.kid[3]);
+                        st.push_back(q.kid[0]);
+                    } else if (q.r0 > nd.r0) {
+                        for (i64 i = 0; i < q.m; ++i) perm[q.poff + i] += (int32_t)(q.r0 - nd.r0);
+                    }
+                }
+            }
+        }
     });
 }
 

@@ -78,6 +78,10 @@ struct Node {
     i64 poff;             // FDENSE: offset of the int32 net row permutation
     i64 ioff = -1;        // FDENSE: offset of the packed leaf inverse (L^-1 strict lower, U^-1 upper)
     int32_t depth;        // block-tree depth
+    // H-arithmetic refinement of a dense leaf larger than 64 x 64 (plan.cpp: refine_dense_leaves):
+    // the leaf keeps its kind for everything else, kid[] then name 2 x 2 virtual children whose
+    // storage is a sub-block of the leaf's (doff relative to the virtual parent vpar)
+    int32_t vpar = -1;
 };
 
 struct Ctx;
@@ -99,6 +103,7 @@ struct HMat {
     double *d_inv = nullptr;          // FDENSE packed leaf inverses
     i64 inv_len = 0;
     bool factored = false;
+    bool refined = false;             // dense leaves > 64 split for the H-arithmetic planner
     double lu_stats[5] = {0, 0, 0, 0, 0};  // tasks, plan s, temp bytes, exec s, chunks
     // lazily built plans (opaque; see matvec.cu / plan.cpp)
     std::shared_ptr<void> mv_plan;

@@ -1052,6 +1052,16 @@ __device__ void task_rand(const ExecArgs &A, const DTask &T) {
     }
 }
 
+// T_CHECK: fail with the task's path if any |v0| exceeds alpha
+__device__ void task_check(const ExecArgs &A, const DTask &T, int tid) {
+    const DView &v = T.v[0];
+    const double *G = vp(A, v);
+    const i64 n = (i64)v.rows * v.cols;
+    bool bad = false;
+    for (i64 e = threadIdx.x; e < n; e += NT) bad |= fabs(G[vi(v, e % v.rows, e / v.rows)]) > T.alpha;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) set_err(A, LH_EINVAL, tid, T.path);
+}
+
 __device__ void task_orth(const ExecArgs &A, const DTask &T, double *sm) {
     const DView &dv = T.v[0];
     dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(sm);
@@ -1144,6 +1154,7 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
             case T_IDENT: task_ident(A, T); break;
             case T_RAND: task_rand(A, T); break;
             case T_ORTH: task_orth(A, T, sm); break;
+            case T_CHECK: task_check(A, T, t); break;
             default: break;
         }
         __syncthreads();
@@ -1379,6 +1390,8 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     }
     if (err[0] == LH_ERANK)
         throw Error(LH_ERANK, "low-rank capacity exceeded during H-arithmetic (increase kcap)");
+    if (err[0] == LH_EINVAL && err[2] >= 0 && err[2] < (int)P.paths.size())
+        throw Error(LH_EINVAL, P.paths[err[2]]);
     if (err[0] != 0) throw Error(err[0], "executor failure (task " + std::to_string(err[1]) + ")");
 }
 
@@ -1417,6 +1430,7 @@ struct PlanJob {
 };
 
 static void copy_structure(HMat &D, const HMat &S) {
+    D.refined = S.refined;
     D.rt = S.rt;
     D.ct = S.ct;
     D.rt_hold = S.rt_hold;
@@ -1442,6 +1456,7 @@ static void patch_eps(Plan &P, double eps2) {
 void start_background_plans(HMat &H) {
     if (H.nrows != H.ncols || H.factored || getenv("LEVYH_NO_BG_PLAN")) return;
     auto job = std::make_shared<PlanJob>();
+    refine_dense_leaves(H);
     copy_structure(job->shadow, H);
     copy_structure(job->fshadow, H);
     PlanJob *j = job.get();
@@ -1681,6 +1696,12 @@ void block_layout(HMat &X, const HMat &F, int part, int kcap) {
     X.ncols = F.ncols;
     X.root = F.root;
     X.nodes = F.nodes;
+    X.refined = F.refined;
+    for (Node &nd : X.nodes)  // virtual children of refined leaves: plain dense storage here
+        if (nd.vpar >= 0) {
+            nd.kind = K_DENSE;
+            nd.ioff = -1;
+        }
     i64 off = 0;
     int32_t slots = 0;
     walk_leaves(X);

@@ -144,13 +144,96 @@ u64 Planner::key(int base, i64 id, int which) const {
     return (u64)(3 * (nF + nX) + 1 + id);  // B_TMP
 }
 
+// storage of a dense leaf or of a virtual child of a refined leaf: absolute offset, ld
+void dense_loc(const HMat &H, int32_t b, i64 &off, i64 &ld) {
+    off = 0;
+    int32_t q = b;
+    while (H.nodes[q].vpar >= 0) {
+        off += H.nodes[q].doff;
+        q = H.nodes[q].vpar;
+    }
+    off += H.nodes[q].doff;
+    ld = H.nodes[q].m;
+}
+
+// Dense leaves larger than 64 x 64 are split 2 x 2 for the H-arithmetic planner (recursively):
+// along the cluster tree where the leaf's cluster has children, else at row / column 64.
+// The split leaf keeps its kind for the structure, the matvec and the exports; only the
+// planner recurses into it, so every task runs on the 64-row fast paths.  (Leaf pivoting then
+// acts per 64-row half: identical to partial pivoting over the whole leaf whenever that picks
+// no cross-half pivot, which a T_CHECK task verifies after the leaf's L21 solve.)
+void refine_dense_leaves(HMat &H) {
+    if (H.refined) return;
+    H.refined = true;
+    if (getenv("LEVYH_NO_LEAF_SPLIT")) return;
+    std::vector<int32_t> todo;
+    for (int32_t b : H.leafblocks) {
+        const Node &nd = H.nodes[b];
+        if ((nd.kind == K_DENSE || nd.kind == K_FDENSE) && nd.kid[0] < 0 && nd.m > 64 && nd.n > 64)
+            todo.push_back(b);
+    }
+    auto split = [](const Tree *T, int32_t cl, i64 size, int32_t &k0, int32_t &k1) -> i64 {
+        if (T && cl >= 0 && !T->nodes[cl].leaf()) {
+            k0 = T->nodes[cl].kid[0];
+            k1 = T->nodes[cl].kid[1];
+            return T->nodes[k0].size();
+        }
+        k0 = k1 = -1;
+        return std::min<i64>(64, size / 2 > 0 ? 64 : size);
+    };
+    while (!todo.empty()) {
+        const int32_t b = todo.back();
+        todo.pop_back();
+        const Node p = H.nodes[b];
+        i64 poff, pld;
+        dense_loc(H, b, poff, pld);
+        (void)poff;
+        int32_t r0c, r1c, c0c, c1c;
+        const i64 rs = split(H.rt, p.rcl, p.m, r0c, r1c), cs = split(H.ct, p.ccl, p.n, c0c, c1c);
+        if (rs <= 0 || rs >= p.m || cs <= 0 || cs >= p.n) continue;
+        int32_t kids[4];
+        for (int q = 0; q < 4; ++q) {
+            Node c;
+            std::memset(&c, 0, sizeof(c));
+            const bool lo = q >> 1, rt = q & 1;
+            c.kind = K_DENSE;
+            c.rcl = lo ? r1c : r0c;
+            c.ccl = rt ? c1c : c0c;
+            c.r0 = p.r0 + (lo ? rs : 0);
+            c.c0 = p.c0 + (rt ? cs : 0);
+            c.m = lo ? p.m - rs : rs;
+            c.n = rt ? p.n - cs : cs;
+            for (auto &k : c.kid) k = -1;
+            c.doff = (lo ? rs : 0) + (rt ? cs : 0) * pld;
+            c.uoff = c.voff = -1;
+            c.rslot = -1;
+            c.ioff = -1;
+            c.depth = p.depth + 1;
+            c.vpar = b;
+            kids[q] = (int32_t)H.nodes.size();
+            H.nodes.push_back(c);
+            if (c.m > 64 && c.n > 64) todo.push_back(kids[q]);
+        }
+        Node &pp = H.nodes[b];
+        for (int q = 0; q < 4; ++q) pp.kid[q] = kids[q];
+        pp.rs = rs;
+        pp.cs = cs;
+    }
+}
+
 PView Planner::dense_view(const Mref &M, int32_t b) const {
     const Node &nd = M.H->nodes[b];
+    i64 off, ld;
+    dense_loc(*M.H, b, off, ld);
     PView v{};
-    v.d = DView{nd.doff, (int32_t)nd.m, (int32_t)nd.n, (int32_t)nd.m, -1, (int8_t)M.base, 0, 0};
+    v.d = DView{off, (int32_t)nd.m, (int32_t)nd.n, (int32_t)ld, -1, (int8_t)M.base, 0, 0};
     v.obj = key(M.base, b, 0);
     v.r0 = 0;
     v.whole = false;
+    if (nd.kind != K_HIER && nd.kid[0] >= 0) {
+        v.vnode = b;
+        v.vh = M.H;
+    }
     return v;
 }
 PView Planner::u_view(const Mref &M, int32_t b) const {
@@ -235,6 +318,18 @@ int32_t Planner::emit(DTask t, std::initializer_list<std::pair<const PView *, bo
         i64 a = v.whole ? 0 : v.r0;
         i64 b = v.whole ? INT64_MAX : v.r0 + v.d.rows;
         deps.access(id, v.obj, a, b, w, d);
+        if (v.vnode >= 0) {  // the refined leaf's storage is also its virtual children's
+            std::vector<int32_t> st{v.vnode};
+            while (!st.empty()) {
+                const Node &q = v.vh->nodes[st.back()];
+                st.pop_back();
+                for (int k = 0; k < 4; ++k)
+                    if (q.kid[k] >= 0) {
+                        deps.access(id, key(v.d.base, q.kid[k], 0), 0, INT64_MAX, w, d);
+                        st.push_back(q.kid[k]);
+                    }
+            }
+        }
         if (v.tmp >= 0) {
             auto it = temps.find(v.tmp);
             if (it != temps.end()) {
@@ -305,7 +400,7 @@ static DTask mk(int32_t type) {
 // leaf blocks of a subtree with offsets relative to the subtree root
 void Planner::leaves_of(const Mref &M, int32_t b, i64 r, i64 c, std::vector<LeafRef> &out) const {
     const Node &nd = M.H->nodes[b];
-    if (nd.kind == K_HIER) {
+    if (hier(nd)) {
         leaves_of(M, nd.kid[0], r, c, out);
         leaves_of(M, nd.kid[1], r, c + nd.cs, out);
         leaves_of(M, nd.kid[2], r + nd.rs, c, out);
@@ -318,8 +413,15 @@ void Planner::leaves_of(const Mref &M, int32_t b, i64 r, i64 c, std::vector<Leaf
 // row segments (leaf clusters) of a cluster subtree, relative to its start
 void Planner::segments_of(const Tree &T, int32_t cl, std::vector<std::pair<i64, i64>> &out) const {
     const Cluster &c = T.nodes[cl];
+    auto leaf_rows = [&](i64 lo, i64 size) {  // leaf clusters > 64 rows: 64-row segments
+        if (!F.refined || getenv("LEVYH_NO_LEAF_SPLIT")) {
+            out.push_back({lo, size});
+            return;
+        }
+        for (i64 a = 0; a < size; a += 64) out.push_back({lo + a, std::min<i64>(64, size - a)});
+    };
     if (c.leaf()) {
-        out.push_back({0, c.size()});
+        leaf_rows(0, c.size());
         return;
     }
     std::vector<int32_t> st{cl};
@@ -327,7 +429,7 @@ void Planner::segments_of(const Tree &T, int32_t cl, std::vector<std::pair<i64, 
         int32_t k = st.back();
         st.pop_back();
         const Cluster &q = T.nodes[k];
-        if (q.leaf()) out.push_back({q.lo - c.lo, q.size()});
+        if (q.leaf()) leaf_rows(q.lo - c.lo, q.size());
         else {
             st.push_back(q.kid[1]);
             st.push_back(q.kid[0]);
@@ -379,7 +481,9 @@ void Planner::segmul(const PView &Y, const Mref &M, int32_t a, const PView &X, b
     }
     // phase 2: one task per output row segment; leaves bucketed by the segments they cover
     std::vector<std::pair<i64, i64>> segs;
-    segments_of(trans ? *M.H->ct : *M.H->rt, trans ? A.ccl : A.rcl, segs);
+    const int32_t scl = trans ? A.ccl : A.rcl;
+    if (scl >= 0) segments_of(trans ? *M.H->ct : *M.H->rt, scl, segs);
+    else segs.push_back({0, trans ? A.n : A.m});  // virtual child of a refined leaf (<= 64)
     std::vector<i64> starts(segs.size());
     for (size_t k = 0; k < segs.size(); ++k) starts[k] = segs[k].first;
     std::vector<std::vector<int32_t>> bucket(segs.size());
@@ -443,7 +547,7 @@ void Planner::segmul(const PView &Y, const Mref &M, int32_t a, const PView &X, b
 void Planner::solve_dense(const Mref &T, int32_t t, const PView &B, int mode, bool unit,
                           const std::string &path) {
     const Node &nd = T.H->nodes[t];
-    if (nd.kind != K_HIER) {
+    if (!hier(nd)) {
         LH_REQUIRE(nd.kind == K_FDENSE || nd.kind == K_DENSE, LH_ETYPE,
                    "triangular solve needs a dense diagonal leaf at " + path);
         PView Tv = dense_view(T, t);
@@ -469,18 +573,20 @@ void Planner::solve_dense(const Mref &T, int32_t t, const PView &B, int mode, bo
     }
     i64 s = nd.rs;
     PView B1 = B.rows_(0, s), B2 = B.rows_(s, nd.m - s);
+    const bool virt = nd.kind != K_HIER;  // refined leaf: its halves report the leaf's path
+    const std::string p11 = virt ? path : path + ".11", p22 = virt ? path : path + ".22";
     if (mode == 0) {
-        solve_dense(T, nd.kid[0], B1, mode, unit, path + ".11");
+        solve_dense(T, nd.kid[0], B1, mode, unit, p11);
         segmul(B2, T, nd.kid[2], B1, false, -1.0, false);
-        solve_dense(T, nd.kid[3], B2, mode, unit, path + ".22");
+        solve_dense(T, nd.kid[3], B2, mode, unit, p22);
     } else if (mode == 1) {
-        solve_dense(T, nd.kid[3], B2, mode, unit, path + ".22");
+        solve_dense(T, nd.kid[3], B2, mode, unit, p22);
         segmul(B1, T, nd.kid[1], B2, false, -1.0, false);
-        solve_dense(T, nd.kid[0], B1, mode, unit, path + ".11");
+        solve_dense(T, nd.kid[0], B1, mode, unit, p11);
     } else {
-        solve_dense(T, nd.kid[0], B1, mode, unit, path + ".11");
+        solve_dense(T, nd.kid[0], B1, mode, unit, p11);
         segmul(B2, T, nd.kid[1], B1, true, -1.0, false);
-        solve_dense(T, nd.kid[3], B2, mode, unit, path + ".22");
+        solve_dense(T, nd.kid[3], B2, mode, unit, p22);
     }
 }
 
@@ -499,34 +605,37 @@ void Planner::trisolve_left(const Mref &T, int32_t t, const Mref &Bm, int32_t b,
     if (B.kind == K_ZERO) return;
     const int cp = colpart(Bm, b);
     if (cp == 0) return;
-    if (cp == 2 && B.kind != K_HIER) throw Error(LH_EINTERNAL, "column split straddles a leaf");
+    if (cp == 2 && !hier(B)) throw Error(LH_EINTERNAL, "column split straddles a leaf");
     if (B.kind == K_LR) {
         solve_dense(T, t, u_view(Bm, b), mode, unit, path);
         return;
     }
-    if (B.kind == K_DENSE) {
+    const Node &Tn = T.H->nodes[t];
+    if (dense_leaf(B) || !hier(Tn)) {
+        LH_REQUIRE(B.kind == K_DENSE, LH_ETYPE,
+                   "hierarchical right-hand side against a leaf triangle at " + path);
         solve_dense(T, t, dense_view(Bm, b), mode, unit, path);
         return;
     }
-    const Node &Tn = T.H->nodes[t];
-    LH_REQUIRE(Tn.kind == K_HIER, LH_ETYPE,
-               "hierarchical right-hand side against a leaf triangle at " + path);
+    LH_REQUIRE(hier(B), LH_ETYPE, "hierarchical right-hand side against a leaf triangle at " + path);
     const int32_t c00 = Tn.kid[0], c01 = Tn.kid[1], c10 = Tn.kid[2], c11 = Tn.kid[3];
     const int32_t b00 = B.kid[0], b01 = B.kid[1], b10 = B.kid[2], b11 = B.kid[3];
+    const bool virt = Tn.kind != K_HIER;
+    const std::string p11 = virt ? path : path + ".11", p22 = virt ? path : path + ".22";
     if (mode == 0) {
-        trisolve_left(T, c00, Bm, b00, mode, unit, path + ".11");
-        trisolve_left(T, c00, Bm, b01, mode, unit, path + ".11");
+        trisolve_left(T, c00, Bm, b00, mode, unit, p11);
+        trisolve_left(T, c00, Bm, b01, mode, unit, p11);
         schur(Bm, b10, T, c10, Bm, b00);
         schur(Bm, b11, T, c10, Bm, b01);
-        trisolve_left(T, c11, Bm, b10, mode, unit, path + ".22");
-        trisolve_left(T, c11, Bm, b11, mode, unit, path + ".22");
+        trisolve_left(T, c11, Bm, b10, mode, unit, p22);
+        trisolve_left(T, c11, Bm, b11, mode, unit, p22);
     } else {
-        trisolve_left(T, c11, Bm, b10, mode, unit, path + ".22");
-        trisolve_left(T, c11, Bm, b11, mode, unit, path + ".22");
+        trisolve_left(T, c11, Bm, b10, mode, unit, p22);
+        trisolve_left(T, c11, Bm, b11, mode, unit, p22);
         schur(Bm, b00, T, c01, Bm, b10);
         schur(Bm, b01, T, c01, Bm, b11);
-        trisolve_left(T, c00, Bm, b00, mode, unit, path + ".11");
-        trisolve_left(T, c00, Bm, b01, mode, unit, path + ".11");
+        trisolve_left(T, c00, Bm, b00, mode, unit, p11);
+        trisolve_left(T, c00, Bm, b01, mode, unit, p11);
     }
 }
 
@@ -539,28 +648,31 @@ void Planner::trisolve_right_upper(const Mref &T, int32_t t, const Mref &Bm, int
         solve_dense(T, t, v_view(Bm, b), 2, true, path);
         return;
     }
-    if (B.kind == K_DENSE) {
+    const Node &Tn = T.H->nodes[t];
+    if (dense_leaf(B) || !hier(Tn)) {
+        LH_REQUIRE(B.kind == K_DENSE, LH_ETYPE,
+                   "hierarchical right-hand side against a leaf triangle at " + path);
         solve_dense(T, t, dense_view(Bm, b).T(), 2, true, path);
         return;
     }
-    const Node &Tn = T.H->nodes[t];
-    LH_REQUIRE(Tn.kind == K_HIER, LH_ETYPE,
-               "hierarchical right-hand side against a leaf triangle at " + path);
+    LH_REQUIRE(hier(B), LH_ETYPE, "hierarchical right-hand side against a leaf triangle at " + path);
     const int32_t c00 = Tn.kid[0], c01 = Tn.kid[1], c11 = Tn.kid[3];
     const int32_t b00 = B.kid[0], b01 = B.kid[1], b10 = B.kid[2], b11 = B.kid[3];
-    trisolve_right_upper(T, c00, Bm, b00, path + ".11");
-    trisolve_right_upper(T, c00, Bm, b10, path + ".11");
+    const bool virt = Tn.kind != K_HIER;
+    const std::string p11 = virt ? path : path + ".11", p22 = virt ? path : path + ".22";
+    trisolve_right_upper(T, c00, Bm, b00, p11);
+    trisolve_right_upper(T, c00, Bm, b10, p11);
     schur(Bm, b01, Bm, b00, T, c01);
     schur(Bm, b11, Bm, b10, T, c01);
-    trisolve_right_upper(T, c11, Bm, b01, path + ".22");
-    trisolve_right_upper(T, c11, Bm, b11, path + ".22");
+    trisolve_right_upper(T, c11, Bm, b01, p22);
+    trisolve_right_upper(T, c11, Bm, b11, p22);
 }
 
 // hops.py:318-331: C -= U V^T
 void Planner::sub_lowrank(const Mref &Cm, int32_t c, const PView &U, const PView &V) {
     const Node &C = Cm.H->nodes[c];
     if (C.kind == K_ZERO) throw Error(LH_EINTERNAL, "update into a structurally zero block");
-    if (C.kind == K_DENSE) {
+    if (dense_leaf(C)) {
         PView Cv = dense_view(Cm, c);
         DTask t = mk(T_DGEMM);
         t.alpha = -1.0;
@@ -592,7 +704,7 @@ void Planner::sub_lowrank(const Mref &Cm, int32_t c, const PView &U, const PView
 // hops.py:334-345: C -= D
 void Planner::sub_dense(const Mref &Cm, int32_t c, const PView &D) {
     const Node &C = Cm.H->nodes[c];
-    if (C.kind == K_DENSE) {
+    if (dense_leaf(C)) {
         PView Cv = dense_view(Cm, c);
         DTask t = mk(T_DADD);
         t.alpha = -1.0;
@@ -716,8 +828,7 @@ void Planner::schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const 
     const int cp = colpart(Cm, c);
     if (cp == 0) return;
     if (cp == 2) {  // only the block recursion may cross a column split
-        if (!(C.kind == K_HIER && A.kind == K_HIER && B.kind == K_HIER && A.cs == B.rs &&
-              C.rs == A.rs && C.cs == B.cs))
+        if (!(hier(C) && hier(A) && hier(B) && A.cs == B.rs && C.rs == A.rs && C.cs == B.cs))
             throw Error(LH_EINTERNAL, "column split straddles a product update");
     }
     if (A.kind == K_LR) {
@@ -735,9 +846,9 @@ void Planner::schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const 
     } else if (C.kind == K_LR) {
         // dense product into an admissible target: sketched instead of a dense SVD
         lr_sketch_update(Cm, c, &Am, a, &Bm, b, nullptr);
-    } else if (A.kind == K_DENSE && B.kind == K_DENSE) {
+    } else if (dense_leaf(A) && dense_leaf(B)) {
         PView Ad = dense_view(Am, a), Bd = dense_view(Bm, b);
-        if (C.kind == K_DENSE) {
+        if (dense_leaf(C)) {
             PView Cv = dense_view(Cm, c);
             DTask t = mk(T_DGEMM);
             t.alpha = -1.0;
@@ -757,20 +868,20 @@ void Planner::schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const 
             sub_dense(Cm, c, D);
             release(D);
         }
-    } else if (A.kind == K_DENSE) {
+    } else if (dense_leaf(A)) {
         // tmul_dense(B, A.d^T)^T
         PView Ad = dense_view(Am, a);
         PView D = temp(B.n, A.m, -1);
         segmul(D, Bm, b, Ad.T(), true, 1.0, true);
         sub_dense(Cm, c, D.T());
         release(D);
-    } else if (B.kind == K_DENSE) {
+    } else if (dense_leaf(B)) {
         PView Bd = dense_view(Bm, b);
         PView D = temp(A.m, B.n, -1);
         segmul(D, Am, a, Bd, false, 1.0, true);
         sub_dense(Cm, c, D);
         release(D);
-    } else if (C.kind == K_HIER && A.kind == K_HIER && B.kind == K_HIER) {
+    } else if (hier(C) && hier(A) && hier(B)) {
         if (A.cs != B.rs || C.rs != A.rs || C.cs != B.cs) {
             PView Bd = densify(Bm, b);
             PView D = temp(A.m, B.n, -1);
@@ -798,7 +909,7 @@ void Planner::schur(const Mref &Cm, int32_t c, const Mref &Am, int32_t a, const 
 void Planner::lu_block(int32_t b, const std::string &path) {
     Node &nd = F.nodes[b];
     Mref Fm{&F, B_F, 0};
-    if (nd.kind == K_DENSE) {
+    if (dense_leaf(nd)) {
         LH_REQUIRE(nd.m == nd.n, LH_EINTERNAL, "non-square diagonal leaf");
         PView D = dense_view(Fm, b);
         DTask t = mk(T_GETRF);
@@ -817,14 +928,33 @@ void Planner::lu_block(int32_t b, const std::string &path) {
         nd.kind = K_FDENSE;
         return;
     }
-    LH_REQUIRE(nd.kind == K_HIER, LH_ETYPE,
+    LH_REQUIRE(hier(nd), LH_ETYPE,
                std::string("cannot LU-factorize diagonal block of type ") +
                    (nd.kind == K_LR ? "LowRank" : "Dense") + " at " + path);
-    lu_block(nd.kid[0], path + ".11");
-    trisolve_left(Fm, nd.kid[0], Fm, nd.kid[1], 0, true, path + ".12");
-    trisolve_right_upper(Fm, nd.kid[0], Fm, nd.kid[2], path + ".21");
-    schur(Fm, nd.kid[3], Fm, nd.kid[2], Fm, nd.kid[1]);
-    lu_block(nd.kid[3], path + ".22");
+    const bool virt = nd.kind != K_HIER;  // refined dense leaf: blocked LU of its halves
+    const int32_t k0 = nd.kid[0], k1 = nd.kid[1], k2 = nd.kid[2], k3 = nd.kid[3];
+    lu_block(k0, virt ? path : path + ".11");
+    trisolve_left(Fm, k0, Fm, k1, 0, true, virt ? path : path + ".12");
+    trisolve_right_upper(Fm, k0, Fm, k2, virt ? path : path + ".21");
+    if (virt) {
+        // partial pivoting over the whole leaf would have picked a pivot from the lower half
+        // iff some |L21| > 1: fail loudly rather than return a differently pivoted factor
+        PView L21 = dense_view(Fm, k2);
+        DTask t = mk(T_CHECK);
+        t.alpha = 1.0 + 1e-12;
+        t.v[0] = L21.d;
+        t.path = add_path("leaf LU needs pivoting across its 64-row halves at " + path +
+                          " (set LEVYH_NO_LEAF_SPLIT=1)");
+        emit(t, {{&L21, false}});
+    }
+    schur(Fm, k3, Fm, k2, Fm, k1);
+    lu_block(k3, virt ? path : path + ".22");
+    if (virt) {  // the leaf itself now holds its LU (factored for every other consumer)
+        Node &me = F.nodes[b];
+        me.kind = K_FDENSE;
+        me.poff = F.nodes[k0].poff;
+        me.ioff = -1;
+    }
 }
 
 int32_t Planner::add_path(const std::string &s) {
@@ -902,6 +1032,7 @@ int64_t critical_path(const Plan &P) {
 // ---------------------------------------------------------------------------
 std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out, PlanStream *stream) {
     auto t0 = std::chrono::steady_clock::now();
+    refine_dense_leaves(F);
     Planner pl(F, nullptr);
     pl.eps2 = eps2;
     pl.stream = stream;
@@ -917,6 +1048,7 @@ std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out, PlanStre
 // forward (unit L with leaf pivots) + backward (U) substitution on a dense RHS (hops.py:424-432)
 std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap) {
     auto t0 = std::chrono::steady_clock::now();
+    refine_dense_leaves(F);
     Planner pl(F, nullptr);
     Mref Fm{&F, B_F, 0};
     PView B{};
@@ -936,6 +1068,7 @@ std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap) {
 std::shared_ptr<Plan> plan_trisolve_dense(HMat &T, i64 n, int nrhs_cap, int mode, bool unit,
                                           const std::string &root) {
     auto t0 = std::chrono::steady_clock::now();
+    refine_dense_leaves(T);
     Planner pl(T, nullptr);
     Mref Tm{&T, B_F, 0};
     PView B{};
@@ -1026,6 +1159,7 @@ static std::shared_ptr<Plan> plan_propagator_part(HMat &F, HMat &Z, double eps2,
 }
 
 static void structure_copy(HMat &D, const HMat &S) {
+    D.refined = S.refined;
     D.rt = S.rt;
     D.ct = S.ct;
     D.rt_hold = S.rt_hold;
@@ -1179,7 +1313,7 @@ std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_par
 // reads the factor start before the H-LU plan exists
 static void mark_rec(HMat &F, int32_t b, i64 &perm_len, i64 &inv_len) {
     Node &nd = F.nodes[b];
-    if (nd.kind == K_DENSE) {
+    if (dense_leaf(nd)) {
         nd.poff = perm_len;
         perm_len += nd.m;
         if (nd.m <= LEAF_INV_MAX) {
@@ -1189,12 +1323,18 @@ static void mark_rec(HMat &F, int32_t b, i64 &perm_len, i64 &inv_len) {
         nd.kind = K_FDENSE;
         return;
     }
-    LH_REQUIRE(nd.kind == K_HIER, LH_ETYPE, "cannot LU-factorize a low-rank diagonal block");
+    LH_REQUIRE(hier(nd), LH_ETYPE, "cannot LU-factorize a low-rank diagonal block");
     mark_rec(F, nd.kid[0], perm_len, inv_len);
     mark_rec(F, nd.kid[3], perm_len, inv_len);
+    if (nd.kind != K_HIER) {  // refined leaf (see lu_block)
+        nd.kind = K_FDENSE;
+        nd.poff = F.nodes[nd.kid[0]].poff;
+        nd.ioff = -1;
+    }
 }
 
 void mark_lu_leaves(HMat &F, i64 &perm_len, i64 &inv_len) {
+    refine_dense_leaves(F);
     perm_len = inv_len = 0;
     mark_rec(F, F.root, perm_len, inv_len);
     F.inv_len = inv_len;

@@ -82,6 +82,7 @@ enum TaskType : int32_t {
     T_NOP = 10,    // dependency barrier (temp-buffer reuse)
     T_RAND = 11,   // v0 <- N(0,1) samples, seed aux
     T_ORTH = 12,   // v0 (m x p) <- Q of its CGS2 QR, in place
+    T_CHECK = 13,  // fail (path) if any |v0| > 1: a refined leaf's L21 needs cross-half pivoting
 };
 
 struct DTask {

@@ -27,6 +27,8 @@ struct PView {
     i64 r0;       // first row of this view inside its object
     bool whole;   // transposed: dependency on the whole object
     int32_t tmp = -1;
+    int32_t vnode = -1;            // refined dense leaf: accesses also cover its virtual children
+    const HMat *vh = nullptr;
     PView rows_(i64 a, i64 cnt) const;
     PView cols_(i64 a, i64 cnt) const;
     PView T() const;
@@ -138,6 +140,14 @@ struct Planner {
     void cut_chunk();
 };
 void assign_priorities(Plan &P);
+
+// a node the planner recurses into: a real hierarchical block or a refined dense leaf
+inline bool hier(const Node &n) {
+    return n.kind == K_HIER || ((n.kind == K_DENSE || n.kind == K_FDENSE) && n.kid[0] >= 0);
+}
+inline bool dense_leaf(const Node &n) { return n.kind == K_DENSE && n.kid[0] < 0; }
+void refine_dense_leaves(HMat &H);
+void dense_loc(const HMat &H, int32_t b, i64 &off, i64 &ld);
 
 std::shared_ptr<Plan> plan_hlu(HMat &F, double eps2, i64 &perm_len_out,
                                PlanStream *stream = nullptr);

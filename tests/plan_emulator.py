@@ -13,7 +13,8 @@ import struct
 import numpy as np
 import scipy.linalg as sla
 
-T_GETRF, T_TRSM, T_SEGMUL, T_VTX, T_LRADD, T_DGEMM, T_DADD, T_DENSIFY, T_IDENT, T_NOP, T_RAND, T_ORTH = range(1, 13)
+(T_GETRF, T_TRSM, T_SEGMUL, T_VTX, T_LRADD, T_DGEMM, T_DADD, T_DENSIFY, T_IDENT, T_NOP, T_RAND,
+ T_ORTH, T_CHECK) = range(1, 14)
 B_F, B_TMP, B_RHS, B_X = range(4)
 KC = 32
 KC_MAX = 32
@@ -127,14 +128,17 @@ class Machine:
                 B = self.get(v[1])
                 if B.shape[1] == 0:
                     continue
-                mode = flags & 15
+                mode, unit = flags & 15, bool(flags & 16)
+                if flags & 128 and np.any(np.diag(T) == 0):
+                    raise np.linalg.LinAlgError(f"path {path}")
                 if mode == 0:
-                    B = B[self.perm[aux:aux + m]]
-                    X = sla.solve_triangular(T, B, lower=True, unit_diagonal=True)
+                    if flags & 32:
+                        B = B[self.perm[aux:aux + m]]
+                    X = sla.solve_triangular(T, B, lower=True, unit_diagonal=unit)
                 elif mode == 1:
-                    X = sla.solve_triangular(T, B, lower=False)
+                    X = sla.solve_triangular(T, B, lower=False, unit_diagonal=unit)
                 else:
-                    X = sla.solve_triangular(T, B, lower=False, trans="T")
+                    X = sla.solve_triangular(T, B, lower=False, trans="T", unit_diagonal=unit)
                 self.put(v[1], X)
             elif typ == T_SEGMUL:
                 Y = self.get(v[0])
@@ -213,6 +217,8 @@ class Machine:
                 self.put(v[0], q)
             elif typ == T_NOP:
                 pass
+            elif typ == T_CHECK:
+                assert np.abs(self.get(v[0])).max() <= alpha, f"cross-half pivot (path {path})"
             else:
                 raise ValueError(f"unknown task type {typ}")
 
