@@ -483,6 +483,8 @@ def run_cfg5(args, world, rank, local):
 
     cfg = CFG5
     method = args.method if args.method_set else "substitution"
+    if method != "propagator":
+        os.environ["LEVYH_NO_BG_PROP"] = "1"  # no propagator plan (host and device memory)
     t0 = time.perf_counter()
     s = P.FracCNSystem(P.power_measure(1, 0.8), 0.1, 0.0, 0.0, cfg["n"], 1.0 / cfg["n"],
                        distributed=world > 1)

@@ -1479,6 +1479,7 @@ void start_background_plans(HMat &H) {
         }
     });
     cudaGetDevice(&j->device);
+    if (!getenv("LEVYH_NO_BG_PROP"))
     job->f_prop = std::async(std::launch::async, [j] {
         try {
             block_layout(j->Z, j->fshadow, 2, prop_kcap());
@@ -1487,6 +1488,16 @@ void start_background_plans(HMat &H) {
             // streamed H-LU chunk uploads) is done: the copies overlap the H-LU's last chunks
             if (j->device >= 0 && !getenv("LEVYH_NO_BG_UPLOAD")) {
                 j->f_lu.wait();
+                // only when the plan is small against free device memory (the propagator may
+                // never be requested: e.g. stepping by substitution at the largest sizes)
+                LH_CUDA(cudaSetDevice(j->device));
+                size_t fr = 0, tot = 0;
+                LH_CUDA(cudaMemGetInfo(&fr, &tot));
+                const Plan &pp = *j->prop;
+                const double need = (double)pp.tasks.size() * (sizeof(DTask) + 24) +
+                                    (double)pp.deps.size() * 8 + (double)pp.pieces.size() * sizeof(DPiece) +
+                                    (double)pp.temp_len * 8;
+                if (need > 0.25 * (double)fr) return;
                 LH_CUDA(cudaSetDevice(j->device));
                 cudaStream_t st;
                 LH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
