@@ -1100,11 +1100,18 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
     extern __shared__ double4 smem_raw[];
     double *sm = reinterpret_cast<double *>(smem_raw);
     __shared__ int s_t;
+    __shared__ int s_carry;  // successor this CTA made ready and keeps (work-first)
     __shared__ DTask s_task;
+    if (threadIdx.x == 0) s_carry = -1;
+    __syncthreads();
     while (true) {
         // pop the most urgent ready task: buckets by b-level class, highest first; a slot
         // below `tail` is reserved by a pusher and filled momentarily
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && s_carry >= 0) {
+            s_t = s_carry;
+            s_task = A.tasks[s_carry];
+            s_carry = -1;
+        } else if (threadIdx.x == 0) {
             int t = -1;
             long long spins = 0;
             unsigned ns = 32;
@@ -1164,19 +1171,38 @@ __global__ void __launch_bounds__(NT, 1) exec_kernel(ExecArgs A) {
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
             if (A.times && threadIdx.x == 0) A.times[2 * t + 1] = gtimer();
             const int sb = A.succ_beg[t], se = A.succ_beg[t + 1];
+            auto push = [&](int s, int b) {
+                const int pos = atomicAdd(A.tails + b, 1);
+                st_release(A.queue + A.qoff[b] + pos, s);
+            };
+            // successors made ready by this completion: the most urgent one is kept and run
+            // next by this CTA (no queue round trip on a dependency chain), the rest pushed
+            int hold = -1, hold_b = -1;
             for (int q = sb + threadIdx.x; q < se; q += 32) {
                 const int e = A.succ[q];
                 const int s = e & SUCC_MASK, b = (int)((unsigned)e >> SUCC_SHIFT);
                 if (atomicSub(A.remaining + s, 1) == 1) {
-                    // last predecessor: acquire the other predecessors' releases, then push
+                    // last predecessor: acquire the other predecessors' releases
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    const int pos = atomicAdd(A.tails + b, 1);
-                    st_release(A.queue + A.qoff[b] + pos, s);
+                    if (b > hold_b) {
+                        if (hold >= 0) push(hold, hold_b);
+                        hold = s;
+                        hold_b = b;
+                    } else {
+                        push(s, b);
+                    }
                 }
             }
+            const int key = hold >= 0 ? (hold_b << 5) | (31 - threadIdx.x) : -1;
+            int best = key;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+            if (hold >= 0 && key != best) push(hold, hold_b);
+            if (best >= 0 && key == best) s_carry = hold;
             __syncwarp();
             if (threadIdx.x == 0) atomicAdd(A.done_count, 1);
         }
+        __syncthreads();
     }
 }
 
