@@ -1336,8 +1336,16 @@ static void report_profile(const Plan &P, const std::vector<unsigned long long> 
 }
 
 // Run a plan; F / X / RHS bases.  Ranks of F (and X) are copied in and back out.
-static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val,
-                     const char *label = "plan") {
+// run_plan_launch enqueues (stream-ordered, returns at once), run_plan_finish waits and
+// raises the executor's errors.
+struct PlanRun {
+    ExecArgs A;
+    bool prof = false;
+    int err[4] = {0, 0, 0, 0};
+};
+
+static void run_plan_launch(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val,
+                            PlanRun &R) {
     cudaStream_t s = ctx.stream;
     LH_CUDA(cudaMemsetAsync(P.d_done, 0, sizeof(int32_t) * (P.tasks.size() + 2), s));
     LH_CUDA(cudaMemsetAsync(P.d_err, 0, sizeof(int32_t) * 4, s));
@@ -1358,7 +1366,7 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     if (rhs_slot_val >= 0)
         LH_CUDA(cudaMemcpyAsync(P.d_ranks + P.rhs_slot, &rhs_slot_val, sizeof(int32_t),
                                 cudaMemcpyHostToDevice, s));
-    ExecArgs A;
+    ExecArgs &A = R.A;
     A.tasks = P.d_tasks;
     A.ntasks = (int32_t)P.tasks.size();
     A.deps = P.d_deps;
@@ -1381,34 +1389,37 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     A.ranks = P.d_ranks;
     A.perm = F.d_perm;
     A.times = nullptr;
-    const bool prof = (getenv("LEVYH_TASK_PROFILE") != nullptr ||
-                       getenv("LEVYH_TASK_PROFILE_STATS") != nullptr) && A.ntasks > 0;
-    if (prof) A.times = dalloc<unsigned long long>(2 * (i64)A.ntasks);
+    R.prof = (getenv("LEVYH_TASK_PROFILE") != nullptr ||
+              getenv("LEVYH_TASK_PROFILE_STATS") != nullptr) && A.ntasks > 0;
+    if (R.prof) A.times = dalloc<unsigned long long>(2 * (i64)A.ntasks);
     if (A.ntasks > 0) {
         int grid = exec_grid(ctx);
         void *args[] = {&A};
         LH_CUDA(cudaLaunchCooperativeKernel((const void *)exec_kernel, grid, NT, args, SMEM_BYTES, s));
     }
-    int err[4];
-    LH_CUDA(cudaMemcpyAsync(err, P.d_err, sizeof(err), cudaMemcpyDeviceToHost, s));
-    LH_CUDA(cudaStreamSynchronize(s));
-    if (prof) {
-        std::vector<unsigned long long> tm(2 * (size_t)A.ntasks);
-        LH_CUDA(cudaMemcpy(tm.data(), A.times, sizeof(unsigned long long) * tm.size(),
-                           cudaMemcpyDeviceToHost));
-        cudaFree(A.times);
-        double s = 0.0;
-        for (int i = 0; i < A.ntasks; ++i) s += (tm[2 * i + 1] - tm[2 * i]) * 1e-3;
-        g_last_mean_task_us = s / A.ntasks;
-        report_profile(P, tm, label);
-    }
+    LH_CUDA(cudaMemcpyAsync(R.err, P.d_err, sizeof(R.err), cudaMemcpyDeviceToHost, s));
     if (F.nslots)
         LH_CUDA(cudaMemcpyAsync(F.d_ranks, P.d_ranks, sizeof(int32_t) * F.nslots,
                                 cudaMemcpyDeviceToDevice, s));
     if (X && X->nslots)
         LH_CUDA(cudaMemcpyAsync(X->d_ranks, P.d_ranks + P.slot_off_x, sizeof(int32_t) * X->nslots,
                                 cudaMemcpyDeviceToDevice, s));
-    LH_CUDA(cudaStreamSynchronize(s));
+}
+
+static void run_plan_finish(Ctx &ctx, Plan &P, PlanRun &R, const char *label) {
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    ExecArgs &A = R.A;
+    if (R.prof) {
+        std::vector<unsigned long long> tm(2 * (size_t)A.ntasks);
+        LH_CUDA(cudaMemcpy(tm.data(), A.times, sizeof(unsigned long long) * tm.size(),
+                           cudaMemcpyDeviceToHost));
+        cudaFree(A.times);
+        double sum = 0.0;
+        for (int i = 0; i < A.ntasks; ++i) sum += (tm[2 * i + 1] - tm[2 * i]) * 1e-3;
+        g_last_mean_task_us = sum / A.ntasks;
+        report_profile(P, tm, label);
+    }
+    const int *err = R.err;
     if (err[0] == LH_ESINGULAR) {
         std::string msg = err[2] >= 0 && err[2] < (int)P.paths.size() ? P.paths[err[2]]
                                                                       : "singular diagonal block";
@@ -1419,6 +1430,13 @@ static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_s
     if (err[0] == LH_EINVAL && err[2] >= 0 && err[2] < (int)P.paths.size())
         throw Error(LH_EINVAL, P.paths[err[2]]);
     if (err[0] != 0) throw Error(err[0], "executor failure (task " + std::to_string(err[1]) + ")");
+}
+
+static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val,
+                     const char *label = "plan") {
+    PlanRun R;
+    run_plan_launch(ctx, P, F, X, rhs, rhs_slot_val, R);
+    run_plan_finish(ctx, P, R, label);
 }
 
 // ---------------------------------------------------------------------------
@@ -1563,26 +1581,38 @@ static void check_leaf_layout(const HMat &F, const PlanJob &job) {
     }
 }
 
-// Run the H-LU as chunks of the plan still being built on the background thread; the
-// chunks share one temp pool (grown by copy when a later chunk needs more).
+// Run the H-LU as chunks of the plan still being built on the background thread, one chunk
+// ahead: the next cut is requested when a chunk launches, uploaded on a second stream while
+// it runs, and launched as soon as it finishes.  The chunks share one temp pool (grown by
+// copy between chunks).
 static void hlu_streamed(Ctx &ctx, HMat &F, double eps2, PlanJob &job) {
     PlanStream &st = job.lu_stream;
     double *temp = nullptr;
     i64 temp_cap = 0;
-    double exec_s = 0.0;
     int nchunks = 0;
     i64 ntasks = 0;
-    std::unique_lock<std::mutex> lk(st.mu);
-    for (;;) {
+    cudaStream_t up;
+    LH_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    LH_CUDA(cudaEventCreate(&e0));
+    LH_CUDA(cudaEventCreate(&e1));
+    float exec_ms = 0.f;
+    auto take = [&]() -> std::shared_ptr<Plan> {
+        std::unique_lock<std::mutex> lk(st.mu);
         st.want.store(true);
         st.cv.wait(lk, [&] { return !st.chunks.empty() || st.done; });
-        if (st.chunks.empty()) break;
+        if (st.chunks.empty()) return nullptr;
         std::shared_ptr<Plan> C = st.chunks.front();
         st.chunks.pop_front();
-        lk.unlock();
-        if (eps2 != 1e-10) patch_eps(*C, eps2);
-        if (C->temp_len > temp_cap) {
-            double *nt = dalloc<double>(std::max<i64>(C->temp_len, 1));
+        return C;
+    };
+    auto prepare = [&](Plan &C) {
+        if (eps2 != 1e-10) patch_eps(C, eps2);
+        C.upload(up);  // host CSR + copies on the second stream (synchronous on it)
+    };
+    auto grow_temp = [&](Plan &C) {
+        if (C.temp_len > temp_cap) {
+            double *nt = dalloc<double>(std::max<i64>(C.temp_len, 1));
             if (temp) {
                 LH_CUDA(cudaMemcpyAsync(nt, temp, sizeof(double) * temp_cap, cudaMemcpyDeviceToDevice,
                                         ctx.stream));
@@ -1590,28 +1620,56 @@ static void hlu_streamed(Ctx &ctx, HMat &F, double eps2, PlanJob &job) {
                 cudaFree(temp);
             }
             temp = nt;
-            temp_cap = C->temp_len;
+            temp_cap = C.temp_len;
         }
-        C->upload(ctx.stream);
-        C->d_temp = temp;
-        auto t0 = std::chrono::steady_clock::now();
-        try {
-            run_plan(ctx, *C, F, nullptr, nullptr, -1, "hlu");
-        } catch (...) {
-            cudaFree(temp);
-            throw;
+        C.d_temp = temp;
+    };
+    try {
+        std::shared_ptr<Plan> cur = take();
+        if (cur) {
+            prepare(*cur);
+            grow_temp(*cur);
         }
-        exec_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        ++nchunks;
-        ntasks += (i64)C->tasks.size();
-        lk.lock();
+        PlanRun R;
+        while (cur) {
+            LH_CUDA(cudaEventRecord(e0, ctx.stream));
+            run_plan_launch(ctx, *cur, F, nullptr, nullptr, -1, R);
+            LH_CUDA(cudaEventRecord(e1, ctx.stream));
+            auto tl = std::chrono::steady_clock::now();
+            std::shared_ptr<Plan> nxt = take();  // cut while `cur` runs
+            if (nxt) prepare(*nxt);
+            run_plan_finish(ctx, *cur, R, "hlu");
+            float ms = 0.f;
+            LH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            exec_ms += ms;
+            if (getenv("LEVYH_PLAN_VERBOSE"))
+                fprintf(stderr, "[levyh] hlu chunk %d: %zu tasks, exec %.3f s (host wall %.3f s)\n", nchunks,
+                        cur->tasks.size(), ms / 1e3,
+                        std::chrono::duration<double>(std::chrono::steady_clock::now() - tl).count());
+            ++nchunks;
+            ntasks += (i64)cur->tasks.size();
+            cur.reset();  // frees the chunk's device arrays (not the shared temp pool)
+            if (nxt) grow_temp(*nxt);
+            cur = nxt;
+        }
+    } catch (...) {
+        cudaFree(temp);
+        cudaStreamDestroy(up);
+        throw;
     }
-    lk.unlock();
     cudaFree(temp);
+    cudaStreamDestroy(up);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    auto tw = std::chrono::steady_clock::now();
     job.f_lu.wait();
     LH_REQUIRE(job.error.empty(), LH_EINTERNAL, "H-LU planning failed: " + job.error);
     LH_REQUIRE(ntasks == (i64)job.lu->tasks.size(), LH_EINTERNAL, "streamed H-LU plan incomplete");
-    F.lu_stats[3] = exec_s;
+    if (getenv("LEVYH_PLAN_VERBOSE"))
+        fprintf(stderr, "[levyh] hlu streamed: %d chunks, exec %.3f s, waited for the plan end %.3f s\n",
+                nchunks, exec_ms / 1e3,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - tw).count());
+    F.lu_stats[3] = exec_ms / 1e3;
     F.lu_stats[4] = nchunks;
 }
 
@@ -1638,10 +1696,16 @@ void hlu(Ctx &ctx, HMat &F, double eps2) {
             F.d_inv = dalloc<double>(std::max<i64>(F.inv_len, 1));
             F.factored = true;
             F.mv_plan.reset();
+            auto ts0 = std::chrono::steady_clock::now();
             hlu_streamed(ctx, F, eps2, *job);
+            auto ts1 = std::chrono::steady_clock::now();
             F.nodes = job->shadow.nodes;
             check_leaf_layout(F, *job);
             F.sync_ranks(ctx.stream);
+            if (getenv("LEVYH_PLAN_VERBOSE"))
+                fprintf(stderr, "[levyh] hlu streamed: chunks %.3f s, finish %.3f s\n",
+                        std::chrono::duration<double>(ts1 - ts0).count(),
+                        std::chrono::duration<double>(std::chrono::steady_clock::now() - ts1).count());
             F.lu_stats[0] = (double)job->lu->tasks.size();
             F.lu_stats[1] = job->lu->build_seconds;
             F.lu_stats[2] = (double)job->lu->temp_len * 8.0;

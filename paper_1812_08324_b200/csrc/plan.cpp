@@ -982,24 +982,37 @@ void assign_priorities(Plan &P) {
             default: return 8.0;
         }
     };
-    // b-level (cost of the longest path from the task to the end) -> NPRIO buckets
-    std::vector<double> bl(n);
-    for (int32_t i = 0; i < n; ++i) bl[i] = cost(T[i]);
+    // b-level (cost of the longest path from the task to the end) -> NPRIO buckets; the
+    // backward pass touches only dense float arrays (not the 184-byte task records)
+    std::vector<float> c(n), bl(n);
+    std::vector<int32_t> db(n), dc(n);
+    for (int32_t i = 0; i < n; ++i) {
+        c[i] = bl[i] = (float)cost(T[i]);
+        db[i] = T[i].dep_beg;
+        dc[i] = T[i].dep_cnt;
+    }
+    const int32_t *deps = P.deps.data();
     for (int32_t i = n - 1; i >= 0; --i) {
-        const int32_t *dp = P.deps.data() + T[i].dep_beg;
-        for (int32_t k = 0; k < T[i].dep_cnt; ++k) {
+        const int32_t *dp = deps + db[i];
+        const float bi = bl[i];
+        for (int32_t k = 0; k < dc[i]; ++k) {
             const int32_t p = dp[k];
-            bl[p] = std::max(bl[p], cost(T[p]) + bl[i]);
+            bl[p] = std::max(bl[p], c[p] + bi);
         }
     }
-    double mx = 1e-30;
+    float mx = 1e-30f;
     for (int32_t i = 0; i < n; ++i) mx = std::max(mx, bl[i]);
     for (int32_t i = 0; i < n; ++i) T[i].prio = std::min(NPRIO - 1, (int)(NPRIO * bl[i] / mx));
 }
 
 void Planner::finalize() {
     P->nslots_total = next_slot;
-    assign_priorities(*P);
+    bool engaged = false;
+    if (stream) {
+        std::lock_guard<std::mutex> lk(stream->mu);
+        engaged = stream->engaged;
+    }
+    if (!engaged) assign_priorities(*P);  // streamed chunks carry their own priorities
     if (stream) {  // hand the tail to an engaged consumer, then signal completion
         bool engaged;
         {
