@@ -196,6 +196,11 @@ int lh_hlu_stats(const lh_hmat *factor, double *out_host);
  * chained (each depends on the previous) or independent.  out[0] = wall us per task,
  * out[1] = mean task body us (device timestamps). */
 int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out_host);
+/* Debug: phase-timed recompression (QR(U), QR(V), Ru Rv^T, Jacobi SVD, truncation + apply) of
+ * host U (m x K), V (n x K) on every SM, reps times; out[0..5] mean ns per phase, out[6] rank.
+ * Times the kernel behind hops.py:134-144 (_lowrank_add_recompress). */
+int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const double *u_host,
+                          const double *v_host, double *out_host);
 
 /* ---- entry generation: fractional.py:285-405 + levy.py:169-206 -------- */
 typedef struct {

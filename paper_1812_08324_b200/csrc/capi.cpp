@@ -39,6 +39,7 @@ int lowrank_add_recompress(Ctx &ctx, i64 m, i64 n, const double *u1, const doubl
                            const double *u2, const double *v2, int r2, double eps2, double *uo,
                            double *vo);
 void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
+void recomp_bench(Ctx &ctx, int m, int n, int K, int reps, const double *U, const double *V, double *out);
 void start_background_plans(HMat &H);
 
 double *DevBuf::ensure(i64 n) {
@@ -550,6 +551,11 @@ int lh_step_profile(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int32
 
 int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out) {
     return guard(ctx, [&] { task_bench(ctx->c, kind, R, k, chain != 0, out); });
+}
+
+int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const double *u, const double *v,
+                          double *out) {
+    return guard(ctx, [&] { recomp_bench(ctx->c, m, n, K, reps, u, v, out); });
 }
 
 int lh_hlu_stats(const lh_hmat *f, double *out) {

@@ -184,7 +184,13 @@ __device__ __noinline__ static void cgs2(double *Q, i64 ldq, i64 m, int K, doubl
 // One-sided Jacobi SVD (Hestenes) of C (K x K, col-major, ld KA_MAX, shared).
 // On exit C <- C V (columns = sigma_i * w_i), V (K x K) orthogonal.  Then
 // sigma[i] = ||C[:,i]|| and ord[] sorts them descending (stable by index).
-__device__ __noinline__ static void jacobi_svd(double *C, double *V, int K, double *sigma, int *ord, double *red) {
+// Round-robin ordering: each step rotates P/2 disjoint column pairs, one warp per pair
+// (K <= 32: one row per lane; K <= 48: two).  The step is a latency chain (shared loads,
+// three interleaved warp reductions, the rotation, one barrier), so the rotation uses two
+// long-latency FP64 ops: h = hypot(d, g), then w = 1/sqrt((|d| + h)^2 + g^2), with
+// d = ||b||^2 - ||a||^2, g = 2 <a, b>: c = (|d| + h) w, s = sign(d) g w (Rutishauser's
+// t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = d / g, scaled by |d| + h).
+__device__ __noinline__ static int jacobi_svd(double *C, double *V, int K, double *sigma, int *ord, double *red) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < K * KA_MAX; e += NT) {
         int i = e % KA_MAX, j = e / KA_MAX;
@@ -192,50 +198,68 @@ __device__ __noinline__ static void jacobi_svd(double *C, double *V, int K, doub
     }
     __shared__ int s_rot;
     const int P = (K + 1) & ~1;  // even number of slots (one dummy if K odd)
-    for (int sweep = 0; sweep < 40 && K > 1; ++sweep) {
+    const int L = P - 1;
+    const bool two = K > 32;
+    const int i0 = lane, i1 = lane + 32;
+    const bool h0 = i0 < K, h1 = two && i1 < K;
+    int sweep = 0;
+    for (; sweep < 40 && K > 1; ++sweep) {
         if (threadIdx.x == 0) s_rot = 0;
         __syncthreads();
-        for (int step = 0; step < P - 1; ++step) {
-            // round-robin pairing: slot 0 fixed, others rotate
+        bool rot = false;
+        for (int step = 0; step < L; ++step) {
             for (int pr = w; pr < P / 2; pr += NW) {
-                int a = (pr == 0) ? 0 : 1 + (pr - 1 + step) % (P - 1);
-                int b = 1 + (P - 2 - pr + step) % (P - 1);
+                // slot 0 fixed, the others rotate by one position per step
+                int a = pr - 1 + step, b = L - 1 - pr + step;
+                a = a >= L ? a - L : a;
+                b = b >= L ? b - L : b;
+                a = pr == 0 ? 0 : a + 1;
+                b += 1;
                 if (a >= K || b >= K) continue;
                 if (a > b) {
-                    int t = a;
+                    const int t = a;
                     a = b;
                     b = t;
                 }
                 double *ca = C + a * KA_MAX, *cb = C + b * KA_MAX;
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int i = lane; i < K; i += 32) {
-                    al += ca[i] * ca[i];
-                    be += cb[i] * cb[i];
-                    ga += ca[i] * cb[i];
+                double *va = V + a * KA_MAX, *vb = V + b * KA_MAX;
+                const double x0 = h0 ? ca[i0] : 0.0, y0 = h0 ? cb[i0] : 0.0;
+                const double x1 = h1 ? ca[i1] : 0.0, y1 = h1 ? cb[i1] : 0.0;
+                const double p0 = h0 ? va[i0] : 0.0, q0 = h0 ? vb[i0] : 0.0;
+                const double p1 = h1 ? va[i1] : 0.0, q1 = h1 ? vb[i1] : 0.0;
+                double al = x0 * x0 + x1 * x1, be = y0 * y0 + y1 * y1, ga = x0 * y0 + x1 * y1;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
                 }
-                al = warp_sum(al);
-                be = warp_sum(be);
-                ga = warp_sum(ga);
-                if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
-                    double zeta = (be - al) / (2.0 * ga);
-                    double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-                    double *va = V + a * KA_MAX, *vb = V + b * KA_MAX;
-                    for (int i = lane; i < K; i += 32) {
-                        double x = ca[i], y = cb[i];
-                        ca[i] = c * x - s * y;
-                        cb[i] = s * x + c * y;
-                        x = va[i];
-                        y = vb[i];
-                        va[i] = c * x - s * y;
-                        vb[i] = s * x + c * y;
+                // |<a,b>| > 1e-15 ||a|| ||b||, squared (no square roots on the chain)
+                if (ga != 0.0 && ga * ga > 1e-30 * (al * be)) {
+                    const double d = be - al, g = 2.0 * ga;
+                    const double u = fabs(d) + hypot(d, g);
+                    const double wn = rsqrt(u * u + g * g);
+                    const double c = u * wn, sn = (d >= 0.0 ? g : -g) * wn;
+                    if (h0) {
+                        ca[i0] = c * x0 - sn * y0;
+                        cb[i0] = sn * x0 + c * y0;
+                        va[i0] = c * p0 - sn * q0;
+                        vb[i0] = sn * p0 + c * q0;
                     }
-                    if (lane == 0) s_rot = 1;
+                    if (h1) {
+                        ca[i1] = c * x1 - sn * y1;
+                        cb[i1] = sn * x1 + c * y1;
+                        va[i1] = c * p1 - sn * q1;
+                        vb[i1] = sn * p1 + c * q1;
+                    }
+                    rot = true;
                 }
             }
             __syncthreads();
         }
-        int any = s_rot;
+        if (rot && lane == 0) s_rot = 1;
+        __syncthreads();
+        const int any = s_rot;
         __syncthreads();
         if (!any) break;
     }
@@ -260,6 +284,7 @@ __device__ __noinline__ static void jacobi_svd(double *C, double *V, int K, doub
         }
     }
     __syncthreads();
+    return sweep;
 }
 
 // rule 0: count sigma > eps * sigma_1 (hmatrix.py:297-300, build);

@@ -2237,7 +2237,7 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
         for (size_t q = 0; q < mv.size(); ++q) {
             const Mv &m = mv[q];
             LH_CUDA(cudaEventRecord(ev[2 * q], ctx.stream));
-            mv_vtx_launch(*m.P, *m.H, m.x, ctx.num_sms * 16, ctx.stream);
+            mv_vtx_launch(*m.P, *m.H, m.x, ctx.num_sms, ctx.stream);
             LH_CUDA(cudaEventRecord(ev[2 * q + 1], ctx.stream));
             mv_seg_launch(*m.P, *m.H, m.x, m.y, m.alpha, m.beta, ctx.stream, ctx.num_sms, m.z);
         }
@@ -2383,4 +2383,94 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
     }
 }
 
+}  // namespace lh
+
+namespace lh {
+// Phase-timed recompression (debug): every CTA recompresses its own copy of U (m x K),
+// V (n x K) staged in shared memory, `reps` times; out[p] = mean ns of phase p
+// (0 stage, 1 QR(U), 2 QR(V), 3 C = Ru Rv^T, 4 Jacobi SVD, 5 truncation + apply; 6 rank).
+__global__ void __launch_bounds__(NT, 1) recomp_bench_kernel(const double *U0, const double *V0, int m,
+                                                             int n, int K, int reps,
+                                                             unsigned long long *acc) {
+    extern __shared__ double4 smem_raw[];
+    double *sm = reinterpret_cast<double *>(smem_raw);
+    dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(sm);
+    constexpr int RS = (int)((sizeof(dev::RecompSmem) + 15) / 8) & ~1;
+    double *Us = sm + RS, *Vs = Us + (i64)m * K;
+    unsigned long long t[7];
+    unsigned long long tot[6] = {0, 0, 0, 0, 0, 0};
+    int r = 0, sweeps = 0;
+    for (int rep = 0; rep < reps; ++rep) {
+        __syncthreads();
+        t[0] = gtimer();
+        for (int e = threadIdx.x; e < m * K; e += NT) Us[e] = U0[e];
+        for (int e = threadIdx.x; e < n * K; e += NT) Vs[e] = V0[e];
+        __syncthreads();
+        t[1] = gtimer();
+        dev::cgs2(Us, m, m, K, S.Ru, S.h, S.red);
+        __syncthreads();
+        t[2] = gtimer();
+        dev::cgs2(Vs, n, n, K, S.Rv, S.h, S.red);
+        __syncthreads();
+        t[3] = gtimer();
+        for (int e = threadIdx.x; e < K * K; e += NT) {
+            int i = e % K, j = e / K;
+            double s = 0.0;
+            for (int l = 0; l < K; ++l) s += S.Ru[i + l * dev::KA_MAX] * S.Rv[j + l * dev::KA_MAX];
+            S.Cc[i + j * dev::KA_MAX] = s;
+        }
+        __syncthreads();
+        t[4] = gtimer();
+        sweeps = dev::jacobi_svd(S.Cc, S.Rv, K, S.sigma, S.ord, S.red);
+        __syncthreads();
+        t[5] = gtimer();
+        r = dev::truncation_rank(S.sigma, S.ord, K, 1, 1e-10);
+        for (int e = threadIdx.x; e < K * r; e += NT) {
+            int l = e % K, c = e / K;
+            S.Ru[l + c * dev::KA_MAX] = S.Cc[l + S.ord[c] * dev::KA_MAX];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < K * r; e += NT) {
+            int l = e % K, c = e / K;
+            S.Cc[l + c * dev::KA_MAX] = S.Rv[l + S.ord[c] * dev::KA_MAX];
+        }
+        __syncthreads();
+        dev::apply_coeffs(Us, m, m, K, S.Ru, dev::KA_MAX, r, Us, m);
+        dev::apply_coeffs(Vs, n, n, K, S.Cc, dev::KA_MAX, r, Vs, n);
+        __syncthreads();
+        t[6] = gtimer();
+        for (int p = 0; p < 6; ++p) tot[p] += t[p + 1] - t[p];
+    }
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < 6; ++p) atomicAdd(acc + p, tot[p]);
+        atomicAdd(acc + 6, (unsigned long long)r);
+        atomicAdd(acc + 7, (unsigned long long)sweeps);
+    }
+}
+
+void recomp_bench(Ctx &ctx, int m, int n, int K, int reps, const double *U_host, const double *V_host,
+                  double *out) {
+    LH_REQUIRE(K >= 1 && K <= KA_MAX && m >= 1 && n >= 1, LH_EINVAL, "recomp_bench: bad shape");
+    constexpr int RS = (int)((sizeof(dev::RecompSmem) + 15) / 8) & ~1;
+    const i64 smem = 8 * (RS + (i64)(m + n) * K);
+    LH_REQUIRE(smem <= SMEM_BYTES, LH_EINVAL, "recomp_bench: operands exceed shared memory");
+    double *U = dalloc<double>((i64)m * K), *V = dalloc<double>((i64)n * K);
+    unsigned long long *acc = dalloc<unsigned long long>(8);
+    LH_CUDA(cudaMemcpyAsync(U, U_host, sizeof(double) * m * K, cudaMemcpyHostToDevice, ctx.stream));
+    LH_CUDA(cudaMemcpyAsync(V, V_host, sizeof(double) * n * K, cudaMemcpyHostToDevice, ctx.stream));
+    LH_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 8, ctx.stream));
+    LH_CUDA(cudaFuncSetAttribute((const void *)recomp_bench_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    recomp_bench_kernel<<<ctx.num_sms, NT, SMEM_BYTES, ctx.stream>>>(U, V, m, n, K, reps, acc);
+    LH_CUDA(cudaGetLastError());
+    unsigned long long h[8];
+    LH_CUDA(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    for (int p = 0; p < 6; ++p) out[p] = (double)h[p] / ((double)ctx.num_sms * reps);
+    out[6] = (double)h[6] / ctx.num_sms;
+    out[7] = (double)h[7] / ctx.num_sms;
+    LH_CUDA(cudaFree(U));
+    LH_CUDA(cudaFree(V));
+    LH_CUDA(cudaFree(acc));
+}
 }  // namespace lh

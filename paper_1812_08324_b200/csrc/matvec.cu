@@ -27,7 +27,11 @@ using dev::NT;
 
 constexpr int SEG = 64;         // rows per segment
 constexpr int GRP = NT / SEG;   // thread groups per segment
-constexpr i64 VCHUNK = 1024;    // rows of V per phase-1 chunk (one warp)
+constexpr i64 VCHUNK_DEFAULT = 1024;  // rows of V per phase-1 chunk (one warp)
+static i64 vchunk_rows() {
+    static const i64 v = getenv("LEVYH_VCHUNK") ? std::max(64, atoi(getenv("LEVYH_VCHUNK"))) : VCHUNK_DEFAULT;
+    return v;
+}
 #ifndef SEG_MIN_BLOCKS
 #define SEG_MIN_BLOCKS 4        // CTAs per SM for the direct-load segment kernel
 #endif
@@ -43,61 +47,126 @@ constexpr int TMA_THREADS = TMA_CONS + 32;  // one producer warp + 16 consumer w
 // ---------------------------------------------------------------------------
 // phase 1
 // ---------------------------------------------------------------------------
-// one warp per chunk: each lane accumulates all r columns for its rows (x[i] read once,
-// r independent coalesced loads per row, two rows in flight), then warp shuffles reduce
+// Sum RB per-lane values over the warp, column c ending in lane group c (see vtx_warp).
 template <int RB>
+__device__ __forceinline__ void warp_transpose_reduce(double (&acc)[RB], int lane) {
+#pragma unroll
+    for (int o = 16, h = RB / 2; h >= 1; o >>= 1, h >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+            const double send = up ? acc[k] : acc[k + h];
+            const double keep = up ? acc[k + h] : acc[k];
+            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    constexpr int LOW = 32 / RB;
+#pragma unroll
+    for (int o = LOW / 2; o >= 1; o >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+}
+
+// one warp per chunk: each lane accumulates all r columns for its rows (x[i] read once,
+// r coalesced loads per row), then warp shuffles reduce.  Every iteration issues all of its
+// RB * ROWS loads before the first FMA (one memory round trip per iteration); RB * ROWS = 16
+// loaded values + RB accumulators fit the 64-register budget of 4 CTAs per SM without spills.
+template <int RB, int ROWS>
 __device__ __forceinline__ void vtx_warp(const VChunk &C, const double *pbuf, const double *x,
                                          double *out, int lane) {
     const int r = C.r;
+    const int len = C.len;
     const double *V = pbuf + C.voff;
     const double *xx = x + C.xc0;
-    const i64 ld = C.len;
+    const int ld = len;
     double acc[RB];
 #pragma unroll
     for (int c = 0; c < RB; ++c) acc[c] = 0.0;
     int i = lane;
-    for (; i + 32 < C.len; i += 64) {
-        const double x0 = xx[i], x1 = xx[i + 32];
-        double v0[RB], v1[RB];
+    for (; i + 32 * (ROWS - 1) < len; i += 32 * ROWS) {
+        double xv[ROWS], v[ROWS][RB];
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) xv[q] = __ldg(xx + i + 32 * q);
+        const double *p = V + i;
 #pragma unroll
         for (int c = 0; c < RB; ++c) {
-            v0[c] = c < r ? V[i + c * ld] : 0.0;
-            v1[c] = c < r ? V[i + 32 + c * ld] : 0.0;
-        }
 #pragma unroll
-        for (int c = 0; c < RB; ++c) acc[c] += v0[c] * x0 + v1[c] * x1;
-    }
-    if (i < C.len) {
-        const double xi = xx[i];
+            for (int q = 0; q < ROWS; ++q) v[q][c] = c < r ? __ldcs(p + 32 * q) : 0.0;
+            p += ld;
+        }
 #pragma unroll
         for (int c = 0; c < RB; ++c)
-            if (c < r) acc[c] += V[i + c * ld] * xi;
-    }
 #pragma unroll
-    for (int c = 0; c < RB; ++c)
-        if (c < r) {
-            const double v = dev::warp_sum(acc[c]);
-            if (lane == 0) out[c] = v;
+            for (int q = 0; q < ROWS; ++q) acc[c] = fma(v[q][c], xv[q], acc[c]);
+    }
+    for (; i < len; i += 32) {
+        const double xi = xx[i];
+        const double *p = V + i;
+#pragma unroll
+        for (int c = 0; c < RB; ++c) {
+            if (c < r) acc[c] = fma(__ldcs(p), xi, acc[c]);
+            p += ld;
         }
+    }
+    // transpose-reduce: each butterfly level halves the columns a lane carries (send the half
+    // the partner keeps), so RB columns cost RB/2 + RB/4 + ... + 1 + 2 shuffles instead of
+    // 5 RB; afterwards lane l holds the full sum of column col(l) (bits 4.. of l, MSB first)
+    warp_transpose_reduce<RB>(acc, lane);
+    {
+        int c = 0;
+#pragma unroll
+        for (int o = 16, h = RB / 2; h >= 1; o >>= 1, h >>= 1) c = 2 * c + ((lane & o) ? 1 : 0);
+        constexpr int LOW = 32 / RB;  // lanes sharing one column after the exchange levels
+        if ((lane & (LOW - 1)) == 0 && c < r) out[c] = acc[0];
+    }
     // ranks above RB: remaining columns one at a time
     for (int c = RB; c < r; ++c) {
-        const double *v = V + c * ld;
-        double s = 0.0;
-        for (int q = lane; q < C.len; q += 32) s += v[q] * xx[q];
-        s = dev::warp_sum(s);
-        if (lane == 0) out[c] = s;
+        const double *v = V + (i64)c * ld;
+        double t = 0.0;
+        for (int q = lane; q < len; q += 32) t += v[q] * xx[q];
+        t = dev::warp_sum(t);
+        if (lane == 0) out[c] = t;
     }
 }
 
+#ifndef VTX_MIN_BLOCKS
+#define VTX_MIN_BLOCKS 3
+#endif
 template <int RB>
-__global__ void __launch_bounds__(NT, (RB <= 8 ? 6 : 4))
+__global__ void __launch_bounds__(NT, VTX_MIN_BLOCKS)
     vtx_kernel(const VChunk *chunks, int nch, const double *pbuf, const double *x, double *part,
                double *tvec) {
     const int lane = threadIdx.x & 31;
-    for (int q = blockIdx.x * dev::NW + (threadIdx.x >> 5); q < nch; q += gridDim.x * dev::NW) {
-        const VChunk C = chunks[q];
+    const int stride = gridDim.x * dev::NW;
+    int q = blockIdx.x * dev::NW + (threadIdx.x >> 5);
+    if (q >= nch) return;
+    // the next chunk's descriptor is loaded while this chunk streams (one fewer dependent
+    // memory round trip per chunk), spread one 32-bit word per lane so that it holds a single
+    // register through the streaming loop
+    static_assert(sizeof(VChunk) == 32, "VChunk is 8 words");
+    auto word = [&](int qq) {
+        return lane < 8 ? __ldg(reinterpret_cast<const int32_t *>(chunks + qq) + lane) : 0;
+    };
+    auto unpack = [&](int32_t w) {
+        VChunk C;
+        int32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __shfl_sync(0xffffffffu, w, k);
+        C.voff = (i64)(((unsigned long long)(uint32_t)v[1] << 32) | (uint32_t)v[0]);
+        C.xc0 = (i64)(((unsigned long long)(uint32_t)v[3] << 32) | (uint32_t)v[2]);
+        C.len = v[4];
+        C.r = v[5];
+        C.blk = v[6];
+        C.pidx = v[7];
+        return C;
+    };
+    int32_t w = word(q);
+    while (true) {
+        const VChunk C = unpack(w);
+        const int qn = q + stride;
+        if (qn < nch) w = word(qn);
         double *out = C.pidx >= 0 ? part + (i64)C.pidx * KC_MAX : tvec + (i64)C.blk * KC_MAX;
-        vtx_warp<RB>(C, pbuf, x, out, lane);
+        vtx_warp<RB, 16 / RB>(C, pbuf, x, out, lane);
+        if (qn >= nch) break;
+        q = qn;
     }
 }
 
@@ -453,6 +522,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
             const int blk = nblk++;
             std::vector<VChunk> &dst = r > 8 ? chunks16 : chunks;
             std::vector<i64> &dld = r > 8 ? vld16 : vld;
+            const i64 VCHUNK = vchunk_rows();
             if (nd.n <= VCHUNK) {
                 dst.push_back({nd.voff, nd.c0, (int32_t)nd.n, r, blk, -1});
                 dld.push_back(nd.n);
@@ -471,6 +541,24 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
                            "low-rank block not aligned with row segments");
                 lps[sg].push_back({nd.uoff + (a - nd.r0), nd.m, r, blk});
             }
+        }
+    }
+    if (getenv("LEVYH_PLAN_VERBOSE")) {
+        for (int k = 0; k < 2; ++k) {
+            const std::vector<VChunk> &cv = k ? chunks16 : chunks;
+            std::map<std::pair<int, int>, std::pair<i64, double>> h;  // (len class, r) -> count, MB
+            for (const VChunk &c : cv) {
+                int lc = 1;
+                while (lc < c.len) lc *= 2;
+                auto &e = h[{lc, c.r}];
+                e.first++;
+                e.second += 8.0 * c.len * c.r / 1e6;
+            }
+            fprintf(stderr, "[mv plan] %s chunks %zu:", k ? "rank>8" : "rank<=8", cv.size());
+            for (auto &e : h)
+                fprintf(stderr, " len<=%d,r=%d:%lld(%.0fMB)", e.first.first, e.first.second,
+                        (long long)e.second.first, e.second.second);
+            fprintf(stderr, "\n");
         }
     }
     // packed layout (columns of ld = even(rows)) + bulk-copy batches of <= SLOT_D doubles,
@@ -570,6 +658,12 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
             c.voff = poff;
             poff += even((i64)c.len * c.r);
         }
+        // largest chunks first: the grid-stride warps (and the hardware block scheduler behind
+        // them) then finish on the small chunks instead of starting a 1024-row chunk last
+        if (!getenv("LEVYH_VTX_NOSORT"))
+            std::stable_sort(cv.begin(), cv.end(), [](const VChunk &a, const VChunk &b) {
+                return (i64)a.len * a.r > (i64)b.len * b.r;
+            });
     }
     // TMA kernel: contiguous, byte-balanced segment ranges, one CTA per SM
     int dev_id = 0, num_sms = 148;
@@ -651,14 +745,29 @@ MvPlan::~MvPlan() {
 }
 
 // phase 1 (V^T x per chunk) + t_b reduction of multi-chunk blocks
-void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int grid, cudaStream_t s) {
+// grid of the grid-stride V^T x kernels: 32 CTAs per SM (about ten resident waves; the
+// block scheduler then balances the largest-first chunk list), LEVYH_VTX_BPS overrides;
+// measured at N = 2^20: one wave 0.261 ms, 32 per SM 0.257 ms (chunks sorted), unsorted 0.300
+template <int RB>
+static int vtx_grid(int num_sms) {
+    static int bps = 0;
+    if (!bps) {
+        const char *e = getenv("LEVYH_VTX_BPS");
+        bps = e ? atoi(e) : 32;
+        if (bps <= 0) LH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, vtx_kernel<RB>, NT, 0));
+        bps = std::max(bps, 1);
+    }
+    return num_sms * bps;
+}
+
+void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms, cudaStream_t s) {
     (void)H;
     if (P.nch > 0) {
-        int g = std::max(1, std::min(grid, (P.nch + dev::NW - 1) / dev::NW));
+        int g = std::max(1, std::min(vtx_grid<8>(num_sms), (P.nch + dev::NW - 1) / dev::NW));
         vtx_kernel<8><<<g, NT, 0, s>>>(P.chunks, P.nch, P.pbuf, x, P.part, P.tvec);
     }
     if (P.nch16 > 0) {
-        int g = std::max(1, std::min(grid, (P.nch16 + dev::NW - 1) / dev::NW));
+        int g = std::max(1, std::min(vtx_grid<16>(num_sms), (P.nch16 + dev::NW - 1) / dev::NW));
         vtx_kernel<16><<<g, NT, 0, s>>>(P.chunks16, P.nch16, P.pbuf, x, P.part, P.tvec);
     }
     if (P.ntj > 0) {
@@ -695,7 +804,7 @@ void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, d
 // y = alpha * H x + beta * z (z = y when null) for one right-hand side
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
             cudaStream_t s, int num_sms, const double *z) {
-    mv_vtx_launch(P, H, x, num_sms * 16, s);
+    mv_vtx_launch(P, H, x, num_sms, s);
     mv_seg_launch(P, H, x, y, alpha, beta, s, num_sms, z);
     LH_CUDA(cudaGetLastError());
 }

@@ -87,7 +87,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
             cudaStream_t s, int num_sms, const double *z = nullptr);
 MvPlan &get_mv_plan(HMat &H, cudaStream_t s);
-void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int grid, cudaStream_t s);
+void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms, cudaStream_t s);
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
                    double beta, cudaStream_t s, int num_sms, const double *z = nullptr);
 void matvec(Ctx &ctx, HMat &H, const double *x, i64 ldx, double *y, i64 ldy, int nrhs);
