@@ -221,6 +221,29 @@ typedef struct {
     double dt;      /* CN time step                        */
 } lh_cn_params;
 
+/* Smooth-measure series H-builder: build_from_expansion (hmatrix.py:243-291) with the
+ * Gaussian family of gaussian_expansion_1d (hmatrix.py:171-186), as levy.CNSystem.hmatrix
+ * calls it (levy.py:224-239).  Partition of hmatrix.py:319-337 (admissible blocks with
+ * min(m,n) > n_min are low-rank, no dense fallback); low-rank factors around the row
+ * cluster centre with n_terms = fixed_rank, or rank_bound_gaussian(...) + 1 per block when
+ * delta > 0 (hmatrix.py:270-290); U carries `scale`.  Dense leaves: A[i,j] =
+ * t_dev[n_rows - 1 + j - i] (entry_fn of a Toeplitz CN system) or, with t_dev NULL, the
+ * kernel scale * exp(-eps_sq (x_i - y_j)^2).  Points are device arrays in tree order. */
+int lh_hmat_build_gauss_series(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,
+                               const double *row_pts_dev, const double *col_pts_dev, double eps_sq,
+                               double scale, int fixed_rank, double delta, const lh_hconfig *cfg,
+                               lh_hmat **out);
+/* _expansion_terms (hmatrix.py:284-290): fixed_rank, or rank_bound_gaussian(sqrt(eps_sq),
+ * diameter, delta) + 1 (hmatrix.py:270-281) when delta > 0; 1 for a zero diameter. */
+int lh_gauss_series_terms(double eps_sq, double diameter, int fixed_rank, double delta);
+/* Toeplitz symbols of levy.CNSystem for the Gaussian density scale*exp(-eps_sq y^2)
+ * (levy.py:72-81, :169-176, :194-206, :249-263): A[i,j] = -nu((j-i)h) h, band -a/h^2 -+ b/2h,
+ * diagonal 2a/h^2 - c + lam h with lam = sum_{j=1..n_off} nu(-jh) + nu(jh); A+- = I +- dt/2 A.
+ * Lengths 2N-1 (device); lam_host (nullable) receives lam. */
+int lh_gauss_cn_symbol(lh_ctx *ctx, int64_t N, double h, double eps_sq, double scale, int64_t n_off,
+                       double a, double b, double c, double dt, double *tA_dev, double *tPlus_dev,
+                       double *tMinus_dev, double *lam_host);
+
 /* Writes the Toeplitz symbols tA, tPlus, tMinus (2N-1 each, device) of A and
  * A+- = I +- dt/2 A, and sums_host[0..2] = S0, Sg, Sd (GPU reduction). */
 int lh_cn_symbol(lh_ctx *ctx, const lh_measure *nu, const lh_cn_params *p, double *tA_dev,

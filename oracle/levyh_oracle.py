@@ -654,3 +654,100 @@ def build_cn(tA, dt, x, leaf, eps1, n_block=4, eta=1.0):
     Hp = compress_dense(Ap[np.ix_(order, order)], root, eps1, leaf, n_block, eta)
     Hm = compress_dense(Am[np.ix_(order, order)], root, eps1, leaf, n_block, eta)
     return root, order, Hp, Hm
+
+
+# ---------------------------------------------------------------------------
+# smooth-measure (Gaussian) system + series H-builder
+# (levy.py:72-81, :169-206, :249-263; hmatrix.py:156-186, :243-291)
+# ---------------------------------------------------------------------------
+
+
+def gauss_density(eps_sq, scale=1.0):
+    """levy.py:72-81: nu(y) = scale * exp(-eps_sq y^2)."""
+    return lambda y: scale * np.exp(-eps_sq * np.asarray(y, dtype=float) ** 2)
+
+
+def gauss_cn_symbol(n, h, eps_sq, scale, a, b, c, n_off):
+    """Toeplitz symbol t[k + n - 1] = A[i, i + k] of levy.CNSystem's A (levy.py:169-176) with
+    lam = sum over the window offsets (assemble_cn_1d, levy.py:257-262)."""
+    nu = gauss_density(eps_sq, scale)
+    j = np.arange(1, n_off + 1)
+    lam = float(np.concatenate([nu(-j * h), nu(j * h)]).sum())
+    k = np.arange(-(n - 1), n)
+    t = -nu(k * h) * h
+    if n > 1:
+        t[n] += -a / h ** 2 - b / (2 * h)
+        t[n - 2] += -a / h ** 2 + b / (2 * h)
+    t[n - 1] = 2 * a / h ** 2 - c + lam * h
+    return t, lam
+
+
+def series_cols(t, eps_sq, n_terms, alpha, scale=1.0):
+    """hmatrix.py:156-169: column k = scale (2 eps_sq t)^k e^{-eps_sq t^2} / k! (alpha) or
+    t^k e^{-eps_sq t^2}, by the recurrence col_k = col_{k-1} * base / k."""
+    cols = [scale * np.exp(-eps_sq * t * t)]
+    base = 2.0 * eps_sq * t if alpha else t
+    for k in range(1, n_terms):
+        cols.append(cols[-1] * base / (k if alpha else 1))
+    return np.stack(cols, axis=1)
+
+
+def series_terms(eps_sq, D, fixed_rank, delta):
+    """_expansion_terms + rank_bound_gaussian (hmatrix.py:270-290)."""
+    if delta is None:
+        return fixed_rank
+    if D <= 0:
+        return 1
+    eps = math.sqrt(eps_sq)
+    e2 = 2.0 * eps * eps * D * D
+    bound = max(e2 / math.log(2.0) - math.log2(delta) - 1.0, 6.0 * e2 - 1.0)
+    return max(0, math.floor(bound) + 1) + 1
+
+
+def build_series(x, leaf, eps_sq, scale, t, fixed_rank=10, delta=None, n_block=4, eta=1.0):
+    """build_from_expansion (hmatrix.py:243-291) with gaussian_expansion_1d around the row
+    cluster centre, dense leaves from the Toeplitz symbol t (the CNSystem entry_fn,
+    levy.py:235-237).  Returns (root, order, blk)."""
+    x = np.asarray(x, dtype=float)
+    root, order = cluster_tree(x, leaf)
+    pts = x[order]
+    n = x.shape[0]
+    nmax = math.ceil(n / n_block)
+
+    def dense(r, c):
+        rows = order[r.lo:r.hi]
+        cols = order[c.lo:c.hi]
+        return Blk("D", d=t[n - 1 + cols[None, :] - rows[:, None]].copy())
+
+    def rec(r, c):
+        m, k = r.size, c.size
+        splittable = (not r.leaf) and (not c.leaf)
+        if splittable and (m > nmax or k > nmax):
+            pass
+        elif is_admissible(r, c, eta) and min(m, k) > leaf:
+            ctr = 0.5 * (r.blo + r.bhi)
+            K = series_terms(eps_sq, r.diam(), fixed_rank, delta)
+            u = series_cols(pts[r.lo:r.hi] - ctr[0], eps_sq, K, True, scale)
+            v = series_cols(pts[c.lo:c.hi] - ctr[0], eps_sq, K, False)
+            return Blk("R", u=u, v=v)
+        elif min(m, k) <= leaf or not splittable:
+            return dense(r, c)
+        (r0, r1), (c0, c1) = r.kids, c.kids
+        return Blk("H", k=[[rec(r0, c0), rec(r0, c1)], [rec(r1, c0), rec(r1, c1)]],
+                   rs=r0.size, cs=c0.size)
+
+    return root, order, rec(root, root)
+
+
+def build_gauss_cn(n, eps_sq, scale, a, b, c, dt, leaf, fixed_rank=10, delta=None, lo=-1.0, hi=1.0):
+    """levy.assemble_cn_1d + CNSystem.hmatrix('plus'/'minus') (levy.py:224-263) on
+    UniformGrid1D(n, lo, hi) (levy.py:84-102).  Returns (x, tA, lam, root, Hp, Hm)."""
+    h = (hi - lo) / n
+    x = lo + h * np.arange(n)
+    n_off = int(round((hi - lo) / h))
+    tA, lam = gauss_cn_symbol(n, h, eps_sq, scale, a, b, c, n_off)
+    tP = symbol_pm(tA, dt, "plus")
+    tM = symbol_pm(tA, dt, "minus")
+    root, _, Hp = build_series(x, leaf, eps_sq, -0.5 * dt * scale * h, tP, fixed_rank, delta)
+    _, _, Hm = build_series(x, leaf, eps_sq, +0.5 * dt * scale * h, tM, fixed_rank, delta)
+    return x, tA, lam, root, Hp, Hm

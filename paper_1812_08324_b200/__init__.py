@@ -12,11 +12,13 @@ from .fractional import (FracConfig, LevyMeasure, assemble_fractional_poisson_1d
                          quartic_window, tail_mass_power_1d, windowed_second_moment)
 from .geometry import (ClusterNode, ClusterTree, Permutation, PointSet, admissible,  # noqa: F401
                        build_cluster_tree)
-from .hmatrix import (HConfig, HMatrix, build_from_dense, build_toeplitz, derive_toeplitz,  # noqa: F401
-                      dump_structure, export_blocks, h_entry, memory_report, structure_summary,
-                      to_dense)
+from .hmatrix import (HConfig, HMatrix, KernelExpansion, ToeplitzEntries, build_from_dense,  # noqa: F401
+                      build_from_expansion, build_toeplitz, derive_toeplitz, dump_structure,
+                      export_blocks, gaussian_expansion_1d, h_entry, memory_report,
+                      rank_bound_gaussian, structure_summary, to_dense)
 from .hops import (SOLVE_METHODS, HFactorization, hlu, lowrank_add_recompress, matvec,  # noqa: F401
                    mul_dense, solve, trisolve_lower, trisolve_upper_right)
-from .levy import FracCNSystem, run_cn, step_cn  # noqa: F401
+from .levy import (CNSystem, FracCNSystem, UniformGrid1D, assemble_cn_1d, gaussian_measure,  # noqa: F401
+                   run_cn, step_cn)
 
 __version__ = "0.1.0"

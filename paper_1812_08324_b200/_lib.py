@@ -82,6 +82,11 @@ SIGNATURES = [
     ("lh_step_profile", C.c_int, [P, P, P, P, I32, I32, P]),
     ("lh_hlu_stats", C.c_int, [P, P]),
     ("lh_debug_task_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
+    ("lh_hmat_build_gauss_series", C.c_int, [P, P, P, P, P, P, C.c_double, C.c_double, C.c_int,
+                                             C.c_double, P, P]),
+    ("lh_gauss_series_terms", C.c_int, [C.c_double, C.c_double, C.c_int, C.c_double]),
+    ("lh_gauss_cn_symbol", C.c_int, [P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64,
+                                     C.c_double, C.c_double, C.c_double, C.c_double, P, P, P, P]),
     ("lh_debug_recomp_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
     ("lh_cn_symbol", C.c_int, [P, C.POINTER(MeasureC), C.POINTER(CNParamsC), P, P, P, P]),
 ]

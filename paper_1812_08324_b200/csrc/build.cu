@@ -155,6 +155,77 @@ void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA,
     }
 }
 
+// ---------------------------------------------------------------------------
+// smooth (Gaussian) jump density: nu(y) = scale e^{-eps_sq y^2} (levy.py:72-81)
+// CN operator of levy.CNSystem (levy.py:169-206, assemble_cn_1d :249-263):
+//   A[i, j] = -nu((j - i) h) h,  (i, i +- 1) += -a/h^2 -+ b/(2h),
+//   A[i, i] = 2a/h^2 - c + lam h,  lam = sum_{j=1..n_off} nu(-jh) + nu(jh)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double gauss_nu(double eps_sq, double scale, double y) {
+    return scale * exp(-eps_sq * (y * y));
+}
+
+__global__ void gauss_lam_kernel(double eps_sq, double scale, double h, i64 n_off, double *partials) {
+    __shared__ double red[dev::NW];
+    const i64 j0 = 1 + (i64)blockIdx.x * SUM_CHUNK;
+    const i64 j1 = min(j0 + SUM_CHUNK, n_off + 1);
+    double s = 0.0;
+    for (i64 j = j0 + threadIdx.x; j < j1; j += NT) {
+        const double y = (double)j * h;
+        s += gauss_nu(eps_sq, scale, -y) + gauss_nu(eps_sq, scale, y);
+    }
+    s = dev::block_sum(s, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void reduce_one_kernel(const double *partials, int nparts, double *out) {
+    __shared__ double red[dev::NW];
+    double s = 0.0;
+    for (int k = threadIdx.x; k < nparts; k += NT) s += partials[k];
+    s = dev::block_sum(s, red);
+    if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void gauss_symbol_kernel(double eps_sq, double scale, double h, i64 N, double a,
+                                    double b, double c, double dt, const double *lam, double *tA,
+                                    double *tP, double *tM) {
+    const double hd = 0.5 * dt;
+    const double h2 = h * h;
+    for (i64 idx = (i64)blockIdx.x * NT + threadIdx.x; idx < 2 * N - 1; idx += (i64)gridDim.x * NT) {
+        const i64 k = idx - (N - 1);
+        double t;
+        if (k == 0) {
+            t = 2 * a / h2 - c + lam[0] * h;
+        } else {
+            t = -gauss_nu(eps_sq, scale, (double)k * h) * h;
+            if (k == 1) t += -a / h2 - b / (2 * h);
+            if (k == -1) t += -a / h2 + b / (2 * h);
+        }
+        tA[idx] = t;
+        if (tP) tP[idx] = (k == 0 ? 1.0 : 0.0) + hd * t;
+        if (tM) tM[idx] = (k == 0 ? 1.0 : 0.0) - hd * t;
+    }
+}
+
+void gauss_cn_symbol(Ctx &ctx, i64 N, double h, double eps_sq, double scale, i64 n_off, double a,
+                     double b, double c, double dt, double *tA, double *tP, double *tM,
+                     double *lam_host) {
+    LH_REQUIRE(N >= 1 && n_off >= 1 && h > 0, LH_EINVAL, "need N >= 1, n_off >= 1 and h > 0");
+    LH_REQUIRE(eps_sq > 0 && scale >= 0, LH_EINVAL, "Gaussian density needs eps_sq > 0, scale >= 0");
+    const int nparts = (int)((n_off + SUM_CHUNK - 1) / SUM_CHUNK);
+    double *buf = (double *)ctx.ensure_scratch(sizeof(double) * ((size_t)nparts + 2));
+    double *lam = buf + nparts;
+    gauss_lam_kernel<<<nparts, NT, 0, ctx.stream>>>(eps_sq, scale, h, n_off, buf);
+    reduce_one_kernel<<<1, NT, 0, ctx.stream>>>(buf, nparts, lam);
+    const int grid = (int)std::min<i64>((2 * N - 1 + NT - 1) / NT, 148 * 16);
+    gauss_symbol_kernel<<<grid, NT, 0, ctx.stream>>>(eps_sq, scale, h, N, a, b, c, dt, lam, tA, tP, tM);
+    LH_CUDA(cudaGetLastError());
+    if (lam_host) {
+        LH_CUDA(cudaMemcpyAsync(lam_host, lam, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+}
+
 // ===========================================================================
 // entry sources
 // ===========================================================================
@@ -169,6 +240,15 @@ struct DenseSrc {  // row-major (numpy C order) or column-major
     int row_major;
     __device__ __forceinline__ double operator()(i64 i, i64 j) const {
         return row_major ? A[i * lda + j] : A[i + j * lda];
+    }
+};
+
+struct GaussSrc {  // expansion.kernel: scale e^{-eps_sq (x_i - y_j)^2} (hmatrix.py:174-176)
+    const double *x, *y;
+    double eps_sq, scale;
+    __device__ __forceinline__ double operator()(i64 i, i64 j) const {
+        const double d = x[i] - y[j];
+        return scale * exp(-eps_sq * d * d);
     }
 };
 
@@ -373,7 +453,8 @@ static void set_smem(const void *fn, size_t bytes) {
 
 // storage layout: dense region then low-rank region; returns the low-rank leaves in ACA
 // order (size-sorted, largest first)
-static std::vector<int32_t> build_layout(Ctx &ctx, HMat &H, const lh_hconfig &cfg) {
+static std::vector<int32_t> build_layout(Ctx &ctx, HMat &H, const lh_hconfig &cfg,
+                                         const std::vector<int32_t> *cap_of = nullptr) {
     const int kcap = std::min(std::max(cfg.kcap, 1), KC_MAX);
     i64 off = 0;
     int nslots = 0;
@@ -388,12 +469,14 @@ static std::vector<int32_t> build_layout(Ctx &ctx, HMat &H, const lh_hconfig &cf
     for (int32_t b : H.leafblocks) {
         Node &nd = H.nodes[b];
         if (nd.kind == K_LR) {
-            nd.kcap = kcap;
+            // capacity = stored rank + H-LU fill before recompression (<= KA_MAX); kept ranks
+            // stay <= KC_MAX
+            nd.kcap = cap_of ? std::min(std::max((*cap_of)[b], kcap), KA_MAX) : kcap;
             nd.rslot = nslots++;
             nd.uoff = off;
-            off += nd.m * kcap;
+            off += nd.m * nd.kcap;
             nd.voff = off;
-            off += nd.n * kcap;
+            off += nd.n * nd.kcap;
             lr.push_back(b);
         }
     }
@@ -684,6 +767,95 @@ void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg) {
 void build_dense(Ctx &ctx, HMat &H, const double *A, i64 lda, int row_major, const lh_hconfig &cfg) {
     DenseSrc s{A, lda, row_major};
     run_build(ctx, H, s, cfg);
+}
+
+// ===========================================================================
+// series builder (hmatrix.py:243-291 build_from_expansion with the Gaussian family of
+// gaussian_expansion_1d, :156-186): every admissible block with min(m, n) > n_min is
+// low-rank with n_terms analytic columns around the ROW cluster centre c,
+//   U[i, k] = scale (2 eps_sq s_i)^k e^{-eps_sq s_i^2} / k!   (s_i = x_i - c)
+//   V[j, k] = t_j^k e^{-eps_sq t_j^2}                         (t_j = y_j - c)
+// by the reference's column recurrence (col_k = col_{k-1} * base / k), one thread per
+// row, one CTA per block; no dense fallback (the series rank is kept as is).
+// ===========================================================================
+struct SeriesJob {
+    i64 r0, c0, m, n, uoff, voff;
+    double centre;
+    int32_t K, slot;
+};
+
+__global__ void series_kernel(const SeriesJob *jobs, int njobs, const double *xr, const double *yc,
+                              double eps_sq, double scale, double *arena, int32_t *ranks) {
+    for (int b = blockIdx.x; b < njobs; b += gridDim.x) {
+        const SeriesJob J = jobs[b];
+        for (i64 e = threadIdx.x; e < J.m + J.n; e += NT) {
+            const bool row = e < J.m;
+            const double t = row ? xr[J.r0 + e] - J.centre : yc[J.c0 + e - J.m] - J.centre;
+            double *out = row ? arena + J.uoff + e : arena + J.voff + (e - J.m);
+            const i64 ld = row ? J.m : J.n;
+            double v = (row ? scale : 1.0) * exp(-eps_sq * t * t);
+            const double base = row ? 2.0 * eps_sq * t : t;
+            out[0] = v;
+            for (int k = 1; k < J.K; ++k) {
+                v = row ? v * base / (double)k : v * base;
+                out[(i64)k * ld] = v;
+            }
+        }
+        if (threadIdx.x == 0) ranks[J.slot] = J.K;
+    }
+}
+
+// hmatrix.py:270-281 (rank_bound_gaussian) and :284-290 (_expansion_terms)
+int gauss_series_terms(double eps_sq, double D, int fixed_rank, double delta) {
+    if (!(delta > 0.0)) return fixed_rank;
+    if (D <= 0.0) return 1;
+    const double eps = std::sqrt(eps_sq);
+    const double e2 = 2.0 * eps * eps * D * D;
+    const double bound = std::max(e2 / std::log(2.0) - std::log2(delta) - 1.0, 6.0 * e2 - 1.0);
+    return std::max(0, (int)std::floor(bound) + 1) + 1;
+}
+
+void build_gauss_series(Ctx &ctx, HMat &H, const double *t, const double *xr, const double *yc,
+                        double eps_sq, double scale, int fixed_rank, double delta,
+                        const lh_hconfig &cfg) {
+    LH_REQUIRE(eps_sq > 0, LH_EINVAL, "series builder needs eps_sq > 0");
+    LH_REQUIRE(delta > 0 || fixed_rank >= 1, LH_EINVAL, "fixed_rank must be >= 1");
+    LH_REQUIRE(H.rt->dim == 1 && H.ct->dim == 1, LH_EINVAL, "the device series builder is 1D");
+    // per-block series rank; blocks whose rank exceeds KC_MAX / 2 get the full recompression
+    // width (rank + an H-LU update of up to the same order) as capacity
+    std::vector<int32_t> terms(H.nodes.size(), 0), cap(H.nodes.size(), 0);
+    for (int32_t b : H.leafblocks) {
+        const Node &nd = H.nodes[b];
+        if (nd.kind != K_LR) continue;
+        terms[b] = gauss_series_terms(eps_sq, diameter(H.rt->nodes[nd.rcl], 1), fixed_rank, delta);
+        cap[b] = 2 * terms[b] > KC_MAX ? KA_MAX : 0;
+    }
+    std::vector<int32_t> lr = build_layout(ctx, H, cfg, &cap);
+    std::vector<SeriesJob> jobs;
+    jobs.reserve(lr.size());
+    for (int32_t b : lr) {
+        const Node &nd = H.nodes[b];
+        const Cluster &rc = H.rt->nodes[nd.rcl];
+        const int K = terms[b];
+        if (K > KC_MAX)
+            throw Error(LH_ERANK, "series rank " + std::to_string(K) + " exceeds the stored-rank limit " +
+                                      std::to_string(KC_MAX) + " for block (" +
+                                      std::to_string(nd.r0) + "," + std::to_string(nd.c0) + "," +
+                                      std::to_string(nd.m) + "x" + std::to_string(nd.n) + ")");
+        jobs.push_back({nd.r0, nd.c0, nd.m, nd.n, nd.uoff, nd.voff, 0.5 * (rc.blo[0] + rc.bhi[0]), K,
+                        nd.rslot});
+    }
+    if (!jobs.empty()) {
+        SeriesJob *d = dupload(jobs, ctx.stream);
+        const int grid = (int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 16);
+        series_kernel<<<grid, NT, 0, ctx.stream>>>(d, (int)jobs.size(), xr, yc, eps_sq, scale,
+                                                   H.d_arena, H.d_ranks);
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(d);
+    }
+    if (t) build_finalize(ctx, H, ToepSrc{t, H.nrows}, {});
+    else build_finalize(ctx, H, GaussSrc{xr, yc, eps_sq, scale}, {});
 }
 
 // ===========================================================================

@@ -19,6 +19,13 @@ namespace lh {
 void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA, double *tP,
                double *tM, double *sums_host);
 void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg);
+void build_gauss_series(Ctx &ctx, HMat &H, const double *t, const double *xr, const double *yc,
+                        double eps_sq, double scale, int fixed_rank, double delta,
+                        const lh_hconfig &cfg);
+int gauss_series_terms(double eps_sq, double D, int fixed_rank, double delta);
+void gauss_cn_symbol(Ctx &ctx, i64 N, double h, double eps_sq, double scale, i64 n_off, double a,
+                     double b, double c, double dt, double *tA, double *tP, double *tM,
+                     double *lam_host);
 void build_dense(Ctx &ctx, HMat &H, const double *A, i64 lda, int row_major, const lh_hconfig &cfg);
 void derive(Ctx &ctx, const HMat &S, HMat &D, const double *t, double scale, int kcap);
 void hlu(Ctx &ctx, HMat &H, double eps2);
@@ -289,6 +296,41 @@ int lh_hmat_shard_unpack(lh_ctx *ctx, lh_hmat *h, int32_t src_rank, const double
 
 int lh_hmat_shard_finalize(lh_ctx *ctx, lh_hmat *h) {
     return guard(ctx, [&] { shard_finalize(ctx->c, h->h); });
+}
+
+int lh_hmat_build_gauss_series(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,
+                               const double *row_pts_dev, const double *col_pts_dev, double eps_sq,
+                               double scale, int fixed_rank, double delta, const lh_hconfig *cfg,
+                               lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        check_cfg(cfg);
+        LH_REQUIRE(row_pts_dev && col_pts_dev, LH_EINVAL, "series builder needs the tree-order points");
+        o = new_hmat(rt, ct);
+        partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
+        build_gauss_series(ctx->c, o->h, t_dev, row_pts_dev, col_pts_dev, eps_sq, scale, fixed_rank,
+                           delta, *cfg);
+        start_background_plans(o->h);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+int lh_gauss_series_terms(double eps_sq, double diameter, int fixed_rank, double delta) {
+    return gauss_series_terms(eps_sq, diameter, fixed_rank, delta);
+}
+
+int lh_gauss_cn_symbol(lh_ctx *ctx, int64_t N, double h, double eps_sq, double scale, int64_t n_off,
+                       double a, double b, double c, double dt, double *tA_dev, double *tPlus_dev,
+                       double *tMinus_dev, double *lam_host) {
+    return guard(ctx, [&] {
+        gauss_cn_symbol(ctx->c, N, h, eps_sq, scale, n_off, a, b, c, dt, tA_dev, tPlus_dev,
+                        tMinus_dev, lam_host);
+    });
 }
 
 int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,

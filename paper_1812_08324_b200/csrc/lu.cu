@@ -1457,6 +1457,15 @@ static int prop_kcap() {
     return v;
 }
 
+// the propagator's capacity for a factor whose low-rank blocks were laid out wider than
+// KC_MAX (series builds with high expansion ranks): the full recompression width
+static int prop_kcap_for(const HMat &F) {
+    int mx = 0;
+    for (const Node &nd : F.nodes)
+        if (nd.kind == K_LR && nd.vpar < 0) mx = std::max(mx, nd.kcap);
+    return mx > KC_MAX ? KA_MAX : prop_kcap();
+}
+
 struct PlanJob {
     HMat shadow;   // structure-only copy the H-LU planner mutates (no device memory)
     HMat fshadow;  // the factor's structure as the H-LU leaves it (mark_lu_leaves), read-only
@@ -1526,7 +1535,7 @@ void start_background_plans(HMat &H) {
     if (!getenv("LEVYH_NO_BG_PROP"))
     job->f_prop = std::async(std::launch::async, [j] {
         try {
-            block_layout(j->Z, j->fshadow, 2, prop_kcap());
+            block_layout(j->Z, j->fshadow, 2, prop_kcap_for(j->fshadow));
             j->prop = plan_propagator(j->fshadow, j->Z, 1e-10);
             // upload on a stream of this thread once the H-LU planning (and with it the
             // streamed H-LU chunk uploads) is done: the copies overlap the H-LU's last chunks
@@ -1906,7 +1915,7 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
         }
     }
     if (!P) {
-        block_layout(*Z, F, 2, prop_kcap());
+        block_layout(*Z, F, 2, prop_kcap_for(F));
         P = plan_propagator(F, *Z, eps2);
     }
     auto now = [] { return std::chrono::steady_clock::now(); };

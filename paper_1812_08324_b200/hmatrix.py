@@ -20,8 +20,9 @@ from . import _lib
 from .geometry import ClusterTree
 
 __all__ = ["HConfig", "HMatrix", "Dense", "LowRank", "Hier", "FactoredDense", "build_from_dense",
-           "build_toeplitz", "memory_report", "structure_summary", "dump_structure", "to_dense",
-           "h_entry", "export_blocks"]
+           "build_toeplitz", "build_from_expansion", "KernelExpansion", "gaussian_expansion_1d",
+           "rank_bound_gaussian", "ToeplitzEntries", "memory_report", "structure_summary",
+           "dump_structure", "to_dense", "h_entry", "export_blocks"]
 
 KIND_NAMES = {0: "dense", 1: "lowrank", 2: "dense_lu"}
 
@@ -206,6 +207,122 @@ def build_toeplitz(t, row_ct, col_ct, cfg=None, distributed=False):
     nc = cfg.native()
     rc = _lib.lib().lh_hmat_build_toeplitz(ctx.h, row_ct.handle, col_ct.handle,
                                            C.c_void_p(t.data_ptr()), C.byref(nc), C.byref(h))
+    _lib.check(rc, ctx.h)
+    return HMatrix(h, row_ct, col_ct, cfg.eta, ctx, cfg)
+
+
+@dataclass
+class KernelExpansion:
+    """hmatrix.py:140-153: separable expansion k(x, y) ~ sum_n a_n(x - c) b_n(y - c).
+
+    ``kernel`` / ``row_factors`` / ``col_factors`` are the reference's host callables (API
+    surface; the device builder never calls them).  ``family`` names an expansion the device
+    builder generates itself: ("gauss1d", eps_sq, scale) for gaussian_expansion_1d."""
+
+    kernel: object
+    row_factors: object
+    col_factors: object
+    eps: float = 1.0
+    family: tuple | None = None
+
+
+def _gauss_columns(t, eps_sq, n_terms, alpha, scale=1.0):
+    # hmatrix.py:156-169 (host evaluation for the reference API; the device builder runs the
+    # same recurrence in csrc/build.cu series_kernel)
+    out = np.empty((t.shape[0], n_terms))
+    col = scale * np.exp(-eps_sq * t * t)
+    out[:, 0] = col
+    base = 2.0 * eps_sq * t if alpha else t
+    for k in range(1, n_terms):
+        col = col * base / k if alpha else col * base
+        out[:, k] = col
+    return out
+
+
+def gaussian_expansion_1d(eps_sq, scale=1.0):
+    """hmatrix.py:171-186: expansion of scale * exp(-eps_sq (x - y)^2) on 1D points."""
+
+    def kernel(X, Y):
+        d = X[:, :1] - Y[:, :1].T
+        return scale * np.exp(-eps_sq * d * d)
+
+    def row_factors(X, center, n_terms):
+        return _gauss_columns(X[:, 0] - center[0], eps_sq, n_terms, True, scale)
+
+    def col_factors(Y, center, n_terms):
+        return _gauss_columns(Y[:, 0] - center[0], eps_sq, n_terms, False)
+
+    return KernelExpansion(kernel, row_factors, col_factors, eps=math.sqrt(eps_sq),
+                           family=("gauss1d", float(eps_sq), float(scale)))
+
+
+def rank_bound_gaussian(eps, D, delta):
+    """hmatrix.py:270-281: smallest r > max(log2(e^{2 eps^2 D^2}/delta) - 1, 12 eps^2 D^2 - 1)."""
+    if D <= 0 or delta <= 0:
+        raise ValueError("D and delta must be positive")
+    e2 = 2.0 * eps * eps * D * D
+    bound = max(e2 / math.log(2.0) - math.log2(delta) - 1.0, 6.0 * e2 - 1.0)
+    return max(0, math.floor(bound) + 1)
+
+
+@dataclass
+class ToeplitzEntries:
+    """Entry source of a Toeplitz matrix, A[i, j] = symbol[n_rows - 1 + j - i] in tree order
+    (the entry_fn levy.CNSystem.hmatrix passes, levy.py:235-237, for 1D uniform grids).
+    ``symbol`` is a device (torch) or host array of length n_rows + n_cols - 1."""
+
+    symbol: object
+
+    def __call__(self, rows, cols):
+        t = self.symbol
+        t = t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+        n_rows = (t.shape[0] + 1) // 2
+        return t[n_rows - 1 + np.asarray(cols)[None, :] - np.asarray(rows)[:, None]]
+
+
+def build_from_expansion(row_ct, col_ct, expansion, cfg=None, entry_fn=None):
+    """hmatrix.py:243-291 on the GPU: partition of :319-337 with every admissible block
+    (min(m,n) > n_min) low-rank from the series (cfg.fixed_rank terms, or the Gaussian rank
+    bound + 1 per block when cfg.delta is set), dense leaves from ``entry_fn`` (a
+    ToeplitzEntries) or, without one, from the expansion kernel.
+
+    The device builder generates the Gaussian family (gaussian_expansion_1d); other
+    expansions and arbitrary entry callables raise TypeError (they would have to run on the
+    host)."""
+    import torch
+
+    cfg = cfg or HConfig()
+    if cfg.n_block < 2:
+        raise ValueError("n_block must be >= 2")
+    fam = getattr(expansion, "family", None)
+    if not fam or fam[0] != "gauss1d":
+        raise TypeError("the device series builder generates the 1D Gaussian expansion "
+                        "(gaussian_expansion_1d); got " + repr(fam))
+    if row_ct.dim != 1 or col_ct.dim != 1:
+        raise ValueError("gaussian_expansion_1d needs 1D cluster trees")
+    ctx = _lib.Context.get()
+    dev = f"cuda:{ctx.device}"
+    xr = torch.as_tensor(np.ascontiguousarray(row_ct.points[:, 0], dtype=np.float64)).to(dev)
+    yc = torch.as_tensor(np.ascontiguousarray(col_ct.points[:, 0], dtype=np.float64)).to(dev)
+    t = None
+    if entry_fn is not None:
+        if not isinstance(entry_fn, ToeplitzEntries):
+            raise TypeError("entry_fn must be a ToeplitzEntries (device entry source)")
+        t = entry_fn.symbol
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+            t = torch.as_tensor(np.asarray(t, dtype=np.float64)).to(dev)
+        t = t.contiguous()
+        if t.numel() != len(row_ct) + len(col_ct) - 1:
+            raise ValueError("symbol length must be n_rows + n_cols - 1")
+    delta = float(cfg.delta) if cfg.delta is not None else 0.0
+    if cfg.delta is not None and not cfg.delta > 0:
+        raise ValueError("D and delta must be positive")
+    h = C.c_void_p()
+    nc = cfg.native()
+    rc = _lib.lib().lh_hmat_build_gauss_series(
+        ctx.h, row_ct.handle, col_ct.handle, C.c_void_p(t.data_ptr()) if t is not None else None,
+        C.c_void_p(xr.data_ptr()), C.c_void_p(yc.data_ptr()), fam[1], fam[2], int(cfg.fixed_rank),
+        delta, C.byref(nc), C.byref(h))
     _lib.check(rc, ctx.h)
     return HMatrix(h, row_ct, col_ct, cfg.eta, ctx, cfg)
 

@@ -7,17 +7,189 @@ on the interior nodes x_k = k h of [-L, L] with u = 0 outside.  A is the
 negated singularity-subtraction stencil (fractional.py:362-405) plus the
 local band of levy._entries_a_1d (levy.py:169-176) with b_eff = b + beta
 (SURVEY G4), and A+- = I +- dt/2 A (levy.py:194-206).
+
+The smooth-measure system of the reference itself (levy.CNSystem with gaussian_measure,
+assemble_cn_1d, the series H-builder; the reference's own `levyh bench` path, cli.py:163-224)
+is CNSystem below: same Toeplitz machinery, low-rank blocks from the analytic expansion.
 """
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import numpy as np
 
 from . import fractional as frac
+from .fractional import LevyMeasure
 from .geometry import build_cluster_tree
-from .hmatrix import HConfig, build_toeplitz, derive_toeplitz
+from .hmatrix import (HConfig, ToeplitzEntries, build_from_expansion, build_toeplitz, derive_toeplitz,
+                      gaussian_expansion_1d)
 from .hops import SOLVE_METHODS, hlu, matvec, solve
 
-__all__ = ["FracCNSystem", "step_cn", "run_cn"]
+__all__ = ["FracCNSystem", "CNSystem", "LevyMeasure", "UniformGrid1D", "gaussian_measure",
+           "assemble_cn_1d", "step_cn", "run_cn"]
+
+
+def gaussian_measure(eps_sq=5.0, scale=1.0):
+    """levy.py:72-81: jump density scale * exp(-eps_sq y^2) (enables the series builder)."""
+    return LevyMeasure(
+        density=lambda y: scale * np.exp(-eps_sq * np.asarray(y, dtype=float) ** 2),
+        kind="smooth_semi_heavy", symmetric=True,
+        density2=lambda dx, dy: scale * np.exp(-eps_sq * (dx * dx + dy * dy)),
+        gauss_eps_sq=eps_sq, scale=scale)
+
+
+@dataclass(frozen=True)
+class UniformGrid1D:
+    """levy.py:84-102: n points x_i = lo + i h, h = (hi - lo) / n."""
+
+    n: int
+    lo: float = -1.0
+    hi: float = 1.0
+
+    @property
+    def h(self):
+        return (self.hi - self.lo) / self.n
+
+    @property
+    def points(self):
+        return self.lo + self.h * np.arange(self.n)
+
+    @property
+    def size(self):
+        return self.n
+
+
+class CNSystem:
+    """levy.py:131-246 for the smooth (Gaussian) jump density on a 1D uniform grid: the CN
+    operators are Toeplitz, their symbols are generated on the GPU (lh_gauss_cn_symbol) and
+    ``hmatrix`` runs the series builder (build_from_expansion with gaussian_expansion_1d and
+    the exact entries as dense leaves, levy.py:224-239) on the device."""
+
+    def __init__(self, grid, nu, a, b, c, dt, n_off, lam, dim, symbols):
+        self.grid, self.nu, self.a, self.b, self.c, self.dt = grid, nu, a, b, c, dt
+        self.n_off = n_off
+        self.lam = lam
+        self.dim = dim
+        self.h = grid.h
+        self.tA, self.tPlus, self.tMinus = symbols
+        self.tree = None
+        self.factor = None
+        self.h_minus = None
+        self.method = "inverse"
+        self._host = {}
+
+    @property
+    def n(self):
+        return self.grid.size
+
+    @property
+    def N(self):
+        return self.grid.size
+
+    size = n
+
+    def weight(self, j):
+        """levy.py:158-163."""
+        j = np.asarray(j)
+        w = np.full(j.shape, self.h, dtype=float)
+        w[np.abs(j) >= self.n_off] = self.h / 2.0
+        return w
+
+    def _symbol(self, which):
+        if which not in ("A", "plus", "minus"):
+            raise ValueError(which)
+        if which not in self._host:
+            t = {"A": self.tA, "plus": self.tPlus, "minus": self.tMinus}[which]
+            self._host[which] = t.cpu().numpy()
+        return self._host[which]
+
+    def entries(self, rows, cols, which="A"):
+        """levy.py:194-206: exact entries for original-order index arrays (read from the
+        device-generated symbol; the operator is Toeplitz)."""
+        t = self._symbol(which)
+        rows = np.asarray(rows, dtype=np.intp)
+        cols = np.asarray(cols, dtype=np.intp)
+        return t[self.n - 1 + cols[None, :] - rows[:, None]]
+
+    def dense_matrix(self, which="A"):
+        """levy.py:210-214 (small sizes: n x n host array)."""
+        idx = np.arange(self.n)
+        return self.entries(idx, idx, which)
+
+    def cluster_tree(self, leaf_size=64, strategy="bisection"):
+        """levy.py:216-222."""
+        if self.tree is None:
+            self.tree = build_cluster_tree(self.grid.points[:, None], leaf_size=leaf_size,
+                                           strategy=strategy)
+        return self.tree
+
+    def hmatrix(self, which="plus", cfg=None):
+        """levy.py:224-239: the series H-builder on the GPU."""
+        cfg = cfg or HConfig()
+        if self.nu.gauss_eps_sq is None:
+            raise ValueError("series H-builder requires a Gaussian jump density")
+        ct = self.cluster_tree(leaf_size=cfg.n_min)
+        if not np.array_equal(ct.perm.inverse, np.arange(self.n)):
+            raise ValueError("the Toeplitz entry source needs the identity tree permutation")
+        sign = {"A": -1.0, "plus": -0.5 * self.dt, "minus": +0.5 * self.dt}[which]
+        scale = sign * self.nu.scale * self.h ** self.dim
+        expansion = gaussian_expansion_1d(self.nu.gauss_eps_sq, scale=scale)
+        t = {"A": self.tA, "plus": self.tPlus, "minus": self.tMinus}[which]
+        return build_from_expansion(ct, ct, expansion, cfg, entry_fn=ToeplitzEntries(t))
+
+    def build_pair(self, cfg=None):
+        """H+ and H- with H-'s factors derived from H+'s: the series U carries the sign
+        (scale = -+ dt/2 * nu.scale * h), so H-'s low-rank blocks are exactly (-U, V)."""
+        cfg = cfg or HConfig()
+        Hp = self.hmatrix("plus", cfg)
+        Hm = derive_toeplitz(Hp, self.tMinus, lr_scale=-1.0, kcap=0)
+        return Hp, Hm
+
+    def prepare(self, cfg=None, eps2=1e-10, method="inverse"):
+        """levy.py:241-246: factorise A+ once and keep A- for stepping."""
+        Hp, Hm = self.build_pair(cfg)
+        self.h_minus = Hm
+        self.factor = hlu(Hp, eps2)
+        if method == "inverse":
+            self.factor.prepare_inverse()
+        elif method == "propagator":
+            self.factor.prepare_propagator()
+        self.method = method
+        return self.factor
+
+
+def assemble_cn_1d(nu, a, b, c, grid, dt, window=None):
+    """levy.py:249-263 (+ _check_coeffs :240-246): the Toeplitz symbols of A, A+ and A- are
+    generated on the GPU for the Gaussian density (lh_gauss_cn_symbol)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+
+    if a < 0 or c > 0:
+        raise ValueError("stability requires a >= 0 and c <= 0")
+    if nu.kind != "smooth_semi_heavy":
+        raise ValueError("CN assembly needs a smooth semi-heavy density; "
+                         "use levyh.fractional for singular measures")
+    if nu.gauss_eps_sq is None:
+        raise ValueError("the device CN assembly generates the Gaussian density "
+                         "(gaussian_measure); use FracCNSystem for power / CGMY measures")
+    if nu.gauss_eps_sq <= 0 or nu.scale < 0:
+        raise ValueError("jump density must be nonnegative")
+    span = window if window is not None else (grid.hi - grid.lo)
+    n_off = int(round(span / grid.h))
+    ctx = _lib.Context.get()
+    n = grid.size
+    dev = f"cuda:{ctx.device}"
+    tA, tP, tM = (torch.empty(2 * n - 1, dtype=torch.float64, device=dev) for _ in range(3))
+    lam = C.c_double()
+    _lib.check(_lib.lib().lh_gauss_cn_symbol(ctx.h, n, grid.h, float(nu.gauss_eps_sq),
+                                             float(nu.scale), n_off, float(a), float(b), float(c),
+                                             float(dt), C.c_void_p(tA.data_ptr()),
+                                             C.c_void_p(tP.data_ptr()), C.c_void_p(tM.data_ptr()),
+                                             C.byref(lam)), ctx.h)
+    return CNSystem(grid, nu, a, b, c, dt, n_off, float(lam.value), 1, (tA, tP, tM))
 
 
 class FracCNSystem:
@@ -116,8 +288,13 @@ def step_cn(sys, u_n, F=None, method=None):
     return perm.from_tree(solve(F, rhs, method or getattr(sys, "method", "substitution")))
 
 
-def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method="inverse"):
-    """levy.py:309-330: factor once, march n_steps on the device (CUDA-graph loop)."""
+def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method="inverse", mode="hmatrix"):
+    """levy.py:309-330: factor once, march n_steps on the device (CUDA-graph loop).
+    ``mode='dense'`` (the reference's dense LU oracle) is test infrastructure, not a product
+    path."""
+    if mode != "hmatrix":
+        raise ValueError("only mode='hmatrix' runs on the device (the dense oracle lives in "
+                         "oracle/levyh_oracle.py)")
     import torch
 
     from . import _lib
