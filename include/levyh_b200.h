@@ -202,6 +202,42 @@ int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *
 int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const double *u_host,
                           const double *v_host, double *out_host);
 
+/* ---- Krylov consumers: levyh.solvers (solvers.py:39-153) ---------------- */
+/* Operator for the Krylov solvers, y = op(x) on device vectors of length n, ordered on the
+ * context's stream.  solvers.py:39-43 _as_operator accepts a callable or a dense matrix;
+ * here: an H-matvec (hops.matvec), an H-LU solve (hops.solve with lh_solve's method), a
+ * dense row-major matrix, or a host callback (returns an lh status code). */
+typedef int (*lh_apply_fn)(void *user, const double *x_dev, double *y_dev);
+enum { LH_OP_IDENTITY = 0, LH_OP_HMATVEC = 1, LH_OP_HSOLVE = 2, LH_OP_DENSE = 3, LH_OP_CALLBACK = 4 };
+typedef struct {
+    int32_t kind;         /* LH_OP_*                                           */
+    lh_hmat *hmat;        /* HMATVEC: H; HSOLVE: the factored H-matrix (hlu)   */
+    int32_t method;       /* HSOLVE: 0 substitution, 1 inverse, 2 propagator   */
+    const double *a_dev;  /* DENSE: n x n row-major, leading dimension lda     */
+    int64_t lda;
+    lh_apply_fn fn;       /* CALLBACK                                          */
+    void *user;
+} lh_operator;
+
+/* solvers.py:46-88 pcg: preconditioned conjugate gradient from x = 0; Minv NULL or
+ * LH_OP_IDENTITY = no preconditioner.  residuals_host[k] = ||r_k|| / ||b|| for every
+ * iteration (capacity max_iter); *iters, *converged as IterationLog.  p'Ap <= 0 fails with
+ * LH_ESINGULAR "PCG breakdown: operator is not positive definite" (solvers.py:71-72). */
+int lh_pcg(lh_ctx *ctx, const lh_operator *A, const lh_operator *Minv, const double *b_dev,
+           int64_t n, double tol, int32_t max_iter, double *x_dev, double *residuals_host,
+           int32_t *iters, int32_t *converged);
+/* solvers.py:91-153 gmres_restarted: right-preconditioned restarted GMRES (modified
+ * Gram-Schmidt Arnoldi, Givens rotations), restart <= 64; residuals as lh_pcg.
+ * Stagnation returns LH_OK with *converged = 0. */
+int lh_gmres_restarted(lh_ctx *ctx, const lh_operator *A, const lh_operator *Minv,
+                       const double *b_dev, int64_t n, double tol, int32_t restart,
+                       int32_t max_iter, double *x_dev, double *residuals_host, int32_t *iters,
+                       int32_t *converged);
+/* y = A x for a dense row-major m x n device matrix (the dense-operator path of the Krylov
+ * solvers, solvers.py:42-43). */
+int lh_dense_gemv(lh_ctx *ctx, const double *a_dev, int64_t lda, int64_t m, int64_t n,
+                  const double *x_dev, double *y_dev);
+
 /* ---- entry generation: fractional.py:285-405 + levy.py:169-206 -------- */
 typedef struct {
     int32_t kind;   /* 0: power c|y|^(-1-2s); 1: CGMY; 2: tabulated nu(j*h), j=-M..M */

@@ -751,3 +751,104 @@ def build_gauss_cn(n, eps_sq, scale, a, b, c, dt, leaf, fixed_rank=10, delta=Non
     root, _, Hp = build_series(x, leaf, eps_sq, -0.5 * dt * scale * h, tP, fixed_rank, delta)
     _, _, Hm = build_series(x, leaf, eps_sq, +0.5 * dt * scale * h, tM, fixed_rank, delta)
     return x, tA, lam, root, Hp, Hm
+
+
+# ---------------------------------------------------------------------------
+# Krylov consumers   (solvers.py:46-153)
+# ---------------------------------------------------------------------------
+
+
+def _op(f):
+    """solvers.py:39-43: callables pass through, arrays become a matvec."""
+    if f is None:
+        return lambda v: v
+    if callable(f):
+        return f
+    mat = np.asarray(f)
+    return lambda v: mat @ v
+
+
+def pcg(A, Minv, b, tol=1e-8, max_iter=500):
+    """Preconditioned CG from x = 0 (solvers.py:46-88).  Returns (x, residuals, converged);
+    raises LinAlgError when p'Ap <= 0 (solvers.py:71-72)."""
+    A, M = _op(A), _op(Minv)
+    b = np.asarray(b, dtype=float)
+    x = np.zeros_like(b)
+    nb = np.linalg.norm(b)
+    if nb == 0:
+        return x, [], True
+    r = b.copy()
+    z = M(r)
+    p = np.array(z, copy=True)
+    rz = float(np.dot(r, z))
+    hist = []
+    for _ in range(max_iter):
+        q = A(p)
+        curv = float(np.dot(p, q))
+        if curv <= 0:
+            raise np.linalg.LinAlgError("PCG breakdown: operator is not positive definite")
+        step = rz / curv
+        x += step * p
+        r -= step * q
+        hist.append(float(np.linalg.norm(r) / nb))
+        if hist[-1] <= tol:
+            return x, hist, True
+        z = M(r)
+        rz_next = float(np.dot(r, z))
+        p = z + (rz_next / rz) * p
+        rz = rz_next
+    return x, hist, False
+
+
+def gmres_restarted(A, Minv, b, tol=1e-8, restart=50, max_iter=500):
+    """Right-preconditioned restarted GMRES (solvers.py:91-153): modified Gram-Schmidt
+    Arnoldi, Givens rotations, residual of the original system.  Returns
+    (x, residuals, converged)."""
+    A, M = _op(A), _op(Minv)
+    b = np.asarray(b, dtype=float)
+    n = b.size
+    x = np.zeros_like(b)
+    nb = np.linalg.norm(b)
+    if nb == 0:
+        return x, [], True
+    hist, done, count = [], False, 0
+    while count < max_iter and not done:
+        r = b - A(x)
+        beta = float(np.linalg.norm(r))
+        if beta / nb <= tol:
+            done = True
+            break
+        m = min(restart, max_iter - count)
+        Q = np.zeros((n, m + 1))
+        Hs = np.zeros((m + 1, m))
+        rot = np.zeros((m, 2))  # (cos, sin)
+        g = np.zeros(m + 1)
+        g[0] = beta
+        Q[:, 0] = r / beta
+        k = 0
+        for j in range(m):
+            w = A(M(Q[:, j]))
+            for i in range(j + 1):  # MGS
+                Hs[i, j] = float(np.dot(w, Q[:, i]))
+                w = w - Hs[i, j] * Q[:, i]
+            Hs[j + 1, j] = float(np.linalg.norm(w))
+            if Hs[j + 1, j] > 0:
+                Q[:, j + 1] = w / Hs[j + 1, j]
+            for i in range(j):  # earlier rotations on the new column
+                c, s = rot[i]
+                hi, hn = Hs[i, j], Hs[i + 1, j]
+                Hs[i, j], Hs[i + 1, j] = c * hi + s * hn, -s * hi + c * hn
+            rho = np.hypot(Hs[j, j], Hs[j + 1, j])
+            rot[j] = Hs[j, j] / rho, Hs[j + 1, j] / rho
+            Hs[j, j], Hs[j + 1, j] = rho, 0.0
+            g[j], g[j + 1] = rot[j, 0] * g[j], -rot[j, 1] * g[j]
+            k = j + 1
+            count += 1
+            hist.append(float(abs(g[j + 1]) / nb))
+            if hist[-1] <= tol:
+                break
+        y = np.linalg.solve(Hs[:k, :k], g[:k]) if k else np.zeros(0)
+        x = x + M(Q[:, :k] @ y)
+        if hist and hist[-1] <= tol:
+            done = True
+    return x, hist, done

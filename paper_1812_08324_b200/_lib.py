@@ -88,6 +88,9 @@ SIGNATURES = [
     ("lh_gauss_cn_symbol", C.c_int, [P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64,
                                      C.c_double, C.c_double, C.c_double, C.c_double, P, P, P, P]),
     ("lh_debug_recomp_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
+    ("lh_pcg", C.c_int, [P, P, P, P, I64, D, I32, P, P, P, P]),
+    ("lh_gmres_restarted", C.c_int, [P, P, P, P, I64, D, I32, I32, P, P, P, P]),
+    ("lh_dense_gemv", C.c_int, [P, P, I64, I64, I64, P, P]),
     ("lh_cn_symbol", C.c_int, [P, C.POINTER(MeasureC), C.POINTER(CNParamsC), P, P, P, P]),
 ]
 

@@ -48,6 +48,20 @@ int lowrank_add_recompress(Ctx &ctx, i64 m, i64 n, const double *u1, const doubl
 void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
 void recomp_bench(Ctx &ctx, int m, int n, int K, int reps, const double *U, const double *V, double *out);
 void start_background_plans(HMat &H);
+struct KOp {
+    int kind = LH_OP_IDENTITY;
+    HMat *h = nullptr;
+    int method = 0;
+    const double *a = nullptr;
+    i64 lda = 0;
+    lh_apply_fn fn = nullptr;
+    void *user = nullptr;
+};
+void pcg(Ctx &ctx, const KOp &A, const KOp &M, const double *b, i64 n, double tol, int max_iter,
+         double *x, double *res, int *iters, int *conv);
+void gmres(Ctx &ctx, const KOp &A, const KOp &M, const double *b, i64 n, double tol, int restart,
+           int max_iter, double *x, double *res, int *iters, int *conv);
+void dense_gemv(Ctx &ctx, const double *A, i64 lda, i64 m, i64 n, const double *x, double *y);
 
 double *DevBuf::ensure(i64 n) {
     if (n > cap) {
@@ -603,6 +617,58 @@ int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const doub
 int lh_hlu_stats(const lh_hmat *f, double *out) {
     for (int k = 0; k < 5; ++k) out[k] = f->h.lu_stats[k];
     return LH_OK;
+}
+
+static KOp resolve_op(const lh_operator *op) {
+    KOp k;
+    if (!op) return k;
+    k.kind = op->kind;
+    k.h = op->hmat ? &op->hmat->h : nullptr;
+    k.method = op->method;
+    k.a = op->a_dev;
+    k.lda = op->lda;
+    k.fn = op->fn;
+    k.user = op->user;
+    return k;
+}
+
+int lh_pcg(lh_ctx *ctx, const lh_operator *A, const lh_operator *Minv, const double *b, int64_t n,
+           double tol, int32_t max_iter, double *x, double *res, int32_t *iters, int32_t *conv) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(A != nullptr, LH_EINVAL, "pcg: null operator");
+        LH_REQUIRE(n >= 0 && max_iter >= 0, LH_EINVAL, "pcg: negative size or iteration count");
+        int it = 0, cv = 0;
+        try {
+            pcg(ctx->c, resolve_op(A), resolve_op(Minv), b, n, tol, max_iter, x, res, &it, &cv);
+        } catch (...) {
+            *iters = it;
+            *conv = cv;
+            throw;
+        }
+        *iters = it;
+        *conv = cv;
+    });
+}
+
+int lh_gmres_restarted(lh_ctx *ctx, const lh_operator *A, const lh_operator *Minv, const double *b,
+                       int64_t n, double tol, int32_t restart, int32_t max_iter, double *x,
+                       double *res, int32_t *iters, int32_t *conv) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(A != nullptr, LH_EINVAL, "gmres: null operator");
+        LH_REQUIRE(n >= 0 && max_iter >= 0, LH_EINVAL, "gmres: negative size or iteration count");
+        int it = 0, cv = 0;
+        gmres(ctx->c, resolve_op(A), resolve_op(Minv), b, n, tol, restart, max_iter, x, res, &it, &cv);
+        *iters = it;
+        *conv = cv;
+    });
+}
+
+int lh_dense_gemv(lh_ctx *ctx, const double *a, int64_t lda, int64_t m, int64_t n, const double *x,
+                  double *y) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(m >= 0 && n >= 0 && lda >= n, LH_EINVAL, "dense_gemv: bad shape");
+        dense_gemv(ctx->c, a, lda, m, n, x, y);
+    });
 }
 
 int lh_cn_symbol(lh_ctx *ctx, const lh_measure *nu, const lh_cn_params *p, double *tA, double *tP,

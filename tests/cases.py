@@ -44,3 +44,24 @@ def make_system(name, g=None):
 
 def struct_from_golden(arr):
     return arr.copy()
+
+
+def krylov_operators(tag):
+    """Dense operator and grid of a tests/golden/krylov.npz case (oracle restatement of
+    make_golden_krylov.py's operators: the cfg1 fractional Laplacian, and the cfg2-style
+    convection-diffusion operator and its CN matrix)."""
+    from oracle import levyh_oracle as O
+
+    if tag.startswith("poisson") or tag == "pcg_hlu":
+        n = int(tag[7:]) if tag.startswith("poisson") else 512
+        s, a, b, c = 0.5, 0.0, 0.0, 0.0
+    else:
+        n, s, a, b, c = 512, 0.25, 0.5, 1.0, -1.0
+    h = 1.0 / n
+    N = 2 * n - 1
+    tA, _ = O.symbol_A(O.nu_power(s), h, N, 2.0, 0.2, O.tail_power(s, 2.0), a, b, c)
+    A = O.toeplitz_dense(tA)
+    x = h * np.arange(-n + 1, n)
+    if tag == "gmres_r5":
+        A = np.eye(N) + 0.5 * h * A
+    return A, x
