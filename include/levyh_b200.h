@@ -139,6 +139,17 @@ int lh_hmat_layout(const lh_hmat *h, int64_t *recs_host, int64_t *sizes_host);
 int lh_hmat_export_arena(lh_ctx *ctx, const lh_hmat *h, double *arena_host, int32_t *ranks_host,
                          int32_t *perm_host);
 
+/* Checkpoints: one self-contained file with both cluster trees (and
+ * their points), the block tree, the storage layout and the device arrays (arena, ranks,
+ * leaf pivots, leaf inverses) of an H-matrix or an H-LU factor; eps2 is stored as metadata.
+ * A loaded matrix is bit-identical to the saved one.  LH_EINVAL on a foreign, truncated or
+ * corrupt file.  lh_hmat_load returns new tree handles (destroy with lh_tree_destroy). */
+int lh_hmat_save(lh_ctx *ctx, const lh_hmat *h, double eps2, const char *path);
+int lh_hmat_load(lh_ctx *ctx, const char *path, lh_tree **row_tree, lh_tree **col_tree,
+                 lh_hmat **out, int32_t *factored, double *eps2);
+/* The tree's input points (original order, n x dim row-major; NULL = query); returns dim. */
+int lh_tree_points(const lh_tree *t, double *pts_host);
+
 /* ---- H-arithmetic ------------------------------------------------------ */
 /* hops.py:65-70 matvec / :73-85 mul_dense:  Y = H X, X is ncols x nrhs (col-major, ldx) */
 int lh_hmat_matvec(lh_ctx *ctx, const lh_hmat *h, const double *x_dev, int64_t ldx, double *y_dev,

@@ -20,6 +20,7 @@ from .hops import (SOLVE_METHODS, HFactorization, hlu, lowrank_add_recompress, m
                    mul_dense, solve, trisolve_lower, trisolve_upper_right)
 from .levy import (CNSystem, FracCNSystem, UniformGrid1D, assemble_cn_1d, gaussian_measure,  # noqa: F401
                    run_cn, step_cn)
+from .checkpoint import load_hmatrix, save_hmatrix  # noqa: F401
 from .solvers import IterationLog, gmres_restarted, operator, pcg  # noqa: F401
 
 __version__ = "0.1.0"

@@ -91,6 +91,9 @@ SIGNATURES = [
     ("lh_pcg", C.c_int, [P, P, P, P, I64, D, I32, P, P, P, P]),
     ("lh_gmres_restarted", C.c_int, [P, P, P, P, I64, D, I32, I32, P, P, P, P]),
     ("lh_dense_gemv", C.c_int, [P, P, I64, I64, I64, P, P]),
+    ("lh_hmat_save", C.c_int, [P, P, D, C.c_char_p]),
+    ("lh_hmat_load", C.c_int, [P, C.c_char_p, C.POINTER(P), C.POINTER(P), C.POINTER(P), P, P]),
+    ("lh_tree_points", C.c_int, [P, P]),
     ("lh_cn_symbol", C.c_int, [P, C.POINTER(MeasureC), C.POINTER(CNParamsC), P, P, P, P]),
 ]
 

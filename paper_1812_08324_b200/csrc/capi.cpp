@@ -62,6 +62,9 @@ void pcg(Ctx &ctx, const KOp &A, const KOp &M, const double *b, i64 n, double to
 void gmres(Ctx &ctx, const KOp &A, const KOp &M, const double *b, i64 n, double tol, int restart,
            int max_iter, double *x, double *res, int *iters, int *conv);
 void dense_gemv(Ctx &ctx, const double *A, i64 lda, i64 m, i64 n, const double *x, double *y);
+void save_hmat(Ctx &ctx, HMat &H, double eps2, const char *path);
+void load_hmat(Ctx &ctx, const char *path, HMat &H, std::shared_ptr<Tree> &rt,
+               std::shared_ptr<Tree> &ct, double &eps2);
 
 double *DevBuf::ensure(i64 n) {
     if (n > cap) {
@@ -617,6 +620,47 @@ int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const doub
 int lh_hlu_stats(const lh_hmat *f, double *out) {
     for (int k = 0; k < 5; ++k) out[k] = f->h.lu_stats[k];
     return LH_OK;
+}
+
+int lh_hmat_save(lh_ctx *ctx, const lh_hmat *h, double eps2, const char *path) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(h != nullptr && path != nullptr, LH_EINVAL, "save: null argument");
+        save_hmat(ctx->c, const_cast<HMat &>(h->h), eps2, path);
+    });
+}
+
+int lh_hmat_load(lh_ctx *ctx, const char *path, lh_tree **rt_out, lh_tree **ct_out, lh_hmat **out,
+                 int32_t *factored, double *eps2) {
+    lh_hmat *o = nullptr;
+    lh_tree *r = nullptr, *c = nullptr;
+    int rc = guard(ctx, [&] {
+        LH_REQUIRE(path != nullptr, LH_EINVAL, "load: null path");
+        o = new lh_hmat();
+        r = new lh_tree();
+        c = new lh_tree();
+        double e = 0;
+        load_hmat(ctx->c, path, o->h, r->t, c->t, e);
+        *factored = o->h.factored ? 1 : 0;
+        *eps2 = e;
+        start_background_plans(o->h);  // no-op for a factor
+    });
+    if (rc != LH_OK) {
+        delete o;
+        delete r;
+        delete c;
+        o = nullptr;
+        r = c = nullptr;
+    }
+    *out = o;
+    *rt_out = r;
+    *ct_out = c;
+    return rc;
+}
+
+int lh_tree_points(const lh_tree *t, double *pts_host) {
+    const Tree &T = *t->t;
+    if (pts_host) std::memcpy(pts_host, T.pts.data(), sizeof(double) * T.pts.size());
+    return T.dim;
 }
 
 static KOp resolve_op(const lh_operator *op) {

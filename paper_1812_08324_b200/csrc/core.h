@@ -54,6 +54,7 @@ struct Tree {
     std::vector<Cluster> nodes;  // nodes[0] is the root
     std::vector<i64> order;      // order[i_tree] = i_orig
     std::vector<int32_t> leaves; // leaf cluster ids in tree order
+    std::vector<double> pts;     // the input points, original order, n x dim row-major
 };
 
 Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size);

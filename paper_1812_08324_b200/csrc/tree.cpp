@@ -115,6 +115,7 @@ Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size) {
     T->dim = dim;
     T->n = n;
     T->leaf_size = leaf_size;
+    T->pts.assign(pts, pts + n * dim);
     T->order.assign(n, 0);
     std::vector<i64> idx(n);
     std::iota(idx.begin(), idx.end(), (i64)0);
