@@ -196,7 +196,8 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
     if method == "propagator":
         ps = F.propagator_stats()
         times.update(propagator_s=t_prep, propagator_plan_s=float(ps[1]),
-                     propagator_exec_s=float(ps[3]), propagator_tasks=int(ps[0]))
+                     propagator_exec_s=float(ps[3]), propagator_tasks=int(ps[0]),
+                     propagator_nearfield_lowrank_leaves=int(ps[4]))
     elif method == "inverse":
         times.update(inverse_factors_s=t_prep)
     free_b, total_b = torch.cuda.mem_get_info()

@@ -970,3 +970,118 @@ void derive(Ctx &ctx, const HMat &S, HMat &D, const double *t, double scale, int
 }
 
 }  // namespace lh
+
+// ===========================================================================
+// Near-field compression of a computed H-matrix (the propagator Z = (LU)^-1):
+// every dense leaf off the diagonal whose numerical rank at `eps` (Frobenius tail relative to
+// the block, the hops.py:124-131 rule) is small is converted to a low-rank leaf in place
+// (U then V inside the leaf's own m x n storage).  The block structure of the reference
+// partition is kept; only the leaf's representation changes.  One CTA per block: ACA with
+// partial pivoting on the stored entries, CGS2 QR of both factors, Jacobi SVD, truncation.
+// ===========================================================================
+namespace lh {
+namespace {
+
+struct NfJob {
+    i64 m, n, doff, wu, wv;
+};
+
+__global__ void __launch_bounds__(NT) nf_compress_kernel(const NfJob *jobs, int njobs, int *counter,
+                                                         double *work, double *arena, int *ranks_out,
+                                                         int KA, double aca_tol, double eps) {
+    extern __shared__ double4 smem_raw[];
+    AcaSmem &S = *reinterpret_cast<AcaSmem *>(smem_raw);
+    __shared__ int s_job;
+    while (true) {
+        if (threadIdx.x == 0) s_job = atomicAdd(counter, 1);
+        __syncthreads();
+        const int jb = s_job;
+        __syncthreads();
+        if (jb >= njobs) break;
+        const NfJob J = jobs[jb];
+        double *U = work + J.wu, *V = work + J.wv;
+        double *D = arena + J.doff;
+        DenseSrc src{D, J.m, 0};
+        int conv = 0;
+        const int K = aca_block(src, 0, 0, J.m, J.n, U, V, KA, aca_tol, S, conv);
+        // keep only conversions that at least halve the storage
+        const int rmax = (int)min((i64)KC_MAX, (J.m * J.n) / (2 * (J.m + J.n)));
+        int r = conv ? dev::recompress(U, J.m, J.m, V, J.n, J.n, K, 1, eps, U, J.m, V, J.n, rmax, S.R)
+                     : rmax + 1;
+        const bool ok = conv && r <= rmax;
+        if (ok) {  // every ACA read of D is done (recompress ends with a barrier)
+            for (i64 e = threadIdx.x; e < J.m * r; e += NT) D[e] = U[e];
+            for (i64 e = threadIdx.x; e < J.n * r; e += NT) D[J.m * r + e] = V[e];
+        }
+        if (threadIdx.x == 0) ranks_out[jb] = ok ? r : -1;
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+// Returns the number of converted leaves.  Updates the node table and the rank slots; any
+// matvec plan of H must be rebuilt afterwards.
+i64 compress_near_field(Ctx &ctx, HMat &H, double eps) {
+    std::vector<int32_t> cand;
+    for (int32_t b : H.leafblocks) {
+        const Node &nd = H.nodes[b];
+        const bool off_diag = nd.r0 + nd.m <= nd.c0 || nd.c0 + nd.n <= nd.r0;
+        if (nd.kind == K_DENSE && off_diag && nd.vpar < 0 && std::min(nd.m, nd.n) >= 16)
+            cand.push_back(b);
+    }
+    if (cand.empty()) return 0;
+    const int KA = KA_MAX;
+    std::vector<NfJob> jobs;
+    i64 w = 0;
+    for (int32_t b : cand) {
+        const Node &nd = H.nodes[b];
+        jobs.push_back({nd.m, nd.n, nd.doff, w, w + nd.m * KA});
+        w += (nd.m + nd.n) * KA;
+    }
+    double *work = dalloc<double>(w);
+    NfJob *djobs = dupload(jobs, ctx.stream);
+    int *dcnt = dalloc<int>(1 + (i64)jobs.size());
+    int *dranks = dcnt + 1;
+    LH_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int), ctx.stream));
+    const size_t smem = sizeof(AcaSmem);
+    set_smem((const void *)nf_compress_kernel, smem);
+    const int grid = (int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 2);
+    nf_compress_kernel<<<grid, NT, smem, ctx.stream>>>(djobs, (int)jobs.size(), dcnt, work, H.d_arena,
+                                                       dranks, KA, 0.1 * eps, eps);
+    LH_CUDA(cudaGetLastError());
+    std::vector<int> r(jobs.size());
+    LH_CUDA(cudaMemcpyAsync(r.data(), dranks, sizeof(int) * r.size(), cudaMemcpyDeviceToHost, ctx.stream));
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaFree(work);
+    cudaFree(djobs);
+    cudaFree(dcnt);
+    // new rank slots for the converted leaves
+    H.sync_ranks(ctx.stream);
+    std::vector<int32_t> ranks = H.h_ranks;
+    i64 nconv = 0;
+    for (size_t k = 0; k < cand.size(); ++k) {
+        if (r[k] < 0) continue;
+        Node &nd = H.nodes[cand[k]];
+        nd.kind = K_LR;
+        nd.kcap = std::max(r[k], 1);
+        nd.uoff = nd.doff;
+        nd.voff = nd.doff + nd.m * r[k];
+        nd.rslot = (int32_t)ranks.size();
+        nd.doff = -1;
+        for (int q = 0; q < 4; ++q) nd.kid[q] = -1;
+        ranks.push_back(r[k]);
+        ++nconv;
+    }
+    if (nconv) {
+        int32_t *nr = dupload(ranks, ctx.stream);
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(H.d_ranks);
+        H.d_ranks = nr;
+        H.nslots = (int32_t)ranks.size();
+        H.h_ranks = ranks;
+    }
+    return nconv;
+}
+
+}  // namespace lh

@@ -1890,6 +1890,8 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
     }
 }
 
+i64 compress_near_field(Ctx &ctx, HMat &H, double eps);
+
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.factored, LH_EINVAL, "prepare_propagator needs an H-LU factorization");
     SolvePlans &S = plans_of(F);
@@ -1935,10 +1937,19 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     Z->lu_stats[3] = sec(t0, t1);
     P.reset();
     auto t2 = now();
+    // near-field compression of Z: its off-diagonal dense leaves are
+    // numerically low-rank, which cuts the bytes every CN step streams
+    if (!getenv("LEVYH_NO_NF_COMPRESS")) {
+        double nf_eps = 1e-2 * std::min(eps2, 1e-10);
+        if (const char *e = getenv("LEVYH_NF_EPS")) nf_eps = atof(e);
+        Z->lu_stats[4] = (double)compress_near_field(ctx, *Z, nf_eps);
+    }
+    auto t3 = now();
     S.mvZ = build_mv_plan(*Z, Z->leafblocks, ctx.stream);
     if (getenv("LEVYH_PLAN_VERBOSE"))
         fprintf(stderr, "[levyh] propagator: alloc+upload %.3f s, exec %.3f s, free plan %.3f s, "
-                        "matvec plan %.3f s\n", sec(ta, t0), sec(t0, t1), sec(t1, t2), sec(t2, now()));
+                        "near-field compression %.3f s (%.0f leaves), matvec plan %.3f s\n", sec(ta, t0),
+                sec(t0, t1), sec(t1, t2), sec(t2, t3), Z->lu_stats[4], sec(t3, now()));
     S.Z = Z;
     if (!S.tmp) {
         S.tmp_len = F.nrows;
@@ -1951,7 +1962,7 @@ int step_graph_kernels(HMat &F) { return plans_of(F).g_kernels; }
 void propagator_stats(HMat &F, double *out) {
     SolvePlans &S = plans_of(F);
     LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
-    for (int k = 0; k < 4; ++k) out[k] = S.Z->lu_stats[k];
+    for (int k = 0; k < 5; ++k) out[k] = S.Z->lu_stats[k];
 }
 
 static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {

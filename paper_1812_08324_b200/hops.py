@@ -99,8 +99,9 @@ class HFactorization:
             self.propagator_ready = True
 
     def propagator_stats(self):
-        """(task count, planning s, temp bytes, executor s) of the propagator build."""
-        out = np.zeros(4)
+        """(task count, planning s, temp bytes, executor s, near-field leaves compressed) of
+        the propagator build."""
+        out = np.zeros(5)
         _lib.check(_lib.lib().lh_propagator_stats(self.h.handle, _lib.host_ptr(out)))
         return out
 
