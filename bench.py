@@ -293,23 +293,25 @@ def run_b200(args, world, rank, local):
     value = world * args.steps / (ms / 1000.0)
 
     # ---- end to end through the C ABI with HOST buffers (pinned), one step per call
+    # (lh_cn_step_host: u in pinned host memory; every call copies u in and the new u out,
+    # overlapped piece by piece with the step's kernels, and returns when u is on the host)
     u_host = torch.from_numpy(u0.copy()).pin_memory()
-    u_dev = torch.empty_like(u)
     e2e_steps = max(1, min(args.steps, 50))
-    steps_e2e_dev = u_dev
-    # warm (graph for this vector)
-    u_dev.copy_(u_host, non_blocking=True)
-    steps(1, steps_e2e_dev)
+
+    def host_step():
+        P._lib.check(L.lh_cn_step_host(ctx.h, Hm.handle, F.h.handle, u_host.data_ptr(),
+                                       u_host.data_ptr(), mcode), ctx.h)
+
+    host_step()  # warm (graph for this buffer)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        u_dev.copy_(u_host, non_blocking=True)
-        steps(1, steps_e2e_dev)
-        u_host.copy_(u_dev, non_blocking=True)
-        torch.cuda.synchronize()
+        host_step()
     t_e2e = time.perf_counter() - t0
     e2e = {"value": world * e2e_steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * N,
-           "d2h_bytes_per_step": 8 * N, "path": "lh_cn_steps (C ABI) with pinned host u per step"}
+           "d2h_bytes_per_step": 8 * N,
+           "path": "lh_cn_step_host (C ABI, levy.step_cn) with u in pinned host memory, one call per "
+                   "step (copies in and out inside the call)"}
 
     # ---- per-kernel roofline (CUDA events on the library stream)
     prof = np.zeros(16)

@@ -193,6 +193,13 @@ int32_t lh_step_graph_kernels(lh_hmat *factor);
 int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev, int64_t ldu,
                 int32_t nrhs, int32_t nsteps, int32_t method);
 
+/* levy.py:295-306 step_cn on HOST vectors: u_out = one CN step of u_in (u_out may equal
+ * u_in; both length n).  With pinned buffers and method 2 on the CN pair, u arrives and the
+ * new u leaves in pieces overlapped with the step's kernels (one cached graph per buffer
+ * pair); otherwise copy in, step, copy out.  Returns when u_out is written. */
+int lh_cn_step_host(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, const double *u_in_host,
+                    double *u_out_host, int32_t method);
+
 /* Measurement: CUDA-event timing of each kernel of one CN step, averaged over `iters`
  * steps applied to u_dev in place.  method 1: out[0..5] mean ms of vtx(H-), seg(H-),
  * vtx(L^-1), seg(L^-1), vtx(U^-1), seg(U^-1); out[6..11] their algorithmic bytes;

@@ -79,6 +79,7 @@ SIGNATURES = [
     ("lh_trisolve_dense", C.c_int, [P, P, I32, I32, P, I64, I32]),
     ("lh_lowrank_add_recompress", C.c_int, [P, I64, I64, P, P, I32, P, P, I32, D, P, P, P]),
     ("lh_cn_steps", C.c_int, [P, P, P, P, I64, I32, I32, I32]),
+    ("lh_cn_step_host", C.c_int, [P, P, P, P, P, I32]),
     ("lh_step_profile", C.c_int, [P, P, P, P, I32, I32, P]),
     ("lh_hlu_stats", C.c_int, [P, P]),
     ("lh_debug_task_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),

@@ -32,6 +32,7 @@ void hlu(Ctx &ctx, HMat &H, double eps2);
 void solve(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs, int method);
 void prepare_inverse(Ctx &ctx, HMat &F, double eps2);
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method);
+void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out, int method);
 void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method, double *out);
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2);
 void propagator_stats(HMat &F, double *out);
@@ -598,6 +599,14 @@ int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int64_t l
                 int32_t nsteps, int32_t method) {
     return guard(ctx, [&] {
         cn_steps(ctx->c, const_cast<HMat &>(hm->h), f->h, u, ldu, nrhs, nsteps, method);
+    });
+}
+
+int lh_cn_step_host(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, const double *u_in_host,
+                    double *u_out_host, int32_t method) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(u_in_host && u_out_host, LH_EINVAL, "cn_step_host: null vector");
+        cn_step_host(ctx->c, const_cast<HMat &>(hm->h), f->h, u_in_host, u_out_host, method);
     });
 }
 

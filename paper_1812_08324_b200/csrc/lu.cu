@@ -1766,8 +1766,21 @@ struct SolvePlans {
     cudaGraphExec_t graph = nullptr;  // cached CN step
     const double *g_u = nullptr, *g_y = nullptr;
     const HMat *g_hm = nullptr;
+    // host-buffer CN step (cn_step_host): pipelined graph keyed by the host pointers
+    cudaGraphExec_t hgraph = nullptr;
+    const double *hg_in = nullptr;
+    double *hg_out = nullptr;
+    const HMat *hg_hm = nullptr;
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> hev;
+    double *hx = nullptr, *hy = nullptr;  // device x and y of the host step
     ~SolvePlans() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (hgraph) cudaGraphExecDestroy(hgraph);
+        for (cudaEvent_t e : hev) cudaEventDestroy(e);
+        if (side) cudaStreamDestroy(side);
+        if (hx) cudaFree(hx);
+        if (hy) cudaFree(hy);
         if (tmp) cudaFree(tmp);
     }
 };
@@ -2401,6 +2414,73 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
             solve_substitution(ctx, F, uq, Hm.nrows, 1);
         }
     }
+}
+
+static bool is_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// One CN step with HOST buffers (the reference-facing call: levy.step_cn, levy.py:295-306,
+// on numpy vectors).  Method 2 with the CN pair (u <- 2 Z u - u) runs as one captured graph
+// in which u arrives and the new u leaves in pieces overlapped with the V^T u and segment
+// kernels (mv_run_host); any other case copies in, steps on the device and copies out.
+void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out, int method) {
+    LH_REQUIRE(F.factored, LH_EINVAL, "cn_steps needs an H-LU factorization of A+");
+    LH_REQUIRE(Hm.nrows == F.nrows, LH_EINVAL, "operator sizes differ");
+    const i64 n = Hm.nrows;
+    SolvePlans &S = plans_of(F);
+    if (!S.hx) {
+        S.hx = dalloc<double>(n);
+        S.hy = dalloc<double>(n);
+    }
+    bool pipelined = method == 2 && S.Z && is_pinned(u_in) && is_pinned(u_out) &&
+                     !getenv("LEVYH_NO_HOST_PIPE");
+    if (pipelined) {
+        MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
+        pipelined = cn_pair_ok(ctx, S, Hm, Pm) && S.mvZ->npiece > 0 && S.mvZ->nbatch > 0;
+    }
+    if (!pipelined) {
+        LH_CUDA(cudaMemcpyAsync(S.hx, u_in, sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
+        cn_steps(ctx, Hm, F, S.hx, n, 1, 1, method);
+        LH_CUDA(cudaMemcpyAsync(u_out, S.hx, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        return;
+    }
+    const MvPlan &P = *S.mvZ;
+    if (!(S.hgraph && S.hg_in == u_in && S.hg_out == u_out && S.hg_hm == &Hm)) {
+        if (S.hgraph) {
+            cudaGraphExecDestroy(S.hgraph);
+            S.hgraph = nullptr;
+        }
+        if (!S.side) LH_CUDA(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
+        while ((int)S.hev.size() < 2 * P.npiece + 2) {
+            cudaEvent_t e;
+            LH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            S.hev.push_back(e);
+        }
+        cudaGraph_t g;
+        LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            mv_run_host(P, u_in, S.hx, S.hy, u_out, 2.0, -1.0, true, ctx.stream, S.side, S.hev.data(),
+                        ctx.num_sms);
+        } catch (...) {
+            cudaStreamEndCapture(ctx.stream, &g);
+            throw;
+        }
+        LH_CUDA(cudaStreamEndCapture(ctx.stream, &g));
+        LH_CUDA(cudaGraphInstantiate(&S.hgraph, g, 0));
+        cudaGraphDestroy(g);
+        S.hg_in = u_in;
+        S.hg_out = u_out;
+        S.hg_hm = &Hm;
+    }
+    LH_CUDA(cudaGraphLaunch(S.hgraph, ctx.stream));
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
 }  // namespace lh

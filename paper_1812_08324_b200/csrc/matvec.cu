@@ -708,6 +708,62 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
     P->part = dalloc<double>((i64)std::max(npart, 1) * KC_MAX);
     P->batches = dupload(batches, s);
     P->cta_seg = dupload(cta_seg, s);
+    // host-buffer pipelining: piece-ordered chunk copies and per-piece segment ranges
+    {
+        int NP = 4;
+        if (const char *e = getenv("LEVYH_PIPE_PIECES")) NP = std::max(1, atoi(e));
+        NP = (int)std::max<i64>(1, std::min<i64>(NP, nseg));
+        P->npiece = NP;
+        P->xcut.resize(NP + 1);
+        for (int p = 0; p <= NP; ++p) P->xcut[p] = std::min<i64>(H.ncols, ((H.ncols * p / NP) + 1) & ~i64(1));
+        P->xcut[0] = 0;
+        P->xcut[NP] = H.ncols;
+        auto piece_of = [&](const VChunk &c) {
+            int p = (int)(std::upper_bound(P->xcut.begin(), P->xcut.end(), c.xc0 + c.len - 1) -
+                          P->xcut.begin()) - 1;
+            return std::min(std::max(p, 0), NP - 1);
+        };
+        for (int k = 0; k < 2; ++k) {
+            const std::vector<VChunk> &cv = k ? chunks16 : chunks;
+            std::vector<VChunk> cp(cv.begin(), cv.end());
+            std::stable_sort(cp.begin(), cp.end(), [&](const VChunk &a, const VChunk &b) {
+                return piece_of(a) < piece_of(b);
+            });  // within a piece: still largest first
+            std::vector<int32_t> &off = k ? P->pch16 : P->pch;
+            off.assign(NP + 1, 0);
+            for (const VChunk &c : cp) off[piece_of(c) + 1]++;
+            for (int p = 0; p < NP; ++p) off[p + 1] += off[p];
+            (k ? P->chunks16_pp : P->chunks_pp) = dupload(cp, s);
+        }
+        // segment pieces (segments are in row order)
+        std::vector<int> ps(NP + 1, nseg);
+        ps[0] = 0;
+        for (int p = 1; p < NP; ++p) {
+            const i64 target = H.nrows * p / NP;
+            int sg = ps[p - 1];
+            while (sg < nseg && segs[sg].y0 < target) ++sg;
+            ps[p] = sg;
+        }
+        P->ycut.resize(NP + 1);
+        for (int p = 0; p <= NP; ++p) P->ycut[p] = ps[p] < nseg ? segs[ps[p]].y0 : H.nrows;
+        std::vector<int32_t> csp((size_t)NP * (G + 1));
+        for (int p = 0; p < NP; ++p) {
+            int32_t *cs = csp.data() + (size_t)p * (G + 1);
+            i64 total = 0;
+            for (int sg = ps[p]; sg < ps[p + 1]; ++sg) total += seg_bytes[sg];
+            for (int c = 0; c <= G; ++c) cs[c] = ps[p + 1];
+            cs[0] = ps[p];
+            i64 accb = 0;
+            int c = 1;
+            for (int sg = ps[p]; sg < ps[p + 1] && c < G; ++sg) {
+                accb += seg_bytes[sg];
+                while (c < G && accb * G >= total * c) cs[c++] = sg + 1;
+            }
+        }
+        P->cta_seg_pp = dupload(csp, s);
+        for (int sg = 1; sg < nseg; ++sg)
+            LH_REQUIRE(segs[sg].y0 > segs[sg - 1].y0, LH_EINTERNAL, "segments out of row order");
+    }
     P->n_dpieces = (i64)dall.size();
     P->n_lpieces = (i64)lall.size();
     P->colmap = dupload(colmap, s);
@@ -742,6 +798,9 @@ MvPlan::~MvPlan() {
     cudaFree(tvec);
     cudaFree(batches);
     cudaFree(cta_seg);
+    cudaFree(chunks_pp);
+    cudaFree(chunks16_pp);
+    cudaFree(cta_seg_pp);
 }
 
 // phase 1 (V^T x per chunk) + t_b reduction of multi-chunk blocks
@@ -806,6 +865,62 @@ void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double a
             cudaStream_t s, int num_sms, const double *z) {
     mv_vtx_launch(P, H, x, num_sms, s);
     mv_seg_launch(P, H, x, y, alpha, beta, s, num_sms, z);
+    LH_CUDA(cudaGetLastError());
+}
+
+void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y_dev,
+                 double *y_host, double alpha, double beta, bool z_is_x, cudaStream_t s,
+                 cudaStream_t side, cudaEvent_t *ev, int num_sms) {
+    const int NP = P.npiece;
+    LH_REQUIRE(NP >= 1 && P.nbatch > 0, LH_EINTERNAL, "matvec plan without pipelining data");
+    static bool attr = false;
+    if (!attr) {
+        LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
+        attr = true;
+    }
+    cudaEvent_t fork = ev[2 * NP], join = ev[2 * NP + 1];
+    LH_CUDA(cudaEventRecord(fork, s));
+    LH_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    for (int p = 0; p < NP; ++p) {  // x pieces in order on the copy stream
+        const i64 a = P.xcut[p], b = P.xcut[p + 1];
+        LH_CUDA(cudaMemcpyAsync(x_dev + a, x_host + a, sizeof(double) * (b - a), cudaMemcpyHostToDevice,
+                                side));
+        LH_CUDA(cudaEventRecord(ev[p], side));
+    }
+    for (int p = 0; p < NP; ++p) {  // V^T x of the chunks whose x rows have arrived
+        LH_CUDA(cudaStreamWaitEvent(s, ev[p], 0));
+        const int n8 = P.pch[p + 1] - P.pch[p], n16 = P.pch16[p + 1] - P.pch16[p];
+        if (n8 > 0) {
+            int g = std::max(1, std::min(vtx_grid<8>(num_sms), (n8 + dev::NW - 1) / dev::NW));
+            vtx_kernel<8><<<g, NT, 0, s>>>(P.chunks_pp + P.pch[p], n8, P.pbuf, x_dev, P.part, P.tvec);
+        }
+        if (n16 > 0) {
+            int g = std::max(1, std::min(vtx_grid<16>(num_sms), (n16 + dev::NW - 1) / dev::NW));
+            vtx_kernel<16><<<g, NT, 0, s>>>(P.chunks16_pp + P.pch16[p], n16, P.pbuf, x_dev, P.part,
+                                            P.tvec);
+        }
+    }
+    if (P.ntj > 0) {
+        int g = std::max(1, std::min(148 * 8, (P.ntj + dev::NW - 1) / dev::NW));
+        treduce_kernel<<<g, NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
+    }
+    const i64 n = P.tcol_len + P.nx + 2;
+    int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
+    tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x_dev, P.nx, P.xpad);
+    const double *z = z_is_x ? x_dev : y_dev;
+    for (int p = 0; p < NP; ++p) {  // y pieces leave as soon as their segments are done
+        seg_tma_kernel<<<P.tma_grid, TMA_THREADS, TMA_SMEM, s>>>(
+            P.segs, P.cta_seg_pp + (size_t)p * (P.tma_grid + 1), P.batches, P.pbuf, P.tcol, P.xpad,
+            y_dev, alpha, beta, z);
+        LH_CUDA(cudaEventRecord(ev[NP + p], s));
+        LH_CUDA(cudaStreamWaitEvent(side, ev[NP + p], 0));
+        const i64 a = P.ycut[p], b = P.ycut[p + 1];
+        LH_CUDA(cudaMemcpyAsync(y_host + a, y_dev + a, sizeof(double) * (b - a), cudaMemcpyDeviceToHost,
+                                side));
+    }
+    LH_CUDA(cudaEventRecord(join, side));
+    LH_CUDA(cudaStreamWaitEvent(s, join, 0));
     LH_CUDA(cudaGetLastError());
 }
 

@@ -79,6 +79,14 @@ struct MvPlan {
     SBatch *batches = nullptr;
     int32_t *cta_seg = nullptr;  // TMA kernel: segments [cta_seg[c], cta_seg[c+1]) per CTA
     i64 n_dpieces = 0, n_lpieces = 0;
+    // host-buffer pipelining (mv_run_host): x arrives and y leaves in npiece column / row
+    // pieces; the V chunks are also stored piece by piece (a chunk belongs to the piece of
+    // its last x row), the segments split at ycut with their own byte-balanced CTA ranges
+    int npiece = 0;
+    std::vector<i64> xcut, ycut;          // npiece + 1 each
+    std::vector<int32_t> pch, pch16;      // chunk ranges per piece in chunks_pp / chunks16_pp
+    VChunk *chunks_pp = nullptr, *chunks16_pp = nullptr;
+    int32_t *cta_seg_pp = nullptr;        // npiece x (tma_grid + 1)
     ~MvPlan();
 };
 
@@ -91,6 +99,12 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms,
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
                    double beta, cudaStream_t s, int num_sms, const double *z = nullptr);
 void matvec(Ctx &ctx, HMat &H, const double *x, i64 ldx, double *y, i64 ldy, int nrhs);
+// y = alpha H x + beta z with x arriving from pinned host memory and y leaving to it, the
+// transfers overlapped with the kernels piece by piece (copies on `side`, kernels on `s`;
+// ev: >= 2 npiece + 2 events).  z = x_dev (z_is_x) or y_dev.  Capturable.
+void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y_dev,
+                 double *y_host, double alpha, double beta, bool z_is_x, cudaStream_t s,
+                 cudaStream_t side, cudaEvent_t *ev, int num_sms);
 
 // multi-RHS (matmat.cu); row-major X, Y, Z with ldk = mm_pad(K)
 i64 mm_pad(int k);

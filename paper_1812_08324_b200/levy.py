@@ -279,13 +279,43 @@ class FracCNSystem:
 
 
 def step_cn(sys, u_n, F=None, method=None):
-    """levy.py:295-306: solve A+ u = A- u_n."""
+    """levy.py:295-306: solve A+ u = A- u_n, one C-ABI call (lh_cn_step_host) on host vectors.
+
+    A pinned CPU torch tensor (tree order = grid order for these 1D grids) takes the
+    pipelined path: u streams in and the new u streams out in pieces overlapped with the
+    step's kernels.  numpy in -> numpy out."""
+    import torch
+
+    from . import _lib
+
     F = F if F is not None else sys.factor
     if F is None or sys.h_minus is None:
         raise ValueError("call prepare() before stepping")
+    m = SOLVE_METHODS[method or getattr(sys, "method", "substitution")]
+    if m == 2:
+        F.prepare_propagator()
+    elif m == 1:
+        F.prepare_inverse()
     perm = sys.tree.perm
-    rhs = matvec(sys.h_minus, perm.to_tree(u_n))
-    return perm.from_tree(solve(F, rhs, method or getattr(sys, "method", "substitution")))
+    ctx = sys.h_minus.ctx
+    if isinstance(u_n, torch.Tensor):
+        if u_n.is_cuda or u_n.dtype != torch.float64 or u_n.shape != (sys.N,):
+            raise ValueError("step_cn takes a host float64 vector of length N")
+        if not np.array_equal(perm.inverse, np.arange(sys.N)):
+            raise ValueError("torch host vectors need the identity tree permutation")
+        src = u_n.contiguous()
+        out = torch.empty_like(src, pin_memory=src.is_pinned())
+        _lib.check(_lib.lib().lh_cn_step_host(ctx.h, sys.h_minus.handle, F.h.handle, src.data_ptr(),
+                                              out.data_ptr(), m), ctx.h)
+        return out
+    u_n = np.asarray(u_n, dtype=float)
+    if u_n.shape != (sys.N,):
+        raise ValueError(f"vector shape {u_n.shape} does not match N={sys.N}")
+    src = np.ascontiguousarray(perm.to_tree(u_n))
+    out = np.empty_like(src)
+    _lib.check(_lib.lib().lh_cn_step_host(ctx.h, sys.h_minus.handle, F.h.handle, _lib.host_ptr(src),
+                                          _lib.host_ptr(out), m), ctx.h)
+    return perm.from_tree(out)
 
 
 def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method="inverse", mode="hmatrix"):
