@@ -197,7 +197,8 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
         ps = F.propagator_stats()
         times.update(propagator_s=t_prep, propagator_plan_s=float(ps[1]),
                      propagator_exec_s=float(ps[3]), propagator_tasks=int(ps[0]),
-                     propagator_nearfield_lowrank_leaves=int(ps[4]))
+                     propagator_nearfield_lowrank_leaves=int(ps[4]),
+                     propagator_coarsening_merges=int(ps[5]))
     elif method == "inverse":
         times.update(inverse_factors_s=t_prep)
     free_b, total_b = torch.cuda.mem_get_info()
@@ -558,6 +559,93 @@ def run_cfg5(args, world, rank, local):
         print(json.dumps(out), flush=True)
 
 
+METRIC_G = ("reference bench system (cli.bench_point: Gaussian jumps, rank 10, leaf 64) at N=2^20: "
+            "construct / matvec / H-LU / solve seconds; CN steps/s")
+
+
+def run_gauss(args, world, rank, local):
+    """The reference's own benchmark system (cli.bench_point, cli.py:163-224):
+    gaussian_measure(5.0), a=b=c=0, UniformGrid1D(2^20), dt=0.01, HConfig(n_min=64,
+    fixed_rank=10, eps1=1e-4), eps2=1e-10.  Times the four bench kinds (construct = series
+    H-build of A+, matvec, H-LU, solve by substitution = the reference algorithm) with the
+    reference's median-of-repeats convention, plus CN steps/s (one H-matvec of Z per step)."""
+    if rank != 0:
+        return
+    import torch
+
+    import paper_1812_08324_b200 as P
+
+    n = 2 ** 20
+    rep = 3
+
+    def med(fn):
+        ts = []
+        for k in range(rep + 1):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            r = fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t)
+        return float(np.median(ts[1:])), r
+
+    s = P.assemble_cn_1d(P.gaussian_measure(5.0), 0.0, 0.0, 0.0, P.UniformGrid1D(n), 0.01)
+    cfg = P.HConfig(n_min=64, fixed_rank=10, eps1=1e-4)
+    t_con, H = med(lambda: s.hmatrix("plus", cfg))
+    stored = P.memory_report(H)["stored_scalars"]
+    x = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).cuda()
+    t_mv, _ = med(lambda: P.matvec(H, x))
+    lu_times = []
+    for k in range(rep + 1):
+        Hk = s.hmatrix("plus", cfg)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        F = P.hlu(Hk, 1e-10)
+        torch.cuda.synchronize()
+        lu_times.append(time.perf_counter() - t)
+    t_lu = float(np.median(lu_times[1:]))
+    t_sol, _ = med(lambda: P.solve(F, x, method="substitution"))
+    t0 = time.perf_counter()
+    F.prepare_propagator()
+    torch.cuda.synchronize()
+    t_prop = time.perf_counter() - t0
+    t_solz, _ = med(lambda: P.solve(F, x, method="propagator"))
+    s.h_minus, s.factor, s.method = s.hmatrix("minus", cfg), F, "propagator"
+    u = torch.from_numpy(np.exp(-50 * s.grid.points ** 2)).cuda()
+    L, ctx = P._lib.lib(), s.h_minus.ctx
+
+    def steps(k):
+        P._lib.check(L.lh_cn_steps(ctx.h, s.h_minus.handle, F.h.handle, u.data_ptr(), n, 1, int(k), 2),
+                     ctx.h)
+
+    steps(args.warmup)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lib_stream = ctx.torch_stream()
+    start.record(lib_stream)
+    steps(args.steps)
+    end.record(lib_stream)
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / args.steps
+    out = {"metric": METRIC_G, "value": round(1000.0 / ms, 3), "unit": "steps/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (the reference bench system, closed-form symbol)",
+           "config": {"workload": "cli.bench_point system: gaussian_measure(5.0), a=b=c=0, N=2^20, "
+                                  "dt=0.01, leaf 64, fixed_rank 10, eps1 1e-4, eps2 1e-10",
+                      "N": n, "repeat": rep, "warmup_repeats": 1},
+           "bench_point_seconds": {"construct": round(t_con, 4), "matvec": round(t_mv, 6),
+                                   "lu": round(t_lu, 4), "solve": round(t_sol, 6),
+                                   "solve_propagator": round(t_solz, 6),
+                                   "propagator_prepare": round(t_prop, 4)},
+           "stored_scalars": stored,
+           "reference_context": {"source": "BASELINE.md 2(a) (reference levyh bench, survey container, "
+                                           "8 vCPU; not this run) and BASELINE.md 1 (paper, Julia)",
+                                 "reference_cpu_2^20": {"matvec": 2.363, "solve": 2.033, "lu": 239.6},
+                                 "paper_julia_2^20": {"construct": 81.86, "matvec": 1.7325,
+                                                      "lu": 125.12, "solve": 1.4913}}}
+    print(json.dumps(out), flush=True)
+
+
 def run_reference(args, world, rank, local):
     """--impl reference: the reference algorithm on host cores (rank 0 only)."""
     if rank != 0:
@@ -602,7 +690,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--ref-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "cfg5", "gauss"])
     ap.add_argument("--method", default=None, choices=["propagator", "inverse", "substitution"],
                     help="per-step solve: one H-matvec of Z=(A+)^-1 (default; cfg5: substitution)")
     args = ap.parse_args()
@@ -618,6 +706,8 @@ def main():
         run_cfg4(args, world, rank, local)
     elif args.workload == "cfg5":
         run_cfg5(args, world, rank, local)
+    elif args.workload == "gauss":
+        run_gauss(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
     if world > 1:

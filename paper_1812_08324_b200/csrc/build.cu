@@ -5,6 +5,8 @@
 // Reference: fractional.py:78-86 (window), :108-127 (power density),
 // :285-301 (_window_sums_1d), :362-405 (frac_stencil_1d / Poisson assembly),
 // levy.py:169-206 (local band, A+-), hmatrix.py:294-340 (build_from_dense).
+#include <chrono>
+#include <limits>
 #include <algorithm>
 #include <cmath>
 #include <numeric>
@@ -1082,6 +1084,224 @@ i64 compress_near_field(Ctx &ctx, HMat &H, double eps) {
         H.h_ranks = ranks;
     }
     return nconv;
+}
+
+}  // namespace lh
+
+// ===========================================================================
+// Coarsening of a computed H-matrix (the propagator Z): bottom-up, a 2 x 2
+// hierarchical block off the diagonal whose four children are low-rank is replaced by one
+// low-rank block when the recompressed sum of its children (QR of the embedded U's and V's,
+// Jacobi SVD, the hops.py:124-131 Frobenius-tail rule at eps relative to the merged block)
+// needs fewer scalars than the children.  Repeats level by level while merges pay.
+// ===========================================================================
+namespace lh {
+void walk_leaves(HMat &H);
+namespace {
+
+struct MergeKid {
+    i64 uoff, voff, ro, co, m, n;
+    int32_t r, pad;
+};
+struct MergeJob {
+    i64 M, N, wu, wv;
+    MergeKid kid[4];
+    int32_t K, rmax;
+};
+
+__global__ void __launch_bounds__(NT) merge_kernel(const MergeJob *jobs, int njobs, int *counter,
+                                                   double *work, const double *arena, int *ranks_out,
+                                                   double eps) {
+    extern __shared__ double4 smem_raw[];
+    dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(smem_raw);
+    __shared__ int s_job;
+    while (true) {
+        if (threadIdx.x == 0) s_job = atomicAdd(counter, 1);
+        __syncthreads();
+        const int jb = s_job;
+        __syncthreads();
+        if (jb >= njobs) break;
+        const MergeJob &J = jobs[jb];
+        double *U = work + J.wu, *V = work + J.wv;
+        // embedded factors: column block of kid q holds its U rows at ro and V rows at co
+        for (i64 e = threadIdx.x; e < J.M * J.K; e += NT) U[e] = 0.0;
+        for (i64 e = threadIdx.x; e < J.N * J.K; e += NT) V[e] = 0.0;
+        __syncthreads();
+        int k0 = 0;
+        for (int q = 0; q < 4; ++q) {
+            const MergeKid &c = J.kid[q];
+            for (i64 e = threadIdx.x; e < c.m * c.r; e += NT) {
+                const i64 i = e % c.m, l = e / c.m;
+                U[c.ro + i + (k0 + l) * J.M] = arena[c.uoff + i + l * c.m];
+            }
+            for (i64 e = threadIdx.x; e < c.n * c.r; e += NT) {
+                const i64 j = e % c.n, l = e / c.n;
+                V[c.co + j + (k0 + l) * J.N] = arena[c.voff + j + l * c.n];
+            }
+            k0 += c.r;
+        }
+        __syncthreads();
+        const int r = dev::recompress(U, J.M, J.M, V, J.N, J.N, J.K, 1, eps, U, J.M, V, J.N, J.rmax, S);
+        if (threadIdx.x == 0) ranks_out[jb] = r <= J.rmax ? r : -1;
+        __syncthreads();
+    }
+}
+
+__global__ void merge_copy_kernel(const i64 *src, const i64 *dst, const i64 *len, int njobs,
+                                  const double *work, double *arena) {
+    for (int b = blockIdx.x; b < njobs; b += gridDim.x)
+        for (i64 e = threadIdx.x; e < len[b]; e += NT) arena[dst[b] + e] = work[src[b] + e];
+}
+
+}  // namespace
+
+i64 coarsen_hmat(Ctx &ctx, HMat &H, double eps) {
+    // node depths (root 0)
+    std::vector<int> depth(H.nodes.size(), -1);
+    std::vector<int32_t> st{H.root};
+    depth[H.root] = 0;
+    int maxd = 0;
+    while (!st.empty()) {
+        int32_t b = st.back();
+        st.pop_back();
+        const Node &nd = H.nodes[b];
+        if (nd.kind == K_HIER)
+            for (int k = 0; k < 4; ++k) {
+                depth[nd.kid[k]] = depth[b] + 1;
+                maxd = std::max(maxd, depth[b] + 1);
+                st.push_back(nd.kid[k]);
+            }
+    }
+    H.sync_ranks(ctx.stream);
+    std::vector<int32_t> ranks = H.h_ranks;
+    i64 merged = 0;
+    i64 max_rows = std::numeric_limits<i64>::max();
+    if (const char *e = getenv("LEVYH_COARSEN_MAXROWS")) max_rows = atoll(e);
+    const size_t smem = sizeof(dev::RecompSmem);
+    set_smem((const void *)merge_kernel, smem);
+    for (int d = maxd - 1; d >= 0; --d) {
+        const auto tl = std::chrono::steady_clock::now();
+        std::vector<int32_t> cand;
+        std::vector<MergeJob> jobs;
+        i64 w = 0;
+        for (size_t b = 0; b < H.nodes.size(); ++b) {
+            const Node &nd = H.nodes[b];
+            if (depth[b] != d || nd.kind != K_HIER) continue;
+            const bool off_diag = nd.r0 + nd.m <= nd.c0 || nd.c0 + nd.n <= nd.r0;
+            if (!off_diag || std::max(nd.m, nd.n) > max_rows) continue;
+            MergeJob J{};
+            J.M = nd.m;
+            J.N = nd.n;
+            bool ok = true;
+            i64 kid_store = 0;
+            int K = 0;
+            for (int q = 0; q < 4 && ok; ++q) {
+                const Node &c = H.nodes[nd.kid[q]];
+                ok = c.kind == K_LR && c.vpar < 0;
+                if (!ok) break;
+                const int r = ranks[c.rslot];
+                J.kid[q] = {c.uoff, c.voff, c.r0 - nd.r0, c.c0 - nd.c0, c.m, c.n, r, 0};
+                K += r;
+                kid_store += (i64)r * (c.m + c.n);
+            }
+            if (!ok || K > KA_MAX) continue;
+            J.K = std::max(K, 1);
+            // merged rank must beat the children's storage and fit the low-rank capacity
+            J.rmax = (int)std::min<i64>(KC_MAX, (kid_store - 1) / (nd.m + nd.n));
+            if (J.rmax < 0 || K == 0) {
+                if (K != 0) continue;
+                J.rmax = 0;
+            }
+            J.wu = w;
+            J.wv = w + nd.m * J.K;
+            w += (nd.m + nd.n) * J.K;
+            jobs.push_back(J);
+            cand.push_back((int32_t)b);
+        }
+        if (jobs.empty()) continue;
+        double *work = dalloc<double>(std::max<i64>(w, 1));
+        MergeJob *djobs = dupload(jobs, ctx.stream);
+        int *dcnt = dalloc<int>(1 + (i64)jobs.size());
+        LH_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int), ctx.stream));
+        const int grid = (int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 2);
+        merge_kernel<<<grid, NT, smem, ctx.stream>>>(djobs, (int)jobs.size(), dcnt, work, H.d_arena,
+                                                     dcnt + 1, eps);
+        LH_CUDA(cudaGetLastError());
+        std::vector<int> r(jobs.size());
+        LH_CUDA(cudaMemcpyAsync(r.data(), dcnt + 1, sizeof(int) * r.size(), cudaMemcpyDeviceToHost,
+                                ctx.stream));
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        // append the accepted factors to the arena
+        std::vector<i64> src, dst, len;
+        i64 add = 0;
+        for (size_t k = 0; k < jobs.size(); ++k) {
+            if (r[k] < 0) continue;
+            const MergeJob &J = jobs[k];
+            src.push_back(J.wu);
+            dst.push_back(H.arena_len + add);
+            len.push_back(J.M * r[k]);
+            add += J.M * r[k];
+            src.push_back(J.wv);
+            dst.push_back(H.arena_len + add);
+            len.push_back(J.N * r[k]);
+            add += J.N * r[k];
+        }
+        if (add > 0) {
+            double *na = dalloc<double>(H.arena_len + add);
+            LH_CUDA(cudaMemcpyAsync(na, H.d_arena, sizeof(double) * H.arena_len, cudaMemcpyDeviceToDevice,
+                                    ctx.stream));
+            i64 *dsrc = dupload(src, ctx.stream), *ddst = dupload(dst, ctx.stream),
+                *dlen = dupload(len, ctx.stream);
+            merge_copy_kernel<<<(int)std::min<size_t>(src.size(), 148 * 16), NT, 0, ctx.stream>>>(
+                dsrc, ddst, dlen, (int)src.size(), work, na);
+            LH_CUDA(cudaGetLastError());
+            LH_CUDA(cudaStreamSynchronize(ctx.stream));
+            cudaFree(dsrc);
+            cudaFree(ddst);
+            cudaFree(dlen);
+            cudaFree(H.d_arena);
+            H.d_arena = na;
+            size_t q = 0;
+            for (size_t k = 0; k < jobs.size(); ++k) {
+                if (r[k] < 0) continue;
+                Node &nd = H.nodes[cand[k]];
+                nd.kind = K_LR;
+                nd.uoff = dst[q];
+                nd.voff = dst[q + 1];
+                q += 2;
+                nd.kcap = std::max(r[k], 1);
+                nd.rslot = (int32_t)ranks.size();
+                ranks.push_back(r[k]);
+                for (int t = 0; t < 4; ++t) nd.kid[t] = -1;
+                ++merged;
+            }
+            H.arena_len += add;
+        }
+        cudaFree(work);
+        cudaFree(djobs);
+        cudaFree(dcnt);
+        if (getenv("LEVYH_PLAN_VERBOSE")) {
+            i64 acc = 0, bigM = 0;
+            for (size_t k = 0; k < jobs.size(); ++k) {
+                acc += r[k] >= 0;
+                bigM = std::max(bigM, jobs[k].M);
+            }
+            fprintf(stderr, "[levyh] coarsen depth %d: %zu candidates, %lld merged, largest %lld rows, "
+                            "workspace %.2f GB, %.3f s\n", d, jobs.size(), (long long)acc, (long long)bigM,
+                    8e-9 * (double)w,
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - tl).count());
+        }
+    }
+    if (merged) {
+        int32_t *nr = dupload(ranks, ctx.stream);
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(H.d_ranks);
+        H.d_ranks = nr;
+        H.nslots = (int32_t)ranks.size();
+        H.h_ranks = ranks;
+        walk_leaves(H);
+    }
+    return merged;
 }
 
 }  // namespace lh

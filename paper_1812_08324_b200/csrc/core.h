@@ -105,7 +105,7 @@ struct HMat {
     i64 inv_len = 0;
     bool factored = false;
     bool refined = false;             // dense leaves > 64 split for the H-arithmetic planner
-    double lu_stats[5] = {0, 0, 0, 0, 0};  // tasks, plan s, temp bytes, exec s, chunks
+    double lu_stats[6] = {0, 0, 0, 0, 0, 0};  // tasks, plan s, temp bytes, exec s, chunks / NF leaves, merges
     // lazily built plans (opaque; see matvec.cu / plan.cpp)
     std::shared_ptr<void> mv_plan;
     std::shared_ptr<void> solve_plan;

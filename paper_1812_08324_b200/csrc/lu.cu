@@ -1904,6 +1904,7 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
 }
 
 i64 compress_near_field(Ctx &ctx, HMat &H, double eps);
+i64 coarsen_hmat(Ctx &ctx, HMat &H, double eps);
 
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.factored, LH_EINVAL, "prepare_propagator needs an H-LU factorization");
@@ -1957,12 +1958,19 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
         if (const char *e = getenv("LEVYH_NF_EPS")) nf_eps = atof(e);
         Z->lu_stats[4] = (double)compress_near_field(ctx, *Z, nf_eps);
     }
+    // coarsening: 2 x 2 low-rank siblings merged into one block where that saves bytes
+    if (!getenv("LEVYH_NO_COARSEN")) {
+        double c_eps = eps2;
+        if (const char *e = getenv("LEVYH_COARSEN_EPS")) c_eps = atof(e);
+        Z->lu_stats[5] = (double)coarsen_hmat(ctx, *Z, c_eps);
+    }
     auto t3 = now();
     S.mvZ = build_mv_plan(*Z, Z->leafblocks, ctx.stream);
     if (getenv("LEVYH_PLAN_VERBOSE"))
         fprintf(stderr, "[levyh] propagator: alloc+upload %.3f s, exec %.3f s, free plan %.3f s, "
-                        "near-field compression %.3f s (%.0f leaves), matvec plan %.3f s\n", sec(ta, t0),
-                sec(t0, t1), sec(t1, t2), sec(t2, t3), Z->lu_stats[4], sec(t3, now()));
+                        "near-field compression + coarsening %.3f s (%.0f leaves, %.0f merges), matvec plan "
+                        "%.3f s\n", sec(ta, t0), sec(t0, t1), sec(t1, t2), sec(t2, t3), Z->lu_stats[4],
+                Z->lu_stats[5], sec(t3, now()));
     S.Z = Z;
     if (!S.tmp) {
         S.tmp_len = F.nrows;
@@ -1975,7 +1983,7 @@ int step_graph_kernels(HMat &F) { return plans_of(F).g_kernels; }
 void propagator_stats(HMat &F, double *out) {
     SolvePlans &S = plans_of(F);
     LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
-    for (int k = 0; k < 5; ++k) out[k] = S.Z->lu_stats[k];
+    for (int k = 0; k < 6; ++k) out[k] = S.Z->lu_stats[k];
 }
 
 static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(NT) vtx_mm_kernel(const VChunk *chunks, const 
     const VChunk C = chunks[blockIdx.x];
     const int kc = blockIdx.y * MM_N;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int r = C.r, mt = (r + 7) >> 3;
+    const int r = vc_rank(C), mt = (r + 7) >> 3;
     const double *V = pbuf + C.voff;
     double acc[4][2] = {};
     for (int k0 = 0; k0 < C.len; k0 += MM_KB) {
@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(NT) vtx_mm_kernel(const VChunk *chunks, const 
         }
         __syncthreads();
     }
-    double *out = C.pidx >= 0 ? part + (i64)C.pidx * KC_MAX * ldk : T + (i64)C.blk * KC_MAX * ldk;
+    double *out = (C.pidx >= 0 ? part + (i64)C.pidx * KC_MAX * ldk : T + (i64)C.blk * KC_MAX * ldk) +
+                  (i64)vc_col0(C) * ldk;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const int c = t * 8 + (l >> 2);

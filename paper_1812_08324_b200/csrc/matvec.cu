@@ -72,7 +72,7 @@ __device__ __forceinline__ void warp_transpose_reduce(double (&acc)[RB], int lan
 template <int RB, int ROWS>
 __device__ __forceinline__ void vtx_warp(const VChunk &C, const double *pbuf, const double *x,
                                          double *out, int lane) {
-    const int r = C.r;
+    const int r = vc_rank(C);
     const int len = C.len;
     const double *V = pbuf + C.voff;
     const double *xx = x + C.xc0;
@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(NT, VTX_MIN_BLOCKS)
         const VChunk C = unpack(w);
         const int qn = q + stride;
         if (qn < nch) w = word(qn);
-        double *out = C.pidx >= 0 ? part + (i64)C.pidx * KC_MAX : tvec + (i64)C.blk * KC_MAX;
+        double *out = (C.pidx >= 0 ? part + (i64)C.pidx * KC_MAX : tvec + (i64)C.blk * KC_MAX) +
+                      vc_col0(C);
         vtx_warp<RB, 16 / RB>(C, pbuf, x, out, lane);
         if (qn >= nch) break;
         q = qn;
@@ -520,19 +521,25 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
             LH_REQUIRE(r <= KC_MAX, LH_EINTERNAL, "rank above the matvec capacity");
             if (r == 0) continue;
             const int blk = nblk++;
-            std::vector<VChunk> &dst = r > 8 ? chunks16 : chunks;
-            std::vector<i64> &dld = r > 8 ? vld16 : vld;
-            const i64 VCHUNK = vchunk_rows();
-            if (nd.n <= VCHUNK) {
-                dst.push_back({nd.voff, nd.c0, (int32_t)nd.n, r, blk, -1});
-                dld.push_back(nd.n);
-            } else {
-                int cb = npart;
-                for (i64 a = 0; a < nd.n; a += VCHUNK) {
-                    int len = (int)std::min(VCHUNK, nd.n - a);
-                    dst.push_back({nd.voff + a, nd.c0 + a, len, r, blk, npart++});
+            // ranks above 8 are split into column groups of <= 8 (the rank-8 V^T x kernel
+            // keeps twice the loads in flight per register of the rank-16 one)
+            static const bool split = !getenv("LEVYH_VTX16");
+            std::vector<VChunk> &dst = (r > 8 && !split) ? chunks16 : chunks;
+            std::vector<i64> &dld = (r > 8 && !split) ? vld16 : vld;
+            const int cg = split ? 8 : r;
+            auto emit = [&](i64 a, int len, int pidx) {
+                for (int c0 = 0; c0 < r; c0 += cg) {
+                    const int rr = std::min(cg, r - c0);
+                    dst.push_back({nd.voff + a + (i64)c0 * nd.n, nd.c0 + a, len, rr | (c0 << 16), blk, pidx});
                     dld.push_back(nd.n);
                 }
+            };
+            const i64 VCHUNK = vchunk_rows();
+            if (nd.n <= VCHUNK) {
+                emit(0, (int)nd.n, -1);
+            } else {
+                int cb = npart;
+                for (i64 a = 0; a < nd.n; a += VCHUNK) emit(a, (int)std::min(VCHUNK, nd.n - a), npart++);
                 tjobs.push_back({blk, r, cb, npart});
             }
             for (int sg = seg_of(nd.r0); sg < nseg && seg_start[sg] < nd.r0 + nd.m; ++sg) {
@@ -550,9 +557,9 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
             for (const VChunk &c : cv) {
                 int lc = 1;
                 while (lc < c.len) lc *= 2;
-                auto &e = h[{lc, c.r}];
+                auto &e = h[{lc, vc_rank(c)}];
                 e.first++;
-                e.second += 8.0 * c.len * c.r / 1e6;
+                e.second += 8.0 * c.len * vc_rank(c) / 1e6;
             }
             fprintf(stderr, "[mv plan] %s chunks %zu:", k ? "rank>8" : "rank<=8", cv.size());
             for (auto &e : h)
@@ -654,15 +661,15 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
         const std::vector<i64> &ld = k ? vld16 : vld;
         for (size_t q = 0; q < cv.size(); ++q) {
             VChunk &c = cv[q];
-            jobs.push_back({c.voff, ld[q], poff, c.len, c.r, c.len, 0});
+            jobs.push_back({c.voff, ld[q], poff, c.len, vc_rank(c), c.len, 0});
             c.voff = poff;
-            poff += even((i64)c.len * c.r);
+            poff += even((i64)c.len * vc_rank(c));
         }
         // largest chunks first: the grid-stride warps (and the hardware block scheduler behind
         // them) then finish on the small chunks instead of starting a 1024-row chunk last
         if (!getenv("LEVYH_VTX_NOSORT"))
             std::stable_sort(cv.begin(), cv.end(), [](const VChunk &a, const VChunk &b) {
-                return (i64)a.len * a.r > (i64)b.len * b.r;
+                return (i64)a.len * vc_rank(a) > (i64)b.len * vc_rank(b);
             });
     }
     // TMA kernel: contiguous, byte-balanced segment ranges, one CTA per SM
@@ -715,7 +722,16 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
         NP = (int)std::max<i64>(1, std::min<i64>(NP, nseg));
         P->npiece = NP;
         P->xcut.resize(NP + 1);
-        for (int p = 0; p <= NP; ++p) P->xcut[p] = std::min<i64>(H.ncols, ((H.ncols * p / NP) + 1) & ~i64(1));
+        // only the first x piece and the last y piece are exposed (the copy engine runs ahead
+        // of V^T x and behind the segments): make those 1/16 of the vector, the rest equal
+        auto frac = [&](int p, bool first_small) {
+            if (NP == 1) return (double)p;
+            const double f = 1.0 / 16;
+            if (first_small) return p == 0 ? 0.0 : f + (1.0 - f) * (p - 1) / (NP - 1);
+            return p == NP ? 1.0 : (1.0 - f) * p / (NP - 1);
+        };
+        for (int p = 0; p <= NP; ++p)
+            P->xcut[p] = std::min<i64>(H.ncols, ((i64)(H.ncols * frac(p, true)) + 1) & ~i64(1));
         P->xcut[0] = 0;
         P->xcut[NP] = H.ncols;
         auto piece_of = [&](const VChunk &c) {
@@ -739,7 +755,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
         std::vector<int> ps(NP + 1, nseg);
         ps[0] = 0;
         for (int p = 1; p < NP; ++p) {
-            const i64 target = H.nrows * p / NP;
+            const i64 target = (i64)(H.nrows * frac(p, false));
             int sg = ps[p - 1];
             while (sg < nseg && segs[sg].y0 < target) ++sg;
             ps[p] = sg;

@@ -32,10 +32,13 @@ struct MvLr {  // U rows at pbuf[off + i + c * ld], c < r; t_b = tvec[blk * KC_M
 };
 struct VChunk {  // V rows at pbuf[voff + i + c * len], i < len, c < r, multiplies x[xc0 + i]
     i64 voff, xc0;
-    int32_t len, r;
+    int32_t len, r;  // r: rank | (first column << 16); a block of rank > 8 is split by columns
+                     // into chunks of <= 8 (vc_rank / vc_col0)
     int32_t blk;   // the block's row of tvec (t_b = tvec[blk * KC_MAX + c])
     int32_t pidx;  // < 0: the chunk is the whole block (write t_b); else partial row index
 };
+__host__ __device__ inline int vc_rank(const VChunk &c) { return c.r & 0xffff; }
+__host__ __device__ inline int vc_col0(const VChunk &c) { return c.r >> 16; }
 struct TJob {  // t_b = sum of the partials of chunks [cbeg, cend), written to tvec row blk
     int32_t blk, r, cbeg, cend;
 };

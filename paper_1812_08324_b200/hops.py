@@ -99,9 +99,9 @@ class HFactorization:
             self.propagator_ready = True
 
     def propagator_stats(self):
-        """(task count, planning s, temp bytes, executor s, near-field leaves compressed) of
-        the propagator build."""
-        out = np.zeros(5)
+        """(task count, planning s, temp bytes, executor s, near-field leaves compressed,
+        coarsening merges) of the propagator build."""
+        out = np.zeros(6)
         _lib.check(_lib.lib().lh_propagator_stats(self.h.handle, _lib.host_ptr(out)))
         return out
 
