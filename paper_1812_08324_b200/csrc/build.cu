@@ -1091,27 +1091,63 @@ i64 compress_near_field(Ctx &ctx, HMat &H, double eps) {
 // ===========================================================================
 // Coarsening of a computed H-matrix (the propagator Z): bottom-up, a 2 x 2
 // hierarchical block off the diagonal whose four children are low-rank is replaced by one
-// low-rank block when the recompressed sum of its children (QR of the embedded U's and V's,
-// Jacobi SVD, the hops.py:124-131 Frobenius-tail rule at eps relative to the merged block)
-// needs fewer scalars than the children.  Repeats level by level while merges pay.
+// low-rank block when the recompressed sum of its children needs fewer scalars.  The
+// embedded factors of the sum are block-structured (the U's of kids 11, 12 share the top
+// rows, those of 21, 22 the bottom rows; the V's of 11, 21 the left columns, of 12, 22 the
+// right ones), so their QR factorisations split into four independent half-height QRs
+// (CGS2, one CTA each), the K x K core R_u R_v^T is formed from the four R's and
+// SVD-truncated (Jacobi, the hops.py:124-131 Frobenius-tail rule at eps relative to the
+// merged block) on one CTA, and the merged factors Q_side * coefficients are written
+// row-parallel straight into the grown arena.
 // ===========================================================================
 namespace lh {
 void walk_leaves(HMat &H);
 namespace {
 
-struct MergeKid {
-    i64 uoff, voff, ro, co, m, n;
-    int32_t r, pad;
+struct QrSide {        // [A | B]: rows x (ra + rb), from two kids' factors (ld = rows)
+    i64 rows, srca, srcb, w;
+    int32_t ra, rb;
 };
-struct MergeJob {
-    i64 M, N, wu, wv;
-    MergeKid kid[4];
-    int32_t K, rmax;
+struct CoreJob {       // merge k: sides 4k..4k+3 = top, bottom, left, right
+    int32_t r11, r12, r21, r22;
+    int32_t rmax, pad;
+};
+struct ApplyJob {      // out[row0 + i + c * ld] = sum_l Q[i + l * rows] * coef[coff + l + c * KA_MAX]
+    i64 q, rows, out, ld, row0;
+    int32_t K, r, coff, pad;
 };
 
-__global__ void __launch_bounds__(NT) merge_kernel(const MergeJob *jobs, int njobs, int *counter,
-                                                   double *work, const double *arena, int *ranks_out,
-                                                   double eps) {
+constexpr int QR_SMEM_D = KA_MAX * KA_MAX + KA_MAX + 2 * dev::NW;
+
+__global__ void __launch_bounds__(NT) side_qr_kernel(const QrSide *sides, int nsides, int *counter,
+                                                     const double *arena, double *work, double *Rout) {
+    extern __shared__ double4 smem_raw[];
+    double *R = reinterpret_cast<double *>(smem_raw);
+    double *h = R + KA_MAX * KA_MAX;
+    double *red = h + KA_MAX;
+    __shared__ int s_job;
+    while (true) {
+        if (threadIdx.x == 0) s_job = atomicAdd(counter, 1);
+        __syncthreads();
+        const int jb = s_job;
+        __syncthreads();
+        if (jb >= nsides) break;
+        const QrSide S = sides[jb];
+        double *W = work + S.w;
+        for (i64 e = threadIdx.x; e < S.rows * S.ra; e += NT) W[e] = arena[S.srca + e];
+        for (i64 e = threadIdx.x; e < S.rows * S.rb; e += NT) W[S.rows * S.ra + e] = arena[S.srcb + e];
+        __syncthreads();
+        const int K = S.ra + S.rb;
+        dev::cgs2(W, S.rows, S.rows, K, R, h, red);
+        for (int e = threadIdx.x; e < KA_MAX * KA_MAX; e += NT)
+            Rout[(i64)jb * KA_MAX * KA_MAX + e] = R[e];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(NT) core_kernel(const CoreJob *jobs, int njobs, int *counter,
+                                                  const double *Rin, double *coef, int *ranks_out,
+                                                  double eps) {
     extern __shared__ double4 smem_raw[];
     dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(smem_raw);
     __shared__ int s_job;
@@ -1121,42 +1157,96 @@ __global__ void __launch_bounds__(NT) merge_kernel(const MergeJob *jobs, int njo
         const int jb = s_job;
         __syncthreads();
         if (jb >= njobs) break;
-        const MergeJob &J = jobs[jb];
-        double *U = work + J.wu, *V = work + J.wv;
-        // embedded factors: column block of kid q holds its U rows at ro and V rows at co
-        for (i64 e = threadIdx.x; e < J.M * J.K; e += NT) U[e] = 0.0;
-        for (i64 e = threadIdx.x; e < J.N * J.K; e += NT) V[e] = 0.0;
-        __syncthreads();
-        int k0 = 0;
-        for (int q = 0; q < 4; ++q) {
-            const MergeKid &c = J.kid[q];
-            for (i64 e = threadIdx.x; e < c.m * c.r; e += NT) {
-                const i64 i = e % c.m, l = e / c.m;
-                U[c.ro + i + (k0 + l) * J.M] = arena[c.uoff + i + l * c.m];
-            }
-            for (i64 e = threadIdx.x; e < c.n * c.r; e += NT) {
-                const i64 j = e % c.n, l = e / c.n;
-                V[c.co + j + (k0 + l) * J.N] = arena[c.voff + j + l * c.n];
-            }
-            k0 += c.r;
+        const CoreJob J = jobs[jb];
+        const double *Rt = Rin + (i64)(4 * jb + 0) * KA_MAX * KA_MAX;
+        const double *Rb = Rin + (i64)(4 * jb + 1) * KA_MAX * KA_MAX;
+        const double *Rl = Rin + (i64)(4 * jb + 2) * KA_MAX * KA_MAX;
+        const double *Rr = Rin + (i64)(4 * jb + 3) * KA_MAX * KA_MAX;
+        const int Kt = J.r11 + J.r12, Kb = J.r21 + J.r22, Kl = J.r11 + J.r21, K = Kt + Kb;
+        // R_u (K x K): diag(R_top, R_bot), columns ordered kids 11, 12, 21, 22
+        // R_v (K x K): rows = left basis then right basis; columns 11, 12, 21, 22
+        for (int e = threadIdx.x; e < KA_MAX * KA_MAX; e += NT) {
+            S.Ru[e] = 0.0;
+            S.Rv[e] = 0.0;
         }
         __syncthreads();
-        const int r = dev::recompress(U, J.M, J.M, V, J.N, J.N, J.K, 1, eps, U, J.M, V, J.N, J.rmax, S);
-        if (threadIdx.x == 0) ranks_out[jb] = r <= J.rmax ? r : -1;
+        for (int e = threadIdx.x; e < K * K; e += NT) {
+            const int i = e % K, j = e / K;
+            if (i < Kt && j < Kt) S.Ru[i + j * KA_MAX] = Rt[i + j * KA_MAX];
+            if (i >= Kt && j >= Kt) S.Ru[i + j * KA_MAX] = Rb[(i - Kt) + (j - Kt) * KA_MAX];
+            // column j of V_big: kid and its column within the kid
+            double v = 0.0;
+            if (j < J.r11) {
+                if (i < Kl) v = Rl[i + j * KA_MAX];
+            } else if (j < Kt) {
+                if (i >= Kl) v = Rr[(i - Kl) + (j - J.r11) * KA_MAX];
+            } else if (j < Kt + J.r21) {
+                if (i < Kl) v = Rl[i + (J.r11 + j - Kt) * KA_MAX];
+            } else {
+                if (i >= Kl) v = Rr[(i - Kl) + (J.r12 + j - Kt - J.r21) * KA_MAX];
+            }
+            S.Rv[i + j * KA_MAX] = v;
+        }
+        __syncthreads();
+        // C = R_u R_v^T
+        for (int e = threadIdx.x; e < K * K; e += NT) {
+            const int i = e % K, j = e / K;
+            double acc = 0.0;
+            for (int l = 0; l < K; ++l) acc += S.Ru[i + l * KA_MAX] * S.Rv[j + l * KA_MAX];
+            S.Cc[i + j * KA_MAX] = acc;
+        }
+        __syncthreads();
+        dev::jacobi_svd(S.Cc, S.Rv, K, S.sigma, S.ord, S.red);
+        const int r = dev::truncation_rank(S.sigma, S.ord, K, 1, eps);
+        const bool ok = r <= J.rmax;
+        if (ok) {  // coefficients: Cu[:, c] = (C Z)[:, ord[c]], Cv[:, c] = Z[:, ord[c]]
+            double *cu = coef + (i64)(2 * jb) * KA_MAX * KC_MAX;
+            double *cv = coef + (i64)(2 * jb + 1) * KA_MAX * KC_MAX;
+            for (int e = threadIdx.x; e < K * r; e += NT) {
+                const int l = e % K, c = e / K;
+                cu[l + c * KA_MAX] = S.Cc[l + S.ord[c] * KA_MAX];
+                cv[l + c * KA_MAX] = S.Rv[l + S.ord[c] * KA_MAX];
+            }
+        }
+        if (threadIdx.x == 0) ranks_out[jb] = ok ? r : -1;
         __syncthreads();
     }
 }
 
-__global__ void merge_copy_kernel(const i64 *src, const i64 *dst, const i64 *len, int njobs,
-                                  const double *work, double *arena) {
-    for (int b = blockIdx.x; b < njobs; b += gridDim.x)
-        for (i64 e = threadIdx.x; e < len[b]; e += NT) arena[dst[b] + e] = work[src[b] + e];
+// row-parallel: one CTA per (job, 256-row tile), grid-stride over tiles
+__global__ void __launch_bounds__(NT) apply_kernel(const ApplyJob *jobs, const i64 *tile0, int njobs,
+                                                   i64 ntiles, const double *work, const double *coef,
+                                                   double *arena) {
+    for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int lo = 0, hi = njobs - 1;  // job of tile t: last j with tile0[j] <= t
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tile0[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const ApplyJob J = jobs[lo];
+        const i64 i = (t - tile0[lo]) * NT + threadIdx.x;
+        if (i >= J.rows) continue;
+        const double *Q = work + J.q;
+        const double *cf = coef + J.coff;
+        double acc[KC_MAX];
+#pragma unroll
+        for (int c = 0; c < KC_MAX; ++c) acc[c] = 0.0;
+        for (int l = 0; l < J.K; ++l) {
+            const double q = Q[i + (i64)l * J.rows];
+#pragma unroll
+            for (int c = 0; c < KC_MAX; ++c)
+                if (c < J.r) acc[c] += q * cf[l + c * KA_MAX];
+        }
+#pragma unroll
+        for (int c = 0; c < KC_MAX; ++c)
+            if (c < J.r) arena[J.out + J.row0 + i + (i64)c * J.ld] = acc[c];
+    }
 }
 
 }  // namespace
 
 i64 coarsen_hmat(Ctx &ctx, HMat &H, double eps) {
-    // node depths (root 0)
     std::vector<int> depth(H.nodes.size(), -1);
     std::vector<int32_t> st{H.root};
     depth[H.root] = 0;
@@ -1177,118 +1267,149 @@ i64 coarsen_hmat(Ctx &ctx, HMat &H, double eps) {
     i64 merged = 0;
     i64 max_rows = std::numeric_limits<i64>::max();
     if (const char *e = getenv("LEVYH_COARSEN_MAXROWS")) max_rows = atoll(e);
-    const size_t smem = sizeof(dev::RecompSmem);
-    set_smem((const void *)merge_kernel, smem);
+    const size_t qr_smem = sizeof(double) * QR_SMEM_D, core_smem = sizeof(dev::RecompSmem);
+    set_smem((const void *)side_qr_kernel, qr_smem);
+    set_smem((const void *)core_kernel, core_smem);
     for (int d = maxd - 1; d >= 0; --d) {
         const auto tl = std::chrono::steady_clock::now();
         std::vector<int32_t> cand;
-        std::vector<MergeJob> jobs;
+        std::vector<CoreJob> cores;
+        std::vector<QrSide> sides;
         i64 w = 0;
         for (size_t b = 0; b < H.nodes.size(); ++b) {
             const Node &nd = H.nodes[b];
             if (depth[b] != d || nd.kind != K_HIER) continue;
             const bool off_diag = nd.r0 + nd.m <= nd.c0 || nd.c0 + nd.n <= nd.r0;
             if (!off_diag || std::max(nd.m, nd.n) > max_rows) continue;
-            MergeJob J{};
-            J.M = nd.m;
-            J.N = nd.n;
+            const Node *k[4];
             bool ok = true;
-            i64 kid_store = 0;
-            int K = 0;
+            int r[4];
+            i64 store = 0;
             for (int q = 0; q < 4 && ok; ++q) {
-                const Node &c = H.nodes[nd.kid[q]];
-                ok = c.kind == K_LR && c.vpar < 0;
-                if (!ok) break;
-                const int r = ranks[c.rslot];
-                J.kid[q] = {c.uoff, c.voff, c.r0 - nd.r0, c.c0 - nd.c0, c.m, c.n, r, 0};
-                K += r;
-                kid_store += (i64)r * (c.m + c.n);
+                k[q] = &H.nodes[nd.kid[q]];
+                ok = k[q]->kind == K_LR && k[q]->vpar < 0;
+                if (ok) {
+                    r[q] = ranks[k[q]->rslot];
+                    store += (i64)r[q] * (k[q]->m + k[q]->n);
+                }
             }
-            if (!ok || K > KA_MAX) continue;
-            J.K = std::max(K, 1);
-            // merged rank must beat the children's storage and fit the low-rank capacity
-            J.rmax = (int)std::min<i64>(KC_MAX, (kid_store - 1) / (nd.m + nd.n));
-            if (J.rmax < 0 || K == 0) {
-                if (K != 0) continue;
-                J.rmax = 0;
+            if (!ok) continue;
+            const int K = r[0] + r[1] + r[2] + r[3];
+            if (K > KA_MAX || K == 0) continue;  // all-zero groups are left alone
+            CoreJob J{r[0], r[1], r[2], r[3], (int32_t)std::min<i64>(KC_MAX, (store - 1) / (nd.m + nd.n)), 0};
+            if (J.rmax < 0) continue;
+            // sides: top = [U11 U12], bottom = [U21 U22], left = [V11 V21], right = [V12 V22]
+            const QrSide sd[4] = {
+                {k[0]->m, k[0]->uoff, k[1]->uoff, 0, r[0], r[1]},
+                {k[2]->m, k[2]->uoff, k[3]->uoff, 0, r[2], r[3]},
+                {k[0]->n, k[0]->voff, k[2]->voff, 0, r[0], r[2]},
+                {k[1]->n, k[1]->voff, k[3]->voff, 0, r[1], r[3]}};
+            for (int q = 0; q < 4; ++q) {
+                QrSide S = sd[q];
+                S.w = w;
+                w += S.rows * std::max(S.ra + S.rb, 1);
+                sides.push_back(S);
             }
-            J.wu = w;
-            J.wv = w + nd.m * J.K;
-            w += (nd.m + nd.n) * J.K;
-            jobs.push_back(J);
+            cores.push_back(J);
             cand.push_back((int32_t)b);
         }
-        if (jobs.empty()) continue;
+        if (cores.empty()) continue;
+        const int nc = (int)cores.size(), ns = (int)sides.size();
         double *work = dalloc<double>(std::max<i64>(w, 1));
-        MergeJob *djobs = dupload(jobs, ctx.stream);
-        int *dcnt = dalloc<int>(1 + (i64)jobs.size());
-        LH_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int), ctx.stream));
-        const int grid = (int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 2);
-        merge_kernel<<<grid, NT, smem, ctx.stream>>>(djobs, (int)jobs.size(), dcnt, work, H.d_arena,
-                                                     dcnt + 1, eps);
+        double *Rbuf = dalloc<double>((i64)ns * KA_MAX * KA_MAX);
+        double *coef = dalloc<double>((i64)2 * nc * KA_MAX * KC_MAX);
+        QrSide *dsides = dupload(sides, ctx.stream);
+        CoreJob *dcores = dupload(cores, ctx.stream);
+        int *dcnt = dalloc<int>(2 + (i64)nc);
+        LH_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * 2, ctx.stream));
+        side_qr_kernel<<<(int)std::min<i64>(ns, (i64)ctx.num_sms * 2), NT, qr_smem, ctx.stream>>>(
+            dsides, ns, dcnt, H.d_arena, work, Rbuf);
         LH_CUDA(cudaGetLastError());
-        std::vector<int> r(jobs.size());
-        LH_CUDA(cudaMemcpyAsync(r.data(), dcnt + 1, sizeof(int) * r.size(), cudaMemcpyDeviceToHost,
-                                ctx.stream));
+        core_kernel<<<(int)std::min<i64>(nc, (i64)ctx.num_sms * 2), NT, core_smem, ctx.stream>>>(
+            dcores, nc, dcnt + 1, Rbuf, coef, dcnt + 2, eps);
+        LH_CUDA(cudaGetLastError());
+        std::vector<int> rk(nc);
+        LH_CUDA(cudaMemcpyAsync(rk.data(), dcnt + 2, sizeof(int) * nc, cudaMemcpyDeviceToHost, ctx.stream));
         LH_CUDA(cudaStreamSynchronize(ctx.stream));
-        // append the accepted factors to the arena
-        std::vector<i64> src, dst, len;
+        // grow the arena by the accepted factors and write them row-parallel
         i64 add = 0;
-        for (size_t k = 0; k < jobs.size(); ++k) {
-            if (r[k] < 0) continue;
-            const MergeJob &J = jobs[k];
-            src.push_back(J.wu);
-            dst.push_back(H.arena_len + add);
-            len.push_back(J.M * r[k]);
-            add += J.M * r[k];
-            src.push_back(J.wv);
-            dst.push_back(H.arena_len + add);
-            len.push_back(J.N * r[k]);
-            add += J.N * r[k];
+        std::vector<i64> uo(nc, -1), vo(nc, -1);
+        std::vector<ApplyJob> aj;
+        std::vector<i64> tile0;
+        i64 ntiles = 0;
+        for (int c = 0; c < nc; ++c) {
+            if (rk[c] < 0) continue;
+            const Node &nd = H.nodes[cand[c]];
+            const int r = rk[c];
+            uo[c] = H.arena_len + add;
+            add += nd.m * r;
+            vo[c] = H.arena_len + add;
+            add += nd.n * r;
+            if (r == 0) continue;
+            const QrSide *sd = &sides[4 * c];
+            const CoreJob &J = cores[c];
+            const int Kt = J.r11 + J.r12, Kl = J.r11 + J.r21;
+            const i64 cu = (i64)(2 * c) * KA_MAX * KC_MAX, cv = (i64)(2 * c + 1) * KA_MAX * KC_MAX;
+            const ApplyJob jobs4[4] = {
+                {sd[0].w, sd[0].rows, uo[c], nd.m, 0, Kt, r, (int32_t)0, 0},
+                {sd[1].w, sd[1].rows, uo[c], nd.m, sd[0].rows, J.r21 + J.r22, r, (int32_t)Kt, 0},
+                {sd[2].w, sd[2].rows, vo[c], nd.n, 0, Kl, r, (int32_t)0, 0},
+                {sd[3].w, sd[3].rows, vo[c], nd.n, sd[2].rows, J.r12 + J.r22, r, (int32_t)Kl, 0}};
+            for (int q = 0; q < 4; ++q) {
+                ApplyJob A = jobs4[q];
+                A.coff += (int32_t)(q < 2 ? cu : cv);  // absolute coefficient offset
+                if (A.K == 0 || A.rows == 0) continue;
+                tile0.push_back(ntiles);
+                ntiles += (A.rows + NT - 1) / NT;
+                aj.push_back(A);
+            }
         }
         if (add > 0) {
             double *na = dalloc<double>(H.arena_len + add);
             LH_CUDA(cudaMemcpyAsync(na, H.d_arena, sizeof(double) * H.arena_len, cudaMemcpyDeviceToDevice,
                                     ctx.stream));
-            i64 *dsrc = dupload(src, ctx.stream), *ddst = dupload(dst, ctx.stream),
-                *dlen = dupload(len, ctx.stream);
-            merge_copy_kernel<<<(int)std::min<size_t>(src.size(), 148 * 16), NT, 0, ctx.stream>>>(
-                dsrc, ddst, dlen, (int)src.size(), work, na);
-            LH_CUDA(cudaGetLastError());
+            LH_CUDA(cudaMemsetAsync(na + H.arena_len, 0, sizeof(double) * add, ctx.stream));
+            if (!aj.empty()) {
+                ApplyJob *daj = dupload(aj, ctx.stream);
+                i64 *dt0 = dupload(tile0, ctx.stream);
+                apply_kernel<<<(int)std::min<i64>(ntiles, (i64)ctx.num_sms * 16), NT, 0, ctx.stream>>>(
+                    daj, dt0, (int)aj.size(), ntiles, work, coef, na);
+                LH_CUDA(cudaGetLastError());
+                LH_CUDA(cudaStreamSynchronize(ctx.stream));
+                cudaFree(daj);
+                cudaFree(dt0);
+            }
             LH_CUDA(cudaStreamSynchronize(ctx.stream));
-            cudaFree(dsrc);
-            cudaFree(ddst);
-            cudaFree(dlen);
             cudaFree(H.d_arena);
             H.d_arena = na;
-            size_t q = 0;
-            for (size_t k = 0; k < jobs.size(); ++k) {
-                if (r[k] < 0) continue;
-                Node &nd = H.nodes[cand[k]];
+            for (int c = 0; c < nc; ++c) {
+                if (rk[c] < 0) continue;
+                Node &nd = H.nodes[cand[c]];
                 nd.kind = K_LR;
-                nd.uoff = dst[q];
-                nd.voff = dst[q + 1];
-                q += 2;
-                nd.kcap = std::max(r[k], 1);
+                nd.uoff = uo[c];
+                nd.voff = vo[c];
+                nd.kcap = std::max(rk[c], 1);
                 nd.rslot = (int32_t)ranks.size();
-                ranks.push_back(r[k]);
+                ranks.push_back(rk[c]);
                 for (int t = 0; t < 4; ++t) nd.kid[t] = -1;
                 ++merged;
             }
             H.arena_len += add;
         }
         cudaFree(work);
-        cudaFree(djobs);
+        cudaFree(Rbuf);
+        cudaFree(coef);
+        cudaFree(dsides);
+        cudaFree(dcores);
         cudaFree(dcnt);
         if (getenv("LEVYH_PLAN_VERBOSE")) {
             i64 acc = 0, bigM = 0;
-            for (size_t k = 0; k < jobs.size(); ++k) {
-                acc += r[k] >= 0;
-                bigM = std::max(bigM, jobs[k].M);
+            for (int c = 0; c < nc; ++c) {
+                acc += rk[c] >= 0;
+                bigM = std::max(bigM, H.nodes[cand[c]].m);
             }
-            fprintf(stderr, "[levyh] coarsen depth %d: %zu candidates, %lld merged, largest %lld rows, "
-                            "workspace %.2f GB, %.3f s\n", d, jobs.size(), (long long)acc, (long long)bigM,
-                    8e-9 * (double)w,
+            fprintf(stderr, "[levyh] coarsen depth %d: %d candidates, %lld merged, largest %lld rows, "
+                            "workspace %.2f GB, %.3f s\n", d, nc, (long long)acc, (long long)bigM, 8e-9 * (double)w,
                     std::chrono::duration<double>(std::chrono::steady_clock::now() - tl).count());
         }
     }
