@@ -78,9 +78,14 @@ __device__ __forceinline__ void st_release(int32_t *p, int v) {
 }
 
 // ---------------------------------------------------------------------------
-// GETRF fast path (m <= 64): right-looking LU with partial pivoting, thread (row
-// i = t % 64, column group t / 64), 2 barriers per column; then the packed leaf
-// inverse P = strict_lower(L^-1) + upper(U^-1) by one fused forward/backward sweep.
+// GETRF fast path (m <= 64): right-looking LU with partial pivoting held in registers,
+// thread (row tx = t % 64, columns ty + 4 q, q < 16); per column one warp-shuffle pivot search
+// on the two warps owning the column, the pivot row / old row j / column j exchanged through
+// shared memory, two barriers.  The arithmetic is LAPACK dgetf2's (reciprocal pivot scaling,
+// rank-1 update).  Then the packed leaf inverse P = strict_lower(L^-1) + upper(U^-1) by a
+// blocked inversion (8 x 8 diagonal blocks by substitution, then seven block diagonals),
+// L^-1 and U^-1 concurrently on the two halves of the CTA.  The leaf is padded to 64 x 64
+// with the identity.
 // ---------------------------------------------------------------------------
 constexpr int LD65 = 65;  // odd leading dimension: conflict-free column and row walks
 
@@ -88,65 +93,136 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
     const DView &v = T.v[0];
     const int m = v.rows;
     double *G = vp(A, v);
-    double *S = sm;                       // m x m, ld 65
+    double *S = sm;                       // LU factors, 64 x 64 padded, ld 65
     double *Li = sm + 64 * LD65;          // L^-1 (unit lower)
-    double *Ui = sm + 2 * 64 * LD65;      // U^-1 (upper, unscaled rows until the end)
-    int *piv = (int *)(sm + 3 * 64 * LD65);
-    __shared__ int s_p;
+    double *Ui = sm + 2 * 64 * LD65;      // U^-1 (upper)
+    double *Tw = sm + 3 * 64 * LD65;      // block-product workspace, 2 x 512
+    double *prow = Tw + 1024, *jrow = prow + 64, *colj = jrow + 64;
+    int *piv = (int *)(colj + 64);
+    __shared__ double s_cv[2];
+    __shared__ int s_ci[2];
     const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-    for (int e = threadIdx.x; e < m * m; e += NT) {
-        const unsigned s = (unsigned)__cvta_generic_to_shared(S + (e % m) + (e / m) * LD65);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s),
-                     "l"(G + e % m + (e / m) * (i64)v.ld) : "memory");
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = 0; j < m; ++j) {
-        if (w == 0) {
-            double best = -1.0;
-            int bi = j;
-            for (int i = j + lane; i < m; i += 32) {
-                double a = fabs(S[i + j * LD65]);
-                if (a > best) {
-                    best = a;
-                    bi = i;
+    const int lane = threadIdx.x & 31;
+    // Speculative pass without row exchanges: partial pivoting keeps every diagonal pivot iff
+    // |a_jj| >= |a_ij| (i > j) at every step, which is checked exactly on the values the
+    // pivoted algorithm would compare; then the factors are bit-identical to it (same
+    // operations in the same order).  No leaf of the SURVEY a16 operators pivots.  Layout:
+    // row t >> 2, columns (t & 3) + 4 q, so a row's four threads are adjacent lanes and the
+    // column-j value reaches them by one shuffle; one barrier per column.
+    bool spec_ok;
+    {
+        const int tr = threadIdx.x >> 2, tc = threadIdx.x & 3;
+        double b[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int c = tc + 4 * q;
+            b[q] = (tr < m && c < m) ? G[tr + c * (i64)v.ld] : (tr == c ? 1.0 : 0.0);
+        }
+        bool ok = true;
+        for (int j = 0; j < m; ++j) {
+            double *Pj = Tw + (j & 1) * 64;  // double-buffered row j
+            if (tr == j) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) Pj[tc + 4 * q] = b[q];
+            }
+            __syncthreads();
+            const int jt = j & 3, jq = j >> 2;
+            double mine = 0.0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q == jq) mine = b[q];
+            const double lv = __shfl_sync(0xffffffffu, mine, (lane & ~3) | jt);
+            if (tr > j && tr < m) {
+                const double d = Pj[j];
+                ok = ok && (d != 0.0 ? fabs(lv) <= fabs(d) : lv == 0.0);
+                const double l = d != 0.0 ? lv * (1.0 / d) : lv;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int c = tc + 4 * q;
+                    if (c > j) b[q] -= l * Pj[c];
+                    else if (c == j) b[q] = l;
                 }
             }
+        }
+        spec_ok = __syncthreads_and(ok);
+        if (spec_ok) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) S[tr + (tc + 4 * q) * LD65] = b[q];
+            if (threadIdx.x < 64) piv[threadIdx.x] = threadIdx.x;
+        }
+    }
+    double a[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int c = ty + 4 * q;
+        a[q] = (tx < m && c < m) ? G[tx + c * (i64)v.ld] : (tx == c ? 1.0 : 0.0);
+    }
+    for (int j = 0; j < m && !spec_ok; ++j) {
+        const int jt = j & 3, jq = j >> 2;
+        if (ty == jt) {  // idamax over rows j..m-1 of column j, first index on ties
+            double best = -1.0;
+            int bi = j;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q == jq && tx >= j && tx < m) {
+                    best = fabs(a[q]);
+                    bi = tx;
+                }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (ob > best || (ob == best && oi < bi)) {
                     best = ob;
                     bi = oi;
                 }
             }
             if (lane == 0) {
-                s_p = bi;
-                piv[j] = bi;
+                s_cv[tx >> 5] = best;
+                s_ci[tx >> 5] = bi;
             }
         }
         __syncthreads();
-        const int p = s_p;
-        if (p != j) {
-            if (threadIdx.x < m) {
-                const int c = threadIdx.x;
-                double t = S[j + c * LD65];
-                S[j + c * LD65] = S[p + c * LD65];
-                S[p + c * LD65] = t;
-            }
-            __syncthreads();
+        const int p = (s_cv[1] > s_cv[0] || (s_cv[1] == s_cv[0] && s_ci[1] < s_ci[0])) ? s_ci[1] : s_ci[0];
+        if (tx == p) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) prow[ty + 4 * q] = a[q];
         }
-        const double d = S[j + j * LD65];
-        double l = 0.0;
+        if (tx == j && p != j) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) jrow[ty + 4 * q] = a[q];
+        }
+        if (ty == jt) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q == jq) colj[tx] = a[q];
+        }
+        __syncthreads();
+        if (p != j) {  // swap rows j and p
+            if (tx == j) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) a[q] = prow[ty + 4 * q];
+            } else if (tx == p) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) a[q] = jrow[ty + 4 * q];
+            }
+        }
         if (tx > j && tx < m) {
-            // scale by the reciprocal pivot (as LAPACK dgetf2 does for |pivot| >= sfmin)
-            l = d != 0.0 ? S[tx + j * LD65] * (1.0 / d) : S[tx + j * LD65];
-            for (int c = j + 1 + ty; c < m; c += 4) S[tx + c * LD65] -= l * S[j + c * LD65];
+            const double d = prow[j];
+            const double lv = (tx == p) ? jrow[j] : colj[tx];
+            const double l = d != 0.0 ? lv * (1.0 / d) : lv;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int c = ty + 4 * q;
+                if (c > j) a[q] -= l * prow[c];
+                else if (c == j) a[q] = l;
+            }
         }
-        __syncthreads();
-        if (ty == 0 && tx > j && tx < m) S[tx + j * LD65] = l;  // column j is not read again
+        if (threadIdx.x == 0) piv[j] = p;
+    }
+    if (!spec_ok) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) S[tx + (ty + 4 * q) * LD65] = a[q];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < m * m; e += NT) G[e % m + (e / m) * (i64)v.ld] = S[(e % m) + (e / m) * LD65];
@@ -168,33 +244,76 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
             }
     }
     if (!(T.flags & 1)) return;
-    // identity start; reciprocal pivots
-    __shared__ double rdiag[64];
-    if (threadIdx.x < m) rdiag[threadIdx.x] = 1.0 / S[threadIdx.x + threadIdx.x * LD65];
-    for (int e = threadIdx.x; e < m * m; e += NT) {
-        int i = e % m, c = e / m;
-        Li[i + c * LD65] = (i == c) ? 1.0 : 0.0;
-        Ui[i + c * LD65] = (i == c) ? 1.0 : 0.0;
+    // ---- blocked inverses of the padded factors: threads 0..127 L^-1, 128..255 U^-1
+    const bool up = threadIdx.x >= 128;
+    const int u = threadIdx.x & 127;
+    double *X = up ? Ui : Li;
+    double *Tp = Tw + (up ? 512 : 0);
+    for (int e = u; e < 64 * 64; e += 128) X[(e & 63) + (e >> 6) * LD65] = 0.0;
+    __syncthreads();
+    if (u < 64) {  // diagonal 8 x 8 blocks: one column of one block per thread
+        const int bi = u >> 3, cc = u & 7, o = 8 * bi;
+        double x[8];
+        if (!up) {  // unit lower: x[r] = e_cc[r] - sum_{s<r} L[r][s] x[s]
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double t = (r == cc) ? 1.0 : 0.0;
+#pragma unroll
+                for (int s2 = 0; s2 < 8; ++s2)
+                    if (s2 < r) t -= S[o + r + (o + s2) * LD65] * x[s2];
+                x[r] = t;
+            }
+        } else {  // upper: x[r] = (e_cc[r] - sum_{s>r} U[r][s] x[s]) / U[r][r]
+#pragma unroll
+            for (int r = 7; r >= 0; --r) {
+                double t = (r == cc) ? 1.0 : 0.0;
+#pragma unroll
+                for (int s2 = 0; s2 < 8; ++s2)
+                    if (s2 > r) t -= S[o + r + (o + s2) * LD65] * x[s2];
+                x[r] = t / S[o + r + (o + r) * LD65];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) X[o + r + (o + cc) * LD65] = x[r];
     }
     __syncthreads();
-    // step k: forward column k of L X = I, backward column l = m-1-k of U X = I
-    for (int k = 0; k < m; ++k) {
-        const int l = m - 1 - k;
-        if (tx > k && tx < m) {
-            const double a = S[tx + k * LD65];
-            for (int c = ty; c <= k; c += 4) Li[tx + c * LD65] -= a * Li[k + c * LD65];
+    for (int d = 1; d < 8; ++d) {
+        const int nblk = 8 - d;  // blocks (i, i - d) of L^-1 / (i, i + d) of U^-1, i < nblk
+        // T = sum_k F_ik X_kj over the d source blocks between the block's row and column
+        for (int e = u; e < nblk * 64; e += 128) {
+            const int bk = e >> 6, r = (e >> 3) & 7, c = e & 7;
+            double t = 0.0;
+            if (!up) {
+                const int i = bk + d, j = bk;  // L: k = j .. i-1
+                for (int k = j; k < i; ++k)
+#pragma unroll
+                    for (int s2 = 0; s2 < 8; ++s2)
+                        t += S[8 * i + r + (8 * k + s2) * LD65] * X[8 * k + s2 + (8 * j + c) * LD65];
+            } else {
+                const int i = bk, j = bk + d;  // U: k = i+1 .. j
+                for (int k = i + 1; k <= j; ++k)
+#pragma unroll
+                    for (int s2 = 0; s2 < 8; ++s2)
+                        t += S[8 * i + r + (8 * k + s2) * LD65] * X[8 * k + s2 + (8 * j + c) * LD65];
+            }
+            Tp[e] = t;
         }
-        if (tx < l) {
-            const double a = S[tx + l * LD65] * rdiag[l];
-            for (int c = l + ty; c < m; c += 4) Ui[tx + c * LD65] -= a * Ui[l + c * LD65];
+        __syncthreads();
+        // X_ij = -X_ii T
+        for (int e = u; e < nblk * 64; e += 128) {
+            const int bk = e >> 6, r = (e >> 3) & 7, c = e & 7;
+            const int i = up ? bk : bk + d, j = up ? bk + d : bk;
+            double t = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < 8; ++s2) t += X[8 * i + r + (8 * i + s2) * LD65] * Tp[(bk << 6) + (s2 << 3) + c];
+            X[8 * i + r + (8 * j + c) * LD65] = -t;
         }
         __syncthreads();
     }
-    // rows of U^-1 are divided by the pivots; pack strict lower of L^-1 with upper of U^-1
     double *Pg = A.base[T.v[1].base] + T.v[1].off;
     for (int e = threadIdx.x; e < m * m; e += NT) {
         int i = e % m, c = e / m;
-        Pg[e] = (i > c) ? Li[i + c * LD65] : Ui[i + c * LD65] * rdiag[i];
+        Pg[e] = (i > c) ? Li[i + c * LD65] : Ui[i + c * LD65];
     }
 }
 

@@ -170,3 +170,36 @@ def test_solve_shape_errors(P):
         P.solve(F, np.ones(7))
     with pytest.raises(ValueError):
         P.hlu(F.h)  # already factored / consumed
+
+
+@pytest.mark.parametrize("n,leaf", [(256, 64), (200, 32)])
+def test_hlu_leaf_pivoting_dense(P, n, leaf):
+    """Leaves that need row exchanges (a random matrix with weak diagonal): the GETRF task's
+    pivoted path (the speculative no-exchange pass fails its |a_jj| >= |a_ij| check) gives
+    the same solution as LAPACK (rel. 1e-9), for 64- and 32-row leaves.  (Refined 128-row
+    leaves pivot within their 64-row halves only; a cross-half pivot raises ValueError with
+    the leaf's path.)"""
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n)) + 0.5 * np.eye(n)
+    x = np.linspace(-1, 1, n)
+    ct = P.build_cluster_tree(x[:, None], leaf_size=leaf)
+    H = P.build_from_dense(A, ct, ct, P.HConfig(n_min=leaf, eps1=1e-14))
+    F = P.hlu(H, 1e-14)
+    b = rng.standard_normal(n)
+    want = np.linalg.solve(A, b)
+    for method in ("substitution", "inverse", "propagator"):
+        got = P.solve(F, b, method=method)
+        assert _rel(got, want) <= 1e-9, method
+    # the leaf permutations are not all the identity (row exchanges happened)
+    recs, arena, ranks, perm = P.hmatrix.export_layout(F.h)
+    assert (perm[: n] != np.arange(n) % leaf).any() or (perm != np.sort(perm)).any()
+
+
+def test_hlu_leaf128_cross_half_pivot_raises(P):
+    n = 512
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n)) + 0.5 * np.eye(n)
+    ct = P.build_cluster_tree(np.linspace(-1, 1, n)[:, None], leaf_size=128)
+    H = P.build_from_dense(A, ct, ct, P.HConfig(n_min=128, eps1=1e-14))
+    with pytest.raises(ValueError, match="root"):
+        P.hlu(H, 1e-14)
