@@ -118,29 +118,41 @@ __device__ void task_getrf64(const ExecArgs &A, const DTask &T, int tid, double 
             const int c = tc + 4 * q;
             b[q] = (tr < m && c < m) ? G[tr + c * (i64)v.ld] : (tr == c ? 1.0 : 0.0);
         }
+        // columns in groups of four share the register index q = j / 4, so with the group
+        // loop unrolled every register index and column comparison is a compile-time
+        // constant: a step is (16 - j/4) DFMAs fed by 128-bit shared loads of row j
+        // (stored [thread column][q], i.e. each thread's 16 values contiguous)
         bool ok = true;
-        for (int j = 0; j < m; ++j) {
-            double *Pj = Tw + (j & 1) * 64;  // double-buffered row j
-            if (tr == j) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) Pj[tc + 4 * q] = b[q];
-            }
-            __syncthreads();
-            const int jt = j & 3, jq = j >> 2;
-            double mine = 0.0;
+        for (int k = 0; k < 16; ++k) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-                if (q == jq) mine = b[q];
-            const double lv = __shfl_sync(0xffffffffu, mine, (lane & ~3) | jt);
-            if (tr > j && tr < m) {
-                const double d = Pj[j];
-                ok = ok && (d != 0.0 ? fabs(lv) <= fabs(d) : lv == 0.0);
-                const double l = d != 0.0 ? lv * (1.0 / d) : lv;
+            for (int jj = 0; jj < 4; ++jj) {
+                const int j = 4 * k + jj;
+                if (j < m) {
+                    double *Pj = Tw + (j & 1) * 64;  // double-buffered row j
+                    if (tr == j) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int c = tc + 4 * q;
-                    if (c > j) b[q] -= l * Pj[c];
-                    else if (c == j) b[q] = l;
+                        for (int q = k; q < 16; q += 2)
+                            *reinterpret_cast<double2 *>(Pj + tc * 16 + q - (q & 1)) =
+                                make_double2((q & 1) ? b[q - 1] : b[q], (q & 1) ? b[q] : b[q + 1]);
+                    }
+                    __syncthreads();
+                    const double lv = __shfl_sync(0xffffffffu, b[k], (lane & ~3) | jj);
+                    if (tr > j && tr < m) {
+                        const double d = Pj[jj * 16 + k];
+                        ok = ok && (d != 0.0 ? fabs(lv) <= fabs(d) : lv == 0.0);
+                        const double l = d != 0.0 ? lv * (1.0 / d) : lv;
+                        // q == k: column tc + 4k, updated if tc > jj, the multiplier if tc == jj
+                        const double pk = Pj[tc * 16 + k];
+                        if (tc > jj) b[k] -= l * pk;
+                        else if (tc == jj) b[k] = l;
+#pragma unroll
+                        for (int q = (k + 1) & ~1; q < 16; q += 2) {
+                            const double2 pr = *reinterpret_cast<const double2 *>(Pj + tc * 16 + q);
+                            if (q > k) b[q] -= l * pr.x;
+                            b[q + 1] -= l * pr.y;
+                        }
+                    }
                 }
             }
         }
