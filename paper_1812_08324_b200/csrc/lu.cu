@@ -1887,6 +1887,11 @@ struct SolvePlans {
     std::shared_ptr<MvPlan> mvL, mvU;
     std::shared_ptr<HMat> Z;        // propagator (A+)^{-1} = (L U)^{-1} on the full block tree
     std::shared_ptr<MvPlan> mvZ;
+    std::shared_ptr<HMat> ZS;       // Z with shared leaf bases (zshared.cu), single-RHS path
+    std::shared_ptr<MvPlan> mvZS;
+    double zs_stats[3] = {0, 0, 0};
+    const MvPlan &z1plan() const { return mvZS ? *mvZS : *mvZ; }
+    HMat &z1mat() const { return mvZS ? *ZS : *Z; }
     const HMat *pair_hm = nullptr;  // hminus last checked against 2I - A+
     bool pair_ok = false;
     int g_method = -1;
@@ -2036,6 +2041,8 @@ void prepare_inverse(Ctx &ctx, HMat &F, double eps2) {
 
 i64 compress_near_field(Ctx &ctx, HMat &H, double eps);
 i64 coarsen_hmat(Ctx &ctx, HMat &H, double eps);
+bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr<MvPlan> &plan,
+                        double *stats);
 
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.factored, LH_EINVAL, "prepare_propagator needs an H-LU factorization");
@@ -2097,6 +2104,17 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     }
     auto t3 = now();
     S.mvZ = build_mv_plan(*Z, Z->leafblocks, ctx.stream);
+    // shared leaf bases for the single-RHS step (zshared.cu)
+    if (!getenv("LEVYH_NO_SHARED_BASIS")) {
+        double sb_eps = 1e-2 * std::min(eps2, 1e-10);
+        if (const char *e = getenv("LEVYH_SB_EPS")) sb_eps = atof(e);
+        auto zs = std::make_shared<HMat>();
+        std::shared_ptr<MvPlan> pz;
+        if (build_shared_basis(ctx, *Z, sb_eps, *zs, pz, S.zs_stats)) {
+            S.ZS = zs;
+            S.mvZS = pz;
+        }
+    }
     if (getenv("LEVYH_PLAN_VERBOSE"))
         fprintf(stderr, "[levyh] propagator: alloc+upload %.3f s, exec %.3f s, free plan %.3f s, "
                         "near-field compression + coarsening %.3f s (%.0f leaves, %.0f merges), matvec plan "
@@ -2132,7 +2150,7 @@ static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
     }
     for (int q = 0; q < nrhs; ++q) {
         double *bq = b + (i64)q * ldb;
-        mv_run(*S.mvZ, *S.Z, bq, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
+        mv_run(S.z1plan(), S.z1mat(), bq, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
         LH_CUDA(cudaMemcpyAsync(bq, S.tmp, sizeof(double) * F.nrows, cudaMemcpyDeviceToDevice,
                                 ctx.stream));
     }
@@ -2156,8 +2174,8 @@ static bool cn_pair_ok(Ctx &ctx, SolvePlans &S, HMat &Hm, MvPlan &Pm) {
     double *w = dalloc<double>(4 * n);
     probe_fill_kernel<<<1024, NT, 0, ctx.stream>>>(w, n);
     mv_run(Pm, Hm, w, w + n, 1.0, 0.0, ctx.stream, ctx.num_sms);                  // A- x
-    mv_run(*S.mvZ, *S.Z, w + n, w + 2 * n, 1.0, 0.0, ctx.stream, ctx.num_sms);     // Z A- x
-    mv_run(*S.mvZ, *S.Z, w, w + 3 * n, 2.0, -1.0, ctx.stream, ctx.num_sms, w);     // 2 Z x - x
+    mv_run(S.z1plan(), S.z1mat(), w + n, w + 2 * n, 1.0, 0.0, ctx.stream, ctx.num_sms);  // Z A- x
+    mv_run(S.z1plan(), S.z1mat(), w, w + 3 * n, 2.0, -1.0, ctx.stream, ctx.num_sms, w);  // 2 Z x - x
     std::vector<double> h((size_t)2 * n);
     LH_CUDA(cudaMemcpyAsync(h.data(), w + 2 * n, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost,
                             ctx.stream));
@@ -2392,8 +2410,8 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
     };
     std::vector<Mv> mv;
     if (method == 2) {
-        S.Z->sync_ranks(ctx.stream);
-        mv.push_back({S.mvZ.get(), S.Z.get(), u, y, 2.0, -1.0, u});
+        S.z1mat().sync_ranks(ctx.stream);
+        mv.push_back({&S.z1plan(), &S.z1mat(), u, y, 2.0, -1.0, u});
     } else {
         S.XL->sync_ranks(ctx.stream);
         S.XU->sync_ranks(ctx.stream);
@@ -2447,10 +2465,11 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
         const auto bl = nonzero(*mv[q].H);
         mv_bytes(*mv[q].H, bl, out[6 + 2 * q], out[7 + 2 * q]);
         if (mv[q].z && mv[q].z != mv[q].y) out[7 + 2 * q] += 8.0 * mv[q].H->nrows;  // reads z
+        if (mv[q].P->cpl) out[6 + 2 * q] += (double)mv[q].P->cpl->bytes;  // coupling (phase 1 side)
     }
     out[12] = stored(Hm, Hm.leafblocks);
     if (method == 2) {
-        out[13] = stored(*S.Z, S.Z->leafblocks);
+        out[13] = stored(S.z1mat(), S.z1mat().leafblocks) + (S.mvZS ? S.zs_stats[1] : 0.0);
     } else {
         out[13] = stored(*S.XL, nonzero(*S.XL));
         out[14] = stored(*S.XU, nonzero(*S.XU));
@@ -2509,12 +2528,12 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                         mv_run(*S.mvL, *S.XL, y, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
                         mv_run(*S.mvU, *S.XU, S.tmp, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
                     } else if (shape == 2) {
-                        mv_run(*S.mvZ, *S.Z, uq, y, 2.0, -1.0, ctx.stream, ctx.num_sms, uq);
+                        mv_run(S.z1plan(), S.z1mat(), uq, y, 2.0, -1.0, ctx.stream, ctx.num_sms, uq);
                         LH_CUDA(cudaMemcpyAsync(uq, y, sizeof(double) * Hm.nrows,
                                                 cudaMemcpyDeviceToDevice, ctx.stream));
                     } else {
                         mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
-                        mv_run(*S.mvZ, *S.Z, y, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                        mv_run(S.z1plan(), S.z1mat(), y, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
                     }
                 } catch (...) {
                     cudaStreamEndCapture(ctx.stream, &g);
@@ -2581,7 +2600,7 @@ void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out
                      !getenv("LEVYH_NO_HOST_PIPE");
     if (pipelined) {
         MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
-        pipelined = cn_pair_ok(ctx, S, Hm, Pm) && S.mvZ->npiece > 0 && S.mvZ->nbatch > 0;
+        pipelined = cn_pair_ok(ctx, S, Hm, Pm) && S.z1plan().npiece > 0 && S.z1plan().nbatch > 0;
     }
     if (!pipelined) {
         LH_CUDA(cudaMemcpyAsync(S.hx, u_in, sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
@@ -2590,7 +2609,7 @@ void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out
         LH_CUDA(cudaStreamSynchronize(ctx.stream));
         return;
     }
-    const MvPlan &P = *S.mvZ;
+    const MvPlan &P = S.z1plan();
     if (!(S.hgraph && S.hg_in == u_in && S.hg_out == u_out && S.hg_hm == &Hm)) {
         if (S.hgraph) {
             cudaGraphExecDestroy(S.hgraph);

@@ -36,7 +36,7 @@ static i64 vchunk_rows() {
 #define SEG_MIN_BLOCKS 4        // CTAs per SM for the direct-load segment kernel
 #endif
 constexpr int TMA_STAGES = 5;
-constexpr int SLOT_D = 4096;    // doubles of operand data per ring slot (32 KB)
+constexpr int SLOT_D = 5120;    // doubles of operand data per ring slot (40 KB: a 64 x 64 dense leaf plus a basis of <= 16 columns)
 constexpr int SLOT_A = 1024;    // doubles of aux (descriptors, t_b span, x slice) per slot
 constexpr int DESC_D = 64;      // aux doubles reserved for piece descriptors (32 x 16 B)
 constexpr int MAX_PIECES = 32;  // pieces per batch
@@ -171,19 +171,35 @@ __global__ void __launch_bounds__(NT, VTX_MIN_BLOCKS)
     }
 }
 
-// t_b[c] = sum of the chunk partials of a multi-chunk block (one warp per block, fixed order)
+// t_b[c] = sum of the chunk partials of a multi-chunk block: one CTA per block, warp w sums
+// the chunks w, w + 8, ... (lane = column, four loads in flight), then warp 0 adds the eight
+// warp sums in order (deterministic)
 __global__ void treduce_kernel(const TJob *jobs, int njobs, const double *part, double *tvec) {
-    const int lane = threadIdx.x & 31;
-    for (int j = blockIdx.x * dev::NW + (threadIdx.x >> 5); j < njobs; j += gridDim.x * dev::NW) {
+    __shared__ double sm[dev::NW][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int j = blockIdx.x; j < njobs; j += gridDim.x) {
         const TJob J = jobs[j];
-        double mine = 0.0;
-        for (int c = 0; c < J.r; ++c) {
-            double t = 0.0;
-            for (int k = J.cbeg + lane; k < J.cend; k += 32) t += part[(i64)k * KC_MAX + c];
-            t = dev::warp_sum(t);
-            if (lane == c) mine = t;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (lane < J.r) {
+            const double *p = part + lane;
+            int k = J.cbeg + w;
+            for (; k + 3 * dev::NW < J.cend; k += 4 * dev::NW) {
+                a0 += p[(i64)k * KC_MAX];
+                a1 += p[(i64)(k + dev::NW) * KC_MAX];
+                a2 += p[(i64)(k + 2 * dev::NW) * KC_MAX];
+                a3 += p[(i64)(k + 3 * dev::NW) * KC_MAX];
+            }
+            for (; k < J.cend; k += dev::NW) a0 += p[(i64)k * KC_MAX];
         }
-        if (lane < J.r) tvec[(i64)J.blk * KC_MAX + lane] = mine;
+        sm[w][lane] = (a0 + a1) + (a2 + a3);
+        __syncthreads();
+        if (w == 0 && lane < J.r) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < dev::NW; ++q) s += sm[q][lane];
+            tvec[(i64)J.blk * KC_MAX + lane] = s;
+        }
+        __syncthreads();
     }
 }
 
@@ -504,6 +520,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
     std::vector<i64> vld, vld16;  // source ld (block row count of V) per chunk
     std::vector<TJob> tjobs;
     int nblk = 0, npart = 0;
+    P->blk_of_node.assign(H.nodes.size(), -1);
     for (int32_t b : blocks) {
         const Node &nd = H.nodes[b];
         if (nd.kind == K_DENSE || nd.kind == K_FDENSE) {
@@ -521,6 +538,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
             LH_REQUIRE(r <= KC_MAX, LH_EINTERNAL, "rank above the matvec capacity");
             if (r == 0) continue;
             const int blk = nblk++;
+            P->blk_of_node[b] = blk;
             // ranks above 8 are split into column groups of <= 8 (the rank-8 V^T x kernel
             // keeps twice the loads in flight per register of the rank-16 one)
             static const bool split = !getenv("LEVYH_VTX16");
@@ -535,7 +553,9 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
                 }
             };
             const i64 VCHUNK = vchunk_rows();
-            if (nd.n <= VCHUNK) {
+            if (nd.n == 0) {
+                // row-only node (shared row basis): t_b comes from the coupling kernels
+            } else if (nd.n <= VCHUNK) {
                 emit(0, (int)nd.n, -1);
             } else {
                 int cb = npart;
@@ -845,10 +865,8 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms,
         int g = std::max(1, std::min(vtx_grid<16>(num_sms), (P.nch16 + dev::NW - 1) / dev::NW));
         vtx_kernel<16><<<g, NT, 0, s>>>(P.chunks16, P.nch16, P.pbuf, x, P.part, P.tvec);
     }
-    if (P.ntj > 0) {
-        int g = std::max(1, std::min(148 * 8, (P.ntj + dev::NW - 1) / dev::NW));
-        treduce_kernel<<<g, NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
-    }
+    if (P.ntj > 0) treduce_kernel<<<std::min(P.ntj, 148 * 16), NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
+    if (P.cpl) coupling_launch(*P.cpl, P.tvec, P.tvec, s);
 }
 
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
@@ -917,10 +935,8 @@ void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y
                                             P.tvec);
         }
     }
-    if (P.ntj > 0) {
-        int g = std::max(1, std::min(148 * 8, (P.ntj + dev::NW - 1) / dev::NW));
-        treduce_kernel<<<g, NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
-    }
+    if (P.ntj > 0) treduce_kernel<<<std::min(P.ntj, 148 * 16), NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
+    if (P.cpl) coupling_launch(*P.cpl, P.tvec, P.tvec, s);
     const i64 n = P.tcol_len + P.nx + 2;
     int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
     tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x_dev, P.nx, P.xpad);
@@ -938,6 +954,11 @@ void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y
     LH_CUDA(cudaEventRecord(join, side));
     LH_CUDA(cudaStreamWaitEvent(s, join, 0));
     LH_CUDA(cudaGetLastError());
+}
+
+void treduce_launch(const TJob *jobs, int n, const double *part, double *out, cudaStream_t s) {
+    if (n <= 0) return;
+    treduce_kernel<<<std::min(n, 148 * 16), NT, 0, s>>>(jobs, n, part, out);
 }
 
 MvPlan &get_mv_plan(HMat &H, cudaStream_t s) {

@@ -57,8 +57,37 @@ struct PackJob {  // pbuf[dst + i + j * ld] = arena[src + i + j * src_ld], i < r
     int32_t ld, pad;
 };
 
+// Shared-leaf-basis coupling (zshared.cu): between phase 1 (x_hat_s = P_s^T x per column
+// leaf, computed by the V^T x kernel) and phase 2 (the segments stream Q_t with coefficients
+// y_hat_t), t_b = sum_s E_{s,b}^T x_hat_s per block and y_hat_t = sum_b C_{t,b} t_b per row leaf.
+struct CplChunk {  // t_b partial: rows [0, nrow) of E data at ebuf[e0 + row * r + c], x_hat via xidx
+    i64 e0;
+    int32_t nrow, r, out, x0;  // out >= 0: partial row index; < 0: -(1 + block) direct
+};
+struct CplRow {    // y_hat_t[i] = sum_g cbuf[e0 + i + g * k] * tb[tidx[t0 + g]], g < ncol; -> tvec row blk
+    i64 e0;
+    int32_t ncol, k, blk, t0;
+};
+struct Coupling {
+    int nchunk = 0, nrow = 0, ntj = 0, nb = 0;
+    CplChunk *chunks = nullptr;
+    int32_t *xidx = nullptr;  // tvec index of every E row (x_hat_s[l])
+    CplRow *rows = nullptr;
+    int32_t *tidx = nullptr;  // tb index of every C column (t_b[c])
+    TJob *tjobs = nullptr;
+    double *ebuf = nullptr, *cbuf = nullptr, *tb = nullptr, *part = nullptr;
+    double *xg = nullptr, *tg = nullptr;  // x_hat / t_b gathered in coefficient order
+    i64 nx = 0, nt = 0;
+    i64 bytes = 0;  // algorithmic bytes of the coupling data per application
+    ~Coupling();
+};
+void coupling_launch(const Coupling &C, const double *tvec_in, double *tvec_out, cudaStream_t s);
+void treduce_launch(const TJob *jobs, int n, const double *part, double *out, cudaStream_t s);
+
 struct MvPlan {
     int nseg = 0, nch = 0, nch16 = 0, ntj = 0, nbatch = 0, tma_grid = 0;
+    std::shared_ptr<Coupling> cpl;     // set for shared-leaf-basis operators
+    std::vector<int32_t> blk_of_node;  // tvec row of every low-rank node (-1 otherwise)
     double *pbuf = nullptr;  // packed operands
     i64 pbuf_len = 0;
     double *tvec = nullptr;  // t_b per low-rank block, KC_MAX per block
