@@ -181,9 +181,12 @@ int lh_prepare_inverse(lh_ctx *ctx, lh_hmat *factor, double eps2);
 /* Precompute the propagator Z = (LU)^-1 as an H-matrix on the factor's block tree
  * (L- then U-solve of the identity, eps2 recompression), used by method 2. */
 int lh_prepare_propagator(lh_ctx *ctx, lh_hmat *factor, double eps2);
-/* out[0..5] = propagator task count, planning seconds, temp bytes, executor seconds,
+/* out[0..9] = propagator task count, planning seconds, temp bytes, executor seconds,
  * off-diagonal dense leaves of Z stored low-rank after near-field compression, 2 x 2
- * low-rank sibling groups of Z merged by coarsening */
+ * low-rank sibling groups of Z merged by coarsening, the single-RHS form of Z (0 H-matrix,
+ * 1 shared leaf bases, 2 nested H2 bases), the relative error of that form against the
+ * H-matrix on a seeded probe vector, the mean leaf basis size, and the scalars of bases,
+ * transfers and couplings outside the dense leaves and row bases */
 int lh_propagator_stats(lh_hmat *factor, double *out_host);
 /* Kernel launches per CN step: kernel nodes of the step graph lh_cn_steps last captured
  * (methods 1 and 2), 0 before the first call. */

@@ -1890,6 +1890,7 @@ struct SolvePlans {
     std::shared_ptr<HMat> ZS;       // Z with shared leaf bases (zshared.cu), single-RHS path
     std::shared_ptr<MvPlan> mvZS;
     double zs_stats[3] = {0, 0, 0};
+    double zs_probe = 0.0;  // relative probe error of the single-RHS form against Z
     const MvPlan &z1plan() const { return mvZS ? *mvZS : *mvZ; }
     HMat &z1mat() const { return mvZS ? *ZS : *Z; }
     const HMat *pair_hm = nullptr;  // hminus last checked against 2I - A+
@@ -2043,6 +2044,34 @@ i64 compress_near_field(Ctx &ctx, HMat &H, double eps);
 i64 coarsen_hmat(Ctx &ctx, HMat &H, double eps);
 bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr<MvPlan> &plan,
                         double *stats);
+bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_ptr<MvPlan> &plan,
+              double *stats);
+
+// relative 2-norm difference of two matvec plans of the same operator on a seeded probe vector
+static double probe_rel_err(Ctx &ctx, const MvPlan &Pa, HMat &Ha, const MvPlan &Pb, HMat &Hb) {
+    const i64 n = Ha.ncols;
+    std::vector<double> x(n);
+    uint64_t st = 0x9E3779B97F4A7C15ull;
+    for (i64 i = 0; i < n; ++i) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        x[i] = (double)(st >> 11) * 0x1.0p-53 - 0.5;
+    }
+    double *d = dalloc<double>(3 * n);
+    LH_CUDA(cudaMemcpyAsync(d, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
+    mv_run(Pa, Ha, d, d + n, 1.0, 0.0, ctx.stream, ctx.num_sms);
+    mv_run(Pb, Hb, d, d + 2 * n, 1.0, 0.0, ctx.stream, ctx.num_sms);
+    std::vector<double> ya(n), yb(n);
+    LH_CUDA(cudaMemcpyAsync(ya.data(), d + n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+    LH_CUDA(cudaMemcpyAsync(yb.data(), d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaFree(d);
+    double num = 0.0, den = 0.0;
+    for (i64 i = 0; i < n; ++i) {
+        num += (ya[i] - yb[i]) * (ya[i] - yb[i]);
+        den += ya[i] * ya[i];
+    }
+    return den > 0.0 ? std::sqrt(num / den) : std::sqrt(num);
+}
 
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.factored, LH_EINVAL, "prepare_propagator needs an H-LU factorization");
@@ -2104,8 +2133,25 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     }
     auto t3 = now();
     S.mvZ = build_mv_plan(*Z, Z->leafblocks, ctx.stream);
-    // shared leaf bases for the single-RHS step (zshared.cu)
-    if (!getenv("LEVYH_NO_SHARED_BASIS")) {
+    // nested (H2) bases for the single-RHS step (zshared.cu), checked against the H-form of Z
+    // on a probe vector; else shared leaf bases
+    if (!getenv("LEVYH_NO_H2")) {
+        double sb_eps = 1e-2 * std::min(eps2, 1e-10);
+        if (const char *e = getenv("LEVYH_SB_EPS")) sb_eps = atof(e);
+        const int split = getenv("LEVYH_H2_SPLIT") ? atoi(getenv("LEVYH_H2_SPLIT")) : -1;  // -1: automatic
+        auto zs = std::make_shared<HMat>();
+        std::shared_ptr<MvPlan> pz;
+        if (build_h2(ctx, *Z, sb_eps, split, *zs, pz, S.zs_stats)) {
+            const double err = probe_rel_err(ctx, *S.mvZ, *Z, *pz, *zs);
+            if (getenv("LEVYH_PLAN_VERBOSE")) fprintf(stderr, "[levyh] H2 probe: relative error %.3e\n", err);
+            if (err <= 1e-10) {
+                S.ZS = zs;
+                S.mvZS = pz;
+                S.zs_probe = err;
+            }
+        }
+    }
+    if (!S.mvZS && !getenv("LEVYH_NO_SHARED_BASIS")) {
         double sb_eps = 1e-2 * std::min(eps2, 1e-10);
         if (const char *e = getenv("LEVYH_SB_EPS")) sb_eps = atof(e);
         auto zs = std::make_shared<HMat>();
@@ -2133,6 +2179,10 @@ void propagator_stats(HMat &F, double *out) {
     SolvePlans &S = plans_of(F);
     LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
     for (int k = 0; k < 6; ++k) out[k] = S.Z->lu_stats[k];
+    out[6] = S.mvZS ? (S.mvZS->h2 ? 2.0 : 1.0) : 0.0;
+    out[7] = S.zs_probe;
+    out[8] = S.zs_stats[0];
+    out[9] = S.zs_stats[1];
 }
 
 static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
@@ -2466,6 +2516,7 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
         mv_bytes(*mv[q].H, bl, out[6 + 2 * q], out[7 + 2 * q]);
         if (mv[q].z && mv[q].z != mv[q].y) out[7 + 2 * q] += 8.0 * mv[q].H->nrows;  // reads z
         if (mv[q].P->cpl) out[6 + 2 * q] += (double)mv[q].P->cpl->bytes;  // coupling (phase 1 side)
+        if (mv[q].P->h2) out[6 + 2 * q] += (double)mv[q].P->h2->bytes;  // H2 walk (phase 1 side)
     }
     out[12] = stored(Hm, Hm.leafblocks);
     if (method == 2) {

@@ -211,7 +211,7 @@ MmBufs mm_bufs(Ctx &ctx, const MvPlan &P, i64 ldk) {
 // Y = alpha H X + beta Z, all row-major with ldk = mm_pad(K) (columns >= K are don't-care)
 void mm_run(const MvPlan &P, const double *X, double *Y, i64 ldk, double alpha, double beta,
             const double *Z, double *T, double *part, cudaStream_t s) {
-    LH_REQUIRE(!P.cpl, LH_EINTERNAL, "the multi-RHS matmat runs on the H-form plan");
+    LH_REQUIRE(!P.cpl && !P.h2, LH_EINTERNAL, "the multi-RHS matmat runs on the H-form plan");
     const unsigned nk = (unsigned)(ldk / MM_N);
     if (P.nch > 0) vtx_mm_kernel<<<dim3(P.nch, nk), NT, 0, s>>>(P.chunks, P.pbuf, X, ldk, T, part);
     if (P.nch16 > 0)

@@ -353,7 +353,7 @@ constexpr int MAXK = 128;  // columns per batch (segments of < 32 rows would all
 struct TmaSmem {
     double data[TMA_STAGES][SLOT_D];
     double aux[TMA_STAGES][TOFF + MAXK];
-    double red[TGRP][SEG];
+    double red[2][TGRP][SEG];  // double-buffered: one consumer barrier per segment
     uint64_t full[TMA_STAGES], empty[TMA_STAGES];
     int32_t hdr[TMA_STAGES][4];  // K, kd, xadj
 };
@@ -418,6 +418,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     SegDesc sd = s0 < s1 ? segs[s0] : SegDesc{};
     for (int s = s0; s < s1; ++s) {
         const SegDesc cur = sd;
+        // z row issued now, consumed after the batches: its latency hides behind them
+        const double zv = (g == 0 && beta != 0.0 && row < cur.rows) ? z[cur.y0 + row] : 0.0;
         if (s + 1 < s1) sd = segs[s + 1];  // prefetch
         const int ld = cur.ld;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -461,15 +463,15 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                 phase ^= 1;
             }
         }
-        S.red[g][row] = (a0 + a1) + (a2 + a3);
+        double(*red)[SEG] = S.red[(s - s0) & 1];
+        red[g][row] = (a0 + a1) + (a2 + a3);
         consumer_sync();
         if (g == 0 && row < cur.rows) {
-            double v = S.red[0][row];
-            for (int q = 1; q < TGRP; ++q) v += S.red[q][row];
-            const i64 i = cur.y0 + row;
-            y[i] = (beta == 0.0 ? 0.0 : beta * z[i]) + alpha * v;
+            double v = red[0][row];
+#pragma unroll
+            for (int q = 1; q < TGRP; ++q) v += red[q][row];
+            y[cur.y0 + row] = (beta == 0.0 ? 0.0 : beta * zv) + alpha * v;
         }
-        consumer_sync();
     }
 }
 
@@ -867,6 +869,7 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms,
     }
     if (P.ntj > 0) treduce_kernel<<<std::min(P.ntj, 148 * 16), NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
     if (P.cpl) coupling_launch(*P.cpl, P.tvec, P.tvec, s);
+    if (P.h2) h2_launch(*P.h2, x, P.tvec, s);
 }
 
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
@@ -937,6 +940,7 @@ void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y
     }
     if (P.ntj > 0) treduce_kernel<<<std::min(P.ntj, 148 * 16), NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
     if (P.cpl) coupling_launch(*P.cpl, P.tvec, P.tvec, s);
+    if (P.h2) h2_launch(*P.h2, x_dev, P.tvec, s);
     const i64 n = P.tcol_len + P.nx + 2;
     int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
     tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x_dev, P.nx, P.xpad);

@@ -82,11 +82,67 @@ struct Coupling {
     ~Coupling();
 };
 void coupling_launch(const Coupling &C, const double *tvec_in, double *tvec_out, cudaStream_t s);
+
+// Nested (H2) cluster bases for Z (zshared.cu: build_h2).  Every cluster tau of the column
+// tree carries x_hat_tau = Pnest_tau^T x, computed bottom-up (leaf: P_s^T x_s; internal: Tc_tau^T
+// [x_hat_c1; x_hat_c2]); every block b = (rho, sigma) is a k_rho x k_sigma coupling S_b; the row
+// tree is walked top-down, y_hat_c = sum_{b: rho(b) = c} S_b x_hat_sigma(b) + Tr_p[c rows] y_hat_p,
+// and y_hat of a row leaf is the coefficient of its basis Q_t in the segment kernel.
+// Both walks are cut at subtrees of height <= split: one CTA per subtree, the column subtrees
+// finish the top of the tree by last-arrival climbing, every row subtree walks its own path
+// from the top.
+struct H2Leaf {  // xh[xoff + j] = sum_i pb[poff + i + 64 j] x[x0 + i], i < rows, j < k
+    i64 poff, x0;
+    int32_t rows, k, xoff, pad;
+};
+struct H2Up {  // xh[xoff + j] = sum_i tu[toff + i k + j] [xh[xoff1 ..+k1]; xh[xoff2 ..+k2]]_i
+    i64 toff;
+    int32_t k, k1, k2, xoff, xoff1, xoff2, parent, pad;  // parent: H2Up index, -1 none
+};
+struct H2Down {  // y = sum_{e in [c0, c1)} S_e x_hat + td[toff + roff + i + j ldt] y_parent[j], j < kp
+    i64 toff;
+    int32_t ldt, roff, kp, k, yoff, yoffp, c0, c1, out, pad;  // yoffp < 0: parent = path end
+};                     // (yoff: the node's y_hat slot, subtree nodes only; out: tvec row of a leaf)
+struct H2Cpl {  // w[i] += sum_j sb[soff + i + j kr] xh[xoff + j], j < kc
+    i64 soff;
+    int32_t kr, kc, xoff, pad;
+};
+struct H2Sub {  // a subtree's transfer matrices [tbeg, tbeg + tlen) are staged in shared memory;
+                // its x_hat / y_hat entries are [base, base + ...) locally
+    i64 tbeg;
+    int32_t tlen, base;
+};
+struct H2 {
+    int nsub_up = 0, nsub_dn = 0, maxh_up = 0, maxh_dn = 0, split = 0;
+    H2Leaf *leaves = nullptr;
+    H2Up *ups = nullptr;
+    H2Down *dns = nullptr;
+    H2Cpl *cpls = nullptr;
+    int32_t *up_lv = nullptr;    // nsub_up x (maxh_up + 1): ups ranges by height
+    int32_t *cnt = nullptr;      // arrival counters per H2Up (zero between launches)
+    H2Sub *up_sub = nullptr, *dn_sub = nullptr;
+    int32_t *dn_path = nullptr;  // path node ids (H2Down) per row subtree, top-down
+    int32_t *dn_pbeg = nullptr;  // nsub_dn + 1
+    int32_t *dn_lv = nullptr;    // nsub_dn x (maxh_dn + 2): subtree nodes by depth, top-down
+    double *pb = nullptr, *tu = nullptr, *td = nullptr, *sb = nullptr;
+    double *xh = nullptr;
+    double *wg = nullptr;          // couplings w of every row cluster (at its yoff)
+    int4 *crec = nullptr;          // row clusters with couplings: {c0, c1, k, slot}
+    int32_t *up_chain = nullptr, *up_cbeg = nullptr;  // climb chain (H2Up ids) per column subtree
+    int32_t *up_xcnt = nullptr, *dn_ycnt = nullptr;  // x_hat / y_hat slots per subtree
+    int nleaf = 0, ncnode = 0;
+    int up_tmax = 0, up_xmax = 0, dn_tmax = 0, dn_ymax = 0;  // staged doubles per CTA
+    int maxpath = 0;
+    i64 bytes = 0;  // algorithmic bytes per application (P, transfers, couplings)
+    ~H2();
+};
+void h2_launch(const H2 &h, const double *x, double *tvec, cudaStream_t s);
 void treduce_launch(const TJob *jobs, int n, const double *part, double *out, cudaStream_t s);
 
 struct MvPlan {
     int nseg = 0, nch = 0, nch16 = 0, ntj = 0, nbatch = 0, tma_grid = 0;
     std::shared_ptr<Coupling> cpl;     // set for shared-leaf-basis operators
+    std::shared_ptr<H2> h2;            // set for nested-basis (H2) operators
     std::vector<int32_t> blk_of_node;  // tvec row of every low-rank node (-1 otherwise)
     double *pbuf = nullptr;  // packed operands
     i64 pbuf_len = 0;

@@ -16,6 +16,7 @@
 // columns (and vice versa), so the Frobenius residual of the gathered matrix bounds the error
 // of every block's product, and it is truncated at eps relative to the leaf's row block.
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <numeric>
 
@@ -48,9 +49,10 @@ constexpr int KQ = 32;     // basis capacity per leaf (the low-rank column capac
 constexpr int LR = 64;     // leaf rows
 constexpr int MAXC = 368;  // gathered columns per leaf (shared memory)
 
-struct GPiece {  // gathered columns [col0, col0 + r): src[off + i + c * ld] * wts[woff + c]
+struct GPiece {  // M[row0 + i, col0 + c] = src[off + i + c * ld] * wts[woff + c], i < nr, c < r
     i64 off, ld, woff;
     int32_t r, col0;
+    int32_t row0, nr;  // row0 > 0 only for the second child's rows of a nested (H2) basis
 };
 struct BJob {  // one leaf: rows, pieces [p0, p1), total columns
     int32_t rows, p0, p1, ncol;
@@ -61,7 +63,7 @@ struct CopyJob {  // dst[d0 + i * dsi + c * dsc] = src[s0 + i * ssi + c * ssc], 
     int32_t ni, nc;
 };
 
-constexpr size_t BASIS_SMEM = sizeof(double) * ((size_t)LR * MAXC + MAXC + LR * KQ + KQ + 2 * NW + 8);
+constexpr size_t BASIS_SMEM = sizeof(double) * ((size_t)LR * MAXC + 2 * MAXC + LR * KQ + KQ + 2 * NW + 8);
 
 // column norms of every low-rank block's U and V (the weights)
 __global__ void colnorm_kernel(const i64 *off, const i64 *len, int n, const double *arena, double *out) {
@@ -75,13 +77,15 @@ __global__ void colnorm_kernel(const i64 *off, const i64 *len, int n, const doub
     }
 }
 
+// kout[j] = basis size, or -1 when KQ columns do not reach the tolerance
 __global__ void __launch_bounds__(NT) basis_kernel(const BJob *jobs, int njobs, const GPiece *pieces,
                                                    const double *arena, const double *wts, double eps,
                                                    int *kout, double *Qt, double *Ct) {
     extern __shared__ double4 smem_raw[];
     double *M = reinterpret_cast<double *>(smem_raw);  // LR x MAXC, ld LR
     double *res = M + (size_t)LR * MAXC;                // column residual norms^2
-    double *Vr = res + MAXC;                            // reflectors, LR x KQ
+    double *wcol = res + MAXC;                          // weight of every gathered column
+    double *Vr = wcol + MAXC;                           // reflectors, LR x KQ
     double *beta = Vr + LR * KQ;
     double *red = beta + KQ;
     __shared__ int s_p;
@@ -94,17 +98,20 @@ __global__ void __launch_bounds__(NT) basis_kernel(const BJob *jobs, int njobs, 
         __syncthreads();
         for (int p = J.p0; p < J.p1; ++p) {
             const GPiece G = pieces[p];
-            for (int e = threadIdx.x; e < rows * G.r; e += NT) {
-                const int i = e % rows, c = e / rows;
-                M[i + (G.col0 + c) * LR] = arena[G.off + i + (i64)c * G.ld] * wts[G.woff + c];
+            for (int e = threadIdx.x; e < G.nr * G.r; e += NT) {
+                const int i = e % G.nr, c = e / G.nr;
+                M[G.row0 + i + (G.col0 + c) * LR] = arena[G.off + i + (i64)c * G.ld] * wts[G.woff + c];
             }
+            if (G.row0 == 0)
+                for (int c = threadIdx.x; c < G.r; c += NT) wcol[G.col0 + c] = wts[G.woff + c];
         }
         __syncthreads();
         double tot = 0.0;
         for (int e = threadIdx.x; e < LR * nc; e += NT) tot += M[e] * M[e];
         tot = dev::block_sum(tot, red);
         int k = 0;
-        for (; k < KQ && k < rows; ++k) {
+        bool fail = false;
+        for (;; ++k) {
             // residual column norms over rows k..rows-1
             double rem = 0.0;
             for (int j = threadIdx.x; j < nc; j += NT) {
@@ -115,6 +122,10 @@ __global__ void __launch_bounds__(NT) basis_kernel(const BJob *jobs, int njobs, 
             }
             rem = dev::block_sum(rem, red);
             if (!(rem > eps * eps * tot)) break;
+            if (k == KQ || k == rows) {
+                fail = k < rows;
+                break;
+            }
             // pivot: largest residual column (first on ties)
             if (threadIdx.x < 32) {
                 double best = -1.0;
@@ -160,18 +171,10 @@ __global__ void __launch_bounds__(NT) basis_kernel(const BJob *jobs, int njobs, 
         // coefficients: the first k rows of H M, unweighted
         for (int e = threadIdx.x; e < k * nc; e += NT) {
             const int i = e % k, j = e / k;
-            Ct[J.cout + i + (i64)j * KQ] = M[i + j * LR];
+            const double w = wcol[j];
+            Ct[J.cout + i + (i64)j * KQ] = w > 0.0 ? M[i + j * LR] / w : 0.0;
         }
         __syncthreads();
-        for (int p = J.p0; p < J.p1; ++p) {
-            const GPiece G = pieces[p];
-            for (int e = threadIdx.x; e < k * G.r; e += NT) {
-                const int i = e % k, c = e / k;
-                const double w = wts[G.woff + c];
-                double *dst = Ct + J.cout + i + (i64)(G.col0 + c) * KQ;
-                *dst = w > 0.0 ? *dst / w : 0.0;
-            }
-        }
         // Q = H_0 ... H_{k-1} [I; 0] (reuse M)
         for (int e = threadIdx.x; e < LR * k; e += NT) M[e] = ((e % LR) == (e / LR)) ? 1.0 : 0.0;
         __syncthreads();
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(NT) basis_kernel(const BJob *jobs, int njobs, 
             const int i = e % rows, c = e / rows;
             Qt[J.qout + i + (i64)c * rows] = M[i + c * LR];
         }
-        if (threadIdx.x == 0) kout[jb] = k;
+        if (threadIdx.x == 0) kout[jb] = fail ? -1 : k;
         __syncthreads();
     }
 }
@@ -401,10 +404,11 @@ bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr
             for (auto &pc : side[sd].cover[l]) {
                 const Node &nd = Z.nodes[lr[pc.first]];
                 const int r = Z.h_ranks[nd.rslot];
+                const int32_t nr = (int32_t)(lo[l + 1] - lo[l]);
                 if (sd == 0)
-                    pieces.push_back({nd.uoff + (lo[l] - nd.r0), nd.m, woff[pc.first] + r, r, pc.second});
+                    pieces.push_back({nd.uoff + (lo[l] - nd.r0), nd.m, woff[pc.first] + r, r, pc.second, 0, nr});
                 else
-                    pieces.push_back({nd.voff + (lo[l] - nd.c0), nd.n, woff[pc.first], r, pc.second});
+                    pieces.push_back({nd.voff + (lo[l] - nd.c0), nd.n, woff[pc.first], r, pc.second, 0, nr});
             }
             J.p1 = (int32_t)pieces.size();
             qlen += (i64)J.rows * KQ;
@@ -431,6 +435,11 @@ bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr
     std::vector<int> k(njobs);
     LH_CUDA(cudaMemcpy(k.data(), dk, sizeof(int) * njobs, cudaMemcpyDeviceToHost));
     cudaFree(dk);
+    if (std::any_of(k.begin(), k.end(), [](int v) { return v < 0; })) {
+        cudaFree(Qt);
+        cudaFree(Ct);
+        return false;  // a basis above KQ columns
+    }
     // ---- ZS: dense leaves of Z, then row-basis nodes, then column-basis nodes
     ZS.rt = Z.rt;
     ZS.ct = Z.ct;
@@ -612,6 +621,903 @@ bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr
         stats[1] = (double)(elen + cl);       // coupling scalars
         stats[2] = (double)aoff;              // dense + bases scalars
     }
+    return true;
+}
+
+
+// ===========================================================================
+// Nested (H2) cluster bases (matvec.h: H2).  The leaf bases above become the bottom level of a
+// nested basis: an internal cluster tau's basis is [Q_c1 0; 0 Q_c2] T_tau, with T_tau from the same
+// truncated column-pivoted QR applied to the stacked child coefficients [C_{c1,b}; C_{c2,b}] of
+// every block b covering tau (weighted as at the leaves).  A block b = (rho, sigma) is then the
+// small coupling S_b = C_{rho,b} E_{sigma,b}^T, so a matvec streams the dense diagonal leaves,
+// the leaf bases, the transfer matrices and the couplings: no per-leaf coefficient of a large
+// block is stored any more.
+// ===========================================================================
+H2::~H2() {
+    for (void *p : {(void *)leaves, (void *)ups, (void *)dns, (void *)cpls, (void *)up_lv, (void *)cnt, (void *)up_sub, (void *)dn_sub, (void *)dn_path, (void *)dn_pbeg,
+                    (void *)dn_lv, (void *)pb, (void *)tu, (void *)td, (void *)sb, (void *)xh, (void *)wg,
+                    (void *)crec, (void *)up_chain, (void *)up_cbeg, (void *)up_xcnt, (void *)dn_ycnt})
+        cudaFree(p);
+}
+
+namespace {
+
+constexpr int H2_MAXP = 24;     // path length (top clusters above a row subtree)
+constexpr unsigned FULL = 0xffffffffu;
+
+// x_hat of one column leaf: lanes hold rows lane and lane + 32, one warp sum per basis column
+__device__ __forceinline__ double h2_leaf(const H2Leaf &L, const double *pb, const double *x, int lane) {
+    const double *P = pb + L.poff;
+    const double x0 = lane < L.rows ? x[L.x0 + lane] : 0.0;
+    const double x1 = lane + 32 < L.rows ? x[L.x0 + lane + 32] : 0.0;
+    double mine = 0.0;
+    for (int c = 0; c < L.k; c += 8) {
+        double p[8], q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const bool ok = c + u < L.k;
+            p[u] = ok ? P[lane + 64 * (c + u)] : 0.0;
+            q[u] = ok ? P[lane + 32 + 64 * (c + u)] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double v = dev::warp_sum(fma(p[u], x0, q[u] * x1));
+            if (lane == c + u) mine = v;
+        }
+    }
+    return mine;  // lane j < L.k holds x_hat[j]
+}
+
+// y[j] = sum_i T[i * ldi + j * ldj] v[i], i < n, for lane j (act); v[i] held by lane i; T in shared memory
+__device__ __forceinline__ double h2_apply_s(const double *T, int ldi, int n, double v, bool act) {
+    double a0 = 0.0, a1 = 0.0;
+    int i = 0;
+    for (; i + 1 < n; i += 2) {
+        const double t0 = act ? T[i * ldi] : 0.0, t1 = act ? T[(i + 1) * ldi] : 0.0;
+        a0 = fma(t0, __shfl_sync(FULL, v, i), a0);
+        a1 = fma(t1, __shfl_sync(FULL, v, i + 1), a1);
+    }
+    if (i < n) a0 = fma(act ? T[i * ldi] : 0.0, __shfl_sync(FULL, v, i), a0);
+    return a0 + a1;
+}
+// the same with T in global memory: all loads issued before the first FMA
+__device__ __forceinline__ double h2_apply_g(const double *T, i64 ldi, int n, double v, bool act) {
+    double t[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t[i] = (act && i < n) ? T[i * ldi] : 0.0;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+        a0 = fma(t[i], __shfl_sync(FULL, v, i), a0);
+        a1 = fma(t[i + 1], __shfl_sync(FULL, v, i + 1), a1);
+    }
+    return a0 + a1;
+}
+
+// couplings of one row cluster, w[i] = sum_e S_e x_hat_e, lane i < k
+__device__ __forceinline__ double h2_couple(const H2Down &D, const H2Cpl *cpls, const double *sb,
+                                            const double *xh, int lane) {
+    double acc = 0.0;
+    for (int e = D.c0; e < D.c1; ++e) {
+        const H2Cpl C = cpls[e];
+        const double xv = lane < C.kc ? __ldcg(xh + C.xoff + lane) : 0.0;
+        acc += h2_apply_g(sb + C.soff + lane, C.kr, C.kc, xv, lane < D.k);
+    }
+    return acc;
+}
+
+// x_hat of every column leaf: one warp per leaf, all CTAs resident (bandwidth-bound: P streams once)
+__global__ void __launch_bounds__(NT) h2_leaf_kernel(const H2Leaf *leaves, int n, const double *pb, const double *x,
+                                                    double *xh) {
+    const int lane = threadIdx.x & 31;
+    for (int l = blockIdx.x * NW + (threadIdx.x >> 5); l < n; l += gridDim.x * NW) {
+        const H2Leaf L = leaves[l];
+        const double v = h2_leaf(L, pb, x, lane);
+        if (lane < L.k) xh[L.xoff + lane] = v;
+    }
+}
+
+// Column walk above the leaves: one CTA per subtree (x_hat of its nodes kept in shared memory,
+// levels by height, one memory round trip per level), then the top of the tree by
+// last-arrival climbing: the second child to finish computes the parent (warp 0 only).
+constexpr int H2_MAXN = 128;  // staged node descriptors per subtree
+__global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int32_t *up_lv, const int32_t *up_chain,
+                                                      const int32_t *up_cbeg, const H2Sub *sub, const int32_t *up_xcnt,
+                                                      int32_t *cnt, int maxh, const double *tu, double *xh) {
+    extern __shared__ __align__(16) double h2s[];
+    double *xs = h2s;
+    __shared__ H2Up su[H2_MAXN];
+    __shared__ H2Up sc[H2_MAXP];
+    const int s = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const H2Sub SB = sub[s];
+    const int32_t *lv = up_lv + (i64)s * (maxh + 1);
+    const int u0 = lv[0], nu = lv[maxh] - u0, c0 = up_cbeg[s], nc = up_cbeg[s + 1] - c0;
+    {  // descriptors (subtree + climb chain) and x_hat slots to shared memory; transfers to L2
+        const int32_t *src = reinterpret_cast<const int32_t *>(ups + u0);
+        int32_t *dst = reinterpret_cast<int32_t *>(su);
+        constexpr int W = (int)(sizeof(H2Up) / 4);
+        for (int i = threadIdx.x; i < nu * W; i += NT) dst[i] = src[i];
+        for (int i = threadIdx.x; i < nc * W; i += NT)
+            reinterpret_cast<int32_t *>(sc)[i] = reinterpret_cast<const int32_t *>(ups + up_chain[c0 + i / W])[i % W];
+        const int nx = up_xcnt[s];
+        for (int i = threadIdx.x; i < nx; i += NT) xs[i] = xh[SB.base + i];
+        const char *t = reinterpret_cast<const char *>(tu + SB.tbeg);
+        for (i64 o = 128 * (i64)threadIdx.x; o < 8 * (i64)SB.tlen; o += 128 * NT)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
+    }
+    __syncthreads();
+    for (int q = w; q < nc; q += NW) {  // the climb's transfers to L2
+        const char *t = reinterpret_cast<const char *>(tu + sc[q].toff);
+        const int bytes = 8 * (sc[q].k1 + sc[q].k2) * sc[q].k;
+        for (int o = 128 * lane; o < bytes; o += 128 * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
+    }
+    for (int hh = 0; hh < maxh; ++hh) {
+        const int a = lv[hh] - u0, b = lv[hh + 1] - u0;
+        if (a == b) continue;
+        for (int u = a + w; u < b; u += NW) {
+            const H2Up &U = su[u];
+            const double *T = tu + U.toff + lane;
+            const double xa = lane < U.k1 ? xs[U.xoff1 - SB.base + lane] : 0.0;
+            const double xb = lane < U.k2 ? xs[U.xoff2 - SB.base + lane] : 0.0;
+            const bool act = lane < U.k;
+            const double v = h2_apply_g(T, U.k, U.k1, xa, act) + h2_apply_g(T + (i64)U.k1 * U.k, U.k, U.k2, xb, act);
+            if (act) {
+                xh[U.xoff + lane] = v;
+                xs[U.xoff - SB.base + lane] = v;
+            }
+        }
+        __syncthreads();
+    }
+    if (w != 0) return;
+    for (int q = 0; q < nc; ++q) {
+        const int p = up_chain[c0 + q];
+        const H2Up &U = sc[q];
+        __syncwarp();
+        int old = 0;
+        if (lane == 0) {
+            int32_t *c = cnt + p;
+            asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(c), "r"(1) : "memory");
+        }
+        old = __shfl_sync(FULL, old, 0);
+        if (old == 0) return;
+        if (lane == 0) cnt[p] = 0;  // ready for the next application
+        const double xa = lane < U.k1 ? __ldcg(xh + U.xoff1 + lane) : 0.0;
+        const double xb = lane < U.k2 ? __ldcg(xh + U.xoff2 + lane) : 0.0;
+        const bool act = lane < U.k;
+        const double *T = tu + U.toff + lane;
+        const double v = h2_apply_g(T, U.k, U.k1, xa, act) + h2_apply_g(T + (i64)U.k1 * U.k, U.k, U.k2, xb, act);
+        if (act) xh[U.xoff + lane] = v;
+    }
+}
+
+// couplings of every row cluster: w[yoff + i] = sum_e S_e x_hat_e (one warp per cluster)
+__device__ __forceinline__ double h2_apply_g16(const double *T, i64 ldi, int n, double v, bool act) {
+    double a0 = 0.0, a1 = 0.0;
+    for (int b = 0; b < n; b += 16) {
+        double t[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) t[i] = (act && b + i < n) ? T[(b + i) * ldi] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+            a0 = fma(t[i], __shfl_sync(FULL, v, (b + i) & 31), a0);
+            a1 = fma(t[i + 1], __shfl_sync(FULL, v, (b + i + 1) & 31), a1);
+        }
+    }
+    return a0 + a1;
+}
+__global__ void __launch_bounds__(NT, 4) h2_couple_kernel(const int4 *crec, int n, const H2Cpl *cpls,
+                                                         const double *sb, const double *xh, double *wg) {
+    const int lane = threadIdx.x & 31;
+    for (int q = blockIdx.x * NW + (threadIdx.x >> 5); q < n; q += gridDim.x * NW) {
+        const int4 R = crec[q];  // couplings [x, y), k = z, slot w
+        double acc = 0.0;
+        for (int e = R.x; e < R.y; ++e) {
+            const H2Cpl C = cpls[e];
+            const double xv = lane < C.kc ? __ldcg(xh + C.xoff + lane) : 0.0;
+            acc += h2_apply_g16(sb + C.soff + lane, C.kr, C.kc, xv, lane < R.z);
+        }
+        if (lane < R.z) wg[R.w + lane] = acc;
+    }
+}
+
+// Row walk: one CTA per subtree.  The transfers down the path above the subtree (one warp),
+// then the subtree's levels (y_hat kept in shared memory, one round trip per level).
+__global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const int32_t *dn_path,
+                                                        const int32_t *dn_pbeg, const int32_t *dn_lv,
+                                                        const H2Sub *sub, const int32_t *dn_ycnt, int maxh, int ymax,
+                                                        const double *td, const double *wg, double *tvec) {
+    extern __shared__ __align__(16) double h2s[];
+    double *ws = h2s, *ys = ws + ymax;
+    __shared__ double pw[H2_MAXP][KC_MAX];
+    __shared__ H2Down pd[H2_MAXP];
+    const int s = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const H2Sub SB = sub[s];
+    const int pa = dn_pbeg[s], np = dn_pbeg[s + 1] - pa;
+    const int32_t *lv = dn_lv + (i64)s * (maxh + 2);
+    __shared__ H2Down sd[H2_MAXN];
+    const int n0 = lv[0], nn = lv[maxh + 1] - n0;
+    {
+        const int32_t *src = reinterpret_cast<const int32_t *>(dns + n0);
+        int32_t *dst = reinterpret_cast<int32_t *>(sd);
+        for (int i = threadIdx.x; i < nn * (int)(sizeof(H2Down) / 4); i += NT) dst[i] = src[i];
+        const int ny = dn_ycnt[s];
+        for (int i = threadIdx.x; i < ny; i += NT) ws[i] = wg[SB.base + i];
+        for (int q = w; q < np; q += NW) {
+            const H2Down D = dns[dn_path[pa + q]];
+            if (lane < D.k) pw[q][lane] = wg[D.yoff + lane];
+            if (lane == 0) pd[q] = D;
+        }
+        const char *t = reinterpret_cast<const char *>(td + SB.tbeg);
+        for (i64 o = 128 * (i64)threadIdx.x; o < 8 * (i64)SB.tlen; o += 128 * NT)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
+    }
+    __syncthreads();
+    if (w == 0 && np > 1) {  // transfers down the path
+        for (int q = 1; q < np; ++q) {
+            const H2Down &D = pd[q];
+            const double yv = lane < D.kp ? pw[q - 1][lane] : 0.0;
+            const double v = h2_apply_g(td + D.toff + D.roff + lane, D.ldt, D.kp, yv, lane < D.k);
+            if (lane < D.k) pw[q][lane] += v;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int d = 0; d <= maxh; ++d) {
+        const int a = lv[d] - n0, b = lv[d + 1] - n0;
+        if (a == b) continue;
+        for (int u = a + w; u < b; u += NW) {
+            const H2Down &D = sd[u];
+            const bool act = lane < D.k;
+            double v = act ? ws[D.yoff - SB.base + lane] : 0.0;
+            if (D.kp > 0) {
+                const double yv = lane < D.kp ? (D.yoffp >= 0 ? ys[D.yoffp - SB.base + lane] : pw[np - 1][lane]) : 0.0;
+                v += h2_apply_g(td + D.toff + D.roff + lane, D.ldt, D.kp, yv, act);
+            }
+            if (act) {
+                ys[D.yoff - SB.base + lane] = v;
+                if (D.out >= 0) tvec[(i64)D.out * KC_MAX + lane] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// S_b = Cr (kr x r, ld KQ) Cc^T (r x kc, ld KQ) -> sb[soff + i + j kr]; one warp per block
+struct SJob {
+    i64 cr, cc, soff;
+    int32_t kr, kc, r, pad;
+};
+__global__ void spro_kernel(const SJob *jobs, int n, const double *Cr, const double *Cc, double *sb) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int q = blockIdx.x * NW + w; q < n; q += gridDim.x * NW) {
+        const SJob J = jobs[q];
+        for (int e = lane; e < J.kr * J.kc; e += 32) {
+            const int i = e % J.kr, j = e / J.kr;
+            double acc = 0.0;
+            for (int c = 0; c < J.r; ++c) acc = fma(Cr[J.cr + i + (i64)c * KQ], Cc[J.cc + j + (i64)c * KQ], acc);
+            sb[J.soff + e] = acc;
+        }
+    }
+}
+
+struct DevFrees {  // frees build temporaries on every exit path
+    std::vector<void *> p;
+    template <class T>
+    T *add(T *q) {
+        p.push_back((void *)q);
+        return q;
+    }
+    ~DevFrees() {
+        for (void *q : p) cudaFree(q);
+    }
+};
+
+}  // namespace
+
+void h2_launch(const H2 &h, const double *x, double *tvec, cudaStream_t s) {
+    auto grid = [](i64 n, int per_sm) { return (int)std::max<i64>(1, std::min<i64>(148 * per_sm, (n + NW - 1) / NW)); };
+    h2_leaf_kernel<<<grid(h.nleaf, 8), NT, 0, s>>>(h.leaves, h.nleaf, h.pb, x, h.xh);
+    h2_up_kernel<<<h.nsub_up, NT, 8 * (size_t)h.up_xmax, s>>>(h.ups, h.up_lv, h.up_chain, h.up_cbeg, h.up_sub,
+                                                             h.up_xcnt, h.cnt, h.maxh_up, h.tu, h.xh);
+    h2_couple_kernel<<<grid(h.ncnode, 4), NT, 0, s>>>(h.crec, h.ncnode, h.cpls, h.sb, h.xh, h.wg);
+    h2_down_kernel<<<h.nsub_dn, NT, 16 * (size_t)h.dn_ymax, s>>>(h.dns, h.dn_path, h.dn_pbeg, h.dn_lv, h.dn_sub,
+                                                                h.dn_ycnt, h.maxh_dn, h.dn_ymax, h.td, h.wg, tvec);
+    LH_CUDA(cudaGetLastError());
+}
+
+// Builds the nested-basis form of Z: ZS holds the dense leaves and one row-basis node Q_t per row
+// leaf (the segment kernel's operands), the plan carries the H2 walk.  Returns false (nothing
+// changed) when Z does not qualify: leaves above 64 rows, a cluster whose gathered factors exceed
+// the shared-memory capacity, a basis above KQ columns, or a path deeper than H2_MAXP.
+bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_ptr<MvPlan> &plan,
+              double *stats) {
+    const cudaStream_t st = ctx.stream;
+    Z.sync_ranks(st);
+    const Tree *trees[2] = {Z.rt, Z.ct};
+    for (int sd = 0; sd < 2; ++sd)
+        for (int32_t lc : trees[sd]->leaves)
+            if (trees[sd]->nodes[lc].size() > LR) return false;
+    std::vector<int32_t> lr;
+    for (int32_t b : Z.leafblocks)
+        if (Z.nodes[b].kind == K_LR && Z.h_ranks[Z.nodes[b].rslot] > 0) lr.push_back(b);
+    const int nb = (int)lr.size();
+    if (nb == 0) return false;
+    DevFrees tmp;
+    // weights: column norms of U (for the V side) and V (for the U side)
+    std::vector<i64> woff(nb), noff, nlen;
+    i64 nw = 0;
+    for (int q = 0; q < nb; ++q) {
+        const Node &nd = Z.nodes[lr[q]];
+        const int r = Z.h_ranks[nd.rslot];
+        woff[q] = nw;
+        for (int c = 0; c < r; ++c) {
+            noff.push_back(nd.uoff + (i64)c * nd.m);
+            nlen.push_back(nd.m);
+        }
+        for (int c = 0; c < r; ++c) {
+            noff.push_back(nd.voff + (i64)c * nd.n);
+            nlen.push_back(nd.n);
+        }
+        nw += 2 * r;
+    }
+    double *dw = tmp.add(dalloc<double>(std::max<i64>(nw, 1)));
+    {
+        i64 *doff = tmp.add(dupload(noff, st)), *dlen = tmp.add(dupload(nlen, st));
+        colnorm_kernel<<<(int)std::min<i64>(148 * 16, (nw + NW - 1) / NW), NT, 0, st>>>(doff, dlen, (int)nw,
+                                                                                     Z.d_arena, dw);
+        LH_CUDA(cudaGetLastError());
+    }
+    LH_CUDA(cudaFuncSetAttribute((const void *)basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)BASIS_SMEM));
+    // ---- bases, bottom-up per side (0: rows / U, 1: columns / V)
+    struct Side {
+        std::vector<std::vector<std::pair<int, int>>> cover;  // cluster -> (block q, column offset)
+        std::vector<int> ncol, k, height, parent, rows;
+        std::vector<char> has;
+        std::vector<i64> cout, qout;
+        double *Ct = nullptr, *Qt = nullptr;
+        int maxh = 0;
+    } S[2];
+    auto col0_in = [](const std::vector<std::pair<int, int>> &cv, int q) {
+        auto it = std::lower_bound(cv.begin(), cv.end(), std::make_pair(q, -1));
+        return it != cv.end() && it->first == q ? it->second : -1;
+    };
+    for (int sd = 0; sd < 2; ++sd) {
+        Side &D = S[sd];
+        const Tree &T = *trees[sd];
+        const int nn = (int)T.nodes.size();
+        D.cover.assign(nn, {});
+        D.ncol.assign(nn, 0);
+        D.k.assign(nn, 0);
+        D.height.assign(nn, 0);
+        D.parent.assign(nn, -1);
+        D.rows.assign(nn, 0);
+        D.has.assign(nn, 0);
+        D.cout.assign(nn, -1);
+        D.qout.assign(nn, -1);
+        std::vector<int32_t> order;  // preorder
+        {
+            std::vector<int32_t> stk{0};
+            while (!stk.empty()) {
+                const int32_t c = stk.back();
+                stk.pop_back();
+                order.push_back(c);
+                const Cluster &cl = T.nodes[c];
+                if (!cl.leaf())
+                    for (int t = 1; t >= 0; --t) {
+                        D.parent[cl.kid[t]] = c;
+                        stk.push_back(cl.kid[t]);
+                    }
+            }
+        }
+        for (auto it = order.rbegin(); it != order.rend(); ++it) {
+            const Cluster &cl = T.nodes[*it];
+            if (!cl.leaf()) D.height[*it] = 1 + std::max(D.height[cl.kid[0]], D.height[cl.kid[1]]);
+        }
+        for (int q = 0; q < nb; ++q) {
+            const Node &nd = Z.nodes[lr[q]];
+            const int r = Z.h_ranks[nd.rslot];
+            std::vector<int32_t> stk{sd ? nd.ccl : nd.rcl};
+            while (!stk.empty()) {
+                const int32_t c = stk.back();
+                stk.pop_back();
+                D.cover[c].push_back({q, D.ncol[c]});
+                D.ncol[c] += r;
+                D.has[c] = 1;
+                const Cluster &cl = T.nodes[c];
+                if (!cl.leaf()) {
+                    stk.push_back(cl.kid[0]);
+                    stk.push_back(cl.kid[1]);
+                }
+            }
+        }
+        i64 clen = 0, qlen = 0;
+        for (int c = 0; c < nn; ++c) {
+            if (!D.has[c]) continue;
+            if (D.ncol[c] > MAXC) return false;
+            D.maxh = std::max(D.maxh, D.height[c]);
+            D.cout[c] = clen;
+            clen += (i64)KQ * D.ncol[c];
+            D.qout[c] = qlen;
+            qlen += (i64)(T.nodes[c].leaf() ? T.nodes[c].size() : LR) * KQ;
+        }
+        D.Ct = tmp.add(dalloc<double>(std::max<i64>(clen, 1)));
+        D.Qt = tmp.add(dalloc<double>(std::max<i64>(qlen, 1)));
+        for (int hh = 0; hh <= D.maxh; ++hh) {
+            std::vector<BJob> jobs;
+            std::vector<GPiece> pieces;
+            std::vector<int32_t> who;
+            for (int c = 0; c < nn; ++c) {
+                if (!D.has[c] || D.height[c] != hh) continue;
+                const Cluster &cl = T.nodes[c];
+                BJob J{0, (int32_t)pieces.size(), 0, D.ncol[c], D.qout[c], D.cout[c]};
+                if (cl.leaf()) {
+                    J.rows = (int32_t)cl.size();
+                    for (auto &pc : D.cover[c]) {
+                        const Node &nd = Z.nodes[lr[pc.first]];
+                        const int r = Z.h_ranks[nd.rslot];
+                        if (sd == 0)
+                            pieces.push_back({nd.uoff + (cl.lo - nd.r0), nd.m, woff[pc.first] + r, r, pc.second, 0,
+                                              J.rows});
+                        else
+                            pieces.push_back({nd.voff + (cl.lo - nd.c0), nd.n, woff[pc.first], r, pc.second, 0,
+                                              J.rows});
+                    }
+                } else {
+                    const int c1 = cl.kid[0], c2 = cl.kid[1], k1 = D.k[c1], k2 = D.k[c2];
+                    J.rows = k1 + k2;
+                    if (J.rows == 0) continue;  // k = 0
+                    for (auto &pc : D.cover[c]) {
+                        const Node &nd = Z.nodes[lr[pc.first]];
+                        const int r = Z.h_ranks[nd.rslot];
+                        const i64 wo = woff[pc.first] + (sd == 0 ? r : 0);
+                        const int a1 = col0_in(D.cover[c1], pc.first), a2 = col0_in(D.cover[c2], pc.first);
+                        if (k1 > 0) pieces.push_back({D.cout[c1] + (i64)a1 * KQ, KQ, wo, r, pc.second, 0, k1});
+                        if (k2 > 0) pieces.push_back({D.cout[c2] + (i64)a2 * KQ, KQ, wo, r, pc.second, k1, k2});
+                    }
+                }
+                D.rows[c] = J.rows;
+                J.p1 = (int32_t)pieces.size();
+                jobs.push_back(J);
+                who.push_back(c);
+            }
+            if (jobs.empty()) continue;
+            const int nj = (int)jobs.size();
+            BJob *dj = dupload(jobs, st);
+            GPiece *dp = dupload(pieces, st);
+            int *dk = dalloc<int>(nj);
+            basis_kernel<<<std::min(nj, ctx.num_sms), NT, BASIS_SMEM, st>>>(dj, nj, dp, hh == 0 ? Z.d_arena : D.Ct,
+                                                                           dw, eps, dk, D.Qt, D.Ct);
+            LH_CUDA(cudaGetLastError());
+            std::vector<int> kk(nj);
+            LH_CUDA(cudaMemcpyAsync(kk.data(), dk, sizeof(int) * nj, cudaMemcpyDeviceToHost, st));
+            LH_CUDA(cudaStreamSynchronize(st));
+            cudaFree(dj);
+            cudaFree(dp);
+            cudaFree(dk);
+            for (int j = 0; j < nj; ++j) {
+                if (kk[j] < 0) return false;
+                D.k[who[j]] = kk[j];
+            }
+        }
+    }
+    const Tree &RT = *trees[0], &CT = *trees[1];
+    if (getenv("LEVYH_H2_CHECK")) {  // host check: U_b ~ Qnest_rho C_{rho,b}, V_b ~ Pnest_sigma E_{sigma,b}
+        LH_CUDA(cudaStreamSynchronize(st));
+        std::vector<double> arena(Z.arena_len);
+        LH_CUDA(cudaMemcpy(arena.data(), Z.d_arena, 8 * Z.arena_len, cudaMemcpyDeviceToHost));
+        for (int sd = 0; sd < 2; ++sd) {
+            const Side &D = S[sd];
+            const Tree &T = *trees[sd];
+            i64 ql = 0, cl = 0;
+            for (size_t c = 0; c < T.nodes.size(); ++c)
+                if (D.has[c]) {
+                    ql = std::max<i64>(ql, D.qout[c] + (i64)(T.nodes[c].leaf() ? T.nodes[c].size() : LR) * KQ);
+                    cl = std::max<i64>(cl, D.cout[c] + (i64)KQ * D.ncol[c]);
+                }
+            std::vector<double> Qh(ql), Ch(cl);
+            LH_CUDA(cudaMemcpy(Qh.data(), D.Qt, 8 * ql, cudaMemcpyDeviceToHost));
+            LH_CUDA(cudaMemcpy(Ch.data(), D.Ct, 8 * cl, cudaMemcpyDeviceToHost));
+            // explicit nested basis of cluster c: size x k, column-major
+            std::function<std::vector<double>(int)> basis = [&](int c) {
+                const Cluster &cc = T.nodes[c];
+                const int k = D.k[c];
+                const i64 m = cc.size();
+                std::vector<double> B(m * k, 0.0);
+                if (cc.leaf()) {
+                    for (i64 e = 0; e < m * k; ++e) B[e] = Qh[D.qout[c] + e];
+                    return B;
+                }
+                const int c1 = cc.kid[0], c2 = cc.kid[1], k1 = D.k[c1], rows = D.rows[c];
+                const i64 m1 = T.nodes[c1].size();
+                auto B1 = basis(c1), B2 = basis(c2);
+                for (int j = 0; j < k; ++j)
+                    for (i64 i = 0; i < m; ++i) {
+                        double v = 0.0;
+                        if (i < m1)
+                            for (int a = 0; a < k1; ++a) v += B1[i + a * m1] * Qh[D.qout[c] + a + (i64)j * rows];
+                        else
+                            for (int a = 0; a < D.k[c2]; ++a)
+                                v += B2[(i - m1) + a * (m - m1)] * Qh[D.qout[c] + k1 + a + (i64)j * rows];
+                        B[i + j * m] = v;
+                    }
+                return B;
+            };
+            double worst = 0.0;
+            int wq = -1;
+            for (int q = 0; q < nb; ++q) {
+                const Node &nd = Z.nodes[lr[q]];
+                const int r = Z.h_ranks[nd.rslot], c = sd ? nd.ccl : nd.rcl, k = D.k[c];
+                const i64 m = sd ? nd.n : nd.m, off = sd ? nd.voff : nd.uoff;
+                auto B = basis(c);
+                int a = col0_in(D.cover[c], q);
+                double num = 0.0, den = 0.0;
+                for (int cc = 0; cc < r; ++cc)
+                    for (i64 i = 0; i < m; ++i) {
+                        double v = 0.0;
+                        for (int t = 0; t < k; ++t) v += B[i + t * m] * Ch[D.cout[c] + t + (i64)(a + cc) * KQ];
+                        const double u = arena[off + i + cc * m];
+                        num += (u - v) * (u - v);
+                        den += u * u;
+                    }
+                const double e = std::sqrt(num / std::max(den, 1e-300));
+                if (e > worst) worst = e, wq = q;
+            }
+            fprintf(stderr, "[levyh] H2 check side %d: worst factor relative error %.3e (block %d, height %d)\n", sd,
+                    worst, wq, wq >= 0 ? D.height[sd ? Z.nodes[lr[wq]].ccl : Z.nodes[lr[wq]].rcl] : -1);
+        }
+    }
+    // ---- ZS: dense leaves of Z, then one basis node Q_t per row leaf
+    ZS.rt = Z.rt;
+    ZS.ct = Z.ct;
+    ZS.rt_hold = Z.rt_hold;
+    ZS.ct_hold = Z.ct_hold;
+    ZS.nrows = Z.nrows;
+    ZS.ncols = Z.ncols;
+    ZS.nodes.clear();
+    ZS.leafblocks.clear();
+    std::vector<CopyJob> cj, qj;
+    i64 aoff = 0;
+    for (int32_t b : Z.leafblocks) {
+        const Node &sn = Z.nodes[b];
+        if (sn.kind != K_DENSE && sn.kind != K_FDENSE) continue;
+        Node d = sn;
+        d.kind = K_DENSE;
+        d.doff = aoff;
+        for (int t = 0; t < 4; ++t) d.kid[t] = -1;
+        d.vpar = -1;
+        cj.push_back({sn.doff, 1, sn.m, aoff, 1, sn.m, (int32_t)sn.m, (int32_t)sn.n});
+        aoff += sn.m * sn.n;
+        ZS.leafblocks.push_back((int32_t)ZS.nodes.size());
+        ZS.nodes.push_back(d);
+    }
+    std::vector<int32_t> ranks, qnode(RT.nodes.size(), -1);
+    for (int32_t lc : RT.leaves) {
+        const int kq = S[0].k[lc];
+        if (!S[0].has[lc] || kq == 0) continue;
+        const Cluster &cl = RT.nodes[lc];
+        Node d{};
+        d.kind = K_LR;
+        d.rcl = lc;
+        d.ccl = -1;
+        d.r0 = cl.lo;
+        d.m = cl.size();
+        d.c0 = 0;
+        d.n = 0;
+        for (int t = 0; t < 4; ++t) d.kid[t] = -1;
+        d.kcap = kq;
+        d.rslot = (int32_t)ranks.size();
+        ranks.push_back(kq);
+        d.uoff = d.voff = aoff;
+        d.doff = -1;
+        d.vpar = -1;
+        qj.push_back({S[0].qout[lc], 1, d.m, aoff, 1, d.m, (int32_t)d.m, kq});
+        aoff += d.m * kq;
+        qnode[lc] = (int32_t)ZS.nodes.size();
+        ZS.leafblocks.push_back((int32_t)ZS.nodes.size());
+        ZS.nodes.push_back(d);
+    }
+    ZS.root = 0;
+    ZS.arena_len = aoff;
+    ZS.d_arena = dalloc<double>(std::max<i64>(aoff, 1));
+    ZS.nslots = (int32_t)ranks.size();
+    ZS.d_ranks = dupload(ranks, st);
+    ZS.h_ranks = ranks;
+    auto run_copies = [&](const std::vector<CopyJob> &v, const double *src, double *dst) {
+        if (v.empty()) return;
+        CopyJob *d = dupload(v, st);
+        copy_kernel<<<(int)std::min<size_t>(v.size(), 148 * 16), NT, 0, st>>>(d, (int)v.size(), src, dst);
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d);
+    };
+    run_copies(cj, Z.d_arena, ZS.d_arena);
+    run_copies(qj, S[0].Qt, ZS.d_arena);
+    plan = build_mv_plan(ZS, ZS.leafblocks, st);
+    auto h = std::make_shared<H2>();
+    const Side &C = S[1], &R = S[0];
+    // subtrees of height <= split; the split is the largest (<= 6) whose subtrees' transfer
+    // matrices fit the shared-memory stage on both sides
+    auto is_root = [&](const Side &D, int c, int sp) {
+        const int p = D.parent[c];
+        return D.has[c] && D.height[c] <= sp && (p < 0 || !D.has[p] || D.height[p] > sp);
+    };
+    auto subtree = [](const Tree &T, int r0) {  // preorder
+        std::vector<int32_t> out, stk{r0};
+        while (!stk.empty()) {
+            const int32_t c = stk.back();
+            stk.pop_back();
+            out.push_back(c);
+            const Cluster &cl = T.nodes[c];
+            if (!cl.leaf()) {
+                stk.push_back(cl.kid[1]);
+                stk.push_back(cl.kid[0]);
+            }
+        }
+        return out;
+    };
+    auto roots = [&](const Tree &T, const Side &D, int sp) {
+        std::vector<int32_t> r;
+        for (size_t c = 0; c < T.nodes.size(); ++c)
+            if (is_root(D, (int)c, sp)) r.push_back((int32_t)c);
+        std::sort(r.begin(), r.end(), [&](int x, int y) { return T.nodes[x].lo < T.nodes[y].lo; });
+        return r;
+    };
+    if (split < 0) {  // the smallest split whose subtrees fit one wave (two CTAs per SM)
+        split = 0;
+        while (split < 12 && (int)std::max(roots(CT, C, split).size(), roots(RT, R, split).size()) > 2 * ctx.num_sms)
+            ++split;
+    }
+    auto even = [](i64 v) { return (v + 1) & ~(i64)1; };
+    // ---- column side: x_hat slots per subtree, leaves (P_s, ld 64), transfers transposed
+    std::vector<int32_t> xoff(CT.nodes.size(), -1);
+    std::vector<H2Leaf> leaves;
+    std::vector<H2Up> ups;
+    std::vector<H2Sub> up_sub;
+    std::vector<int32_t> up_lv, upidx(CT.nodes.size(), -1), up_xcnt, dn_ycnt;
+    std::vector<CopyJob> pj, tj;
+    i64 plen = 0, tulen = 0;
+    int32_t nxh = 0;
+    int up_tmax = 0, up_xmax = 0;
+    const std::vector<int32_t> subs_up = roots(CT, C, split);
+    int maxh_up = 0;
+    for (int32_t r0 : subs_up) maxh_up = std::max(maxh_up, C.height[r0]);
+    auto make_up = [&](int c) {
+        const Cluster &cl = CT.nodes[c];
+        H2Up U{tulen, C.k[c], C.k[cl.kid[0]], C.k[cl.kid[1]], xoff[c], xoff[cl.kid[0]], xoff[cl.kid[1]], -1, 0};
+        if (C.k[c] > 0 && C.rows[c] > 0)
+            tj.push_back({C.qout[c], 1, C.rows[c], tulen, C.k[c], 1, C.rows[c], C.k[c]});
+        tulen += (i64)C.rows[c] * C.k[c];
+        return U;
+    };
+    for (int32_t r0 : subs_up) {
+        const std::vector<int32_t> nodes = subtree(CT, r0);
+        const int32_t xb = nxh;
+        for (int32_t c : nodes) {
+            xoff[c] = nxh;
+            nxh += C.k[c];
+        }
+        up_xmax = std::max(up_xmax, (int)(nxh - xb));
+        up_xcnt.push_back(nxh - xb);
+        for (int32_t c : nodes) {
+            const Cluster &cl = CT.nodes[c];
+            if (!cl.leaf() || C.k[c] == 0) continue;
+            leaves.push_back({plen, cl.lo, (int32_t)cl.size(), C.k[c], xoff[c], 0});
+            pj.push_back({C.qout[c], 1, cl.size(), plen, 1, LR, (int32_t)cl.size(), C.k[c]});
+            plen += (i64)LR * C.k[c];
+        }
+        tulen = even(tulen);
+        const i64 tb = tulen;
+        up_lv.push_back((int32_t)ups.size());
+        for (int hh = 1; hh <= maxh_up; ++hh) {
+            for (int32_t c : nodes)
+                if (!CT.nodes[c].leaf() && C.height[c] == hh) {
+                    upidx[c] = (int32_t)ups.size();
+                    ups.push_back(make_up(c));
+                }
+            up_lv.push_back((int32_t)ups.size());
+        }
+        tulen = even(tulen);
+        up_sub.push_back({tb, (int32_t)(tulen - tb), xb});
+        up_tmax = std::max(up_tmax, (int)(tulen - tb));
+    }
+    for (size_t c = 0; c < CT.nodes.size(); ++c)  // the top: clusters above the subtrees
+        if (C.has[c] && C.height[c] > split) {
+            xoff[c] = nxh;
+            nxh += C.k[c];
+        }
+    for (size_t c = 0; c < CT.nodes.size(); ++c)
+        if (C.has[c] && C.height[c] > split) {
+            upidx[c] = (int32_t)ups.size();
+            ups.push_back(make_up((int)c));
+        }
+    for (size_t c = 0; c < CT.nodes.size(); ++c)
+        if (C.has[c] && C.height[c] > split) {
+            const int p = C.parent[c];
+            ups[upidx[c]].parent = (p >= 0 && C.has[p]) ? upidx[p] : -1;
+        }
+    // ---- row side: transfers per subtree (staged), y_hat slots, paths, couplings
+    const std::vector<int32_t> subs_dn = roots(RT, R, split);
+    std::vector<int32_t> yoff(RT.nodes.size(), -1), dnidx(RT.nodes.size(), -1), insub(RT.nodes.size(), -1);
+    std::vector<i64> tdoff(RT.nodes.size(), -1);
+    std::vector<CopyJob> dj2;
+    std::vector<H2Sub> dn_sub;
+    i64 tdlen = 0, sblen = 0;
+    int dn_tmax = 0, dn_ymax = 0;
+    int32_t nyh = 0;
+    auto add_td = [&](int c) {
+        if (R.has[c] && !RT.nodes[c].leaf() && R.rows[c] > 0 && R.k[c] > 0) {
+            tdoff[c] = tdlen;
+            dj2.push_back({R.qout[c], 1, R.rows[c], tdlen, 1, R.rows[c], R.rows[c], R.k[c]});
+            tdlen += (i64)R.rows[c] * R.k[c];
+        }
+    };
+    for (size_t q = 0; q < subs_dn.size(); ++q) {
+        const std::vector<int32_t> nodes = subtree(RT, subs_dn[q]);
+        tdlen = even(tdlen);
+        const i64 tb = tdlen;
+        const int32_t yb = nyh;
+        for (int32_t c : nodes) {
+            insub[c] = (int32_t)q;
+            add_td(c);
+            yoff[c] = nyh;
+            nyh += R.k[c];
+        }
+        tdlen = even(tdlen);
+        dn_sub.push_back({tb, (int32_t)(tdlen - tb), yb});
+        dn_tmax = std::max(dn_tmax, (int)(tdlen - tb));
+        dn_ymax = std::max(dn_ymax, (int)(nyh - yb));
+        dn_ycnt.push_back(nyh - yb);
+    }
+    for (size_t c = 0; c < RT.nodes.size(); ++c)  // w slots of the top clusters
+        if (R.has[c] && R.height[c] > split) {
+            yoff[c] = nyh;
+            nyh += R.k[c];
+        }
+    for (size_t c = 0; c < RT.nodes.size(); ++c)
+        if (R.has[c] && R.height[c] > split) add_td((int)c);
+    std::vector<H2Down> dns;
+    std::vector<H2Cpl> cpls;
+    std::vector<SJob> sj;
+    std::vector<int32_t> dn_path, dn_pbeg{0}, dn_lv;
+    std::vector<std::vector<int>> blocks_of(RT.nodes.size());
+    for (int q = 0; q < nb; ++q) blocks_of[Z.nodes[lr[q]].rcl].push_back(q);
+    auto make_dn = [&](int c) {
+        const Cluster &cl = RT.nodes[c];
+        H2Down D{0, 0, 0, 0, R.k[c], yoff[c], -1, (int32_t)cpls.size(), 0, -1, 0};
+        const int p = R.parent[c];
+        if (p >= 0 && R.has[p] && R.k[p] > 0 && tdoff[p] >= 0) {
+            D.toff = tdoff[p];
+            D.ldt = R.rows[p];
+            D.roff = RT.nodes[p].kid[0] == c ? 0 : R.k[RT.nodes[p].kid[0]];
+            D.kp = R.k[p];
+            if (insub[c] >= 0 && insub[p] == insub[c]) D.yoffp = yoff[p];
+        }
+        for (int q : blocks_of[c]) {
+            const Node &nd = Z.nodes[lr[q]];
+            const int kr = R.k[c], kc = C.k[nd.ccl];
+            if (kr == 0 || kc == 0) continue;
+            const int ar = col0_in(R.cover[c], q), ac = col0_in(C.cover[nd.ccl], q);
+            sj.push_back({R.cout[c] + (i64)ar * KQ, C.cout[nd.ccl] + (i64)ac * KQ, sblen, kr, kc,
+                          Z.h_ranks[nd.rslot], 0});
+            cpls.push_back({sblen, kr, kc, xoff[nd.ccl], 0});
+            sblen += (i64)kr * kc;
+        }
+        D.c1 = (int32_t)cpls.size();
+        if (insub[c] >= 0 && cl.leaf() && qnode[c] >= 0) D.out = plan->blk_of_node[qnode[c]];
+        return D;
+    };
+    int maxh_dn = 0, maxpath = 0;
+    for (int32_t r0 : subs_dn) maxh_dn = std::max(maxh_dn, R.height[r0]);
+    for (int32_t r0 : subs_dn) {  // subtree nodes by depth (contiguous per subtree)
+        std::vector<int32_t> cur{r0};
+        dn_lv.push_back((int32_t)dns.size());
+        for (int d = 0; d <= maxh_dn; ++d) {
+            std::vector<int32_t> nxt;
+            for (int32_t c : cur) {
+                dnidx[c] = (int32_t)dns.size();
+                dns.push_back(make_dn(c));
+                const Cluster &cl = RT.nodes[c];
+                if (!cl.leaf())
+                    for (int t = 0; t < 2; ++t)
+                        if (R.has[cl.kid[t]]) nxt.push_back(cl.kid[t]);
+            }
+            dn_lv.push_back((int32_t)dns.size());
+            cur.swap(nxt);
+        }
+    }
+    for (size_t c = 0; c < RT.nodes.size(); ++c)  // the top clusters (path nodes)
+        if (R.has[c] && R.height[c] > split) {
+            dnidx[c] = (int32_t)dns.size();
+            dns.push_back(make_dn((int)c));
+        }
+    for (int32_t r0 : subs_dn) {
+        std::vector<int32_t> path;
+        for (int p = R.parent[r0]; p >= 0 && R.has[p]; p = R.parent[p]) path.push_back(dnidx[p]);
+        if ((int)path.size() > H2_MAXP) return false;
+        maxpath = std::max(maxpath, (int)path.size());
+        std::reverse(path.begin(), path.end());
+        dn_path.insert(dn_path.end(), path.begin(), path.end());
+        dn_pbeg.push_back((int32_t)dn_path.size());
+    }
+    // ---- device data
+    h->split = split;
+    h->nsub_up = (int)subs_up.size();
+    h->nsub_dn = (int)subs_dn.size();
+    h->maxh_up = maxh_up;
+    h->maxh_dn = maxh_dn;
+    h->maxpath = maxpath;
+    h->up_tmax = up_tmax;
+    h->up_xmax = (up_xmax + 1) & ~1;
+    h->dn_tmax = dn_tmax;
+    h->dn_ymax = (dn_ymax + 1) & ~1;
+    std::vector<int4> crec;
+    for (size_t q = 0; q < dns.size(); ++q)
+        if (dns[q].c1 > dns[q].c0 && dns[q].k > 0) crec.push_back({dns[q].c0, dns[q].c1, dns[q].k, dns[q].yoff});
+    std::vector<int32_t> up_chain, up_cbeg{0};
+    for (int32_t r0 : subs_up) {
+        for (int p = C.parent[r0]; p >= 0 && C.has[p]; p = C.parent[p]) up_chain.push_back(upidx[p]);
+        if ((int)(up_chain.size() - up_cbeg.back()) > H2_MAXP) return false;
+        up_cbeg.push_back((int32_t)up_chain.size());
+    }
+    for (size_t q = 0; q + 1 < up_lv.size(); q += (size_t)maxh_up + 1)
+        if (up_lv[q + maxh_up] - up_lv[q] > H2_MAXN) return false;
+    for (size_t q = 0; q + 1 < dn_lv.size(); q += (size_t)maxh_dn + 2)
+        if (dn_lv[q + maxh_dn + 1] - dn_lv[q] > H2_MAXN) return false;
+    h->up_chain = dupload(up_chain, st);
+    h->up_cbeg = dupload(up_cbeg, st);
+    h->crec = dupload(crec, st);
+    h->nleaf = (int)leaves.size();
+    h->ncnode = (int)crec.size();
+    h->up_xcnt = dupload(up_xcnt, st);
+    h->dn_ycnt = dupload(dn_ycnt, st);
+    h->wg = dalloc<double>(std::max<i64>(nyh, 1));
+    h->leaves = dupload(leaves, st);
+    h->ups = dupload(ups, st);
+    h->dns = dupload(dns, st);
+    h->cpls = dupload(cpls, st);
+    h->up_lv = dupload(up_lv, st);
+    h->up_sub = dupload(up_sub, st);
+    h->dn_sub = dupload(dn_sub, st);
+    h->cnt = dalloc<int32_t>(std::max<size_t>(ups.size(), 1));
+    LH_CUDA(cudaMemsetAsync(h->cnt, 0, sizeof(int32_t) * std::max<size_t>(ups.size(), 1), st));
+    h->dn_path = dupload(dn_path, st);
+    h->dn_pbeg = dupload(dn_pbeg, st);
+    h->dn_lv = dupload(dn_lv, st);
+    h->pb = dalloc<double>(std::max<i64>(plen, 1));
+    LH_CUDA(cudaMemsetAsync(h->pb, 0, sizeof(double) * std::max<i64>(plen, 1), st));
+    h->tu = dalloc<double>(std::max<i64>(tulen, 2));
+    h->td = dalloc<double>(std::max<i64>(tdlen, 2));
+    h->sb = dalloc<double>(std::max<i64>(sblen, 1));
+    h->xh = dalloc<double>(std::max<i64>(nxh, 1));
+    run_copies(pj, C.Qt, h->pb);
+    run_copies(tj, C.Qt, h->tu);
+    run_copies(dj2, R.Qt, h->td);
+    if (!sj.empty()) {
+        SJob *d = dupload(sj, st);
+        spro_kernel<<<(int)std::min<size_t>((sj.size() + NW - 1) / NW, 148 * 16), NT, 0, st>>>(d, (int)sj.size(), R.Ct,
+                                                                                            C.Ct, h->sb);
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d);
+    }
+    LH_CUDA(cudaStreamSynchronize(st));
+    h->bytes = 8 * (plen + tulen + tdlen + sblen) + 8 * (i64)Z.ncols;
+    plan->h2 = h;
+    if (stats) {
+        double ks = 0, nl = 0;
+        for (int32_t lc : RT.leaves) ks += R.k[lc], nl += 1;
+        for (int32_t lc : CT.leaves) ks += C.k[lc], nl += 1;
+        stats[0] = ks / std::max(nl, 1.0);                  // mean leaf basis size
+        stats[1] = (double)(plen + tulen + tdlen + sblen);  // column bases + transfers + couplings
+        stats[2] = (double)aoff;                            // dense + row bases scalars
+    }
+    if (getenv("LEVYH_PLAN_VERBOSE"))
+        fprintf(stderr, "[levyh] H2: %d/%d subtrees (split %d), path <= %d, P %.1f M, Tc %.1f M, Tr %.1f M, "
+                        "S %.1f M, dense + Q %.1f M scalars, max height %d/%d, stage %d/%d doubles\n", h->nsub_up,
+                h->nsub_dn, split, maxpath, plen * 1e-6, tulen * 1e-6, tdlen * 1e-6, sblen * 1e-6, aoff * 1e-6,
+                R.maxh, C.maxh, up_tmax, dn_tmax);
     return true;
 }
 

@@ -100,8 +100,10 @@ class HFactorization:
 
     def propagator_stats(self):
         """(task count, planning s, temp bytes, executor s, near-field leaves compressed,
-        coarsening merges) of the propagator build."""
-        out = np.zeros(6)
+        coarsening merges, single-RHS form (0 H, 1 shared leaf bases, 2 nested H2), its probe
+        error against the H-form, mean leaf basis size, basis/transfer/coupling scalars) of the
+        propagator build."""
+        out = np.zeros(10)
         _lib.check(_lib.lib().lh_propagator_stats(self.h.handle, _lib.host_ptr(out)))
         return out
 

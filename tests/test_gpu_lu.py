@@ -97,6 +97,7 @@ def test_propagator_solve(P, name):
     assert _rel(b, g["solve_probe"]) <= 1e-9
     st = F.propagator_stats()
     assert st[0] > 0 and st[3] > 0  # tasks, executor seconds
+    assert st[6] in (0.0, 1.0, 2.0) and st[7] <= 1e-10  # single-RHS form of Z and its probe error
 
 
 def test_propagator_general_hminus(P):
