@@ -869,7 +869,7 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms,
     }
     if (P.ntj > 0) treduce_kernel<<<std::min(P.ntj, 148 * 16), NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
     if (P.cpl) coupling_launch(*P.cpl, P.tvec, P.tvec, s);
-    if (P.h2) h2_launch(*P.h2, x, P.tvec, s);
+    if (P.h2) h2_launch(*P.h2, x, P.tcol, P.xpad, P.nx, s);
 }
 
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
@@ -885,7 +885,7 @@ void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, d
         }
         const i64 n = P.tcol_len + P.nx + 2;
         int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
-        tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x, P.nx, P.xpad);
+        if (!P.h2) tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x, P.nx, P.xpad);
         seg_tma_kernel<<<P.tma_grid, TMA_THREADS, TMA_SMEM, s>>>(P.segs, P.cta_seg, P.batches, P.pbuf,
                                                                 P.tcol, P.xpad, y, alpha, beta,
                                                                 z ? z : y);
@@ -940,10 +940,10 @@ void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y
     }
     if (P.ntj > 0) treduce_kernel<<<std::min(P.ntj, 148 * 16), NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
     if (P.cpl) coupling_launch(*P.cpl, P.tvec, P.tvec, s);
-    if (P.h2) h2_launch(*P.h2, x_dev, P.tvec, s);
+    if (P.h2) h2_launch(*P.h2, x_dev, P.tcol, P.xpad, P.nx, s);
     const i64 n = P.tcol_len + P.nx + 2;
     int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
-    tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x_dev, P.nx, P.xpad);
+    if (!P.h2) tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x_dev, P.nx, P.xpad);
     const double *z = z_is_x ? x_dev : y_dev;
     for (int p = 0; p < NP; ++p) {  // y pieces leave as soon as their segments are done
         seg_tma_kernel<<<P.tma_grid, TMA_THREADS, TMA_SMEM, s>>>(

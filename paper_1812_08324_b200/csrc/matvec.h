@@ -102,10 +102,14 @@ struct H2Up {  // xh[xoff + j] = sum_i tu[toff + i k + j] [xh[xoff1 ..+k1]; xh[x
 struct H2Down {  // y = sum_{e in [c0, c1)} S_e x_hat + td[toff + roff + i + j ldt] y_parent[j], j < kp
     i64 toff;
     int32_t ldt, roff, kp, k, yoff, yoffp, c0, c1, out, pad;  // yoffp < 0: parent = path end
-};                     // (yoff: the node's y_hat slot, subtree nodes only; out: tvec row of a leaf)
+};                     // (yoff: the node's y_hat / w slot; out: tcol offset of a row leaf's coefficients)
 struct H2Cpl {  // w[i] += sum_j sb[soff + i + j kr] xh[xoff + j], j < kc
     i64 soff;
     int32_t kr, kc, xoff, pad;
+};
+struct H2CRec {  // a row cluster's couplings [c0, c1) with the first one inlined; w slot yoff
+    i64 soff;
+    int32_t kr, kc, xoff, yoff, c0, c1;
 };
 struct H2Sub {  // a subtree's transfer matrices [tbeg, tbeg + tlen) are staged in shared memory;
                 // its x_hat / y_hat entries are [base, base + ...) locally
@@ -127,7 +131,7 @@ struct H2 {
     double *pb = nullptr, *tu = nullptr, *td = nullptr, *sb = nullptr;
     double *xh = nullptr;
     double *wg = nullptr;          // couplings w of every row cluster (at its yoff)
-    int4 *crec = nullptr;          // row clusters with couplings: {c0, c1, k, slot}
+    H2CRec *crec = nullptr;        // row clusters with couplings
     int32_t *up_chain = nullptr, *up_cbeg = nullptr;  // climb chain (H2Up ids) per column subtree
     int32_t *up_xcnt = nullptr, *dn_ycnt = nullptr;  // x_hat / y_hat slots per subtree
     int nleaf = 0, ncnode = 0;
@@ -136,7 +140,9 @@ struct H2 {
     i64 bytes = 0;  // algorithmic bytes per application (P, transfers, couplings)
     ~H2();
 };
-void h2_launch(const H2 &h, const double *x, double *tvec, cudaStream_t s);
+// the walk writes the row-leaf coefficients straight into the segment kernel's tcol and the
+// padded copy of x (xpad), so an H2 plan needs no tgather launch
+void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s);
 void treduce_launch(const TJob *jobs, int n, const double *part, double *out, cudaStream_t s);
 
 struct MvPlan {

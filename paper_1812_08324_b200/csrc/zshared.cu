@@ -695,6 +695,30 @@ __device__ __forceinline__ double h2_apply_g(const double *T, i64 ldi, int n, do
     return a0 + a1;
 }
 
+// two independent products, r1 = T1 v1 (n1 terms) and r2 = T2 v2 (n2 terms), all loads in flight
+// together: one memory round trip for both
+__device__ __forceinline__ void h2_apply_g2(const double *T1, i64 ld1, int n1, double v1, bool act1,
+                                            const double *T2, i64 ld2, int n2, double v2, bool act2, double &r1,
+                                            double &r2) {
+    double a1 = 0.0, a2 = 0.0;
+    const int n = max(n1, n2);
+    for (int b = 0; b < n; b += 16) {  // one batch (one round trip) for k <= 16
+        double t1[16], t2[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            t1[i] = (act1 && b + i < n1) ? T1[(b + i) * ld1] : 0.0;
+            t2[i] = (act2 && b + i < n2) ? T2[(b + i) * ld2] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            a1 = fma(t1[i], __shfl_sync(FULL, v1, (b + i) & 31), a1);
+            a2 = fma(t2[i], __shfl_sync(FULL, v2, (b + i) & 31), a2);
+        }
+    }
+    r1 = a1;
+    r2 = a2;
+}
+
 // couplings of one row cluster, w[i] = sum_e S_e x_hat_e, lane i < k
 __device__ __forceinline__ double h2_couple(const H2Down &D, const H2Cpl *cpls, const double *sb,
                                             const double *xh, int lane) {
@@ -707,10 +731,31 @@ __device__ __forceinline__ double h2_couple(const H2Down &D, const H2Cpl *cpls, 
     return acc;
 }
 
+// global -> shared copy by the whole CTA with every load of a thread in flight at once
+template <class T>
+__device__ __forceinline__ void h2_copy_in(T *dst, const T *src, int n) {
+    constexpr int U = 8;
+    for (int b = 0; b < n; b += U * NT) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = b + u * NT + threadIdx.x;
+            v[u] = i < n ? src[i] : T();
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = b + u * NT + threadIdx.x;
+            if (i < n) dst[i] = v[u];
+        }
+    }
+}
+
 // x_hat of every column leaf: one warp per leaf, all CTAs resident (bandwidth-bound: P streams once)
 __global__ void __launch_bounds__(NT) h2_leaf_kernel(const H2Leaf *leaves, int n, const double *pb, const double *x,
-                                                    double *xh) {
+                                                    double *xh, i64 nx, double *xpad) {
     const int lane = threadIdx.x & 31;
+    for (i64 i = (i64)blockIdx.x * NT + threadIdx.x; i < nx + 2; i += (i64)gridDim.x * NT)
+        xpad[i] = i < nx ? x[i] : 0.0;  // the segment kernel's aligned, padded copy of x
     for (int l = blockIdx.x * NW + (threadIdx.x >> 5); l < n; l += gridDim.x * NW) {
         const H2Leaf L = leaves[l];
         const double v = h2_leaf(L, pb, x, lane);
@@ -724,7 +769,7 @@ __global__ void __launch_bounds__(NT) h2_leaf_kernel(const H2Leaf *leaves, int n
 constexpr int H2_MAXN = 128;  // staged node descriptors per subtree
 __global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int32_t *up_lv, const int32_t *up_chain,
                                                       const int32_t *up_cbeg, const H2Sub *sub, const int32_t *up_xcnt,
-                                                      int32_t *cnt, int maxh, const double *tu, double *xh) {
+                                                      int32_t *cnt, int maxh, const double *tu, double *xh, int dbg) {
     extern __shared__ __align__(16) double h2s[];
     double *xs = h2s;
     __shared__ H2Up su[H2_MAXN];
@@ -734,14 +779,11 @@ __global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int
     const int32_t *lv = up_lv + (i64)s * (maxh + 1);
     const int u0 = lv[0], nu = lv[maxh] - u0, c0 = up_cbeg[s], nc = up_cbeg[s + 1] - c0;
     {  // descriptors (subtree + climb chain) and x_hat slots to shared memory; transfers to L2
-        const int32_t *src = reinterpret_cast<const int32_t *>(ups + u0);
-        int32_t *dst = reinterpret_cast<int32_t *>(su);
         constexpr int W = (int)(sizeof(H2Up) / 4);
-        for (int i = threadIdx.x; i < nu * W; i += NT) dst[i] = src[i];
+        h2_copy_in(reinterpret_cast<int32_t *>(su), reinterpret_cast<const int32_t *>(ups + u0), nu * W);
         for (int i = threadIdx.x; i < nc * W; i += NT)
             reinterpret_cast<int32_t *>(sc)[i] = reinterpret_cast<const int32_t *>(ups + up_chain[c0 + i / W])[i % W];
-        const int nx = up_xcnt[s];
-        for (int i = threadIdx.x; i < nx; i += NT) xs[i] = xh[SB.base + i];
+        h2_copy_in(xs, xh + SB.base, up_xcnt[s]);
         const char *t = reinterpret_cast<const char *>(tu + SB.tbeg);
         for (i64 o = 128 * (i64)threadIdx.x; o < 8 * (i64)SB.tlen; o += 128 * NT)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
@@ -752,7 +794,7 @@ __global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int
         const int bytes = 8 * (sc[q].k1 + sc[q].k2) * sc[q].k;
         for (int o = 128 * lane; o < bytes; o += 128 * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
     }
-    for (int hh = 0; hh < maxh; ++hh) {
+    for (int hh = 0; hh < ((dbg & 2) ? 0 : maxh); ++hh) {
         const int a = lv[hh] - u0, b = lv[hh + 1] - u0;
         if (a == b) continue;
         for (int u = a + w; u < b; u += NW) {
@@ -761,7 +803,9 @@ __global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int
             const double xa = lane < U.k1 ? xs[U.xoff1 - SB.base + lane] : 0.0;
             const double xb = lane < U.k2 ? xs[U.xoff2 - SB.base + lane] : 0.0;
             const bool act = lane < U.k;
-            const double v = h2_apply_g(T, U.k, U.k1, xa, act) + h2_apply_g(T + (i64)U.k1 * U.k, U.k, U.k2, xb, act);
+            double v1, v2;
+            h2_apply_g2(T, U.k, U.k1, xa, act, T + (i64)U.k1 * U.k, U.k, U.k2, xb, act, v1, v2);
+            const double v = v1 + v2;
             if (act) {
                 xh[U.xoff + lane] = v;
                 xs[U.xoff - SB.base + lane] = v;
@@ -769,7 +813,7 @@ __global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int
         }
         __syncthreads();
     }
-    if (w != 0) return;
+    if (w != 0 || (dbg & 1)) return;
     for (int q = 0; q < nc; ++q) {
         const int p = up_chain[c0 + q];
         const H2Up &U = sc[q];
@@ -786,8 +830,9 @@ __global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int
         const double xb = lane < U.k2 ? __ldcg(xh + U.xoff2 + lane) : 0.0;
         const bool act = lane < U.k;
         const double *T = tu + U.toff + lane;
-        const double v = h2_apply_g(T, U.k, U.k1, xa, act) + h2_apply_g(T + (i64)U.k1 * U.k, U.k, U.k2, xb, act);
-        if (act) xh[U.xoff + lane] = v;
+        double v1, v2;
+        h2_apply_g2(T, U.k, U.k1, xa, act, T + (i64)U.k1 * U.k, U.k, U.k2, xb, act, v1, v2);
+        if (act) xh[U.xoff + lane] = v1 + v2;
     }
 }
 
@@ -806,18 +851,19 @@ __device__ __forceinline__ double h2_apply_g16(const double *T, i64 ldi, int n, 
     }
     return a0 + a1;
 }
-__global__ void __launch_bounds__(NT, 4) h2_couple_kernel(const int4 *crec, int n, const H2Cpl *cpls,
+__global__ void __launch_bounds__(NT, 4) h2_couple_kernel(const H2CRec *crec, int n, const H2Cpl *cpls,
                                                          const double *sb, const double *xh, double *wg) {
     const int lane = threadIdx.x & 31;
     for (int q = blockIdx.x * NW + (threadIdx.x >> 5); q < n; q += gridDim.x * NW) {
-        const int4 R = crec[q];  // couplings [x, y), k = z, slot w
-        double acc = 0.0;
-        for (int e = R.x; e < R.y; ++e) {
+        const H2CRec R = crec[q];
+        const double xv = lane < R.kc ? __ldcg(xh + R.xoff + lane) : 0.0;
+        double acc = h2_apply_g16(sb + R.soff + lane, R.kr, R.kc, xv, lane < R.kr);
+        for (int e = R.c0 + 1; e < R.c1; ++e) {  // further couplings of the same cluster (rare)
             const H2Cpl C = cpls[e];
-            const double xv = lane < C.kc ? __ldcg(xh + C.xoff + lane) : 0.0;
-            acc += h2_apply_g16(sb + C.soff + lane, C.kr, C.kc, xv, lane < R.z);
+            const double x2 = lane < C.kc ? __ldcg(xh + C.xoff + lane) : 0.0;
+            acc += h2_apply_g16(sb + C.soff + lane, C.kr, C.kc, x2, lane < R.kr);
         }
-        if (lane < R.z) wg[R.w + lane] = acc;
+        if (lane < R.kr) wg[R.yoff + lane] = acc;
     }
 }
 
@@ -826,7 +872,7 @@ __global__ void __launch_bounds__(NT, 4) h2_couple_kernel(const int4 *crec, int 
 __global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const int32_t *dn_path,
                                                         const int32_t *dn_pbeg, const int32_t *dn_lv,
                                                         const H2Sub *sub, const int32_t *dn_ycnt, int maxh, int ymax,
-                                                        const double *td, const double *wg, double *tvec) {
+                                                        const double *td, const double *wg, double *tcol, int dbg) {
     extern __shared__ __align__(16) double h2s[];
     double *ws = h2s, *ys = ws + ymax;
     __shared__ double pw[H2_MAXP][KC_MAX];
@@ -838,11 +884,9 @@ __global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const
     __shared__ H2Down sd[H2_MAXN];
     const int n0 = lv[0], nn = lv[maxh + 1] - n0;
     {
-        const int32_t *src = reinterpret_cast<const int32_t *>(dns + n0);
-        int32_t *dst = reinterpret_cast<int32_t *>(sd);
-        for (int i = threadIdx.x; i < nn * (int)(sizeof(H2Down) / 4); i += NT) dst[i] = src[i];
-        const int ny = dn_ycnt[s];
-        for (int i = threadIdx.x; i < ny; i += NT) ws[i] = wg[SB.base + i];
+        h2_copy_in(reinterpret_cast<int32_t *>(sd), reinterpret_cast<const int32_t *>(dns + n0),
+                   nn * (int)(sizeof(H2Down) / 4));
+        h2_copy_in(ws, wg + SB.base, dn_ycnt[s]);
         for (int q = w; q < np; q += NW) {
             const H2Down D = dns[dn_path[pa + q]];
             if (lane < D.k) pw[q][lane] = wg[D.yoff + lane];
@@ -853,7 +897,7 @@ __global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const
             asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
     }
     __syncthreads();
-    if (w == 0 && np > 1) {  // transfers down the path
+    if (w == 0 && np > 1 && !(dbg & 4)) {  // transfers down the path
         for (int q = 1; q < np; ++q) {
             const H2Down &D = pd[q];
             const double yv = lane < D.kp ? pw[q - 1][lane] : 0.0;
@@ -863,20 +907,29 @@ __global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const
         }
     }
     __syncthreads();
-    for (int d = 0; d <= maxh; ++d) {
+    for (int d = 0; d <= ((dbg & 8) ? -1 : maxh); ++d) {
         const int a = lv[d] - n0, b = lv[d + 1] - n0;
         if (a == b) continue;
-        for (int u = a + w; u < b; u += NW) {
-            const H2Down &D = sd[u];
-            const bool act = lane < D.k;
-            double v = act ? ws[D.yoff - SB.base + lane] : 0.0;
-            if (D.kp > 0) {
-                const double yv = lane < D.kp ? (D.yoffp >= 0 ? ys[D.yoffp - SB.base + lane] : pw[np - 1][lane]) : 0.0;
-                v += h2_apply_g(td + D.toff + D.roff + lane, D.ldt, D.kp, yv, act);
+        for (int u = a + w; u < b; u += 2 * NW) {  // two nodes per warp and round trip
+            const bool two = u + NW < b;
+            const H2Down &D1 = sd[u];
+            const H2Down &D2 = sd[two ? u + NW : u];
+            auto parent_y = [&](const H2Down &D) {
+                return lane < D.kp ? (D.yoffp >= 0 ? ys[D.yoffp - SB.base + lane] : pw[np - 1][lane]) : 0.0;
+            };
+            const bool act1 = lane < D1.k, act2 = two && lane < D2.k;
+            double r1, r2;
+            h2_apply_g2(td + D1.toff + D1.roff + lane, D1.ldt, D1.kp, parent_y(D1), act1, td + D2.toff + D2.roff + lane,
+                        D2.ldt, D2.kp, parent_y(D2), act2, r1, r2);
+            if (act1) {
+                const double v = ws[D1.yoff - SB.base + lane] + r1;
+                ys[D1.yoff - SB.base + lane] = v;
+                if (D1.out >= 0) tcol[D1.out + lane] = v;
             }
-            if (act) {
-                ys[D.yoff - SB.base + lane] = v;
-                if (D.out >= 0) tvec[(i64)D.out * KC_MAX + lane] = v;
+            if (act2) {
+                const double v = ws[D2.yoff - SB.base + lane] + r2;
+                ys[D2.yoff - SB.base + lane] = v;
+                if (D2.out >= 0) tcol[D2.out + lane] = v;
             }
         }
         __syncthreads();
@@ -915,14 +968,15 @@ struct DevFrees {  // frees build temporaries on every exit path
 
 }  // namespace
 
-void h2_launch(const H2 &h, const double *x, double *tvec, cudaStream_t s) {
+void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s) {
+    static const int dbg = getenv("LEVYH_H2_DBG") ? atoi(getenv("LEVYH_H2_DBG")) : 0;  // timing experiments only
     auto grid = [](i64 n, int per_sm) { return (int)std::max<i64>(1, std::min<i64>(148 * per_sm, (n + NW - 1) / NW)); };
-    h2_leaf_kernel<<<grid(h.nleaf, 8), NT, 0, s>>>(h.leaves, h.nleaf, h.pb, x, h.xh);
+    h2_leaf_kernel<<<grid(h.nleaf, 8), NT, 0, s>>>(h.leaves, h.nleaf, h.pb, x, h.xh, nx, xpad);
     h2_up_kernel<<<h.nsub_up, NT, 8 * (size_t)h.up_xmax, s>>>(h.ups, h.up_lv, h.up_chain, h.up_cbeg, h.up_sub,
-                                                             h.up_xcnt, h.cnt, h.maxh_up, h.tu, h.xh);
+                                                             h.up_xcnt, h.cnt, h.maxh_up, h.tu, h.xh, dbg);
     h2_couple_kernel<<<grid(h.ncnode, 4), NT, 0, s>>>(h.crec, h.ncnode, h.cpls, h.sb, h.xh, h.wg);
     h2_down_kernel<<<h.nsub_dn, NT, 16 * (size_t)h.dn_ymax, s>>>(h.dns, h.dn_path, h.dn_pbeg, h.dn_lv, h.dn_sub,
-                                                                h.dn_ycnt, h.maxh_dn, h.dn_ymax, h.td, h.wg, tvec);
+                                                                h.dn_ycnt, h.maxh_dn, h.dn_ymax, h.td, h.wg, tcol, dbg);
     LH_CUDA(cudaGetLastError());
 }
 
@@ -1377,6 +1431,13 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
         }
     for (size_t c = 0; c < RT.nodes.size(); ++c)
         if (R.has[c] && R.height[c] > split) add_td((int)c);
+    // tcol position of every tvec entry (the segment kernel's batch-ordered coefficients)
+    std::vector<int32_t> tmap(plan->tcol_len);
+    LH_CUDA(cudaMemcpy(tmap.data(), plan->tmap, sizeof(int32_t) * plan->tcol_len, cudaMemcpyDeviceToHost));
+    std::vector<i64> tpos((i64)plan->nblk * KC_MAX + 1, -1);
+    for (i64 e = 0; e < plan->tcol_len; ++e)
+        if (tmap[e] >= 0) tpos[tmap[e]] = e;
+    bool tcol_ok = plan->tcol_len < (i64)INT32_MAX;
     std::vector<H2Down> dns;
     std::vector<H2Cpl> cpls;
     std::vector<SJob> sj;
@@ -1405,7 +1466,12 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
             sblen += (i64)kr * kc;
         }
         D.c1 = (int32_t)cpls.size();
-        if (insub[c] >= 0 && cl.leaf() && qnode[c] >= 0) D.out = plan->blk_of_node[qnode[c]];
+        if (insub[c] >= 0 && cl.leaf() && qnode[c] >= 0) {
+            const i64 t0 = tpos[(i64)plan->blk_of_node[qnode[c]] * KC_MAX];
+            for (int i = 0; i < R.k[c]; ++i)
+                if (t0 < 0 || tpos[(i64)plan->blk_of_node[qnode[c]] * KC_MAX + i] != t0 + i) tcol_ok = false;
+            D.out = (int32_t)t0;
+        }
         return D;
     };
     int maxh_dn = 0, maxpath = 0;
@@ -1441,6 +1507,8 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
         dn_path.insert(dn_path.end(), path.begin(), path.end());
         dn_pbeg.push_back((int32_t)dn_path.size());
     }
+    if (!tcol_ok) return false;
+    LH_CUDA(cudaMemsetAsync(plan->tcol, 0, sizeof(double) * plan->tcol_len, st));  // padding stays zero
     // ---- device data
     h->split = split;
     h->nsub_up = (int)subs_up.size();
@@ -1452,9 +1520,12 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     h->up_xmax = (up_xmax + 1) & ~1;
     h->dn_tmax = dn_tmax;
     h->dn_ymax = (dn_ymax + 1) & ~1;
-    std::vector<int4> crec;
+    std::vector<H2CRec> crec;
     for (size_t q = 0; q < dns.size(); ++q)
-        if (dns[q].c1 > dns[q].c0 && dns[q].k > 0) crec.push_back({dns[q].c0, dns[q].c1, dns[q].k, dns[q].yoff});
+        if (dns[q].c1 > dns[q].c0 && dns[q].k > 0) {
+            const H2Cpl &E = cpls[dns[q].c0];
+            crec.push_back({E.soff, E.kr, E.kc, E.xoff, dns[q].yoff, dns[q].c0, dns[q].c1});
+        }
     std::vector<int32_t> up_chain, up_cbeg{0};
     for (int32_t r0 : subs_up) {
         for (int p = C.parent[r0]; p >= 0 && C.has[p]; p = C.parent[p]) up_chain.push_back(upidx[p]);
