@@ -35,14 +35,10 @@ static i64 vchunk_rows() {
 #ifndef SEG_MIN_BLOCKS
 #define SEG_MIN_BLOCKS 4        // CTAs per SM for the direct-load segment kernel
 #endif
-constexpr int TMA_STAGES = 5;
 constexpr int SLOT_D = 5120;    // doubles of operand data per ring slot (40 KB: a 64 x 64 dense leaf plus a basis of <= 16 columns)
 constexpr int SLOT_A = 1024;    // doubles of aux (descriptors, t_b span, x slice) per slot
 constexpr int DESC_D = 64;      // aux doubles reserved for piece descriptors (32 x 16 B)
 constexpr int MAX_PIECES = 32;  // pieces per batch
-constexpr int TMA_CONS = 512;             // consumer threads: 64 rows x 8 column groups
-constexpr int TGRP = TMA_CONS / SEG;
-constexpr int TMA_THREADS = TMA_CONS + 32;  // one producer warp + 16 consumer warps
 
 // ---------------------------------------------------------------------------
 // phase 1
@@ -342,29 +338,37 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
 }
+template <int CONS>
 __device__ __forceinline__ void consumer_sync() {  // the consumer warps only
-    asm volatile("bar.sync 1, %0;" ::"n"(TMA_CONS) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(CONS) : "memory");
 }
 
 constexpr int XOFF = 0;    // aux: x slice (<= 66 doubles)
 constexpr int TOFF = 128;  // aux: low-rank coefficients (<= MAXK)
 constexpr int MAXK = 128;  // columns per batch (segments of < 32 rows would allow more)
 
+// ST ring stages, CONS consumer threads (64 rows x CONS / 64 column groups).  The full
+// configuration (5 stages, 16 consumer warps) owns an SM; the lean one (3 stages, 8 consumer
+// warps: 128 KB, ~28 K registers) leaves room for the H2 walk CTAs that run beside it.
+template <int ST, int CONS>
 struct TmaSmem {
-    double data[TMA_STAGES][SLOT_D];
-    double aux[TMA_STAGES][TOFF + MAXK];
-    double red[2][TGRP][SEG];  // double-buffered: one consumer barrier per segment
-    uint64_t full[TMA_STAGES], empty[TMA_STAGES];
-    int32_t hdr[TMA_STAGES][4];  // K, kd, xadj
+    double data[ST][SLOT_D];
+    double aux[ST][TOFF + MAXK];
+    double red[2][CONS / SEG][SEG];  // double-buffered: one consumer barrier per segment
+    uint64_t full[ST], empty[ST];
+    int32_t hdr[ST][4];  // K, kd, xadj
 };
-constexpr size_t TMA_SMEM = sizeof(TmaSmem) + 128;
+template <int ST, int CONS>
+constexpr size_t tma_smem() { return sizeof(TmaSmem<ST, CONS>) + 128; }
 
-__global__ void __launch_bounds__(TMA_THREADS, 1)
+template <int ST, int CONS>
+__global__ void __launch_bounds__(CONS + 32, 1)
     seg_tma_kernel(const SegDesc *segs, const int32_t *cta_seg, const SBatch *batches,
                    const double *pbuf, const double *tcol, const double *x, double *y,
                    double alpha, double beta, const double *z) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    TmaSmem &S = *reinterpret_cast<TmaSmem *>(smem_raw);
+    constexpr int TMA_STAGES = ST, TMA_CONS = CONS, TGRP = CONS / SEG;
+    TmaSmem<ST, CONS> &S = *reinterpret_cast<TmaSmem<ST, CONS> *>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < TMA_STAGES; ++i) {
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         }
         double(*red)[SEG] = S.red[(s - s0) & 1];
         red[g][row] = (a0 + a1) + (a2 + a3);
-        consumer_sync();
+        consumer_sync<CONS>();
         if (g == 0 && row < cur.rows) {
             double v = red[0][row];
 #pragma unroll
@@ -821,6 +825,9 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
 }
 
 MvPlan::~MvPlan() {
+    if (fork) cudaStreamDestroy(fork);
+    for (cudaEvent_t e : fev)
+        if (e) cudaEventDestroy(e);
     cudaFree(pbuf);
     cudaFree(tcol);
     cudaFree(tmap);
@@ -872,23 +879,47 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms,
     if (P.h2) h2_launch(*P.h2, x, P.tcol, P.xpad, P.nx, s);
 }
 
+// one launch of the TMA segment kernel over the CTA ranges cta (full or lean configuration)
+static void seg_tma_launch(const MvPlan &P, const int32_t *cta, double *y, double alpha, double beta,
+                           const double *z, cudaStream_t s) {
+    if (P.lean) {
+        static bool attr = false;
+        if (!attr) {
+            LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel<3, 256>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem<3, 256>()));
+            attr = true;
+        }
+        seg_tma_kernel<3, 256><<<P.tma_grid, 256 + 32, tma_smem<3, 256>(), s>>>(P.segs, cta, P.batches, P.pbuf, P.tcol,
+                                                                             P.xpad, y, alpha, beta, z);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel<5, 512>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem<5, 512>()));
+            attr = true;
+        }
+        seg_tma_kernel<5, 512><<<P.tma_grid, 512 + 32, tma_smem<5, 512>(), s>>>(P.segs, cta, P.batches, P.pbuf, P.tcol,
+                                                                             P.xpad, y, alpha, beta, z);
+    }
+}
+
 void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha,
                    double beta, cudaStream_t s, int num_sms, const double *z) {
     (void)H;
     static const bool direct = getenv("LEVYH_SEG_DIRECT") != nullptr;
+    if (P.dense) {  // split H2 plan, serial form: dense leaves, then the row-basis pieces
+        const MvPlan &D = *P.dense;
+        tgather_kernel<<<(int)std::min<i64>((D.nx + 2 + NT - 1) / NT, 148 * 8), NT, 0, s>>>(
+            D.tmap, 0, D.tvec, D.tcol, x, D.nx, D.xpad);
+        seg_tma_launch(D, D.cta_seg, y, alpha, beta, z ? z : y, s);
+        seg_tma_launch(P, P.cta_seg, y, alpha, 1.0, y, s);
+        return;
+    }
     if (!direct && P.nbatch > 0) {
-        static bool attr = false;
-        if (!attr) {
-            LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
-            attr = true;
-        }
         const i64 n = P.tcol_len + P.nx + 2;
         int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
         if (!P.h2) tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x, P.nx, P.xpad);
-        seg_tma_kernel<<<P.tma_grid, TMA_THREADS, TMA_SMEM, s>>>(P.segs, P.cta_seg, P.batches, P.pbuf,
-                                                                P.tcol, P.xpad, y, alpha, beta,
-                                                                z ? z : y);
+        seg_tma_launch(P, P.cta_seg, y, alpha, beta, z ? z : y, s);
         return;
     }
     // (A one-warp-per-32-rows variant without shared memory measured slower on B200.)
@@ -900,6 +931,22 @@ void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, d
 // y = alpha * H x + beta * z (z = y when null) for one right-hand side
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
             cudaStream_t s, int num_sms, const double *z) {
+    if (P.dense) {
+        // split H2 plan: the dense diagonal leaves stream on a forked stream (lean segment
+        // kernel) while the latency-bound H2 walk runs; the row-basis pieces add in after both
+        const MvPlan &D = *P.dense;
+        LH_CUDA(cudaEventRecord(P.fev[0], s));
+        LH_CUDA(cudaStreamWaitEvent(P.fork, P.fev[0], 0));
+        tgather_kernel<<<(int)std::min<i64>((D.nx + 2 + NT - 1) / NT, 148 * 8), NT, 0, P.fork>>>(
+            D.tmap, 0, D.tvec, D.tcol, x, D.nx, D.xpad);
+        seg_tma_launch(D, D.cta_seg, y, alpha, beta, z ? z : y, P.fork);
+        LH_CUDA(cudaEventRecord(P.fev[1], P.fork));
+        h2_launch(*P.h2, x, P.tcol, P.xpad, 0, s);
+        LH_CUDA(cudaStreamWaitEvent(s, P.fev[1], 0));
+        seg_tma_launch(P, P.cta_seg, y, alpha, 1.0, y, s);
+        LH_CUDA(cudaGetLastError());
+        return;
+    }
     mv_vtx_launch(P, H, x, num_sms, s);
     mv_seg_launch(P, H, x, y, alpha, beta, s, num_sms, z);
     LH_CUDA(cudaGetLastError());
@@ -910,12 +957,6 @@ void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y
                  cudaStream_t side, cudaEvent_t *ev, int num_sms) {
     const int NP = P.npiece;
     LH_REQUIRE(NP >= 1 && P.nbatch > 0, LH_EINTERNAL, "matvec plan without pipelining data");
-    static bool attr = false;
-    if (!attr) {
-        LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
-        attr = true;
-    }
     cudaEvent_t fork = ev[2 * NP], join = ev[2 * NP + 1];
     LH_CUDA(cudaEventRecord(fork, s));
     LH_CUDA(cudaStreamWaitEvent(side, fork, 0));
@@ -925,8 +966,25 @@ void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y
                                 side));
         LH_CUDA(cudaEventRecord(ev[p], side));
     }
+    const double *z = z_is_x ? x_dev : y_dev;
+    if (P.dense) {  // split H2 plan: dense leaves on the copy stream once x is in, beside the walk
+        const MvPlan &D = *P.dense;
+        tgather_kernel<<<(int)std::min<i64>((D.nx + 2 + NT - 1) / NT, 148 * 8), NT, 0, side>>>(
+            D.tmap, 0, D.tvec, D.tcol, x_dev, D.nx, D.xpad);
+        seg_tma_launch(D, D.cta_seg, y_dev, alpha, beta, z, side);
+        LH_CUDA(cudaEventRecord(P.fev[1], side));
+    }
+    int hl = 0;  // H2: column leaves whose x rows have arrived
     for (int p = 0; p < NP; ++p) {  // V^T x of the chunks whose x rows have arrived
         LH_CUDA(cudaStreamWaitEvent(s, ev[p], 0));
+        if (P.h2) {
+            const H2 &h = *P.h2;
+            int he = hl;
+            while (he < h.nleaf && h.leaf_end[he] <= P.xcut[p + 1]) ++he;
+            if (p == NP - 1) he = h.nleaf;
+            h2_leaf_launch(h, hl, he, x_dev, s);
+            hl = he;
+        }
         const int n8 = P.pch[p + 1] - P.pch[p], n16 = P.pch16[p + 1] - P.pch16[p];
         if (n8 > 0) {
             int g = std::max(1, std::min(vtx_grid<8>(num_sms), (n8 + dev::NW - 1) / dev::NW));
@@ -940,15 +998,14 @@ void mv_run_host(const MvPlan &P, const double *x_host, double *x_dev, double *y
     }
     if (P.ntj > 0) treduce_kernel<<<std::min(P.ntj, 148 * 16), NT, 0, s>>>(P.tjobs, P.ntj, P.part, P.tvec);
     if (P.cpl) coupling_launch(*P.cpl, P.tvec, P.tvec, s);
-    if (P.h2) h2_launch(*P.h2, x_dev, P.tcol, P.xpad, P.nx, s);
+    if (P.h2) h2_launch(*P.h2, x_dev, P.tcol, P.xpad, P.dense ? 0 : P.nx, s, false);
     const i64 n = P.tcol_len + P.nx + 2;
     int g = (int)std::min<i64>((n + NT - 1) / NT, 148 * 8);
     if (!P.h2) tgather_kernel<<<g, NT, 0, s>>>(P.tmap, P.tcol_len, P.tvec, P.tcol, x_dev, P.nx, P.xpad);
-    const double *z = z_is_x ? x_dev : y_dev;
+    if (P.dense) LH_CUDA(cudaStreamWaitEvent(s, P.fev[1], 0));
     for (int p = 0; p < NP; ++p) {  // y pieces leave as soon as their segments are done
-        seg_tma_kernel<<<P.tma_grid, TMA_THREADS, TMA_SMEM, s>>>(
-            P.segs, P.cta_seg_pp + (size_t)p * (P.tma_grid + 1), P.batches, P.pbuf, P.tcol, P.xpad,
-            y_dev, alpha, beta, z);
+        if (P.dense) seg_tma_launch(P, P.cta_seg_pp + (size_t)p * (P.tma_grid + 1), y_dev, alpha, 1.0, y_dev, s);
+        else seg_tma_launch(P, P.cta_seg_pp + (size_t)p * (P.tma_grid + 1), y_dev, alpha, beta, z, s);
         LH_CUDA(cudaEventRecord(ev[NP + p], s));
         LH_CUDA(cudaStreamWaitEvent(side, ev[NP + p], 0));
         const i64 a = P.ycut[p], b = P.ycut[p + 1];

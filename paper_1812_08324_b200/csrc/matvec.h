@@ -135,6 +135,7 @@ struct H2 {
     int32_t *up_chain = nullptr, *up_cbeg = nullptr;  // climb chain (H2Up ids) per column subtree
     int32_t *up_xcnt = nullptr, *dn_ycnt = nullptr;  // x_hat / y_hat slots per subtree
     int nleaf = 0, ncnode = 0;
+    std::vector<i64> leaf_end;  // host: last row + 1 of every column leaf (leaves are in row order)
     int up_tmax = 0, up_xmax = 0, dn_tmax = 0, dn_ymax = 0;  // staged doubles per CTA
     int maxpath = 0;
     i64 bytes = 0;  // algorithmic bytes per application (P, transfers, couplings)
@@ -142,13 +143,21 @@ struct H2 {
 };
 // the walk writes the row-leaf coefficients straight into the segment kernel's tcol and the
 // padded copy of x (xpad), so an H2 plan needs no tgather launch
-void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s);
+// leaves = false: the column-leaf x_hat are already in place (h2_leaf_launch per x piece)
+void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s, bool leaves = true);
+void h2_leaf_launch(const H2 &h, int l0, int l1, const double *x, cudaStream_t s);
 void treduce_launch(const TJob *jobs, int n, const double *part, double *out, cudaStream_t s);
 
 struct MvPlan {
     int nseg = 0, nch = 0, nch16 = 0, ntj = 0, nbatch = 0, tma_grid = 0;
     std::shared_ptr<Coupling> cpl;     // set for shared-leaf-basis operators
     std::shared_ptr<H2> h2;            // set for nested-basis (H2) operators
+    // split H2 plan: this plan holds the row-basis pieces; `dense` the dense leaves (lean
+    // segment kernel, run on the forked stream beside the walk)
+    std::shared_ptr<MvPlan> dense;
+    bool lean = false;                 // segment kernel in its lean configuration
+    cudaStream_t fork = nullptr;
+    cudaEvent_t fev[2] = {nullptr, nullptr};
     std::vector<int32_t> blk_of_node;  // tvec row of every low-rank node (-1 otherwise)
     double *pbuf = nullptr;  // packed operands
     i64 pbuf_len = 0;

@@ -754,8 +754,9 @@ __device__ __forceinline__ void h2_copy_in(T *dst, const T *src, int n) {
 __global__ void __launch_bounds__(NT) h2_leaf_kernel(const H2Leaf *leaves, int n, const double *pb, const double *x,
                                                     double *xh, i64 nx, double *xpad) {
     const int lane = threadIdx.x & 31;
-    for (i64 i = (i64)blockIdx.x * NT + threadIdx.x; i < nx + 2; i += (i64)gridDim.x * NT)
-        xpad[i] = i < nx ? x[i] : 0.0;  // the segment kernel's aligned, padded copy of x
+    if (xpad)
+        for (i64 i = (i64)blockIdx.x * NT + threadIdx.x; i < nx + 2; i += (i64)gridDim.x * NT)
+            xpad[i] = i < nx ? x[i] : 0.0;  // the segment kernel's aligned, padded copy of x
     for (int l = blockIdx.x * NW + (threadIdx.x >> 5); l < n; l += gridDim.x * NW) {
         const H2Leaf L = leaves[l];
         const double v = h2_leaf(L, pb, x, lane);
@@ -968,10 +969,18 @@ struct DevFrees {  // frees build temporaries on every exit path
 
 }  // namespace
 
-void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s) {
+// x_hat of the column leaves [l0, l1) (the host pipeline runs this per arrived x piece)
+void h2_leaf_launch(const H2 &h, int l0, int l1, const double *x, cudaStream_t s) {
+    if (l1 <= l0) return;
+    const int g = (int)std::max<i64>(1, std::min<i64>(148 * 8, (l1 - l0 + NW - 1) / NW));
+    h2_leaf_kernel<<<g, NT, 0, s>>>(h.leaves + l0, l1 - l0, h.pb, x, h.xh, 0, nullptr);
+}
+
+void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s, bool leaves) {
     static const int dbg = getenv("LEVYH_H2_DBG") ? atoi(getenv("LEVYH_H2_DBG")) : 0;  // timing experiments only
     auto grid = [](i64 n, int per_sm) { return (int)std::max<i64>(1, std::min<i64>(148 * per_sm, (n + NW - 1) / NW)); };
-    h2_leaf_kernel<<<grid(h.nleaf, 8), NT, 0, s>>>(h.leaves, h.nleaf, h.pb, x, h.xh, nx, xpad);
+    if (leaves) h2_leaf_kernel<<<grid(h.nleaf, 8), NT, 0, s>>>(h.leaves, h.nleaf, h.pb, x, h.xh, nx, xpad);
+    else if (nx > 0) h2_leaf_kernel<<<grid(nx / 256 + 1, 8), NT, 0, s>>>(h.leaves, 0, h.pb, x, h.xh, nx, xpad);
     h2_up_kernel<<<h.nsub_up, NT, 8 * (size_t)h.up_xmax, s>>>(h.ups, h.up_lv, h.up_chain, h.up_cbeg, h.up_sub,
                                                              h.up_xcnt, h.cnt, h.maxh_up, h.tu, h.xh, dbg);
     h2_couple_kernel<<<grid(h.ncnode, 4), NT, 0, s>>>(h.crec, h.ncnode, h.cpls, h.sb, h.xh, h.wg);
@@ -1288,7 +1297,21 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     };
     run_copies(cj, Z.d_arena, ZS.d_arena);
     run_copies(qj, S[0].Qt, ZS.d_arena);
-    plan = build_mv_plan(ZS, ZS.leafblocks, st);
+    // LEVYH_H2_SPLIT_DENSE=1: row-basis pieces here, dense leaves in a lean plan of their own
+    // streamed on a forked stream beside the walk.  Measured slower at N = 2^20 (the row-basis
+    // pass alone is per-segment latency bound, 74 us, and the two branches barely overlap), so
+    // the combined plan (dense leaf + row basis in one ring slot) is the default.
+    if (getenv("LEVYH_H2_SPLIT_DENSE")) {
+        std::vector<int32_t> dense_ids, q_ids;
+        for (int32_t b : ZS.leafblocks) (ZS.nodes[b].kind == K_DENSE ? dense_ids : q_ids).push_back(b);
+        plan = build_mv_plan(ZS, q_ids, st);
+        plan->dense = build_mv_plan(ZS, dense_ids, st);
+        plan->dense->lean = true;
+        LH_CUDA(cudaStreamCreateWithFlags(&plan->fork, cudaStreamNonBlocking));
+        for (cudaEvent_t &e : plan->fev) LH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    } else {
+        plan = build_mv_plan(ZS, ZS.leafblocks, st);
+    }
     auto h = std::make_shared<H2>();
     const Side &C = S[1], &R = S[0];
     // subtrees of height <= split; the split is the largest (<= 6) whose subtrees' transfer
@@ -1540,6 +1563,10 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     h->up_cbeg = dupload(up_cbeg, st);
     h->crec = dupload(crec, st);
     h->nleaf = (int)leaves.size();
+    for (size_t l = 0; l < leaves.size(); ++l) {
+        if (l > 0 && leaves[l].x0 < leaves[l - 1].x0) return false;  // row order (host pipeline)
+        h->leaf_end.push_back(leaves[l].x0 + leaves[l].rows);
+    }
     h->ncnode = (int)crec.size();
     h->up_xcnt = dupload(up_xcnt, st);
     h->dn_ycnt = dupload(dn_ycnt, st);

@@ -12,6 +12,6 @@ import csv
 rows=list(csv.reader(open('gpurun_out/lh2.csv')))
 hi=[i for i,r in enumerate(rows) if r and r[0]=='ID'][0]; h=rows[hi]
 ki,mi,vi=h.index('Kernel Name'),h.index('Metric Name'),h.index('Metric Value')
-for r in rows[hi+1:][-10:]:
+for r in rows[hi+1:][-14:]:
     if len(r)>vi: print(r[ki][:50], r[vi])
 PY
