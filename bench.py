@@ -200,7 +200,7 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
                      propagator_nearfield_lowrank_leaves=int(ps[4]),
                      propagator_coarsening_merges=int(ps[5]),
                      propagator_single_rhs_form=["H-matrix", "shared leaf bases", "nested H2 bases"][int(ps[6])],
-                     propagator_form_probe_rel_err=float(ps[7]), propagator_leaf_basis_mean=float(ps[8]),
+                     propagator_form_probe_rel_err=f"{float(ps[7]):.2e}", propagator_leaf_basis_mean=float(ps[8]),
                      propagator_basis_transfer_coupling_scalars=int(ps[9]))
     elif method == "inverse":
         times.update(inverse_factors_s=t_prep)

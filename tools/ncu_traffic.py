@@ -10,7 +10,8 @@ import json
 import subprocess
 import sys
 
-NAMES = {"seg_tma_kernel": "seg(Z)", "vtx_kernel<8>": "vtx(Z)"}
+NAMES = {"seg_tma_kernel": "seg(Z)", "vtx_kernel<8>": "vtx(Z)", "h2_leaf_kernel": "h2_leaf",
+         "h2_up_kernel": "h2_up", "h2_couple_kernel": "h2_couple", "h2_down_kernel": "h2_down"}
 
 
 def main():
@@ -25,7 +26,7 @@ def main():
     res = {}
     for r in rows[2:]:
         name = r[h.index("Kernel Name")]
-        key = next((v for k, v in NAMES.items() if name.replace("void ", "").startswith(k)), None)
+        key = next((v for k, v in NAMES.items() if k in name.split("(")[0]), None)
         if key is None or key in res:
             continue
         rd = float(r[h.index("dram__bytes_read.sum")]) * scale[units[h.index("dram__bytes_read.sum")]]
