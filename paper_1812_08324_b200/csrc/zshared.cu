@@ -731,6 +731,11 @@ __device__ __forceinline__ double h2_couple(const H2Down &D, const H2Cpl *cpls, 
     return acc;
 }
 
+// Programmatic dependent launch: a walk kernel stages its static operands (descriptors,
+// transfer / coupling prefetches) while the previous kernel drains, then waits for its results.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // global -> shared copy by the whole CTA with every load of a thread in flight at once
 template <class T>
 __device__ __forceinline__ void h2_copy_in(T *dst, const T *src, int n) {
@@ -754,6 +759,7 @@ __device__ __forceinline__ void h2_copy_in(T *dst, const T *src, int n) {
 __global__ void __launch_bounds__(NT) h2_leaf_kernel(const H2Leaf *leaves, int n, const double *pb, const double *x,
                                                     double *xh, i64 nx, double *xpad) {
     const int lane = threadIdx.x & 31;
+    pdl_trigger();
     if (xpad)
         for (i64 i = (i64)blockIdx.x * NT + threadIdx.x; i < nx + 2; i += (i64)gridDim.x * NT)
             xpad[i] = i < nx ? x[i] : 0.0;  // the segment kernel's aligned, padded copy of x
@@ -780,14 +786,16 @@ __global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int
     const int32_t *lv = up_lv + (i64)s * (maxh + 1);
     const int u0 = lv[0], nu = lv[maxh] - u0, c0 = up_cbeg[s], nc = up_cbeg[s + 1] - c0;
     {  // descriptors (subtree + climb chain) and x_hat slots to shared memory; transfers to L2
+        pdl_trigger();
         constexpr int W = (int)(sizeof(H2Up) / 4);
         h2_copy_in(reinterpret_cast<int32_t *>(su), reinterpret_cast<const int32_t *>(ups + u0), nu * W);
         for (int i = threadIdx.x; i < nc * W; i += NT)
             reinterpret_cast<int32_t *>(sc)[i] = reinterpret_cast<const int32_t *>(ups + up_chain[c0 + i / W])[i % W];
-        h2_copy_in(xs, xh + SB.base, up_xcnt[s]);
         const char *t = reinterpret_cast<const char *>(tu + SB.tbeg);
         for (i64 o = 128 * (i64)threadIdx.x; o < 8 * (i64)SB.tlen; o += 128 * NT)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
+        pdl_wait();  // the leaves' x_hat
+        h2_copy_in(xs, xh + SB.base, up_xcnt[s]);
     }
     __syncthreads();
     for (int q = w; q < nc; q += NW) {  // the climb's transfers to L2
@@ -855,6 +863,13 @@ __device__ __forceinline__ double h2_apply_g16(const double *T, i64 ldi, int n, 
 __global__ void __launch_bounds__(NT, 4) h2_couple_kernel(const H2CRec *crec, int n, const H2Cpl *cpls,
                                                          const double *sb, const double *xh, double *wg) {
     const int lane = threadIdx.x & 31;
+    pdl_trigger();
+    for (int q = blockIdx.x * NW + (threadIdx.x >> 5); q < n; q += gridDim.x * NW) {  // couplings -> L2
+        const H2CRec R = crec[q];
+        const char *t = reinterpret_cast<const char *>(sb + R.soff);
+        for (int o = 128 * lane; o < 8 * R.kr * R.kc; o += 128 * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
+    }
+    pdl_wait();  // x_hat of every column cluster
     for (int q = blockIdx.x * NW + (threadIdx.x >> 5); q < n; q += gridDim.x * NW) {
         const H2CRec R = crec[q];
         const double xv = lane < R.kc ? __ldcg(xh + R.xoff + lane) : 0.0;
@@ -887,15 +902,16 @@ __global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const
     {
         h2_copy_in(reinterpret_cast<int32_t *>(sd), reinterpret_cast<const int32_t *>(dns + n0),
                    nn * (int)(sizeof(H2Down) / 4));
-        h2_copy_in(ws, wg + SB.base, dn_ycnt[s]);
-        for (int q = w; q < np; q += NW) {
-            const H2Down D = dns[dn_path[pa + q]];
-            if (lane < D.k) pw[q][lane] = wg[D.yoff + lane];
-            if (lane == 0) pd[q] = D;
-        }
+        for (int q = w; q < np; q += NW)
+            if (lane == 0) pd[q] = dns[dn_path[pa + q]];
         const char *t = reinterpret_cast<const char *>(td + SB.tbeg);
         for (i64 o = 128 * (i64)threadIdx.x; o < 8 * (i64)SB.tlen; o += 128 * NT)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(t + o));
+        pdl_wait();  // the couplings w
+        h2_copy_in(ws, wg + SB.base, dn_ycnt[s]);
+        __syncthreads();
+        for (int q = w; q < np; q += NW)
+            if (lane < pd[q].k) pw[q][lane] = wg[pd[q].yoff + lane];
     }
     __syncthreads();
     if (w == 0 && np > 1 && !(dbg & 4)) {  // transfers down the path
@@ -981,11 +997,30 @@ void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx,
     auto grid = [](i64 n, int per_sm) { return (int)std::max<i64>(1, std::min<i64>(148 * per_sm, (n + NW - 1) / NW)); };
     if (leaves) h2_leaf_kernel<<<grid(h.nleaf, 8), NT, 0, s>>>(h.leaves, h.nleaf, h.pb, x, h.xh, nx, xpad);
     else if (nx > 0) h2_leaf_kernel<<<grid(nx / 256 + 1, 8), NT, 0, s>>>(h.leaves, 0, h.pb, x, h.xh, nx, xpad);
-    h2_up_kernel<<<h.nsub_up, NT, 8 * (size_t)h.up_xmax, s>>>(h.ups, h.up_lv, h.up_chain, h.up_cbeg, h.up_sub,
-                                                             h.up_xcnt, h.cnt, h.maxh_up, h.tu, h.xh, dbg);
-    h2_couple_kernel<<<grid(h.ncnode, 4), NT, 0, s>>>(h.crec, h.ncnode, h.cpls, h.sb, h.xh, h.wg);
-    h2_down_kernel<<<h.nsub_dn, NT, 16 * (size_t)h.dn_ymax, s>>>(h.dns, h.dn_path, h.dn_pbeg, h.dn_lv, h.dn_sub,
-                                                                h.dn_ycnt, h.maxh_dn, h.dn_ymax, h.td, h.wg, tcol, dbg);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    auto cfg = [&](int g, size_t smem) {
+        cudaLaunchConfig_t c = {};
+        c.gridDim = dim3(g);
+        c.blockDim = dim3(NT);
+        c.dynamicSmemBytes = smem;
+        c.stream = s;
+        c.attrs = at;
+        c.numAttrs = 1;
+        return c;
+    };
+    cudaLaunchConfig_t cu = cfg(h.nsub_up, 8 * (size_t)h.up_xmax), cc = cfg(grid(h.ncnode, 4), 0),
+                       cd = cfg(h.nsub_dn, 16 * (size_t)h.dn_ymax);
+    LH_CUDA(cudaLaunchKernelEx(&cu, h2_up_kernel, (const H2Up *)h.ups, (const int32_t *)h.up_lv,
+                               (const int32_t *)h.up_chain, (const int32_t *)h.up_cbeg, (const H2Sub *)h.up_sub,
+                               (const int32_t *)h.up_xcnt, h.cnt, h.maxh_up, (const double *)h.tu, h.xh, dbg));
+    LH_CUDA(cudaLaunchKernelEx(&cc, h2_couple_kernel, (const H2CRec *)h.crec, h.ncnode, (const H2Cpl *)h.cpls,
+                               (const double *)h.sb, (const double *)h.xh, h.wg));
+    LH_CUDA(cudaLaunchKernelEx(&cd, h2_down_kernel, (const H2Down *)h.dns, (const int32_t *)h.dn_path,
+                               (const int32_t *)h.dn_pbeg, (const int32_t *)h.dn_lv, (const H2Sub *)h.dn_sub,
+                               (const int32_t *)h.dn_ycnt, h.maxh_dn, h.dn_ymax, (const double *)h.td,
+                               (const double *)h.wg, tcol, dbg));
     LH_CUDA(cudaGetLastError());
 }
 
