@@ -2547,8 +2547,11 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
             // (or two) DMMA matmats: U <- 2 Z U - U, or U <- Z (A- U)
             const i64 n = Hm.nrows, ldk = mm_pad(nrhs);
             double *Xr = ctx.mm[0].ensure(n * ldk), *Yr = ctx.mm[1].ensure(n * ldk);
-            MmBufs bz = mm_bufs(ctx, *S.mvZ, ldk);
+            // the two plans share the context's grow-only scratch: size it for both before taking
+            // pointers (a later, larger request would reallocate under the first plan's pointers)
+            mm_bufs(ctx, *S.mvZ, ldk);
             MmBufs bm = mm_bufs(ctx, Pm, ldk);
+            MmBufs bz = mm_bufs(ctx, *S.mvZ, ldk);
             mm_transpose(u, ldu, Xr, ldk, n, nrhs, true, ctx.stream);
             for (int k = 0; k < nsteps; ++k) {
                 if (shape == 2) {

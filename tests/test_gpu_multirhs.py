@@ -76,3 +76,17 @@ def test_run_cn_multi_rhs(P, name):
     Fo = O.hlu(Op, 1e-10)
     uo = O.run_cn(Om, Fo, U0[:, 5], steps)
     assert _rel(UK[:, 5], uo) <= 1e-8
+
+
+def test_run_cn_multi_rhs_coarsened_propagator(P):
+    """cfg4's operator at N = 32767: the coarsened propagator has fewer low-rank blocks than A-,
+    so the two matmat plans size the shared multi-RHS scratch differently (regression: the
+    first plan's scratch pointers must survive the second plan's request)."""
+    n = 2 ** 14
+    s = P.FracCNSystem(P.power_measure(1, 0.5), 0.0, 0.0, 0.0, n, 1.0 / n)
+    s.prepare(P.HConfig(n_min=64, eps1=1e-10), 1e-10, method="propagator")
+    U0 = np.random.default_rng(3).standard_normal((s.N, 64))
+    UK = P.run_cn(s, U0, 3)
+    for k in (0, 37, 63):
+        uk = P.run_cn(s, U0[:, k], 3)
+        assert np.linalg.norm(UK[:, k] - uk) <= 1e-10 * np.linalg.norm(uk)
