@@ -208,7 +208,9 @@ int lh_cn_step_host(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, const d
  * steps applied to u_dev in place.  method 1: out[0..5] mean ms of vtx(H-), seg(H-),
  * vtx(L^-1), seg(L^-1), vtx(U^-1), seg(U^-1); out[6..11] their algorithmic bytes;
  * out[12..14] stored scalars of H-, L^-1, U^-1.  method 2: out[0..1], out[6..7] for
- * vtx(Z), seg(Z) (others 0); out[12] H-, out[13] Z.  out[15] stored scalars of the factor. */
+ * phase 1 of Z (V^T x, or the H2 walk when lh_propagator_stats reports form 2) and the
+ * segment kernel (others 0); out[12] H-, out[13] Z in the form the step streams.  out[15]
+ * stored scalars of the factor. */
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev,
                     int32_t iters, int32_t method, double *out_host);
 /* out[0..4] = H-LU task count, planning seconds, temp bytes, executor seconds, number of

@@ -652,6 +652,8 @@ __device__ __forceinline__ double h2_leaf(const H2Leaf &L, const double *pb, con
     const double x0 = lane < L.rows ? x[L.x0 + lane] : 0.0;
     const double x1 = lane + 32 < L.rows ? x[L.x0 + lane + 32] : 0.0;
     double mine = 0.0;
+    // 8 basis columns per round trip: 16 columns (one trip for most leaves) measured slower,
+    // 30.9 vs 24.4 us, the register cost halves the resident warps
     for (int c = 0; c < L.k; c += 8) {
         double p[8], q[8];
 #pragma unroll
