@@ -85,3 +85,13 @@ def test_cfg4_multi_rhs_columns(P):
     UK = P.run_cn(s, U0, 10)
     for k in (0, 13, 31):
         assert _rel(UK[:, k], P.run_cn(s, U0[:, k], 10)) <= 1e-11
+
+
+def test_cfg3_propagator_nested_bases(P, cfg3):
+    """At N = 2^20 the CN step streams Z in nested (H2) form, checked at build time against the
+    H-form of Z on a probe vector."""
+    s, _ = cfg3
+    st = s.factor.propagator_stats()
+    assert st[6] == 2.0  # nested H2 bases in use
+    assert st[7] <= 1e-10  # probe relative error of the H2 form against the H-form
+    assert 4.0 <= st[8] <= 32.0  # mean leaf basis size
