@@ -58,6 +58,16 @@ CFG5 = dict(workload="cfg5: fractional Laplacian s=0.8 on [-1,1], N=2^22-1, a=0.
 METRIC5 = "cfg5 (N=2^22): assembly + H-LU time, CN steps/s"
 
 
+def cfg3_config(args, N, world):
+    """The `config` of a cfg3 line: identical in the b200 and the reference arm (the algorithm
+    each arm runs is the top-level `algorithm` key)."""
+    return {"workload": CFG3["workload"] if args.n is None else f"cfg3 operator at n={args.n}",
+            "N": N, "leaf": CFG3["leaf"], "eps1": CFG3["eps1"], "eps2": CFG3["eps2"],
+            "parallelism": (f"stepping: replicas x{world}; assembly (ACA): admissible blocks sharded over "
+                            f"{world} ranks + NCCL all-gather of the factors" if world > 1 else "replicas x1"),
+            "l2": "inputs larger than L2 (the operator streamed every step is >= 0.8 GB vs 126 MB L2)"}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -214,24 +224,37 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
 
 
 def cpu_reference_steps(P, s, F, Hm, u0, n_steps, max_seconds=None):
-    """The reference algorithm (oracle restatement of hops.matvec + hops.solve) on host cores."""
-    from oracle import export_bridge as EB
-    from oracle import levyh_oracle as O
+    """The reference algorithm on host cores, on the GPU-built factors exported to host:
+    levyh.hops.solve(F, levyh.hops.matvec(H-, u)) of the unmodified reference (baseline/_ref)
+    when it is installed (kind "reference"), else the oracle restatement (kind "port")."""
+    from oracle import levyh_bridge as LB
 
     leaf = CFG3["leaf"]
     t0 = time.perf_counter()
-    Fr = EB.tree_from_export(s.x, leaf, *P.hmatrix.export_layout(F.h))
-    Hr = EB.tree_from_export(s.x, leaf, *P.hmatrix.export_layout(Hm))
+    levyh = LB.import_levyh()
+    if levyh is not None:
+        hops = levyh.hops
+        Fr = hops.HFactorization(LB.hmatrix_from_export(levyh, s.x, leaf, *P.hmatrix.export_layout(F.h)),
+                                 CFG3["eps2"])
+        Hr = LB.hmatrix_from_export(levyh, s.x, leaf, *P.hmatrix.export_layout(Hm))
+        step, kind = (lambda u: hops.solve(Fr, hops.matvec(Hr, u))), "reference"
+    else:
+        from oracle import export_bridge as EB
+        from oracle import levyh_oracle as O
+
+        Fr = EB.tree_from_export(s.x, leaf, *P.hmatrix.export_layout(F.h))
+        Hr = EB.tree_from_export(s.x, leaf, *P.hmatrix.export_layout(Hm))
+        step, kind = (lambda u: O.lu_solve(Fr, O.hmatvec(Hr, u))), "port"
     t_export = time.perf_counter() - t0
     u = np.asarray(u0, dtype=float).copy()
     times = []
     for k in range(n_steps):
         t = time.perf_counter()
-        u = O.lu_solve(Fr, O.hmatvec(Hr, u))
+        u = step(u)
         times.append(time.perf_counter() - t)
         if max_seconds and sum(times) > max_seconds:
             break
-    return u, times, t_export
+    return u, times, t_export, kind
 
 
 def cpu_info():
@@ -317,6 +340,30 @@ def run_b200(args, world, rank, local):
            "path": "lh_cn_step_host (C ABI, levy.step_cn) with u in pinned host memory, one call per "
                    "step (copies in and out inside the call)"}
 
+    # ---- the reference algorithm on the GPU (A- matvec + substitution solve on the DAG
+    # executor, hops.py:65-70 + :424-432) on the same factors, next to the default path
+    if args.method != "substitution" and not args.no_sub:
+        usub = torch.from_numpy(u0.copy()).cuda()
+
+        def sub_steps(k):
+            P._lib.check(L.lh_cn_steps(ctx.h, Hm.handle, F.h.handle, usub.data_ptr(), N, 1, int(k), 0), ctx.h)
+
+        sub_steps(1)
+        torch.cuda.synchronize()
+        ks = 3
+        lib_stream = ctx.torch_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(lib_stream)
+        sub_steps(ks)
+        e1.record(lib_stream)
+        torch.cuda.synchronize()
+        sub_ms = e0.elapsed_time(e1) / ks
+        sub_line = {"steps_per_s": round(1000.0 / sub_ms, 3), "ms_per_step": round(sub_ms, 3), "steps": ks,
+                    "algorithm": "A- matvec + forward/backward substitution (the reference algorithm) on "
+                                 "the persistent DAG executor, same factors"}
+    else:
+        sub_line = None
+
     # ---- per-kernel roofline (CUDA events on the library stream)
     prof = np.zeros(16)
     uprof = torch.from_numpy(u0.copy()).cuda()
@@ -362,26 +409,36 @@ def run_b200(args, world, rank, local):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (BASELINE.json configs[2]; seeded/closed-form inputs, no dataset)",
-           "config": {"workload": CFG3["workload"] if args.n is None else f"cfg3 operator at n={args.n}",
-                      "N": N, "leaf": CFG3["leaf"], "eps1": CFG3["eps1"], "eps2": CFG3["eps2"],
-                      "solve": SOLVE_DESC[args.method],
-                      "parallelism": (f"stepping: replicas x{world}; assembly (ACA): admissible blocks "
-                                      f"sharded over {world} ranks + NCCL all-gather of the factors"
-                                      if world > 1 else "replicas x1"),
-                      "l2": f"inputs larger than L2 ({step_bytes / 1e9:.1f} GB streamed per step vs 126 MB L2)"},
+           "config": cfg3_config(args, N, world), "algorithm": SOLVE_DESC[args.method],
            "clocks": sampler.summary(), "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
            "gpu_launches_per_step": launches_per_step,
+           "substitution_on_gpu": sub_line,
            "roofline": roofline, "phases": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in times.items()}}
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        ucpu, ts, t_exp = cpu_reference_steps(P, s, F, Hm, u0, args.cpu_steps, max_seconds=30)
+        ucpu, ts, t_exp, kind = cpu_reference_steps(P, s, F, Hm, u0, args.cpu_steps, max_seconds=30)
         ci = cpu_info()
+        impl = ("levyh.hops.matvec + levyh.hops.solve of the unmodified reference (baseline/_ref)"
+                if kind == "reference" else "oracle/levyh_oracle.py (restated hops.matvec + hops.solve)")
         out["cpu_baseline"] = {"value": round(len(ts) / sum(ts), 5), "unit": "steps/s",
                                "cores": ci["cores"], "blas_threads": ci.get("blas_threads"),
-                               "cpu_model": ci.get("cpu_model"), "kind": "port",
+                               "cpu_model": ci.get("cpu_model"), "kind": kind,
                                "sample": f"{len(ts)} CN steps (matvec + substitution solve) of the cfg3 operator "
-                                         f"at N=2^20 with oracle/levyh_oracle.py on GPU-built factors exported "
+                                         f"at N=2^20 with {impl} on the GPU-built factors exported "
                                          f"to host ({t_exp:.1f}s export, untimed)"}
+        # parity at the headline size: the same k steps from u0 on the GPU (default method and
+        # the reference algorithm) against the CPU reference on the same factors
+        k = len(ts)
+        ug = torch.from_numpy(u0.copy()).cuda()
+        steps(k, ug)
+        us = torch.from_numpy(u0.copy()).cuda()
+        P._lib.check(L.lh_cn_steps(ctx.h, Hm.handle, F.h.handle, us.data_ptr(), N, 1, k, 0), ctx.h)
+        torch.cuda.synchronize()
+        rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+        out["parity"] = {"steps": k, "rel_l2_vs_oracle": rel(ug.cpu().numpy(), ucpu),
+                         "rel_l2_substitution_vs_oracle": rel(us.cpu().numpy(), ucpu),
+                         "method": args.method, "tolerance": 1e-8,
+                         "oracle": f"{impl} on the same exported factors, from the same u0"}
     if rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -652,35 +709,142 @@ def run_gauss(args, world, rank, local):
     print(json.dumps(out), flush=True)
 
 
-def run_reference(args, world, rank, local):
-    """--impl reference: the reference algorithm on host cores (rank 0 only)."""
-    if rank != 0:
-        return
-    import torch
-
+def export_factors(args):
+    """--export-factors DIR: the reference arm's input preparation, run as a CHILD process so
+    the process that times the reference never loads the native library.  Builds the cfg3
+    operators on the GPU (the reference cannot assemble them at N = 2^20) and writes
+    the exported layouts (oracle/levyh_bridge.py reads them) of A- and of the H-LU factor of A+,
+    and with --export-plus also the unfactored A+ (for timing the reference hops.hlu)."""
     import paper_1812_08324_b200 as P
 
-    s, F, Hm, times = build_system(P, n=args.n, method="none")  # factors only
-    u0 = np.maximum(np.exp(s.x) - 1.0, 0.0)
+    cfg = CFG3
+    n = args.n or cfg["n"]
+    s = P.FracCNSystem(P.cgmy_measure(1.0, 5.0, 10.0, 0.5), cfg["a"], cfg["b"], cfg["c"], n, cfg["dt"],
+                       L=cfg["L"], L_W=cfg["L_W"], drift_compensation=True)
+    Hp, Hm = s.build_pair(P.HConfig(n_min=cfg["leaf"], eps1=cfg["eps1"]))
+
+    def dump(H, name):
+        d = os.path.join(args.export_factors, name)
+        os.makedirs(d, exist_ok=True)
+        for k, v in zip(("recs", "arena", "ranks", "perm"), P.hmatrix.export_layout(H)):
+            np.save(os.path.join(d, k + ".npy"), v)
+
+    np.save(os.path.join(args.export_factors, "x.npy"), s.x)
+    if args.export_plus:
+        dump(Hp, "plus")
+    dump(Hm, "minus")
+    F = P.hlu(Hp, cfg["eps2"])
+    dump(F.h, "factor")
+
+
+def _scratch_dir(need_gb):
+    import shutil
+    import tempfile
+
+    for base in ("/dev/shm", None):
+        try:
+            if base is None or shutil.disk_usage(base).free > need_gb * 1e9:
+                return tempfile.mkdtemp(prefix="levyh_ref_", dir=base)
+        except Exception:
+            continue
+    return tempfile.mkdtemp(prefix="levyh_ref_")
+
+
+def reference_inputs(args, plus=False):
+    """Run the export child and load the factors as the REAL reference's block types
+    (levyh from baseline/_ref) -- or as the oracle restatement's when levyh is not installed.
+    Returns (kind, api, x, Fh, Hm, Hp_or_None, export_seconds)."""
+    import shutil
+
+    from oracle import levyh_bridge as LB
+
+    d = _scratch_dir(40 if plus else 30)
+    t0 = time.perf_counter()
+    try:
+        cmd = [sys.executable, os.path.abspath(__file__), "--export-factors", d]
+        if args.n:
+            cmd += ["--n", str(args.n)]
+        if plus:
+            cmd += ["--export-plus"]
+        env = dict(os.environ)
+        for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+            env.pop(k, None)
+        subprocess.run(cmd, check=True, env=env)
+        t_exp = time.perf_counter() - t0
+        x = np.load(os.path.join(d, "x.npy"))
+        levyh = LB.import_levyh()
+        leaf = CFG3["leaf"]
+        if levyh is not None:
+            mk = lambda name: LB.hmatrix_from_export(levyh, x, leaf, *LB.load_export(os.path.join(d, name)))
+            Fh, Hm = mk("factor"), mk("minus")
+            Hp = mk("plus") if plus else None
+            return "reference", levyh, x, Fh, Hm, Hp, t_exp
+        from oracle import export_bridge as EB
+
+        mk = lambda name: EB.tree_from_export(x, leaf, *LB.load_export(os.path.join(d, name)))
+        return "port", None, x, mk("factor"), mk("minus"), (mk("plus") if plus else None), t_exp
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+
+
+def run_reference(args, world, rank, local):
+    """--impl reference: the reference's own CPU implementation of the path on the host cores
+    (rank 0 only): levyh.hops.matvec + levyh.hops.solve (hops.py:65-70, :424-432) of the
+    UNMODIFIED reference installed in baseline/_ref, stepping levyh.levy.run_cn's loop
+    (levy.py:309-330) on the cfg3 operators (exported from the GPU build by a child process).
+    --ref-phase hlu times levyh.hops.hlu on the exported, unfactored A+ instead."""
+    if rank != 0:
+        return
+    kind, levyh, x, Fh, Hm, Hp, t_exp = reference_inputs(args, plus=args.ref_phase == "hlu")
+    N = len(x)
+    if kind == "reference":
+        hops = levyh.hops
+        F = hops.HFactorization(Fh, CFG3["eps2"])
+        step = lambda u: hops.solve(F, hops.matvec(Hm, u))
+        impl_desc = ("levyh.hops.solve(F, levyh.hops.matvec(H-, u)) of the unmodified reference "
+                     "(baseline/_ref, levyh 0.1.0)")
+    else:
+        from oracle import levyh_oracle as O
+
+        step = lambda u: O.lu_solve(Fh, O.hmatvec(Hm, u))
+        impl_desc = "oracle/levyh_oracle.py restatement of hops.matvec + hops.solve (levyh not installed)"
+    ci = cpu_info()
+    if args.ref_phase == "hlu":
+        t = time.perf_counter()
+        if kind == "reference":
+            levyh.hops.hlu(Hp, CFG3["eps2"])
+        else:
+            from oracle import levyh_oracle as O
+
+            O.hlu(Hp, CFG3["eps2"])
+        t_lu = time.perf_counter() - t
+        print(json.dumps({"impl": "reference", "phase": "hlu", "N": N, "hlu_s": round(t_lu, 3),
+                          "kind": kind, "cores": ci["cores"], "blas_threads": ci.get("blas_threads"),
+                          "cpu_model": ci.get("cpu_model")}), flush=True)
+        return
+    u = np.maximum(np.exp(x) - 1.0, 0.0)
     warm = min(args.warmup, 1)
     k = max(1, min(args.steps, args.ref_steps))
-    u, ts, t_exp = cpu_reference_steps(P, s, F, Hm, u0, warm + k)
+    ts = []
+    for i in range(warm + k):
+        t = time.perf_counter()
+        u = step(u)
+        ts.append(time.perf_counter() - t)
     ts = ts[warm:]
-    ci = cpu_info()
     value = len(ts) / sum(ts)
     out = {"metric": METRIC, "value": round(value, 5), "unit": "steps/s", "n_gpus": world,
            "steps": len(ts), "warmup": warm, "ms_per_step": round(1000 * sum(ts) / len(ts), 2),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (BASELINE.json configs[2])", "impl": "reference",
-           "config": {"workload": CFG3["workload"], "N": s.N, "leaf": CFG3["leaf"], "eps1": CFG3["eps1"],
-                      "parallelism": "host cores (OpenBLAS threads)"},
+           "data": "synthetic (BASELINE.json configs[2]; seeded/closed-form inputs, no dataset)",
+           "impl": "reference", "config": cfg3_config(args, N, world),
+           "algorithm": "A- matvec + forward/backward substitution solve per step (hops.py:65-70, :424-432)",
            "cpu_baseline": {"value": round(value, 5), "unit": "steps/s", "cores": ci["cores"],
                             "blas_threads": ci.get("blas_threads"), "cpu_model": ci.get("cpu_model"),
-                            "kind": "port",
-                            "sample": f"{len(ts)} timed CN steps (+{warm} warm-up) of oracle hmatvec + lu_solve "
-                                      f"(restated levyh hops.matvec/hops.solve) on GPU-built cfg3 factors "
-                                      f"exported to host ({t_exp:.1f}s export, untimed); the reference "
-                                      f"cannot assemble at N=2^20 (SURVEY G7)"},
+                            "kind": kind,
+                            "sample": f"{len(ts)} timed CN steps (+{warm} warm-up) of {impl_desc} on the cfg3 "
+                                      f"factors built on the GPU by a child process and exported to host "
+                                      f"({t_exp:.1f}s, untimed; the reference cannot assemble at N=2^20, "
+                                      f"SURVEY G7); this process never loads the native library"},
            "e2e": {"value": round(value, 5), "unit": "steps/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -694,8 +858,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override half-grid n (N = 2n-1); default 2^19")
     ap.add_argument("--cpu-steps", type=int, default=3)
-    ap.add_argument("--ref-steps", type=int, default=5)
+    ap.add_argument("--ref-steps", type=int, default=100, help="cap on the reference arm's timed steps")
+    ap.add_argument("--ref-phase", default="steps", choices=["steps", "hlu"])
+    ap.add_argument("--export-factors", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--export-plus", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the GPU substitution-step timing")
     ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4", "cfg5", "gauss"])
     ap.add_argument("--method", default=None, choices=["propagator", "inverse", "substitution"],
                     help="per-step solve: one H-matvec of Z=(A+)^-1 (default; cfg5: substitution)")
@@ -703,12 +871,18 @@ def main():
     args.method_set = args.method is not None
     if args.method is None:
         args.method = "propagator"
+    if args.export_factors:
+        export_factors(args)
+        return
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
-    world, rank, local = dist_setup()
     if args.impl == "reference":
-        run_reference(args, world, rank, local)
-    elif args.workload == "cfg4":
+        # the reference arm runs on host cores only: no CUDA context, no native library
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        run_reference(args, world, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")))
+        return
+    world, rank, local = dist_setup()
+    if args.workload == "cfg4":
         run_cfg4(args, world, rank, local)
     elif args.workload == "cfg5":
         run_cfg5(args, world, rank, local)

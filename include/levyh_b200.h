@@ -130,6 +130,11 @@ int lh_hmat_memory(lh_ctx *ctx, const lh_hmat *h, int64_t *stats_host);
  * lowrank: a = U (m*rank col-major), b = V (n*rank col-major). */
 int lh_hmat_export_block(lh_ctx *ctx, const lh_hmat *h, int64_t block, double *a_host,
                          double *b_host);
+/* hmatrix.py:416-433 h_entry: entry (i, j) in tree order, found by descending the block tree
+ * on the host and reading only the containing leaf on the device (one value of a dense leaf,
+ * one row of U and of V of a low-rank leaf).  LH_EINVAL outside the matrix, LH_ETYPE in an
+ * LU-factored leaf. */
+int lh_hmat_entry(lh_ctx *ctx, const lh_hmat *h, int64_t i, int64_t j, double *out_host);
 
 /* Bulk export (host copies) for checkpointing and for timing the reference CPU path on
  * GPU-built factors.  sizes[0..2] = arena length (doubles), rank slots, permutation length.
@@ -170,6 +175,15 @@ int lh_solve(lh_ctx *ctx, lh_hmat *factor, double *b_dev, int64_t ldb, int32_t n
  * "singular triangular diagonal block at L.11..." (hops.py:179-182). */
 int lh_trisolve_dense(lh_ctx *ctx, lh_hmat *t, int32_t mode, int32_t unit, double *b_dev,
                       int64_t ldb, int32_t nrhs);
+/* hops.py:282-310 trisolve_lower / trisolve_upper_right with an H-matrix right-hand side B
+ * (same cluster trees as T): *out = a new H-matrix X, a deep copy of B (low-rank capacity 32;
+ * B is not modified) solved in place by the block recursion: mode 0 L X = B (unit_diagonal =
+ * unit, _trisolve_block "L"), mode 2 X U = B (_trisolve_right_upper; unit must be 0).
+ * Low-rank targets are recompressed at a Frobenius tail of eps2 relative (the reference passes
+ * 0 and keeps rounding-noise singular values; 1e-14 keeps the ranks bounded).
+ * A rank beyond the capacity fails with LH_ERANK. */
+int lh_trisolve_block(lh_ctx *ctx, lh_hmat *t, const lh_hmat *b, int32_t mode, int32_t unit, double eps2,
+                      lh_hmat **out);
 /* hops.py:147-156 lowrank_add_recompress: (u_out, v_out) = recompressed u1 v1^T + u2 v2^T,
  * smallest rank r with ||tail||_F <= eps2 ||sum||_F (QR, QR, SVD).  Device, column-major,
  * ld = m (u) / n (v); outputs hold r1 + r2 <= 48 columns; *r_out = r. */
@@ -191,9 +205,16 @@ int lh_propagator_stats(lh_hmat *factor, double *out_host);
 /* Kernel launches per CN step: kernel nodes of the step graph lh_cn_steps last captured
  * (methods 1 and 2), 0 before the first call. */
 int32_t lh_step_graph_kernels(lh_hmat *factor);
+/* Path the last lh_cn_steps / lh_cn_step_host call on this factor took: out[0] = step shape
+ * (0 substitution, 1 triangular inverses, 2 u <- 2 Z u - u on the CN pair, 3 u <- Z (A- u)),
+ * out[1] = 1 when the K right-hand sides ran as DMMA matmats (multi-RHS), out[2] = 1 when the
+ * host step ran pipelined, out[3] = kernel nodes of the single-RHS step graph. */
+int lh_cn_last_path(lh_hmat *factor, int32_t *out_host);
 /* levy.py:309-330 run_cn loop: U <- solve(F, Hm U), nsteps times, in place.
- * method 2 with Hm = 2I - A+ (the CN pair; checked once with a probe vector) runs
- * U <- 2 Z U - U, one H-matvec per step; any other Hm runs U <- Z (Hm U). */
+ * method 2 with Hm = 2I - A+ (the CN pair: Hm derived from this factor's A+ by
+ * lh_hmat_derive_toeplitz with lr_scale -1, every entry verified there) runs
+ * U <- 2 Z U - U, one H-matvec per step; any other Hm runs U <- Z (Hm U).
+ * nrhs >= 8 columns run as FP64 tensor-core (DMMA) matmats. */
 int lh_cn_steps(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev, int64_t ldu,
                 int32_t nrhs, int32_t nsteps, int32_t method);
 

@@ -63,6 +63,7 @@ SIGNATURES = [
     ("lh_hmat_structure", C.c_int, [P, P, P]),
     ("lh_hmat_memory", C.c_int, [P, P, P]),
     ("lh_hmat_export_block", C.c_int, [P, P, I64, P, P]),
+    ("lh_hmat_entry", C.c_int, [P, P, I64, I64, P]),
     ("lh_hmat_layout", C.c_int, [P, P, P]),
     ("lh_hmat_export_arena", C.c_int, [P, P, P, P, P]),
     ("lh_hmat_matvec", C.c_int, [P, P, P, I64, P, I64, I32]),
@@ -76,7 +77,9 @@ SIGNATURES = [
     ("lh_hmat_shard_unpack", C.c_int, [P, P, I32, P, I64]),
     ("lh_hmat_shard_finalize", C.c_int, [P, P]),
     ("lh_step_graph_kernels", I32, [P]),
+    ("lh_cn_last_path", C.c_int, [P, P]),
     ("lh_trisolve_dense", C.c_int, [P, P, I32, I32, P, I64, I32]),
+    ("lh_trisolve_block", C.c_int, [P, P, P, I32, I32, D, C.POINTER(P)]),
     ("lh_lowrank_add_recompress", C.c_int, [P, I64, I64, P, P, I32, P, P, I32, D, P, P, P]),
     ("lh_cn_steps", C.c_int, [P, P, P, P, I64, I32, I32, I32]),
     ("lh_cn_step_host", C.c_int, [P, P, P, P, P, I32]),

@@ -5,6 +5,9 @@
 // Reference: fractional.py:78-86 (window), :108-127 (power density),
 // :285-301 (_window_sums_1d), :362-405 (frac_stencil_1d / Poisson assembly),
 // levy.py:169-206 (local band, A+-), hmatrix.py:294-340 (build_from_dense).
+#include <unistd.h>
+
+#include <atomic>
 #include <chrono>
 #include <limits>
 #include <algorithm>
@@ -892,10 +895,40 @@ __global__ void copy_dense_kernel(const FillJob *jobs, int njobs, const double *
     }
 }
 
+// 64-bit tag unique across processes with overwhelming probability (checkpoints carry it)
+static uint64_t fresh_pair_tag() {
+    static std::atomic<uint64_t> ctr{0};
+    uint64_t z = (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count() ^
+                 ((uint64_t)getpid() << 32) ^ (0x9E3779B97F4A7C15ull * (ctr.fetch_add(1) + 1));
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z ? z : 1;
+}
+
+// Counts dense entries of D that are not those of 2I - S: exact negatives off the diagonal,
+// 2 - s within 8 ulp of 2 on it (1 +- dt/2 a_ii rounded separately).
+__global__ void pair_check_kernel(const FillJob *jobs, int njobs, const double *src,
+                                  const i64 *src_off, const double *dst, unsigned long long *bad) {
+    for (int b = blockIdx.x; b < njobs; b += gridDim.x) {
+        FillJob J = jobs[b];
+        unsigned long long nb = 0;
+        for (i64 e = threadIdx.x; e < J.m * J.n; e += NT) {
+            const i64 i = e % J.m, j = e / J.m;
+            const double sv = src[src_off[b] + e], dv = dst[J.off + e];
+            if (J.r0 + i == J.c0 + j) nb += !(fabs(dv - (2.0 - sv)) <= 8.0 * 2.220446049250313e-16 * 2.0);
+            else nb += !(dv == -sv);
+        }
+        if (nb) atomicAdd(bad, nb);
+    }
+}
+
 // Copy of `S` with LR capacity kcap (<= 0: tight = rank), LR U scaled by `scale`.
 // If t != nullptr dense blocks are refilled from the Toeplitz symbol, else copied.
 void derive(Ctx &ctx, const HMat &S, HMat &D, const double *t, double scale, int kcap) {
     LH_REQUIRE(!S.factored, LH_EINVAL, "cannot derive from a factored H-matrix");
+    D.cn_pair_tag = 0;
+    D.pair_tag = 0;
     D.rt = S.rt;
     D.ct = S.ct;
     D.rt_hold = S.rt_hold;
@@ -959,6 +992,25 @@ void derive(Ctx &ctx, const HMat &S, HMat &D, const double *t, double scale, int
         if (t) {
             ToepSrc s{t, D.nrows};
             dense_fill_kernel<ToepSrc><<<grid, NT, 0, ctx.stream>>>(s, d, (int)fj.size(), D.d_arena);
+            if (scale == -1.0) {
+                // CN pair provenance (lh_cn_steps: u <- 2 Z u - u is exact only for A- = 2I - A+):
+                // the low-rank blocks are (-U, V) by construction; check every dense entry
+                i64 *dso = dupload(so, ctx.stream);
+                unsigned long long *bad = dalloc<unsigned long long>(1);
+                LH_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), ctx.stream));
+                pair_check_kernel<<<grid, NT, 0, ctx.stream>>>(d, (int)fj.size(), S.d_arena, dso,
+                                                               D.d_arena, bad);
+                LH_CUDA(cudaGetLastError());
+                unsigned long long nbad = 1;
+                LH_CUDA(cudaMemcpyAsync(&nbad, bad, sizeof(nbad), cudaMemcpyDeviceToHost, ctx.stream));
+                LH_CUDA(cudaStreamSynchronize(ctx.stream));
+                cudaFree(bad);
+                cudaFree(dso);
+                if (nbad == 0) {
+                    if (!S.pair_tag) S.pair_tag = fresh_pair_tag();
+                    D.cn_pair_tag = S.pair_tag;
+                }
+            }
         } else {
             i64 *dso = dupload(so, ctx.stream);
             copy_dense_kernel<<<grid, NT, 0, ctx.stream>>>(d, (int)fj.size(), S.d_arena, D.d_arena, dso);

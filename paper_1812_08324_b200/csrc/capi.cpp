@@ -1,4 +1,5 @@
 // C-ABI of the B200 H-matrix engine (include/levyh_b200.h).
+#include <atomic>
 #include <cstring>
 
 #include "core.h"
@@ -37,7 +38,9 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2);
 void propagator_stats(HMat &F, double *out);
 int step_graph_kernels(HMat &F);
+void cn_last_path(HMat &F, int32_t *out);
 void trisolve_dense(Ctx &ctx, HMat &T, int mode, bool unit, double *b, i64 ldb, int nrhs);
+void trisolve_block(Ctx &ctx, HMat &T, HMat &X, int mode, bool unit, double eps2);
 void build_toeplitz_shard(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg, int rank,
                           int world);
 i64 shard_pack(Ctx &ctx, HMat &H, double *buf, i64 cap);
@@ -97,6 +100,11 @@ Ctx::~Ctx() {
     if (scratch) cudaFree(scratch);
     if (owns_stream) cudaStreamDestroy(stream);
 }
+uint64_t next_hmat_id() {
+    static std::atomic<uint64_t> ctr{1};
+    return ctr.fetch_add(1);
+}
+
 HMat::~HMat() {
     mv_plan.reset();
     solve_plan.reset();
@@ -461,6 +469,44 @@ int lh_hmat_memory(lh_ctx *ctx, const lh_hmat *h, int64_t *stats) {
     });
 }
 
+int lh_hmat_entry(lh_ctx *ctx, const lh_hmat *h, int64_t i, int64_t j, double *out) {
+    return guard(ctx, [&] {
+        const HMat &H = h->h;
+        LH_REQUIRE(i >= 0 && i < H.nrows && j >= 0 && j < H.ncols, LH_EINVAL, "entry outside the matrix");
+        int32_t b = H.root;
+        while (H.nodes[b].kind == K_HIER) {  // refined dense leaves keep their leaf kind
+            const Node &nd = H.nodes[b];
+            const int q = (i - nd.r0 >= nd.rs ? 2 : 0) + (j - nd.c0 >= nd.cs ? 1 : 0);
+            b = nd.kid[q];
+        }
+        const Node &nd = H.nodes[b];
+        LH_REQUIRE(nd.kind != K_FDENSE, LH_ETYPE, "cannot read an entry of an LU-factored leaf");
+        cudaStream_t s = ctx->c.stream;
+        const i64 li = i - nd.r0, lj = j - nd.c0;
+        if (nd.kind == K_LR) {
+            int32_t r = 0;
+            LH_CUDA(cudaMemcpyAsync(&r, H.d_ranks + nd.rslot, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            LH_CUDA(cudaStreamSynchronize(s));
+            std::vector<double> u(std::max(r, 1)), v(std::max(r, 1));
+            if (r > 0) {
+                LH_CUDA(cudaMemcpy2DAsync(u.data(), sizeof(double), H.d_arena + nd.uoff + li,
+                                          sizeof(double) * nd.m, sizeof(double), r, cudaMemcpyDeviceToHost, s));
+                LH_CUDA(cudaMemcpy2DAsync(v.data(), sizeof(double), H.d_arena + nd.voff + lj,
+                                          sizeof(double) * nd.n, sizeof(double), r, cudaMemcpyDeviceToHost, s));
+                LH_CUDA(cudaStreamSynchronize(s));
+            }
+            double acc = 0.0;
+            for (int c = 0; c < r; ++c) acc += u[c] * v[c];
+            *out = acc;
+        } else {
+            LH_REQUIRE(nd.kind == K_DENSE, LH_ETYPE, "entry in a structurally zero block");
+            LH_CUDA(cudaMemcpyAsync(out, H.d_arena + nd.doff + li + lj * nd.m, sizeof(double),
+                                    cudaMemcpyDeviceToHost, s));
+            LH_CUDA(cudaStreamSynchronize(s));
+        }
+    });
+}
+
 int lh_hmat_export_block(lh_ctx *ctx, const lh_hmat *h, int64_t block, double *a, double *b) {
     return guard(ctx, [&] {
         const HMat &H = h->h;
@@ -582,9 +628,35 @@ int lh_propagator_stats(lh_hmat *f, double *out) {
 
 int32_t lh_step_graph_kernels(lh_hmat *f) { return step_graph_kernels(f->h); }
 
+int lh_cn_last_path(lh_hmat *f, int32_t *out) {
+    return guard(nullptr, [&] { cn_last_path(f->h, out); });
+}
+
 int lh_trisolve_dense(lh_ctx *ctx, lh_hmat *t, int32_t mode, int32_t unit, double *b, int64_t ldb,
                       int32_t nrhs) {
     return guard(ctx, [&] { trisolve_dense(ctx->c, t->h, mode, unit != 0, b, ldb, nrhs); });
+}
+
+int lh_trisolve_block(lh_ctx *ctx, lh_hmat *t, const lh_hmat *b, int32_t mode, int32_t unit, double eps2,
+                      lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        LH_REQUIRE(mode == 0 || mode == 2, LH_EINVAL, "block right-hand sides: mode 0 (L X = B) or 2 (X U = B)");
+        LH_REQUIRE(!(mode == 2 && unit), LH_EINVAL, "unit_diagonal right solves are not supported on blocks");
+        LH_REQUIRE(!b->h.factored, LH_EINVAL, "right-hand side must not be LU-factored");
+        LH_REQUIRE(b->h.nrows == t->h.nrows && b->h.ncols == t->h.ncols && b->h.rt == t->h.rt &&
+                       b->h.ct == t->h.ct,
+                   LH_EINVAL, "block right-hand side must share the triangle's cluster trees");
+        o = new lh_hmat();
+        derive(ctx->c, b->h, o->h, nullptr, 1.0, 32);  // deep copy (hops.py:294, :307)
+        trisolve_block(ctx->c, t->h, o->h, mode, unit != 0, eps2);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
 }
 
 int lh_lowrank_add_recompress(lh_ctx *ctx, int64_t m, int64_t n, const double *u1, const double *v1,

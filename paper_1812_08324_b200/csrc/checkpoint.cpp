@@ -27,7 +27,7 @@ namespace {
 
 const char MAGIC[8] = {'L', 'H', 'B', '2', '0', '0', 'H', '1'};
 const char TAIL[9] = {'L', 'H', 'B', '2', '0', '0', 'E', 'N', 'D'};
-constexpr uint32_t VERSION = 1;
+constexpr uint32_t VERSION = 2;  // 2: CN-pair tags in the header
 constexpr size_t STAGE = 64ull << 20;
 
 struct File {
@@ -163,6 +163,71 @@ std::shared_ptr<Tree> get_tree(File &F) {
     return T;
 }
 
+void check_tree(const Tree &T, const std::string &path) {
+    const i64 nn = (i64)T.nodes.size();
+    auto bad = [&](const char *what) {
+        throw Error(LH_EINVAL, std::string("corrupt checkpoint (cluster tree ") + what + "): " + path);
+    };
+    if (nn < 1) bad("empty");
+    for (const Cluster &c : T.nodes) {
+        if (!(c.lo >= 0 && c.lo <= c.hi && c.hi <= T.n)) bad("range");
+        for (int k = 0; k < 2; ++k)
+            if (c.kid[k] < -1 || c.kid[k] >= nn) bad("child");
+    }
+    for (i64 v : T.order)
+        if (v < 0 || v >= T.n) bad("order");
+    for (int32_t l : T.leaves)
+        if (l < 0 || l >= nn) bad("leaf");
+}
+
+// Every offset and index a later kernel dereferences must lie inside the arrays the file
+// brought: a truncated or edited file is rejected here instead of faulting on the device.
+void check_nodes(const HMat &H, const Tree &rt, const Tree &ct, const std::string &path) {
+    const i64 nb = (i64)H.nodes.size();
+    auto bad = [&](i64 b, const char *what) {
+        throw Error(LH_EINVAL, std::string("corrupt checkpoint (block ") + std::to_string(b) + ": " + what +
+                                   "): " + path);
+    };
+    auto in = [](i64 off, i64 len, i64 cap) { return off >= 0 && len >= 0 && off <= cap && len <= cap - off; };
+    for (i64 b = 0; b < nb; ++b) {
+        const Node &nd = H.nodes[b];
+        if (nd.kind < K_HIER || nd.kind > 4) bad(b, "kind");
+        const i64 cmin = nd.vpar >= 0 ? -1 : 0;  // virtual children split inside a leaf cluster: -1
+        if (nd.rcl < cmin || nd.rcl >= (i64)rt.nodes.size() || nd.ccl < cmin || nd.ccl >= (i64)ct.nodes.size())
+            bad(b, "cluster");
+        if (!in(nd.r0, nd.m, H.nrows) || !in(nd.c0, nd.n, H.ncols)) bad(b, "position");
+        if (nd.vpar < -1 || nd.vpar >= nb) bad(b, "parent");
+        if (nd.kind == K_HIER || nd.vpar >= 0 || (nd.kind == K_DENSE || nd.kind == K_FDENSE))
+            for (int k = 0; k < 4; ++k)
+                if (nd.kid[k] < -1 || nd.kid[k] >= nb) bad(b, "child");
+        if (nd.kind == K_DENSE || nd.kind == K_FDENSE) {
+            // virtual children of a refined leaf (vpar >= 0) hold offsets relative to their parent
+            i64 off = 0, ld = nd.m;
+            int32_t q = (int32_t)b;
+            for (int hops = 0; q >= 0 && hops < 64; ++hops) {
+                off += H.nodes[q].doff;
+                ld = H.nodes[q].m;
+                if (H.nodes[q].vpar < 0) break;
+                q = H.nodes[q].vpar;
+            }
+            if (q < 0 || H.nodes[q].vpar >= 0) bad(b, "refinement chain");
+            if (nd.m > 0 && nd.n > 0 && !in(off, (nd.n - 1) * ld + nd.m, H.arena_len)) bad(b, "dense storage");
+        }
+        if (nd.kind == K_FDENSE) {
+            if (!in(nd.poff, nd.m, H.perm_len)) bad(b, "pivots");
+            if (nd.ioff != -1 && !in(nd.ioff, nd.m * nd.m, H.inv_len)) bad(b, "leaf inverse");
+        }
+        if (nd.kind == K_LR) {
+            if (nd.kcap < 0 || nd.kcap > 64) bad(b, "capacity");
+            if (nd.rslot < 0 || nd.rslot >= H.nslots) bad(b, "rank slot");
+            if (!in(nd.uoff, nd.m * nd.kcap, H.arena_len) || !in(nd.voff, nd.n * nd.kcap, H.arena_len))
+                bad(b, "low-rank storage");
+        }
+    }
+    for (int32_t b : H.leafblocks)
+        if (b < 0 || b >= nb || H.nodes[b].kind == K_HIER) bad(b, "leaf list");
+}
+
 }  // namespace
 
 void save_hmat(Ctx &ctx, HMat &H, double eps2, const char *path) {
@@ -181,6 +246,8 @@ void save_hmat(Ctx &ctx, HMat &H, double eps2, const char *path) {
     F.put<i64>(H.perm_len);
     F.put<i64>(H.inv_len);
     F.put<double>(eps2);
+    F.put<uint64_t>(H.pair_tag);
+    F.put<uint64_t>(H.cn_pair_tag);
     put_tree(F, *H.rt);
     if (!one_tree) put_tree(F, *H.ct);
     F.put_vec(H.nodes);
@@ -212,6 +279,8 @@ void load_hmat(Ctx &ctx, const char *path, HMat &H, std::shared_ptr<Tree> &rt,
     H.perm_len = F.get<i64>();
     H.inv_len = F.get<i64>();
     eps2 = F.get<double>();
+    H.pair_tag = F.get<uint64_t>();
+    H.cn_pair_tag = F.get<uint64_t>();
     LH_REQUIRE(H.nrows > 0 && H.ncols > 0 && H.nslots >= 0 && H.arena_len >= 0 && H.perm_len >= 0 &&
                    H.inv_len >= 0,
                LH_EINVAL, std::string("corrupt checkpoint header: ") + path);
@@ -227,6 +296,9 @@ void load_hmat(Ctx &ctx, const char *path, HMat &H, std::shared_ptr<Tree> &rt,
     F.get_vec(H.leafblocks, (i64)H.nodes.size());
     LH_REQUIRE(H.root >= 0 && H.root < (int32_t)H.nodes.size(), LH_EINVAL,
                std::string("corrupt checkpoint (root): ") + path);
+    check_tree(*rt, path);
+    if (ct != rt) check_tree(*ct, path);
+    check_nodes(H, *rt, *ct, path);
     H.factored = flags & 1u;
     H.refined = flags & 2u;
     Pinned pin;
@@ -246,6 +318,18 @@ void load_hmat(Ctx &ctx, const char *path, HMat &H, std::shared_ptr<Tree> &rt,
     F.get(tail, 9);
     LH_REQUIRE(memcmp(tail, TAIL, 9) == 0, LH_EINVAL, std::string("corrupt checkpoint (trailer): ") + path);
     H.sync_ranks(ctx.stream);
+    for (const Node &nd : H.nodes)
+        LH_REQUIRE(nd.kind != K_LR || (H.h_ranks[nd.rslot] >= 0 && H.h_ranks[nd.rslot] <= nd.kcap), LH_EINVAL,
+                   std::string("corrupt checkpoint (rank exceeds capacity): ") + path);
+    if (H.perm_len > 0) {
+        std::vector<int32_t> perm(H.perm_len);
+        LH_CUDA(cudaMemcpy(perm.data(), H.d_perm, sizeof(int32_t) * H.perm_len, cudaMemcpyDeviceToHost));
+        for (const Node &nd : H.nodes)
+            if (nd.kind == K_FDENSE)
+                for (i64 i = 0; i < nd.m; ++i)
+                    LH_REQUIRE(perm[nd.poff + i] >= 0 && perm[nd.poff + i] < std::max<i64>(nd.m, 128), LH_EINVAL,
+                               std::string("corrupt checkpoint (pivot out of range): ") + path);
+    }
 }
 
 }  // namespace lh

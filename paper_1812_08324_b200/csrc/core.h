@@ -87,7 +87,18 @@ struct Node {
 
 struct Ctx;
 
+uint64_t next_hmat_id();
+
 struct HMat {
+    // process-unique identity: caches keyed on it never confuse a freed operator with a new one
+    // allocated at the same address
+    const uint64_t id = next_hmat_id();
+    // CN pair provenance.  derive() gives the unfactored A+ a persistent random tag and copies it
+    // into the A- it builds when it verified entry by entry that A- equals 2I - A+ (dense leaves
+    // within 8 ulp of 2 on the diagonal, exact negatives elsewhere; low-rank blocks (-U, V)).
+    // Both tags survive the in-place H-LU and checkpoints; 0 = none.
+    mutable uint64_t pair_tag = 0;
+    uint64_t cn_pair_tag = 0;
     const Tree *rt = nullptr, *ct = nullptr;
     std::shared_ptr<const Tree> rt_hold, ct_hold;  // keep trees alive
     i64 nrows = 0, ncols = 0;

@@ -1893,21 +1893,20 @@ struct SolvePlans {
     double zs_probe = 0.0;  // relative probe error of the single-RHS form against Z
     const MvPlan &z1plan() const { return mvZS ? *mvZS : *mvZ; }
     HMat &z1mat() const { return mvZS ? *ZS : *Z; }
-    const HMat *pair_hm = nullptr;  // hminus last checked against 2I - A+
-    bool pair_ok = false;
     int g_method = -1;
     int g_kernels = 0;  // kernel nodes in the cached step graph
+    int32_t last_path[3] = {-1, 0, 0};  // lh_cn_last_path: shape, multi-RHS DMMA, pipelined host step
     std::shared_ptr<Plan> tri[3][2];  // dense-RHS triangular solves by (mode, unit)
     double *tmp = nullptr;          // scratch vector(s)
     i64 tmp_len = 0;
     cudaGraphExec_t graph = nullptr;  // cached CN step
     const double *g_u = nullptr, *g_y = nullptr;
-    const HMat *g_hm = nullptr;
+    uint64_t g_hm = 0;  // HMat::id of the hminus the graph was captured with
     // host-buffer CN step (cn_step_host): pipelined graph keyed by the host pointers
     cudaGraphExec_t hgraph = nullptr;
     const double *hg_in = nullptr;
     double *hg_out = nullptr;
-    const HMat *hg_hm = nullptr;
+    uint64_t hg_hm = 0;
     cudaStream_t side = nullptr;
     std::vector<cudaEvent_t> hev;
     double *hx = nullptr, *hy = nullptr;  // device x and y of the host step
@@ -2157,8 +2156,16 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
         auto zs = std::make_shared<HMat>();
         std::shared_ptr<MvPlan> pz;
         if (build_shared_basis(ctx, *Z, sb_eps, *zs, pz, S.zs_stats)) {
-            S.ZS = zs;
-            S.mvZS = pz;
+            // same acceptance rule as the H2 form: a form that misses the probe is not installed
+            // and the step streams the H-form of Z itself
+            const double err = probe_rel_err(ctx, *S.mvZ, *Z, *pz, *zs);
+            if (getenv("LEVYH_PLAN_VERBOSE"))
+                fprintf(stderr, "[levyh] shared-basis probe: relative error %.3e\n", err);
+            if (err <= 1e-10) {
+                S.ZS = zs;
+                S.mvZS = pz;
+                S.zs_probe = err;
+            }
         }
     }
     if (getenv("LEVYH_PLAN_VERBOSE"))
@@ -2174,6 +2181,12 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
 }
 
 int step_graph_kernels(HMat &F) { return plans_of(F).g_kernels; }
+
+void cn_last_path(HMat &F, int32_t *out) {
+    SolvePlans &S = plans_of(F);
+    for (int k = 0; k < 3; ++k) out[k] = S.last_path[k];
+    out[3] = S.g_kernels;
+}
 
 void propagator_stats(HMat &F, double *out) {
     SolvePlans &S = plans_of(F);
@@ -2206,41 +2219,11 @@ static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
     }
 }
 
-__global__ void probe_fill_kernel(double *p, i64 n) {
-    for (i64 e = (i64)blockIdx.x * NT + threadIdx.x; e < n; e += (i64)gridDim.x * NT) {
-        uint64_t z = (uint64_t)e * 0x9E3779B97F4A7C15ull + 777;
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-        z ^= z >> 31;
-        p[e] = ((z >> 11) * (1.0 / 9007199254740992.0)) - 0.5;
-    }
-}
-
-// One probe per (hminus, factor) pair: the one-matvec CN step u <- 2 Z u - u is exact only
-// for hminus = 2I - A+ (the CN pair derive_toeplitz builds).  Compare Z (hminus x) with
-// 2 Z x - x on a pseudo-random x; a mismatch selects the general two-matvec step.
-static bool cn_pair_ok(Ctx &ctx, SolvePlans &S, HMat &Hm, MvPlan &Pm) {
-    if (S.pair_hm == &Hm) return S.pair_ok;
-    const i64 n = Hm.nrows;
-    double *w = dalloc<double>(4 * n);
-    probe_fill_kernel<<<1024, NT, 0, ctx.stream>>>(w, n);
-    mv_run(Pm, Hm, w, w + n, 1.0, 0.0, ctx.stream, ctx.num_sms);                  // A- x
-    mv_run(S.z1plan(), S.z1mat(), w + n, w + 2 * n, 1.0, 0.0, ctx.stream, ctx.num_sms);  // Z A- x
-    mv_run(S.z1plan(), S.z1mat(), w, w + 3 * n, 2.0, -1.0, ctx.stream, ctx.num_sms, w);  // 2 Z x - x
-    std::vector<double> h((size_t)2 * n);
-    LH_CUDA(cudaMemcpyAsync(h.data(), w + 2 * n, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost,
-                            ctx.stream));
-    LH_CUDA(cudaStreamSynchronize(ctx.stream));
-    cudaFree(w);
-    double num = 0.0, den = 0.0;
-    for (i64 i = 0; i < n; ++i) {
-        const double d = h[i] - h[n + i];
-        num += d * d;
-        den += h[n + i] * h[n + i];
-    }
-    S.pair_hm = &Hm;
-    S.pair_ok = num <= 1e-12 * den;  // relative 1e-6: an unrelated hminus differs at O(1)
-    return S.pair_ok;
-}
+// The one-matvec CN step u <- 2 Z u - u equals Z (A- u) only for A- = 2I - A+.  That is decided
+// from provenance, not measured: derive() sets cn_pair_of when it built hminus from this
+// factor's A+ and verified every stored entry (build.cu: pair_check_kernel); checkpoints keep
+// the tags.  Anything else (an independently assembled A-) runs u <- Z (A- u).
+static bool cn_pair_ok(const HMat &Hm, const HMat &F) { return Hm.cn_pair_tag != 0 && Hm.cn_pair_tag == F.pair_tag; }
 
 static void solve_inverse(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
     SolvePlans &S = plans_of(F);
@@ -2270,6 +2253,17 @@ void trisolve_dense(Ctx &ctx, HMat &T, int mode, bool unit, double *b, i64 ldb, 
         const int kc = std::min(CAP, nrhs - c0);
         run_plan(ctx, *P, T, nullptr, b + (i64)c0 * ldb, kc, "trisolve");
     }
+}
+
+// trisolve_lower / trisolve_upper_right with an H-matrix right-hand side (hops.py:282-310):
+// X (already a deep copy of B) solved in place on the executor
+void trisolve_block(Ctx &ctx, HMat &T, HMat &X, int mode, bool unit, double eps2) {
+    LH_REQUIRE(T.nrows == T.ncols, LH_EINVAL, "triangular solve needs a square H-matrix");
+    auto P = plan_trisolve_block(T, X, mode, unit, eps2);
+    P->upload(ctx.stream);
+    run_plan(ctx, *P, T, &X, nullptr, -1, mode == 0 ? "trisolve_lower (block)" : "trisolve_upper_right (block)");
+    X.sync_ranks(ctx.stream);
+    X.mv_plan.reset();
 }
 
 // lowrank_add_recompress (hops.py:147-156): (u, v) <- recompressed u1 v1^T + u2 v2^T with the
@@ -2541,7 +2535,10 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
         // method 1: one step = 3 H-matvecs (A-, L^-1, U^-1); method 2: u <- 2 Z u - u, one
         // H-matvec of the propagator (Z A- u with two when hminus is not 2I - A+).  The step
         // is captured once as a CUDA graph, cached per (operator, vector, scratch, method).
-        const int shape = method == 2 ? (cn_pair_ok(ctx, S, Hm, Pm) ? 2 : 3) : 1;
+        const int shape = method == 2 ? (cn_pair_ok(Hm, F) ? 2 : 3) : 1;
+        S.last_path[0] = shape;
+        S.last_path[1] = method == 2 && nrhs >= mm_min_rhs();
+        S.last_path[2] = 0;
         if (method == 2 && nrhs >= mm_min_rhs()) {
             // K right-hand sides: U row-major on the device for the whole run, each step one
             // (or two) DMMA matmats: U <- 2 Z U - U, or U <- Z (A- U)
@@ -2569,7 +2566,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
         }
         for (int q = 0; q < nrhs; ++q) {
             double *uq = u + (i64)q * ldu;
-            if (!(S.graph && S.g_u == uq && S.g_hm == &Hm && S.g_y == y && S.g_method == shape)) {
+            if (!(S.graph && S.g_u == uq && S.g_hm == Hm.id && S.g_y == y && S.g_method == shape)) {
                 if (S.graph) {
                     cudaGraphExecDestroy(S.graph);
                     S.graph = nullptr;
@@ -2607,7 +2604,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                 LH_CUDA(cudaGraphInstantiate(&S.graph, g, 0));
                 cudaGraphDestroy(g);
                 S.g_u = uq;
-                S.g_hm = &Hm;
+                S.g_hm = Hm.id;
                 S.g_y = y;
                 S.g_method = shape;
             }
@@ -2617,6 +2614,11 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
         return;
     }
     LH_REQUIRE(method == 0, LH_EINVAL, "cn_steps method must be 0, 1 or 2");
+    {
+        SolvePlans &S = plans_of(F);
+        S.last_path[0] = 0;
+        S.last_path[1] = S.last_path[2] = 0;
+    }
     for (int q = 0; q < nrhs; ++q) {
         double *uq = u + (i64)q * ldu;
         for (int k = 0; k < nsteps; ++k) {
@@ -2652,10 +2654,7 @@ void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out
     }
     bool pipelined = method == 2 && S.Z && is_pinned(u_in) && is_pinned(u_out) &&
                      !getenv("LEVYH_NO_HOST_PIPE");
-    if (pipelined) {
-        MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
-        pipelined = cn_pair_ok(ctx, S, Hm, Pm) && S.z1plan().npiece > 0 && S.z1plan().nbatch > 0;
-    }
+    if (pipelined) pipelined = cn_pair_ok(Hm, F) && S.z1plan().npiece > 0 && S.z1plan().nbatch > 0;
     if (!pipelined) {
         LH_CUDA(cudaMemcpyAsync(S.hx, u_in, sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
         cn_steps(ctx, Hm, F, S.hx, n, 1, 1, method);
@@ -2664,7 +2663,7 @@ void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out
         return;
     }
     const MvPlan &P = S.z1plan();
-    if (!(S.hgraph && S.hg_in == u_in && S.hg_out == u_out && S.hg_hm == &Hm)) {
+    if (!(S.hgraph && S.hg_in == u_in && S.hg_out == u_out && S.hg_hm == Hm.id)) {
         if (S.hgraph) {
             cudaGraphExecDestroy(S.hgraph);
             S.hgraph = nullptr;
@@ -2689,10 +2688,13 @@ void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out
         cudaGraphDestroy(g);
         S.hg_in = u_in;
         S.hg_out = u_out;
-        S.hg_hm = &Hm;
+        S.hg_hm = Hm.id;
     }
     LH_CUDA(cudaGraphLaunch(S.hgraph, ctx.stream));
     LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    S.last_path[0] = 2;
+    S.last_path[1] = 0;
+    S.last_path[2] = 1;
 }
 
 }  // namespace lh

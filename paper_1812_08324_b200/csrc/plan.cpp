@@ -1095,6 +1095,24 @@ std::shared_ptr<Plan> plan_trisolve_dense(HMat &T, i64 n, int nrhs_cap, int mode
     return pl.P;
 }
 
+// hops.py:282-310 with an H-matrix right-hand side: X (a deep copy of B, same block tree as T's
+// columns) <- T^{-1} X in place by the block recursion (_trisolve_block for mode 0 / 1,
+// _trisolve_right_upper for mode 2: X U = B), low-rank targets recompressed at eps2
+std::shared_ptr<Plan> plan_trisolve_block(HMat &T, HMat &X, int mode, bool unit, double eps2) {
+    auto t0 = std::chrono::steady_clock::now();
+    refine_dense_leaves(T);
+    Planner pl(T, &X);
+    pl.eps2 = eps2;
+    Mref Tm{&T, B_F, 0};
+    Mref Xm{&X, B_X, T.nslots};
+    if (mode == 2) pl.trisolve_right_upper(Tm, T.root, Xm, X.root, "U");
+    else pl.trisolve_left(Tm, T.root, Xm, X.root, mode, unit, mode == 0 ? "L" : "U");
+    pl.finalize();
+    pl.P->build_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return pl.P;
+}
+
 // X <- T^{-1} X with X initialised to the identity (lower: mode 0 unit L with pivots; upper: mode 1)
 std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2) {
     auto t0 = std::chrono::steady_clock::now();

@@ -155,6 +155,7 @@ std::shared_ptr<Plan> plan_solve(HMat &F, i64 n, int nrhs_cap);
 std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2);
 std::shared_ptr<Plan> plan_trisolve_dense(HMat &T, i64 n, int nrhs_cap, int mode, bool unit,
                                           const std::string &root);
+std::shared_ptr<Plan> plan_trisolve_block(HMat &T, HMat &X, int mode, bool unit, double eps2);
 std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_parts = 8);
 std::shared_ptr<Plan> merge_plans(const std::vector<std::shared_ptr<Plan>> &parts);
 void mark_lu_leaves(HMat &F, i64 &perm_len, i64 &inv_len);

@@ -494,14 +494,11 @@ def to_dense(H):
 
 
 def h_entry(H, i, j):
-    """hmatrix.py:416-433 (entry in tree order)."""
-    for r0, c0, blk in export_blocks(H):
-        if isinstance(blk, LowRank):
-            m, n = blk.u.shape[0], blk.v.shape[0]
-            if r0 <= i < r0 + m and c0 <= j < c0 + n:
-                return float(blk.u[i - r0] @ blk.v[j - c0])
-        else:
-            m, n = blk.data.shape
-            if r0 <= i < r0 + m and c0 <= j < c0 + n:
-                return blk.data[i - r0, j - c0]
-    raise IndexError("entry outside the matrix")
+    """hmatrix.py:416-433: entry (i, j) in tree order, reading only the leaf block that holds it
+    (lh_hmat_entry descends the block tree on the host)."""
+    i, j = int(i), int(j)
+    if not (0 <= i < H.n_rows and 0 <= j < H.n_cols):
+        raise IndexError("entry outside the matrix")
+    out = np.zeros(1)
+    _lib.check(_lib.lib().lh_hmat_entry(H.ctx.h, H.handle, i, j, _lib.host_ptr(out)), H.ctx.h)
+    return float(out[0])

@@ -82,8 +82,18 @@ class HFactorization:
     inverse_ready: bool = False
     propagator_ready: bool = False
 
-    def solve(self, b, method="substitution"):
+    def solve(self, b, method=None):
         return solve(self, b, method)
+
+    @property
+    def default_method(self):
+        """The fastest method already prepared: propagator, then inverse factors, then
+        substitution (which needs no preparation)."""
+        if self.propagator_ready:
+            return "propagator"
+        if self.inverse_ready:
+            return "inverse"
+        return "substitution"
 
     def prepare_inverse(self):
         if not self.inverse_ready:
@@ -117,12 +127,19 @@ def hlu(H: HMatrix, eps2=1e-10):
     return HFactorization(H, eps2)
 
 
-def solve(F: HFactorization, b, method="substitution"):
-    """hops.py:424-432: forward (unit L with leaf pivots) then backward (U)."""
+def solve(F: HFactorization, b, method=None):
+    """hops.py:424-432: x = (LU)^-1 b.  ``method`` None uses the fastest method already
+    prepared on F (F.default_method: one H-matvec of the propagator after
+    prepare_propagator / CNSystem.prepare, else the triangular-inverse factors, else the
+    reference's forward (unit L with leaf pivots) then backward (U) substitution)."""
     ctx = F.h.ctx
     bt, was_torch = _to_device(b, ctx)
     if bt.shape[0] != F.h.n_rows:
         raise ValueError("right-hand side length mismatch")
+    if method is None:
+        method = F.default_method
+    if method not in SOLVE_METHODS:
+        raise ValueError(f"unknown solve method {method!r}; expected one of {sorted(SOLVE_METHODS)}")
     m = SOLVE_METHODS[method]
     if m == 1:
         F.prepare_inverse()
@@ -136,13 +153,31 @@ def solve(F: HFactorization, b, method="substitution"):
     return out if was_torch else out.cpu().numpy()
 
 
+# Truncation of the low-rank updates in block triangular solves.  The reference passes
+# eps2 = 0 (hops.py:295, :310), which keeps every nonzero singular value -- rounding noise
+# included -- so its ranks are decided by noise; a Frobenius tail of 1e-14 relative keeps the
+# result within rounding of the exact solve with bounded ranks.
+BLOCK_SOLVE_EPS2 = 1e-14
+
+
+def _tri_solve_block(T, B, mode, unit):
+    Th = T.h if isinstance(T, HFactorization) else T
+    if not isinstance(Th, HMatrix):
+        raise TypeError("triangular operand must be an HMatrix or HFactorization")
+    if B.n_rows != Th.n_rows:
+        raise ValueError("right-hand side shape mismatch")
+    h = C.c_void_p()
+    _lib.check(_lib.lib().lh_trisolve_block(Th.ctx.h, Th.handle, B.handle, int(mode), int(bool(unit)),
+                                            float(BLOCK_SOLVE_EPS2), C.byref(h)), Th.ctx.h)
+    return HMatrix(h, B.row_tree, B.col_tree, B.eta, B.ctx, B.cfg)
+
+
 def _tri_solve(T, B, mode, unit):
     Th = T.h if isinstance(T, HFactorization) else T
     if not isinstance(Th, HMatrix):
         raise TypeError("triangular operand must be an HMatrix or HFactorization")
     if not (isinstance(B, np.ndarray) or _is_torch(B)):
-        raise NotImplementedError("block (HMatrix) right-hand sides are not supported; "
-                                  "pass a dense array")
+        raise TypeError("right-hand side must be a dense array or an HMatrix")
     ctx = Th.ctx
     bt, was_torch = _to_device(B, ctx)
     return Th, ctx, bt, was_torch
@@ -161,7 +196,11 @@ def trisolve_lower(L, B, unit_diagonal=False):
 
     LU-factored diagonal leaves use their unit-L factor and pivots; plain dense leaves use
     their lower triangle (unit diagonal if requested) and raise LinAlgError("singular
-    triangular diagonal block at L...") on a zero diagonal entry.  B is not modified."""
+    triangular diagonal block at L...") on a zero diagonal entry.  B is not modified.  An
+    HMatrix B (same cluster trees) returns a new HMatrix: a deep copy of B solved block by
+    block (_trisolve_block, hops.py:232-258)."""
+    if isinstance(B, HMatrix):
+        return _tri_solve_block(L, B, 0, unit_diagonal)
     Th, ctx, bt, was_torch = _tri_solve(L, B, 0, unit_diagonal)
     if bt.shape[0] != Th.n_rows:
         raise ValueError("right-hand side length mismatch")
@@ -177,6 +216,10 @@ def trisolve_lower(L, B, unit_diagonal=False):
 def trisolve_upper_right(U, B, unit_diagonal=False):
     """hops.py:298-310: solve X U = B with the upper triangle of U, as U^T X^T = B^T
     (dense B of shape (m, n), or (n,) for one row)."""
+    if isinstance(B, HMatrix):  # _trisolve_right_upper (hops.py:261-279) on a deep copy
+        if unit_diagonal:
+            raise ValueError("unit_diagonal right solves are not supported on blocks")
+        return _tri_solve_block(U, B, 2, False)
     Th, ctx, bt, was_torch = _tri_solve(U, B, 2, unit_diagonal)
     n = Th.n_rows
     rows = bt.reshape(1, -1) if bt.ndim == 1 else bt.reshape(bt.shape[0], -1)

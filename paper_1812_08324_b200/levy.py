@@ -75,7 +75,7 @@ class CNSystem:
         self.tree = None
         self.factor = None
         self.h_minus = None
-        self.method = "inverse"
+        self.method = "propagator"
         self._host = {}
 
     @property
@@ -145,8 +145,11 @@ class CNSystem:
         Hm = derive_toeplitz(Hp, self.tMinus, lr_scale=-1.0, kcap=0)
         return Hp, Hm
 
-    def prepare(self, cfg=None, eps2=1e-10, method="inverse"):
-        """levy.py:241-246: factorise A+ once and keep A- for stepping."""
+    def prepare(self, cfg=None, eps2=1e-10, method="propagator"):
+        """levy.py:241-246: factorise A+ once and keep A- for stepping.  ``method`` picks the
+        per-step solve (hops.solve): "propagator" (default, one streaming H-matvec of
+        Z = (A+)^-1 per step), "inverse" (triangular-inverse factors) or "substitution"
+        (the reference's forward/backward substitution); run_cn / step_cn use it."""
         Hp, Hm = self.build_pair(cfg)
         self.h_minus = Hm
         self.factor = hlu(Hp, eps2)
@@ -236,6 +239,7 @@ class FracCNSystem:
         self.factor = None
         self.h_minus = None
         self.h_plus = None
+        self.method = "propagator"
         # True / a process group: shard the ACA compression across the ranks
         self.distributed = distributed
 
@@ -265,8 +269,9 @@ class FracCNSystem:
         Hm = derive_toeplitz(Hp, self.tMinus, lr_scale=-1.0, kcap=0)
         return Hp, Hm
 
-    def prepare(self, cfg=None, eps2=1e-10, method="inverse"):
-        """Factorise A+ once and keep A- for stepping (levy.py:241-246)."""
+    def prepare(self, cfg=None, eps2=1e-10, method="propagator"):
+        """Factorise A+ once and keep A- for stepping (levy.py:241-246).  ``method`` as in
+        CNSystem.prepare: "propagator" (default), "inverse" or "substitution"."""
         Hp, Hm = self.build_pair(cfg)
         self.h_minus = Hm
         self.factor = hlu(Hp, eps2)
@@ -291,7 +296,7 @@ def step_cn(sys, u_n, F=None, method=None):
     F = F if F is not None else sys.factor
     if F is None or sys.h_minus is None:
         raise ValueError("call prepare() before stepping")
-    m = SOLVE_METHODS[method or getattr(sys, "method", "substitution")]
+    m = SOLVE_METHODS[method or getattr(sys, "method", None) or "propagator"]
     if m == 2:
         F.prepare_propagator()
     elif m == 1:
@@ -318,8 +323,10 @@ def step_cn(sys, u_n, F=None, method=None):
     return perm.from_tree(out)
 
 
-def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method="inverse", mode="hmatrix"):
+def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method=None, mode="hmatrix"):
     """levy.py:309-330: factor once, march n_steps on the device (CUDA-graph loop).
+    ``method`` None steps with the method ``prepare`` set up (sys.method, default
+    "propagator"); an explicit method prepares what it needs on the existing factor.
     ``mode='dense'`` (the reference's dense LU oracle) is test infrastructure, not a product
     path."""
     if mode != "hmatrix":
@@ -330,13 +337,13 @@ def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method="inverse", mode="hmatr
     from . import _lib
 
     if sys.factor is None:
-        sys.prepare(cfg, eps2, method)
+        sys.prepare(cfg, eps2, method or getattr(sys, "method", None) or "propagator")
     perm = sys.tree.perm
     ctx = sys.h_minus.ctx
     u = torch.as_tensor(perm.to_tree(np.asarray(u0, dtype=float))).to(f"cuda:{ctx.device}")
     uc = u.reshape(1, -1).contiguous() if u.ndim == 1 else u.t().contiguous()
     k = 1 if u.ndim == 1 else u.shape[1]
-    m = SOLVE_METHODS[sys.method if method is None else method]
+    m = SOLVE_METHODS[method or getattr(sys, "method", None) or "propagator"]
     if m == 2:
         sys.factor.prepare_propagator()
     elif m == 1:

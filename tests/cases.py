@@ -65,3 +65,22 @@ def krylov_operators(tag):
     if tag == "gmres_r5":
         A = np.eye(N) + 0.5 * h * A
     return A, x
+
+
+def report_rank_mismatch(name, what, nblocks, diff):
+    """Record per-block rank differences against the reference (G1: report, do not hide):
+    printed (visible with -s / in the captured log) and appended to
+    gpurun_out/rank_mismatch.jsonl when that directory exists."""
+    import json
+
+    diff = np.asarray(diff)
+    rec = {"case": name, "what": what, "lowrank_blocks": int(nblocks),
+           "mismatches": int(np.count_nonzero(diff)),
+           "max_abs": int(np.abs(diff).max(initial=0)),
+           "higher": int((diff > 0).sum()), "lower": int((diff < 0).sum())}
+    print("rank-mismatch", json.dumps(rec))
+    out = os.path.join(os.path.dirname(GOLDEN), "..", "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "rank_mismatch.jsonl"), "a") as f:
+            f.write(json.dumps(rec) + "\n")
+    return rec
