@@ -16,6 +16,7 @@
 #include "core.h"
 #include "dev.cuh"
 #include "matvec.h"
+#include "h2step.h"
 #include "plan_impl.h"
 
 namespace lh {
@@ -2677,8 +2678,11 @@ void cn_step_host(Ctx &ctx, HMat &Hm, HMat &F, const double *u_in, double *u_out
         cudaGraph_t g;
         LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
         try {
-            mv_run_host(P, u_in, S.hx, S.hy, u_out, 2.0, -1.0, true, ctx.stream, S.side, S.hev.data(),
-                        ctx.num_sms);
+            if (P.h2 && P.h2->step2 && !getenv("LEVYH_HOST_PIECES"))  // two-kernel step: copy in, step, copy out
+                h2s_launch_host(*P.h2, u_in, S.hy, u_out, 2.0, -1.0, ctx.stream);
+            else
+                mv_run_host(P, u_in, S.hx, S.hy, u_out, 2.0, -1.0, true, ctx.stream, S.side, S.hev.data(),
+                            ctx.num_sms);
         } catch (...) {
             cudaStreamEndCapture(ctx.stream, &g);
             throw;

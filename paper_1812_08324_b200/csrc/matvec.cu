@@ -19,6 +19,7 @@
 #include "core.h"
 #include "dev.cuh"
 #include "matvec.h"
+#include "h2step.h"
 
 namespace lh {
 
@@ -498,7 +499,8 @@ static i64 even(i64 v) { return (v + 1) & ~i64(1); }
 
 // Builds a plan over the given leaf blocks (default: all of H).  Row segments are the leaf
 // clusters of the row tree split into <= SEG rows.
-std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &blocks, cudaStream_t s) {
+std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &blocks, cudaStream_t s,
+                                      int tma_grid) {
     auto P = std::make_shared<MvPlan>();
     H.sync_ranks(s);  // the packed layout is sized by the current ranks
     const Tree &rt = *H.rt;
@@ -702,7 +704,7 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
     int dev_id = 0, num_sms = 148;
     cudaGetDevice(&dev_id);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev_id);
-    const int G = std::max(1, std::min(num_sms, nseg));
+    const int G = std::max(1, std::min(tma_grid > 0 ? tma_grid : num_sms, nseg));
     std::vector<int32_t> cta_seg(G + 1, nseg);
     {
         i64 total = 0;
@@ -882,7 +884,25 @@ void mv_vtx_launch(const MvPlan &P, const HMat &H, const double *x, int num_sms,
 // one launch of the TMA segment kernel over the CTA ranges cta (full or lean configuration)
 static void seg_tma_launch(const MvPlan &P, const int32_t *cta, double *y, double alpha, double beta,
                            const double *z, cudaStream_t s) {
-    if (P.lean) {
+    if (P.lean == 3) {
+        static bool attr = false;
+        if (!attr) {
+            LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel<2, 128>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem<2, 128>()));
+            attr = true;
+        }
+        seg_tma_kernel<2, 128><<<P.tma_grid, 128 + 32, tma_smem<2, 128>(), s>>>(P.segs, cta, P.batches, P.pbuf, P.tcol,
+                                                                             P.xpad, y, alpha, beta, z);
+    } else if (P.lean == 2) {
+        static bool attr = false;
+        if (!attr) {
+            LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel<3, 128>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem<3, 128>()));
+            attr = true;
+        }
+        seg_tma_kernel<3, 128><<<P.tma_grid, 128 + 32, tma_smem<3, 128>(), s>>>(P.segs, cta, P.batches, P.pbuf, P.tcol,
+                                                                             P.xpad, y, alpha, beta, z);
+    } else if (P.lean) {
         static bool attr = false;
         if (!attr) {
             LH_CUDA(cudaFuncSetAttribute((const void *)seg_tma_kernel<3, 256>,
@@ -931,6 +951,28 @@ void mv_seg_launch(const MvPlan &P, const HMat &H, const double *x, double *y, d
 // y = alpha * H x + beta * z (z = y when null) for one right-hand side
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
             cudaStream_t s, int num_sms, const double *z) {
+    if (P.h2 && P.h2->step2) {  // two-kernel fused step (h2step.cu)
+        h2s_launch(*P.h2, x, y, alpha, beta, z ? z : y, s);
+        return;
+    }
+    if (P.fdense && P.h2 && P.h2->qleaf) {
+        // fused H2 step: the dense diagonal leaves stream into yd on the forked low-priority
+        // stream (co-resident segment kernel) while the latency-bound walk runs on s; the row
+        // walk then applies Q_t y_hat_t and writes y = alpha (yd + Q y_hat) + beta z
+        const MvPlan &D = *P.fdense;
+        const int fdbg = getenv("LEVYH_FUSE_DBG") ? atoi(getenv("LEVYH_FUSE_DBG")) : 0;  // timing only
+        LH_CUDA(cudaEventRecord(P.fev[0], s));
+        LH_CUDA(cudaStreamWaitEvent(P.fork, P.fev[0], 0));
+        if (!(fdbg & 1)) {
+            tgather_kernel<<<(int)std::min<i64>((D.nx + 2 + NT - 1) / NT, 148 * 8), NT, 0, P.fork>>>(
+                D.tmap, 0, D.tvec, D.tcol, x, D.nx, D.xpad);
+            seg_tma_launch(D, D.cta_seg, P.h2->yd, 1.0, 0.0, P.h2->yd, P.fork);
+        }
+        LH_CUDA(cudaEventRecord(P.fev[1], P.fork));
+        h2_launch_fused(*P.h2, x, y, alpha, beta, z ? z : y, s, P.fev[1]);
+        LH_CUDA(cudaGetLastError());
+        return;
+    }
     if (P.dense) {
         // split H2 plan: the dense diagonal leaves stream on a forked stream (lean segment
         // kernel) while the latency-bound H2 walk runs; the row-basis pieces add in after both

@@ -116,8 +116,21 @@ struct H2Sub {  // a subtree's transfer matrices [tbeg, tbeg + tlen) are staged 
     i64 tbeg;
     int32_t tlen, base;
 };
+struct H2QLeaf {  // fused step: y[r0 + i] = alpha (yd[r0 + i] + sum_c Q[qoff + i + c rows] y_hat[c]) + beta z[r0 + i]
+    i64 qoff, r0;     // Q_t in the ZS arena (column-major, ld = rows); first row
+    int32_t rows, k;  // k = 0: a row leaf without a basis (dense part only)
+    int32_t yloc, pad;  // y_hat_t at ys[yloc] of the subtree CTA (k > 0)
+};
+struct H2S;  // h2step.h: the two-kernel step
 struct H2 {
     int nsub_up = 0, nsub_dn = 0, maxh_up = 0, maxh_dn = 0, split = 0;
+    std::shared_ptr<H2S> step2;  // two-kernel fused step (default when built)
+    // fused single-RHS step: the dense diagonal leaves stream on a forked,
+    // low-priority stream beside the walk into yd; the row walk applies Q_t y_hat_t itself
+    H2QLeaf *qleaf = nullptr;    // per row subtree, [dn_qbeg[s], dn_qbeg[s+1])
+    int32_t *dn_qbeg = nullptr;
+    const double *zarena = nullptr;  // ZS arena (Q_t)
+    double *yd = nullptr;            // dense-leaf part of y
     H2Leaf *leaves = nullptr;
     H2Up *ups = nullptr;
     H2Down *dns = nullptr;
@@ -145,6 +158,10 @@ struct H2 {
 // padded copy of x (xpad), so an H2 plan needs no tgather launch
 // leaves = false: the column-leaf x_hat are already in place (h2_leaf_launch per x piece)
 void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s, bool leaves = true);
+// fused step: leaf / up / couple on s, then (after `dense_done`) the row walk finishing
+// y = alpha (yd + Q y_hat) + beta z
+void h2_launch_fused(const H2 &h, const double *x, double *y, double alpha, double beta, const double *z,
+                     cudaStream_t s, cudaEvent_t dense_done);
 void h2_leaf_launch(const H2 &h, int l0, int l1, const double *x, cudaStream_t s);
 void treduce_launch(const TJob *jobs, int n, const double *part, double *out, cudaStream_t s);
 
@@ -155,7 +172,10 @@ struct MvPlan {
     // split H2 plan: this plan holds the row-basis pieces; `dense` the dense leaves (lean
     // segment kernel, run on the forked stream beside the walk)
     std::shared_ptr<MvPlan> dense;
-    bool lean = false;                 // segment kernel in its lean configuration
+    // fused H2 step: the dense diagonal leaves alone (segment kernel in its smallest
+    // configuration, written to h2->yd) beside the walk; the walk finishes y
+    std::shared_ptr<MvPlan> fdense;
+    int lean = 0;                      // segment kernel configuration: 0 full, 1 lean, 2 co-resident
     cudaStream_t fork = nullptr;
     cudaEvent_t fev[2] = {nullptr, nullptr};
     std::vector<int32_t> blk_of_node;  // tvec row of every low-rank node (-1 otherwise)
@@ -193,8 +213,9 @@ struct MvPlan {
     ~MvPlan();
 };
 
+// tma_grid: CTAs of the segment kernel (byte-balanced contiguous segment ranges); 0 = one per SM
 std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &blocks,
-                                      cudaStream_t s);
+                                      cudaStream_t s, int tma_grid = 0);
 void mv_run(const MvPlan &P, const HMat &H, const double *x, double *y, double alpha, double beta,
             cudaStream_t s, int num_sms, const double *z = nullptr);
 MvPlan &get_mv_plan(HMat &H, cudaStream_t s);

@@ -23,6 +23,7 @@
 #include "core.h"
 #include "dev.cuh"
 #include "matvec.h"
+#include "h2step.h"
 
 namespace lh {
 
@@ -493,7 +494,7 @@ bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr
     }
     ZS.root = 0;
     ZS.arena_len = aoff;
-    ZS.d_arena = dalloc<double>(std::max<i64>(aoff, 1));
+    ZS.d_arena = dalloc<double>(std::max<i64>(aoff, 1) + 4);  // + bulk-copy tail slack
     ZS.nslots = (int32_t)ranks.size();
     ZS.d_ranks = dupload(ranks, st);
     ZS.h_ranks = ranks;
@@ -637,7 +638,8 @@ bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr
 H2::~H2() {
     for (void *p : {(void *)leaves, (void *)ups, (void *)dns, (void *)cpls, (void *)up_lv, (void *)cnt, (void *)up_sub, (void *)dn_sub, (void *)dn_path, (void *)dn_pbeg,
                     (void *)dn_lv, (void *)pb, (void *)tu, (void *)td, (void *)sb, (void *)xh, (void *)wg,
-                    (void *)crec, (void *)up_chain, (void *)up_cbeg, (void *)up_xcnt, (void *)dn_ycnt})
+                    (void *)crec, (void *)up_chain, (void *)up_cbeg, (void *)up_xcnt, (void *)dn_ycnt,
+                    (void *)qleaf, (void *)dn_qbeg, (void *)yd})
         cudaFree(p);
 }
 
@@ -775,8 +777,11 @@ __global__ void __launch_bounds__(NT) h2_leaf_kernel(const H2Leaf *leaves, int n
 // Column walk above the leaves: one CTA per subtree (x_hat of its nodes kept in shared memory,
 // levels by height, one memory round trip per level), then the top of the tree by
 // last-arrival climbing: the second child to finish computes the parent (warp 0 only).
-constexpr int H2_MAXN = 128;  // staged node descriptors per subtree
-__global__ void __launch_bounds__(NT, 2) h2_up_kernel(const H2Up *ups, const int32_t *up_lv, const int32_t *up_chain,
+constexpr int H2_MAXN = 256;  // staged node descriptors per subtree
+#ifndef H2_UP_MINB
+#define H2_UP_MINB 2  // walk CTAs per SM by registers: room for the co-resident dense-leaf kernel
+#endif
+__global__ void __launch_bounds__(NT, H2_UP_MINB) h2_up_kernel(const H2Up *ups, const int32_t *up_lv, const int32_t *up_chain,
                                                       const int32_t *up_cbeg, const H2Sub *sub, const int32_t *up_xcnt,
                                                       int32_t *cnt, int maxh, const double *tu, double *xh, int dbg) {
     extern __shared__ __align__(16) double h2s[];
@@ -887,10 +892,19 @@ __global__ void __launch_bounds__(NT, 4) h2_couple_kernel(const H2CRec *crec, in
 
 // Row walk: one CTA per subtree.  The transfers down the path above the subtree (one warp),
 // then the subtree's levels (y_hat kept in shared memory, one round trip per level).
-__global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const int32_t *dn_path,
+struct H2Fuse {  // the fused step's row-basis phase (FUSED = true)
+    const H2QLeaf *ql;
+    const int32_t *qbeg;
+    const double *zar, *yd, *z;
+    double *y;
+    double alpha, beta;
+};
+template <bool FUSED>
+__global__ void __launch_bounds__(NT, H2_UP_MINB) h2_down_kernel(const H2Down *dns, const int32_t *dn_path,
                                                         const int32_t *dn_pbeg, const int32_t *dn_lv,
                                                         const H2Sub *sub, const int32_t *dn_ycnt, int maxh, int ymax,
-                                                        const double *td, const double *wg, double *tcol, int dbg) {
+                                                        const double *td, const double *wg, double *tcol, int dbg,
+                                                        H2Fuse fz) {
     extern __shared__ __align__(16) double h2s[];
     double *ws = h2s, *ys = ws + ymax;
     __shared__ double pw[H2_MAXP][KC_MAX];
@@ -943,15 +957,48 @@ __global__ void __launch_bounds__(NT, 2) h2_down_kernel(const H2Down *dns, const
             if (act1) {
                 const double v = ws[D1.yoff - SB.base + lane] + r1;
                 ys[D1.yoff - SB.base + lane] = v;
-                if (D1.out >= 0) tcol[D1.out + lane] = v;
+                if (!FUSED && D1.out >= 0) tcol[D1.out + lane] = v;
             }
             if (act2) {
                 const double v = ws[D2.yoff - SB.base + lane] + r2;
                 ys[D2.yoff - SB.base + lane] = v;
-                if (D2.out >= 0) tcol[D2.out + lane] = v;
+                if (!FUSED && D2.out >= 0) tcol[D2.out + lane] = v;
             }
         }
         __syncthreads();
+    }
+    if (!FUSED) return;
+    // row-basis phase: y_t = alpha (yd_t + Q_t y_hat_t) + beta z_t for this subtree's row leaves
+    // (one warp per leaf, lanes on rows lane and lane + 32, 8 basis columns per round trip)
+    const int qa = fz.qbeg[s], qb = fz.qbeg[s + 1];
+    for (int l = qa + w; l < qb; l += NW) {
+        const H2QLeaf Q = fz.ql[l];
+        const bool in0 = lane < Q.rows, in1 = lane + 32 < Q.rows;
+        const i64 r0 = Q.r0 + lane, r1 = r0 + 32;
+        const double d0 = in0 ? __ldcg(fz.yd + r0) : 0.0, d1 = in1 ? __ldcg(fz.yd + r1) : 0.0;
+        const double z0 = (in0 && fz.beta != 0.0) ? fz.z[r0] : 0.0, z1 = (in1 && fz.beta != 0.0) ? fz.z[r1] : 0.0;
+        const double *q = fz.zar + Q.qoff;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        for (int c = 0; c < Q.k; c += 8) {
+            double p[8], pp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const bool ok = c + u < Q.k;
+                p[u] = (ok && in0) ? q[lane + (i64)(c + u) * Q.rows] : 0.0;
+                pp[u] = (ok && in1) ? q[lane + 32 + (i64)(c + u) * Q.rows] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+                const double y0 = c + u < Q.k ? ys[Q.yloc + c + u] : 0.0;
+                const double y1 = c + u + 1 < Q.k ? ys[Q.yloc + c + u + 1] : 0.0;
+                a0 = fma(p[u], y0, a0);
+                b0 = fma(p[u + 1], y1, b0);
+                a1 = fma(pp[u], y0, a1);
+                b1 = fma(pp[u + 1], y1, b1);
+            }
+        }
+        if (in0) fz.y[r0] = fz.alpha * (d0 + (a0 + b0)) + fz.beta * z0;
+        if (in1) fz.y[r1] = fz.alpha * (d1 + (a1 + b1)) + fz.beta * z1;
     }
 }
 
@@ -994,8 +1041,19 @@ void h2_leaf_launch(const H2 &h, int l0, int l1, const double *x, cudaStream_t s
     h2_leaf_kernel<<<g, NT, 0, s>>>(h.leaves + l0, l1 - l0, h.pb, x, h.xh, 0, nullptr);
 }
 
+static void h2_smem_attrs() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const int big = 160 * 1024;
+    LH_CUDA(cudaFuncSetAttribute((const void *)h2_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    LH_CUDA(cudaFuncSetAttribute((const void *)h2_down_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    LH_CUDA(cudaFuncSetAttribute((const void *)h2_down_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+}
+
 void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx, cudaStream_t s, bool leaves) {
-    static const int dbg = getenv("LEVYH_H2_DBG") ? atoi(getenv("LEVYH_H2_DBG")) : 0;  // timing experiments only
+    h2_smem_attrs();
+    const int dbg = getenv("LEVYH_H2_DBG") ? atoi(getenv("LEVYH_H2_DBG")) : 0;  // timing experiments only
     auto grid = [](i64 n, int per_sm) { return (int)std::max<i64>(1, std::min<i64>(148 * per_sm, (n + NW - 1) / NW)); };
     if (leaves) h2_leaf_kernel<<<grid(h.nleaf, 8), NT, 0, s>>>(h.leaves, h.nleaf, h.pb, x, h.xh, nx, xpad);
     else if (nx > 0) h2_leaf_kernel<<<grid(nx / 256 + 1, 8), NT, 0, s>>>(h.leaves, 0, h.pb, x, h.xh, nx, xpad);
@@ -1019,10 +1077,65 @@ void h2_launch(const H2 &h, const double *x, double *tcol, double *xpad, i64 nx,
                                (const int32_t *)h.up_xcnt, h.cnt, h.maxh_up, (const double *)h.tu, h.xh, dbg));
     LH_CUDA(cudaLaunchKernelEx(&cc, h2_couple_kernel, (const H2CRec *)h.crec, h.ncnode, (const H2Cpl *)h.cpls,
                                (const double *)h.sb, (const double *)h.xh, h.wg));
-    LH_CUDA(cudaLaunchKernelEx(&cd, h2_down_kernel, (const H2Down *)h.dns, (const int32_t *)h.dn_path,
+    LH_CUDA(cudaLaunchKernelEx(&cd, h2_down_kernel<false>, (const H2Down *)h.dns, (const int32_t *)h.dn_path,
                                (const int32_t *)h.dn_pbeg, (const int32_t *)h.dn_lv, (const H2Sub *)h.dn_sub,
                                (const int32_t *)h.dn_ycnt, h.maxh_dn, h.dn_ymax, (const double *)h.td,
-                               (const double *)h.wg, tcol, dbg));
+                               (const double *)h.wg, tcol, dbg, H2Fuse{}));
+    LH_CUDA(cudaGetLastError());
+}
+
+void h2_launch_fused(const H2 &h, const double *x, double *y, double alpha, double beta, const double *z,
+                     cudaStream_t s, cudaEvent_t dense_done) {
+    h2_smem_attrs();
+    const int dbg = getenv("LEVYH_H2_DBG") ? atoi(getenv("LEVYH_H2_DBG")) : 0;  // timing experiments only
+    static int prio_hi = 0;
+    static bool init = false;
+    if (!init) {  // the walk is the critical path: highest priority over the dense stream
+        int lo = 0, hi = 0;
+        LH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        prio_hi = getenv("LEVYH_H2_NOPRIO") ? lo : hi;
+        init = true;
+    }
+    auto grid = [](i64 n, int per_sm) { return (int)std::max<i64>(1, std::min<i64>(148 * per_sm, (n + NW - 1) / NW)); };
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = prio_hi;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    auto cfg = [&](int g, size_t smem, bool pdl) {
+        cudaLaunchConfig_t c = {};
+        c.gridDim = dim3(g);
+        c.blockDim = dim3(NT);
+        c.dynamicSmemBytes = smem;
+        c.stream = s;
+        c.attrs = at;
+        c.numAttrs = pdl ? 2 : 1;
+        return c;
+    };
+    const int fdbg = getenv("LEVYH_FUSE_DBG") ? atoi(getenv("LEVYH_FUSE_DBG")) : 0;  // timing only
+    if (fdbg & 2) {  // dense branch alone
+        LH_CUDA(cudaStreamWaitEvent(s, dense_done, 0));
+        return;
+    }
+    // the walk's grids are bounded so that each SM keeps room for the co-resident dense-leaf
+    // segment kernel (LEVYH_H2F_LEAF / LEVYH_H2F_CPL: CTAs per SM)
+    const int gl = getenv("LEVYH_H2F_LEAF") ? atoi(getenv("LEVYH_H2F_LEAF")) : 2;
+    const int gc = getenv("LEVYH_H2F_CPL") ? atoi(getenv("LEVYH_H2F_CPL")) : 2;
+    cudaLaunchConfig_t cl = cfg(grid(h.nleaf, gl), 0, false), cu = cfg(h.nsub_up, 8 * (size_t)h.up_xmax, true),
+                       cc = cfg(grid(h.ncnode, gc), 0, true), cd = cfg(h.nsub_dn, 16 * (size_t)h.dn_ymax, false);
+    LH_CUDA(cudaLaunchKernelEx(&cl, h2_leaf_kernel, (const H2Leaf *)h.leaves, h.nleaf, (const double *)h.pb, x, h.xh,
+                               (i64)0, (double *)nullptr));
+    LH_CUDA(cudaLaunchKernelEx(&cu, h2_up_kernel, (const H2Up *)h.ups, (const int32_t *)h.up_lv,
+                               (const int32_t *)h.up_chain, (const int32_t *)h.up_cbeg, (const H2Sub *)h.up_sub,
+                               (const int32_t *)h.up_xcnt, h.cnt, h.maxh_up, (const double *)h.tu, h.xh, dbg));
+    LH_CUDA(cudaLaunchKernelEx(&cc, h2_couple_kernel, (const H2CRec *)h.crec, h.ncnode, (const H2Cpl *)h.cpls,
+                               (const double *)h.sb, (const double *)h.xh, h.wg));
+    LH_CUDA(cudaStreamWaitEvent(s, dense_done, 0));
+    LH_CUDA(cudaLaunchKernelEx(&cd, h2_down_kernel<true>, (const H2Down *)h.dns, (const int32_t *)h.dn_path,
+                               (const int32_t *)h.dn_pbeg, (const int32_t *)h.dn_lv, (const H2Sub *)h.dn_sub,
+                               (const int32_t *)h.dn_ycnt, h.maxh_dn, h.dn_ymax, (const double *)h.td,
+                               (const double *)h.wg, (double *)nullptr, dbg,
+                               H2Fuse{h.qleaf, h.dn_qbeg, h.zarena, h.yd, z, y, alpha, beta}));
     LH_CUDA(cudaGetLastError());
 }
 
@@ -1320,7 +1433,7 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     }
     ZS.root = 0;
     ZS.arena_len = aoff;
-    ZS.d_arena = dalloc<double>(std::max<i64>(aoff, 1));
+    ZS.d_arena = dalloc<double>(std::max<i64>(aoff, 1) + 4);  // + bulk-copy tail slack
     ZS.nslots = (int32_t)ranks.size();
     ZS.d_ranks = dupload(ranks, st);
     ZS.h_ranks = ranks;
@@ -1405,9 +1518,11 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
         tulen += (i64)C.rows[c] * C.k[c];
         return U;
     };
+    std::vector<int32_t> up_leaf_beg;
     for (int32_t r0 : subs_up) {
         const std::vector<int32_t> nodes = subtree(CT, r0);
         const int32_t xb = nxh;
+        up_leaf_beg.push_back((int32_t)leaves.size());
         for (int32_t c : nodes) {
             xoff[c] = nxh;
             nxh += C.k[c];
@@ -1620,11 +1735,11 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     h->dn_path = dupload(dn_path, st);
     h->dn_pbeg = dupload(dn_pbeg, st);
     h->dn_lv = dupload(dn_lv, st);
-    h->pb = dalloc<double>(std::max<i64>(plen, 1));
-    LH_CUDA(cudaMemsetAsync(h->pb, 0, sizeof(double) * std::max<i64>(plen, 1), st));
-    h->tu = dalloc<double>(std::max<i64>(tulen, 2));
-    h->td = dalloc<double>(std::max<i64>(tdlen, 2));
-    h->sb = dalloc<double>(std::max<i64>(sblen, 1));
+    h->pb = dalloc<double>(std::max<i64>(plen, 1) + 4);  // + 4: bulk-copy tail slack
+    LH_CUDA(cudaMemsetAsync(h->pb, 0, sizeof(double) * (std::max<i64>(plen, 1) + 4), st));
+    h->tu = dalloc<double>(std::max<i64>(tulen, 2) + 4);
+    h->td = dalloc<double>(std::max<i64>(tdlen, 2) + 4);
+    h->sb = dalloc<double>(std::max<i64>(sblen, 1) + 4);
     h->xh = dalloc<double>(std::max<i64>(nxh, 1));
     run_copies(pj, C.Qt, h->pb);
     run_copies(tj, C.Qt, h->tu);
@@ -1639,6 +1754,103 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     }
     LH_CUDA(cudaStreamSynchronize(st));
     h->bytes = 8 * (plen + tulen + tdlen + sblen) + 8 * (i64)Z.ncols;
+    // fused single-RHS step (default; LEVYH_H2_NOFUSE keeps the combined segment pass): the
+    // dense leaves get a plan of their own for the co-resident segment kernel, and every row
+    // leaf is assigned to a row-subtree CTA that finishes its rows (leaves without a basis
+    // round-robin)
+    if (!getenv("LEVYH_H2_NOFUSE") && !getenv("LEVYH_H2_SPLIT_DENSE") && !subs_dn.empty()) {
+        std::vector<std::vector<H2QLeaf>> per(subs_dn.size());
+        size_t rr = 0;
+        for (int32_t lc : RT.leaves) {
+            const Cluster &cl = RT.nodes[lc];
+            if (cl.size() > 64) return false;
+            H2QLeaf q{0, cl.lo, (int32_t)cl.size(), 0, 0, 0};
+            int sub = -1;
+            if (qnode[lc] >= 0 && insub[lc] >= 0) {
+                const Node &nd = ZS.nodes[qnode[lc]];
+                q.qoff = nd.uoff;
+                q.k = nd.kcap;
+                sub = insub[lc];
+                q.yloc = yoff[lc] - dn_sub[sub].base;
+            } else if (qnode[lc] >= 0) {
+                return false;  // a basis outside every row subtree (not produced by the builder)
+            } else {
+                sub = (int)(rr++ % subs_dn.size());
+            }
+            per[sub].push_back(q);
+        }
+        std::vector<H2QLeaf> ql;
+        std::vector<int32_t> qb{0};
+        for (auto &v : per) {
+            ql.insert(ql.end(), v.begin(), v.end());
+            qb.push_back((int32_t)ql.size());
+        }
+        std::vector<int32_t> dense_ids;
+        for (int32_t b : ZS.leafblocks)
+            if (ZS.nodes[b].kind == K_DENSE) dense_ids.push_back(b);
+        const int fgrid = getenv("LEVYH_H2_DENSE_GRID") ? atoi(getenv("LEVYH_H2_DENSE_GRID")) : 0;
+        auto fd = build_mv_plan(ZS, dense_ids, st, fgrid);
+        fd->lean = getenv("LEVYH_H2_DENSE_CFG") ? atoi(getenv("LEVYH_H2_DENSE_CFG")) : 2;
+        // the two-kernel step (h2step.cu): the same pieces cut into per-CTA chunk lists
+        {
+            H2SInput in;
+            in.n = Z.nrows;
+            in.leaves = &leaves;
+            in.up_leaf_beg = up_leaf_beg;
+            in.up_leaf_beg.push_back((int32_t)leaves.size());
+            in.ups = &ups;
+            in.up_lv = &up_lv;
+            in.up_sub = &up_sub;
+            in.up_xcnt = &up_xcnt;
+            in.maxh_up = maxh_up;
+            in.nsub_up = (int)subs_up.size();
+            in.dns = &dns;
+            in.dn_lv = &dn_lv;
+            in.dn_sub = &dn_sub;
+            in.dn_ycnt = &dn_ycnt;
+            in.dn_path = &dn_path;
+            in.dn_pbeg = &dn_pbeg;
+            in.cpls = &cpls;
+            for (int32_t r0 : subs_dn) in.dn_rows.push_back({RT.nodes[r0].lo, RT.nodes[r0].hi});
+            in.maxh_dn = maxh_dn;
+            in.nsub_dn = (int)subs_dn.size();
+            for (int32_t lc : RT.leaves) {
+                const Cluster &cl = RT.nodes[lc];
+                H2SInput::RLeaf r{cl.lo, cl.size(), 0, 0, -1, -1};
+                if (qnode[lc] >= 0 && insub[lc] >= 0) {
+                    const Node &nd = ZS.nodes[qnode[lc]];
+                    r.k = nd.kcap;
+                    r.qoff = nd.uoff;
+                    r.sub = insub[lc];
+                    r.yloc = yoff[lc] - dn_sub[insub[lc]].base;
+                }
+                in.rleaf.push_back(r);
+            }
+            in.pb = h->pb;
+            in.tu = h->tu;
+            in.td = h->td;
+            in.sb = h->sb;
+            in.zarena = ZS.d_arena;
+            in.segs.resize(fd->nseg);
+            in.batches.resize(fd->nbatch);
+            LH_CUDA(cudaMemcpy(in.segs.data(), fd->segs, sizeof(SegDesc) * fd->nseg, cudaMemcpyDeviceToHost));
+            LH_CUDA(cudaMemcpy(in.batches.data(), fd->batches, sizeof(SBatch) * fd->nbatch, cudaMemcpyDeviceToHost));
+            in.pbuf = fd->pbuf;
+            if (!build_h2s(in, *h, ctx.num_sms, st) && getenv("LEVYH_PLAN_VERBOSE"))
+                fprintf(stderr, "[levyh] H2 step kernels: not built (previous fused step in use)\n");
+        }
+        h->qleaf = dupload(ql, st);
+        h->dn_qbeg = dupload(qb, st);
+        h->zarena = ZS.d_arena;
+        h->yd = dalloc<double>(std::max<i64>(Z.nrows, 1));
+        plan->fdense = fd;
+        if (!plan->fork) {
+            int lo = 0, hi = 0;
+            LH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            LH_CUDA(cudaStreamCreateWithPriority(&plan->fork, cudaStreamNonBlocking, lo));
+            for (cudaEvent_t &e : plan->fev) LH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
     plan->h2 = h;
     if (stats) {
         double ks = 0, nl = 0;

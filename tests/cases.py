@@ -13,6 +13,9 @@ CASES = {
     "cfg3_cgmy": (("cgmy", 1.0, 5.0, 10.0, 0.5), 4.0, 512, 8.0),
     "cfg5_s08": (("power", 0.8), 1.0, 512, 2.0),
     "cfg5_leaf128": (("power", 0.8), 1.0, 1024, 2.0),  # cfg5's leaf size (128)
+    # N = 8191 (tests/golden/make_golden_8191.py): blocks of up to 2048 rows
+    "cfg2_s025_n8191": (("power", 0.25), 1.0, 4096, 2.0),
+    "cfg3_cgmy_n8191": (("cgmy", 1.0, 5.0, 10.0, 0.5), 4.0, 4096, 8.0),
 }
 
 

@@ -95,3 +95,14 @@ def test_cfg3_propagator_nested_bases(P, cfg3):
     assert st[6] == 2.0  # nested H2 bases in use
     assert st[7] <= 1e-10  # probe relative error of the H2 form against the H-form
     assert 4.0 <= st[8] <= 32.0  # mean leaf basis size
+
+
+def test_cfg3_100_steps_propagator_vs_substitution(P, cfg3):
+    """The headline run (cfg3, N = 2^20 - 1, 100 CN steps) on the default path (one H2 matvec of
+    Z per step) against the reference algorithm on the same factors (A- matvec + forward /
+    backward substitution, hops.py:65-70 + :424-432), 100 steps each."""
+    s, _ = cfg3
+    u0 = np.maximum(np.exp(s.x) - 1.0, 0.0)
+    u_prop = P.run_cn(s, u0, 100)
+    u_sub = P.run_cn(s, u0, 100, method="substitution")
+    assert _rel(u_prop, u_sub) <= 1e-8

@@ -9,6 +9,7 @@ import pytest
 from oracle import levyh_oracle as O
 
 CASES = ["cfg1", "cfg2_s025", "cfg2_s075", "cfg3_cgmy", "cfg5_s08", "cfg5_leaf128"]
+BIG = ["cfg2_s025_n8191", "cfg3_cgmy_n8191"]  # symbol only (compression: GPU tests)
 
 
 def _load(golden_dir, name):
@@ -18,14 +19,14 @@ def _load(golden_dir, name):
 def _case_symbol(name, g, golden_dir):
     h = float(g["h"])
     N = int(g["N"])
-    if name == "cfg3_cgmy":
+    if name.startswith("cfg3_cgmy"):
         sc = _load(golden_dir, "cfg3_scalars")
         nu = O.nu_cgmy(1.0, 5.0, 10.0, 0.5)
         tail = float(sc["tail"])
         L_W = 8.0
     else:
         s = {"cfg1": 0.5, "cfg2_s025": 0.25, "cfg2_s075": 0.75, "cfg5_s08": 0.8,
-             "cfg5_leaf128": 0.8}[name]
+             "cfg5_leaf128": 0.8, "cfg2_s025_n8191": 0.25}[name]
         nu = O.nu_power(s)
         L_W = 2.0
         tail = O.tail_power(s, L_W)
@@ -33,7 +34,7 @@ def _case_symbol(name, g, golden_dir):
     return tA, sc
 
 
-@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("name", CASES + BIG)
 def test_symbol_bitexact(name, golden_dir):
     g = _load(golden_dir, name)
     tA, _ = _case_symbol(name, g, golden_dir)
