@@ -182,6 +182,13 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
     t_aca = time.perf_counter() - t1
     s.h_minus = Hm
     mem_p = P.memory_report(Hp)
+    mem["after_assembly"] = used_gb()
+    t_spill = 0.0
+    if method == "propagator":
+        ts = time.perf_counter()
+        Hm.spill()
+        t_spill = time.perf_counter() - ts
+        mem["after_spill_of_A-"] = used_gb()
     t2 = time.perf_counter()
     F = P.hlu(Hp, cfg["eps2"])
     torch.cuda.synchronize()
@@ -195,6 +202,7 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
         F.prepare_inverse()
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t3
+    mem["after_prepare"] = used_gb()
     s.factor = F
     s.method = method
     times = dict(symbol_s=t_symbol, aca_s=t_aca, assembly_s=t_symbol + t_aca, hlu_s=t_lu,
@@ -373,7 +381,12 @@ def run_b200(args, world, rank, local):
     P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, uprof.data_ptr(), 5, mcode,
                                    P._lib.host_ptr(prof)), ctx.h)
     zform = int(F.propagator_stats()[6]) if args.method == "propagator" else 0
-    if args.method == "propagator":
+    if args.method == "propagator" and prof[11] == 1.0:
+        # two-kernel H2 step (h2step.cu): x staging copy, K1 (column walk + the
+        # dense diagonal leaves), K2 (couplings, row walk, row bases Q_t, epilogue)
+        names = ["xpad", "h2s_up(K1)", "h2s_down(K2)"]
+        stored = {"A-": int(prof[12]), "Z=(A+)^-1": int(prof[13]), "LU factor": int(prof[15])}
+    elif args.method == "propagator":
         # nested (H2) form: the walk is four short latency-bound launches (leaf / up / couple /
         # down); the segment kernel is the dominant single kernel
         names = ["walk(Z)" if zform == 2 else "vtx(Z)", "seg(Z)"]
@@ -385,7 +398,10 @@ def run_b200(args, world, rank, local):
     nk = len(names)
     kms = prof[:nk]
     kbytes = prof[6:6 + nk]
-    dom = 1 if zform == 2 else int(np.argmax(kms))
+    if prof[11] == 1.0:
+        dom = 1 + int(np.argmax(kms[1:]))
+    else:
+        dom = 1 if zform == 2 else int(np.argmax(kms))
     peak, peak_src = measured_peaks()
     achieved = kbytes[dom] / (kms[dom] / 1000.0) / 1e9
     step_bytes = float(kbytes.sum())
@@ -545,16 +561,23 @@ def run_cfg4(args, world, rank, local):
 def run_cfg5(args, world, rank, local):
     """BASELINE configs[4]: the large-N phases.  Assembly (symbol + ACA) is sharded across the
     ranks with an NCCL all-gather of the factors; H-LU and the 50 steps run on every rank.
-    The step uses the reference algorithm (matvec + substitution solve) unless --method says
-    otherwise: at N = 2^22 a propagator next to A+ and A- exceeds one GPU's memory."""
+    The step is u <- 2 Z u - u with the propagator Z = (A+)^-1 (default): A- of the CN pair is
+    never read by that step, so it is spilled to pinned host memory (HMatrix.spill) and the HBM
+    holds the factor and Z.  --method substitution runs the reference algorithm (A- matvec +
+    forward/backward substitution) instead."""
     import torch
 
     import paper_1812_08324_b200 as P
 
     cfg = CFG5
-    method = args.method if args.method_set else "substitution"
+    method = args.method if args.method_set else "propagator"
     if method != "propagator":
         os.environ["LEVYH_NO_BG_PROP"] = "1"  # no propagator plan (host and device memory)
+    mem = {}
+
+    def used_gb():
+        free_b, total_b = torch.cuda.mem_get_info()
+        return round((total_b - free_b) / 1e9, 2)
     t0 = time.perf_counter()
     s = P.FracCNSystem(P.power_measure(1, 0.8), 0.1, 0.0, 0.0, cfg["n"], 1.0 / cfg["n"],
                        distributed=world > 1)
@@ -568,6 +591,13 @@ def run_cfg5(args, world, rank, local):
     torch.cuda.synchronize()
     t_aca = time.perf_counter() - t1
     mem_p = P.memory_report(Hp)
+    mem["after_assembly"] = used_gb()
+    t_spill = 0.0
+    if method == "propagator":
+        ts = time.perf_counter()
+        Hm.spill()
+        t_spill = time.perf_counter() - ts
+        mem["after_spill_of_A-"] = used_gb()
     t2 = time.perf_counter()
     F = P.hlu(Hp, cfg["eps2"])
     torch.cuda.synchronize()
@@ -581,6 +611,7 @@ def run_cfg5(args, world, rank, local):
         F.prepare_inverse()
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t3
+    mem["after_prepare"] = used_gb()
     ctx, L, N = Hm.ctx, P._lib.lib(), s.N
     u0 = np.maximum(1.0 - s.x ** 2, 0.0) ** 3
     u = torch.from_numpy(u0.copy()).cuda()
@@ -620,7 +651,12 @@ def run_cfg5(args, world, rank, local):
                       "assembly_sharding": (Hp.shard_stats if getattr(Hp, "shard_stats", None)
                                             else "unsharded (1 rank)"),
                       "stored_scalars_plus": mem_p["stored_scalars"],
-                      "device_mem_used_gb": round((total_b - free_b) / 1e9, 2)}}
+                      "spill_A-_s": round(t_spill, 3),
+                      "device_mem_used_gb": round((total_b - free_b) / 1e9, 2), "device_mem_gb": mem}}
+    if method == "propagator":
+        zs = F.propagator_stats()
+        out["phases"]["propagator_form"] = int(zs[6])
+        out["phases"]["propagator_form_probe_rel_err"] = f"{zs[7]:.2e}"
     if rank == 0:
         print(json.dumps(out), flush=True)
 

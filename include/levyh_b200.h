@@ -119,6 +119,14 @@ int lh_hmat_derive_toeplitz(lh_ctx *ctx, const lh_hmat *src, const double *t_dev
                             int32_t kcap, lh_hmat **out);
 int lh_hmat_clone(lh_ctx *ctx, const lh_hmat *src, int32_t kcap, lh_hmat **out);
 void lh_hmat_destroy(lh_hmat *h);
+/* Memory management (no reference counterpart: levyh keeps every operator in host RAM).
+ * lh_hmat_spill moves an unfactored H-matrix's arena to pinned host memory and frees its device
+ * copy and matvec plan; every call that reads the arena (matvec, entry, exports, derive, hlu,
+ * trisolve, save, steps that read A-) brings it back first.  Used for A- of the CN pair when
+ * the step is u <- 2 Z u - u and never reads A- (levy.FracCNSystem.prepare(spill_minus=True),
+ * cfg5 at N = 2^22).  lh_hmat_resident: 1 on the device, 0 spilled. */
+int lh_hmat_spill(lh_ctx *ctx, lh_hmat *h);
+int lh_hmat_resident(const lh_hmat *h);
 
 /* ---- introspection: hmatrix.py:343-433 -------------------------------- */
 int64_t lh_hmat_num_blocks(const lh_hmat *h);
@@ -230,7 +238,9 @@ int lh_cn_step_host(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, const d
  * vtx(L^-1), seg(L^-1), vtx(U^-1), seg(U^-1); out[6..11] their algorithmic bytes;
  * out[12..14] stored scalars of H-, L^-1, U^-1.  method 2: out[0..1], out[6..7] for
  * phase 1 of Z (V^T x, or the H2 walk when lh_propagator_stats reports form 2) and the
- * segment kernel (others 0); out[12] H-, out[13] Z in the form the step streams.  out[15]
+ * segment kernel (others 0); when Z runs the two-kernel H2 step, out[11] = 1 and out[0..2] /
+ * out[6..8] are the x staging copy, K1 (column walk + dense diagonal leaves) and K2 (couplings,
+ * row walk, row bases).  out[12] H-, out[13] Z in the form the step streams.  out[15]
  * stored scalars of the factor. */
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev,
                     int32_t iters, int32_t method, double *out_host);

@@ -58,6 +58,8 @@ SIGNATURES = [
     ("lh_hmat_build_dense", C.c_int, [P, P, P, P, I64, C.c_int, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_derive_toeplitz", C.c_int, [P, P, P, D, I32, C.POINTER(P)]),
     ("lh_hmat_clone", C.c_int, [P, P, I32, C.POINTER(P)]),
+    ("lh_hmat_spill", C.c_int, [P, P]),
+    ("lh_hmat_resident", C.c_int, [P]),
     ("lh_hmat_destroy", None, [P]),
     ("lh_hmat_num_blocks", I64, [P]),
     ("lh_hmat_structure", C.c_int, [P, P, P]),

@@ -113,6 +113,54 @@ HMat::~HMat() {
     if (d_ranks) cudaFree(d_ranks);
     if (d_perm) cudaFree(d_perm);
     if (d_inv) cudaFree(d_inv);
+    if (h_spill) cudaFreeHost(h_spill);
+}
+void spill_arena(HMat &H, cudaStream_t s) {
+    if (H.h_spill || !H.d_arena) return;
+    LH_REQUIRE(!H.shard, LH_EINVAL, "cannot spill an H-matrix with a pending sharded assembly");
+    {  // refuse rather than push the host into swap / the OOM killer: keep half of it free
+        long long avail_kb = -1;
+        if (FILE *f = fopen("/proc/meminfo", "r")) {
+            char key[64];
+            long long v = 0;
+            while (fscanf(f, "%63s %lld kB\n", key, &v) == 2)
+                if (!strcmp(key, "MemAvailable:")) {
+                    avail_kb = v;
+                    break;
+                }
+            fclose(f);
+        }
+        const double need = 8.0 * (double)H.arena_len;
+        LH_REQUIRE(avail_kb < 0 || need <= 0.5 * 1024.0 * (double)avail_kb, LH_ENOMEM,
+                   "spill: not enough available host memory for the arena");
+    }
+    double *hp = nullptr;
+    LH_CUDA(cudaMallocHost(&hp, sizeof(double) * (size_t)std::max<i64>(H.arena_len, 1)));
+    cudaError_t e = cudaMemcpyAsync(hp, H.d_arena, sizeof(double) * (size_t)H.arena_len, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cudaFreeHost(hp);
+        LH_CUDA(e);
+    }
+    H.mv_plan.reset();
+    cudaFree(H.d_arena);
+    H.d_arena = nullptr;
+    H.h_spill = hp;
+    ++H.gen;
+}
+void ensure_resident(HMat &H, cudaStream_t s) {
+    if (!H.h_spill) return;
+    double *d = dalloc<double>(std::max<i64>(H.arena_len, 1));
+    cudaError_t e = cudaMemcpyAsync(d, H.h_spill, sizeof(double) * (size_t)H.arena_len, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        LH_CUDA(e);
+    }
+    cudaFreeHost(H.h_spill);
+    H.h_spill = nullptr;
+    H.d_arena = d;
+    ++H.gen;
 }
 void HMat::sync_ranks(cudaStream_t s) {
     h_ranks.assign(std::max(nslots, 0), 0);
@@ -141,6 +189,13 @@ static int guard(lh_ctx *ctx, F &&f) {
         if (ctx) ctx->c.last_error = e.what();
         return LH_EINTERNAL;
     }
+}
+
+// the H-matrix with its arena on the device (brings a spilled arena back first)
+static HMat &resident(lh_ctx *ctx, const lh_hmat *h) {
+    HMat &H = const_cast<HMat &>(h->h);
+    ensure_resident(H, ctx->c.stream);
+    return H;
 }
 
 static void check_cfg(const lh_hconfig *cfg) {
@@ -312,7 +367,7 @@ int lh_hmat_build_toeplitz_shard(lh_ctx *ctx, const lh_tree *rt, const lh_tree *
 }
 
 int lh_hmat_shard_pack(lh_ctx *ctx, lh_hmat *h, double *buf_dev, int64_t cap, int64_t *len) {
-    return guard(ctx, [&] { *len = shard_pack(ctx->c, h->h, buf_dev, cap); });
+    return guard(ctx, [&] { *len = shard_pack(ctx->c, resident(ctx, h), buf_dev, cap); });
 }
 
 int lh_hmat_shard_unpack(lh_ctx *ctx, lh_hmat *h, int32_t src_rank, const double *buf_dev,
@@ -400,7 +455,7 @@ int lh_hmat_derive_toeplitz(lh_ctx *ctx, const lh_hmat *src, const double *t_dev
     lh_hmat *o = nullptr;
     int rc = guard(ctx, [&] {
         o = new lh_hmat();
-        derive(ctx->c, src->h, o->h, t_dev, lr_scale, kcap);
+        derive(ctx->c, resident(ctx, src), o->h, t_dev, lr_scale, kcap);
     });
     if (rc != LH_OK) {
         delete o;
@@ -414,7 +469,7 @@ int lh_hmat_clone(lh_ctx *ctx, const lh_hmat *src, int32_t kcap, lh_hmat **out) 
     lh_hmat *o = nullptr;
     int rc = guard(ctx, [&] {
         o = new lh_hmat();
-        derive(ctx->c, src->h, o->h, nullptr, 1.0, kcap);
+        derive(ctx->c, resident(ctx, src), o->h, nullptr, 1.0, kcap);
     });
     if (rc != LH_OK) {
         delete o;
@@ -427,6 +482,17 @@ int lh_hmat_clone(lh_ctx *ctx, const lh_hmat *src, int32_t kcap, lh_hmat **out) 
 void lh_hmat_destroy(lh_hmat *h) { delete h; }
 
 int64_t lh_hmat_num_blocks(const lh_hmat *h) { return (int64_t)h->h.leafblocks.size(); }
+
+int lh_hmat_spill(lh_ctx *ctx, lh_hmat *h) {
+    return guard(ctx, [&] {
+        HMat &H = h->h;
+        LH_REQUIRE(!H.factored && !H.solve_plan && !H.inv_plan, LH_EINVAL,
+                   "only an unfactored H-matrix without solve plans can be spilled");
+        spill_arena(H, ctx->c.stream);
+    });
+}
+
+int lh_hmat_resident(const lh_hmat *h) { return h->h.h_spill ? 0 : 1; }
 
 int lh_hmat_structure(lh_ctx *ctx, const lh_hmat *h, int64_t *recs) {
     return guard(ctx, [&] {
@@ -471,7 +537,7 @@ int lh_hmat_memory(lh_ctx *ctx, const lh_hmat *h, int64_t *stats) {
 
 int lh_hmat_entry(lh_ctx *ctx, const lh_hmat *h, int64_t i, int64_t j, double *out) {
     return guard(ctx, [&] {
-        const HMat &H = h->h;
+        const HMat &H = resident(ctx, h);
         LH_REQUIRE(i >= 0 && i < H.nrows && j >= 0 && j < H.ncols, LH_EINVAL, "entry outside the matrix");
         int32_t b = H.root;
         while (H.nodes[b].kind == K_HIER) {  // refined dense leaves keep their leaf kind
@@ -509,7 +575,7 @@ int lh_hmat_entry(lh_ctx *ctx, const lh_hmat *h, int64_t i, int64_t j, double *o
 
 int lh_hmat_export_block(lh_ctx *ctx, const lh_hmat *h, int64_t block, double *a, double *b) {
     return guard(ctx, [&] {
-        const HMat &H = h->h;
+        const HMat &H = resident(ctx, h);
         LH_REQUIRE(block >= 0 && block < (int64_t)H.leafblocks.size(), LH_EINVAL, "block index");
         const Node &nd = H.nodes[H.leafblocks[block]];
         cudaStream_t s = ctx->c.stream;
@@ -567,7 +633,7 @@ int lh_hmat_layout(const lh_hmat *h, int64_t *recs, int64_t *sizes) {
 int lh_hmat_export_arena(lh_ctx *ctx, const lh_hmat *h, double *arena, int32_t *ranks,
                          int32_t *perm) {
     return guard(ctx, [&] {
-        const HMat &H = h->h;
+        const HMat &H = resident(ctx, h);
         cudaStream_t s = ctx->c.stream;
         if (arena && H.arena_len)
             LH_CUDA(cudaMemcpyAsync(arena, H.d_arena, sizeof(double) * H.arena_len,
@@ -603,11 +669,11 @@ int lh_hmat_export_arena(lh_ctx *ctx, const lh_hmat *h, double *arena, int32_t *
 
 int lh_hmat_matvec(lh_ctx *ctx, const lh_hmat *h, const double *x, int64_t ldx, double *y,
                    int64_t ldy, int32_t nrhs) {
-    return guard(ctx, [&] { matvec(ctx->c, const_cast<HMat &>(h->h), x, ldx, y, ldy, nrhs); });
+    return guard(ctx, [&] { matvec(ctx->c, resident(ctx, h), x, ldx, y, ldy, nrhs); });
 }
 
 int lh_hlu(lh_ctx *ctx, lh_hmat *h, double eps2) {
-    return guard(ctx, [&] { hlu(ctx->c, h->h, eps2); });
+    return guard(ctx, [&] { hlu(ctx->c, resident(ctx, h), eps2); });
 }
 
 int lh_solve(lh_ctx *ctx, lh_hmat *f, double *b, int64_t ldb, int32_t nrhs, int32_t method) {
@@ -634,7 +700,7 @@ int lh_cn_last_path(lh_hmat *f, int32_t *out) {
 
 int lh_trisolve_dense(lh_ctx *ctx, lh_hmat *t, int32_t mode, int32_t unit, double *b, int64_t ldb,
                       int32_t nrhs) {
-    return guard(ctx, [&] { trisolve_dense(ctx->c, t->h, mode, unit != 0, b, ldb, nrhs); });
+    return guard(ctx, [&] { trisolve_dense(ctx->c, resident(ctx, t), mode, unit != 0, b, ldb, nrhs); });
 }
 
 int lh_trisolve_block(lh_ctx *ctx, lh_hmat *t, const lh_hmat *b, int32_t mode, int32_t unit, double eps2,
@@ -648,8 +714,8 @@ int lh_trisolve_block(lh_ctx *ctx, lh_hmat *t, const lh_hmat *b, int32_t mode, i
                        b->h.ct == t->h.ct,
                    LH_EINVAL, "block right-hand side must share the triangle's cluster trees");
         o = new lh_hmat();
-        derive(ctx->c, b->h, o->h, nullptr, 1.0, 32);  // deep copy (hops.py:294, :307)
-        trisolve_block(ctx->c, t->h, o->h, mode, unit != 0, eps2);
+        derive(ctx->c, resident(ctx, b), o->h, nullptr, 1.0, 32);  // deep copy (hops.py:294, :307)
+        trisolve_block(ctx->c, resident(ctx, t), o->h, mode, unit != 0, eps2);
     });
     if (rc != LH_OK) {
         delete o;
@@ -706,7 +772,7 @@ int lh_hlu_stats(const lh_hmat *f, double *out) {
 int lh_hmat_save(lh_ctx *ctx, const lh_hmat *h, double eps2, const char *path) {
     return guard(ctx, [&] {
         LH_REQUIRE(h != nullptr && path != nullptr, LH_EINVAL, "save: null argument");
-        save_hmat(ctx->c, const_cast<HMat &>(h->h), eps2, path);
+        save_hmat(ctx->c, resident(ctx, h), eps2, path);
     });
 }
 

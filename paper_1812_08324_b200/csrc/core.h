@@ -114,6 +114,10 @@ struct HMat {
     i64 perm_len = 0;
     double *d_inv = nullptr;          // FDENSE packed leaf inverses
     i64 inv_len = 0;
+    // host spill (lh_hmat_spill): the arena lives in pinned host memory and d_arena is null until
+    // ensure_resident() brings it back; gen counts the moves (caches holding arena pointers key on it)
+    double *h_spill = nullptr;
+    uint64_t gen = 0;
     bool factored = false;
     bool refined = false;             // dense leaves > 64 split for the H-arithmetic planner
     double lu_stats[6] = {0, 0, 0, 0, 0, 0};  // tasks, plan s, temp bytes, exec s, chunks / NF leaves, merges
@@ -126,6 +130,12 @@ struct HMat {
     ~HMat();
     void sync_ranks(cudaStream_t s);
 };
+
+// Moves H's arena to pinned host memory and frees the device copy and H's matvec plan
+// (derived operators that a step never reads: A- of the CN pair under the propagator).
+void spill_arena(HMat &H, cudaStream_t s);
+// Brings a spilled arena back (no-op when resident); every path that reads H's arena calls it.
+void ensure_resident(HMat &H, cudaStream_t s);
 
 // Partition exactly as build_from_dense decides it (hmatrix.py:319-337), with every
 // admissible block with min(m,n) > n_min marked K_LR (compression decides later).

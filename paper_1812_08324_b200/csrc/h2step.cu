@@ -1095,7 +1095,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
 }
 
 static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const double *z, int zmode,
-                        cudaStream_t s) {
+                        cudaStream_t s, cudaEvent_t *ev = nullptr) {
     const H2S &S = *h.step2;
     static bool attr = false;
     if (!attr) {
@@ -1108,7 +1108,9 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     K1Args a1{S.c1, S.cb1, S.lb1, S.ub1, S.sb1, S.sl1, S.leaf, S.up, h.xh, S.yd, S.xsmax,
               h.ups, h.up_chain, h.up_cbeg, h.cnt, h.tu, (dbg >> 2) & 7, nullptr};
     static unsigned long long *trace = nullptr;
-    if (getenv("LEVYH_H2S_TRACE")) {  // timing experiments only: per-CTA phase times of K1
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    LH_CUDA(cudaStreamIsCapturing(s, &cap));
+    if (getenv("LEVYH_H2S_TRACE") && cap == cudaStreamCaptureStatusNone) {  // timing experiments only: per-CTA phase times
         if (!trace) trace = dalloc<unsigned long long>((i64)S.G * 16);
         a1.trace = trace;
     }
@@ -1116,11 +1118,14 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     if (a1.trace)
         for (auto &e : te) cudaEventCreate(&e);
     if (a1.trace) cudaEventRecord(te[0], s);
+    if (ev) LH_CUDA(cudaEventRecord(ev[0], s));
     if (!(dbg & 1)) h2s_up_kernel<<<S.G, CONS_T + 64, S.smem1, s>>>(a1);
+    if (ev) LH_CUDA(cudaEventRecord(ev[1], s));
     if (a1.trace) cudaEventRecord(te[1], s);
     K2Args a2{S.c2, S.cb2, S.nb2, S.eb2, S.pb2, S.db2, S.qb2, S.cn, S.ce, S.path, S.dn, S.q, h.xh,
               S.wsmax, S.ysmax, z, y, alpha, beta, zmode, a1.trace ? a1.trace + (size_t)S.G * 8 : nullptr};
     if (!(dbg & 2)) h2s_down_kernel<<<S.G, CONS_T + 32, S.smem2, s>>>(a2);
+    if (ev) LH_CUDA(cudaEventRecord(ev[2], s));
     LH_CUDA(cudaGetLastError());
     if (a1.trace && !getenv("LEVYH_H2S_TRACE_DONE")) {
         std::vector<unsigned long long> t((size_t)S.G * 16);
@@ -1165,6 +1170,14 @@ void h2s_launch(const H2 &h, const double *x, double *y, double alpha, double be
     const H2S &S = *h.step2;
     xpad_kernel<<<(int)std::min<i64>((S.n + 2 + NT - 1) / NT, 148 * 8), NT, 0, s>>>(x, S.n, S.xpad);
     h2s_kernels(h, y, alpha, beta, z, beta == 0.0 ? 0 : (z == x ? 1 : 2), s);
+}
+
+void h2s_launch_timed(const H2 &h, const double *x, double *y, double alpha, double beta, const double *z,
+                      cudaStream_t s, cudaEvent_t *ev) {
+    const H2S &S = *h.step2;
+    LH_CUDA(cudaEventRecord(ev[0], s));
+    xpad_kernel<<<(int)std::min<i64>((S.n + 2 + NT - 1) / NT, 148 * 8), NT, 0, s>>>(x, S.n, S.xpad);
+    h2s_kernels(h, y, alpha, beta, z, beta == 0.0 ? 0 : (z == x ? 1 : 2), s, ev + 1);
 }
 
 void h2s_launch_host(const H2 &h, const double *x_host, double *y_dev, double *y_host, double alpha, double beta,

@@ -126,6 +126,9 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st);
 // y = alpha Z x + beta z (z = x when z_is_x) with the two kernels, on stream s
 void h2s_launch(const H2 &h, const double *x, double *y, double alpha, double beta, const double *z,
                 cudaStream_t s);
+// the same with events around the three launches (ev[0] xpad ev[1] K1 ev[2] K2 ev[3]); profiling
+void h2s_launch_timed(const H2 &h, const double *x, double *y, double alpha, double beta, const double *z,
+                      cudaStream_t s, cudaEvent_t *ev);
 // the same with x arriving from (pinned) host memory straight into the aligned staging copy and
 // y leaving to host memory; z = x (beta != 0).  Capturable.
 void h2s_launch_host(const H2 &h, const double *x_host, double *y_dev, double *y_host, double alpha, double beta,

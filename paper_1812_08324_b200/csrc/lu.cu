@@ -1903,6 +1903,7 @@ struct SolvePlans {
     cudaGraphExec_t graph = nullptr;  // cached CN step
     const double *g_u = nullptr, *g_y = nullptr;
     uint64_t g_hm = 0;  // HMat::id of the hminus the graph was captured with
+    uint64_t g_gen = 0;  // and its storage generation (HMat::gen)
     // host-buffer CN step (cn_step_host): pipelined graph keyed by the host pointers
     cudaGraphExec_t hgraph = nullptr;
     const double *hg_in = nullptr;
@@ -2443,7 +2444,6 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
     SolvePlans &S = plans_of(F);
     if (method == 2) LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
     else LH_REQUIRE(S.XL != nullptr, LH_EINVAL, "call prepare_inverse first");
-    MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
     double *y = (double *)ctx.ensure_scratch(sizeof(double) * (size_t)Hm.nrows);
     Hm.sync_ranks(ctx.stream);
     struct Mv {
@@ -2460,10 +2460,39 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
     } else {
         S.XL->sync_ranks(ctx.stream);
         S.XU->sync_ranks(ctx.stream);
-        mv.push_back({&Pm, &Hm, u, y, 1.0, 0.0, nullptr});
+        mv.push_back({&get_mv_plan(Hm, ctx.stream), &Hm, u, y, 1.0, 0.0, nullptr});
         mv.push_back({S.mvL.get(), S.XL.get(), y, S.tmp, 1.0, 0.0, nullptr});
         mv.push_back({S.mvU.get(), S.XU.get(), S.tmp, u, 1.0, 0.0, nullptr});
     }
+    if (method == 2 && S.z1plan().h2 && S.z1plan().h2->step2) {
+        const MvPlan &Pz = S.z1plan();
+        // two-kernel H2 step (h2step.cu): xpad / K1 / K2 timed separately; bytes are the ring
+        // operands each kernel streams plus its vector writes (yd by K1, y by K2) and the
+        // staging copy of x (read + write)
+        cudaEvent_t ev[4];
+        for (auto &e : ev) LH_CUDA(cudaEventCreate(&e));
+        double acc3[3] = {0, 0, 0};
+        for (int it = 0; it < iters; ++it) {
+            h2s_launch_timed(*Pz.h2, u, y, 2.0, -1.0, u, ctx.stream, ev);
+            LH_CUDA(cudaEventRecord(ev[3], ctx.stream));
+            LH_CUDA(cudaMemcpyAsync(u, y, sizeof(double) * Hm.nrows, cudaMemcpyDeviceToDevice, ctx.stream));
+            LH_CUDA(cudaEventSynchronize(ev[3]));
+            for (int k = 0; k < 3; ++k) {
+                float ms = 0.f;
+                LH_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+                acc3[k] += ms;
+            }
+        }
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        for (auto &e : ev) cudaEventDestroy(e);
+        for (int k = 0; k < 16; ++k) out[k] = 0.0;
+        const H2S &S2 = *Pz.h2->step2;
+        for (int k = 0; k < 3; ++k) out[k] = acc3[k] / std::max(iters, 1);
+        out[6] = 16.0 * Hm.nrows;
+        out[7] = (double)S2.bytes1 + 8.0 * Hm.nrows;
+        out[8] = (double)S2.bytes2 + 8.0 * Hm.nrows;
+        out[11] = 1.0;  // layout flag: xpad, K1, K2
+    } else {
     const int nk = 2 * (int)mv.size();
     cudaEvent_t ev[7];
     for (auto &e : ev) LH_CUDA(cudaEventCreate(&e));
@@ -2491,6 +2520,7 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
     for (auto &e : ev) cudaEventDestroy(e);
     for (int k = 0; k < 16; ++k) out[k] = 0.0;
     for (int k = 0; k < nk; ++k) out[k] = acc[k] / std::max(iters, 1);
+    }
     auto nonzero = [](const HMat &H) {
         std::vector<int32_t> bl;
         for (int32_t b : H.leafblocks)
@@ -2506,7 +2536,7 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
         }
         return s;
     };
-    for (size_t q = 0; q < mv.size(); ++q) {
+    for (size_t q = 0; q < mv.size() && out[11] == 0.0; ++q) {
         const auto bl = nonzero(*mv[q].H);
         mv_bytes(*mv[q].H, bl, out[6 + 2 * q], out[7 + 2 * q]);
         if (mv[q].z && mv[q].z != mv[q].y) out[7 + 2 * q] += 8.0 * mv[q].H->nrows;  // reads z
@@ -2527,7 +2557,10 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method) {
     LH_REQUIRE(F.factored, LH_EINVAL, "cn_steps needs an H-LU factorization of A+");
     LH_REQUIRE(Hm.nrows == F.nrows, LH_EINVAL, "operator sizes differ");
-    MvPlan &Pm = get_mv_plan(Hm, ctx.stream);
+    // A-'s matvec plan only when the step reads A- (not for u <- 2 Z u - u on the CN pair, so a
+    // spilled A- stays on the host)
+    const bool pair2 = method == 2 && cn_pair_ok(Hm, F);
+    MvPlan *Pmp = pair2 ? nullptr : &get_mv_plan(Hm, ctx.stream);
     double *y = (double *)ctx.ensure_scratch(sizeof(double) * (size_t)Hm.nrows);
     if (method == 1 || method == 2) {
         SolvePlans &S = plans_of(F);
@@ -2548,14 +2581,14 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
             // the two plans share the context's grow-only scratch: size it for both before taking
             // pointers (a later, larger request would reallocate under the first plan's pointers)
             mm_bufs(ctx, *S.mvZ, ldk);
-            MmBufs bm = mm_bufs(ctx, Pm, ldk);
+            MmBufs bm = shape == 3 ? mm_bufs(ctx, *Pmp, ldk) : MmBufs{};
             MmBufs bz = mm_bufs(ctx, *S.mvZ, ldk);
             mm_transpose(u, ldu, Xr, ldk, n, nrhs, true, ctx.stream);
             for (int k = 0; k < nsteps; ++k) {
                 if (shape == 2) {
                     mm_run(*S.mvZ, Xr, Yr, ldk, 2.0, -1.0, Xr, bz.T, bz.part, ctx.stream);
                 } else {
-                    mm_run(Pm, Xr, Yr, ldk, 1.0, 0.0, nullptr, bm.T, bm.part, ctx.stream);
+                    mm_run(*Pmp, Xr, Yr, ldk, 1.0, 0.0, nullptr, bm.T, bm.part, ctx.stream);
                     std::swap(Xr, Yr);
                     mm_run(*S.mvZ, Xr, Yr, ldk, 1.0, 0.0, nullptr, bz.T, bz.part, ctx.stream);
                 }
@@ -2567,7 +2600,8 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
         }
         for (int q = 0; q < nrhs; ++q) {
             double *uq = u + (i64)q * ldu;
-            if (!(S.graph && S.g_u == uq && S.g_hm == Hm.id && S.g_y == y && S.g_method == shape)) {
+            if (!(S.graph && S.g_u == uq && S.g_hm == Hm.id && S.g_gen == Hm.gen && S.g_y == y &&
+                  S.g_method == shape)) {
                 if (S.graph) {
                     cudaGraphExecDestroy(S.graph);
                     S.graph = nullptr;
@@ -2576,7 +2610,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                 LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
                 try {
                     if (shape == 1) {
-                        mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                        mv_run(*Pmp, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
                         mv_run(*S.mvL, *S.XL, y, S.tmp, 1.0, 0.0, ctx.stream, ctx.num_sms);
                         mv_run(*S.mvU, *S.XU, S.tmp, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
                     } else if (shape == 2) {
@@ -2584,7 +2618,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                         LH_CUDA(cudaMemcpyAsync(uq, y, sizeof(double) * Hm.nrows,
                                                 cudaMemcpyDeviceToDevice, ctx.stream));
                     } else {
-                        mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+                        mv_run(*Pmp, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
                         mv_run(S.z1plan(), S.z1mat(), y, uq, 1.0, 0.0, ctx.stream, ctx.num_sms);
                     }
                 } catch (...) {
@@ -2606,6 +2640,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                 cudaGraphDestroy(g);
                 S.g_u = uq;
                 S.g_hm = Hm.id;
+                S.g_gen = Hm.gen;
                 S.g_y = y;
                 S.g_method = shape;
             }
@@ -2623,7 +2658,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
     for (int q = 0; q < nrhs; ++q) {
         double *uq = u + (i64)q * ldu;
         for (int k = 0; k < nsteps; ++k) {
-            mv_run(Pm, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
+            mv_run(*Pmp, Hm, uq, y, 1.0, 0.0, ctx.stream, ctx.num_sms);
             LH_CUDA(cudaMemcpyAsync(uq, y, sizeof(double) * Hm.nrows, cudaMemcpyDeviceToDevice,
                                     ctx.stream));
             solve_substitution(ctx, F, uq, Hm.nrows, 1);

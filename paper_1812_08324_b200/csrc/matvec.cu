@@ -1065,6 +1065,7 @@ void treduce_launch(const TJob *jobs, int n, const double *part, double *out, cu
 }
 
 MvPlan &get_mv_plan(HMat &H, cudaStream_t s) {
+    ensure_resident(H, s);
     if (!H.mv_plan) {
         auto p = build_mv_plan(H, H.leafblocks, s);
         H.mv_plan = std::static_pointer_cast<void>(p);

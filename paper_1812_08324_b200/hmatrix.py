@@ -130,6 +130,15 @@ class HMatrix:
         out = HMatrix(h, self.row_tree, self.col_tree, self.eta, self.ctx, self.cfg)
         return out
 
+    def spill(self):
+        """Move the stored blocks to pinned host memory, freeing their HBM; any later call that
+        reads them brings them back (lh_hmat_spill).  Unfactored H-matrices only."""
+        _lib.check(_lib.lib().lh_hmat_spill(self.ctx.h, self.handle), self.ctx.h)
+
+    @property
+    def resident(self):
+        return bool(_lib.lib().lh_hmat_resident(self.handle))
+
     def release(self):
         if self._h is not None:
             _lib.lib().lh_hmat_destroy(self._h)

@@ -269,11 +269,16 @@ class FracCNSystem:
         Hm = derive_toeplitz(Hp, self.tMinus, lr_scale=-1.0, kcap=0)
         return Hp, Hm
 
-    def prepare(self, cfg=None, eps2=1e-10, method="propagator"):
+    def prepare(self, cfg=None, eps2=1e-10, method="propagator", spill_minus=False):
         """Factorise A+ once and keep A- for stepping (levy.py:241-246).  ``method`` as in
-        CNSystem.prepare: "propagator" (default), "inverse" or "substitution"."""
+        CNSystem.prepare: "propagator" (default), "inverse" or "substitution".
+        ``spill_minus``: with the propagator the CN step is u <- 2 Z u - u and never reads A-,
+        so A- moves to pinned host memory (HMatrix.spill) and its HBM holds Z instead (N = 2^22);
+        it comes back on first use."""
         Hp, Hm = self.build_pair(cfg)
         self.h_minus = Hm
+        if spill_minus and method == "propagator":
+            Hm.spill()
         self.factor = hlu(Hp, eps2)
         if method == "inverse":
             self.factor.prepare_inverse()

@@ -11,7 +11,8 @@ import subprocess
 import sys
 
 NAMES = {"seg_tma_kernel": "seg(Z)", "vtx_kernel<8>": "vtx(Z)", "h2_leaf_kernel": "h2_leaf",
-         "h2_up_kernel": "h2_up", "h2_couple_kernel": "h2_couple", "h2_down_kernel": "h2_down"}
+         "h2_up_kernel": "h2_up", "h2_couple_kernel": "h2_couple", "h2_down_kernel": "h2_down",
+         "h2s_up_kernel": "h2s_up(K1)", "h2s_down_kernel": "h2s_down(K2)", "xpad_kernel": "xpad"}
 
 
 def main():

@@ -10,6 +10,6 @@ timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/bench_small.jso
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/ncu_launch.log 2>&1
 echo "launch list rc=$?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"seg_tma_kernel|h2_leaf|h2_up|h2_couple|h2_down" \
-    -s 20 -c 10 -o $OUT/step_prof python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/ncu_full.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"h2s_up_kernel|h2s_down_kernel|xpad_kernel" \
+    -s 12 -c 6 -o $OUT/step_prof python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/ncu_full.log 2>&1
 echo "full capture rc=$?"
