@@ -182,13 +182,6 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
     t_aca = time.perf_counter() - t1
     s.h_minus = Hm
     mem_p = P.memory_report(Hp)
-    mem["after_assembly"] = used_gb()
-    t_spill = 0.0
-    if method == "propagator":
-        ts = time.perf_counter()
-        Hm.spill()
-        t_spill = time.perf_counter() - ts
-        mem["after_spill_of_A-"] = used_gb()
     t2 = time.perf_counter()
     F = P.hlu(Hp, cfg["eps2"])
     torch.cuda.synchronize()
@@ -202,7 +195,6 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
         F.prepare_inverse()
     torch.cuda.synchronize()
     t_prep = time.perf_counter() - t3
-    mem["after_prepare"] = used_gb()
     s.factor = F
     s.method = method
     times = dict(symbol_s=t_symbol, aca_s=t_aca, assembly_s=t_symbol + t_aca, hlu_s=t_lu,
@@ -281,6 +273,64 @@ def cpu_info():
     except Exception:
         pass
     return info
+
+
+def step_roofline(P, ctx, Hm, F, u0, method, ms_per_step, N, traffic_file=True):
+    """Per-kernel roofline of one CN step (lh_step_profile: CUDA events on the library stream
+    around each launch, 5 steps, algorithmic bytes per launch) against the measured HBM peak."""
+    import torch
+
+    L = P._lib.lib()
+    mcode = P.SOLVE_METHODS[method]
+    prof = np.zeros(16)
+    uprof = torch.from_numpy(np.asarray(u0, dtype=float).copy()).cuda()
+    P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, uprof.data_ptr(), 5, mcode,
+                                   P._lib.host_ptr(prof)), ctx.h)
+    zform = int(F.propagator_stats()[6]) if method == "propagator" else 0
+    if method == "propagator" and prof[11] == 1.0:
+        # two-kernel H2 step (h2step.cu, DESIGN.md 4): x staging copy, K1 (column walk + the
+        # dense diagonal leaves), K2 (couplings, row walk, row bases Q_t, epilogue)
+        names = ["xpad", "h2s_up(K1)", "h2s_down(K2)"]
+        stored = {"A-": int(prof[12]), "Z=(A+)^-1": int(prof[13]), "LU factor": int(prof[15])}
+    elif method == "propagator":
+        # nested (H2) form: the walk is four short latency-bound launches (leaf / up / couple /
+        # down, DESIGN.md 5); the segment kernel is the dominant single kernel
+        names = ["walk(Z)" if zform == 2 else "vtx(Z)", "seg(Z)"]
+        stored = {"A-": int(prof[12]), "Z=(A+)^-1": int(prof[13]), "LU factor": int(prof[15])}
+    else:
+        names = ["vtx(A-)", "seg(A-)", "vtx(L^-1)", "seg(L^-1)", "vtx(U^-1)", "seg(U^-1)"]
+        stored = {"A-": int(prof[12]), "L^-1": int(prof[13]), "U^-1": int(prof[14]),
+                  "LU factor": int(prof[15])}
+    nk = len(names)
+    kms = prof[:nk]
+    kbytes = prof[6:6 + nk]
+    if prof[11] == 1.0:
+        dom = 1 + int(np.argmax(kms[1:]))
+    else:
+        dom = 1 if zform == 2 else int(np.argmax(kms))
+    peak, peak_src = measured_peaks()
+    achieved = kbytes[dom] / (kms[dom] / 1000.0) / 1e9
+    step_bytes = float(kbytes.sum())
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if traffic_file and os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(names[dom])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": float(kbytes[dom]),
+                "kernel_ms": float(kms[dom]),
+                "per_kernel": {nm: {"ms": round(float(kms[i]), 4), "GBps": round(kbytes[i] / (kms[i] / 1e3) / 1e9, 1)}
+                               for i, nm in enumerate(names)},
+                "step_bytes": step_bytes,
+                "step_GBps_sum_of_kernels": round(step_bytes / (kms.sum() / 1e3) / 1e9, 1),
+                "step_GBps_timed": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1),
+                "stored_scalars": stored,
+                "reference_algorithm_bytes_per_step": 8.0 * (prof[12] + prof[15] + 6 * N)}
+
+    return roofline
 
 
 def run_b200(args, world, rank, local):
@@ -375,54 +425,7 @@ def run_b200(args, world, rank, local):
     else:
         sub_line = None
 
-    # ---- per-kernel roofline (CUDA events on the library stream)
-    prof = np.zeros(16)
-    uprof = torch.from_numpy(u0.copy()).cuda()
-    P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, uprof.data_ptr(), 5, mcode,
-                                   P._lib.host_ptr(prof)), ctx.h)
-    zform = int(F.propagator_stats()[6]) if args.method == "propagator" else 0
-    if args.method == "propagator" and prof[11] == 1.0:
-        # two-kernel H2 step (h2step.cu): x staging copy, K1 (column walk + the
-        # dense diagonal leaves), K2 (couplings, row walk, row bases Q_t, epilogue)
-        names = ["xpad", "h2s_up(K1)", "h2s_down(K2)"]
-        stored = {"A-": int(prof[12]), "Z=(A+)^-1": int(prof[13]), "LU factor": int(prof[15])}
-    elif args.method == "propagator":
-        # nested (H2) form: the walk is four short latency-bound launches (leaf / up / couple /
-        # down); the segment kernel is the dominant single kernel
-        names = ["walk(Z)" if zform == 2 else "vtx(Z)", "seg(Z)"]
-        stored = {"A-": int(prof[12]), "Z=(A+)^-1": int(prof[13]), "LU factor": int(prof[15])}
-    else:
-        names = ["vtx(A-)", "seg(A-)", "vtx(L^-1)", "seg(L^-1)", "vtx(U^-1)", "seg(U^-1)"]
-        stored = {"A-": int(prof[12]), "L^-1": int(prof[13]), "U^-1": int(prof[14]),
-                  "LU factor": int(prof[15])}
-    nk = len(names)
-    kms = prof[:nk]
-    kbytes = prof[6:6 + nk]
-    if prof[11] == 1.0:
-        dom = 1 + int(np.argmax(kms[1:]))
-    else:
-        dom = 1 if zform == 2 else int(np.argmax(kms))
-    peak, peak_src = measured_peaks()
-    achieved = kbytes[dom] / (kms[dom] / 1000.0) / 1e9
-    step_bytes = float(kbytes.sum())
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(names[dom])
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_source": peak_src, "algorithmic_bytes_per_launch": float(kbytes[dom]),
-                "kernel_ms": float(kms[dom]),
-                "per_kernel": {nm: {"ms": round(float(kms[i]), 4), "GBps": round(kbytes[i] / (kms[i] / 1e3) / 1e9, 1)}
-                               for i, nm in enumerate(names)},
-                "step_bytes": step_bytes,
-                "step_GBps_sum_of_kernels": round(step_bytes / (kms.sum() / 1e3) / 1e9, 1),
-                "step_GBps_timed": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1),
-                "stored_scalars": stored,
-                "reference_algorithm_bytes_per_step": 8.0 * (prof[12] + prof[15] + 6 * N)}
+    roofline = step_roofline(P, ctx, Hm, F, u0, args.method, ms_per_step, N)
 
     out = {"metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -653,6 +656,8 @@ def run_cfg5(args, world, rank, local):
                       "stored_scalars_plus": mem_p["stored_scalars"],
                       "spill_A-_s": round(t_spill, 3),
                       "device_mem_used_gb": round((total_b - free_b) / 1e9, 2), "device_mem_gb": mem}}
+    if method in ("propagator", "inverse"):
+        out["roofline"] = step_roofline(P, ctx, Hm, F, u0, method, ms / k, N, traffic_file=False)
     if method == "propagator":
         zs = F.propagator_stats()
         out["phases"]["propagator_form"] = int(zs[6])

@@ -120,7 +120,7 @@ int lh_hmat_derive_toeplitz(lh_ctx *ctx, const lh_hmat *src, const double *t_dev
 int lh_hmat_clone(lh_ctx *ctx, const lh_hmat *src, int32_t kcap, lh_hmat **out);
 void lh_hmat_destroy(lh_hmat *h);
 /* Memory management (no reference counterpart: levyh keeps every operator in host RAM).
- * lh_hmat_spill moves an unfactored H-matrix's arena to pinned host memory and frees its device
+ * lh_hmat_spill moves an unfactored H-matrix's arena to host memory and frees its device
  * copy and matvec plan; every call that reads the arena (matvec, entry, exports, derive, hlu,
  * trisolve, save, steps that read A-) brings it back first.  Used for A- of the CN pair when
  * the step is u <- 2 Z u - u and never reads A- (levy.FracCNSystem.prepare(spill_minus=True),

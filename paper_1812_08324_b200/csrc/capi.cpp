@@ -1,6 +1,9 @@
 // C-ABI of the B200 H-matrix engine (include/levyh_b200.h).
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
+
+#include <sys/mman.h>
 
 #include "core.h"
 #include "matvec.h"
@@ -113,7 +116,7 @@ HMat::~HMat() {
     if (d_ranks) cudaFree(d_ranks);
     if (d_perm) cudaFree(d_perm);
     if (d_inv) cudaFree(d_inv);
-    if (h_spill) cudaFreeHost(h_spill);
+    if (h_spill) std::free(h_spill);
 }
 void spill_arena(HMat &H, cudaStream_t s) {
     if (H.h_spill || !H.d_arena) return;
@@ -134,12 +137,17 @@ void spill_arena(HMat &H, cudaStream_t s) {
         LH_REQUIRE(avail_kb < 0 || need <= 0.5 * 1024.0 * (double)avail_kb, LH_ENOMEM,
                    "spill: not enough available host memory for the arena");
     }
-    double *hp = nullptr;
-    LH_CUDA(cudaMallocHost(&hp, sizeof(double) * (size_t)std::max<i64>(H.arena_len, 1)));
+    // pageable host memory on transparent huge pages (pinning tens of GB page by page costs
+    // more than the driver's staged copies)
+    const size_t bytes = sizeof(double) * (size_t)std::max<i64>(H.arena_len, 1);
+    const size_t HP = (size_t)2 << 20;
+    double *hp = static_cast<double *>(std::aligned_alloc(HP, (bytes + HP - 1) / HP * HP));
+    LH_REQUIRE(hp != nullptr, LH_ENOMEM, "spill: host allocation failed");
+    madvise(hp, (bytes + HP - 1) / HP * HP, MADV_HUGEPAGE);
     cudaError_t e = cudaMemcpyAsync(hp, H.d_arena, sizeof(double) * (size_t)H.arena_len, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
-        cudaFreeHost(hp);
+        std::free(hp);
         LH_CUDA(e);
     }
     H.mv_plan.reset();
@@ -157,7 +165,7 @@ void ensure_resident(HMat &H, cudaStream_t s) {
         cudaFree(d);
         LH_CUDA(e);
     }
-    cudaFreeHost(H.h_spill);
+    std::free(H.h_spill);
     H.h_spill = nullptr;
     H.d_arena = d;
     ++H.gen;

@@ -114,7 +114,7 @@ struct HMat {
     i64 perm_len = 0;
     double *d_inv = nullptr;          // FDENSE packed leaf inverses
     i64 inv_len = 0;
-    // host spill (lh_hmat_spill): the arena lives in pinned host memory and d_arena is null until
+    // host spill (lh_hmat_spill): the arena lives in host memory and d_arena is null until
     // ensure_resident() brings it back; gen counts the moves (caches holding arena pointers key on it)
     double *h_spill = nullptr;
     uint64_t gen = 0;

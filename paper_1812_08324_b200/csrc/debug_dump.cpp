@@ -168,7 +168,8 @@ extern "C" int lh_debug_plan_timing(const lh_tree *rt, const lh_tree *ct, int n_
         }
         F.arena_len = off;
         F.nslots = slots;
-        out[0] = out[1] = out[2] = out[3] = 0.0;
+        refine_dense_leaves(F);
+        for (int k = 0; k < 10; ++k) out[k] = 0.0;
         HMat G = F;  // structure copies for the two planners
         G.d_arena = nullptr;
         G.d_ranks = nullptr;
@@ -177,6 +178,8 @@ extern "C" int lh_debug_plan_timing(const lh_tree *rt, const lh_tree *ct, int n_
             auto P = plan_hlu(F, 1e-10, pl);
             out[0] = P->build_seconds;
             out[1] = (double)P->tasks.size();
+            out[4] = 8.0 * (double)P->temp_len;
+            out[7] = plan_device_bytes(*P);
         }
         if (which & 2) {
             i64 pl = 0, il = 0;
@@ -187,6 +190,10 @@ extern "C" int lh_debug_plan_timing(const lh_tree *rt, const lh_tree *ct, int n_
             auto Pz = plan_propagator(G, Z, 1e-10);
             out[2] = Pz->build_seconds;
             out[3] = (double)Pz->tasks.size();
+            out[5] = 8.0 * (double)Pz->temp_len;
+            out[6] = 8.0 * (double)Z.arena_len;
+            out[8] = plan_device_bytes(*Pz);
+            out[9] = 8.0 * (double)F.arena_len;
         }
         F.d_arena = nullptr;
         return LH_OK;

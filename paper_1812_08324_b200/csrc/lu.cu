@@ -1474,6 +1474,7 @@ struct PlanRun {
     ExecArgs A;
     bool prof = false;
     int err[4] = {0, 0, 0, 0};
+    double *xbuf = nullptr;  // scratch of a propagator column part (Plan::x_len >= 0)
 };
 
 static void run_plan_launch(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val,
@@ -1517,6 +1518,12 @@ static void run_plan_launch(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, in
     A.base[B_TMP] = P.d_temp;
     A.base[B_RHS] = rhs;
     A.base[B_X] = X ? X->d_arena : nullptr;
+    if (X && P.x_len >= 0) {
+        // a propagator column part: its views address [x_base, x_base + x_len) of the Z layout,
+        // held by the part's scratch buffer (X->d_arena is not allocated yet)
+        LH_REQUIRE(R.xbuf != nullptr, LH_EINTERNAL, "propagator part without a scratch buffer");
+        A.base[B_X] = R.xbuf - P.x_base;
+    }
     A.base[B_INV] = F.d_inv;
     A.ranks = P.d_ranks;
     A.perm = F.d_perm;
@@ -1565,8 +1572,9 @@ static void run_plan_finish(Ctx &ctx, Plan &P, PlanRun &R, const char *label) {
 }
 
 static void run_plan(Ctx &ctx, Plan &P, HMat &F, HMat *X, double *rhs, int rhs_slot_val,
-                     const char *label = "plan") {
+                     const char *label = "plan", double *xbuf = nullptr) {
     PlanRun R;
+    R.xbuf = xbuf;
     run_plan_launch(ctx, P, F, X, rhs, rhs_slot_val, R);
     run_plan_finish(ctx, P, R, label);
 }
@@ -1607,6 +1615,7 @@ struct PlanJob {
     std::shared_ptr<Plan> inv[2];
     HMat Z;
     std::shared_ptr<Plan> prop;
+    std::vector<std::shared_ptr<Plan>> prop_parts;  // column parts run one by one (large N)
     bool prop_uploaded = false;  // device copies made by the planning thread (own stream)
     int device = -1;             // device of the thread that assembled the matrix
     PlanStream lu_stream;  // the H-LU plan in chunks, when hlu() arrives before planning ends
@@ -1668,7 +1677,8 @@ void start_background_plans(HMat &H) {
     job->f_prop = std::async(std::launch::async, [j] {
         try {
             block_layout(j->Z, j->fshadow, 2, prop_kcap_for(j->fshadow));
-            j->prop = plan_propagator(j->fshadow, j->Z, 1e-10);
+            j->prop = plan_propagator(j->fshadow, j->Z, 1e-10, 8, &j->prop_parts);
+            if (!j->prop) return;  // parts: uploaded one at a time by prepare_propagator
             // upload on a stream of this thread once the H-LU planning (and with it the
             // streamed H-LU chunk uploads) is done: the copies overlap the H-LU's last chunks
             if (j->device >= 0 && !getenv("LEVYH_NO_BG_UPLOAD")) {
@@ -2074,6 +2084,116 @@ static double probe_rel_err(Ctx &ctx, const MvPlan &Pa, HMat &Ha, const MvPlan &
     return den > 0.0 ? std::sqrt(num / den) : std::sqrt(num);
 }
 
+// contiguous device copies dst[d + i] = src[s + i], i < len (jobs cut to <= 64K doubles so the
+// CTAs share the work evenly)
+struct CopyJob {
+    i64 src, dst, len;
+};
+__global__ void copy_jobs_kernel(const CopyJob *jobs, int n, const double *src, double *dst) {
+    for (int j = blockIdx.x; j < n; j += gridDim.x) {
+        const CopyJob J = jobs[j];
+        for (i64 i = threadIdx.x; i < J.len; i += blockDim.x) dst[J.dst + i] = src[J.src + i];
+    }
+}
+static void run_copy_jobs(Ctx &ctx, const std::vector<CopyJob> &in, const double *src, double *dst) {
+    std::vector<CopyJob> jobs;
+    const i64 CH = 65536;
+    for (const CopyJob &J : in)
+        for (i64 o = 0; o < J.len; o += CH) jobs.push_back({J.src + o, J.dst + o, std::min(CH, J.len - o)});
+    if (jobs.empty()) return;
+    CopyJob *d = dupload(jobs, ctx.stream);
+    copy_jobs_kernel<<<(int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 8), NT, 0, ctx.stream>>>(
+        d, (int)jobs.size(), src, dst);
+    LH_CUDA(cudaGetLastError());
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaFree(d);
+}
+
+// Tight re-layout of the blocks of H whose storage lies in [lo, hi) of `src` (offsets in H's
+// layout): dense leaves m x n, low-rank blocks at capacity max(rank, 1); the new storage starts at
+// `base` of the returned buffer's eventual home and the node offsets are rewritten to it.
+// Returns the packed buffer (len doubles, zero beyond the copied ranks).
+static double *compact_range(Ctx &ctx, HMat &H, const double *src, i64 src_base, i64 lo, i64 hi, i64 base,
+                             i64 &len, std::vector<std::pair<i64, i64>> *regions = nullptr) {
+    std::vector<CopyJob> jobs;
+    i64 off = 0;
+    for (int32_t b : H.leafblocks) {
+        Node &nd = H.nodes[b];
+        if (nd.vpar >= 0) continue;
+        if (nd.kind == K_DENSE || nd.kind == K_FDENSE) {
+            if (nd.doff < lo || nd.doff >= hi) continue;
+            if (regions) regions->push_back({nd.doff, base + off});
+            jobs.push_back({nd.doff - src_base, off, nd.m * nd.n});
+            nd.doff = base + off;
+            off += nd.m * nd.n;
+        } else if (nd.kind == K_LR) {
+            if (nd.uoff < lo || nd.uoff >= hi) continue;
+            const int r = H.h_ranks[nd.rslot], kc = std::max(r, 1);
+            if (regions) {
+                regions->push_back({nd.uoff, base + off});
+                regions->push_back({nd.voff, base + off + nd.m * kc});
+            }
+            jobs.push_back({nd.uoff - src_base, off, nd.m * r});
+            nd.uoff = base + off;
+            off += nd.m * kc;
+            jobs.push_back({nd.voff - src_base, off, nd.n * r});
+            nd.voff = base + off;
+            off += nd.n * kc;
+            nd.kcap = kc;
+        }
+    }
+    len = off;
+    double *d = dalloc<double>(std::max<i64>(off, 1));
+    LH_CUDA(cudaMemsetAsync(d, 0, sizeof(double) * (size_t)std::max<i64>(off, 1), ctx.stream));
+    run_copy_jobs(ctx, jobs, src, d);
+    return d;
+}
+
+// The H-LU factor's arena at capacity max(rank, 1) (it is only read from here on): every
+// block moves, so the views of the plans still to run on it are re-pointed, and the plans that
+// were cut against the old layout (substitution, triangular solves) are dropped (rebuilt lazily).
+static void compact_factor(Ctx &ctx, HMat &F, std::vector<std::shared_ptr<Plan>> &plans) {
+    F.sync_ranks(ctx.stream);
+    std::vector<std::pair<i64, i64>> starts;  // (old start, new start) of every region
+    const i64 old_len = F.arena_len;
+    i64 len = 0;
+    double *na = compact_range(ctx, F, F.d_arena, 0, 0, old_len, 0, len, &starts);
+    std::sort(starts.begin(), starts.end());
+    auto remap = [&](DView &v) {
+        if (v.base != B_F) return;
+        auto it = std::upper_bound(starts.begin(), starts.end(), std::make_pair(v.off, (i64)INT64_MAX));
+        LH_REQUIRE(it != starts.begin(), LH_EINTERNAL, "factor view outside every block");
+        --it;
+        v.off = v.off - it->first + it->second;
+    };
+    for (auto &P : plans) {
+        for (DTask &t : P->tasks)
+            for (DView &v : t.v) remap(v);
+        for (DPiece &pc : P->pieces) {
+            remap(pc.mat);
+            remap(pc.x);
+        }
+    }
+    cudaFree(F.d_arena);
+    F.d_arena = na;
+    F.arena_len = len;
+    F.mv_plan.reset();
+    F.inv_plan.reset();
+    SolvePlans &S = plans_of(F);
+    S.sub.reset();
+    for (auto &m : S.tri)
+        for (auto &q : m) q.reset();
+    if (F.bg_plan) {
+        PlanJob *job = static_cast<PlanJob *>(F.bg_plan.get());
+        if (job->f_inv.valid()) job->f_inv.wait();
+        job->inv[0].reset();  // cut against the old layout
+        job->inv[1].reset();
+    }
+    ++F.gen;
+    if (getenv("LEVYH_PLAN_VERBOSE"))
+        fprintf(stderr, "[levyh] factor compacted: %.2f GB -> %.2f GB\n", 8e-9 * (double)old_len, 8e-9 * (double)len);
+}
+
 void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.factored, LH_EINVAL, "prepare_propagator needs an H-LU factorization");
     SolvePlans &S = plans_of(F);
@@ -2081,43 +2201,112 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
     PlanJob *job = F.bg_plan ? static_cast<PlanJob *>(F.bg_plan.get()) : nullptr;
     auto Z = std::make_shared<HMat>();
     std::shared_ptr<Plan> P;
+    std::vector<std::shared_ptr<Plan>> parts;
     bool uploaded = false;
     if (job && job->f_prop.valid()) {
         job->f_prop.wait();
-        if (job->prop_error.empty() && job->prop) {
+        if (job->prop_error.empty() && (job->prop || !job->prop_parts.empty())) {
             copy_structure(*Z, job->Z);
             Z->nslots = job->Z.nslots;
             Z->arena_len = job->Z.arena_len;
             P = std::move(job->prop);
-            uploaded = job->prop_uploaded;
+            parts = std::move(job->prop_parts);
+            uploaded = job->prop_uploaded && P;
             if (eps2 != 1e-10) {
-                patch_eps(*P, eps2);
+                if (P) patch_eps(*P, eps2);
+                for (auto &q : parts) patch_eps(*q, eps2);
                 if (uploaded)  // refresh the device task array
                     LH_CUDA(cudaMemcpyAsync(P->d_tasks, P->tasks.data(), sizeof(DTask) * P->tasks.size(),
                                             cudaMemcpyHostToDevice, ctx.stream));
             }
         }
     }
-    if (!P) {
+    if (!P && parts.empty()) {
         block_layout(*Z, F, 2, prop_kcap_for(F));
-        P = plan_propagator(F, *Z, eps2);
+        P = plan_propagator(F, *Z, eps2, 8, &parts);
     }
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    const bool verbose = getenv("LEVYH_PLAN_VERBOSE") != nullptr;
+    auto memlog = [&](const char *what) {
+        if (!verbose) return;
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        fprintf(stderr, "[levyh] propagator memory %s: %.2f GB used of %.2f\n", what, (tot - fr) * 1e-9, tot * 1e-9);
+    };
     auto ta = now();
-    Z->d_arena = dalloc<double>(std::max<i64>(Z->arena_len, 1));
+    memlog("before Z");
+    if (verbose)
+        fprintf(stderr, "[levyh] propagator: Z arena %.2f GB, plan %.2f GB on the device (%zu part(s))\n",
+                8e-9 * (double)Z->arena_len, 1e-9 * (P ? plan_device_bytes(*P) : plan_device_bytes(*parts[0])),
+                P ? (size_t)1 : parts.size());
+    if (P) Z->d_arena = dalloc<double>(std::max<i64>(Z->arena_len, 1));
     Z->d_ranks = dalloc<int32_t>(std::max(Z->nslots, 1));
     LH_CUDA(cudaMemsetAsync(Z->d_ranks, 0, sizeof(int32_t) * std::max(Z->nslots, 1), ctx.stream));
-    if (!uploaded) P->upload(ctx.stream);
+    double ntask = 0.0, build_s = 0.0, temp_b = 0.0;
     auto t0 = now();
-    run_plan(ctx, *P, F, Z.get(), nullptr, -1, "propagator");
+    if (P) {
+        if (!uploaded) P->upload(ctx.stream);
+        t0 = now();
+        run_plan(ctx, *P, F, Z.get(), nullptr, -1, "propagator");
+        ntask = (double)P->tasks.size();
+        build_s = P->build_seconds;
+        temp_b = (double)P->temp_len * 8.0;
+        P.reset();
+    } else {
+        // large N: the independent column parts Z[:, J] = (LU)^-1 I[:, J] one after another.
+        // The factor is compacted first; each part's DAG is uploaded, runs into a scratch buffer
+        // of the part's extent, and the part is then packed at capacity max(rank, 1) and its DAG
+        // freed; the packed parts form Z's arena at the end.
+        compact_factor(ctx, F, parts);
+        memlog("factor compacted");
+        i64 xmax = 0;
+        for (auto &q : parts) xmax = std::max(xmax, q->x_len);
+        double *scratch = dalloc<double>(std::max<i64>(xmax, 1));
+        std::vector<std::pair<double *, i64>> packed;
+        i64 zlen = 0;
+        t0 = now();
+        try {
+            for (auto &q : parts) {
+                q->upload(ctx.stream);
+                memlog("part uploaded");
+                run_plan(ctx, *q, F, Z.get(), nullptr, -1, "propagator", scratch);
+                ntask += (double)q->tasks.size();
+                build_s = std::max(build_s, q->build_seconds);
+                temp_b = std::max(temp_b, (double)q->temp_len * 8.0);
+                Z->sync_ranks(ctx.stream);
+                i64 len = 0;
+                double *buf = compact_range(ctx, *Z, scratch, q->x_base, q->x_base, q->x_base + q->x_len, zlen, len);
+                packed.push_back({buf, len});
+                zlen += len;
+                q.reset();
+            }
+        } catch (...) {
+            cudaFree(scratch);
+            for (auto &pb : packed) cudaFree(pb.first);
+            throw;
+        }
+        parts.clear();
+        cudaFree(scratch);
+        memlog("parts packed");
+        Z->d_arena = dalloc<double>(std::max<i64>(zlen, 1));
+        i64 o = 0;
+        for (auto &pb : packed) {
+            LH_CUDA(cudaMemcpyAsync(Z->d_arena + o, pb.first, sizeof(double) * pb.second, cudaMemcpyDeviceToDevice,
+                                    ctx.stream));
+            LH_CUDA(cudaStreamSynchronize(ctx.stream));
+            cudaFree(pb.first);
+            o += pb.second;
+        }
+        Z->arena_len = zlen;
+    }
     Z->sync_ranks(ctx.stream);
     auto t1 = now();
-    Z->lu_stats[0] = (double)P->tasks.size();
-    Z->lu_stats[1] = P->build_seconds;
-    Z->lu_stats[2] = (double)P->temp_len * 8.0;
+    memlog("Z computed");
+    Z->lu_stats[0] = ntask;
+    Z->lu_stats[1] = build_s;
+    Z->lu_stats[2] = temp_b;
     Z->lu_stats[3] = sec(t0, t1);
-    P.reset();
     auto t2 = now();
     // near-field compression of Z: its off-diagonal dense leaves are
     // numerically low-rank, which cuts the bytes every CN step streams
@@ -2133,7 +2322,9 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
         Z->lu_stats[5] = (double)coarsen_hmat(ctx, *Z, c_eps);
     }
     auto t3 = now();
+    memlog("near-field compressed + coarsened");
     S.mvZ = build_mv_plan(*Z, Z->leafblocks, ctx.stream);
+    memlog("matvec plan of Z");
     // nested (H2) bases for the single-RHS step (zshared.cu), checked against the H-form of Z
     // on a probe vector; else shared leaf bases
     if (!getenv("LEVYH_NO_H2")) {
@@ -2152,6 +2343,7 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
             }
         }
     }
+    memlog("H2 form built");
     if (!S.mvZS && !getenv("LEVYH_NO_SHARED_BASIS")) {
         double sb_eps = 1e-2 * std::min(eps2, 1e-10);
         if (const char *e = getenv("LEVYH_SB_EPS")) sb_eps = atof(e);

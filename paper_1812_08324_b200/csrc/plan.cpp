@@ -262,7 +262,11 @@ PView Planner::temp(i64 rows, i64 cols, int32_t wslot) {
     auto &fl = freelist[cls];
     i64 off;
     std::vector<int32_t> prev;
-    const size_t MIN_AGE = 512;
+    // reuse distance: a freed block is reused once this many blocks of its class were freed
+    // after it (keeps independent work from serialising on WAR edges); large classes keep about
+    // LEVYH_TEMP_WINDOW doubles (default 2^26 = 512 MB) in flight instead of 512 blocks
+    static const i64 window = getenv("LEVYH_TEMP_WINDOW") ? atoll(getenv("LEVYH_TEMP_WINDOW")) : ((i64)1 << 26);
+    const size_t MIN_AGE = (size_t)std::max<i64>(4, std::min<i64>(512, window >> cls));
     if (fl.size() > MIN_AGE) {
         off = fl.front().off;
         prev = std::move(fl.front().users);
@@ -1007,6 +1011,11 @@ void assign_priorities(Plan &P) {
 
 void Planner::finalize() {
     P->nslots_total = next_slot;
+    if (getenv("LEVYH_TEMP_HIST")) {  // planner diagnostics: pooled temp blocks per size class
+        for (auto &kv : freelist)
+            fprintf(stderr, "[levyh] temp class 2^%d: %zu blocks pooled, %.3f GB\n", kv.first, kv.second.size(),
+                    8e-9 * (double)kv.second.size() * (double)((i64)1 << kv.first));
+    }
     bool engaged = false;
     if (stream) {
         std::lock_guard<std::mutex> lk(stream->mu);
@@ -1277,7 +1286,13 @@ static std::vector<std::pair<i64, i64>> column_blocks(const Tree &T, int depth) 
     return out;
 }
 
-std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_parts) {
+double plan_device_bytes(const Plan &P) {
+    return (double)P.tasks.size() * (sizeof(DTask) + 24) + (double)P.deps.size() * 8 +
+           (double)P.pieces.size() * sizeof(DPiece) + (double)P.temp_len * 8;
+}
+
+std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_parts,
+                                      std::vector<std::shared_ptr<Plan>> *keep_parts) {
     auto t0 = std::chrono::steady_clock::now();
     std::shared_ptr<Plan> P;
     if (const char *e = getenv("LEVYH_PROP_PARTS")) max_parts = atoi(e);
@@ -1298,6 +1313,35 @@ std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_par
         for (int q = 0; q < 4; ++q) st.push_back({nd.kid[q], d + 1});
     }
     auto cols = depth > 0 ? column_blocks(*Z.ct, depth) : std::vector<std::pair<i64, i64>>{};
+    // large operators: the column parts run one after another, each into a scratch buffer of its
+    // own extent (prepare_propagator compacts each part as it finishes), so Z is laid out with
+    // every part's blocks contiguous
+    const double parts_gb = getenv("LEVYH_PROP_PARTS_GB") ? atof(getenv("LEVYH_PROP_PARTS_GB")) : 40.0;
+    const bool parts_mode = keep_parts && cols.size() >= 2 && 8e-9 * (double)Z.arena_len > parts_gb;
+    std::vector<i64> part_off;
+    if (parts_mode) {
+        part_off.assign(cols.size() + 1, 0);
+        i64 off = 0;
+        for (size_t k = 0; k < cols.size(); ++k) {
+            part_off[k] = off;
+            for (int32_t b : Z.leafblocks) {
+                Node &nd = Z.nodes[b];
+                if (nd.c0 < cols[k].first || nd.c0 >= cols[k].second) continue;
+                LH_REQUIRE(nd.c0 + nd.n <= cols[k].second, LH_EINTERNAL, "propagator part split crosses a leaf");
+                if (nd.kind == K_DENSE) {
+                    nd.doff = off;
+                    off += nd.m * nd.n;
+                } else if (nd.kind == K_LR) {
+                    nd.uoff = off;
+                    off += nd.m * nd.kcap;
+                    nd.voff = off;
+                    off += nd.n * nd.kcap;
+                }
+            }
+        }
+        part_off[cols.size()] = off;
+        LH_REQUIRE(off == Z.arena_len, LH_EINTERNAL, "propagator part layout lost blocks");
+    }
     if (cols.size() >= 2) {
         std::vector<HMat> Zs(cols.size());
         std::vector<std::future<std::shared_ptr<Plan>>> fut;
@@ -1321,6 +1365,24 @@ std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_par
             } catch (const std::exception &) {
                 ok = false;  // defensive: the split check above should make this unreachable
             }
+        }
+        if (ok && parts_mode) {
+            size_t nt = 0;
+            double dev_bytes = 0.0;
+            for (size_t k = 0; k < parts_v.size(); ++k) {
+                auto &q = parts_v[k];
+                nt += q->tasks.size();
+                dev_bytes = std::max(dev_bytes, plan_device_bytes(*q));
+                q->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                q->x_base = part_off[k];
+                q->x_len = part_off[k + 1] - part_off[k];
+            }
+            if (getenv("LEVYH_PLAN_VERBOSE"))
+                fprintf(stderr, "[levyh] propagator plan: %zu tasks in %zu column parts run one by one (largest "
+                                "part %.1f GB on the device, Z arena %.1f GB), %.3f s\n",
+                        nt, parts_v.size(), dev_bytes * 1e-9, 8e-9 * (double)Z.arena_len, parts_v[0]->build_seconds);
+            *keep_parts = std::move(parts_v);
+            return nullptr;
         }
         if (ok) {
             auto tm = std::chrono::steady_clock::now();

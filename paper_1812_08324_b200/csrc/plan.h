@@ -112,6 +112,9 @@ struct Plan {
     int32_t slot_off_x = 0, slot_off_tmp = 0;
     int32_t rhs_slot = -1;       // slot holding the run-time RHS width (solve plans)
     bool own_temp = true;        // false: d_temp is lent by the caller (streamed chunks)
+    // propagator column part run on its own: its B_X views address [x_base, x_base + x_len) of
+    // the Z layout, which lives in a scratch buffer of x_len doubles while the part runs
+    i64 x_base = 0, x_len = -1;
     // device copies
     DTask *d_tasks = nullptr;
     int32_t *d_deps = nullptr;

@@ -156,7 +156,13 @@ std::shared_ptr<Plan> plan_inverse(HMat &F, HMat &X, int mode, double eps2);
 std::shared_ptr<Plan> plan_trisolve_dense(HMat &T, i64 n, int nrhs_cap, int mode, bool unit,
                                           const std::string &root);
 std::shared_ptr<Plan> plan_trisolve_block(HMat &T, HMat &X, int mode, bool unit, double eps2);
-std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_parts = 8);
+// keep_parts: when the merged DAG's device footprint (plan_device_bytes) would exceed
+// LEVYH_PROP_MERGE_GB (default 8 GB), the independent column parts are returned there instead
+// of merged (and the result is null): they then run one after another, each uploaded, executed
+// and freed (N = 2^22, where the merged DAG does not fit next to the factor and Z)
+std::shared_ptr<Plan> plan_propagator(HMat &F, HMat &Z, double eps2, int max_parts = 8,
+                                      std::vector<std::shared_ptr<Plan>> *keep_parts = nullptr);
+double plan_device_bytes(const Plan &P);
 std::shared_ptr<Plan> merge_plans(const std::vector<std::shared_ptr<Plan>> &parts);
 void mark_lu_leaves(HMat &F, i64 &perm_len, i64 &inv_len);
 int64_t critical_path(const Plan &P);

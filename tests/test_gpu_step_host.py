@@ -59,3 +59,25 @@ def test_step_host_in_place_and_errors(P):
         P.step_cn(s, np.ones(s.N + 1))
     with pytest.raises(ValueError):
         P.step_cn(s, torch.ones(s.N, dtype=torch.float64).cuda())
+
+
+def test_spilled_minus_steps_and_restores(P):
+    """prepare(spill_minus=True): A- of the CN pair lives in pinned host memory while the
+    propagator step u <- 2 Z u - u runs (it never reads A-); the fixture's CN solution is
+    unchanged, and the first call that reads A- (matvec) brings it back bit-identically."""
+    g = cases.load("cfg2_s075")
+    s = cases.make_system("cfg2_s075", g)
+    s.prepare(P.HConfig(n_min=int(g["leaf"]), eps1=float(g["eps1"])), float(g["eps2"]), spill_minus=True)
+    assert not s.h_minus.resident
+    n_steps = int(g["n_steps"])
+    u = P.run_cn(s, g["u0"], n_steps)
+    assert not s.h_minus.resident, "the CN-pair propagator step read the spilled A-"
+    assert np.linalg.norm(u - g["uT"]) <= 1e-8 * np.linalg.norm(g["uT"])
+    x = np.random.default_rng(3).standard_normal(s.N)
+    y = P.matvec(s.h_minus, x)
+    assert s.h_minus.resident
+    t = cases.make_system("cfg2_s075", g)
+    Hp, Hm = t.build_pair(P.HConfig(n_min=int(g["leaf"]), eps1=float(g["eps1"])))
+    assert np.array_equal(y, P.matvec(Hm, x))
+    with pytest.raises(ValueError):
+        s.factor.h.spill()  # factored: refused
