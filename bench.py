@@ -290,7 +290,7 @@ def step_roofline(P, ctx, Hm, F, u0, method, ms_per_step, N, traffic_file=True):
     if method == "propagator" and prof[11] == 1.0:
         # two-kernel H2 step (h2step.cu): x staging copy, K1 (column walk + the
         # dense diagonal leaves), K2 (couplings, row walk, row bases Q_t, epilogue)
-        names = ["xpad", "h2s_up(K1)", "h2s_down(K2)"]
+        names = ["xpad", "h2s_up(K1)", "h2s_down(K2)"]  # xpad: once per call (0 per step)
         stored = {"A-": int(prof[12]), "Z=(A+)^-1": int(prof[13]), "LU factor": int(prof[15])}
     elif method == "propagator":
         # nested (H2) form: the walk is four short latency-bound launches (leaf / up / couple /
@@ -323,7 +323,7 @@ def step_roofline(P, ctx, Hm, F, u0, method, ms_per_step, N, traffic_file=True):
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": float(kbytes[dom]),
                 "kernel_ms": float(kms[dom]),
                 "per_kernel": {nm: {"ms": round(float(kms[i]), 4), "GBps": round(kbytes[i] / (kms[i] / 1e3) / 1e9, 1)}
-                               for i, nm in enumerate(names)},
+                               for i, nm in enumerate(names) if kms[i] > 0},
                 "step_bytes": step_bytes,
                 "step_GBps_sum_of_kernels": round(step_bytes / (kms.sum() / 1e3) / 1e9, 1),
                 "step_GBps_timed": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1),

@@ -238,9 +238,10 @@ int lh_cn_step_host(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, const d
  * vtx(L^-1), seg(L^-1), vtx(U^-1), seg(U^-1); out[6..11] their algorithmic bytes;
  * out[12..14] stored scalars of H-, L^-1, U^-1.  method 2: out[0..1], out[6..7] for
  * phase 1 of Z (V^T x, or the H2 walk when lh_propagator_stats reports form 2) and the
- * segment kernel (others 0); when Z runs the two-kernel H2 step, out[11] = 1 and out[0..2] /
- * out[6..8] are the x staging copy, K1 (column walk + dense diagonal leaves) and K2 (couplings,
- * row walk, row bases).  out[12] H-, out[13] Z in the form the step streams.  out[15]
+ * segment kernel (others 0); when Z runs the two-kernel H2 step, out[11] = 1 and out[1..2] /
+ * out[7..8] are K1 (column walk + dense diagonal leaves) and K2 (couplings, row walk, row bases,
+ * the new u written into the staging copy); out[0] = out[6] = 0 (the staging copy of u is made
+ * once per lh_cn_steps call).  out[12] H-, out[13] Z in the form the step streams.  out[15]
  * stored scalars of the factor. */
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev,
                     int32_t iters, int32_t method, double *out_host);

@@ -97,11 +97,26 @@ __device__ __forceinline__ void preload(unsigned char *dst, const DSlice (&sl)[N
     mb_wait(bar, 0);
 }
 
-__device__ __forceinline__ double wsum(double v) {
+// v[j] (j < 2W) partial sums held by every lane -> lane l ends with the warp total of column
+// l & (2W - 1) (W = 16: all 32 lanes distinct; W = 8: lanes l and l + 16 hold the same column).
+// Halving exchanges: at width w a lane keeps the half of its live slots selected by lane bit w and
+// adds the partner's copy of that half (2W - 1 shuffles), then W = 8 folds the two half-warps.
+template <int W>
+__device__ __forceinline__ double transpose_reduce(double (&v)[32], int lane) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
+    for (int w = W; w >= 1; w >>= 1) {
+        const bool up = (lane & w) != 0;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const double send = up ? v[i] : v[i + w];
+            const double keep = up ? v[i + w] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+        }
+    }
+    if (W == 8) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
+    return v[0];
 }
+
 
 struct K1Args {
     const H2SChunk *ch;
@@ -256,20 +271,26 @@ __global__ void __launch_bounds__(CONS_T + 64, 1) h2s_up_kernel(K1Args A) {
         } else if (C.type == C_LEAF) {
             for (int l = C.a + cw; l < C.b; l += H2S_CONS) {
                 const H2SLeaf &L = lfs[l - l0];
-                // lane j < k: x_hat_j = sum_i P[i + 64 j] x[i], rows visited skewed by j (row
-                // (i + j) mod 64 at step i) so the lanes' shared-memory reads hit distinct banks;
-                // P's rows beyond `rows` are zero (ld 64), x beyond `rows` is masked
+                // x_hat = P^T x with the rows across the lanes (rows lane, lane + 32; P's rows
+                // beyond `rows` are zero, ld 64; x beyond `rows` masked): per column a lane
+                // partial, then one transpose reduction leaves column j's sum in lane j
+                const double *P = slot + L.p + lane, *xv = slot + L.xsl;
+                const double x0 = lane < L.rows ? xv[lane] : 0.0;
+                const double x1 = lane + 32 < L.rows ? xv[lane + 32] : 0.0;
+                double v[32];
+                double r;
+                if (L.k <= 16) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = j < L.k ? fma(P[64 * j], x0, P[64 * j + 32] * x1) : 0.0;
+                    r = transpose_reduce<8>(v, lane);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = j < L.k ? fma(P[64 * j], x0, P[64 * j + 32] * x1) : 0.0;
+                    r = transpose_reduce<16>(v, lane);
+                }
                 if (lane < L.k) {
-                    const double *P = slot + L.p + 64 * lane, *xv = slot + L.xsl;
-                    double s0 = 0.0, s1 = 0.0;
-#pragma unroll 8
-                    for (int i = 0; i < 64; i += 2) {
-                        const int r0 = (i + lane) & 63, r1 = (i + 1 + lane) & 63;
-                        s0 = fma(P[r0], r0 < L.rows ? xv[r0] : 0.0, s0);
-                        s1 = fma(P[r1], r1 < L.rows ? xv[r1] : 0.0, s1);
-                    }
-                    xs[L.xs + lane] = s0 + s1;
-                    A.xh[L.xh + lane] = s0 + s1;
+                    xs[L.xs + lane] = r;
+                    A.xh[L.xh + lane] = r;
                 }
             }
         } else {  // C_ULVL
@@ -382,24 +403,38 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
             for (int it = C.a + cw; it < C.b; it += H2S_CONS) {
                 const H2SCplN &N = cns[it - n0];
                 double acc = 0.0;
-                for (int e = N.c0; e < N.c1; ++e) {
-                    const H2SCplE &E = ces[e - e0];
-                    const double xv = lane < E.kc ? __ldcg(A.xh + E.xh + lane) : 0.0;
-                    const double *S = slot + E.s + lane;
-                    double s0 = 0.0, s1 = 0.0;
-                    int j = 0;
-                    for (; j + 1 < E.kc; j += 2) {
-                        const double v0 = __shfl_sync(FULL, xv, j), v1 = __shfl_sync(FULL, xv, j + 1);
-                        if (lane < N.kr) {
-                            s0 = fma(S[j * N.kr], v0, s0);
-                            s1 = fma(S[(j + 1) * N.kr], v1, s1);
+                // the x_hat of four couplings requested together (one L2 latency per four)
+                for (int e4 = N.c0; e4 < N.c1; e4 += 4) {
+                    double xq[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        xq[u] = 0.0;
+                        if (e4 + u < N.c1) {
+                            const H2SCplE &E = ces[e4 + u - e0];
+                            if (lane < E.kc) xq[u] = __ldcg(A.xh + E.xh + lane);
                         }
                     }
-                    if (j < E.kc) {
-                        const double v0 = __shfl_sync(FULL, xv, j);
-                        if (lane < N.kr) s0 = fma(S[j * N.kr], v0, s0);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (e4 + u >= N.c1) break;
+                        const H2SCplE &E = ces[e4 + u - e0];
+                        const double xv = xq[u];
+                        const double *S = slot + E.s + lane;
+                        double s0 = 0.0, s1 = 0.0;
+                        int j = 0;
+                        for (; j + 1 < E.kc; j += 2) {
+                            const double v0 = __shfl_sync(FULL, xv, j), v1 = __shfl_sync(FULL, xv, j + 1);
+                            if (lane < N.kr) {
+                                s0 = fma(S[j * N.kr], v0, s0);
+                                s1 = fma(S[(j + 1) * N.kr], v1, s1);
+                            }
+                        }
+                        if (j < E.kc) {
+                            const double v0 = __shfl_sync(FULL, xv, j);
+                            if (lane < N.kr) s0 = fma(S[j * N.kr], v0, s0);
+                        }
+                        acc += s0 + s1;
                     }
-                    acc += s0 + s1;
                 }
                 if (lane < N.kr) ws[N.ws + lane] = acc;
             }
@@ -1178,6 +1213,23 @@ void h2s_launch_timed(const H2 &h, const double *x, double *y, double alpha, dou
     LH_CUDA(cudaEventRecord(ev[0], s));
     xpad_kernel<<<(int)std::min<i64>((S.n + 2 + NT - 1) / NT, 148 * 8), NT, 0, s>>>(x, S.n, S.xpad);
     h2s_kernels(h, y, alpha, beta, z, beta == 0.0 ? 0 : (z == x ? 1 : 2), s, ev + 1);
+}
+
+void h2s_load(const H2 &h, const double *x, cudaStream_t s) {
+    const H2S &S = *h.step2;
+    xpad_kernel<<<(int)std::min<i64>((S.n + 2 + NT - 1) / NT, 148 * 8), NT, 0, s>>>(x, S.n, S.xpad);
+    LH_CUDA(cudaGetLastError());
+}
+
+void h2s_step_inplace(const H2 &h, double alpha, double beta, cudaStream_t s, cudaEvent_t *ev) {
+    // K2 stages every z row it reads (its own rows, once) before it writes y there, and K1 of
+    // the next step reads x only after K2 has finished: the staging copy holds the state
+    h2s_kernels(h, h.step2->xpad, alpha, beta, nullptr, beta == 0.0 ? 0 : 1, s, ev);
+}
+
+void h2s_store(const H2 &h, double *y, cudaStream_t s) {
+    const H2S &S = *h.step2;
+    LH_CUDA(cudaMemcpyAsync(y, S.xpad, sizeof(double) * S.n, cudaMemcpyDeviceToDevice, s));
 }
 
 void h2s_launch_host(const H2 &h, const double *x_host, double *y_dev, double *y_host, double alpha, double beta,

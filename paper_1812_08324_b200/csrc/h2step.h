@@ -129,6 +129,12 @@ void h2s_launch(const H2 &h, const double *x, double *y, double alpha, double be
 // the same with events around the three launches (ev[0] xpad ev[1] K1 ev[2] K2 ev[3]); profiling
 void h2s_launch_timed(const H2 &h, const double *x, double *y, double alpha, double beta, const double *z,
                       cudaStream_t s, cudaEvent_t *ev);
+// CN stepping in place on the staging copy: h2s_load copies x in once, every h2s_step_inplace is
+// x <- alpha Z x + beta x with the two kernels only (K2 writes the new x into the staging copy),
+// h2s_store copies the state out.  ev (optional): events before K1, between, after K2.
+void h2s_load(const H2 &h, const double *x, cudaStream_t s);
+void h2s_step_inplace(const H2 &h, double alpha, double beta, cudaStream_t s, cudaEvent_t *ev = nullptr);
+void h2s_store(const H2 &h, double *y, cudaStream_t s);
 // the same with x arriving from (pinned) host memory straight into the aligned staging copy and
 // y leaving to host memory; z = x (beta != 0).  Capturable.
 void h2s_launch_host(const H2 &h, const double *x_host, double *y_dev, double *y_host, double alpha, double beta,

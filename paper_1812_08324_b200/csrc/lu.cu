@@ -2661,29 +2661,34 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
         // two-kernel H2 step (h2step.cu): xpad / K1 / K2 timed separately; bytes are the ring
         // operands each kernel streams plus its vector writes (yd by K1, y by K2) and the
         // staging copy of x (read + write)
+        // as cn_steps runs it: u copied into the staging buffer once, then K1 + K2 in place
         cudaEvent_t ev[4];
         for (auto &e : ev) LH_CUDA(cudaEventCreate(&e));
         double acc3[3] = {0, 0, 0};
+        LH_CUDA(cudaEventRecord(ev[3], ctx.stream));
+        h2s_load(*Pz.h2, u, ctx.stream);
+        LH_CUDA(cudaEventRecord(ev[0], ctx.stream));
+        LH_CUDA(cudaEventSynchronize(ev[0]));
+
         for (int it = 0; it < iters; ++it) {
-            h2s_launch_timed(*Pz.h2, u, y, 2.0, -1.0, u, ctx.stream, ev);
-            LH_CUDA(cudaEventRecord(ev[3], ctx.stream));
-            LH_CUDA(cudaMemcpyAsync(u, y, sizeof(double) * Hm.nrows, cudaMemcpyDeviceToDevice, ctx.stream));
-            LH_CUDA(cudaEventSynchronize(ev[3]));
-            for (int k = 0; k < 3; ++k) {
+            h2s_step_inplace(*Pz.h2, 2.0, -1.0, ctx.stream, ev);
+            LH_CUDA(cudaEventSynchronize(ev[2]));
+            for (int k = 0; k < 2; ++k) {
                 float ms = 0.f;
                 LH_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
-                acc3[k] += ms;
+                acc3[k + 1] += ms;
             }
         }
+        h2s_store(*Pz.h2, u, ctx.stream);
         LH_CUDA(cudaStreamSynchronize(ctx.stream));
         for (auto &e : ev) cudaEventDestroy(e);
         for (int k = 0; k < 16; ++k) out[k] = 0.0;
         const H2S &S2 = *Pz.h2->step2;
         for (int k = 0; k < 3; ++k) out[k] = acc3[k] / std::max(iters, 1);
-        out[6] = 16.0 * Hm.nrows;
+        out[6] = 0.0;  // the staging copy runs once per cn_steps call, not per step
         out[7] = (double)S2.bytes1 + 8.0 * Hm.nrows;
         out[8] = (double)S2.bytes2 + 8.0 * Hm.nrows;
-        out[11] = 1.0;  // layout flag: xpad, K1, K2
+        out[11] = 1.0;  // layout flag: (staging copy: 0 per step), K1, K2
     } else {
     const int nk = 2 * (int)mv.size();
     cudaEvent_t ev[7];
@@ -2746,6 +2751,20 @@ void step_profile(Ctx &ctx, HMat &Hm, HMat &F, double *u, int iters, int method,
     out[15] = stored(F, F.leafblocks);
 }
 
+static int count_kernel_nodes(cudaGraph_t g) {
+    size_t nn = 0;
+    LH_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    LH_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+    int k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        LH_CUDA(cudaGraphNodeGetType(nd, &ty));
+        k += ty == cudaGraphNodeTypeKernel;
+    }
+    return k;
+}
+
 void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nsteps, int method) {
     LH_REQUIRE(F.factored, LH_EINVAL, "cn_steps needs an H-LU factorization of A+");
     LH_REQUIRE(Hm.nrows == F.nrows, LH_EINVAL, "operator sizes differ");
@@ -2790,8 +2809,42 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
             LH_CUDA(cudaStreamSynchronize(ctx.stream));
             return;
         }
+        const MvPlan &Pz1 = S.z1plan();
+        const bool inplace = shape == 2 && Pz1.h2 && Pz1.h2->step2 && !getenv("LEVYH_NO_INPLACE_STEP");
         for (int q = 0; q < nrhs; ++q) {
             double *uq = u + (i64)q * ldu;
+            if (inplace) {
+                // two-kernel H2 step on the staging copy: u in once, K1 + K2 per step (captured
+                // once), u out once
+                const int key = 4;  // graph shape tag of the in-place step
+                if (!(S.graph && S.g_hm == Hm.id && S.g_gen == Hm.gen && S.g_method == key)) {
+                    if (S.graph) {
+                        cudaGraphExecDestroy(S.graph);
+                        S.graph = nullptr;
+                    }
+                    cudaGraph_t g;
+                    LH_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+                    try {
+                        h2s_step_inplace(*Pz1.h2, 2.0, -1.0, ctx.stream);
+                    } catch (...) {
+                        cudaStreamEndCapture(ctx.stream, &g);
+                        throw;
+                    }
+                    LH_CUDA(cudaStreamEndCapture(ctx.stream, &g));
+                    S.g_kernels = count_kernel_nodes(g);
+                    LH_CUDA(cudaGraphInstantiate(&S.graph, g, 0));
+                    cudaGraphDestroy(g);
+                    S.g_u = nullptr;
+                    S.g_hm = Hm.id;
+                    S.g_gen = Hm.gen;
+                    S.g_y = nullptr;
+                    S.g_method = key;
+                }
+                h2s_load(*Pz1.h2, uq, ctx.stream);
+                for (int k = 0; k < nsteps; ++k) LH_CUDA(cudaGraphLaunch(S.graph, ctx.stream));
+                h2s_store(*Pz1.h2, uq, ctx.stream);
+                continue;
+            }
             if (!(S.graph && S.g_u == uq && S.g_hm == Hm.id && S.g_gen == Hm.gen && S.g_y == y &&
                   S.g_method == shape)) {
                 if (S.graph) {
@@ -2818,16 +2871,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
                     throw;
                 }
                 LH_CUDA(cudaStreamEndCapture(ctx.stream, &g));
-                size_t nn = 0;
-                LH_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
-                std::vector<cudaGraphNode_t> nodes(nn);
-                LH_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
-                S.g_kernels = 0;
-                for (auto nd : nodes) {
-                    cudaGraphNodeType ty;
-                    LH_CUDA(cudaGraphNodeGetType(nd, &ty));
-                    S.g_kernels += ty == cudaGraphNodeTypeKernel;
-                }
+                S.g_kernels = count_kernel_nodes(g);
                 LH_CUDA(cudaGraphInstantiate(&S.graph, g, 0));
                 cudaGraphDestroy(g);
                 S.g_u = uq;

@@ -261,3 +261,21 @@ def test_propagator_column_parts_path(P, name, monkeypatch):
     s.h_minus, s.factor, s.method = Hm, F, "propagator"
     u = P.run_cn(s, g["u0"], int(g["n_steps"]))
     assert _rel(u, g["uT"]) <= 1e-8
+
+
+def test_levyh_style_run_cn_takes_the_two_kernel_step(P):
+    """prepare() -> run_cn(sys, u0, n) with defaults (levy.py:241-330 call pattern) steps with the
+    propagator in nested-basis form: the captured step graph is the two persistent kernels
+    (h2step.cu K1 + K2, the state kept in the staging copy between steps), and the result is
+    the reference's."""
+    g = cases.load("cfg3_cgmy_n8191")
+    s = cases.make_system("cfg3_cgmy_n8191", g)
+    s.prepare(P.HConfig(n_min=int(g["leaf"]), eps1=float(g["eps1"])), float(g["eps2"]))
+    u = P.run_cn(s, g["u0"], int(g["n_steps"]))
+    assert _rel(u, g["uT"]) <= 1e-8
+    st = s.factor.propagator_stats()
+    assert st[6] == 2.0, "nested-basis (H2) form not installed"
+    path = np.zeros(4, dtype=np.int32)
+    P._lib.check(P._lib.lib().lh_cn_last_path(s.factor.h.handle, P._lib.host_ptr(path)))
+    assert list(path[:3]) == [2, 0, 0]  # u <- 2 Z u - u, single RHS, device-resident
+    assert int(P._lib.lib().lh_step_graph_kernels(s.factor.h.handle)) == 2
