@@ -51,6 +51,20 @@ __device__ __forceinline__ void bulk(void *dst, uint64_t src, uint32_t bytes, ui
                  "l"(src), "r"(bytes), "r"(saddr(bar))
                  : "memory");
 }
+// streamed operands are read once per application: evict-first in L2, so the small vectors the
+// kernels exchange through L2 (x_hat, yd, the staging copy of x) stay resident
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_ef(void *dst, uint64_t src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            saddr(dst)),
+        "l"(src), "r"(bytes), "r"(saddr(bar)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, %0;" ::"n"(CONS_T) : "memory"); }
 
 // producer: lane 0 of warp 0 streams the chunks [c0, c1) through the ring
@@ -61,6 +75,7 @@ __device__ __forceinline__ void produce(const H2SChunk *ch, int nch, unsigned ch
                                         uint64_t *empty, int skip = 0) {
     int stage = 0;
     uint32_t phase = 0;
+    const uint64_t pol = evict_first_policy();
     for (int c = 0; c < nch; ++c) {
         const H2SChunk &C = ch[c];
         if (skipped(C, skip)) continue;
@@ -69,7 +84,7 @@ __device__ __forceinline__ void produce(const H2SChunk *ch, int nch, unsigned ch
         for (int i = 0; i < C.ncopy; ++i) tot += (uint32_t)C.bytes[i];
         mb_expect(&full[stage], tot);
         unsigned char *slot = ring + (size_t)stage * H2S_SLOTB;
-        for (int i = 0; i < C.ncopy; ++i) bulk(slot + C.dst[i], C.src[i], (uint32_t)C.bytes[i], &full[stage]);
+        for (int i = 0; i < C.ncopy; ++i) bulk_ef(slot + C.dst[i], C.src[i], (uint32_t)C.bytes[i], &full[stage], pol);
         if (++stage == H2S_ST) {
             stage = 0;
             phase ^= 1;
@@ -340,6 +355,7 @@ struct K2Args {
     double alpha, beta;
     int zmode;  // 0: beta = 0, 1: z = x (staged xpad slice), 2: z from global
     unsigned long long *trace;  // timing experiments only
+    int skip;  // timing experiments only: bit 0 skips the coupling products, bit 1 the levels, bit 2 the rows
 };
 
 // K2: producer warp 0, consumer warps 1 .. 8
@@ -382,6 +398,15 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
         return;
     }
     const int cw = warp - 1, ct = threadIdx.x - 32;
+    // the x_hat the couplings read were written by K1 early and have since been pushed out of
+    // L2 by K1's dense stream: bring them back for the whole CTA at once (one DRAM latency
+    // instead of one per chunk of coupling products)
+    for (int e = ct; e < ne; e += CONS_T) {
+        const H2SCplE &E = ces[e];
+        const double *p = A.xh + E.xh;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + E.kc - 1));
+    }
     int stage = 0, pcur = 0;
     uint32_t phase = 0;
     unsigned long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -399,44 +424,43 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
         mb_wait(&full[stage], phase);
         if (A.trace) tw[7] += gtime() - ta;
         const double *slot = reinterpret_cast<const double *>(ring + (size_t)stage * H2S_SLOTB);
-        if (C.type == C_CPL) {
-            for (int it = C.a + cw; it < C.b; it += H2S_CONS) {
-                const H2SCplN &N = cns[it - n0];
-                double acc = 0.0;
-                // the x_hat of four couplings requested together (one L2 latency per four)
-                for (int e4 = N.c0; e4 < N.c1; e4 += 4) {
-                    double xq[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        xq[u] = 0.0;
-                        if (e4 + u < N.c1) {
-                            const H2SCplE &E = ces[e4 + u - e0];
-                            if (lane < E.kc) xq[u] = __ldcg(A.xh + E.xh + lane);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (e4 + u >= N.c1) break;
-                        const H2SCplE &E = ces[e4 + u - e0];
-                        const double xv = xq[u];
-                        const double *S = slot + E.s + lane;
-                        double s0 = 0.0, s1 = 0.0;
-                        int j = 0;
-                        for (; j + 1 < E.kc; j += 2) {
-                            const double v0 = __shfl_sync(FULL, xv, j), v1 = __shfl_sync(FULL, xv, j + 1);
-                            if (lane < N.kr) {
-                                s0 = fma(S[j * N.kr], v0, s0);
-                                s1 = fma(S[(j + 1) * N.kr], v1, s1);
-                            }
-                        }
-                        if (j < E.kc) {
-                            const double v0 = __shfl_sync(FULL, xv, j);
-                            if (lane < N.kr) s0 = fma(S[j * N.kr], v0, s0);
-                        }
-                        acc += s0 + s1;
-                    }
+        if (C.type == C_CPL && (A.skip & 1)) {
+        } else if (C.type == C_DLVL && (A.skip & 2)) {
+        } else if (C.type == C_Q && (A.skip & 4)) {
+        } else if (C.type == C_CPL) {
+            // the chunk's coupling products as one batch: its x_hat slices are gathered into the
+            // slot tail (slot[C.e1 ..], one L2 round trip for the chunk: warp per coupling, lane
+            // per entry), then consumer thread t computes chunk row t (node row i of w = sum_e
+            // S_e x_hat_e); C.e2 rows in all
+            double *xg = const_cast<double *>(slot) + C.e1;
+            const int nn_c = C.b - C.a;
+            const int cb = nn_c > 0 ? cns[C.a - n0].c0 : 0, ce = nn_c > 0 ? cns[C.b - 1 - n0].c1 : 0;
+            for (int q = cb + cw; q < ce; q += H2S_CONS) {
+                const H2SCplE &E = ces[q - e0];
+                if (lane < E.kc) xg[E.xo + lane] = __ldcg(A.xh + E.xh + lane);
+            }
+            cons_bar();
+            for (int t = ct; t < C.e2; t += CONS_T) {
+                int lo = 0, hi = nn_c - 1;  // the node holding chunk row t: last with ro <= t
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if ((cns[C.a + mid - n0].kr_ro >> 8) <= t) lo = mid;
+                    else hi = mid - 1;
                 }
-                if (lane < N.kr) ws[N.ws + lane] = acc;
+                const H2SCplN &N = cns[C.a + lo - n0];
+                const int kr = N.kr_ro & 255, i = t - (N.kr_ro >> 8);
+                double a0 = 0.0, a1 = 0.0;
+                for (int e = N.c0; e < N.c1; ++e) {
+                    const H2SCplE &E = ces[e - e0];
+                    const double *S = slot + E.s + i, *xv = xg + E.xo;
+                    int j = 0;
+                    for (; j + 1 < E.kc; j += 2) {
+                        a0 = fma(S[j * kr], xv[j], a0);
+                        a1 = fma(S[(j + 1) * kr], xv[j + 1], a1);
+                    }
+                    if (j < E.kc) a0 = fma(S[j * kr], xv[j], a0);
+                }
+                ws[N.ws + i] = a0 + a1;
             }
         } else if (C.type == C_PATH) {
             if (cw == 0) {  // the chain above the subtree, one warp
@@ -838,6 +862,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     for (int s = 0; s < nsd; ++s) k2subs[(int)((i64)s * G / std::max(nsd, 1))].push_back(s);
     std::vector<char> leaf_done(in.rleaf.size(), 0);
     std::vector<i64> k2bytes(G, 0);
+    i64 k2type[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // ring bytes by chunk type (diagnostics)
     std::vector<std::vector<H2SChunk>> k2c(G);
     // the rows of row leaves [la, lb): one copy each of their Q bases (contiguous in the ZS
     // arena), yd rows and x rows
@@ -888,6 +913,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
             k.c.b = (int)qv.size();
             out.push_back(k.c);
             k2bytes[b] += k.used;
+            k2type[C_Q] += k.used;
             l = e;
         }
         return true;
@@ -897,6 +923,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
         auto push = [&](Cut &k) {
             out.push_back(k.c);
             k2bytes[b] += k.used;
+            k2type[std::min<int>(k.c.type, 7)] += k.used;
         };
         for (int s : k2subs[b]) {
             const SubOps &O = ops[s];
@@ -908,37 +935,54 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
             wsmax = std::max(wsmax, wsn);
             ysmax = std::max(ysmax, ycnt);
             const int32_t *lv = in.dn_lv->data() + (size_t)s * (in.maxh_dn + 2);
-            // couplings
+            // couplings: a chunk carries its nodes' coupling matrices; its slot tail (from e1)
+            // receives the gathered x_hat slices (xcnt doubles), e2 = rows of w it computes
             Cut k;
+            i64 xcnt = 0, rows = 0;
+            auto cpl_done = [&](Cut &kk) {
+                kk.c.e1 = (int32_t)((kk.used + 15) / 16 * 2);
+                kk.c.e2 = (int32_t)rows;
+                xcnt = rows = 0;
+            };
             start(k, C_CPL, (int)cnv.size());
             k.c.flags = F_BEGIN;
             k.c.e0 = wsn;
             for (size_t t = 0; t < O.cpl_nodes.size(); ++t) {
                 const H2Down &D = (*in.dns)[O.cpl_nodes[t].first];
-                i64 sbytes = 0;
-                for (int e = D.c0; e < D.c1; ++e) sbytes += 8 * (i64)(*in.cpls)[e].kr * (*in.cpls)[e].kc;
-                if (sbytes + 32 > SLOT) return false;
+                i64 sbytes = 0, kcs = 0;
+                for (int e = D.c0; e < D.c1; ++e) {
+                    sbytes += 8 * (i64)(*in.cpls)[e].kr * (*in.cpls)[e].kc;
+                    kcs += (*in.cpls)[e].kc;
+                }
+                if (sbytes + 8 * kcs + 64 > SLOT || D.k > 255) return false;
                 const double *src = sb2 + O.sbeg[t];
-                if (k.c.a < k.c.b && !fits(k, sbytes, merges(k, (uint64_t)(uintptr_t)src) ? 0 : 1)) {
+                const bool mg = merges(k, (uint64_t)(uintptr_t)src);
+                if (k.c.a < k.c.b &&
+                    (!fits(k, sbytes, mg ? 0 : 1) || k.used + sbytes + 32 + 8 * (xcnt + kcs) + 16 > SLOT)) {
+                    cpl_done(k);
                     push(k);
                     start(k, C_CPL, (int)cnv.size());
                 }
                 const int base = add_copy(k, src, sbytes);
-                H2SCplN N{(int32_t)O.cpl_nodes[t].second, D.k, (int)cev.size(), 0};
+                H2SCplN N{(int32_t)O.cpl_nodes[t].second, D.k | (int32_t)(rows << 8), (int)cev.size(), 0};
                 i64 off = 0;
                 for (int e = D.c0; e < D.c1; ++e) {
                     const H2Cpl &E = (*in.cpls)[e];
                     H2SCplE q{};
                     q.s = base + (int)off;
                     q.kc = E.kc;
-                    q.xh = E.xoff;
+                    q.xo = (int32_t)xcnt;
+                    q.xh = (int32_t)E.xoff;
                     cev.push_back(q);
                     off += (i64)E.kr * E.kc;
+                    xcnt += E.kc;
                 }
+                rows += D.k;
                 N.c1 = (int)cev.size();
                 cnv.push_back(N);
                 k.c.b = (int)cnv.size();
             }
+            cpl_done(k);
             push(k);  // possibly without items: it clears the w slots (F_BEGIN)
             // path chain, ending in the subtree root
             start(k, C_PATH, (int)pv.size());
@@ -1122,6 +1166,11 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     S->q = dupload(qv, st);
     LH_CUDA(cudaStreamSynchronize(st));
     if (getenv("LEVYH_PLAN_VERBOSE"))
+        fprintf(stderr, "[levyh] H2 step K2 ring bytes: couplings %.1f MB, path %.1f MB, levels %.1f MB, rows %.1f MB; "
+                        "%zu coupling nodes, %zu couplings, %zu path steps, %zu level nodes, %zu row leaves\n",
+                k2type[C_CPL] * 1e-6, k2type[C_PATH] * 1e-6, k2type[C_DLVL] * 1e-6, k2type[C_Q] * 1e-6, cnv.size(),
+                cev.size(), pv.size(), dnv.size(), qv.size());
+    if (getenv("LEVYH_PLAN_VERBOSE"))
         fprintf(stderr, "[levyh] H2 step kernels: K1 %zu chunks (%.1f MB walk + %.1f MB dense), K2 %zu chunks "
                         "(%.1f MB), smem %d / %d B (descriptors %d / %d B)\n", ch1.size(), wtot * 1e-6, dtot * 1e-6,
                 ch2.size(), S->bytes2 * 1e-6, S->smem1, S->smem2, S->desc1, S->desc2);
@@ -1158,7 +1207,8 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     if (ev) LH_CUDA(cudaEventRecord(ev[1], s));
     if (a1.trace) cudaEventRecord(te[1], s);
     K2Args a2{S.c2, S.cb2, S.nb2, S.eb2, S.pb2, S.db2, S.qb2, S.cn, S.ce, S.path, S.dn, S.q, h.xh,
-              S.wsmax, S.ysmax, z, y, alpha, beta, zmode, a1.trace ? a1.trace + (size_t)S.G * 8 : nullptr};
+              S.wsmax, S.ysmax, z, y, alpha, beta, zmode, a1.trace ? a1.trace + (size_t)S.G * 8 : nullptr,
+              (dbg >> 5) & 15};
     if (!(dbg & 2)) h2s_down_kernel<<<S.G, CONS_T + 32, S.smem2, s>>>(a2);
     if (ev) LH_CUDA(cudaEventRecord(ev[2], s));
     LH_CUDA(cudaGetLastError());

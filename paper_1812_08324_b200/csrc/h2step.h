@@ -49,12 +49,11 @@ struct H2SUp {  // x_hat = T^T [xs[xs1 ..+k1]; xs[xs2 ..+k2]], T row i at slot[t
     int32_t t, k, k1, k2, xs, xs1, xs2, pad;
     i64 xh, pad2;
 };
-struct H2SCplN {  // w[ws ..+kr] = sum_e S_e x_hat_e over couplings [c0, c1)
-    int32_t ws, kr, c0, c1;
+struct H2SCplN {  // w[ws ..+kr] = sum_e S_e x_hat_e over couplings [c0, c1); rows ro .. ro+kr of the chunk
+    int32_t ws, kr_ro, c0, c1;  // kr_ro = kr | ro << 8
 };
-struct H2SCplE {  // S (kr x kc, column-major) at slot[s]; x_hat at xh[xh ..+kc]
-    int32_t s, kc;
-    i64 xh;
+struct H2SCplE {  // S (kr x kc, column-major) at slot[s]; x_hat at xh[xh ..+kc], gathered to slot[x0 + xo]
+    int32_t s, kc, xo, xh;
 };
 struct H2SPath {  // chain step: y = w[ws] (+ T[t + roff + i + j ldt] y_prev[j], j < kp); out >= 0: ys slot
     int32_t ws, k, kp, ldt, roff, t, out, pad;
