@@ -366,7 +366,8 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
     double *ws = reinterpret_cast<double *>(ring + (size_t)H2S_ST * H2S_SLOTB);
     double *ys = ws + A.wsmax;
     double *py = ys + A.ysmax;  // [2][32] path chain state
-    unsigned char *desc = reinterpret_cast<unsigned char *>(py + 64);
+    double *xgb = py + 64;      // [2][H2S_XG] gathered x_hat of the coupling chunks (double-buffered)
+    unsigned char *desc = reinterpret_cast<unsigned char *>(xgb + 2 * H2S_XG);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, b = blockIdx.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < H2S_ST; ++i) {
@@ -407,7 +408,8 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p + E.kc - 1));
     }
-    int stage = 0, pcur = 0;
+    int stage = 0, pcur = 0, xpar = 0;
+    bool pre = false;  // this coupling chunk's x_hat were gathered during the previous chunk
     uint32_t phase = 0;
     unsigned long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const unsigned long long tstart = A.trace ? gtime() : 0;
@@ -424,6 +426,20 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
         mb_wait(&full[stage], phase);
         if (A.trace) tw[7] += gtime() - ta;
         const double *slot = reinterpret_cast<const double *>(ring + (size_t)stage * H2S_SLOTB);
+        // lookahead between consecutive coupling chunks: the next chunk's x_hat are requested
+        // now and stored after this chunk's products, so their L2 round trip overlaps them
+        const bool ahead = C.type == C_CPL && c + 1 < nch && chs[c + 1].type == C_CPL && chs[c + 1].b > chs[c + 1].a;
+        double xr[8];
+        int ncb = 0, nce = 0;
+        if (ahead) {
+            ncb = cns[chs[c + 1].a - n0].c0;
+            nce = cns[chs[c + 1].b - 1 - n0].c1;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int q = ncb + cw + H2S_CONS * i;
+                xr[i] = (q < nce && lane < ces[q - e0].kc) ? __ldcg(A.xh + ces[q - e0].xh + lane) : 0.0;
+            }
+        }
         if (C.type == C_CPL && (A.skip & 1)) {
         } else if (C.type == C_DLVL && (A.skip & 2)) {
         } else if (C.type == C_Q && (A.skip & 4)) {
@@ -432,13 +448,14 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
             // slot tail (slot[C.e1 ..], one L2 round trip for the chunk: warp per coupling, lane
             // per entry), then consumer thread t computes chunk row t (node row i of w = sum_e
             // S_e x_hat_e); C.e2 rows in all
-            double *xg = const_cast<double *>(slot) + C.e1;
+            double *xg = xgb + xpar * H2S_XG;
             const int nn_c = C.b - C.a;
             const int cb = nn_c > 0 ? cns[C.a - n0].c0 : 0, ce = nn_c > 0 ? cns[C.b - 1 - n0].c1 : 0;
-            for (int q = cb + cw; q < ce; q += H2S_CONS) {
-                const H2SCplE &E = ces[q - e0];
-                if (lane < E.kc) xg[E.xo + lane] = __ldcg(A.xh + E.xh + lane);
-            }
+            if (!pre)
+                for (int q = cb + cw; q < ce; q += H2S_CONS) {
+                    const H2SCplE &E = ces[q - e0];
+                    if (lane < E.kc) xg[E.xo + lane] = __ldcg(A.xh + E.xh + lane);
+                }
             cons_bar();
             for (int t = ct; t < C.e2; t += CONS_T) {
                 int lo = 0, hi = nn_c - 1;  // the node holding chunk row t: last with ro <= t
@@ -462,6 +479,7 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
                 }
                 ws[N.ws + i] = a0 + a1;
             }
+            if (nn_c > 0) xpar ^= 1;
         } else if (C.type == C_PATH) {
             if (cw == 0) {  // the chain above the subtree, one warp
                 for (int it = C.a; it < C.b; ++it) {
@@ -521,6 +539,17 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
                 }
             }
         }
+        if (ahead) {  // (every warp passed this chunk's barrier: the other buffer is free)
+            double *xn = xgb + xpar * H2S_XG;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int q = ncb + cw + H2S_CONS * i;
+                if (q < nce && lane < ces[q - e0].kc) xn[ces[q - e0].xo + lane] = xr[i];
+            }
+            for (int q = ncb + cw + 8 * H2S_CONS; q < nce; q += H2S_CONS)
+                if (lane < ces[q - e0].kc) xn[ces[q - e0].xo + lane] = __ldcg(A.xh + ces[q - e0].xh + lane);
+        }
+        pre = ahead;
         __syncwarp();
         if (lane == 0) mb_arrive(&empty[stage]);
         if (A.trace) tw[C.type] += gtime() - ta;
@@ -935,12 +964,11 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
             wsmax = std::max(wsmax, wsn);
             ysmax = std::max(ysmax, ycnt);
             const int32_t *lv = in.dn_lv->data() + (size_t)s * (in.maxh_dn + 2);
-            // couplings: a chunk carries its nodes' coupling matrices; its slot tail (from e1)
-            // receives the gathered x_hat slices (xcnt doubles), e2 = rows of w it computes
+            // couplings: a chunk carries its nodes' coupling matrices; its x_hat slices (<= H2S_XG
+            // doubles) are gathered into a shared-memory buffer, e2 = rows of w it computes
             Cut k;
             i64 xcnt = 0, rows = 0;
             auto cpl_done = [&](Cut &kk) {
-                kk.c.e1 = (int32_t)((kk.used + 15) / 16 * 2);
                 kk.c.e2 = (int32_t)rows;
                 xcnt = rows = 0;
             };
@@ -954,11 +982,11 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                     sbytes += 8 * (i64)(*in.cpls)[e].kr * (*in.cpls)[e].kc;
                     kcs += (*in.cpls)[e].kc;
                 }
-                if (sbytes + 8 * kcs + 64 > SLOT || D.k > 255) return false;
+                if (sbytes + 32 > SLOT || D.k > 255) return false;
                 const double *src = sb2 + O.sbeg[t];
                 const bool mg = merges(k, (uint64_t)(uintptr_t)src);
-                if (k.c.a < k.c.b &&
-                    (!fits(k, sbytes, mg ? 0 : 1) || k.used + sbytes + 32 + 8 * (xcnt + kcs) + 16 > SLOT)) {
+                if (kcs > H2S_XG) return false;
+                if (k.c.a < k.c.b && (!fits(k, sbytes, mg ? 0 : 1) || xcnt + kcs > H2S_XG)) {
                     cpl_done(k);
                     push(k);
                     start(k, C_CPL, (int)cnv.size());
@@ -1139,7 +1167,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     S->wsmax = (int)even(wsmax);
     S->ysmax = (int)even(ysmax);
     S->smem1 = RING_HDR + H2S_ST * H2S_SLOTB + 8 * S->xsmax + 8 * 2 * TGRP * 64 + S->desc1;
-    S->smem2 = RING_HDR + H2S_ST * H2S_SLOTB + 8 * (S->wsmax + S->ysmax + 64) + S->desc2;
+    S->smem2 = RING_HDR + H2S_ST * H2S_SLOTB + 8 * (S->wsmax + S->ysmax + 64 + 2 * H2S_XG) + S->desc2;
     int maxsm = 0, dev_id = 0;
     cudaGetDevice(&dev_id);
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id);

@@ -28,6 +28,7 @@ constexpr int H2S_ST = 4;                    // ring stages
 constexpr int H2S_SLOTB = 40960 + 1024;      // bytes per ring slot (a 64 x 64 leaf + x slice)
 constexpr int H2S_CONS = 8;                  // consumer warps
 constexpr int H2S_MAXP = 24;                 // path length (as H2_MAXP)
+constexpr int H2S_XG = 512;                  // gathered x_hat entries per coupling chunk
 
 enum : int32_t { C_LEAF = 0, C_ULVL = 1, C_DENSE = 2, C_CPL = 3, C_PATH = 4, C_DLVL = 5, C_Q = 6 };
 enum : int32_t { F_NEWLVL = 1, F_END = 2, F_SEGFIRST = 4, F_SEGLAST = 8, F_BEGIN = 16 };
