@@ -527,12 +527,12 @@ def run_cfg4(args, world, rank, local):
         u_host.copy_(u_dev, non_blocking=True)
         torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t1, world, "cuda")
-    # DMMA roofline: 2 K S_Z flops per step (phase 1 V^T X + phase 2 segment GEMMs)
-    prof = np.zeros(16)
-    P._lib.check(L.lh_step_profile(ctx.h, Hm.handle, F.h.handle, torch.zeros(N, dtype=torch.float64,
-                 device="cuda").data_ptr(), 1, 2, P._lib.host_ptr(prof)), ctx.h)
-    S_Z = float(prof[13])
-    flops = 2.0 * K * S_Z
+    # DMMA roofline: the algorithmic flops of the multi-RHS form of Z per step: the nested-basis
+    # walk (leaves, transfers, couplings) plus the segment matmat of dense leaves and row bases
+    # (h2mm.cu), or 2 x stored scalars for the H-form matmat
+    zst = F.propagator_stats()
+    flops = float(zst[10]) * K
+    S_Z = float(zst[10]) / 2.0
     try:
         pk = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_dmma_peak.json")))
         peak, peak_src = float(pk["tflops"]), "measured (profiles/r01_fp64_dmma_peak.json, tools/ubench_dmma.cu)"
@@ -545,7 +545,8 @@ def run_cfg4(args, world, rank, local):
            "data": "synthetic (BASELINE.json configs[3]; seeded bumps, no dataset)",
            "config": {"workload": cfg["workload"], "N": N, "rhs": K, "rhs_per_rank": Kr,
                       "parallelism": f"columns sharded {K}/{world}",
-                      "solve": SOLVE_DESC["propagator"] + "; K right-hand sides as one DMMA matmat per step",
+                      "solve": SOLVE_DESC["propagator"] + "; K right-hand sides per step through the H2 walk as "
+                               "batched DMMA products (h2mm.cu)",
                       "l2": "operator and state larger than L2"},
            "rhs_steps_per_s": round(K * 1000.0 / ms_per_step, 1),
            "clocks": sampler.summary(),
@@ -555,7 +556,9 @@ def run_cfg4(args, world, rank, local):
            "gpu_launches": None,
            "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
                         "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-                        "flops_per_step": flops, "stored_scalars_Z": S_Z},
+                        "flops_per_step": flops, "scalars_Z_multi_rhs_form": S_Z,
+                        "multi_rhs_form": "nested-basis walk as batched DMMA products" if zst[11] == 2 else
+                                          "H-form DMMA matmat"},
            "phases": {"setup_total_s": round(t_setup, 3)}}
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -208,7 +208,9 @@ int lh_prepare_propagator(lh_ctx *ctx, lh_hmat *factor, double eps2);
  * low-rank sibling groups of Z merged by coarsening, the single-RHS form of Z (0 H-matrix,
  * 1 shared leaf bases, 2 nested H2 bases), the relative error of that form against the
  * H-matrix on a seeded probe vector, the mean leaf basis size, and the scalars of bases,
- * transfers and couplings outside the dense leaves and row bases */
+ * transfers and couplings outside the dense leaves and row bases; out[10] flops per right-hand
+ * side of the multi-RHS product with Z and out[11] its form (2: the nested-basis walk as batched
+ * DMMA products, 1: the DMMA matmat of the H-form) */
 int lh_propagator_stats(lh_hmat *factor, double *out_host);
 /* Kernel launches per CN step: kernel nodes of the step graph lh_cn_steps last captured
  * (methods 1 and 2), 0 before the first call. */

@@ -2382,6 +2382,11 @@ void cn_last_path(HMat &F, int32_t *out) {
     out[3] = S.g_kernels;
 }
 
+// Y = alpha Z X + beta W for row-major multi-RHS blocks: the nested-basis walk as batched DMMA
+// products (h2mm.cu) when Z has its H2 form, else the DMMA matmat of Z's H-form
+static bool z_h2mm(const SolvePlans &S) {
+    return S.mvZS && S.mvZS->h2 && S.mvZS->h2->mm && !getenv("LEVYH_NO_H2MM");
+}
 void propagator_stats(HMat &F, double *out) {
     SolvePlans &S = plans_of(F);
     LH_REQUIRE(S.Z != nullptr, LH_EINVAL, "call prepare_propagator first");
@@ -2390,6 +2395,31 @@ void propagator_stats(HMat &F, double *out) {
     out[7] = S.zs_probe;
     out[8] = S.zs_stats[0];
     out[9] = S.zs_stats[1];
+    // multi-RHS form of Z and its flops per right-hand side: the H2 walk (h2mm.cu) plus the
+    // segment matmat of the dense leaves and row bases, or the H-form matmat (2 x stored scalars)
+    auto stored2 = [](HMat &H) {
+        H.sync_ranks(nullptr);
+        double sc = 0.0;
+        for (int32_t b : H.leafblocks) {
+            const Node &nd = H.nodes[b];
+            if (nd.kind == K_LR) sc += (double)H.h_ranks[nd.rslot] * (nd.m + nd.n);
+            else if (nd.kind != K_ZERO && nd.kind != K_HIER) sc += (double)nd.m * nd.n;
+        }
+        return 2.0 * sc;
+    };
+    if (z_h2mm(S)) {
+        out[10] = S.mvZS->h2->mm->flops_per_rhs + stored2(*S.ZS);
+        out[11] = 2.0;
+    } else {
+        out[10] = stored2(*S.Z);
+        out[11] = 1.0;
+    }
+}
+
+static void z_matmat(Ctx &ctx, SolvePlans &S, const double *X, double *Y, i64 ldk, double alpha, double beta,
+                     const double *W, const MmBufs &bz) {
+    if (z_h2mm(S)) h2mm_run(*S.mvZS->h2->mm, *S.mvZS, X, Y, ldk, alpha, beta, W, ctx.stream);
+    else mm_run(*S.mvZ, X, Y, ldk, alpha, beta, W, bz.T, bz.part, ctx.stream);
 }
 
 static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
@@ -2400,7 +2430,7 @@ static void solve_propagator(Ctx &ctx, HMat &F, double *b, i64 ldb, int nrhs) {
         double *Xr = ctx.mm[0].ensure(n * ldk), *Yr = ctx.mm[1].ensure(n * ldk);
         MmBufs bb = mm_bufs(ctx, *S.mvZ, ldk);
         mm_transpose(b, ldb, Xr, ldk, n, nrhs, true, ctx.stream);
-        mm_run(*S.mvZ, Xr, Yr, ldk, 1.0, 0.0, nullptr, bb.T, bb.part, ctx.stream);
+        z_matmat(ctx, S, Xr, Yr, ldk, 1.0, 0.0, nullptr, bb);
         mm_transpose(Yr, ldk, b, ldb, n, nrhs, false, ctx.stream);
         LH_CUDA(cudaStreamSynchronize(ctx.stream));
         return;
@@ -2782,7 +2812,7 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
         // is captured once as a CUDA graph, cached per (operator, vector, scratch, method).
         const int shape = method == 2 ? (cn_pair_ok(Hm, F) ? 2 : 3) : 1;
         S.last_path[0] = shape;
-        S.last_path[1] = method == 2 && nrhs >= mm_min_rhs();
+        S.last_path[1] = method == 2 && nrhs >= mm_min_rhs() ? (z_h2mm(S) ? 2 : 1) : 0;
         S.last_path[2] = 0;
         if (method == 2 && nrhs >= mm_min_rhs()) {
             // K right-hand sides: U row-major on the device for the whole run, each step one
@@ -2797,11 +2827,11 @@ void cn_steps(Ctx &ctx, HMat &Hm, HMat &F, double *u, i64 ldu, int nrhs, int nst
             mm_transpose(u, ldu, Xr, ldk, n, nrhs, true, ctx.stream);
             for (int k = 0; k < nsteps; ++k) {
                 if (shape == 2) {
-                    mm_run(*S.mvZ, Xr, Yr, ldk, 2.0, -1.0, Xr, bz.T, bz.part, ctx.stream);
+                    z_matmat(ctx, S, Xr, Yr, ldk, 2.0, -1.0, Xr, bz);
                 } else {
                     mm_run(*Pmp, Xr, Yr, ldk, 1.0, 0.0, nullptr, bm.T, bm.part, ctx.stream);
                     std::swap(Xr, Yr);
-                    mm_run(*S.mvZ, Xr, Yr, ldk, 1.0, 0.0, nullptr, bz.T, bz.part, ctx.stream);
+                    z_matmat(ctx, S, Xr, Yr, ldk, 1.0, 0.0, nullptr, bz);
                 }
                 std::swap(Xr, Yr);
             }

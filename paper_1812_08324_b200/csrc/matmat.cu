@@ -222,4 +222,11 @@ void mm_run(const MvPlan &P, const double *X, double *Y, i64 ldk, double alpha, 
     LH_CUDA(cudaGetLastError());
 }
 
+void seg_mm_launch(const MvPlan &P, const double *X, const double *T, i64 ldk, double *Y, double alpha,
+                   double beta, const double *Z, cudaStream_t s) {
+    const unsigned nk = (unsigned)(ldk / MM_N);
+    seg_mm_kernel<<<dim3(P.nseg, nk), NT, 0, s>>>(P.segs, P.colmap, P.pbuf, X, T, ldk, Y, alpha, beta, Z ? Z : Y);
+    LH_CUDA(cudaGetLastError());
+}
+
 }  // namespace lh

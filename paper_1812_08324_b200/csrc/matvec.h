@@ -122,9 +122,47 @@ struct H2QLeaf {  // fused step: y[r0 + i] = alpha (yd[r0 + i] + sum_c Q[qoff + 
     int32_t yloc, pad;  // y_hat_t at ys[yloc] of the subtree CTA (k > 0)
 };
 struct H2S;  // h2step.h: the two-kernel step
+// multi-RHS H2 application (h2mm.cu): batched DMMA products, one launch per tree level
+struct H2MMJob {  // C[crow .. +m] (=|+=) A (m x kk) B; A(i, j) = abase[aoff + i sa + j sb];
+    i64 aoff;     // B rows: [b[r], b[r] + n[r]) concatenated, r < 4
+    int32_t m, kk, sa, sb, crow, pad;
+    int32_t b[4], n[4];
+};
+enum : int32_t { H2MM_X = 0, H2MM_XH = 1, H2MM_YH = 2 };               // B source / C target
+enum : int32_t { H2MM_PB = 0, H2MM_TU = 1, H2MM_SB = 2, H2MM_TD = 3 };  // A base
+struct H2MMLevel {
+    int32_t beg, end, src, abase, dst, accum;
+};
+struct H2MM {
+    H2MMJob *jobs = nullptr;
+    int njobs = 0;
+    std::vector<H2MMLevel> levels;
+    i64 nxh = 0, nyrows = 0;  // rows of Xh and of Yh (whose first rows are the ZS plan's T rows)
+    const double *pb = nullptr, *tu = nullptr, *td = nullptr, *sb = nullptr;
+    double flops_per_rhs = 0.0;  // of the walk (the rows add the ZS plan's 2 x stored scalars)
+    DevBuf xh, yh;
+    ~H2MM();
+};
+struct H2MMInput {
+    const std::vector<H2Leaf> *leaves = nullptr;
+    const std::vector<H2Up> *ups = nullptr;
+    std::vector<int> up_height;
+    const std::vector<H2Down> *dns = nullptr;
+    const std::vector<H2Cpl> *cpls = nullptr;
+    std::vector<int> dn_depth;
+    std::vector<int32_t> dn_row, dn_prow;  // Yh row of every node / of its parent (-1 none)
+    i64 nxh = 0, nyrows = 0;
+    const double *pb = nullptr, *tu = nullptr, *td = nullptr, *sb = nullptr;
+};
+std::shared_ptr<H2MM> build_h2mm(const H2MMInput &in, cudaStream_t st);
+struct MvPlan;
+// Y = alpha Z X + beta W (row-major, ldk a multiple of 64); zs: the ZS plan (dense + Q_t pieces)
+void h2mm_run(H2MM &M, const MvPlan &zs, const double *X, double *Y, i64 ldk, double alpha, double beta,
+              const double *W, cudaStream_t s);
 struct H2 {
     int nsub_up = 0, nsub_dn = 0, maxh_up = 0, maxh_dn = 0, split = 0;
     std::shared_ptr<H2S> step2;  // two-kernel fused step (default when built)
+    std::shared_ptr<H2MM> mm;    // multi-RHS walk (h2mm.cu)
     // fused single-RHS step: the dense diagonal leaves stream on a forked,
     // low-priority stream beside the walk into yd; the row walk applies Q_t y_hat_t itself
     H2QLeaf *qleaf = nullptr;    // per row subtree, [dn_qbeg[s], dn_qbeg[s+1])
@@ -241,5 +279,8 @@ struct MmBufs {  // the context's multi-RHS scratch sized for plan P and K right
     double *T, *part;
 };
 MmBufs mm_bufs(Ctx &ctx, const MvPlan &P, i64 ldk);
+// the segment phase of mm_run alone, with T supplied by the caller (T row blk * KC_MAX + c)
+void seg_mm_launch(const MvPlan &P, const double *X, const double *T, i64 ldk, double *Y, double alpha,
+                   double beta, const double *Z, cudaStream_t s);
 
 }  // namespace lh

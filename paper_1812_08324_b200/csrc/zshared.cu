@@ -1143,6 +1143,11 @@ void h2_launch_fused(const H2 &h, const double *x, double *y, double alpha, doub
 // leaf (the segment kernel's operands), the plan carries the H2 walk.  Returns false (nothing
 // changed) when Z does not qualify: leaves above 64 rows, a cluster whose gathered factors exceed
 // the shared-memory capacity, a basis above KQ columns, or a path deeper than H2_MAXP.
+static bool h2_fail(const char *why) {
+    if (getenv("LEVYH_PLAN_VERBOSE")) fprintf(stderr, "[levyh] H2 form not built: %s\n", why);
+    return false;
+}
+
 bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_ptr<MvPlan> &plan,
               double *stats) {
     const cudaStream_t st = ctx.stream;
@@ -1150,12 +1155,12 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     const Tree *trees[2] = {Z.rt, Z.ct};
     for (int sd = 0; sd < 2; ++sd)
         for (int32_t lc : trees[sd]->leaves)
-            if (trees[sd]->nodes[lc].size() > LR) return false;
+            if (trees[sd]->nodes[lc].size() > LR) return h2_fail("leaf above 64 rows");
     std::vector<int32_t> lr;
     for (int32_t b : Z.leafblocks)
         if (Z.nodes[b].kind == K_LR && Z.h_ranks[Z.nodes[b].rslot] > 0) lr.push_back(b);
     const int nb = (int)lr.size();
-    if (nb == 0) return false;
+    if (nb == 0) return h2_fail("no low-rank blocks");
     DevFrees tmp;
     // weights: column norms of U (for the V side) and V (for the U side)
     std::vector<i64> woff(nb), noff, nlen;
@@ -1248,7 +1253,7 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
         i64 clen = 0, qlen = 0;
         for (int c = 0; c < nn; ++c) {
             if (!D.has[c]) continue;
-            if (D.ncol[c] > MAXC) return false;
+            if (D.ncol[c] > MAXC) return h2_fail("gathered factor columns above MAXC");
             D.maxh = std::max(D.maxh, D.height[c]);
             D.cout[c] = clen;
             clen += (i64)KQ * D.ncol[c];
@@ -1310,7 +1315,7 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
             cudaFree(dp);
             cudaFree(dk);
             for (int j = 0; j < nj; ++j) {
-                if (kk[j] < 0) return false;
+                if (kk[j] < 0) return h2_fail("basis above KQ columns");
                 D.k[who[j]] = kk[j];
             }
         }
@@ -1510,8 +1515,10 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     const std::vector<int32_t> subs_up = roots(CT, C, split);
     int maxh_up = 0;
     for (int32_t r0 : subs_up) maxh_up = std::max(maxh_up, C.height[r0]);
+    std::vector<int> up_h;  // height of every ups entry (multi-RHS walk)
     auto make_up = [&](int c) {
         const Cluster &cl = CT.nodes[c];
+        up_h.push_back(C.height[c]);
         H2Up U{tulen, C.k[c], C.k[cl.kid[0]], C.k[cl.kid[1]], xoff[c], xoff[cl.kid[0]], xoff[cl.kid[1]], -1, 0};
         if (C.k[c] > 0 && C.rows[c] > 0)
             tj.push_back({C.qout[c], 1, C.rows[c], tulen, C.k[c], 1, C.rows[c], C.k[c]});
@@ -1619,8 +1626,10 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     std::vector<int32_t> dn_path, dn_pbeg{0}, dn_lv;
     std::vector<std::vector<int>> blocks_of(RT.nodes.size());
     for (int q = 0; q < nb; ++q) blocks_of[Z.nodes[lr[q]].rcl].push_back(q);
+    std::vector<int32_t> dn_cl;  // row cluster of every dns entry (multi-RHS walk)
     auto make_dn = [&](int c) {
         const Cluster &cl = RT.nodes[c];
+        dn_cl.push_back(c);
         H2Down D{0, 0, 0, 0, R.k[c], yoff[c], -1, (int32_t)cpls.size(), 0, -1, 0};
         const int p = R.parent[c];
         if (p >= 0 && R.has[p] && R.k[p] > 0 && tdoff[p] >= 0) {
@@ -1676,13 +1685,13 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     for (int32_t r0 : subs_dn) {
         std::vector<int32_t> path;
         for (int p = R.parent[r0]; p >= 0 && R.has[p]; p = R.parent[p]) path.push_back(dnidx[p]);
-        if ((int)path.size() > H2_MAXP) return false;
+        if ((int)path.size() > H2_MAXP) return h2_fail("row path deeper than H2_MAXP");
         maxpath = std::max(maxpath, (int)path.size());
         std::reverse(path.begin(), path.end());
         dn_path.insert(dn_path.end(), path.begin(), path.end());
         dn_pbeg.push_back((int32_t)dn_path.size());
     }
-    if (!tcol_ok) return false;
+    if (!tcol_ok) return h2_fail("row-leaf coefficients not contiguous in tcol");
     LH_CUDA(cudaMemsetAsync(plan->tcol, 0, sizeof(double) * plan->tcol_len, st));  // padding stays zero
     // ---- device data
     h->split = split;
@@ -1704,19 +1713,19 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     std::vector<int32_t> up_chain, up_cbeg{0};
     for (int32_t r0 : subs_up) {
         for (int p = C.parent[r0]; p >= 0 && C.has[p]; p = C.parent[p]) up_chain.push_back(upidx[p]);
-        if ((int)(up_chain.size() - up_cbeg.back()) > H2_MAXP) return false;
+        if ((int)(up_chain.size() - up_cbeg.back()) > H2_MAXP) return h2_fail("column climb deeper than H2_MAXP");
         up_cbeg.push_back((int32_t)up_chain.size());
     }
     for (size_t q = 0; q + 1 < up_lv.size(); q += (size_t)maxh_up + 1)
-        if (up_lv[q + maxh_up] - up_lv[q] > H2_MAXN) return false;
+        if (up_lv[q + maxh_up] - up_lv[q] > H2_MAXN) return h2_fail("column subtree above H2_MAXN nodes");
     for (size_t q = 0; q + 1 < dn_lv.size(); q += (size_t)maxh_dn + 2)
-        if (dn_lv[q + maxh_dn + 1] - dn_lv[q] > H2_MAXN) return false;
+        if (dn_lv[q + maxh_dn + 1] - dn_lv[q] > H2_MAXN) return h2_fail("row subtree above H2_MAXN nodes");
     h->up_chain = dupload(up_chain, st);
     h->up_cbeg = dupload(up_cbeg, st);
     h->crec = dupload(crec, st);
     h->nleaf = (int)leaves.size();
     for (size_t l = 0; l < leaves.size(); ++l) {
-        if (l > 0 && leaves[l].x0 < leaves[l - 1].x0) return false;  // row order (host pipeline)
+        if (l > 0 && leaves[l].x0 < leaves[l - 1].x0) return h2_fail("column leaves out of row order");  // row order (host pipeline)
         h->leaf_end.push_back(leaves[l].x0 + leaves[l].rows);
     }
     h->ncnode = (int)crec.size();
@@ -1754,6 +1763,33 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
     }
     LH_CUDA(cudaStreamSynchronize(st));
     h->bytes = 8 * (plen + tulen + tdlen + sblen) + 8 * (i64)Z.ncols;
+    {  // multi-RHS walk (h2mm.cu): Yh rows of row leaves with a basis are the ZS plan's T rows
+        H2MMInput mi;
+        mi.leaves = &leaves;
+        mi.ups = &ups;
+        mi.up_height = up_h;
+        mi.dns = &dns;
+        mi.cpls = &cpls;
+        const i64 tbase = (i64)plan->nblk * KC_MAX;
+        std::vector<int32_t> yrow(RT.nodes.size(), -1);
+        for (size_t c = 0; c < RT.nodes.size(); ++c)
+            if (yoff[c] >= 0)
+                yrow[c] = (RT.nodes[c].leaf() && qnode[c] >= 0) ? plan->blk_of_node[qnode[c]] * KC_MAX
+                                                                 : (int32_t)(tbase + yoff[c]);
+        for (size_t d = 0; d < dns.size(); ++d) {
+            const int c = dn_cl[d], p = R.parent[c];
+            mi.dn_depth.push_back(RT.nodes[c].depth);
+            mi.dn_row.push_back(yrow[c]);
+            mi.dn_prow.push_back(dns[d].kp > 0 && p >= 0 ? yrow[p] : -1);
+        }
+        mi.nxh = nxh;
+        mi.nyrows = tbase + nyh;
+        mi.pb = h->pb;
+        mi.tu = h->tu;
+        mi.td = h->td;
+        mi.sb = h->sb;
+        h->mm = build_h2mm(mi, st);
+    }
     // fused single-RHS step (default; LEVYH_H2_NOFUSE keeps the combined segment pass): the
     // dense leaves get a plan of their own for the co-resident segment kernel, and every row
     // leaf is assigned to a row-subtree CTA that finishes its rows (leaves without a basis
@@ -1763,7 +1799,7 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
         size_t rr = 0;
         for (int32_t lc : RT.leaves) {
             const Cluster &cl = RT.nodes[lc];
-            if (cl.size() > 64) return false;
+            if (cl.size() > 64) return h2_fail("row leaf above 64 rows");
             H2QLeaf q{0, cl.lo, (int32_t)cl.size(), 0, 0, 0};
             int sub = -1;
             if (qnode[lc] >= 0 && insub[lc] >= 0) {

@@ -111,9 +111,10 @@ class HFactorization:
     def propagator_stats(self):
         """(task count, planning s, temp bytes, executor s, near-field leaves compressed,
         coarsening merges, single-RHS form (0 H, 1 shared leaf bases, 2 nested H2), its probe
-        error against the H-form, mean leaf basis size, basis/transfer/coupling scalars) of the
+        error against the H-form, mean leaf basis size, basis/transfer/coupling scalars, flops per
+        right-hand side of the multi-RHS product and its form (2 H2 walk, 1 H-form)) of the
         propagator build."""
-        out = np.zeros(10)
+        out = np.zeros(12)
         _lib.check(_lib.lib().lh_propagator_stats(self.h.handle, _lib.host_ptr(out)))
         return out
 

@@ -90,7 +90,7 @@ def test_run_cn_multi_rhs(P, name, K):
     steps = 10
     U0 = _bumps(s.x, K)
     UK = P.run_cn(s, U0, steps, method="propagator")
-    assert list(_path(P, s.factor)[:3]) == [2, 1, 0]  # CN pair, DMMA matmat
+    assert list(_path(P, s.factor)[:3]) == [2, 2, 0]  # CN pair, DMMA walk of the H2 form
     assert UK.shape == (s.N, K)
     ref = _oracle_multi(g, U0, steps)
     for k in range(K):
@@ -116,7 +116,7 @@ def test_run_cn_multi_rhs_general_hminus(P, K):
     U0 = _bumps(s.x, K, seed=5)
     steps = 4
     UK = P.run_cn(s, U0, steps, method="propagator")
-    assert list(_path(P, s.factor)[:3]) == [3, 1, 0]
+    assert list(_path(P, s.factor)[:3]) == [3, 2, 0]
     want = U0.copy()
     for _ in range(steps):
         want = P.solve(s.factor, P.mul_dense(Hq, want), method="substitution")
@@ -137,10 +137,38 @@ def test_run_cn_multi_rhs_coarsened_propagator(P):
     s.prepare(P.HConfig(n_min=64, eps1=1e-10), 1e-10, method="propagator")
     U0 = np.random.default_rng(3).standard_normal((s.N, 64))
     UK = P.run_cn(s, U0, 3, method="propagator")
-    assert list(_path(P, s.factor)[:3]) == [2, 1, 0]
+    form = int(s.factor.propagator_stats()[6])  # this operator's nested bases exceed 32 columns
+    assert list(_path(P, s.factor)[:3]) == [2, 2 if form == 2 else 1, 0]
     for k in (0, 37, 63):
         uk = P.run_cn(s, U0[:, k], 3, method="propagator")
         assert np.linalg.norm(UK[:, k] - uk) <= 1e-10 * np.linalg.norm(uk)
         us = P.run_cn(s, U0[:, k], 3, method="substitution")
         assert list(_path(P, s.factor)[:3]) == [0, 0, 0]
         assert np.linalg.norm(UK[:, k] - us) <= 1e-9 * np.linalg.norm(us)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3_cgmy_n8191", "cfg5_leaf128"])
+def test_multi_rhs_h2_walk_matches_h_form_matmat(P, name, monkeypatch):
+    """The two multi-RHS forms of Z: the nested-basis walk as batched DMMA products (h2mm.cu:
+    leaves, up levels, couplings, down levels, then the segment matmat of the dense leaves and
+    row bases) and the DMMA matmat of Z's H-form (LEVYH_NO_H2MM), against each other, against
+    single-RHS steps and against the reference multi-RHS loop (oracle, N <= 1023).  Leaf-128
+    operators have no H2 form: both runs take the H-form."""
+    g = cases.load(name)
+    s = cases.make_system(name, g)
+    s.prepare(P.HConfig(n_min=int(g["leaf"]), eps1=float(g["eps1"])), float(g["eps2"]))
+    K, steps = 72, 5
+    U0 = _bumps(s.x, K, seed=11)
+    UH2 = P.run_cn(s, U0, steps)
+    form = int(s.factor.propagator_stats()[6])
+    assert _path(P, s.factor)[1] == (2 if form == 2 else 1)
+    monkeypatch.setenv("LEVYH_NO_H2MM", "1")
+    UH = P.run_cn(s, U0, steps)
+    assert _path(P, s.factor)[1] == 1
+    monkeypatch.delenv("LEVYH_NO_H2MM")
+    assert _rel(UH2, UH) <= 1e-10
+    for k in (0, 35, 71):
+        assert _rel(UH2[:, k], P.run_cn(s, U0[:, k], steps)) <= 1e-10
+    if s.N <= 1023:
+        ref = _oracle_multi(g, U0[:, :8], steps)
+        assert _rel(UH2[:, :8], ref) <= 1e-8
