@@ -82,6 +82,113 @@ __global__ void __launch_bounds__(NT) vtx_mm_kernel(const VChunk *chunks, const 
     }
 }
 
+// phase 1, grouped: one CTA per (group of chunks over the same x rows, 64-RHS tile); the X tile
+// of every inner step is staged once for all the group's chunks (<= 64 output rows: 8 row
+// fragments per warp, warp w owns RHS w*8 .. +8)
+__global__ void __launch_bounds__(NT) vtx_mm_group_kernel(const VGroup *groups, const VChunk *gch,
+                                                          const double *pbuf, const double *X, i64 ldk,
+                                                          double *T, double *part) {
+    // two stages of (Vs [MM_KB][64] k-major, rows XOR-swizzled by 8 (k & 3) so both the staging
+    // stores and the DMMA fragment loads touch every bank pair twice; Xs [MM_KB][MM_STR]); the
+    // next inner step is loaded into registers while the current one is multiplied.  Warp w
+    // owns output rows 16 (w % 4) .. +16 and RHS 32 (w / 4) .. +32 (2 x 4 fragments).
+    extern __shared__ double dsm[];
+    constexpr int VS = MM_KB * 64, XS = MM_KB * MM_STR;
+    __shared__ int32_t rq[64], rc[64];  // output row -> (chunk, column)
+    __shared__ i64 ro[64];              // output row -> pbuf offset of its V column
+    const VGroup G = groups[blockIdx.x];
+    const int kc = blockIdx.y * MM_N;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int r0 = (w & 3) * 16, n0 = (w >> 2) * 32;
+    if (threadIdx.x == 0) {
+        int row = 0;
+        for (int q = G.cbeg; q < G.cend; ++q) {
+            const VChunk C = gch[q];
+            for (int c = 0; c < vc_rank(C); ++c, ++row) {
+                rq[row] = q;
+                rc[row] = c;
+                ro[row] = C.voff + (i64)c * C.len;
+            }
+        }
+    }
+    __syncthreads();
+    constexpr int PV = 64 * MM_KB / NT, PX = MM_KB * MM_N / NT;  // elements per thread
+    double rv[PV], rx[PX];
+    // V element of register u: lanes cover 8 rows x 4 consecutive k (32-byte sectors of V)
+    auto vrow = [&](int u) { return (((threadIdx.x + u * NT) >> 5) >> 3) * 8 + (l >> 2); };
+    auto vk = [&](int u) { return (((threadIdx.x + u * NT) >> 5) & 7) * 4 + (l & 3); };
+    auto load = [&](int k0) {
+        const int kb = min(MM_KB, G.len - k0);
+#pragma unroll
+        for (int u = 0; u < PV; ++u) {
+            const int r = vrow(u), k = vk(u);
+            rv[u] = (r < G.m && k < kb) ? pbuf[ro[r] + k0 + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PX; ++u) {
+            const int e = threadIdx.x + u * NT, i = e / MM_N, n = e % MM_N;
+            rx[u] = i < kb ? X[(G.xc0 + k0 + i) * ldk + kc + n] : 0.0;
+        }
+    };
+    auto store = [&](int st) {
+        double *Vs = dsm + st * (VS + XS), *Xs = Vs + VS;
+#pragma unroll
+        for (int u = 0; u < PV; ++u) {
+            const int r = vrow(u), k = vk(u);
+            Vs[k * 64 + (r ^ (8 * (k & 3)))] = rv[u];
+        }
+#pragma unroll
+        for (int u = 0; u < PX; ++u) {
+            const int e = threadIdx.x + u * NT;
+            Xs[(e / MM_N) * MM_STR + e % MM_N] = rx[u];
+        }
+    };
+    const bool act = r0 < G.m;
+    double acc[2][4][2] = {};
+    load(0);
+    store(0);
+    __syncthreads();
+    int st = 0;
+    for (int k0 = 0; k0 < G.len; k0 += MM_KB) {
+        const bool more = k0 + MM_KB < G.len;
+        if (more) load(k0 + MM_KB);
+        const double *Vs = dsm + st * (VS + XS), *Xs = Vs + VS;
+        if (act) {
+#pragma unroll
+            for (int kk = 0; kk < MM_KB; kk += 4) {
+                const int k = kk + (l & 3);
+                double a[2], b[4];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) a[i] = Vs[k * 64 + ((r0 + i * 8 + (l >> 2)) ^ (8 * (l & 3)))];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = Xs[k * MM_STR + n0 + j * 8 + (l >> 2)];
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            }
+        }
+        if (more) store(st ^ 1);
+        __syncthreads();
+        st ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int r = r0 + i * 8 + (l >> 2);
+        if (r >= G.m) continue;
+        const VChunk &C = gch[rq[r]];
+        double *out = (C.pidx >= 0 ? part + (i64)C.pidx * KC_MAX * ldk : T + (i64)C.blk * KC_MAX * ldk) +
+                      (i64)(vc_col0(C) + rc[r]) * ldk;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = kc + n0 + j * 8 + (l & 3) * 2;
+            out[n] = acc[i][j][0];
+            out[n + 1] = acc[i][j][1];
+        }
+    }
+}
+constexpr int VTXG_SMEM = 2 * (MM_KB * 64 + MM_KB * MM_STR) * 8;
+
 // T rows of multi-chunk blocks: sum of their chunk partials (fixed order)
 __global__ void treduce_mm_kernel(const TJob *jobs, const double *part, i64 ldk, int K, double *T) {
     const TJob J = jobs[blockIdx.x];
@@ -99,30 +206,57 @@ __global__ void __launch_bounds__(NT) seg_mm_kernel(const SegDesc *segs, const i
                                                     const double *pbuf, const double *X,
                                                     const double *T, i64 ldk, double *Y,
                                                     double alpha, double beta, const double *Z) {
-    __shared__ double As[MM_KB * MM_STR];  // [q][row]
-    __shared__ double Bs[MM_KB * MM_STR];  // [q][n]
+    // two stages of (As [MM_KB][MM_STR], Bs [MM_KB][MM_STR]), register-staged prefetch of the next
+    // inner step during the current one's DMMA
+    extern __shared__ double dsm[];
+    constexpr int AS = MM_KB * MM_STR;
     const SegDesc S = segs[blockIdx.x];
     const int kc = blockIdx.y * MM_N;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int r0 = (w & 3) * 16, n0 = (w >> 2) * 32;
     double acc[2][4][2] = {};
     const double *A = pbuf + S.poff;
-    for (int q0 = 0; q0 < S.ncol; q0 += MM_KB) {
+    constexpr int PA = MM_KB * 64 / NT, PB = MM_KB * MM_N / NT;
+    double ra[PA], rb[PB];
+    auto load = [&](int q0) {
         const int qb = min(MM_KB, S.ncol - q0);
-        for (int e = threadIdx.x; e < MM_KB * 64; e += NT) {
-            const int q = e / 64, i = e % 64;
-            As[q * MM_STR + i] = (q < qb && i < S.ld) ? A[(i64)(q0 + q) * S.ld + i] : 0.0;
+#pragma unroll
+        for (int u = 0; u < PA; ++u) {
+            const int e = threadIdx.x + u * NT, q = e / 64, i = e % 64;
+            ra[u] = (q < qb && i < S.ld) ? A[(i64)(q0 + q) * S.ld + i] : 0.0;
         }
-        for (int e = threadIdx.x; e < MM_KB * MM_N; e += NT) {
-            const int q = e / MM_N, n = e % MM_N;
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+            const int e = threadIdx.x + u * NT, q = e / MM_N, n = e % MM_N;
             double v = 0.0;
             if (q < qb) {
                 const int32_t src = colmap[S.cmoff + q0 + q];
                 v = src >= 0 ? X[(i64)src * ldk + kc + n] : T[(i64)(-1 - src) * ldk + kc + n];
             }
-            Bs[q * MM_STR + n] = v;
+            rb[u] = v;
         }
-        __syncthreads();
+    };
+    auto store = [&](int st) {
+        double *As = dsm + st * 2 * AS, *Bs = As + AS;
+#pragma unroll
+        for (int u = 0; u < PA; ++u) {
+            const int e = threadIdx.x + u * NT;
+            As[(e / 64) * MM_STR + e % 64] = ra[u];
+        }
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+            const int e = threadIdx.x + u * NT;
+            Bs[(e / MM_N) * MM_STR + e % MM_N] = rb[u];
+        }
+    };
+    load(0);
+    store(0);
+    __syncthreads();
+    int st = 0;
+    for (int q0 = 0; q0 < S.ncol; q0 += MM_KB) {
+        const bool more = q0 + MM_KB < S.ncol;
+        if (more) load(q0 + MM_KB);
+        const double *As = dsm + st * 2 * AS, *Bs = As + AS;
 #pragma unroll
         for (int kk = 0; kk < MM_KB; kk += 4) {
             double a[2], b[4];
@@ -135,7 +269,9 @@ __global__ void __launch_bounds__(NT) seg_mm_kernel(const SegDesc *segs, const i
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
+        if (more) store(st ^ 1);
         __syncthreads();
+        st ^= 1;
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -153,6 +289,7 @@ __global__ void __launch_bounds__(NT) seg_mm_kernel(const SegDesc *segs, const i
         }
     }
 }
+constexpr int SEGMM_SMEM = 2 * 2 * MM_KB * MM_STR * 8;
 
 // column-major (ld) <-> row-major (ldk) conversion of an n x k block, 32 x 32 tiles
 __global__ void transpose_kernel(const double *src, i64 lds, double *dst, i64 ldd, i64 n, int k,
@@ -193,6 +330,16 @@ void mm_transpose(const double *src, i64 lds, double *dst, i64 ldd, i64 n, int k
     LH_CUDA(cudaGetLastError());
 }
 
+static void mm_attrs() {
+    static bool done = false;
+    if (done) return;
+    LH_CUDA(cudaFuncSetAttribute((const void *)vtx_mm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 VTXG_SMEM));
+    LH_CUDA(cudaFuncSetAttribute((const void *)seg_mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SEGMM_SMEM));
+    done = true;
+}
+
 i64 mm_pad(int k) { return ((i64)k + MM_N - 1) / MM_N * MM_N; }
 
 // right-hand-side count from which the DMMA matmat replaces per-column matvecs
@@ -213,19 +360,28 @@ void mm_run(const MvPlan &P, const double *X, double *Y, i64 ldk, double alpha, 
             const double *Z, double *T, double *part, cudaStream_t s) {
     LH_REQUIRE(!P.cpl && !P.h2, LH_EINTERNAL, "the multi-RHS matmat runs on the H-form plan");
     const unsigned nk = (unsigned)(ldk / MM_N);
-    if (P.nch > 0) vtx_mm_kernel<<<dim3(P.nch, nk), NT, 0, s>>>(P.chunks, P.pbuf, X, ldk, T, part);
-    if (P.nch16 > 0)
-        vtx_mm_kernel<<<dim3(P.nch16, nk), NT, 0, s>>>(P.chunks16, P.pbuf, X, ldk, T, part);
+    static const bool ungrouped = getenv("LEVYH_MM_NOGROUP") != nullptr;  // timing experiments only
+    if (!ungrouped && P.ngroup > 0) {
+        mm_attrs();
+        vtx_mm_group_kernel<<<dim3(P.ngroup, nk), NT, VTXG_SMEM, s>>>(P.groups, P.gchunks, P.pbuf, X, ldk, T, part);
+    } else {
+        if (P.nch > 0) vtx_mm_kernel<<<dim3(P.nch, nk), NT, 0, s>>>(P.chunks, P.pbuf, X, ldk, T, part);
+        if (P.nch16 > 0)
+            vtx_mm_kernel<<<dim3(P.nch16, nk), NT, 0, s>>>(P.chunks16, P.pbuf, X, ldk, T, part);
+    }
     if (P.ntj > 0) treduce_mm_kernel<<<P.ntj, NT, 0, s>>>(P.tjobs, part, ldk, (int)ldk, T);
-    seg_mm_kernel<<<dim3(P.nseg, nk), NT, 0, s>>>(P.segs, P.colmap, P.pbuf, X, T, ldk, Y, alpha, beta,
-                                                  Z ? Z : Y);
+    mm_attrs();
+    seg_mm_kernel<<<dim3(P.nseg, nk), NT, SEGMM_SMEM, s>>>(P.segs, P.colmap, P.pbuf, X, T, ldk, Y, alpha, beta,
+                                                           Z ? Z : Y);
     LH_CUDA(cudaGetLastError());
 }
 
 void seg_mm_launch(const MvPlan &P, const double *X, const double *T, i64 ldk, double *Y, double alpha,
                    double beta, const double *Z, cudaStream_t s) {
     const unsigned nk = (unsigned)(ldk / MM_N);
-    seg_mm_kernel<<<dim3(P.nseg, nk), NT, 0, s>>>(P.segs, P.colmap, P.pbuf, X, T, ldk, Y, alpha, beta, Z ? Z : Y);
+    mm_attrs();
+    seg_mm_kernel<<<dim3(P.nseg, nk), NT, SEGMM_SMEM, s>>>(P.segs, P.colmap, P.pbuf, X, T, ldk, Y, alpha, beta,
+                                                           Z ? Z : Y);
     LH_CUDA(cudaGetLastError());
 }
 

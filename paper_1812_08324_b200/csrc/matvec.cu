@@ -739,6 +739,40 @@ std::shared_ptr<MvPlan> build_mv_plan(HMat &H, const std::vector<int32_t> &block
     P->lp = dupload(lall, s);
     P->chunks = dupload(chunks, s);
     P->chunks16 = dupload(chunks16, s);
+    {  // multi-RHS: chunks over the same x rows grouped (<= 64 output rows per group), so the
+       // DMMA V^T X kernel stages each X tile once for all of them (matmat.cu: vtx_mm_group)
+        std::map<std::pair<i64, int>, std::vector<VChunk>> by;
+        std::vector<std::pair<i64, int>> order;
+        for (int k = 0; k < 2; ++k)
+            for (const VChunk &c : (k ? chunks16 : chunks)) {
+                auto key = std::make_pair(c.xc0, c.len);
+                if (!by.count(key)) order.push_back(key);
+                by[key].push_back(c);
+            }
+        std::vector<VChunk> gch;
+        std::vector<VGroup> gr;
+        for (auto &key : order) {
+            VGroup g{key.first, key.second, (int32_t)gch.size(), (int32_t)gch.size(), 0, 0};
+            for (const VChunk &c : by[key]) {
+                if (g.m + vc_rank(c) > 64) {
+                    gr.push_back(g);
+                    g = VGroup{key.first, key.second, (int32_t)gch.size(), (int32_t)gch.size(), 0, 0};
+                }
+                gch.push_back(c);
+                g.cend = (int32_t)gch.size();
+                g.m += vc_rank(c);
+            }
+            gr.push_back(g);
+        }
+        // by x rows: the groups of every level that read the same rows of X run close together,
+        // so X comes from HBM about once and from L2 for the other levels
+        std::stable_sort(gr.begin(), gr.end(), [](const VGroup &a, const VGroup &b) {
+            return a.xc0 != b.xc0 ? a.xc0 < b.xc0 : a.len > b.len;
+        });
+        P->ngroup = (int)gr.size();
+        P->groups = dupload(gr, s);
+        P->gchunks = dupload(gch, s);
+    }
     P->tjobs = dupload(tjobs, s);
     P->part = dalloc<double>((i64)std::max(npart, 1) * KC_MAX);
     P->batches = dupload(batches, s);
@@ -840,6 +874,8 @@ MvPlan::~MvPlan() {
     cudaFree(lp);
     cudaFree(chunks);
     cudaFree(chunks16);
+    cudaFree(groups);
+    cudaFree(gchunks);
     cudaFree(tjobs);
     cudaFree(part);
     cudaFree(tvec);

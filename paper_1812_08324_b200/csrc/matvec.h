@@ -39,6 +39,11 @@ struct VChunk {  // V rows at pbuf[voff + i + c * len], i < len, c < r, multipli
 };
 __host__ __device__ inline int vc_rank(const VChunk &c) { return c.r & 0xffff; }
 __host__ __device__ inline int vc_col0(const VChunk &c) { return c.r >> 16; }
+struct VGroup {  // V chunks over the same x rows [xc0, xc0 + len): gchunks [cbeg, cend), m output rows
+    i64 xc0;
+    int32_t len, cbeg, cend, m;
+    int32_t pad;
+};
 struct TJob {  // t_b = sum of the partials of chunks [cbeg, cend), written to tvec row blk
     int32_t blk, r, cbeg, cend;
 };
@@ -235,6 +240,9 @@ struct MvPlan {
     MvLr *lp = nullptr;
     VChunk *chunks = nullptr;
     VChunk *chunks16 = nullptr;  // chunks of blocks with rank > 8
+    VGroup *groups = nullptr;    // multi-RHS: chunks grouped by x rows (matmat.cu)
+    VChunk *gchunks = nullptr;
+    int ngroup = 0;
     TJob *tjobs = nullptr;
     double *part = nullptr;
     SBatch *batches = nullptr;
