@@ -109,6 +109,25 @@ int lh_hmat_shard_pack(lh_ctx *ctx, lh_hmat *h, double *buf_dev, int64_t cap, in
 int lh_hmat_shard_unpack(lh_ctx *ctx, lh_hmat *h, int32_t src_rank, const double *buf_dev,
                          int64_t len);
 int lh_hmat_shard_finalize(lh_ctx *ctx, lh_hmat *h);
+/* NCCL inside the library.  The context owns one communicator:
+ * rank 0 calls lh_nccl_unique_id, the caller distributes the 128 bytes (any side channel, e.g.
+ * torch.distributed.broadcast_object_list), every rank calls lh_nccl_init.  libnccl.so.2 is
+ * opened at run time (the copy already loaded by the process first).  lh_nccl_ready: 1 once
+ * initialised. */
+int lh_nccl_unique_id(void *uid128_host);
+int lh_nccl_init(lh_ctx *ctx, int32_t rank, int32_t world, const void *uid128_host);
+int lh_nccl_ready(lh_ctx *ctx);
+/* Sharded assembly over the context's communicator: the same result as lh_hmat_build_toeplitz
+ * (bit for bit) with the ACA of the admissible blocks split across the ranks (longest-processing-
+ * time assignment by m + n) and every rank's share cut into `stages` parts: stage s's factors
+ * are all-gathered on a communication stream while stage s + 1 compresses.  stats_host (may be
+ * NULL): compress seconds, host wait for the exchange, finalize seconds, bytes sent, received. */
+int lh_hmat_build_toeplitz_nccl(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,
+                                const lh_hconfig *cfg, int32_t stages, double *stats_host, lh_hmat **out);
+/* Broadcast of an H-matrix's device data (arena, ranks, leaf permutations and inverses) from
+ * `root`; every rank holds the same structure and layout (e.g. an H-LU factor computed once and
+ * shared by ranks that step disjoint right-hand-side columns). */
+int lh_bcast_factors(lh_ctx *ctx, lh_hmat *h, int32_t root);
 /* build_from_dense(A, rt, ct, cfg) with A on the device (tree order), element (i,j) at
  * A[i*lda + j] (row_major=1, numpy C order) or A[i + j*lda] (row_major=0). */
 int lh_hmat_build_dense(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *A_dev,

@@ -13,7 +13,8 @@ from .fractional import (FracConfig, LevyMeasure, assemble_fractional_poisson_1d
 from .geometry import (ClusterNode, ClusterTree, Permutation, PointSet, admissible,  # noqa: F401
                        build_cluster_tree)
 from .hmatrix import (HConfig, HMatrix, KernelExpansion, ToeplitzEntries, build_from_dense,  # noqa: F401
-                      build_from_expansion, build_toeplitz, derive_toeplitz, dump_structure,
+                      bcast_factors, build_from_expansion, build_toeplitz, build_toeplitz_nccl,
+                      derive_toeplitz, dump_structure,
                       export_blocks, gaussian_expansion_1d, h_entry, memory_report,
                       rank_bound_gaussian, structure_summary, to_dense)
 from .hops import (SOLVE_METHODS, HFactorization, hlu, lowrank_add_recompress, matvec,  # noqa: F401

@@ -59,6 +59,11 @@ SIGNATURES = [
     ("lh_hmat_derive_toeplitz", C.c_int, [P, P, P, D, I32, C.POINTER(P)]),
     ("lh_hmat_clone", C.c_int, [P, P, I32, C.POINTER(P)]),
     ("lh_hmat_spill", C.c_int, [P, P]),
+    ("lh_nccl_unique_id", C.c_int, [P]),
+    ("lh_nccl_init", C.c_int, [P, I32, I32, P]),
+    ("lh_nccl_ready", C.c_int, [P]),
+    ("lh_hmat_build_toeplitz_nccl", C.c_int, [P, P, P, P, P, I32, P, C.POINTER(P)]),
+    ("lh_bcast_factors", C.c_int, [P, P, I32]),
     ("lh_hmat_resident", C.c_int, [P]),
     ("lh_hmat_destroy", None, [P]),
     ("lh_hmat_num_blocks", I64, [P]),
@@ -176,6 +181,27 @@ class Context:
 
     def sync(self):
         check(lib().lh_ctx_synchronize(self.h), self.h)
+
+    def nccl_ready(self):
+        return bool(lib().lh_nccl_ready(self.h))
+
+    def init_nccl(self, group=None):
+        """The library's own NCCL communicator over the ranks of `group` (torch.distributed,
+        already initialised): rank 0 creates the unique id, the group broadcasts it, every rank
+        calls lh_nccl_init.  No-op when already initialised."""
+        import torch.distributed as dist
+
+        if self.nccl_ready():
+            return
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            check(lib().lh_nccl_unique_id(C.cast(uid, C.c_void_p)))
+        obj = [bytes(uid.raw) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        check(lib().lh_nccl_init(self.h, rank, world, C.cast(uid, C.c_void_p)), self.h)
 
     def torch_stream(self):
         """The library's CUDA stream as a torch stream (for CUDA-event timing)."""

@@ -764,6 +764,176 @@ void shard_finalize(Ctx &ctx, HMat &H) {
     build_finalize(ctx, H, s, td);
 }
 
+// ---------------------------------------------------------------------------
+// sharded assembly over the context's NCCL communicator, with the
+// exchange overlapped with the compression: every rank's share is cut into `stages` parts
+// (identically on every rank); while stage s + 1 compresses on the context's stream, stage s's
+// packed factors are all-gathered on the communication stream (lengths first, then one padded
+// all-gather).  stats: compress s, host wait for the exchange s, finalize s, bytes sent, received.
+// ---------------------------------------------------------------------------
+static i64 pack_list(Ctx &ctx, HMat &H, const std::vector<int32_t> &blocks, const std::vector<char> &dense,
+                     double *buf, cudaStream_t s) {
+    const i64 nmeta = 1 + (i64)blocks.size();
+    std::vector<double> meta(nmeta);
+    meta[0] = (double)blocks.size();
+    std::vector<GatherJob> jobs;
+    i64 o = nmeta;
+    for (size_t k = 0; k < blocks.size(); ++k) {
+        const Node &nd = H.nodes[blocks[k]];
+        if (dense[blocks[k]]) {
+            meta[1 + k] = -1.0;
+            continue;
+        }
+        const int r = H.h_ranks[nd.rslot];
+        meta[1 + k] = (double)r;
+        jobs.push_back({nd.uoff, o, nd.m, r, 0});
+        o += nd.m * r;
+        jobs.push_back({nd.voff, o, nd.n, r, 0});
+        o += nd.n * r;
+    }
+    if (buf) {
+        LH_CUDA(cudaMemcpyAsync(buf, meta.data(), sizeof(double) * nmeta, cudaMemcpyHostToDevice, s));
+        if (!jobs.empty()) {
+            GatherJob *d = dupload(jobs, s);
+            int grid = (int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 16);
+            shard_copy_kernel<<<grid, NT, 0, s>>>(d, (int)jobs.size(), H.d_arena, buf);
+            LH_CUDA(cudaGetLastError());
+            LH_CUDA(cudaStreamSynchronize(s));
+            cudaFree(d);
+        }
+        LH_CUDA(cudaStreamSynchronize(s));
+    }
+    return o;
+}
+
+void build_toeplitz_nccl(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg, int stages, double *stats) {
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    const int rank = nccl_rank(ctx), world = nccl_world(ctx);
+    cudaStream_t cs = nccl_stream(ctx);
+    stages = std::max(1, stages);
+    std::vector<int32_t> lr = build_layout(ctx, H, cfg);
+    const auto owned = lpt_assign(H, lr, world);
+    auto part = [&](int q, int sidx) {  // stage sidx of rank q's share (in its ACA order)
+        const auto &o = owned[q];
+        const size_t a = o.size() * sidx / stages, b = o.size() * (sidx + 1) / stages;
+        return std::vector<int32_t>(o.begin() + a, o.begin() + b);
+    };
+    auto cap_of = [&](int q, int sidx) {  // upper bound of a packed stage (capacity columns)
+        i64 c = 1;
+        for (int32_t b : part(q, sidx)) c += 1 + (H.nodes[b].m + H.nodes[b].n) * H.nodes[b].kcap;
+        return c;
+    };
+    ToepSrc src{t, H.nrows};
+    std::vector<char> dense(H.nodes.size(), 0);
+    std::vector<int32_t> to_dense;
+    struct Stage {
+        double *send = nullptr, *recv = nullptr;
+        int64_t *dlen = nullptr;
+        std::vector<int64_t> lens;
+        i64 maxlen = 0;
+        cudaEvent_t packed = nullptr;
+    };
+    std::vector<Stage> stg(stages);
+    double t_aca = 0, t_wait = 0, sent = 0, recvd = 0;
+    auto cleanup = [&]() {
+        for (Stage &S : stg) {
+            if (S.send) cudaFree(S.send);
+            if (S.recv) cudaFree(S.recv);
+            if (S.dlen) cudaFree(S.dlen);
+            if (S.packed) cudaEventDestroy(S.packed);
+        }
+    };
+    try {
+        for (int sidx = 0; sidx < stages; ++sidx) {
+            Stage &S = stg[sidx];
+            auto t0 = now();
+            const std::vector<int32_t> mine = part(rank, sidx);
+            std::vector<int32_t> td = run_aca(ctx, H, src, cfg, mine);
+            H.sync_ranks(ctx.stream);
+            t_aca += sec(t0, now());
+            for (int32_t b : td) {
+                dense[b] = 1;
+                to_dense.push_back(b);
+            }
+            i64 bound = 0;
+            for (int q = 0; q < world; ++q) bound = std::max(bound, cap_of(q, sidx));
+            S.send = dalloc<double>(bound);
+            S.dlen = dalloc<int64_t>(2 * (i64)world + 1);
+            const i64 len = pack_list(ctx, H, mine, dense, S.send, ctx.stream);
+            sent += 8.0 * len;
+            LH_CUDA(cudaEventCreateWithFlags(&S.packed, cudaEventDisableTiming));
+            LH_CUDA(cudaEventRecord(S.packed, ctx.stream));
+            // lengths on the communication stream (it first finishes the previous stage's payload)
+            auto tw = now();
+            LH_CUDA(cudaStreamWaitEvent(cs, S.packed, 0));
+            const int64_t mylen = len;
+            LH_CUDA(cudaMemcpyAsync(S.dlen + world, &mylen, sizeof(int64_t), cudaMemcpyHostToDevice, cs));
+            nccl_allgather_i64(ctx, S.dlen + world, S.dlen, 1, cs);
+            S.lens.assign(world, 0);
+            LH_CUDA(cudaMemcpyAsync(S.lens.data(), S.dlen, sizeof(int64_t) * world, cudaMemcpyDeviceToHost, cs));
+            LH_CUDA(cudaStreamSynchronize(cs));
+            t_wait += sec(tw, now());
+            for (int64_t v : S.lens) S.maxlen = std::max<i64>(S.maxlen, v);
+            LH_REQUIRE(S.maxlen <= bound, LH_EINTERNAL, "packed stage above its capacity bound");
+            S.recv = dalloc<double>((i64)world * S.maxlen);
+            nccl_allgather_f64(ctx, S.send, S.recv, (size_t)S.maxlen, cs);  // overlaps the next stage
+        }
+        auto tw = now();
+        LH_CUDA(cudaStreamSynchronize(cs));
+        t_wait += sec(tw, now());
+        auto tf = now();
+        // unpack every other rank's stages (their factors, ranks and dense decisions)
+        for (int sidx = 0; sidx < stages; ++sidx) {
+            Stage &S = stg[sidx];
+            for (int q = 0; q < world; ++q) {
+                recvd += 8.0 * S.lens[q];
+                if (q == rank) continue;
+                const std::vector<int32_t> theirs = part(q, sidx);
+                const double *buf = S.recv + (i64)q * S.maxlen;
+                const i64 nmeta = 1 + (i64)theirs.size();
+                std::vector<double> meta(nmeta);
+                LH_CUDA(cudaMemcpyAsync(meta.data(), buf, sizeof(double) * nmeta, cudaMemcpyDeviceToHost,
+                                        ctx.stream));
+                LH_CUDA(cudaStreamSynchronize(ctx.stream));
+                LH_REQUIRE((i64)meta[0] == (i64)theirs.size(), LH_EINTERNAL, "stage from a different partition");
+                std::vector<GatherJob> jobs;
+                i64 o = nmeta;
+                for (size_t k = 0; k < theirs.size(); ++k) {
+                    const Node &nd = H.nodes[theirs[k]];
+                    const int r = (int)meta[1 + k];
+                    if (r < 0) {
+                        to_dense.push_back(theirs[k]);
+                        continue;
+                    }
+                    H.h_ranks[nd.rslot] = r;
+                    jobs.push_back({nd.uoff, o, nd.m, r, 1});
+                    o += nd.m * r;
+                    jobs.push_back({nd.voff, o, nd.n, r, 1});
+                    o += nd.n * r;
+                }
+                LH_REQUIRE(o <= S.lens[q], LH_EINTERNAL, "stage shorter than its factors");
+                run_jobs(ctx, jobs, H.d_arena, const_cast<double *>(buf));
+            }
+        }
+        LH_CUDA(cudaMemcpyAsync(H.d_ranks, H.h_ranks.data(), sizeof(int32_t) * H.nslots, cudaMemcpyHostToDevice,
+                                ctx.stream));
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cleanup();
+        build_finalize(ctx, H, src, to_dense);
+        if (stats) {
+            stats[0] = t_aca;
+            stats[1] = t_wait;
+            stats[2] = sec(tf, now());
+            stats[3] = sent;
+            stats[4] = recvd;
+        }
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+}
+
 void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg) {
     ToepSrc s{t, H.nrows};
     run_build(ctx, H, s, cfg);

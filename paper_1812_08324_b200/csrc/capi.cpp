@@ -23,6 +23,7 @@ namespace lh {
 void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA, double *tP,
                double *tM, double *sums_host);
 void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg);
+void build_toeplitz_nccl(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg, int stages, double *stats);
 void build_gauss_series(Ctx &ctx, HMat &H, const double *t, const double *xr, const double *yc,
                         double eps_sq, double scale, int fixed_rank, double delta,
                         const lh_hconfig &cfg);
@@ -438,6 +439,38 @@ int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, co
     }
     *out = o;
     return rc;
+}
+
+int lh_nccl_unique_id(void *uid128_host) {
+    return guard(nullptr, [&] { nccl_unique_id(uid128_host); });
+}
+
+int lh_nccl_init(lh_ctx *ctx, int32_t rank, int32_t world, const void *uid128_host) {
+    return guard(ctx, [&] { nccl_init(ctx->c, rank, world, uid128_host); });
+}
+
+int lh_nccl_ready(lh_ctx *ctx) { return nccl_ready(ctx->c) ? 1 : 0; }
+
+int lh_hmat_build_toeplitz_nccl(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,
+                                const lh_hconfig *cfg, int32_t stages, double *stats_host, lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        check_cfg(cfg);
+        o = new_hmat(rt, ct);
+        partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
+        build_toeplitz_nccl(ctx->c, o->h, t_dev, *cfg, stages, stats_host);
+        start_background_plans(o->h);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+int lh_bcast_factors(lh_ctx *ctx, lh_hmat *h, int32_t root) {
+    return guard(ctx, [&] { bcast_hmat(ctx->c, h->h, root); });
 }
 
 int lh_hmat_build_dense(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *A_dev,

@@ -136,6 +136,8 @@ struct HMat {
 void spill_arena(HMat &H, cudaStream_t s);
 // Brings a spilled arena back (no-op when resident); every path that reads H's arena calls it.
 void ensure_resident(HMat &H, cudaStream_t s);
+struct Ctx;
+void bcast_hmat(Ctx &ctx, HMat &H, int root);
 
 // Partition exactly as build_from_dense decides it (hmatrix.py:319-337), with every
 // admissible block with min(m,n) > n_min marked K_LR (compression decides later).
@@ -163,8 +165,20 @@ struct Ctx {
     size_t scratch_bytes = 0;
     void *ensure_scratch(size_t bytes);
     DevBuf mm[4];  // multi-RHS: X, Y (row-major), T = V^T X, chunk partials
+    std::shared_ptr<void> nccl;  // communicator (nccl.cpp: lh_nccl_init)
     ~Ctx();
 };
+
+// NCCL (nccl.cpp): communicator owned by the context
+void nccl_unique_id(void *out128);
+void nccl_init(Ctx &ctx, int rank, int world, const void *uid128);
+bool nccl_ready(Ctx &ctx);
+int nccl_rank(Ctx &ctx);
+int nccl_world(Ctx &ctx);
+cudaStream_t nccl_stream(Ctx &ctx);
+void nccl_allgather_f64(Ctx &ctx, const double *send, double *recv, size_t count, cudaStream_t s);
+void nccl_allgather_i64(Ctx &ctx, const int64_t *send, int64_t *recv, size_t count, cudaStream_t s);
+void nccl_bcast_bytes(Ctx &ctx, void *buf, size_t bytes, int root, cudaStream_t s);
 
 // device memory helpers
 template <class T>

@@ -87,3 +87,32 @@ def test_sharded_build_solves_cn(P):
     s.factor.prepare_propagator()
     u = P.run_cn(s, g["u0"], int(g["n_steps"]))
     assert np.linalg.norm(u - g["uT"]) <= 1e-8 * np.linalg.norm(g["uT"])
+
+
+@pytest.mark.parametrize("name,stages", [("cfg3_cgmy", 1), ("cfg3_cgmy_n8191", 4), ("cfg5_leaf128", 3)])
+def test_nccl_staged_build_bit_exact(P, name, stages):
+    """The library's own NCCL communicator (lh_nccl_unique_id / lh_nccl_init, one rank on this
+    GPU) and the staged, exchange-overlapped sharded build (lh_hmat_build_toeplitz_nccl): the
+    same partition, ranks and factor bits as the single-GPU build; lh_bcast_factors from rank 0
+    leaves it unchanged."""
+    ctx = P._lib.Context.get()
+    if not ctx.nccl_ready():
+        uid = (C.c_char * 128)()
+        P._lib.check(P._lib.lib().lh_nccl_unique_id(C.cast(uid, C.c_void_p)))
+        P._lib.check(P._lib.lib().lh_nccl_init(ctx.h, 0, 1, C.cast(uid, C.c_void_p)), ctx.h)
+    g = cases.load(name)
+    s = cases.make_system(name, g)
+    cfg = P.HConfig(n_min=int(g["leaf"]), eps1=float(g["eps1"]))
+    ct = s.cluster_tree(cfg.n_min)
+    full = P.build_toeplitz(s.tPlus, ct, ct, cfg)
+    st_f, val_f = _content(full, P)
+    H = P.build_toeplitz_nccl(s.tPlus, ct, ct, cfg, stages=stages)
+    assert H.shard_stats["bytes_sent"] > 0
+    for Hx in (H, P.bcast_factors(H, 0)):
+        st, val = _content(Hx, P)
+        assert np.array_equal(st, st_f)
+        for a, b in zip(val, val_f):
+            assert a[0] == b[0] and a[1] == b[1]
+            assert np.array_equal(a[2], b[2])
+            if a[3] is not None:
+                assert np.array_equal(a[3], b[3])
