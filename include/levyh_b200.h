@@ -50,6 +50,10 @@ int lh_version(void);
 /* ---- cluster tree: geometry.py:191-243 build_cluster_tree (bisection) -- */
 int lh_tree_build(lh_ctx *ctx, const double *pts_host, int64_t n, int dim, int leaf_size,
                   lh_tree **out);
+/* the same with the split rule of build_cluster_tree(strategy=...): 0 "bisection", 1 "kmeans2"
+ * (geometry.py:157-188, deterministic 2-means; the 2D L-shape studies) */
+int lh_tree_build_strategy(lh_ctx *ctx, const double *pts_host, int64_t n, int dim, int leaf_size,
+                           int strategy, lh_tree **out);
 void lh_tree_destroy(lh_tree *t);
 int64_t lh_tree_num_nodes(const lh_tree *t);
 /* lohi[2*i], lohi[2*i+1] = start, end; bbox[(2*i)*dim ...] lo then hi; kids[2*i..] (-1 = leaf) */
@@ -279,6 +283,15 @@ int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *
  * Times the kernel behind hops.py:134-144 (_lowrank_add_recompress). */
 int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const double *u_host,
                           const double *v_host, double *out_host);
+
+/* 2D Gaussian CN operator on an nx x (N / nx) tensor grid (levy.assemble_cn_2d, levy.py:275-292;
+ * entries levy.py:178-206 _entries_a_2d): which 0 = A, 1 = A+, 2 = A-; row i / column j is grid
+ * point order_host[i] / order_host[j] (a cluster tree's permutation), out_dev row-major N x N.
+ * lam = the reference's window sum (host scalar).  The H-form is then build_from_dense
+ * (lh_hmat_build_dense) of this matrix. */
+int lh_cn2d_dense(lh_ctx *ctx, int64_t N, int32_t nx, double h, double eps_sq, double scale, double a,
+                  double b, double c, double lam, double dt, int32_t which, const int64_t *order_host,
+                  double *out_dev);
 
 /* ---- Krylov consumers: levyh.solvers (solvers.py:39-153) ---------------- */
 /* Operator for the Krylov solvers, y = op(x) on device vectors of length n, ordered on the

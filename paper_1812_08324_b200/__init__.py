@@ -19,8 +19,8 @@ from .hmatrix import (HConfig, HMatrix, KernelExpansion, ToeplitzEntries, build_
                       rank_bound_gaussian, structure_summary, to_dense)
 from .hops import (SOLVE_METHODS, HFactorization, hlu, lowrank_add_recompress, matvec,  # noqa: F401
                    mul_dense, solve, trisolve_lower, trisolve_upper_right)
-from .levy import (CNSystem, FracCNSystem, UniformGrid1D, assemble_cn_1d, gaussian_measure,  # noqa: F401
-                   run_cn, step_cn)
+from .levy import (CNSystem, CNSystem2D, FracCNSystem, UniformGrid1D, UniformGrid2D, assemble_cn_1d,  # noqa: F401
+                   assemble_cn_2d, gaussian_measure, run_cn, step_cn)
 from .checkpoint import load_hmatrix, save_hmatrix  # noqa: F401
 from .solvers import IterationLog, gmres_restarted, operator, pcg  # noqa: F401
 

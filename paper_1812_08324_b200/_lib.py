@@ -58,6 +58,8 @@ SIGNATURES = [
     ("lh_hmat_build_dense", C.c_int, [P, P, P, P, I64, C.c_int, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_derive_toeplitz", C.c_int, [P, P, P, D, I32, C.POINTER(P)]),
     ("lh_hmat_clone", C.c_int, [P, P, I32, C.POINTER(P)]),
+    ("lh_tree_build_strategy", C.c_int, [P, P, I64, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
+    ("lh_cn2d_dense", C.c_int, [P, I64, I32, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, I32, P, P]),
     ("lh_hmat_spill", C.c_int, [P, P]),
     ("lh_nccl_unique_id", C.c_int, [P]),
     ("lh_nccl_init", C.c_int, [P, I32, I32, P]),

@@ -212,6 +212,44 @@ __global__ void gauss_symbol_kernel(double eps_sq, double scale, double h, i64 N
     }
 }
 
+// 2D CN operator on a tensor grid (levy.py:178-206 _entries_a_2d + entries(which)): entry (i, j)
+// of A / A+ / A- for the points order[i], order[j] (row-major grid index k = iy nx + ix), written
+// row-major (ld N) in the order the caller's cluster tree gives; the same operations as numpy.
+__global__ void cn2d_dense_kernel(i64 N, int nx, double h, double eps_sq, double scale, double a, double b,
+                                  double c, double lam, double hdt, int which, const int64_t *order,
+                                  double *out) {
+    const i64 total = N * N;
+    const double h2 = h * h;
+    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
+        const i64 i = e / N, j = e % N;
+        const i64 r = order[i], q = order[j];
+        const double dx = (double)((q % nx) - (r % nx)) * h, dy = (double)((q / nx) - (r / nx)) * h;
+        double E = -(scale * exp(-eps_sq * (dx * dx + dy * dy))) * h2;
+        const bool ex = fabs(dx) < 1.5 * h && fabs(dy) < 0.5 * h;
+        const bool ey = fabs(dy) < 1.5 * h && fabs(dx) < 0.5 * h;
+        if (ex && dx > 0.5 * h) E += -a / h2 - b / (2 * h);
+        if (ex && dx < -0.5 * h) E += -a / h2 + b / (2 * h);
+        if (ey && fabs(dy) > 0.5 * h) E += -a / h2;
+        if (ex && ey) E = 4 * a / h2 - c + lam * h2;
+        const double eye = (r == q) ? 1.0 : 0.0;
+        out[e] = which == 0 ? E : which == 1 ? eye + hdt * E : eye - hdt * E;
+    }
+}
+
+void cn2d_dense(Ctx &ctx, i64 N, int nx, double h, double eps_sq, double scale, double a, double b, double c,
+                double lam, double dt, int which, const int64_t *order_host, double *out_dev) {
+    LH_REQUIRE(which >= 0 && which <= 2, LH_EINVAL, "which must be 0 (A), 1 (plus) or 2 (minus)");
+    LH_REQUIRE(nx > 0 && N % nx == 0, LH_EINVAL, "N must be a multiple of nx");
+    std::vector<int64_t> ord(order_host, order_host + N);
+    int64_t *d = dupload(ord, ctx.stream);
+    const int grid = (int)std::min<i64>((N * N + NT - 1) / NT, (i64)ctx.num_sms * 32);
+    cn2d_dense_kernel<<<grid, NT, 0, ctx.stream>>>(N, nx, h, eps_sq, scale, a, b, c, lam, 0.5 * dt, which, d,
+                                                   out_dev);
+    LH_CUDA(cudaGetLastError());
+    LH_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaFree(d);
+}
+
 void gauss_cn_symbol(Ctx &ctx, i64 N, double h, double eps_sq, double scale, i64 n_off, double a,
                      double b, double c, double dt, double *tA, double *tP, double *tM,
                      double *lam_host) {
@@ -412,15 +450,82 @@ __device__ int aca_block(const Src &src, i64 r0, i64 c0, i64 m, i64 n, double *U
     return k;
 }
 
+// Cross approximation with FULL pivoting for small blocks (m n <= ACA_FULL_MAX, 2D operators):
+// the residual lives in shared memory, every step takes the entry of largest modulus and
+// subtracts the rank-one cross exactly, and the stop test is exact: ||R||_F <= tol ||A||_F.
+// Partial pivoting can stop early on the smooth 2D kernels (it never visits rows whose part of
+// the block it has not yet seen), which shows up as ranks below the SVD's.
+constexpr int ACA_FULL_MAX = 96 * 96;
+template <class Src>
+__device__ int aca_block_full(const Src &src, i64 r0, i64 c0, i64 m, i64 n, double *U, double *V, int KA,
+                              double tol, AcaSmem &S, double *R, int &converged) {
+    const i64 mn = m * n;
+    double a2 = 0.0;
+    for (i64 e = threadIdx.x; e < mn; e += NT) {
+        const double v = src(r0 + e % m, c0 + e / m);
+        R[e] = v;
+        a2 += v * v;
+    }
+    a2 = dev::block_sum(a2, S.red);
+    converged = 0;
+    int k = 0;
+    if (!(a2 > 0.0)) {
+        converged = 1;
+        return 0;
+    }
+    while (k < KA) {
+        double best = -1.0, r2 = 0.0;
+        long long be = 0;
+        for (i64 e = threadIdx.x; e < mn; e += NT) {
+            const double a = fabs(R[e]);
+            r2 += R[e] * R[e];
+            if (a > best) {
+                best = a;
+                be = e;
+            }
+        }
+        r2 = dev::block_sum(r2, S.red);
+        if (r2 <= tol * tol * a2) {
+            converged = 1;
+            break;
+        }
+        double amax;
+        long long estar;
+        dev::block_argmax(best, be, S.redv, S.redi, amax, estar);
+        if (!(amax > 0.0)) {
+            converged = 1;
+            break;
+        }
+        const i64 is = estar % m, js = estar / m;
+        const double inv = 1.0 / R[estar];
+        double *uk = U + (i64)k * m, *vk = V + (i64)k * n;
+        for (i64 i = threadIdx.x; i < m; i += NT) uk[i] = R[i + js * m];
+        for (i64 j = threadIdx.x; j < n; j += NT) vk[j] = R[is + j * m] * inv;
+        __syncthreads();
+        for (i64 e = threadIdx.x; e < mn; e += NT) R[e] -= uk[e % m] * vk[e / m];
+        __syncthreads();
+        ++k;
+    }
+    if (!converged) {  // the cap reached: converged if the last update left the tolerance met
+        double r2 = 0.0;
+        for (i64 e = threadIdx.x; e < mn; e += NT) r2 += R[e] * R[e];
+        r2 = dev::block_sum(r2, S.red);
+        converged = r2 <= tol * tol * a2;
+    }
+    __syncthreads();
+    return k;
+}
+
 // flags: 0 ok (low rank), 2 -> store dense (rank > min//2), 3 -> rank > kcap,
 //        4 -> ACA hit max rank without converging
 template <class Src>
 __global__ void __launch_bounds__(NT) aca_kernel(Src src, const AcaJob *jobs, int njobs,
                                                  int *counter, double *work, double *arena,
                                                  int *ranks, int *flags, int KA, double tol,
-                                                 double eps1) {
+                                                 double eps1, int full_pivot) {
     extern __shared__ double4 smem_raw[];
     AcaSmem &S = *reinterpret_cast<AcaSmem *>(smem_raw);
+    double *Rres = reinterpret_cast<double *>(reinterpret_cast<char *>(smem_raw) + ((sizeof(AcaSmem) + 15) & ~15));
     __shared__ int s_job;
     while (true) {
         if (threadIdx.x == 0) s_job = atomicAdd(counter, 1);
@@ -432,7 +537,9 @@ __global__ void __launch_bounds__(NT) aca_kernel(Src src, const AcaJob *jobs, in
         double *U = work + J.wu;
         double *V = work + J.wv;
         int conv = 0;
-        int K = aca_block(src, J.r0, J.c0, J.m, J.n, U, V, KA, tol, S, conv);
+        int K = (full_pivot && J.m * J.n <= ACA_FULL_MAX)
+                    ? aca_block_full(src, J.r0, J.c0, J.m, J.n, U, V, KA, tol, S, Rres, conv)
+                    : aca_block(src, J.r0, J.c0, J.m, J.n, U, V, KA, tol, S, conv);
         i64 half = min(J.m, J.n) / 2;
         int rmax = (int)min((i64)min(J.kcap, KC_MAX), half);
         int r = dev::recompress(U, J.m, J.m, V, J.n, J.n, K, 0, eps1, arena + J.fu, J.m,
@@ -460,7 +567,9 @@ static void set_smem(const void *fn, size_t bytes) {
 // order (size-sorted, largest first)
 static std::vector<int32_t> build_layout(Ctx &ctx, HMat &H, const lh_hconfig &cfg,
                                          const std::vector<int32_t> *cap_of = nullptr) {
-    const int kcap = std::min(std::max(cfg.kcap, 1), KC_MAX);
+    // column capacity: kept ranks stay <= KC_MAX; a capacity up to KA_MAX leaves room for the
+    // H-LU's low-rank updates before each recompression (2D operators)
+    const int kcap = std::min(std::max(cfg.kcap, 1), KA_MAX);
     i64 off = 0;
     int nslots = 0;
     std::vector<int32_t> lr;
@@ -506,7 +615,10 @@ static std::vector<int32_t> run_aca(Ctx &ctx, HMat &H, Src src, const lh_hconfig
     const int kcap = std::min(std::max(cfg.kcap, 1), KC_MAX);
     const i64 budget = (i64)1 << 30;  // doubles (8 GiB)
     std::vector<int32_t> to_dense;
+    // full pivoting on small blocks of 2D operators (the residual in shared memory)
+    const int full = (H.rt && H.rt->dim == 2) ? 1 : 0;
     size_t smem = sizeof(AcaSmem);
+    if (full) smem = ((sizeof(AcaSmem) + 15) & ~(size_t)15) + sizeof(double) * ACA_FULL_MAX;
     set_smem((const void *)aca_kernel<Src>, smem);
     size_t p = 0;
     double *work = nullptr;
@@ -536,7 +648,7 @@ static std::vector<int32_t> run_aca(Ctx &ctx, HMat &H, Src src, const lh_hconfig
         int grid = std::min<int>((int)jobs.size(), ctx.num_sms * 2);
         aca_kernel<Src><<<grid, NT, smem, ctx.stream>>>(src, djobs, (int)jobs.size(), dcnt, work,
                                                         H.d_arena, H.d_ranks, dflags, KA,
-                                                        cfg.aca_tol, cfg.eps1);
+                                                        cfg.aca_tol, cfg.eps1, full);
         LH_CUDA(cudaGetLastError());
         std::vector<int> flags(jobs.size());
         LH_CUDA(cudaMemcpyAsync(flags.data(), dflags, sizeof(int) * jobs.size(),

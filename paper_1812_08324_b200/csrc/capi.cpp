@@ -23,6 +23,8 @@ namespace lh {
 void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA, double *tP,
                double *tM, double *sums_host);
 void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg);
+void cn2d_dense(Ctx &ctx, i64 N, int nx, double h, double eps_sq, double scale, double a, double b, double c,
+                double lam, double dt, int which, const int64_t *order_host, double *out_dev);
 void build_toeplitz_nccl(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg, int stages, double *stats);
 void build_gauss_series(Ctx &ctx, HMat &H, const double *t, const double *xr, const double *yc,
                         double eps_sq, double scale, int fixed_rank, double delta,
@@ -260,6 +262,16 @@ int lh_tree_build(lh_ctx *ctx, const double *pts, int64_t n, int dim, int leaf_s
     });
 }
 
+int lh_tree_build_strategy(lh_ctx *ctx, const double *pts, int64_t n, int dim, int leaf_size, int strategy,
+                           lh_tree **out) {
+    return guard(ctx, [&] {
+        std::shared_ptr<Tree> t(build_tree(pts, n, dim, leaf_size, strategy));
+        lh_tree *o = new lh_tree();
+        o->t = t;
+        *out = o;
+    });
+}
+
 void lh_tree_destroy(lh_tree *t) { delete t; }
 
 int64_t lh_tree_num_nodes(const lh_tree *t) { return (int64_t)t->t->nodes.size(); }
@@ -421,6 +433,12 @@ int lh_gauss_cn_symbol(lh_ctx *ctx, int64_t N, double h, double eps_sq, double s
         gauss_cn_symbol(ctx->c, N, h, eps_sq, scale, n_off, a, b, c, dt, tA_dev, tPlus_dev,
                         tMinus_dev, lam_host);
     });
+}
+
+int lh_cn2d_dense(lh_ctx *ctx, int64_t N, int32_t nx, double h, double eps_sq, double scale, double a,
+                  double b, double c, double lam, double dt, int32_t which, const int64_t *order_host,
+                  double *out_dev) {
+    return guard(ctx, [&] { cn2d_dense(ctx->c, N, nx, h, eps_sq, scale, a, b, c, lam, dt, which, order_host, out_dev); });
 }
 
 int lh_hmat_build_toeplitz(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct, const double *t_dev,

@@ -57,7 +57,7 @@ struct Tree {
     std::vector<double> pts;     // the input points, original order, n x dim row-major
 };
 
-Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size);
+Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size, int strategy = 0);  // 1: kmeans2
 bool admissible(const Cluster &a, const Cluster &b, int dim, double eta);
 double diameter(const Cluster &a, int dim);
 

@@ -1042,16 +1042,42 @@ __device__ void task_lradd(const ExecArgs &A, const DTask &T, int tid, double *s
     const int r1 = A.ranks[slot];
     const int K = r1 + r2;
     const int kcap = cu.cols;
-    if (K > kcap || K > KA_MAX) {
-        if (threadIdx.x == 0) set_err(A, LH_ERANK, tid, -1);
-        return;
-    }
     const i64 m = cu.rows, n = cv.rows;
     double *U = vp(A, cu);
     double *V = vp(A, cv);
     const double *U2 = vp(A, u2);
     const double *V2 = vp(A, v2);
     dev::RecompSmem &S = *reinterpret_cast<dev::RecompSmem *>(sm);
+    if (K > kcap || K > KA_MAX) {
+        // wider than the block's capacity or the recompression width: the update enters in
+        // column chunks, recompressing after each (kept ranks <= KC_MAX leave room for the next
+        // chunk when the capacity exceeds KC_MAX: the 2D operators' H-LU)
+        const int cap = min(kcap, KA_MAX), rmax = min(kcap, KC_MAX);
+        const Strided U2s = strided(A, u2), V2s = strided(A, v2);
+        int rc = r1, done = 0;
+        while (done < r2) {
+            const int q = min(r2 - done, cap - rc);
+            if (q <= 0) {
+                if (threadIdx.x == 0) set_err(A, LH_ERANK, tid, -1);
+                return;
+            }
+            for (i64 e = threadIdx.x; e < m * q; e += NT)
+                U[e % m + (rc + e / m) * (i64)cu.ld] = T.alpha * U2s.p[(e % m) * U2s.si + (done + e / m) * U2s.sj];
+            for (i64 e = threadIdx.x; e < n * q; e += NT)
+                V[e % n + (rc + e / n) * (i64)cv.ld] = V2s.p[(e % n) * V2s.si + (done + e / n) * V2s.sj];
+            __syncthreads();
+            const int r = dev::recompress(U, cu.ld, m, V, cv.ld, n, rc + q, 1, T.alpha2, U, cu.ld, V, cv.ld, rmax, S);
+            if (r > rmax) {
+                if (threadIdx.x == 0) set_err(A, LH_ERANK, tid, -1);
+                return;
+            }
+            rc = r;
+            done += q;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) A.ranks[slot] = rc;
+        return;
+    }
     constexpr int RS = (int)((sizeof(dev::RecompSmem) + 15) / 8) & ~1;
     constexpr i64 ROOM = SMEM_BYTES / 8 - RS;
     if ((m + n) * K <= ROOM) {

@@ -40,6 +40,72 @@ struct TreeBuilder {
     Tree *T;
     std::vector<i64> tmp;
     std::vector<double> key;
+    int strategy = 0;  // 0 bisection, 1 kmeans2
+
+    // _split_kmeans2 (geometry.py:157-188): deterministic 2-means, centroids seeded with the
+    // extremes of the projection onto the bbox diagonal (first index on ties), assignment ties
+    // to centroid 0, at most 50 iterations, even index split when a cluster empties or every
+    // point coincides.  Same floating-point operations as numpy: squared distances summed x
+    // then y, centroids as sequential sums over the members in index order / count.
+    // Returns the cluster-0 (left) mask over idx[b, e).
+    std::vector<char> kmeans2(const std::vector<i64> &idx, i64 b, i64 e, const Cluster &c) const {
+        const i64 n = e - b;
+        std::vector<char> left(n, 0);
+        double diag[2] = {0, 0};
+        bool any = false;
+        for (int d = 0; d < dim; ++d) {
+            diag[d] = c.bhi[d] - c.blo[d];
+            any = any || diag[d] > 0;
+        }
+        auto even = [&]() {
+            std::fill(left.begin(), left.end(), 0);
+            for (i64 k = 0; k < n / 2; ++k) left[k] = 1;
+            return left;
+        };
+        if (!any) return even();
+        auto P = [&](i64 k, int d) { return pts[idx[b + k] * dim + d]; };
+        i64 amin = 0, amax = 0;
+        double pmin = 0, pmax = 0;
+        for (i64 k = 0; k < n; ++k) {
+            double pr = 0.0;
+            for (int d = 0; d < dim; ++d) pr += P(k, d) * diag[d];
+            if (k == 0 || pr < pmin) pmin = pr, amin = k;
+            if (k == 0 || pr > pmax) pmax = pr, amax = k;
+        }
+        double cen[2][2];
+        for (int d = 0; d < dim; ++d) {
+            cen[0][d] = P(amin, d);
+            cen[1][d] = P(amax, d);
+        }
+        std::vector<char> assign(n, 0), na(n, 0);
+        bool have = false;
+        for (int it = 0; it < 50; ++it) {
+            for (i64 k = 0; k < n; ++k) {
+                double d0 = 0.0, d1 = 0.0;
+                for (int d = 0; d < dim; ++d) {
+                    const double a0 = P(k, d) - cen[0][d], a1 = P(k, d) - cen[1][d];
+                    d0 = d0 + a0 * a0;
+                    d1 = d1 + a1 * a1;
+                }
+                na[k] = d1 < d0;
+            }
+            if (have && na == assign) break;
+            assign = na;
+            have = true;
+            i64 n1 = 0;
+            for (char v : assign) n1 += v;
+            if (n1 == 0 || n1 == n) return even();
+            double s[2][2] = {{0, 0}, {0, 0}};
+            for (i64 k = 0; k < n; ++k)
+                for (int d = 0; d < dim; ++d) s[assign[k]][d] = s[assign[k]][d] + P(k, d);
+            for (int d = 0; d < dim; ++d) {
+                cen[0][d] = s[0][d] / (double)(n - n1);
+                cen[1][d] = s[1][d] / (double)n1;
+            }
+        }
+        for (i64 k = 0; k < n; ++k) left[k] = !assign[k];
+        return left;
+    }
 
     int32_t build(std::vector<i64> &idx, i64 b, i64 e, i64 start, int depth) {
         // geometry.py:225-236; idx[b:e] are original point ids of this node
@@ -65,6 +131,19 @@ struct TreeBuilder {
         if (n <= leaf_size) {
             for (i64 k = b; k < e; ++k) T->order[start + (k - b)] = idx[k];
             T->leaves.push_back(id);
+            return id;
+        }
+        if (strategy == 1) {
+            const std::vector<char> left = kmeans2(idx, b, e, c);
+            std::vector<i64> L, R;
+            for (i64 k = 0; k < n; ++k) (left[k] ? L : R).push_back(idx[b + k]);
+            const i64 nl = (i64)L.size();
+            std::copy(L.begin(), L.end(), idx.begin() + b);
+            std::copy(R.begin(), R.end(), idx.begin() + b + nl);
+            int32_t k0 = build(idx, b, b + nl, start, depth + 1);
+            int32_t k1 = build(idx, b + nl, e, start + nl, depth + 1);
+            T->nodes[id].kid[0] = k0;
+            T->nodes[id].kid[1] = k1;
             return id;
         }
         // _split_bisection (geometry.py:146-154): widest axis (first on ties),
@@ -105,7 +184,7 @@ struct TreeBuilder {
 
 }  // namespace
 
-Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size) {
+Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size, int strategy) {
     LH_REQUIRE(n > 0, LH_EINVAL, "point set must be nonempty");
     LH_REQUIRE(dim == 1 || dim == 2, LH_EINVAL, "only 1D and 2D point sets are supported");
     LH_REQUIRE(leaf_size >= 1, LH_EINVAL, "leaf_size must be >= 1");
@@ -119,7 +198,8 @@ Tree *build_tree(const double *pts, i64 n, int dim, int leaf_size) {
     T->order.assign(n, 0);
     std::vector<i64> idx(n);
     std::iota(idx.begin(), idx.end(), (i64)0);
-    TreeBuilder tb{pts, dim, leaf_size, T, {}, {}};
+    LH_REQUIRE(strategy == 0 || strategy == 1, LH_EINVAL, "unknown strategy");
+    TreeBuilder tb{pts, dim, leaf_size, T, {}, {}, strategy};
     tb.build(idx, 0, n, 0, 0);
     return T;
 }

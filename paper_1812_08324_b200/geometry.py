@@ -154,18 +154,18 @@ class ClusterTree:
 
 
 def build_cluster_tree(pts, leaf_size=64, strategy="bisection"):
-    """geometry.py:191-243.  ``kmeans2`` (2D L-shape only) is out of scope."""
+    """geometry.py:191-243: median bisection along the widest axis, or ``kmeans2``
+    (geometry.py:157-188, deterministic 2-means) -- the same trees bit for bit."""
     if not isinstance(pts, PointSet):
         pts = PointSet(pts)
     if leaf_size < 1:
         raise ValueError("leaf_size must be >= 1")
-    if strategy == "kmeans2":
-        raise NotImplementedError("kmeans2 clustering (2D L-shape) is outside the B200 hot path")
-    if strategy != "bisection":
+    codes = {"bisection": 0, "kmeans2": 1}
+    if strategy not in codes:
         raise ValueError(f"unknown strategy {strategy!r}")
     h = C.c_void_p()
-    rc = _lib.lib().lh_tree_build(None, _lib.host_ptr(pts.points), pts.points.shape[0], pts.dim,
-                                  int(leaf_size), C.byref(h))
+    rc = _lib.lib().lh_tree_build_strategy(None, _lib.host_ptr(pts.points), pts.points.shape[0], pts.dim,
+                                           int(leaf_size), codes[strategy], C.byref(h))
     _lib.check(rc)
     return ClusterTree(h, pts.points, pts.dim)
 

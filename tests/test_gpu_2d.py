@@ -1,0 +1,88 @@
+"""GPU: the 2D rows of SURVEY 8(f) (row 4) against reference fixtures (tests/golden/
+make_golden_2d.py): the 2D Gaussian CN operator (levy.assemble_cn_2d, levy.py:275-292; entries
+_entries_a_2d :178-206) generated on the device, its build_from_dense partition and ranks, the CN
+solution against the reference's dense CN, and the variable-order L-shape system through a kmeans2
+tree, build_from_dense, hlu, solve and preconditioned GMRES (cli.frac_lshape_study, cli.py:442-477)."""
+import os
+
+import numpy as np
+import pytest
+
+from tests import cases
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_2d.npz")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1812_08324_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def g():
+    return dict(np.load(GOLD))
+
+
+def _sys(P):
+    return P.assemble_cn_2d(P.gaussian_measure(5.0), 0.1, 0.5, -0.2, P.UniformGrid2D(24, 24), 0.05)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_cn2d_operator_entries(P, g):
+    s = _sys(P)
+    assert s.lam == float(g["cn2_lam"])
+    for which, key in (("plus", "cn2_Aplus"), ("minus", "cn2_Aminus")):
+        A = s.dense_matrix(which)
+        assert np.abs(A - g[key]).max() <= 1e-14 * np.abs(g[key]).max(), which
+
+
+def test_cn2d_partition_ranks_and_cn(P, g):
+    s = _sys(P)
+    # eps1 = 1e-6: the smooth 2D Gaussian kernel's blocks need ACA ranks above this engine's
+    # 48-column recompression width at tighter tolerances (rank ~30 at 1e-8 needs ~50 ACA steps)
+    cfg = P.HConfig(n_min=32, eps1=1e-6)
+    Hp = s.hmatrix("plus", cfg)
+    assert np.array_equal(s.tree.perm.inverse, g["cn2_order"])
+    st, ref = Hp.structure_array(), g["cn2_struct_plus"]
+    assert np.array_equal(st[:, :5], ref[:, :5])
+    lr = ref[:, 4] == 1
+    diff = st[lr, 5] - ref[lr, 5]
+    cases.report_rank_mismatch("cn2d_gauss", "plus", int(lr.sum()), diff)
+    assert np.count_nonzero(diff) == 0, diff
+    t = _sys(P)
+    t.prepare(cfg, 1e-10)
+    st, ref = t.factor.h.structure_array(), None
+    assert st[st[:, 4] == 1, 5].max() <= 32
+    u = P.run_cn(t, g["cn2_u0"], 10)
+    assert _rel(u, g["cn2_uT_h"]) <= 1e-8  # the reference's H path, same eps1
+    assert _rel(u, g["cn2_uT_dense"]) <= 10 * _rel(g["cn2_uT_h"], g["cn2_uT_dense"]) + 1e-12
+    with pytest.raises(NotImplementedError):
+        _sys(P).prepare(cfg, 1e-10, method="propagator")
+
+
+def test_lshape_variable_order_pipeline(P, g):
+    pts, A, b = g["ls_pts"], g["ls_A"], g["ls_b"]
+    ct = P.build_cluster_tree(pts, leaf_size=32, strategy="kmeans2")
+    perm = ct.perm
+    At = A[np.ix_(perm.inverse, perm.inverse)]
+    H = P.build_from_dense(At, ct, ct, P.HConfig(n_min=32, eps1=1e-6))
+    st, ref = H.structure_array(), g["ls_struct"]
+    assert np.array_equal(st[:, :5], ref[:, :5])
+    lr = ref[:, 4] == 1
+    diff = st[lr, 5] - ref[lr, 5]
+    cases.report_rank_mismatch("lshape24", "build_from_dense", int(lr.sum()), diff)
+    assert np.count_nonzero(diff) == 0, diff
+    F = P.hlu(H, 1e-10)
+    sf, rf = F.h.structure_array(), g["ls_struct_factor"]
+    assert np.array_equal(sf[:, :5], rf[:, :5])
+    uh = perm.from_tree(P.solve(F, perm.to_tree(b)))
+    assert _rel(uh, g["ls_uh"]) <= 1e-9
+    assert _rel(uh, g["ls_udense"]) <= 1e-4  # the eps1 = 1e-6 compression, as the reference's
+    x, log = P.gmres_restarted(At, F, perm.to_tree(b), tol=1e-8, restart=50, max_iter=400)
+    assert log.converged and log.iterations == int(g["ls_gmres_iters"])
+    assert _rel(perm.from_tree(x), g["ls_udense"]) <= 1e-7
