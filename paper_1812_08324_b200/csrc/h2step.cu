@@ -65,20 +65,29 @@ __device__ __forceinline__ void bulk_ef(void *dst, uint64_t src, uint32_t bytes,
         "l"(src), "r"(bytes), "r"(saddr(bar)), "l"(pol)
         : "memory");
 }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, %0;" ::"n"(CONS_T) : "memory"); }
 
 // producer: lane 0 of warp 0 streams the chunks [c0, c1) through the ring
 __device__ __forceinline__ bool skipped(const H2SChunk &C, int skip) {
     return ((skip & 1) && C.type == C_DENSE) || ((skip & 2) && (C.type == C_LEAF || C.type == C_ULVL));
 }
+// wait_types: chunk types whose operands the previous kernel writes (programmatic dependent
+// launch: griddepcontrol.wait before the first of them; the others stream ahead)
 __device__ __forceinline__ void produce(const H2SChunk *ch, int nch, unsigned char *ring, uint64_t *full,
-                                        uint64_t *empty, int skip = 0) {
+                                        uint64_t *empty, int skip = 0, int wait_types = 0) {
     int stage = 0;
     uint32_t phase = 0;
+    bool waited = wait_types == 0;
     const uint64_t pol = evict_first_policy();
     for (int c = 0; c < nch; ++c) {
         const H2SChunk &C = ch[c];
         if (skipped(C, skip)) continue;
+        if (!waited && ((wait_types >> C.type) & 1)) {
+            pdl_wait();
+            waited = true;
+        }
         mb_wait(&empty[stage], phase ^ 1);
         uint32_t tot = 0;
         for (int i = 0; i < C.ncopy; ++i) tot += (uint32_t)C.bytes[i];
@@ -179,6 +188,7 @@ __global__ void __launch_bounds__(CONS_T + 64, 1) h2s_up_kernel(K1Args A) {
     const H2SLeaf *lfs = reinterpret_cast<const H2SLeaf *>(chs + nch);
     const H2SUp *ups = reinterpret_cast<const H2SUp *>(lfs + nl);
     const unsigned long long tstart = A.trace ? gtime() : 0;
+    pdl_trigger();  // K2 may launch onto SMs this kernel frees (it waits for x_hat and yd itself)
     {
         const DSlice sl[3] = {{A.ch + c0, nch * (int)sizeof(H2SChunk)},
                               {A.leaf + l0, nl * (int)sizeof(H2SLeaf)},
@@ -395,10 +405,13 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
         preload(desc, sl, dbar);
     }
     if (warp == 0) {
-        if (lane == 0) produce(chs, nch, ring, full, empty);
+        // the coupling matrices, transfers and row bases do not depend on K1: they stream while
+        // K1 finishes; the row chunks carry yd (written by K1) and wait for it
+        if (lane == 0) produce(chs, nch, ring, full, empty, 0, 1 << C_Q);
         return;
     }
     const int cw = warp - 1, ct = threadIdx.x - 32;
+    pdl_wait();  // x_hat (K1) before the first coupling gather
     // the x_hat the couplings read were written by K1 early and have since been pushed out of
     // L2 by K1's dense stream: bring them back for the whole CTA at once (one DRAM latency
     // instead of one per chunk of coupling products)
@@ -1237,7 +1250,19 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     K2Args a2{S.c2, S.cb2, S.nb2, S.eb2, S.pb2, S.db2, S.qb2, S.cn, S.ce, S.path, S.dn, S.q, h.xh,
               S.wsmax, S.ysmax, z, y, alpha, beta, zmode, a1.trace ? a1.trace + (size_t)S.G * 8 : nullptr,
               (dbg >> 5) & 15};
-    if (!(dbg & 2)) h2s_down_kernel<<<S.G, CONS_T + 32, S.smem2, s>>>(a2);
+    if (!(dbg & 2)) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(S.G);
+        cfg.blockDim = dim3(CONS_T + 32);
+        cfg.dynamicSmemBytes = S.smem2;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = getenv("LEVYH_NO_PDL") ? 0 : 1;
+        LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel, a2));
+    }
     if (ev) LH_CUDA(cudaEventRecord(ev[2], s));
     LH_CUDA(cudaGetLastError());
     if (a1.trace && !getenv("LEVYH_H2S_TRACE_DONE")) {
