@@ -646,10 +646,18 @@ void run_gather(const std::vector<CopyJob2> &jobs, const double *src, double *ds
 
 }  // namespace
 
+static bool h2s_fail(const char *why) {
+    if (getenv("LEVYH_PLAN_VERBOSE")) fprintf(stderr, "[levyh] H2 step kernels not built: %s\n", why);
+    return false;
+}
+
 bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     if (getenv("LEVYH_H2_V1")) return false;
     auto S = std::make_shared<H2S>();
-    const int G = num_sms;
+    // one CTA per SM; with more than two subtrees per SM (N = 2^22), whole waves of CTAs with
+    // about one subtree each (a CTA's descriptors and walk slots must fit its shared memory)
+    const int nsub = std::max(in.nsub_up, in.nsub_dn);
+    const int G = nsub <= 2 * num_sms ? num_sms : num_sms * ((nsub + num_sms - 1) / num_sms);
     const i64 SLOT = H2S_SLOTB;
     S->G = G;
     S->n = in.n;
@@ -696,7 +704,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                     pb = pnew;
                     ++lb;
                 }
-                if (lb == la) return false;
+                if (lb == la) return h2s_fail("a leaf basis run above one ring slot");
                 const H2Leaf &F = (*in.leaves)[la], &E = (*in.leaves)[lb - 1];
                 Cut k;
                 start(k, C_LEAF, (int)lf.size());
@@ -728,7 +736,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                 for (int u = a; u < e; ++u) {
                     const H2Up &U = (*in.ups)[u];
                     const i64 tb = 8 * (i64)(U.k1 + U.k2) * U.k;
-                    if (tb + 32 > SLOT) return false;
+                    if (tb + 32 > SLOT) return h2s_fail("a column transfer above one ring slot");
                     if (k.c.a < k.c.b && !fits(k, tb, merges(k, (uint64_t)(uintptr_t)(in.tu + U.toff)) ? 0 : 1)) {
                         push(k);
                         start(k, C_ULVL, (int)upv.size());
@@ -798,7 +806,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
             const int ld = D.ld;
             for (int bb = D.bbeg; bb < D.bend; ++bb) {
                 const SBatch &B = in.batches[bb];
-                if (B.K != B.kd) return false;  // a dense-only plan is expected
+                if (B.K != B.kd) return h2s_fail("dense plan batch with low-rank columns");  // a dense-only plan is expected
                 H2SChunk c{};
                 c.type = C_DENSE;
                 c.a = (int32_t)D.y0;
@@ -808,7 +816,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                 c.e2 = B.xadj;
                 c.flags = (bb == D.bbeg ? F_SEGFIRST : 0) | (bb + 1 == D.bend ? F_SEGLAST : 0);
                 const i64 db = 8 * (i64)B.K * ld, xb = 8 * even(B.xadj + B.kd);
-                if (db > 40960 || xb > 1024 || (B.src & 1) || (B.xsrc & 1)) return false;
+                if (db > 40960 || xb > 1024 || (B.src & 1) || (B.xsrc & 1)) return h2s_fail("dense batch above the slot layout");
                 c.ncopy = 2;
                 c.src[0] = (uint64_t)(uintptr_t)(in.pbuf + B.src);
                 c.bytes[0] = (int32_t)((db + 15) & ~(i64)15);
@@ -923,7 +931,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                 qb = qn;
                 ++e;
             }
-            if (e == l) return false;
+            if (e == l) return h2s_fail("a row-leaf run above one ring slot");
             Cut k;
             start(k, C_Q, (int)qv.size());
             if (newlvl && firstc) k.c.flags = F_NEWLVL;
@@ -932,7 +940,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
             for (size_t t = l; t < e; ++t)
                 if (in.rleaf[t].k > 0) {
                     if (q0 < 0) q0 = in.rleaf[t].qoff;
-                    if (qend >= 0 && in.rleaf[t].qoff != qend) return false;  // Q not contiguous
+                    if (qend >= 0 && in.rleaf[t].qoff != qend) return h2s_fail("row bases not contiguous");  // Q not contiguous
                     qend = in.rleaf[t].qoff + in.rleaf[t].rows * in.rleaf[t].k;
                 }
             const int qbase = q0 >= 0 ? add_copy(k, in.zarena + q0, 8 * (qend - q0)) : 0;
@@ -995,10 +1003,10 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                     sbytes += 8 * (i64)(*in.cpls)[e].kr * (*in.cpls)[e].kc;
                     kcs += (*in.cpls)[e].kc;
                 }
-                if (sbytes + 32 > SLOT || D.k > 255) return false;
+                if (sbytes + 32 > SLOT || D.k > 255) return h2s_fail("a coupling node above one slot");
                 const double *src = sb2 + O.sbeg[t];
                 const bool mg = merges(k, (uint64_t)(uintptr_t)src);
-                if (kcs > H2S_XG) return false;
+                if (kcs > H2S_XG) return h2s_fail("a coupling node's x_hat above the gather buffer");
                 if (k.c.a < k.c.b && (!fits(k, sbytes, mg ? 0 : 1) || xcnt + kcs > H2S_XG)) {
                     cpl_done(k);
                     push(k);
@@ -1037,7 +1045,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                 const i64 t = O.path_t[q];
                 if (t >= 0) {
                     const i64 tb = 8 * (i64)D.ldt * D.kp;
-                    if (tb + 32 > SLOT) return false;
+                    if (tb + 32 > SLOT) return h2s_fail("a path transfer above one ring slot");
                     if (k.c.a < k.c.b && !fits(k, tb, merges(k, (uint64_t)(uintptr_t)(td2 + t)) ? 0 : 1)) {
                         push(k);
                         start(k, C_PATH, (int)pv.size());
@@ -1068,7 +1076,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                     const i64 t = O.lvl_t[d][u - a];
                     if (t >= 0) {
                         const i64 tb = 8 * (i64)D.ldt * D.kp;
-                        if (tb + 32 > SLOT) return false;
+                        if (tb + 32 > SLOT) return h2s_fail("a row transfer above one ring slot");
                         if (t != last_t) {
                             if (k.c.a < k.c.b && !fits(k, tb, merges(k, (uint64_t)(uintptr_t)(td2 + t)) ? 0 : 1)) {
                                 push(k);
@@ -1096,8 +1104,8 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
             size_t lb = la;
             while (lb < in.rleaf.size() && in.rleaf[lb].r0 < hi) ++lb;
             for (size_t l = la; l < lb; ++l)
-                if (in.rleaf[l].k > 0 && in.rleaf[l].sub != s) return false;
-            if (!q_chunks(b, la, lb, true)) return false;
+                if (in.rleaf[l].k > 0 && in.rleaf[l].sub != s) return h2s_fail("a row leaf outside its subtree");
+            if (!q_chunks(b, la, lb, true)) return h2s_fail("row chunks");
         }
     }
     // row leaves outside every row subtree (no basis): to the least-loaded CTAs
@@ -1106,11 +1114,11 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
             ++l;
             continue;
         }
-        if (in.rleaf[l].k > 0) return false;
+        if (in.rleaf[l].k > 0) return h2s_fail("a leftover row leaf with a basis");
         size_t e = l;
         while (e < in.rleaf.size() && !leaf_done[e] && e - l < 32) ++e;
         const int b = (int)(std::min_element(k2bytes.begin(), k2bytes.end()) - k2bytes.begin());
-        if (!q_chunks(b, l, e, false)) return false;
+        if (!q_chunks(b, l, e, false)) return h2s_fail("leftover row chunks");
         l = e;
     }
     // K2 items are appended CTA by CTA except the leftover leaves' Q items (appended last):
@@ -1184,7 +1192,12 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     int maxsm = 0, dev_id = 0;
     cudaGetDevice(&dev_id);
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id);
-    if (S->smem1 > maxsm || S->smem2 > maxsm) return false;
+    if (S->smem1 > maxsm || S->smem2 > maxsm) {
+        if (getenv("LEVYH_PLAN_VERBOSE"))
+            fprintf(stderr, "[levyh] H2 step smem %d / %d B (x_hat %d, w %d, y %d doubles; descriptors %d / %d B), limit %d\n",
+                    S->smem1, S->smem2, S->xsmax, S->wsmax, S->ysmax, S->desc1, S->desc2, maxsm);
+        return h2s_fail("shared memory above the opt-in limit");
+    }
     S->c1 = dupload(ch1, st);
     S->c2 = dupload(ch2, st);
     S->cb1 = dupload(cb1, st);

@@ -2083,6 +2083,7 @@ bool build_shared_basis(Ctx &ctx, HMat &Z, double eps, HMat &ZS, std::shared_ptr
                         double *stats);
 bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_ptr<MvPlan> &plan,
               double *stats);
+std::shared_ptr<Tree> refine_tree_leaves(const Tree &T, int maxleaf);
 
 // relative 2-norm difference of two matvec plans of the same operator on a seeded probe vector
 static double probe_rel_err(Ctx &ctx, const MvPlan &Pa, HMat &Ha, const MvPlan &Pb, HMat &Hb) {
@@ -2359,7 +2360,36 @@ void prepare_propagator(Ctx &ctx, HMat &F, double eps2) {
         const int split = getenv("LEVYH_H2_SPLIT") ? atoi(getenv("LEVYH_H2_SPLIT")) : -1;  // -1: automatic
         auto zs = std::make_shared<HMat>();
         std::shared_ptr<MvPlan> pz;
-        if (build_h2(ctx, *Z, sb_eps, split, *zs, pz, S.zs_stats)) {
+        // leaves above 64 rows (cfg5's 128): the nested bases are built on copies of the cluster
+        // trees with those leaves split at 64 rows (Z's blocks keep their clusters)
+        bool big = false;
+        for (const Tree *T : {Z->rt, Z->ct})
+            for (int32_t lc : T->leaves) big = big || T->nodes[lc].size() > 64;
+        const Tree *rt0 = Z->rt, *ct0 = Z->ct;
+        auto rh0 = Z->rt_hold, ch0 = Z->ct_hold;
+        if (big && !getenv("LEVYH_NO_H2_REFINE")) {
+            auto r64 = refine_tree_leaves(*Z->rt, 64);
+            auto c64 = Z->ct == Z->rt ? r64 : refine_tree_leaves(*Z->ct, 64);
+            Z->rt = r64.get();
+            Z->ct = c64.get();
+            Z->rt_hold = r64;
+            Z->ct_hold = c64;
+        }
+        bool built = false;
+        try {
+            built = build_h2(ctx, *Z, sb_eps, split, *zs, pz, S.zs_stats);
+        } catch (...) {
+            Z->rt = rt0;
+            Z->ct = ct0;
+            Z->rt_hold = rh0;
+            Z->ct_hold = ch0;
+            throw;
+        }
+        Z->rt = rt0;
+        Z->ct = ct0;
+        Z->rt_hold = rh0;
+        Z->ct_hold = ch0;
+        if (built) {
             const double err = probe_rel_err(ctx, *S.mvZ, *Z, *pz, *zs);
             if (getenv("LEVYH_PLAN_VERBOSE")) fprintf(stderr, "[levyh] H2 probe: relative error %.3e\n", err);
             if (err <= 1e-10) {

@@ -1143,6 +1143,60 @@ void h2_launch_fused(const H2 &h, const double *x, double *y, double alpha, doub
 // leaf (the segment kernel's operands), the plan carries the H2 walk.  Returns false (nothing
 // changed) when Z does not qualify: leaves above 64 rows, a cluster whose gathered factors exceed
 // the shared-memory capacity, a basis above KQ columns, or a path deeper than H2_MAXP.
+// A copy of T whose leaves above 64 points are split (at 64 points from the start, again while
+// a part exceeds 64: the 64-row segments of the matvec plans); existing node ids are kept, the
+// new children appended.  Lets the nested bases of a leaf-128 operator (cfg5) use 64-row leaf
+// bases: its blocks keep their clusters, which are now internal nodes of the copy.
+std::shared_ptr<Tree> refine_tree_leaves(const Tree &T, int maxleaf) {
+    auto R = std::make_shared<Tree>(T);
+    std::vector<int32_t> todo(R->leaves.begin(), R->leaves.end());
+    auto bbox = [&](Cluster &c) {
+        for (int d = 0; d < R->dim; ++d) {
+            double lo = 0, hi = 0;
+            for (i64 k = c.lo; k < c.hi; ++k) {
+                const double v = R->pts[R->order[k] * R->dim + d];
+                if (k == c.lo || v < lo) lo = v;
+                if (k == c.lo || v > hi) hi = v;
+            }
+            c.blo[d] = lo;
+            c.bhi[d] = hi;
+        }
+    };
+    while (!todo.empty()) {
+        const int32_t c = todo.back();
+        todo.pop_back();
+        if (R->nodes[c].size() <= maxleaf) continue;
+        const Cluster p = R->nodes[c];
+        Cluster a = p, b = p;
+        a.hi = p.lo + maxleaf;
+        b.lo = a.hi;
+        a.depth = b.depth = p.depth + 1;
+        a.kid[0] = a.kid[1] = b.kid[0] = b.kid[1] = -1;
+        bbox(a);
+        bbox(b);
+        const int32_t ia = (int32_t)R->nodes.size();
+        R->nodes.push_back(a);
+        R->nodes.push_back(b);
+        R->nodes[c].kid[0] = ia;
+        R->nodes[c].kid[1] = ia + 1;
+        todo.push_back(ia);
+        todo.push_back(ia + 1);
+    }
+    R->leaves.clear();  // depth-first leaf order
+    std::vector<int32_t> stk{0};
+    while (!stk.empty()) {
+        const int32_t c = stk.back();
+        stk.pop_back();
+        const Cluster &cl = R->nodes[c];
+        if (cl.leaf()) R->leaves.push_back(c);
+        else {
+            stk.push_back(cl.kid[1]);
+            stk.push_back(cl.kid[0]);
+        }
+    }
+    return R;
+}
+
 static bool h2_fail(const char *why) {
     if (getenv("LEVYH_PLAN_VERBOSE")) fprintf(stderr, "[levyh] H2 form not built: %s\n", why);
     return false;
@@ -1500,6 +1554,9 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
         split = 0;
         while (split < 12 && (int)std::max(roots(CT, C, split).size(), roots(RT, R, split).size()) > 2 * ctx.num_sms)
             ++split;
+        // subtrees of at most 127 clusters: larger ones do not fit a CTA's shared memory (their
+        // descriptors and x_hat slots); more subtrees then run as more CTAs (h2step.cu)
+        split = std::min(split, 6);
     }
     auto even = [](i64 v) { return (v + 1) & ~(i64)1; };
     // ---- column side: x_hat slots per subtree, leaves (P_s, ld 64), transfers transposed
@@ -1716,10 +1773,13 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
         if ((int)(up_chain.size() - up_cbeg.back()) > H2_MAXP) return h2_fail("column climb deeper than H2_MAXP");
         up_cbeg.push_back((int32_t)up_chain.size());
     }
+    // subtrees above H2_MAXN nodes only rule out the five-launch walk (its per-subtree staging);
+    // the two-kernel step cuts its own chunk lists and is checked when it is built
+    const char *big_subtree = nullptr;
     for (size_t q = 0; q + 1 < up_lv.size(); q += (size_t)maxh_up + 1)
-        if (up_lv[q + maxh_up] - up_lv[q] > H2_MAXN) return h2_fail("column subtree above H2_MAXN nodes");
+        if (up_lv[q + maxh_up] - up_lv[q] > H2_MAXN) big_subtree = "column subtree above H2_MAXN nodes";
     for (size_t q = 0; q + 1 < dn_lv.size(); q += (size_t)maxh_dn + 2)
-        if (dn_lv[q + maxh_dn + 1] - dn_lv[q] > H2_MAXN) return h2_fail("row subtree above H2_MAXN nodes");
+        if (dn_lv[q + maxh_dn + 1] - dn_lv[q] > H2_MAXN) big_subtree = "row subtree above H2_MAXN nodes";
     h->up_chain = dupload(up_chain, st);
     h->up_cbeg = dupload(up_cbeg, st);
     h->crec = dupload(crec, st);
@@ -1887,6 +1947,7 @@ bool build_h2(Ctx &ctx, HMat &Z, double eps, int split, HMat &ZS, std::shared_pt
             for (cudaEvent_t &e : plan->fev) LH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
     }
+    if (big_subtree && !h->step2) return h2_fail(big_subtree);
     plan->h2 = h;
     if (stats) {
         double ks = 0, nl = 0;
