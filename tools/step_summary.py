@@ -26,7 +26,8 @@ ki, vi = h.index("Kernel Name"), h.index("Metric Value")
 recs = [(short(r[ki]), float(r[vi].replace(",", ""))) for r in rows[hi + 1:] if len(r) > vi]
 # device steps: the consecutive launch sequence of one step (the e2e steps copy x in by memcpy
 # and are excluded): two-kernel H2 step (round 2) or the five-launch walk + segment step (round 1)
-SEQS = [["xpad_kernel", "h2s_up_kernel", "h2s_down_kernel"],
+SEQS = [["h2s_up_kernel", "h2s_down_kernel"],
+        ["xpad_kernel", "h2s_up_kernel", "h2s_down_kernel"],
         ["h2_leaf_kernel", "h2_up_kernel", "h2_couple_kernel", "h2_down_kernel", "seg_tma_kernel<5, 512>"]]
 for SEQ in SEQS:
     L = len(SEQ)
