@@ -73,14 +73,6 @@ int lh_partition(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, d
 int lh_plan_stats(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
                   int kcap, double *stats_host);
 
-/* Host-only: write the block layouts and the H-LU / solve / inverse task DAGs of this
- * partition to `path` (binary, see tests/plan_emulator.py) for CPU verification. */
-int lh_debug_dump_plans(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
-                        int kcap_f, int kcap_x, const char *path);
-/* Host-only planner timing on the partition of (rt, ct): which & 1 plans the H-LU, which & 2
- * the propagator; out[0..3] = H-LU plan seconds, tasks, propagator plan seconds, tasks. */
-int lh_debug_plan_timing(const lh_tree *rt, const lh_tree *ct, int n_min, int n_block, double eta,
-                         int kcap_f, int kcap_x, int which, double *out);
 
 /* ---- H-matrix construction: hmatrix.py:121-137 HConfig, :306-340 build_from_dense */
 typedef struct {
@@ -273,16 +265,6 @@ int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double 
 /* out[0..4] = H-LU task count, planning seconds, temp bytes, executor seconds, number of
  * plan chunks executed (> 1 when the LU ran while its plan was still being built) */
 int lh_hlu_stats(const lh_hmat *factor, double *out_host);
-/* Executor micro-benchmark: R synthetic tasks of one kind (0 GETRF 64x64 + leaf inverse,
- * 1 TRSM via leaf inverse, 2 SEGMUL with one dense 64x64 piece), k right-hand columns,
- * chained (each depends on the previous) or independent.  out[0] = wall us per task,
- * out[1] = mean task body us (device timestamps). */
-int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out_host);
-/* Debug: phase-timed recompression (QR(U), QR(V), Ru Rv^T, Jacobi SVD, truncation + apply) of
- * host U (m x K), V (n x K) on every SM, reps times; out[0..5] mean ns per phase, out[6] rank.
- * Times the kernel behind hops.py:134-144 (_lowrank_add_recompress). */
-int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const double *u_host,
-                          const double *v_host, double *out_host);
 
 /* 2D Gaussian CN operator on an nx x (N / nx) tensor grid (levy.assemble_cn_2d, levy.py:275-292;
  * entries levy.py:178-206 _entries_a_2d): which 0 = A, 1 = A+, 2 = A-; row i / column j is grid

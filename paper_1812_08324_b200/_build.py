@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "liblevyh_b200.so")
+TESTLIB = os.path.join(HERE, "liblevyh_b200_testing.so")  # test / diagnostic hooks (csrc/testing)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
@@ -46,19 +47,30 @@ def _compile(src, extra):
     return obj
 
 
-def build(verbose=False, extra=()):
-    os.makedirs(BUILD, exist_ok=True)
-    srcs = _sources()
-    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, list(extra)), srcs))
-    newest = max(os.path.getmtime(o) for o in objs)
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+def _link(out, objs, libs):
+    cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, *libs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    if verbose:
+
+
+def build(verbose=False, extra=()):
+    os.makedirs(BUILD, exist_ok=True)
+    srcs = _sources()
+    tsrcs = sorted(glob.glob(os.path.join(CSRC, "testing", "*.cpp")))
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, list(extra)), srcs))
+        tobjs = list(ex.map(lambda s: _compile(s, list(extra)), tsrcs))
+    newest = max(os.path.getmtime(o) for o in objs)
+    built = False
+    if not (os.path.exists(LIB) and os.path.getmtime(LIB) >= newest):
+        _link(LIB, objs, ["-lcudart", "-Xlinker", "-soname=liblevyh_b200.so"])
+        built = True
+    tnewest = max([os.path.getmtime(o) for o in tobjs] + [os.path.getmtime(LIB)])
+    if tobjs and not (os.path.exists(TESTLIB) and os.path.getmtime(TESTLIB) >= tnewest):
+        _link(TESTLIB, tobjs, ["-L" + HERE, "-llevyh_b200", "-lcudart", "-Xlinker", "-rpath=$ORIGIN"])
+        built = True
+    if verbose and built:
         print("built", LIB)
     return LIB
 

@@ -52,8 +52,6 @@ SIGNATURES = [
     ("lh_tree_order", C.c_int, [P, P]),
     ("lh_partition", C.c_int, [P, P, C.c_int, C.c_int, D, P, P, P]),
     ("lh_plan_stats", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, P]),
-    ("lh_debug_dump_plans", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, C.c_int, C.c_char_p]),
-    ("lh_debug_plan_timing", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, C.c_int, C.c_int, P]),
     ("lh_hmat_build_toeplitz", C.c_int, [P, P, P, P, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_build_dense", C.c_int, [P, P, P, P, I64, C.c_int, C.POINTER(HConfigC), C.POINTER(P)]),
     ("lh_hmat_derive_toeplitz", C.c_int, [P, P, P, D, I32, C.POINTER(P)]),
@@ -94,13 +92,11 @@ SIGNATURES = [
     ("lh_cn_step_host", C.c_int, [P, P, P, P, P, I32]),
     ("lh_step_profile", C.c_int, [P, P, P, P, I32, I32, P]),
     ("lh_hlu_stats", C.c_int, [P, P]),
-    ("lh_debug_task_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
     ("lh_hmat_build_gauss_series", C.c_int, [P, P, P, P, P, P, C.c_double, C.c_double, C.c_int,
                                              C.c_double, P, P]),
     ("lh_gauss_series_terms", C.c_int, [C.c_double, C.c_double, C.c_int, C.c_double]),
     ("lh_gauss_cn_symbol", C.c_int, [P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64,
                                      C.c_double, C.c_double, C.c_double, C.c_double, P, P, P, P]),
-    ("lh_debug_recomp_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
     ("lh_pcg", C.c_int, [P, P, P, P, I64, D, I32, P, P, P, P]),
     ("lh_gmres_restarted", C.c_int, [P, P, P, P, I64, D, I32, I32, P, P, P, P]),
     ("lh_dense_gemv", C.c_int, [P, P, I64, I64, I64, P, P]),
@@ -131,6 +127,31 @@ def lib():
                     f.argtypes = args
                 _lib = L
     return _lib
+
+
+# test / diagnostic hooks of liblevyh_b200_testing.so (include/levyh_b200_testing.h)
+TESTING_SIGNATURES = [
+    ("lh_debug_dump_plans", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, C.c_int, C.c_char_p]),
+    ("lh_debug_plan_timing", C.c_int, [P, P, C.c_int, C.c_int, D, C.c_int, C.c_int, C.c_int, P]),
+    ("lh_debug_task_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
+    ("lh_debug_recomp_bench", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P]),
+]
+TESTING_LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "liblevyh_b200_testing.so")
+_testing = None
+
+
+def testing():
+    """The testing library (plan export, planner timing, micro-benchmarks); not product code."""
+    global _testing
+    if _testing is None:
+        lib()  # the main library first (the testing one links against it)
+        T = C.CDLL(TESTING_LIB_PATH)
+        for name, res, args in TESTING_SIGNATURES:
+            f = getattr(T, name)
+            f.restype = res
+            f.argtypes = args
+        _testing = T
+    return _testing
 
 
 class NativeError(RuntimeError):

@@ -5,19 +5,10 @@
 
 #include <sys/mman.h>
 
+#include "abi_types.h"
 #include "core.h"
 #include "matvec.h"
 #include "plan_impl.h"
-
-struct lh_ctx {
-    lh::Ctx c;
-};
-struct lh_tree {
-    std::shared_ptr<lh::Tree> t;
-};
-struct lh_hmat {
-    lh::HMat h;
-};
 
 namespace lh {
 void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA, double *tP,
@@ -55,8 +46,6 @@ void shard_finalize(Ctx &ctx, HMat &H);
 int lowrank_add_recompress(Ctx &ctx, i64 m, i64 n, const double *u1, const double *v1, int r1,
                            const double *u2, const double *v2, int r2, double eps2, double *uo,
                            double *vo);
-void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
-void recomp_bench(Ctx &ctx, int m, int n, int K, int reps, const double *U, const double *V, double *out);
 void start_background_plans(HMat &H);
 struct KOp {
     int kind = LH_OP_IDENTITY;
@@ -812,15 +801,6 @@ int lh_step_profile(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int32
     return guard(ctx, [&] {
         step_profile(ctx->c, const_cast<HMat &>(hm->h), f->h, u, iters, method, out);
     });
-}
-
-int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out) {
-    return guard(ctx, [&] { task_bench(ctx->c, kind, R, k, chain != 0, out); });
-}
-
-int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const double *u, const double *v,
-                          double *out) {
-    return guard(ctx, [&] { recomp_bench(ctx->c, m, n, K, reps, u, v, out); });
 }
 
 int lh_hlu_stats(const lh_hmat *f, double *out) {

@@ -3,18 +3,18 @@
 // the oracle.  No device memory is touched.
 #include <cstdio>
 
-#include "plan_impl.h"
+#include "../abi_types.h"
+#include "../plan_impl.h"
+#include "../../../include/levyh_b200_testing.h"
 
 namespace lh {
 void triangle_layout(HMat &X, const HMat &F, bool lower, int kcap);
 void block_layout(HMat &X, const HMat &F, int part, int kcap);
+void task_bench(Ctx &ctx, int kind, int R, int k, bool chain, double *out);
+void recomp_bench(Ctx &ctx, int m, int n, int K, int reps, const double *u, const double *v, double *out);
 }
 
 using namespace lh;
-
-struct lh_tree {
-    std::shared_ptr<lh::Tree> t;
-};
 
 namespace {
 
@@ -201,4 +201,28 @@ extern "C" int lh_debug_plan_timing(const lh_tree *rt, const lh_tree *ct, int n_
         fprintf(stderr, "lh_debug_plan_timing: %s\n", e.what());
         return LH_EINTERNAL;
     }
+}
+
+// executor / recompression micro-benchmarks (lu.cu: task_bench, recomp_bench)
+template <class F>
+static int tguard(lh_ctx *ctx, F &&f) {
+    try {
+        f();
+        return LH_OK;
+    } catch (const lh::Error &e) {
+        if (ctx) ctx->c.last_error = e.what();
+        return e.code;
+    } catch (const std::exception &e) {
+        if (ctx) ctx->c.last_error = e.what();
+        return LH_EINTERNAL;
+    }
+}
+
+extern "C" int lh_debug_task_bench(lh_ctx *ctx, int kind, int R, int k, int chain, double *out) {
+    return tguard(ctx, [&] { task_bench(ctx->c, kind, R, k, chain != 0, out); });
+}
+
+extern "C" int lh_debug_recomp_bench(lh_ctx *ctx, int m, int n, int K, int reps, const double *u,
+                                     const double *v, double *out) {
+    return tguard(ctx, [&] { recomp_bench(ctx->c, m, n, K, reps, u, v, out); });
 }

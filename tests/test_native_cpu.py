@@ -26,6 +26,21 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(L, name), name
     bound = {s[0] for s in _lib.SIGNATURES}
     assert declared == bound
+    assert not any(n.startswith("lh_debug_") for n in declared)
+
+
+def test_testing_library_exports_its_header():
+    """Debug / diagnostic hooks live in liblevyh_b200_testing.so, not in the product library."""
+    hdr = open(os.path.join(ROOT, "include", "levyh_b200_testing.h")).read()
+    declared = set(re.findall(r"\b(lh_[a-z0-9_]+)\s*\(", hdr))
+    assert declared and all(n.startswith("lh_debug_") for n in declared)
+    T = _lib.testing()
+    for name in sorted(declared):
+        assert hasattr(T, name), name
+    assert declared == {s[0] for s in _lib.TESTING_SIGNATURES}
+    L = _lib.lib()
+    for name in sorted(declared):
+        assert not hasattr(L, name), name
 
 
 def _oracle_nodes(root):

@@ -21,7 +21,7 @@ def test_planned_dags_match_oracle(name, tmp_path):
     root, order, Hp, Hm = O.build_cn(g["tA"], float(g["dt"]), g["x"], leaf, float(g["eps1"]))
     ct = P.build_cluster_tree(g["x"][:, None], leaf)
     path = str(tmp_path / "plans.bin")
-    assert _lib.lib().lh_debug_dump_plans(ct.handle, ct.handle, leaf, 4, 1.0, 32, 48, path.encode()) == 0
+    assert _lib.testing().lh_debug_dump_plans(ct.handle, ct.handle, leaf, 4, 1.0, 32, 48, path.encode()) == 0
     D = E.load(path)
     # --- H-LU
     arenaF, ranks = E.fill_from_oracle(D["F0"], Hp, O.leaves)

@@ -10,7 +10,7 @@ import numpy as np  # noqa: E402
 import paper_1812_08324_b200 as P  # noqa: E402
 
 ctx = P._lib.Context.get()
-L = P._lib.lib()
+L = P._lib.testing()
 out = np.zeros(2)
 for kind, name in ((0, "GETRF+inverse"), (3, "GETRF only")):
     for chain in (1, 0):

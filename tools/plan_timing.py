@@ -19,7 +19,7 @@ x = np.linspace(-1, 1, 2 * n + 1)[1:-1]
 ct = P.build_cluster_tree(x[:, None], leaf)
 out = np.zeros(16)
 t = time.time()
-rc = _lib.lib().lh_debug_plan_timing(ct.handle, ct.handle, leaf, 4, 1.0, kf, kz, which, _lib.host_ptr(out))
+rc = _lib.testing().lh_debug_plan_timing(ct.handle, ct.handle, leaf, 4, 1.0, kf, kz, which, _lib.host_ptr(out))
 print(f"rc={rc} N={2 * n - 1} leaf {leaf}: H-LU plan {out[0]:.3f} s ({int(out[1])} tasks, temp {out[4] / 1e9:.2f} GB, "
       f"device {out[7] / 1e9:.2f} GB), propagator plan {out[2]:.3f} s ({int(out[3])} tasks, temp {out[5] / 1e9:.2f} GB, "
       f"device {out[8] / 1e9:.2f} GB); arenas F {out[9] / 1e9:.2f} GB (kcap {kf}), Z {out[6] / 1e9:.2f} GB (kcap {kz}); "

@@ -25,7 +25,7 @@ def case(m, n, r_each):
 
 
 ctx = P._lib.Context.get()
-L = P._lib.lib()
+L = P._lib.testing()
 names = ["stage", "qr_u", "qr_v", "C", "jacobi", "apply"]
 for m, r_each in ((64, 7), (128, 9), (128, 11), (256, 11), (256, 16), (192, 11)):
     U, V = case(m, m, r_each)

@@ -9,7 +9,7 @@ import numpy as np  # noqa: E402
 import paper_1812_08324_b200 as P  # noqa: E402
 
 ctx = P._lib.Context.get()
-L = P._lib.lib()
+L = P._lib.testing()
 out = np.zeros(2)
 for kind, name in ((0, "GETRF"), (1, "TRSM"), (2, "SEGMUL")):
     for k in ((64,) if kind == 0 else (7, 64)):
