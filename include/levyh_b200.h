@@ -358,6 +358,37 @@ int lh_gauss_cn_symbol(lh_ctx *ctx, int64_t N, double h, double eps_sq, double s
 int lh_cn_symbol(lh_ctx *ctx, const lh_measure *nu, const lh_cn_params *p, double *tA_dev,
                  double *tPlus_dev, double *tMinus_dev, double *sums_host);
 
+/* ---- matrix-free evaluators and variable-order assembly (fractional.py) ---- */
+/* frac_apply_1d (fractional.py:338-361) / eval_i1 (:304-319): out[i], i = 0..2K, on the main grid
+ * from the 2(M+K)+1 samples u_dev of the padded grid; conv = np.correlate(u, kern, 'valid') with
+ * kern_j = nu(j h) w_j (_window_sums_1d, :285-301), then
+ *   i1 = conv - u S0 - d1 Sg - d2 Sd,  out = i1 + far - u tail + d2 m2.
+ * part 1 returns i1 alone (eval_i1 at K = 0).  far_dev (2K+1) may be NULL (zero far field).
+ * sums_host (nullable) receives S0, Sg, Sd.  tail and m2 are host scalars as in lh_cn_symbol. */
+int lh_frac_apply_1d(lh_ctx *ctx, const lh_measure *nu, double h, int64_t M, int64_t K, double rho_r,
+                     double tail, double m2, const double *u_dev, const double *far_dev, int32_t part,
+                     double *out_dev, double *sums_host);
+/* frac_apply_2d (fractional.py:435-477) with the square window of _window_sums_2d (:413-432):
+ * u_dev is the padded grid, row-major side x side with side = 2(M+K)+1, out_dev the main grid
+ * (2K+1)^2.  The density is the 2D power density c r^(-2-2s) evaluated on the device, or, with
+ * table_dev != NULL, nu.density2 tabulated by the caller on the (2M+1)^2 window offsets
+ * (row-major, centre ignored).  sums_host (nullable): S0, Sgx, Sgy, Sdxx, Sdyy, Sdxy. */
+int lh_frac_apply_2d(lh_ctx *ctx, double c, double s, const double *table_dev, double h, int64_t M,
+                     int64_t K, double rho_r, double tail, double m2, const double *u_dev,
+                     const double *far_dev, double *out_dev, double *sums_host);
+/* assemble_variable_order (fractional.py:539-622): the dense variable-order stiffness matrix on
+ * the L-shape, A_dev row-major m x m (device).  cells_host: m x 2 integer cell coordinates of
+ * lshape_grid(n) (:504-520); s_host: the order s(x_i) per row, inside (0, 1) (LH_EINVAL
+ * otherwise, :553-554).  Per row on the device: c_{2,s_i} (frac_kernel_constant), the kernel on
+ * the (2 Mw + 1)^2 offsets, the six window sums, the graded second moment
+ * (windowed_second_moment_radial_2d) and tail_mass_square_2d, the nine-point correction.
+ * gl16_host / gl64_host: Gauss-Legendre nodes then weights (16 + 16, 64 + 64) as
+ * numpy.polynomial.legendre.leggauss returns them.  rowinfo_host (nullable, 8 per row): S0, sgx,
+ * sgy, sdxx, sdyy, sdxy, m2, tail. */
+int lh_assemble_variable_order(lh_ctx *ctx, int32_t n, int64_t m, const int32_t *cells_host,
+                               const double *s_host, double L_W, double rho_r, const double *gl16_host,
+                               const double *gl64_host, double *A_dev, double *rowinfo_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,7 +9,10 @@ there is no CPU fallback.
 from . import _lib  # noqa: F401
 from .fractional import (FracConfig, LevyMeasure, assemble_fractional_poisson_1d, cgmy_measure,  # noqa: F401
                          frac_kernel_constant, frac_stencil_1d, frac_symbol_1d, power_measure,
-                         quartic_window, tail_mass_power_1d, windowed_second_moment)
+                         quartic_window, tail_mass_power_1d, windowed_second_moment, eval_i1, eval_i2,
+                         eval_i3, frac_apply_1d, frac_apply_2d, windowed_second_moment_radial_2d,
+                         tail_mass_square_2d, lshape_grid, lshape_boundary_distance, variable_order_field,
+                         three_bump_source, assemble_variable_order, write_field_csv)
 from .geometry import (ClusterNode, ClusterTree, Permutation, PointSet, admissible,  # noqa: F401
                        build_cluster_tree)
 from .hmatrix import (HConfig, HMatrix, KernelExpansion, ToeplitzEntries, build_from_dense,  # noqa: F401

@@ -104,6 +104,9 @@ SIGNATURES = [
     ("lh_hmat_load", C.c_int, [P, C.c_char_p, C.POINTER(P), C.POINTER(P), C.POINTER(P), P, P]),
     ("lh_tree_points", C.c_int, [P, P]),
     ("lh_cn_symbol", C.c_int, [P, C.POINTER(MeasureC), C.POINTER(CNParamsC), P, P, P, P]),
+    ("lh_frac_apply_1d", C.c_int, [P, C.POINTER(MeasureC), D, I64, I64, D, D, D, P, P, I32, P, P]),
+    ("lh_frac_apply_2d", C.c_int, [P, D, D, P, D, I64, I64, D, D, D, P, P, P, P]),
+    ("lh_assemble_variable_order", C.c_int, [P, I32, I64, P, P, D, D, P, P, P, P]),
 ]
 
 _lib = None

@@ -16,6 +16,7 @@
 
 #include "core.h"
 #include "dev.cuh"
+#include "measure.cuh"
 
 namespace lh {
 
@@ -26,40 +27,6 @@ using dev::NT;
 // ===========================================================================
 // entry generation
 // ===========================================================================
-struct MeasureDev {
-    int kind;
-    double c, expo;           // power: c * |y|^expo, expo = -1 - 2s
-    double C, G, M, Yexpo;    // CGMY: C e^{-rate|y|} |y|^Yexpo, Yexpo = -1 - Y
-    const double *table;      // tabulated nu(j h), j = -Mw..Mw
-    i64 Mw;
-};
-
-__device__ __forceinline__ double nu_eval(const MeasureDev &nu, i64 j, double y) {
-    if (nu.kind == 0) return nu.c * pow(fabs(y), nu.expo);
-    if (nu.kind == 1) {
-        double rate = y < 0.0 ? nu.G : nu.M;
-        double ay = fabs(y);
-        return nu.C * exp(-rate * ay) * pow(ay, nu.Yexpo);
-    }
-    return nu.table[j + nu.Mw];
-}
-
-// kern_j = nu(j h) * w_j, w = h (h/2 at |j| = M), kern_0 = 0  (fractional.py:285-296)
-__device__ __forceinline__ double kern_eval(const MeasureDev &nu, i64 j, double h, i64 M) {
-    if (j == 0) return 0.0;
-    double y = (double)j * h;
-    double w = (j == M || j == -M) ? h / 2.0 : h;
-    return nu_eval(nu, j, y) * w;
-}
-
-__device__ __forceinline__ double window_eval(double y, double r) {
-    double t = fabs(y) / r;
-    if (!(t < 1.0)) return 0.0;
-    double p = pow(fmin(t, 1.0), 4.0);
-    double q = 1.0 - p;
-    return q * q;
-}
-
 constexpr int SUM_CHUNK = 4096;
 
 // per-CTA partial sums of kern, rho*y*kern, rho*y*y*kern over a fixed chunk of j
@@ -132,18 +99,7 @@ void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA,
                double *tM, double *sums_host) {
     LH_REQUIRE(p.N >= 1 && p.M >= 1, LH_EINVAL, "need N >= 1 and M >= 1");
     LH_REQUIRE(p.h > 0 && p.rho_r > 0, LH_EINVAL, "need h > 0 and rho_r > 0");
-    MeasureDev nu{};
-    nu.kind = m.kind;
-    nu.c = m.c;
-    nu.expo = -1 - 2 * m.s;
-    nu.C = m.C;
-    nu.G = m.G;
-    nu.M = m.M;
-    nu.Yexpo = -1.0 - m.Y;
-    nu.table = m.table_dev;
-    nu.Mw = p.M;
-    LH_REQUIRE(m.kind >= 0 && m.kind <= 2, LH_EINVAL, "unknown measure kind");
-    LH_REQUIRE(m.kind != 2 || m.table_dev, LH_EINVAL, "tabulated measure needs a table");
+    MeasureDev nu = measure_to_dev(m, p.M);
     i64 cnt = 2 * p.M + 1;
     int nparts = (int)((cnt + SUM_CHUNK - 1) / SUM_CHUNK);
     double *buf = (double *)ctx.ensure_scratch(sizeof(double) * (3 * (size_t)nparts + 4));

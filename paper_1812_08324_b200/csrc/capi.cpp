@@ -14,6 +14,12 @@ namespace lh {
 void cn_symbol(Ctx &ctx, const lh_measure &m, const lh_cn_params &p, double *tA, double *tP,
                double *tM, double *sums_host);
 void build_toeplitz(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg);
+void frac_apply_1d(Ctx &ctx, const lh_measure &m, double h, i64 M, i64 K, double rho_r, double tail, double m2,
+                   const double *u, const double *far, int part, double *out, double *sums_host);
+void frac_apply_2d(Ctx &ctx, double c, double s, const double *table, double h, i64 M, i64 K, double rho_r,
+                   double tail, double m2, const double *u, const double *far, double *out, double *sums_host);
+void assemble_variable_order(Ctx &ctx, int n, i64 m, const int32_t *cells_host, const double *s_host, double L_W,
+                             double rho_r, const double *gl16, const double *gl64, double *A, double *rowinfo_host);
 void cn2d_dense(Ctx &ctx, i64 N, int nx, double h, double eps_sq, double scale, double a, double b, double c,
                 double lam, double dt, int which, const int64_t *order_host, double *out_dev);
 void build_toeplitz_nccl(Ctx &ctx, HMat &H, const double *t, const lh_hconfig &cfg, int stages, double *stats);
@@ -904,6 +910,34 @@ int lh_dense_gemv(lh_ctx *ctx, const double *a, int64_t lda, int64_t m, int64_t 
 int lh_cn_symbol(lh_ctx *ctx, const lh_measure *nu, const lh_cn_params *p, double *tA, double *tP,
                  double *tM, double *sums_host) {
     return guard(ctx, [&] { cn_symbol(ctx->c, *nu, *p, tA, tP, tM, sums_host); });
+}
+
+int lh_frac_apply_1d(lh_ctx *ctx, const lh_measure *nu, double h, int64_t M, int64_t K, double rho_r,
+                     double tail, double m2, const double *u_dev, const double *far_dev, int32_t part,
+                     double *out_dev, double *sums_host) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(nu && u_dev && out_dev, LH_EINVAL, "null argument");
+        frac_apply_1d(ctx->c, *nu, h, M, K, rho_r, tail, m2, u_dev, far_dev, part, out_dev, sums_host);
+    });
+}
+
+int lh_frac_apply_2d(lh_ctx *ctx, double c, double s, const double *table_dev, double h, int64_t M,
+                     int64_t K, double rho_r, double tail, double m2, const double *u_dev,
+                     const double *far_dev, double *out_dev, double *sums_host) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(u_dev && out_dev, LH_EINVAL, "null argument");
+        frac_apply_2d(ctx->c, c, s, table_dev, h, M, K, rho_r, tail, m2, u_dev, far_dev, out_dev, sums_host);
+    });
+}
+
+int lh_assemble_variable_order(lh_ctx *ctx, int32_t n, int64_t m, const int32_t *cells_host,
+                               const double *s_host, double L_W, double rho_r, const double *gl16_host,
+                               const double *gl64_host, double *A_dev, double *rowinfo_host) {
+    return guard(ctx, [&] {
+        LH_REQUIRE(cells_host && s_host && gl16_host && gl64_host && A_dev, LH_EINVAL, "null argument");
+        assemble_variable_order(ctx->c, n, m, cells_host, s_host, L_W, rho_r, gl16_host, gl64_host, A_dev,
+                                rowinfo_host);
+    });
 }
 
 }  // extern "C"

@@ -87,3 +87,59 @@ def report_rank_mismatch(name, what, nblocks, diff):
         with open(os.path.join(out, "rank_mismatch.jsonl"), "a") as f:
             f.write(json.dumps(rec) + "\n")
     return rec
+
+
+# ---------------------------------------------------------------------------
+# matrix-free evaluators / variable-order assembly: seeded inputs shared by the fixture
+# generator (tests/golden/make_golden_apply.py) and the tests
+# ---------------------------------------------------------------------------
+APPLY_1D = {
+    "ap1_power": dict(measure=("power",), s=0.5, h=1.0 / 32, L=1.0, L_W=2.0, rho_r=0.2, far=True, seed=1),
+    "ap1_s08_ragged": dict(measure=("power",), s=0.8, h=1.0 / 50, L=0.74, L_W=1.5, rho_r=0.3, far=False, seed=2),
+    "ap1_cgmy": dict(measure=("cgmy", 1.0, 5.0, 10.0, 0.5), s=0.25, h=1.0 / 40, L=1.0, L_W=2.0, rho_r=0.2,
+                     far=False, tail=0.0123, seed=3),
+    "ap1_point": dict(measure=("power",), s=0.3, h=1.0 / 16, L=0.0, L_W=1.0, rho_r=0.25, far=False, seed=4),
+}
+APPLY_2D = {
+    "ap2_s04": dict(s=0.4, h=1.0 / 8, L=0.5, L_W=1.0, rho_r=0.3, far=True, seed=5),
+    "ap2_s075": dict(s=0.75, h=1.0 / 10, L=0.7, L_W=1.2, rho_r=0.25, far=False, seed=6),
+}
+VARIABLE_ORDER = {
+    "vo8": dict(n=8, L_W=2.0, rho_r=0.2, field="default"),
+    "vo12_short_window": dict(n=12, L_W=0.5, rho_r=0.2, field="wave"),
+    "vo16": dict(n=16, L_W=2.0, rho_r=0.3, field="default"),
+}
+
+
+def cgmy_density(C, G, M, Y):
+    def f(y):
+        y = np.asarray(y, dtype=float)
+        ay = np.abs(y)
+        with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+            return C * np.exp(-np.where(y < 0, G, M) * ay) * ay ** (-1.0 - Y)
+    return f
+
+
+def apply_inputs_1d(c):
+    M, K = int(round(c["L_W"] / c["h"])), int(round(c["L"] / c["h"]))
+    x = c["h"] * np.arange(-(M + K), M + K + 1)
+    rng = np.random.default_rng(c["seed"])
+    u = np.exp(-x * x) * np.cos(3 * x) + 0.05 * rng.standard_normal(x.shape)
+    far = (lambda t: 0.3 * np.sin(2 * np.asarray(t)) + 0.1) if c["far"] else None
+    return u, far
+
+
+def apply_inputs_2d(c):
+    M, K = int(round(c["L_W"] / c["h"])), int(round(c["L"] / c["h"]))
+    x = c["h"] * np.arange(-(M + K), M + K + 1)
+    rng = np.random.default_rng(c["seed"])
+    u = np.exp(-(x[:, None] ** 2 + 0.5 * x[None, :] ** 2)) * np.cos(2 * x[:, None] + x[None, :])
+    u = u + 0.05 * rng.standard_normal(u.shape)
+    far = (lambda a, b: 0.2 * np.cos(np.asarray(a)) * np.asarray(b) + 0.05) if c["far"] else None
+    return u, far
+
+
+def order_field(c):
+    if c["field"] == "default":
+        return None
+    return lambda pts: 0.5 + 0.35 * np.sin(2.0 * pts[:, 0]) * np.cos(3.0 * pts[:, 1])
