@@ -25,6 +25,8 @@ from .hops import (SOLVE_METHODS, HFactorization, hlu, lowrank_add_recompress, m
 from .levy import (CNSystem, CNSystem2D, FracCNSystem, UniformGrid1D, UniformGrid2D, assemble_cn_1d,  # noqa: F401
                    assemble_cn_2d, gaussian_measure, run_cn, step_cn)
 from .checkpoint import load_hmatrix, save_hmatrix  # noqa: F401
+from .formats import (cache_load, cache_store, fit_loglog_slope, fit_order, median_time, read_csv,  # noqa: F401
+                      write_csv)
 from .solvers import IterationLog, gmres_restarted, operator, pcg  # noqa: F401
 
 __version__ = "0.1.0"

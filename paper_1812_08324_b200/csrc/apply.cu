@@ -30,7 +30,8 @@ using dev::NT;
 namespace {
 
 constexpr int AP_R = 8;            // outputs per thread
-constexpr int AP_NT = 128;         // threads per CTA
+constexpr int AP_NT = 128;         // threads per CTA (1D, wide 2D rows); AP_NT_S for narrow 2D rows
+constexpr int AP_NT_S = 32;
 constexpr int AP_TILE = AP_R * AP_NT;  // outputs per CTA
 constexpr int AP_WC = 512;         // taps staged per round
 
@@ -85,11 +86,14 @@ __global__ void kern_table_kernel(MeasureDev nu, double h, i64 M, double *kern) 
         kern[idx] = kern_eval(nu, idx - M, h, M);
 }
 
-// sums of kern, rho y kern, rho y^2 kern over the whole table, one CTA, fixed order
-__global__ void sums1d_kernel(const double *kern, double h, i64 M, double rho_r, double *sums) {
+constexpr int SUM_CHUNK = 4096;
+
+// per-CTA partial sums of kern, rho y kern, rho y^2 kern over a fixed chunk of the table
+__global__ void sums1d_kernel(const double *kern, double h, i64 M, double rho_r, double *partials) {
     __shared__ double red[dev::NW];
     double s0 = 0.0, sg = 0.0, sd = 0.0;
-    for (i64 idx = threadIdx.x; idx < 2 * M + 1; idx += blockDim.x) {
+    const i64 lo = (i64)blockIdx.x * SUM_CHUNK, hi = min(lo + SUM_CHUNK, 2 * M + 1);
+    for (i64 idx = lo + threadIdx.x; idx < hi; idx += blockDim.x) {
         const double y = (double)(idx - M) * h, k = kern[idx];
         const double rho = window_eval(y, rho_r);
         s0 += k;
@@ -100,9 +104,20 @@ __global__ void sums1d_kernel(const double *kern, double h, i64 M, double rho_r,
     sg = dev::block_sum(sg, red);
     sd = dev::block_sum(sd, red);
     if (threadIdx.x == 0) {
-        sums[0] = s0;
-        sums[1] = sg;
-        sums[2] = sd;
+        partials[3 * blockIdx.x + 0] = s0;
+        partials[3 * blockIdx.x + 1] = sg;
+        partials[3 * blockIdx.x + 2] = sd;
+    }
+}
+
+// sums[q] = sum over parts of partials[nq * part + q], one CTA, fixed order
+__global__ void reduce_parts_kernel(const double *partials, int nparts, int nq, double *sums) {
+    __shared__ double red[dev::NW];
+    for (int q = 0; q < nq; ++q) {
+        double v = 0.0;
+        for (int k = threadIdx.x; k < nparts; k += blockDim.x) v += partials[nq * k + q];
+        v = dev::block_sum(v, red);
+        if (threadIdx.x == 0) sums[q] = v;
     }
 }
 
@@ -170,12 +185,13 @@ __global__ void kern2d_kernel(double c, double s, const double *table, double h,
     }
 }
 
-// S0, Sgx, Sgy, Sdxx, Sdyy, Sdxy (fractional.py:424-432), one CTA, fixed order
-__global__ void sums2d_kernel(const double *kern, double h, i64 M, double rho_r, double *sums) {
+// per-CTA partials of S0, Sgx, Sgy, Sdxx, Sdyy, Sdxy (fractional.py:424-432) over a chunk of offsets
+__global__ void sums2d_kernel(const double *kern, double h, i64 M, double rho_r, double *partials) {
     __shared__ double red[dev::NW];
     const i64 W = 2 * M + 1;
+    const i64 lo = (i64)blockIdx.x * SUM_CHUNK, hi = min(lo + SUM_CHUNK, W * W);
     double a[6] = {0, 0, 0, 0, 0, 0};
-    for (i64 idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
+    for (i64 idx = lo + threadIdx.x; idx < hi; idx += blockDim.x) {
         const double x = (double)(idx / W - M) * h, y = (double)(idx % W - M) * h, k = kern[idx];
         const double rho = window_eval(hypot(x, y), rho_r);
         a[0] += k;
@@ -187,47 +203,54 @@ __global__ void sums2d_kernel(const double *kern, double h, i64 M, double rho_r,
     }
     for (int q = 0; q < 6; ++q) {
         const double v = dev::block_sum(a[q], red);
-        if (threadIdx.x == 0) sums[q] = v;
+        if (threadIdx.x == 0) partials[6 * blockIdx.x + q] = v;
     }
 }
 
-// conv[ix, iy] = sum_{jx, jy} u[ix + jx, iy + jy] kern[jx, jy]: CTA = one output row ix and a tile
-// of iy; the window rows jx are walked in sequence, each a 1D sliding-window product
-__global__ void __launch_bounds__(AP_NT) corr2d_kernel(const double *__restrict__ u, const double *__restrict__ kern,
-                                                       i64 nout, i64 W, i64 side, double *__restrict__ conv) {
-    __shared__ __align__(16) double us[AP_USMEM];
+// partial[z][ix, iy] = sum over the part's window rows jx and all jy of u[ix + jx, iy + jy] kern[jx, jy]:
+// CTA = one output row ix, a tile of iy and a range of window rows, each row a 1D sliding-window
+// product
+template <int NTH>
+__global__ void __launch_bounds__(NTH) corr2d_kernel(const double *__restrict__ u, const double *__restrict__ kern,
+                                                     i64 nout, i64 W, i64 side, i64 rows_per_part,
+                                                     double *__restrict__ partial) {
+    constexpr int TILE = AP_R * NTH;
+    __shared__ __align__(16) double us[TILE + AP_WC + 2 * ((TILE + AP_WC) / 16) + 16];
     __shared__ __align__(16) double ks[AP_WC];
     const i64 ix = blockIdx.y;
-    const i64 i0 = (i64)blockIdx.x * AP_TILE;
+    const i64 i0 = (i64)blockIdx.x * TILE;
+    const i64 jx_lo = (i64)blockIdx.z * rows_per_part, jx_hi = min(jx_lo + rows_per_part, W);
     double acc[AP_R];
 #pragma unroll
     for (int r = 0; r < AP_R; ++r) acc[r] = 0.0;
-    for (i64 jx = 0; jx < W; ++jx) {
+    for (i64 jx = jx_lo; jx < jx_hi; ++jx) {
         const double *urow = u + (ix + jx) * side;
         const double *krow = kern + jx * W;
         for (i64 k0 = 0; k0 < W; k0 += AP_WC) {
             const int nt = (int)min((i64)AP_WC, W - k0);
             const int nt8 = (nt + AP_R - 1) / AP_R * AP_R;
             __syncthreads();
-            for (int x = threadIdx.x; x < AP_TILE + nt8 + AP_R; x += AP_NT) {
+            for (int x = threadIdx.x; x < TILE + nt8 + AP_R; x += NTH) {
                 const i64 g = i0 + k0 + x;
                 us[upad(x)] = g < side ? urow[g] : 0.0;
             }
-            for (int x = threadIdx.x; x < nt8; x += AP_NT) ks[x] = x < nt ? krow[k0 + x] : 0.0;
+            for (int x = threadIdx.x; x < nt8; x += NTH) ks[x] = x < nt ? krow[k0 + x] : 0.0;
             __syncthreads();
             corr_accumulate(acc, us, ks, nt8);
         }
     }
+    double *dst = partial + ((i64)blockIdx.z * nout + ix) * nout;
 #pragma unroll
     for (int r = 0; r < AP_R; ++r) {
         const i64 iy = i0 + AP_R * threadIdx.x + r;
-        if (iy < nout) conv[ix * nout + iy] = acc[r];
+        if (iy < nout) dst[iy] = acc[r];
     }
 }
 
 // fractional.py:452-477
-__global__ void finish2d_kernel(const double *conv, i64 nout, const double *u, i64 M, i64 side, double h,
-                                const double *sums, double tail, double m2, const double *far, double *out) {
+__global__ void finish2d_kernel(const double *partial, int nparts, i64 nout, const double *u, i64 M, i64 side,
+                                double h, const double *sums, double tail, double m2, const double *far,
+                                double *out) {
     const double h2 = h * h;
     for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < nout * nout; e += (i64)gridDim.x * blockDim.x) {
         const i64 ix = e / nout + M, iy = e % nout + M;
@@ -238,7 +261,9 @@ __global__ void finish2d_kernel(const double *conv, i64 nout, const double *u, i
         const double uxx = (U(ix + 1, iy) + U(ix - 1, iy) - 2 * uc) / h2;
         const double uyy = (U(ix, iy + 1) + U(ix, iy - 1) - 2 * uc) / h2;
         const double uxy = (U(ix + 1, iy + 1) + U(ix - 1, iy - 1) - U(ix + 1, iy - 1) - U(ix - 1, iy + 1)) / (4 * h2);
-        const double i1 = conv[e] - uc * sums[0] - ux * sums[1] - uy * sums[2] - 0.5 * uxx * sums[3] -
+        double conv = 0.0;
+        for (int p = 0; p < nparts; ++p) conv += partial[(i64)p * nout * nout + e];
+        const double i1 = conv - uc * sums[0] - ux * sums[1] - uy * sums[2] - 0.5 * uxx * sums[3] -
                           0.5 * uyy * sums[4] - uxy * sums[5];
         out[e] = i1 + (far ? far[e] : 0.0) - uc * tail + 0.5 * (uxx + uyy) * m2;
     }
@@ -337,7 +362,8 @@ __global__ void __launch_bounds__(NT) vo_rows_kernel(int n, i64 m, int Mw, doubl
         const int gx = cells[2 * i], gy = cells[2 * i + 1];
         double *row = A + i * m;
         __syncthreads();
-        for (i64 j = threadIdx.x; j < m; j += NT) row[j] = 0.0;
+        if (Mw < n - 1)  // otherwise every column lies inside the window and is written below
+            for (i64 j = threadIdx.x; j < m; j += NT) row[j] = 0.0;
         if (threadIdx.x == NT - 1) {
             int ok = 1;
             sh_m2 = graded_m2(ci, si, rho_r, &ok);
@@ -413,10 +439,12 @@ void frac_apply_1d(Ctx &ctx, const lh_measure &m, double h, i64 M, i64 K, double
     i64 nparts = std::max<i64>(1, std::min<i64>((3 * (i64)ctx.num_sms + tiles - 1) / tiles, (ntap + AP_WC - 1) / AP_WC));
     i64 per = ((ntap + nparts - 1) / nparts + AP_R - 1) / AP_R * AP_R;
     nparts = (ntap + per - 1) / per;
-    double *buf = dalloc<double>(ntap + 4 + nparts * nout);
-    double *kern = buf, *sums = buf + ntap, *partial = buf + ntap + 4;
+    const int nsum = (int)((ntap + SUM_CHUNK - 1) / SUM_CHUNK);
+    double *buf = dalloc<double>(ntap + 4 + 3 * (i64)nsum + nparts * nout);
+    double *kern = buf, *sums = buf + ntap, *sparts = sums + 4, *partial = sparts + 3 * (i64)nsum;
     kern_table_kernel<<<grid_for(ntap, 256, ctx.num_sms * 8), 256, 0, ctx.stream>>>(nu, h, M, kern);
-    sums1d_kernel<<<1, NT, 0, ctx.stream>>>(kern, h, M, rho_r, sums);
+    sums1d_kernel<<<nsum, NT, 0, ctx.stream>>>(kern, h, M, rho_r, sparts);
+    reduce_parts_kernel<<<1, NT, 0, ctx.stream>>>(sparts, nsum, 3, sums);
     corr1d_kernel<<<dim3((unsigned)tiles, (unsigned)nparts), AP_NT, 0, ctx.stream>>>(u, kern, nout, ntap, per, partial);
     finish1d_kernel<<<grid_for(nout, 256, ctx.num_sms * 8), 256, 0, ctx.stream>>>(partial, (int)nparts, nout, u, M, h,
                                                                                  sums, tail, m2, far, part, out);
@@ -433,14 +461,28 @@ void frac_apply_2d(Ctx &ctx, double c, double s, const double *table, double h, 
     LH_REQUIRE(M >= 1 && K >= 0 && h > 0 && rho_r > 0, LH_EINVAL, "need M >= 1, K >= 0, h > 0 and rho_r > 0");
     const i64 nout = 2 * K + 1, W = 2 * M + 1, side = 2 * (M + K) + 1;
     LH_REQUIRE(nout <= 65535, LH_EINVAL, "main grid too large for the 2D evaluator");
-    double *buf = dalloc<double>(W * W + 8 + nout * nout);
-    double *kern = buf, *sums = buf + W * W, *conv = buf + W * W + 8;
+    // narrow rows take 32-thread CTAs (256 outputs); window rows split into parts until about
+    // sixteen warps per SM are in flight
+    const bool narrow = nout <= 2 * AP_R * AP_NT_S;
+    const int nth = narrow ? AP_NT_S : AP_NT;
+    const i64 tiles = (nout + AP_R * nth - 1) / (AP_R * nth);
+    const i64 want = (16 * (i64)ctx.num_sms * 32 + tiles * nout * nth - 1) / (tiles * nout * nth);
+    i64 nparts = std::max<i64>(1, std::min<i64>(std::min<i64>(want, W), 64));
+    const i64 per = (W + nparts - 1) / nparts;
+    nparts = (W + per - 1) / per;
+    const int nsum = (int)((W * W + SUM_CHUNK - 1) / SUM_CHUNK);
+    double *buf = dalloc<double>(W * W + 8 + 6 * (i64)nsum + nparts * nout * nout);
+    double *kern = buf, *sums = buf + W * W, *sparts = sums + 8, *partial = sparts + 6 * (i64)nsum;
     kern2d_kernel<<<grid_for(W * W, 256, ctx.num_sms * 8), 256, 0, ctx.stream>>>(c, s, table, h, M, kern);
-    sums2d_kernel<<<1, NT, 0, ctx.stream>>>(kern, h, M, rho_r, sums);
-    const i64 tiles = (nout + AP_TILE - 1) / AP_TILE;
-    corr2d_kernel<<<dim3((unsigned)tiles, (unsigned)nout), AP_NT, 0, ctx.stream>>>(u, kern, nout, W, side, conv);
-    finish2d_kernel<<<grid_for(nout * nout, 256, ctx.num_sms * 8), 256, 0, ctx.stream>>>(conv, nout, u, M, side, h, sums,
-                                                                                        tail, m2, far, out);
+    sums2d_kernel<<<nsum, NT, 0, ctx.stream>>>(kern, h, M, rho_r, sparts);
+    reduce_parts_kernel<<<1, NT, 0, ctx.stream>>>(sparts, nsum, 6, sums);
+    const dim3 grid((unsigned)tiles, (unsigned)nout, (unsigned)nparts);
+    if (narrow)
+        corr2d_kernel<AP_NT_S><<<grid, AP_NT_S, 0, ctx.stream>>>(u, kern, nout, W, side, per, partial);
+    else
+        corr2d_kernel<AP_NT><<<grid, AP_NT, 0, ctx.stream>>>(u, kern, nout, W, side, per, partial);
+    finish2d_kernel<<<grid_for(nout * nout, 256, ctx.num_sms * 8), 256, 0, ctx.stream>>>(
+        partial, (int)nparts, nout, u, M, side, h, sums, tail, m2, far, out);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && sums_host)
         e = cudaMemcpyAsync(sums_host, sums, 6 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream);

@@ -63,7 +63,8 @@ def test_joint_order_dt_eq_h():
                 uo = np.linalg.solve(Ap, Am @ uo)
             assert np.linalg.norm(u - uo) <= 1e-8 * np.linalg.norm(uo), n
     orders = [np.log(errs[i] / errs[i + 1]) / np.log(2.0) for i in range(len(ns) - 1)]
-    fitted = np.polyfit(np.log(1.0 / np.asarray(ns, float)), np.log(errs), 1)[0]  # fit_order
+    import paper_1812_08324_b200 as P
+    fitted = P.fit_order(np.asarray(ns, float), errs)  # cli.py:116-118 on the parameter N
     print("joint dt = h: max errors", errs, "orders", orders, "fitted", fitted)
     assert all(0.5 <= o <= 0.8 for o in orders), (errs, orders)
     assert 0.55 <= fitted <= 0.8, (errs, fitted)
