@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <memory>
@@ -126,6 +127,9 @@ struct HMat {
     std::shared_ptr<void> solve_plan;
     std::shared_ptr<void> inv_plan;
     std::shared_ptr<void> bg_plan;  // background H-LU + inverse planning (lu.cu: PlanJob)
+    // set on the planners' structure copies: raised when the matrix is destroyed while its plans
+    // are still being built (Planner::emit stops at the next task)
+    std::shared_ptr<std::atomic<bool>> plan_cancel;
     std::shared_ptr<void> shard;    // pending sharded assembly (build.cu: ShardState)
     ~HMat();
     void sync_ranks(cudaStream_t s);

@@ -1645,8 +1645,10 @@ struct PlanJob {
     bool prop_uploaded = false;  // device copies made by the planning thread (own stream)
     int device = -1;             // device of the thread that assembled the matrix
     PlanStream lu_stream;  // the H-LU plan in chunks, when hlu() arrives before planning ends
-    std::future<void> f_lu, f_inv, f_prop;
     std::string error, inv_error, prop_error;
+    std::shared_ptr<std::atomic<bool>> cancel = std::make_shared<std::atomic<bool>>(false);
+    std::future<void> f_lu, f_inv, f_prop;  // last members: joined first, after ~PlanJob raised cancel
+    ~PlanJob() { cancel->store(true); }     // a matrix dropped while planning: stop at the next task
 };
 
 static void copy_structure(HMat &D, const HMat &S) {
@@ -1679,6 +1681,7 @@ void start_background_plans(HMat &H) {
     refine_dense_leaves(H);
     copy_structure(job->shadow, H);
     copy_structure(job->fshadow, H);
+    job->shadow.plan_cancel = job->fshadow.plan_cancel = job->cancel;
     PlanJob *j = job.get();
     if (const char *e = getenv("LEVYH_STREAM_MIN_CHUNK")) j->lu_stream.min_chunk = std::max(1, atoi(e));
     try {

@@ -315,6 +315,8 @@ int32_t Planner::new_slot() { return next_slot++; }
 
 int32_t Planner::emit(DTask t, std::initializer_list<std::pair<const PView *, bool>> acc,
                       const std::vector<std::pair<PView, bool>> *more) {
+    if (F.plan_cancel && F.plan_cancel->load(std::memory_order_relaxed))
+        throw Error(LH_EINTERNAL, "planning cancelled: the matrix was destroyed");
     int32_t id = (int32_t)P->tasks.size();
     std::vector<int32_t> &d = dbuf;
     d.clear();

@@ -219,3 +219,25 @@ def test_h_entry_reads_one_block(P):
         assert P.h_entry(B, int(i), int(j)) == pytest.approx(D[i, j], rel=1e-13, abs=1e-15)
     with pytest.raises(IndexError):
         P.h_entry(B, 300, 0)
+
+
+def test_dropping_a_matrix_cancels_its_background_plans(P):
+    """The H-LU / propagator plans are built on host threads from the moment a square H-matrix
+    exists; destroying the matrix must not wait for them (at N = 2^18 they take over a second)."""
+    import time
+
+    n = 2 ** 17
+    s = P.assemble_cn_1d(P.gaussian_measure(5.0), 0.0, 0.0, 0.0, P.UniformGrid1D(2 * n), 0.01)
+    cfg = P.HConfig(n_min=64, fixed_rank=10, eps1=1e-4)
+    H = s.hmatrix("plus", cfg)
+    t = time.perf_counter()
+    del H
+    import gc
+    gc.collect()
+    assert time.perf_counter() - t < 0.5
+    # a second matrix of the same structure plans, factorises and solves as usual
+    H = s.hmatrix("plus", cfg)
+    F = P.hlu(H, 1e-10)
+    x = np.random.default_rng(0).standard_normal(2 * n)
+    r = P.matvec(s.hmatrix("plus", cfg), P.solve(F, x)) - x
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(x)
