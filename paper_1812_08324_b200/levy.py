@@ -472,15 +472,48 @@ def step_cn(sys, u_n, F=None, method=None):
     return perm.from_tree(out)
 
 
+def _dense_device(sys, which):
+    """The dense A+ / A- in original (grid) order as a device tensor."""
+    import torch
+
+    from . import _lib
+
+    if hasattr(sys, "_device_matrix"):
+        return sys._device_matrix(which, np.arange(sys.N))
+    t = {"plus": sys.tPlus, "minus": sys.tMinus}[which]  # Toeplitz: A[i, j] = t[N - 1 + j - i]
+    n = sys.N
+    if 8.0 * n * n > 64e9:
+        raise MemoryError(f"dense mode refused for N={n}: {8.0 * n * n / 2 ** 30:.1f} GiB")
+    i = torch.arange(n, device=t.device)
+    return t[(n - 1) + i[None, :] - i[:, None]]
+
+
+def _run_cn_dense(sys, u0, n_steps):
+    import torch
+
+    Ap, Am = _dense_device(sys, "plus"), _dense_device(sys, "minus")
+    lu, piv = torch.linalg.lu_factor(Ap)
+    del Ap
+    u = torch.as_tensor(np.asarray(u0, dtype=float)).to(Am.device).reshape(sys.N, -1)
+    for _ in range(int(n_steps)):
+        u = torch.linalg.lu_solve(lu, piv, Am @ u)
+    out = u.cpu().numpy()
+    return out[:, 0] if np.ndim(u0) == 1 else out
+
+
 def run_cn(sys, u0, n_steps, cfg=None, eps2=1e-10, method=None, mode="hmatrix"):
     """levy.py:309-330: factor once, march n_steps on the device (CUDA-graph loop).
     ``method`` None steps with the method ``prepare`` set up (sys.method, default
     "propagator"); an explicit method prepares what it needs on the existing factor.
-    ``mode='dense'`` (the reference's dense LU oracle) is test infrastructure, not a product
-    path."""
+    ``mode='dense'`` is the reference's dense oracle path (levy.py:318-325: LU of the dense A+,
+    u <- lu_solve(A- u)), run on the device: the operators are generated on the GPU (Toeplitz
+    symbol gather in 1D, lh_cn2d_dense in 2D) and factored / applied by torch.linalg (cuSOLVER /
+    cuBLAS -- library code, off the H-matrix path; the convergence studies use it as their
+    reference solution, cli.py:318)."""
+    if mode == "dense":
+        return _run_cn_dense(sys, u0, n_steps)
     if mode != "hmatrix":
-        raise ValueError("only mode='hmatrix' runs on the device (the dense oracle lives in "
-                         "oracle/levyh_oracle.py)")
+        raise ValueError("mode must be 'hmatrix' or 'dense'")
     import torch
 
     from . import _lib
