@@ -186,7 +186,7 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
     F = P.hlu(Hp, cfg["eps2"])
     torch.cuda.synchronize()
     t_lu = time.perf_counter() - t2
-    st = np.zeros(5)
+    st = np.zeros(8)
     P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st))
     t3 = time.perf_counter()
     if method == "propagator":
@@ -202,7 +202,12 @@ def build_system(P, cfg=CFG3, n=None, method="propagator", world=1):
                                          for k, v in Hp.shard_stats.items())
                                     if getattr(Hp, "shard_stats", None) else "unsharded (1 rank)"),
                  hlu_plan_s=float(st[1]), hlu_exec_s=float(st[3]), hlu_tasks=int(st[0]),
-                 hlu_plan_chunks=int(st[4]))
+                 hlu_plan_chunks=int(st[4]),
+                 # the factorisation's algorithmic FP64 work (task list at the factor's
+                 # final ranks) and the rates over the executor's seconds
+                 hlu_gflop=round(float(st[5]) / 1e9, 1), hlu_gbytes=round(float(st[6]) / 1e9, 1),
+                 hlu_tflops=round(float(st[5]) / max(float(st[3]), 1e-9) / 1e12, 3),
+                 hlu_GBps=round(float(st[6]) / max(float(st[3]), 1e-9) / 1e9, 1))
     if method == "propagator":
         ps = F.propagator_stats()
         times.update(propagator_s=t_prep, propagator_plan_s=float(ps[1]),
@@ -608,7 +613,7 @@ def run_cfg5(args, world, rank, local):
     F = P.hlu(Hp, cfg["eps2"])
     torch.cuda.synchronize()
     t_lu = time.perf_counter() - t2
-    st = np.zeros(5)
+    st = np.zeros(8)
     P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st))
     t3 = time.perf_counter()
     if method == "propagator":

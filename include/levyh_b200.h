@@ -262,8 +262,10 @@ int lh_cn_step_host(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, const d
  * stored scalars of the factor. */
 int lh_step_profile(lh_ctx *ctx, const lh_hmat *hminus, lh_hmat *factor, double *u_dev,
                     int32_t iters, int32_t method, double *out_host);
-/* out[0..4] = H-LU task count, planning seconds, temp bytes, executor seconds, number of
- * plan chunks executed (> 1 when the LU ran while its plan was still being built) */
+/* out[0..6] = H-LU task count, planning seconds, temp bytes, executor seconds, number of
+ * plan chunks executed (> 1 when the LU ran while its plan was still being built), and the
+ * factorisation's algorithmic FP64 flops and operand bytes (task list evaluated at the factor's
+ * final ranks; temporaries at the mean stored rank) */
 int lh_hlu_stats(const lh_hmat *factor, double *out_host);
 
 /* 2D Gaussian CN operator on an nx x (N / nx) tensor grid (levy.assemble_cn_2d, levy.py:275-292;

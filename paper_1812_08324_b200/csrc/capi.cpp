@@ -811,6 +811,8 @@ int lh_step_profile(lh_ctx *ctx, const lh_hmat *hm, lh_hmat *f, double *u, int32
 
 int lh_hlu_stats(const lh_hmat *f, double *out) {
     for (int k = 0; k < 5; ++k) out[k] = f->h.lu_stats[k];
+    out[5] = f->h.lu_stats[6];
+    out[6] = f->h.lu_stats[7];
     return LH_OK;
 }
 

@@ -121,7 +121,8 @@ struct HMat {
     uint64_t gen = 0;
     bool factored = false;
     bool refined = false;             // dense leaves > 64 split for the H-arithmetic planner
-    double lu_stats[6] = {0, 0, 0, 0, 0, 0};  // tasks, plan s, temp bytes, exec s, chunks / NF leaves, merges
+    double lu_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // tasks, plan s, temp bytes, exec s, chunks / NF leaves, merges,
+                                                    // [6] algorithmic flops, [7] algorithmic bytes (plan_work)
     // lazily built plans (opaque; see matvec.cu / plan.cpp)
     std::shared_ptr<void> mv_plan;
     std::shared_ptr<void> solve_plan;

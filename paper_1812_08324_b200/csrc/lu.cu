@@ -1853,6 +1853,15 @@ static void hlu_streamed(Ctx &ctx, HMat &F, double eps2, PlanJob &job) {
     F.lu_stats[4] = nchunks;
 }
 
+// lu_stats[6..7]: the plan's algorithmic flops and bytes at the factor's final ranks (temporaries,
+// whose ranks are gone with the plan's rank array, at the mean stored rank)
+static void record_plan_work(HMat &F, const Plan &P) {
+    double mean = 0.0;
+    for (int32_t r : F.h_ranks) mean += r;
+    if (!F.h_ranks.empty()) mean /= (double)F.h_ranks.size();
+    plan_work(P, F.h_ranks, mean, F.lu_stats[6], F.lu_stats[7]);
+}
+
 void hlu(Ctx &ctx, HMat &F, double eps2) {
     LH_REQUIRE(F.nrows == F.ncols, LH_EINVAL, "LU requires a square matrix");
     LH_REQUIRE(!F.factored, LH_EINVAL, "matrix is already factored");
@@ -1889,6 +1898,7 @@ void hlu(Ctx &ctx, HMat &F, double eps2) {
             F.lu_stats[0] = (double)job->lu->tasks.size();
             F.lu_stats[1] = job->lu->build_seconds;
             F.lu_stats[2] = (double)job->lu->temp_len * 8.0;
+            record_plan_work(F, *job->lu);
             job->lu.reset();
             return;
         }
@@ -1918,6 +1928,7 @@ void hlu(Ctx &ctx, HMat &F, double eps2) {
     F.lu_stats[0] = (double)P->tasks.size();
     F.lu_stats[1] = P->build_seconds;
     F.lu_stats[2] = (double)P->temp_len * 8.0;
+    record_plan_work(F, *P);
 }
 
 struct SolvePlans {

@@ -1038,6 +1038,92 @@ void Planner::finalize() {
 }
 
 // longest dependency chain (in tasks, NOPs excluded); tasks are topologically ordered
+void plan_work(const Plan &P, const std::vector<int32_t> &ranks, double rank_other, double &flops, double &bytes) {
+    auto cols = [&](const DView &v) -> double {
+        if (v.wslot < 0) return (double)v.cols;
+        const double r = v.wslot < (int32_t)ranks.size() ? (double)ranks[v.wslot] : rank_other;
+        return std::min(r, (double)v.cols);
+    };
+    auto size = [&](const DView &v) { return (double)v.rows * cols(v); };
+    double fl = 0.0, by = 0.0;
+    for (const DTask &t : P.tasks) {
+        const DView *v = t.v;
+        switch (t.type) {
+        case T_GETRF: {  // LU with partial pivoting of an m x m leaf (+ its packed inverse when stored)
+            const double m = v[0].rows;
+            fl += 2.0 / 3.0 * m * m * m;
+            by += 2.0 * m * m;
+            break;
+        }
+        case T_TRSM: {
+            const double m = v[0].rows, k = cols(v[1]);
+            fl += m * m * k;
+            by += 0.5 * m * m + 2.0 * (double)v[1].rows * k;
+            break;
+        }
+        case T_SEGMUL: {
+            const double k = cols(v[0]);
+            by += 2.0 * size(v[0]);
+            for (int32_t q = t.pc_beg; q < t.pc_end; ++q) {
+                const DPiece &pc = P.pieces[q];
+                const double inner = pc.kind == 0 ? (double)pc.mat.cols : cols(pc.mat);
+                fl += 2.0 * (double)pc.mat.rows * inner * k;
+                by += (double)pc.mat.rows * inner + inner * k;
+            }
+            break;
+        }
+        case T_VTX: {  // W (r x k) = v0^T (n x r) v1 (n x k)
+            const double n = v[0].rows, r = cols(v[0]), k = cols(v[1]);
+            fl += 2.0 * n * r * k;
+            by += n * r + n * k + r * k;
+            break;
+        }
+        case T_LRADD: {  // CGS2 QR of [U U2] and [V V2], K x K core, Jacobi SVD, apply
+            const double m = v[0].rows, n = v[1].rows, r2 = cols(v[2]);
+            const double r1 = std::min(cols(v[0]), std::max(0.0, (double)v[0].cols - r2));
+            const double K = r1 + r2;
+            fl += 4.0 * (m + n) * K * K + 14.0 * K * K * K + 2.0 * (m + n) * K * std::min(K, r1 + 1.0);
+            by += 2.0 * (m + n) * K + (m + n) * r2;
+            break;
+        }
+        case T_DGEMM: {
+            const double m = v[0].rows, n = cols(v[0]);
+            const double k = (t.flags & 1) ? cols(v[2]) : (double)v[2].rows;
+            fl += 2.0 * m * n * std::min(k, cols(v[1]));
+            by += 2.0 * m * n + size(v[1]) + size(v[2]);
+            break;
+        }
+        case T_DADD:
+            fl += size(v[0]);
+            by += 3.0 * size(v[0]);
+            break;
+        case T_DENSIFY: {
+            const double r = v[2].rows > 0 ? cols(v[1]) : 0.0;
+            fl += 2.0 * size(v[0]) * r;
+            by += size(v[0]) + (r > 0 ? ((double)v[1].rows + v[2].rows) * r : size(v[1]));
+            break;
+        }
+        case T_IDENT:
+        case T_RAND:
+            by += size(v[0]);
+            break;
+        case T_ORTH: {
+            const double m = v[0].rows, p = cols(v[0]);
+            fl += 4.0 * m * p * p;
+            by += 2.0 * m * p;
+            break;
+        }
+        case T_CHECK:
+            by += size(v[0]);
+            break;
+        default:
+            break;
+        }
+    }
+    flops = fl;
+    bytes = 8.0 * by;
+}
+
 int64_t critical_path(const Plan &P) {
     std::vector<int64_t> d(P.tasks.size(), 0);
     int64_t best = 0;

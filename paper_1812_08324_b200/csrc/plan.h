@@ -133,4 +133,9 @@ struct Plan {
     void upload(cudaStream_t s);
 };
 
+// Algorithmic FP64 work of a plan: flops and operand bytes (each operand read or written once
+// per task) summed over its tasks, with the run-time column counts taken from `ranks` (the
+// factor's final ranks, indexed by rank slot) and `rank_other` for slots outside it (temporaries).
+void plan_work(const Plan &P, const std::vector<int32_t> &ranks, double rank_other, double &flops, double &bytes);
+
 }  // namespace lh

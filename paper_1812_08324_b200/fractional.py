@@ -218,7 +218,7 @@ def drift_compensation_beta(nu, rho_r):
 def _measure_native(nu, h, M, ctx):
     import torch
 
-    spec = nu.gpu
+    spec = getattr(nu, "gpu", None)  # a levyh LevyMeasure (no device spec) is tabulated
     keep = None
     if spec is not None and spec[0] == "power":
         m = _lib.MeasureC(0, spec[1], spec[2], 0, 0, 0, 0, None)

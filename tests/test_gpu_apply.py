@@ -62,6 +62,18 @@ def test_frac_apply_1d_vs_reference(P, g, name):
     assert np.allclose(i1 + i2 + i3, out[[0, K, 2 * K]], rtol=0, atol=1e-12 * _conv_scale(kern, u))
 
 
+def test_frac_apply_1d_tabulated_measure(P, g):
+    """A measure without a device evaluation spec (e.g. a levyh LevyMeasure: density only) is
+    tabulated on the window offsets by the host layer; same result."""
+    c = cases.APPLY_1D["ap1_power"]
+    u, far = cases.apply_inputs_1d(c)
+    nu = P.LevyMeasure(density=P.power_measure(1, c["s"]).density, kind="singular_heavy_tail")
+    assert nu.gpu is None
+    cfg = P.FracConfig(s=c["s"], h=c["h"], L=c["L"], L_W=c["L_W"], rho_r=c["rho_r"], far_field=far, nu=nu)
+    kern = O.window_sums(nu.density, c["h"], cfg.n_window, c["rho_r"])[0]
+    assert np.abs(P.frac_apply_1d(u, cfg) - g["ap1_power_out"]).max() <= 1e-13 * _conv_scale(kern, u)
+
+
 def test_frac_apply_1d_errors(P):
     cfg = P.FracConfig(s=0.5, h=1.0 / 16, L=1.0, L_W=2.0)
     with pytest.raises(ValueError):

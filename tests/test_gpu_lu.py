@@ -75,7 +75,7 @@ def test_hlu_streamed_chunks(P, monkeypatch):
         cfg = P.HConfig(n_min=64, eps1=1e-10)
         Hp, _ = s.build_pair(cfg)
         F = P.hlu(Hp, 1e-10)
-        st = np.zeros(5)
+        st = np.zeros(8)
         P._lib.check(P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st)))
         return s, cfg, F, st
 
@@ -83,6 +83,12 @@ def test_hlu_streamed_chunks(P, monkeypatch):
     assert st1[4] >= 2, st1  # ran as more than one chunk
     _, _, F0, st0 = factor(False)
     assert st0[4] == 1
+    # algorithmic flops / bytes of the factorisation: the same task list both ways; at least the
+    # diagonal leaves' LU (2/3 64^3 flops each), at most a dense LU of the whole matrix
+    nleaf = s.N // 64
+    assert st0[5] > nleaf * (2.0 / 3.0) * 64 ** 3 and st0[5] < (2.0 / 3.0) * float(s.N) ** 3
+    assert st0[6] > 8.0 * 2 * nleaf * 64 * 64
+    assert abs(st1[5] / st0[5] - 1.0) < 1e-2 and abs(st1[6] / st0[6] - 1.0) < 1e-2
     x1 = P.solve(F1, x, method="substitution")
     x0 = P.solve(F0, x, method="substitution")
     assert _rel(x1, x0) <= 1e-12

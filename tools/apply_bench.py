@@ -61,7 +61,7 @@ def main():
         flops = 2.0 * (2 * K + 1) ** 2 * (2 * M + 1) ** 2
         out["cases"].append({"op": "frac_apply_2d", "main_points": (2 * K + 1) ** 2, "window_taps": (2 * M + 1) ** 2,
                              "ms": ms, "tflops": flops / ms / 1e9, "frac_of_fp64_peak": flops / ms / 1e9 / fp64})
-    for n in (64, 128, 192):
+    for n in (48, 64, 128, 192):
         m = 3 * n * n // 4
         ms = timed(lambda: P.assemble_variable_order(n, device=True), reps=2)
         W = 2 * n + 1

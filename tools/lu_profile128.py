@@ -18,7 +18,7 @@ Hp, Hm = s.build_pair(P.HConfig(n_min=leaf, eps1=1e-10, kcap=24))
 t1 = time.time()
 F = P.hlu(Hp, 1e-10)
 import numpy as np  # noqa: E402
-st = np.zeros(5)
+st = np.zeros(8)
 P._lib.lib().lh_hlu_stats(F.h.handle, P._lib.host_ptr(st))
 print(f"N={s.N} leaf={leaf}: build {t1 - t:.2f} s, hlu {time.time() - t1:.2f} s, tasks {int(st[0])}, "
       f"plan {st[1]:.2f} s, exec {st[3]:.2f} s, chunks {int(st[4])}", flush=True)
