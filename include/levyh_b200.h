@@ -344,6 +344,26 @@ int lh_hmat_build_gauss_series(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct
                                const double *row_pts_dev, const double *col_pts_dev, double eps_sq,
                                double scale, int fixed_rank, double delta, const lh_hconfig *cfg,
                                lh_hmat **out);
+/* The exact entries of a 2D Gaussian CN operator (levy._entries_a_2d / CNSystem.entries,
+ * levy.py:178-206) as a dense-leaf source: the arguments of lh_cn2d_dense with the tree order on
+ * the device. */
+typedef struct {
+    int32_t nx, which;            /* grid width; 0 = A, 1 = A+, 2 = A- */
+    double h, eps_sq, scale;      /* grid spacing, Gaussian density scale * exp(-eps_sq |y|^2) */
+    double a, b, c, lam, dt;
+    const int64_t *order_dev;     /* order_dev[i] = grid index (iy nx + ix) of tree position i */
+} lh_cn2d_entries;
+/* build_from_expansion with gaussian_expansion_2d (hmatrix.py:189-216, :243-291) as
+ * levy.CNSystem.hmatrix calls it for dim = 2 (levy.py:224-239): tensor-product factor families,
+ * T terms per dimension (fixed_rank, or the Gaussian rank bound + 1 on the row cluster's diameter
+ * when delta > 0), block rank T^2, U's first family carries `scale`.  Points: n x 2 row-major
+ * device arrays in tree order.  Dense leaves from `entries` (exact operator entries) or, with
+ * NULL, from the kernel scale * exp(-eps_sq |x_i - y_j|^2).  LH_ERANK when T^2 exceeds the
+ * 32-column stored-rank limit (T > 5): such operators take lh_hmat_build_dense. */
+int lh_hmat_build_gauss_series_2d(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct,
+                                  const double *row_pts_dev, const double *col_pts_dev, double eps_sq,
+                                  double scale, int fixed_rank, double delta, const lh_hconfig *cfg,
+                                  const lh_cn2d_entries *entries, lh_hmat **out);
 /* _expansion_terms (hmatrix.py:284-290): fixed_rank, or rank_bound_gaussian(sqrt(eps_sq),
  * diameter, delta) + 1 (hmatrix.py:270-281) when delta > 0; 1 for a zero diameter. */
 int lh_gauss_series_terms(double eps_sq, double diameter, int fixed_rank, double delta);

@@ -18,7 +18,7 @@ from .geometry import (ClusterNode, ClusterTree, Permutation, PointSet, admissib
 from .hmatrix import (HConfig, HMatrix, KernelExpansion, ToeplitzEntries, build_from_dense,  # noqa: F401
                       bcast_factors, build_from_expansion, build_toeplitz, build_toeplitz_nccl,
                       derive_toeplitz, dump_structure,
-                      export_blocks, gaussian_expansion_1d, h_entry, memory_report,
+                      export_blocks, gaussian_expansion_1d, gaussian_expansion_2d, Cn2dEntries, h_entry, memory_report,
                       rank_bound_gaussian, structure_summary, to_dense)
 from .hops import (SOLVE_METHODS, HFactorization, hlu, lowrank_add_recompress, matvec,  # noqa: F401
                    mul_dense, solve, trisolve_lower, trisolve_upper_right)

@@ -30,6 +30,12 @@ class MeasureC(C.Structure):
                 ("table_dev", C.c_void_p)]
 
 
+class Cn2dEntriesC(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("which", C.c_int32), ("h", C.c_double), ("eps_sq", C.c_double),
+                ("scale", C.c_double), ("a", C.c_double), ("b", C.c_double), ("c", C.c_double),
+                ("lam", C.c_double), ("dt", C.c_double), ("order_dev", C.c_void_p)]
+
+
 class CNParamsC(C.Structure):
     _fields_ = [("h", C.c_double), ("N", C.c_int64), ("M", C.c_int64), ("rho_r", C.c_double),
                 ("tail", C.c_double), ("m2", C.c_double), ("a", C.c_double), ("b", C.c_double),
@@ -95,6 +101,8 @@ SIGNATURES = [
     ("lh_hmat_build_gauss_series", C.c_int, [P, P, P, P, P, P, C.c_double, C.c_double, C.c_int,
                                              C.c_double, P, P]),
     ("lh_gauss_series_terms", C.c_int, [C.c_double, C.c_double, C.c_int, C.c_double]),
+    ("lh_hmat_build_gauss_series_2d", C.c_int, [P, P, P, P, P, C.c_double, C.c_double, C.c_int, C.c_double,
+                                                P, P, P]),
     ("lh_gauss_cn_symbol", C.c_int, [P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64,
                                      C.c_double, C.c_double, C.c_double, C.c_double, P, P, P, P]),
     ("lh_pcg", C.c_int, [P, P, P, P, I64, D, I32, P, P, P, P]),

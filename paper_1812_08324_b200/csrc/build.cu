@@ -169,15 +169,14 @@ __global__ void gauss_symbol_kernel(double eps_sq, double scale, double h, i64 N
 }
 
 // 2D CN operator on a tensor grid (levy.py:178-206 _entries_a_2d + entries(which)): entry (i, j)
-// of A / A+ / A- for the points order[i], order[j] (row-major grid index k = iy nx + ix), written
-// row-major (ld N) in the order the caller's cluster tree gives; the same operations as numpy.
-__global__ void cn2d_dense_kernel(i64 N, int nx, double h, double eps_sq, double scale, double a, double b,
-                                  double c, double lam, double hdt, int which, const int64_t *order,
-                                  double *out) {
-    const i64 total = N * N;
-    const double h2 = h * h;
-    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
-        const i64 i = e / N, j = e % N;
+// of A / A+ / A- for the points order[i], order[j] (row-major grid index k = iy nx + ix) in the
+// order the caller's cluster tree gives; the same operations as numpy.
+struct Cn2dSrc {
+    const int64_t *order;
+    int nx, which;
+    double h, eps_sq, scale, a, b, c, lam, hdt;
+    __device__ __forceinline__ double operator()(i64 i, i64 j) const {
+        const double h2 = h * h;
         const i64 r = order[i], q = order[j];
         const double dx = (double)((q % nx) - (r % nx)) * h, dy = (double)((q / nx) - (r / nx)) * h;
         double E = -(scale * exp(-eps_sq * (dx * dx + dy * dy))) * h2;
@@ -188,8 +187,15 @@ __global__ void cn2d_dense_kernel(i64 N, int nx, double h, double eps_sq, double
         if (ey && fabs(dy) > 0.5 * h) E += -a / h2;
         if (ex && ey) E = 4 * a / h2 - c + lam * h2;
         const double eye = (r == q) ? 1.0 : 0.0;
-        out[e] = which == 0 ? E : which == 1 ? eye + hdt * E : eye - hdt * E;
+        return which == 0 ? E : which == 1 ? eye + hdt * E : eye - hdt * E;
     }
+};
+
+// the whole operator, row-major (ld N)
+__global__ void cn2d_dense_kernel(i64 N, Cn2dSrc src, double *out) {
+    const i64 total = N * N;
+    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x)
+        out[e] = src(e / N, e % N);
 }
 
 void cn2d_dense(Ctx &ctx, i64 N, int nx, double h, double eps_sq, double scale, double a, double b, double c,
@@ -199,7 +205,7 @@ void cn2d_dense(Ctx &ctx, i64 N, int nx, double h, double eps_sq, double scale, 
     std::vector<int64_t> ord(order_host, order_host + N);
     int64_t *d = dupload(ord, ctx.stream);
     const int grid = (int)std::min<i64>((N * N + NT - 1) / NT, (i64)ctx.num_sms * 32);
-    cn2d_dense_kernel<<<grid, NT, 0, ctx.stream>>>(N, nx, h, eps_sq, scale, a, b, c, lam, 0.5 * dt, which, d,
+    cn2d_dense_kernel<<<grid, NT, 0, ctx.stream>>>(N, Cn2dSrc{d, nx, which, h, eps_sq, scale, a, b, c, lam, 0.5 * dt},
                                                    out_dev);
     LH_CUDA(cudaGetLastError());
     LH_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -248,6 +254,15 @@ struct GaussSrc {  // expansion.kernel: scale e^{-eps_sq (x_i - y_j)^2} (hmatrix
     __device__ __forceinline__ double operator()(i64 i, i64 j) const {
         const double d = x[i] - y[j];
         return scale * exp(-eps_sq * d * d);
+    }
+};
+
+struct Gauss2Src {  // gaussian_expansion_2d's kernel: scale e^{-eps_sq |x_i - y_j|^2} (hmatrix.py:197-200)
+    const double *x, *y;  // n x 2 row-major
+    double eps_sq, scale;
+    __device__ __forceinline__ double operator()(i64 i, i64 j) const {
+        const double d0 = x[2 * i] - y[2 * j], d1 = x[2 * i + 1] - y[2 * j + 1];
+        return scale * exp(-eps_sq * (d0 * d0 + d1 * d1));
     }
 };
 
@@ -1099,6 +1114,98 @@ void build_gauss_series(Ctx &ctx, HMat &H, const double *t, const double *xr, co
     }
     if (t) build_finalize(ctx, H, ToepSrc{t, H.nrows}, {});
     else build_finalize(ctx, H, GaussSrc{xr, yc, eps_sq, scale}, {});
+}
+
+// 2D: gaussian_expansion_2d (hmatrix.py:189-216): the factor families are tensor products of the
+// 1D ones, column a T + b = col_a(first coordinate) * col_b(second coordinate), T terms per
+// dimension, block rank T^2; U's first-coordinate family carries `scale`.  Points are n x 2
+// row-major device arrays in tree order; the centre is the row cluster's box centre.
+constexpr int SERIES2D_TMAX = 5;  // T^2 <= KC_MAX
+static_assert(SERIES2D_TMAX * SERIES2D_TMAX <= KC_MAX && (SERIES2D_TMAX + 1) * (SERIES2D_TMAX + 1) > KC_MAX,
+              "2D series terms per dimension follow the stored-rank limit");
+struct SeriesJob2 {
+    i64 r0, c0, m, n, uoff, voff;
+    double cx, cy;
+    int32_t T, slot;
+};
+
+__global__ void series2d_kernel(const SeriesJob2 *jobs, int njobs, const double *xr, const double *yc,
+                                double eps_sq, double scale, double *arena, int32_t *ranks) {
+    for (int b = blockIdx.x; b < njobs; b += gridDim.x) {
+        const SeriesJob2 J = jobs[b];
+        for (i64 e = threadIdx.x; e < J.m + J.n; e += NT) {
+            const bool row = e < J.m;
+            const double *p = row ? xr + 2 * (J.r0 + e) : yc + 2 * (J.c0 + e - J.m);
+            const double t0 = p[0] - J.cx, t1 = p[1] - J.cy;
+            double *out = row ? arena + J.uoff + e : arena + J.voff + (e - J.m);
+            const i64 ld = row ? J.m : J.n;
+            double a1[SERIES2D_TMAX], a2[SERIES2D_TMAX];
+            a1[0] = (row ? scale : 1.0) * exp(-eps_sq * t0 * t0);
+            a2[0] = 1.0 * exp(-eps_sq * t1 * t1);
+            const double b0 = row ? 2.0 * eps_sq * t0 : t0, b1 = row ? 2.0 * eps_sq * t1 : t1;
+#pragma unroll
+            for (int k = 1; k < SERIES2D_TMAX; ++k) {
+                a1[k] = row ? a1[k - 1] * b0 / (double)k : a1[k - 1] * b0;
+                a2[k] = row ? a2[k - 1] * b1 / (double)k : a2[k - 1] * b1;
+            }
+#pragma unroll
+            for (int a = 0; a < SERIES2D_TMAX; ++a)
+#pragma unroll
+                for (int c = 0; c < SERIES2D_TMAX; ++c)
+                    if (a < J.T && c < J.T) out[(i64)(a * J.T + c) * ld] = a1[a] * a2[c];
+        }
+        if (threadIdx.x == 0) ranks[J.slot] = J.T * J.T;
+    }
+}
+
+void build_gauss_series_2d(Ctx &ctx, HMat &H, const double *xr, const double *yc, double eps_sq, double scale,
+                           int fixed_rank, double delta, const lh_hconfig &cfg, const lh_cn2d_entries *ent) {
+    LH_REQUIRE(eps_sq > 0, LH_EINVAL, "series builder needs eps_sq > 0");
+    LH_REQUIRE(delta > 0 || fixed_rank >= 1, LH_EINVAL, "fixed_rank must be >= 1");
+    LH_REQUIRE(H.rt->dim == 2 && H.ct->dim == 2, LH_EINVAL, "the 2D series builder needs 2D cluster trees");
+    std::vector<int32_t> terms(H.nodes.size(), 0), cap(H.nodes.size(), 0);
+    for (int32_t b : H.leafblocks) {
+        const Node &nd = H.nodes[b];
+        if (nd.kind != K_LR) continue;
+        const int T = gauss_series_terms(eps_sq, diameter(H.rt->nodes[nd.rcl], 2), fixed_rank, delta);
+        if (T > SERIES2D_TMAX)
+            throw Error(LH_ERANK, "2D series rank " + std::to_string(T) + "^2 exceeds the stored-rank limit " +
+                                      std::to_string(KC_MAX) + " for block (" + std::to_string(nd.r0) + "," +
+                                      std::to_string(nd.c0) + "," + std::to_string(nd.m) + "x" +
+                                      std::to_string(nd.n) + "): use at most " + std::to_string(SERIES2D_TMAX) +
+                                      " terms per dimension, or build_from_dense");
+        terms[b] = T;
+        cap[b] = 2 * T * T > KC_MAX ? KA_MAX : 0;
+    }
+    std::vector<int32_t> lr = build_layout(ctx, H, cfg, &cap);
+    std::vector<SeriesJob2> jobs;
+    jobs.reserve(lr.size());
+    for (int32_t b : lr) {
+        const Node &nd = H.nodes[b];
+        const Cluster &rc = H.rt->nodes[nd.rcl];
+        jobs.push_back({nd.r0, nd.c0, nd.m, nd.n, nd.uoff, nd.voff, 0.5 * (rc.blo[0] + rc.bhi[0]),
+                        0.5 * (rc.blo[1] + rc.bhi[1]), terms[b], nd.rslot});
+    }
+    if (!jobs.empty()) {
+        SeriesJob2 *d = dupload(jobs, ctx.stream);
+        const int grid = (int)std::min<size_t>(jobs.size(), (size_t)ctx.num_sms * 16);
+        series2d_kernel<<<grid, NT, 0, ctx.stream>>>(d, (int)jobs.size(), xr, yc, eps_sq, scale, H.d_arena,
+                                                     H.d_ranks);
+        LH_CUDA(cudaGetLastError());
+        LH_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(d);
+    }
+    if (ent) {
+        LH_REQUIRE(ent->which >= 0 && ent->which <= 2, LH_EINVAL, "which must be 0 (A), 1 (plus) or 2 (minus)");
+        LH_REQUIRE(ent->nx > 0 && H.nrows % ent->nx == 0 && H.nrows == H.ncols && ent->order_dev, LH_EINVAL,
+                   "entry source: square operator on an nx x (N / nx) grid with its tree order");
+        build_finalize(ctx, H,
+                       Cn2dSrc{ent->order_dev, ent->nx, ent->which, ent->h, ent->eps_sq, ent->scale, ent->a,
+                               ent->b, ent->c, ent->lam, 0.5 * ent->dt},
+                       {});
+    } else {
+        build_finalize(ctx, H, Gauss2Src{xr, yc, eps_sq, scale}, {});
+    }
 }
 
 // ===========================================================================

@@ -27,6 +27,8 @@ void build_gauss_series(Ctx &ctx, HMat &H, const double *t, const double *xr, co
                         double eps_sq, double scale, int fixed_rank, double delta,
                         const lh_hconfig &cfg);
 int gauss_series_terms(double eps_sq, double D, int fixed_rank, double delta);
+void build_gauss_series_2d(Ctx &ctx, HMat &H, const double *xr, const double *yc, double eps_sq, double scale,
+                           int fixed_rank, double delta, const lh_hconfig &cfg, const lh_cn2d_entries *ent);
 void gauss_cn_symbol(Ctx &ctx, i64 N, double h, double eps_sq, double scale, i64 n_off, double a,
                      double b, double c, double dt, double *tA, double *tP, double *tM,
                      double *lam_host);
@@ -407,6 +409,28 @@ int lh_hmat_build_gauss_series(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct
         partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
         build_gauss_series(ctx->c, o->h, t_dev, row_pts_dev, col_pts_dev, eps_sq, scale, fixed_rank,
                            delta, *cfg);
+        start_background_plans(o->h);
+    });
+    if (rc != LH_OK) {
+        delete o;
+        o = nullptr;
+    }
+    *out = o;
+    return rc;
+}
+
+int lh_hmat_build_gauss_series_2d(lh_ctx *ctx, const lh_tree *rt, const lh_tree *ct,
+                                  const double *row_pts_dev, const double *col_pts_dev, double eps_sq,
+                                  double scale, int fixed_rank, double delta, const lh_hconfig *cfg,
+                                  const lh_cn2d_entries *entries, lh_hmat **out) {
+    lh_hmat *o = nullptr;
+    int rc = guard(ctx, [&] {
+        check_cfg(cfg);
+        LH_REQUIRE(row_pts_dev && col_pts_dev, LH_EINVAL, "series builder needs the tree-order points");
+        o = new_hmat(rt, ct);
+        partition(o->h, *rt->t, *ct->t, cfg->n_min, cfg->n_block, cfg->eta);
+        build_gauss_series_2d(ctx->c, o->h, row_pts_dev, col_pts_dev, eps_sq, scale, fixed_rank, delta, *cfg,
+                              entries);
         start_background_plans(o->h);
     });
     if (rc != LH_OK) {

@@ -20,7 +20,7 @@ from . import _lib
 from .geometry import ClusterTree
 
 __all__ = ["HConfig", "HMatrix", "Dense", "LowRank", "Hier", "FactoredDense", "build_from_dense",
-           "build_toeplitz", "build_from_expansion", "KernelExpansion", "gaussian_expansion_1d",
+           "build_toeplitz", "build_from_expansion", "KernelExpansion", "gaussian_expansion_1d", "gaussian_expansion_2d", "Cn2dEntries",
            "rank_bound_gaussian", "ToeplitzEntries", "memory_report", "structure_summary",
            "dump_structure", "to_dense", "h_entry", "export_blocks"]
 
@@ -269,6 +269,31 @@ def gaussian_expansion_1d(eps_sq, scale=1.0):
                            family=("gauss1d", float(eps_sq), float(scale)))
 
 
+def gaussian_expansion_2d(eps_sq, scale=1.0):
+    """hmatrix.py:189-216: expansion of scale * exp(-eps_sq |x - y|^2) on 2D points; the factor
+    families are tensor products of the 1D ones (block rank n_terms ** 2)."""
+
+    def kernel(X, Y):
+        d0 = X[:, 0:1] - Y[:, 0:1].T
+        d1 = X[:, 1:2] - Y[:, 1:2].T
+        return scale * np.exp(-eps_sq * (d0 * d0 + d1 * d1))
+
+    def _tensor(ca, cb):
+        m, t = ca.shape
+        return (ca[:, :, None] * cb[:, None, :]).reshape(m, t * t)
+
+    def row_factors(X, center, n_terms):
+        return _tensor(_gauss_columns(X[:, 0] - center[0], eps_sq, n_terms, True, scale),
+                       _gauss_columns(X[:, 1] - center[1], eps_sq, n_terms, True))
+
+    def col_factors(Y, center, n_terms):
+        return _tensor(_gauss_columns(Y[:, 0] - center[0], eps_sq, n_terms, False),
+                       _gauss_columns(Y[:, 1] - center[1], eps_sq, n_terms, False))
+
+    return KernelExpansion(kernel, row_factors, col_factors, eps=math.sqrt(eps_sq),
+                           family=("gauss2d", float(eps_sq), float(scale)))
+
+
 def rank_bound_gaussian(eps, D, delta):
     """hmatrix.py:270-281: smallest r > max(log2(e^{2 eps^2 D^2}/delta) - 1, 12 eps^2 D^2 - 1)."""
     if D <= 0 or delta <= 0:
@@ -293,6 +318,52 @@ class ToeplitzEntries:
         return t[n_rows - 1 + np.asarray(cols)[None, :] - np.asarray(rows)[:, None]]
 
 
+@dataclass
+class Cn2dEntries:
+    """Entry source of a 2D Gaussian CN operator (the entry_fn levy.CNSystem.hmatrix passes for
+    dim = 2, levy.py:235-237): exact entries generated on the device (lh_cn2d_entries)."""
+
+    system: object
+    which: str = "plus"
+
+    def __call__(self, rows, cols):
+        orig = self.system.tree.perm.inverse
+        return self.system.entries(orig[np.asarray(rows)], orig[np.asarray(cols)], self.which)
+
+
+def _build_from_expansion_2d(row_ct, col_ct, fam, cfg, entry_fn):
+    import torch
+
+    if row_ct.dim != 2 or col_ct.dim != 2:
+        raise ValueError("gaussian_expansion_2d needs 2D cluster trees")
+    ctx = _lib.Context.get()
+    dev = f"cuda:{ctx.device}"
+    xr = torch.as_tensor(np.ascontiguousarray(row_ct.points, dtype=np.float64)).to(dev)
+    yc = torch.as_tensor(np.ascontiguousarray(col_ct.points, dtype=np.float64)).to(dev)
+    ent, order = None, None
+    if entry_fn is not None:
+        if not isinstance(entry_fn, Cn2dEntries):
+            raise TypeError("entry_fn must be a Cn2dEntries (device entry source)")
+        s = entry_fn.system
+        if row_ct is not col_ct or len(row_ct) != s.N:
+            raise ValueError("the entry source needs the system's cluster tree on both sides")
+        order = torch.as_tensor(np.ascontiguousarray(row_ct.perm.inverse, dtype=np.int64)).to(dev)
+        ent = _lib.Cn2dEntriesC(int(s.grid.nx), {"A": 0, "plus": 1, "minus": 2}[entry_fn.which], float(s.h),
+                                float(s.nu.gauss_eps_sq), float(s.nu.scale), float(s.a), float(s.b),
+                                float(s.c), float(s.lam), float(s.dt), C.c_void_p(order.data_ptr()))
+    if cfg.delta is not None and not cfg.delta > 0:
+        raise ValueError("D and delta must be positive")
+    h = C.c_void_p()
+    nc = cfg.native()
+    rc = _lib.lib().lh_hmat_build_gauss_series_2d(
+        ctx.h, row_ct.handle, col_ct.handle, C.c_void_p(xr.data_ptr()), C.c_void_p(yc.data_ptr()), fam[1],
+        fam[2], int(cfg.fixed_rank), float(cfg.delta) if cfg.delta is not None else 0.0, C.byref(nc),
+        C.byref(ent) if ent is not None else None, C.byref(h))
+    _lib.check(rc, ctx.h)
+    del order
+    return HMatrix(h, row_ct, col_ct, cfg.eta, ctx, cfg)
+
+
 def build_from_expansion(row_ct, col_ct, expansion, cfg=None, entry_fn=None):
     """hmatrix.py:243-291 on the GPU: partition of :319-337 with every admissible block
     (min(m,n) > n_min) low-rank from the series (cfg.fixed_rank terms, or the Gaussian rank
@@ -308,9 +379,11 @@ def build_from_expansion(row_ct, col_ct, expansion, cfg=None, entry_fn=None):
     if cfg.n_block < 2:
         raise ValueError("n_block must be >= 2")
     fam = getattr(expansion, "family", None)
+    if fam and fam[0] == "gauss2d":
+        return _build_from_expansion_2d(row_ct, col_ct, fam, cfg, entry_fn)
     if not fam or fam[0] != "gauss1d":
-        raise TypeError("the device series builder generates the 1D Gaussian expansion "
-                        "(gaussian_expansion_1d); got " + repr(fam))
+        raise TypeError("the device series builder generates the Gaussian expansions "
+                        "(gaussian_expansion_1d / gaussian_expansion_2d); got " + repr(fam))
     if row_ct.dim != 1 or col_ct.dim != 1:
         raise ValueError("gaussian_expansion_1d needs 1D cluster trees")
     ctx = _lib.Context.get()

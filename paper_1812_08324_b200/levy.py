@@ -282,18 +282,36 @@ class CNSystem2D:
             self.tree = build_cluster_tree(self.grid.points, leaf_size=leaf_size, strategy=strategy)
         return self.tree
 
-    def hmatrix(self, which="plus", cfg=None):
-        """H-form by build_from_dense of the device-generated operator.  The low-rank capacity
-        defaults to 48 columns (kept ranks <= 32): the 2D factors' H-LU updates need the room."""
+    SERIES_TERMS_MAX = 5  # terms per dimension the engine stores (rank T^2 <= 32)
+
+    def hmatrix(self, which="plus", cfg=None, builder=None):
+        """levy.py:224-239.  ``builder="series"``: the reference's route, build_from_expansion with
+        gaussian_expansion_2d and the exact entries as dense leaves (block rank fixed_rank ** 2,
+        so at most 5 terms per dimension fit the engine's 32-column kept rank);
+        ``builder="dense"``: build_from_dense of the device-generated operator at cfg.eps1
+        (any accuracy, O(N^2) assembly).  None picks the series route when it fits (no delta
+        rule, fixed_rank <= 5) and the dense route otherwise (the default fixed_rank = 10 would
+        be rank 100).  The low-rank capacity defaults to 48 columns: the 2D factors' H-LU updates
+        need the room."""
         import dataclasses
 
-        from .hmatrix import build_from_dense
+        from .hmatrix import Cn2dEntries, build_from_dense, build_from_expansion, gaussian_expansion_2d
 
         cfg = cfg or HConfig()
         if cfg.kcap < 48:
             cfg = dataclasses.replace(cfg, kcap=48)
+        if which not in ("A", "plus", "minus"):
+            raise ValueError(which)
+        if builder is None:
+            builder = "series" if cfg.delta is None and cfg.fixed_rank <= self.SERIES_TERMS_MAX else "dense"
         ct = self.cluster_tree(leaf_size=cfg.n_min)
-        return build_from_dense(self._device_matrix(which, ct.perm.inverse), ct, ct, cfg)
+        if builder == "dense":
+            return build_from_dense(self._device_matrix(which, ct.perm.inverse), ct, ct, cfg)
+        if builder != "series":
+            raise ValueError("builder must be 'series', 'dense' or None")
+        sign = {"A": -1.0, "plus": -0.5 * self.dt, "minus": +0.5 * self.dt}[which]
+        expansion = gaussian_expansion_2d(self.nu.gauss_eps_sq, scale=sign * self.nu.scale * self.h ** 2)
+        return build_from_expansion(ct, ct, expansion, cfg, entry_fn=Cn2dEntries(self, which))
 
     def build_pair(self, cfg=None):
         cfg = cfg or HConfig()
