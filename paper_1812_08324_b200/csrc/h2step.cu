@@ -75,6 +75,7 @@ __device__ __forceinline__ bool skipped(const H2SChunk &C, int skip) {
 }
 // wait_types: chunk types whose operands the previous kernel writes (programmatic dependent
 // launch: griddepcontrol.wait before the first of them; the others stream ahead)
+template <int ST = H2S_ST, int SLOTB = H2S_SLOTB>
 __device__ __forceinline__ void produce(const H2SChunk *ch, int nch, unsigned char *ring, uint64_t *full,
                                         uint64_t *empty, int skip = 0, int wait_types = 0) {
     int stage = 0;
@@ -92,9 +93,9 @@ __device__ __forceinline__ void produce(const H2SChunk *ch, int nch, unsigned ch
         uint32_t tot = 0;
         for (int i = 0; i < C.ncopy; ++i) tot += (uint32_t)C.bytes[i];
         mb_expect(&full[stage], tot);
-        unsigned char *slot = ring + (size_t)stage * H2S_SLOTB;
+        unsigned char *slot = ring + (size_t)stage * SLOTB;
         for (int i = 0; i < C.ncopy; ++i) bulk_ef(slot + C.dst[i], C.src[i], (uint32_t)C.bytes[i], &full[stage], pol);
-        if (++stage == H2S_ST) {
+        if (++stage == ST) {
             stage = 0;
             phase ^= 1;
         }
@@ -369,18 +370,19 @@ struct K2Args {
 };
 
 // K2: producer warp 0, consumer warps 1 .. 8
-__global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
+template <int ST, int SLOTB>
+__global__ void __launch_bounds__(CONS_T + 32, ST == 2 ? 2 : 1) h2s_down_kernel(K2Args A) {
     extern __shared__ __align__(128) unsigned char sm[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(sm), *empty = full + H2S_ST, *dbar = empty + H2S_ST;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm), *empty = full + ST, *dbar = empty + ST;
     unsigned char *ring = sm + RING_HDR;
-    double *ws = reinterpret_cast<double *>(ring + (size_t)H2S_ST * H2S_SLOTB);
+    double *ws = reinterpret_cast<double *>(ring + (size_t)ST * SLOTB);
     double *ys = ws + A.wsmax;
     double *py = ys + A.ysmax;  // [2][32] path chain state
     double *xgb = py + 64;      // [2][H2S_XG] gathered x_hat of the coupling chunks (double-buffered)
     unsigned char *desc = reinterpret_cast<unsigned char *>(xgb + 2 * H2S_XG);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, b = blockIdx.x;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < H2S_ST; ++i) {
+        for (int i = 0; i < ST; ++i) {
             mb_init(&full[i], 1);
             mb_init(&empty[i], H2S_CONS);
         }
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
     if (warp == 0) {
         // the coupling matrices, transfers and row bases do not depend on K1: they stream while
         // K1 finishes; the row chunks carry yd (written by K1) and wait for it
-        if (lane == 0) produce(chs, nch, ring, full, empty, 0, 1 << C_Q);
+        if (lane == 0) produce<ST, SLOTB>(chs, nch, ring, full, empty, 0, 1 << C_Q);
         return;
     }
     const int cw = warp - 1, ct = threadIdx.x - 32;
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
         }
         mb_wait(&full[stage], phase);
         if (A.trace) tw[7] += gtime() - ta;
-        const double *slot = reinterpret_cast<const double *>(ring + (size_t)stage * H2S_SLOTB);
+        const double *slot = reinterpret_cast<const double *>(ring + (size_t)stage * SLOTB);
         // lookahead between consecutive coupling chunks: the next chunk's x_hat are requested
         // now and stored after this chunk's products, so their L2 round trip overlaps them
         const bool ahead = C.type == C_CPL && c + 1 < nch && chs[c + 1].type == C_CPL && chs[c + 1].b > chs[c + 1].a;
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(CONS_T + 32, 1) h2s_down_kernel(K2Args A) {
         __syncwarp();
         if (lane == 0) mb_arrive(&empty[stage]);
         if (A.trace) tw[C.type] += gtime() - ta;
-        if (++stage == H2S_ST) {
+        if (++stage == ST) {
             stage = 0;
             phase ^= 1;
         }
@@ -600,8 +602,9 @@ bool merges(const Cut &k, uint64_t src) {
     return k.c.dst[i] + k.c.bytes[i] == k.used && src >= k.c.src[i] && src <= k.c.src[i] + (uint64_t)k.c.bytes[i];
 }
 // room for `ncopy` more copies of `bytes` in total (16-byte alignment slack included)
+thread_local i64 slot_limit = H2S_SLOTB;  // ring slot bytes of the list being cut (K2 two per SM: H2S_SLOTB2)
 bool fits(const Cut &k, i64 bytes, int ncopy) {
-    return k.c.ncopy + ncopy <= 4 && k.used + bytes + 32 * std::max(ncopy, 1) <= H2S_SLOTB;
+    return k.c.ncopy + ncopy <= 4 && k.used + bytes + 32 * std::max(ncopy, 1) <= slot_limit;
 }
 // appends [src, src + bytes) (any 8-byte aligned source: the copy starts at the 16-byte boundary
 // below it); returns the slot offset, in doubles, of src
@@ -651,7 +654,13 @@ static bool h2s_fail(const char *why) {
     return false;
 }
 
+static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st, bool allow_two);
 bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
+    // K2 with one CTA per row subtree (two per SM) when that fits, else one CTA per SM
+    return build_h2s_impl(in, h, num_sms, st, true) || build_h2s_impl(in, h, num_sms, st, false);
+}
+
+static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st, bool allow_two) {
     if (getenv("LEVYH_H2_V1")) return false;
     auto S = std::make_shared<H2S>();
     // one CTA per SM; with more than two subtrees per SM (N = 2^22), whole waves of CTAs with
@@ -834,6 +843,18 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     // ---------------- K2 operands reordered per row subtree: couplings (path, then subtree
     // nodes) and the parent transfers of the path and of every level, each contiguous
     const int nsd = in.nsub_dn;
+    // K2 is bound by each CTA's dependent chain (couplings -> path -> levels -> rows), so with
+    // between one and two row subtrees per SM it runs one CTA per subtree, two CTAs resident per
+    // SM on two-stage rings, instead of chaining two subtrees in half of the CTAs
+    const bool two = allow_two && !getenv("LEVYH_H2S_ONE_PER_SM") && G == num_sms && nsd > num_sms && nsd <= 2 * num_sms;
+    const int G2 = two ? nsd : G;
+    S->G2 = G2;
+    S->st2 = two ? 2 : H2S_ST;
+    const i64 SLOT2 = two ? H2S_SLOTB2 : H2S_SLOTB;
+    struct LimitGuard {
+        LimitGuard(i64 v) { slot_limit = v; }
+        ~LimitGuard() { slot_limit = H2S_SLOTB; }
+    } limit_guard(SLOT2);
     std::vector<CopyJob2> sjobs, tjobs;
     std::vector<i64> s_of(in.cpls->size(), -1);  // not used across subtrees (path S is duplicated)
     (void)s_of;
@@ -908,12 +929,12 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     std::vector<H2SDn> dnv;
     std::vector<H2SQ> qv;
     int wsmax = 2, ysmax = 2;
-    std::vector<std::vector<int>> k2subs(G);
-    for (int s = 0; s < nsd; ++s) k2subs[(int)((i64)s * G / std::max(nsd, 1))].push_back(s);
+    std::vector<std::vector<int>> k2subs(G2);
+    for (int s = 0; s < nsd; ++s) k2subs[(int)((i64)s * G2 / std::max(nsd, 1))].push_back(s);
     std::vector<char> leaf_done(in.rleaf.size(), 0);
-    std::vector<i64> k2bytes(G, 0);
+    std::vector<i64> k2bytes(G2, 0);
     i64 k2type[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // ring bytes by chunk type (diagnostics)
-    std::vector<std::vector<H2SChunk>> k2c(G);
+    std::vector<std::vector<H2SChunk>> k2c(G2);
     // the rows of row leaves [la, lb): one copy each of their Q bases (contiguous in the ZS
     // arena), yd rows and x rows
     auto q_chunks = [&](int b, size_t la, size_t lb, bool newlvl) {
@@ -927,7 +948,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                 const H2SInput::RLeaf &R = in.rleaf[e];
                 const i64 qn = qb + 8 * R.rows * R.k;
                 const i64 rows = R.r0 + R.rows - in.rleaf[l].r0;
-                if (qn + 16 * rows + 96 > SLOT) break;
+                if (qn + 16 * rows + 96 > SLOT2) break;
                 qb = qn;
                 ++e;
             }
@@ -968,7 +989,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
         }
         return true;
     };
-    for (int b = 0; b < G; ++b) {
+    for (int b = 0; b < G2; ++b) {
         auto &out = k2c[b];
         auto push = [&](Cut &k) {
             out.push_back(k.c);
@@ -1003,7 +1024,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                     sbytes += 8 * (i64)(*in.cpls)[e].kr * (*in.cpls)[e].kc;
                     kcs += (*in.cpls)[e].kc;
                 }
-                if (sbytes + 32 > SLOT || D.k > 255) return h2s_fail("a coupling node above one slot");
+                if (sbytes + 32 > SLOT2 || D.k > 255) return h2s_fail("a coupling node above one slot");
                 const double *src = sb2 + O.sbeg[t];
                 const bool mg = merges(k, (uint64_t)(uintptr_t)src);
                 if (kcs > H2S_XG) return h2s_fail("a coupling node's x_hat above the gather buffer");
@@ -1045,7 +1066,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                 const i64 t = O.path_t[q];
                 if (t >= 0) {
                     const i64 tb = 8 * (i64)D.ldt * D.kp;
-                    if (tb + 32 > SLOT) return h2s_fail("a path transfer above one ring slot");
+                    if (tb + 32 > SLOT2) return h2s_fail("a path transfer above one ring slot");
                     if (k.c.a < k.c.b && !fits(k, tb, merges(k, (uint64_t)(uintptr_t)(td2 + t)) ? 0 : 1)) {
                         push(k);
                         start(k, C_PATH, (int)pv.size());
@@ -1076,7 +1097,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
                     const i64 t = O.lvl_t[d][u - a];
                     if (t >= 0) {
                         const i64 tb = 8 * (i64)D.ldt * D.kp;
-                        if (tb + 32 > SLOT) return h2s_fail("a row transfer above one ring slot");
+                        if (tb + 32 > SLOT2) return h2s_fail("a row transfer above one ring slot");
                         if (t != last_t) {
                             if (k.c.a < k.c.b && !fits(k, tb, merges(k, (uint64_t)(uintptr_t)(td2 + t)) ? 0 : 1)) {
                                 push(k);
@@ -1130,7 +1151,7 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     std::vector<H2SPath> pv2;
     std::vector<H2SDn> dn2;
     std::vector<H2SQ> q2;
-    for (int b = 0; b < G; ++b) {
+    for (int b = 0; b < G2; ++b) {
         for (H2SChunk c : k2c[b]) {
             const int a = c.a, e = c.b;
             if (c.type == C_CPL) {
@@ -1171,10 +1192,11 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     pv.swap(pv2);
     dnv.swap(dn2);
     qv.swap(q2);
-    for (int b = 0; b < G; ++b) {
+    for (int b = 0; b < G; ++b)
         S->desc1 = std::max<int>(S->desc1, (int)((cb1[b + 1] - cb1[b]) * sizeof(H2SChunk) +
                                                   (lb1[b + 1] - lb1[b]) * sizeof(H2SLeaf) +
                                                   (ub1[b + 1] - ub1[b]) * sizeof(H2SUp)));
+    for (int b = 0; b < G2; ++b) {
         S->desc2 = std::max<int>(S->desc2, (int)((cb2[b + 1] - cb2[b]) * sizeof(H2SChunk) +
                                                   (nb2[b + 1] - nb2[b]) * sizeof(H2SCplN) +
                                                   (eb2[b + 1] - eb2[b]) * sizeof(H2SCplE) +
@@ -1188,7 +1210,14 @@ bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
     S->wsmax = (int)even(wsmax);
     S->ysmax = (int)even(ysmax);
     S->smem1 = RING_HDR + H2S_ST * H2S_SLOTB + 8 * S->xsmax + 8 * 2 * TGRP * 64 + S->desc1;
-    S->smem2 = RING_HDR + H2S_ST * H2S_SLOTB + 8 * (S->wsmax + S->ysmax + 64 + 2 * H2S_XG) + S->desc2;
+    S->smem2 = RING_HDR + S->st2 * (int)(S->st2 == 2 ? H2S_SLOTB2 : H2S_SLOTB) +
+               8 * (S->wsmax + S->ysmax + 64 + 2 * H2S_XG) + S->desc2;
+    if (S->st2 == 2 && S->smem2 > 113 * 1024 - 512) {
+        if (getenv("LEVYH_PLAN_VERBOSE"))
+            fprintf(stderr, "[levyh] K2 two per SM: smem %d B (w %d, y %d doubles, descriptors %d B)\n", S->smem2,
+                    S->wsmax, S->ysmax, S->desc2);
+        return h2s_fail("K2 per-subtree CTAs above half an SM's shared memory");
+    }
     int maxsm = 0, dev_id = 0;
     cudaGetDevice(&dev_id);
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id);
@@ -1238,8 +1267,10 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     static bool attr = false;
     if (!attr) {
         LH_CUDA(cudaFuncSetAttribute((const void *)h2s_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        LH_CUDA(cudaFuncSetAttribute((const void *)h2s_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
+        LH_CUDA(cudaFuncSetAttribute((const void *)h2s_down_kernel<H2S_ST, H2S_SLOTB>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        LH_CUDA(cudaFuncSetAttribute((const void *)h2s_down_kernel<2, H2S_SLOTB2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     113 * 1024));
         attr = true;
     }
     const int dbg = getenv("LEVYH_FUSE_DBG") ? atoi(getenv("LEVYH_FUSE_DBG")) : 0;  // timing experiments only
@@ -1249,7 +1280,7 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     LH_CUDA(cudaStreamIsCapturing(s, &cap));
     if (getenv("LEVYH_H2S_TRACE") && cap == cudaStreamCaptureStatusNone) {  // timing experiments only: per-CTA phase times
-        if (!trace) trace = dalloc<unsigned long long>((i64)S.G * 16);
+        if (!trace) trace = dalloc<unsigned long long>((i64)(S.G + S.G2) * 8);
         a1.trace = trace;
     }
     cudaEvent_t te[3] = {nullptr, nullptr, nullptr};
@@ -1265,7 +1296,7 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
               (dbg >> 5) & 15};
     if (!(dbg & 2)) {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(S.G);
+        cfg.gridDim = dim3(S.G2);
         cfg.blockDim = dim3(CONS_T + 32);
         cfg.dynamicSmemBytes = S.smem2;
         cfg.stream = s;
@@ -1274,12 +1305,13 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = getenv("LEVYH_NO_PDL") ? 0 : 1;
-        LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel, a2));
+        if (S.st2 == 2) LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel<2, H2S_SLOTB2>, a2));
+        else LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel<H2S_ST, H2S_SLOTB>, a2));
     }
     if (ev) LH_CUDA(cudaEventRecord(ev[2], s));
     LH_CUDA(cudaGetLastError());
     if (a1.trace && !getenv("LEVYH_H2S_TRACE_DONE")) {
-        std::vector<unsigned long long> t((size_t)S.G * 16);
+        std::vector<unsigned long long> t((size_t)(S.G + S.G2) * 8);
         cudaEventRecord(te[2], s);
         LH_CUDA(cudaStreamSynchronize(s));
         float m1 = 0, m2 = 0;
@@ -1296,12 +1328,12 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
         {
             const unsigned long long *u = t.data() + (size_t)S.G * 8;
             double mx[7] = {0, 0, 0, 0, 0, 0, 0}, mean[7] = {0, 0, 0, 0, 0, 0, 0};
-            for (int b = 0; b < S.G; ++b) {
+            for (int b = 0; b < S.G2; ++b) {
                 const double v[6] = {u[b * 8] * 1e-3, u[b * 8 + 1] * 1e-3, u[b * 8 + 2] * 1e-3, u[b * 8 + 3] * 1e-3,
                                      u[b * 8 + 4] * 1e-3, (u[b * 8 + 6] - u[b * 8 + 5]) * 1e-3};
                 for (int i = 0; i < 6; ++i) {
                     mx[i] = std::max(mx[i], v[i]);
-                    mean[i] += v[i] / S.G;
+                    mean[i] += v[i] / S.G2;
                 }
             }
             fprintf(stderr, "[h2s trace] K2 mean/max us: cpl %.1f/%.1f path %.1f/%.1f lvl %.1f/%.1f q %.1f/%.1f "
