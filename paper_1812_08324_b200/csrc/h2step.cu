@@ -843,11 +843,14 @@ static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t 
     // ---------------- K2 operands reordered per row subtree: couplings (path, then subtree
     // nodes) and the parent transfers of the path and of every level, each contiguous
     const int nsd = in.nsub_dn;
-    // K2 is bound by each CTA's dependent chain (couplings -> path -> levels -> rows), so with
-    // between one and two row subtrees per SM it runs one CTA per subtree, two CTAs resident per
-    // SM on two-stage rings, instead of chaining two subtrees in half of the CTAs
-    const bool two = allow_two && !getenv("LEVYH_H2S_ONE_PER_SM") && G == num_sms && nsd > num_sms && nsd <= 2 * num_sms;
-    const int G2 = two ? nsd : G;
+    // K2 is bound by each CTA's dependent chain (couplings -> path -> levels -> rows), so it runs
+    // one CTA per row subtree with two CTAs resident per SM on two-stage rings: with between one
+    // and two subtrees per SM instead of chaining two subtrees in half of the CTAs, and in the
+    // wave mode (more than two subtrees per SM, about one per CTA already) two waves at a time
+    const bool waves = G > num_sms;
+    const bool two = allow_two && !getenv("LEVYH_H2S_ONE_PER_SM") &&
+                     (waves || (nsd > num_sms && nsd <= 2 * num_sms));
+    const int G2 = (two && !waves) ? nsd : G;
     S->G2 = G2;
     S->st2 = two ? 2 : H2S_ST;
     const i64 SLOT2 = two ? H2S_SLOTB2 : H2S_SLOTB;

@@ -285,3 +285,30 @@ def test_levyh_style_run_cn_takes_the_two_kernel_step(P):
     P._lib.check(P._lib.lib().lh_cn_last_path(s.factor.h.handle, P._lib.host_ptr(path)))
     assert list(path[:3]) == [2, 0, 0]  # u <- 2 Z u - u, single RHS, device-resident
     assert int(P._lib.lib().lh_step_graph_kernels(s.factor.h.handle)) == 2
+
+
+def test_row_walk_one_cta_per_subtree_equals_one_per_sm(P, monkeypatch):
+    """K2 of the two-kernel step cuts its chunk lists per row subtree (two CTAs per SM, 32 KB
+    slots) when there are between one and two subtrees per SM, and per SM otherwise: the same
+    arithmetic in the same order, so both cuttings give the same step (and the reference's)."""
+    n = 2 ** 15
+    h = 1.0 / n
+    outs = []
+    for one_per_sm in (False, True):
+        if one_per_sm:
+            monkeypatch.setenv("LEVYH_H2S_ONE_PER_SM", "1")
+        else:
+            monkeypatch.delenv("LEVYH_H2S_ONE_PER_SM", raising=False)
+        s = P.FracCNSystem(P.power_measure(1, 0.5), 0.05, 0.1, -0.05, n, 4 * h)
+        s.prepare(P.HConfig(n_min=64, eps1=1e-9), 1e-10)
+        assert s.factor.propagator_stats()[6] == 2.0
+        u0 = np.maximum(1.0 - s.x ** 2, 0.0) ** 3
+        outs.append(P.run_cn(s, u0, 25))
+        assert int(P._lib.lib().lh_step_graph_kernels(s.factor.h.handle)) == 2
+        if not one_per_sm:
+            ref = u0
+            perm = s.tree.perm
+            for _ in range(3):
+                ref = perm.from_tree(P.solve(s.factor, P.matvec(s.h_minus, perm.to_tree(ref)), method="substitution"))
+            assert _rel(P.run_cn(s, u0, 3), ref) <= 1e-9
+    assert _rel(outs[0], outs[1]) <= 1e-13

@@ -16,7 +16,8 @@ STEP = ("seg_tma_kernel", "h2_leaf_kernel", "h2_up_kernel", "h2_couple_kernel", 
 
 
 def short(k):
-    return k.replace("void ", "").split("(")[0].split("::")[-1]
+    k = k.replace("void ", "").split("(")[0].split("::")[-1]
+    return k.split("<")[0] if k.startswith("h2s_") else k  # h2s_down_kernel<stages, slot bytes>
 
 
 rows = list(csv.reader(open(launches)))
