@@ -75,9 +75,9 @@ __device__ __forceinline__ bool skipped(const H2SChunk &C, int skip) {
 }
 // wait_types: chunk types whose operands the previous kernel writes (programmatic dependent
 // launch: griddepcontrol.wait before the first of them; the others stream ahead)
-template <int ST = H2S_ST, int SLOTB = H2S_SLOTB>
+template <int ST = H2S_ST>
 __device__ __forceinline__ void produce(const H2SChunk *ch, int nch, unsigned char *ring, uint64_t *full,
-                                        uint64_t *empty, int skip = 0, int wait_types = 0) {
+                                        uint64_t *empty, int skip = 0, int wait_types = 0, int slotb = H2S_SLOTB) {
     int stage = 0;
     uint32_t phase = 0;
     bool waited = wait_types == 0;
@@ -93,7 +93,7 @@ __device__ __forceinline__ void produce(const H2SChunk *ch, int nch, unsigned ch
         uint32_t tot = 0;
         for (int i = 0; i < C.ncopy; ++i) tot += (uint32_t)C.bytes[i];
         mb_expect(&full[stage], tot);
-        unsigned char *slot = ring + (size_t)stage * SLOTB;
+        unsigned char *slot = ring + (size_t)stage * slotb;
         for (int i = 0; i < C.ncopy; ++i) bulk_ef(slot + C.dst[i], C.src[i], (uint32_t)C.bytes[i], &full[stage], pol);
         if (++stage == ST) {
             stage = 0;
@@ -367,15 +367,16 @@ struct K2Args {
     int zmode;  // 0: beta = 0, 1: z = x (staged xpad slice), 2: z from global
     unsigned long long *trace;  // timing experiments only
     int skip;  // timing experiments only: bit 0 skips the coupling products, bit 1 the levels, bit 2 the rows
+    int slotb;  // ring slot bytes
 };
 
 // K2: producer warp 0, consumer warps 1 .. 8
-template <int ST, int SLOTB>
+template <int ST>
 __global__ void __launch_bounds__(CONS_T + 32, ST == 2 ? 2 : 1) h2s_down_kernel(K2Args A) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm), *empty = full + ST, *dbar = empty + ST;
     unsigned char *ring = sm + RING_HDR;
-    double *ws = reinterpret_cast<double *>(ring + (size_t)ST * SLOTB);
+    double *ws = reinterpret_cast<double *>(ring + (size_t)ST * A.slotb);
     double *ys = ws + A.wsmax;
     double *py = ys + A.ysmax;  // [2][32] path chain state
     double *xgb = py + 64;      // [2][H2S_XG] gathered x_hat of the coupling chunks (double-buffered)
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(CONS_T + 32, ST == 2 ? 2 : 1) h2s_down_kernel(
     if (warp == 0) {
         // the coupling matrices, transfers and row bases do not depend on K1: they stream while
         // K1 finishes; the row chunks carry yd (written by K1) and wait for it
-        if (lane == 0) produce<ST, SLOTB>(chs, nch, ring, full, empty, 0, 1 << C_Q);
+        if (lane == 0) produce<ST>(chs, nch, ring, full, empty, 0, 1 << C_Q, A.slotb);
         return;
     }
     const int cw = warp - 1, ct = threadIdx.x - 32;
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(CONS_T + 32, ST == 2 ? 2 : 1) h2s_down_kernel(
         }
         mb_wait(&full[stage], phase);
         if (A.trace) tw[7] += gtime() - ta;
-        const double *slot = reinterpret_cast<const double *>(ring + (size_t)stage * SLOTB);
+        const double *slot = reinterpret_cast<const double *>(ring + (size_t)stage * A.slotb);
         // lookahead between consecutive coupling chunks: the next chunk's x_hat are requested
         // now and stored after this chunk's products, so their L2 round trip overlaps them
         const bool ahead = C.type == C_CPL && c + 1 < nch && chs[c + 1].type == C_CPL && chs[c + 1].b > chs[c + 1].a;
@@ -654,13 +655,17 @@ static bool h2s_fail(const char *why) {
     return false;
 }
 
-static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st, bool allow_two);
+static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st, int two_slot);
 bool build_h2s(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st) {
-    // K2 with one CTA per row subtree (two per SM) when that fits, else one CTA per SM
-    return build_h2s_impl(in, h, num_sms, st, true) || build_h2s_impl(in, h, num_sms, st, false);
+    // K2 with one CTA per row subtree, two per SM, on the largest two-stage ring that leaves room
+    // for the subtree's walk slots and descriptors in half an SM's shared memory; else one per SM
+    for (int slot : {H2S_SLOTB2, 28 * 1024, 24 * 1024, 20 * 1024})
+        if (build_h2s_impl(in, h, num_sms, st, slot)) return true;
+    return build_h2s_impl(in, h, num_sms, st, 0);
 }
 
-static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st, bool allow_two) {
+static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t st, int two_slot) {
+    const bool allow_two = two_slot > 0;
     if (getenv("LEVYH_H2_V1")) return false;
     auto S = std::make_shared<H2S>();
     // one CTA per SM; with more than two subtrees per SM (N = 2^22), whole waves of CTAs with
@@ -853,7 +858,9 @@ static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t 
     const int G2 = (two && !waves) ? nsd : G;
     S->G2 = G2;
     S->st2 = two ? 2 : H2S_ST;
-    const i64 SLOT2 = two ? H2S_SLOTB2 : H2S_SLOTB;
+    if (allow_two && !two) return false;  // nothing to cut per subtree: the caller's one-per-SM pass builds it
+    const i64 SLOT2 = two ? two_slot : H2S_SLOTB;
+    S->slot2 = (int)SLOT2;
     struct LimitGuard {
         LimitGuard(i64 v) { slot_limit = v; }
         ~LimitGuard() { slot_limit = H2S_SLOTB; }
@@ -1213,7 +1220,7 @@ static bool build_h2s_impl(const H2SInput &in, H2 &h, int num_sms, cudaStream_t 
     S->wsmax = (int)even(wsmax);
     S->ysmax = (int)even(ysmax);
     S->smem1 = RING_HDR + H2S_ST * H2S_SLOTB + 8 * S->xsmax + 8 * 2 * TGRP * 64 + S->desc1;
-    S->smem2 = RING_HDR + S->st2 * (int)(S->st2 == 2 ? H2S_SLOTB2 : H2S_SLOTB) +
+    S->smem2 = RING_HDR + S->st2 * S->slot2 +
                8 * (S->wsmax + S->ysmax + 64 + 2 * H2S_XG) + S->desc2;
     if (S->st2 == 2 && S->smem2 > 113 * 1024 - 512) {
         if (getenv("LEVYH_PLAN_VERBOSE"))
@@ -1270,9 +1277,9 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     static bool attr = false;
     if (!attr) {
         LH_CUDA(cudaFuncSetAttribute((const void *)h2s_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        LH_CUDA(cudaFuncSetAttribute((const void *)h2s_down_kernel<H2S_ST, H2S_SLOTB>,
+        LH_CUDA(cudaFuncSetAttribute((const void *)h2s_down_kernel<H2S_ST>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        LH_CUDA(cudaFuncSetAttribute((const void *)h2s_down_kernel<2, H2S_SLOTB2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LH_CUDA(cudaFuncSetAttribute((const void *)h2s_down_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      113 * 1024));
         attr = true;
     }
@@ -1296,7 +1303,7 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
     if (a1.trace) cudaEventRecord(te[1], s);
     K2Args a2{S.c2, S.cb2, S.nb2, S.eb2, S.pb2, S.db2, S.qb2, S.cn, S.ce, S.path, S.dn, S.q, h.xh,
               S.wsmax, S.ysmax, z, y, alpha, beta, zmode, a1.trace ? a1.trace + (size_t)S.G * 8 : nullptr,
-              (dbg >> 5) & 15};
+              (dbg >> 5) & 15, S.slot2};
     if (!(dbg & 2)) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(S.G2);
@@ -1308,8 +1315,8 @@ static void h2s_kernels(const H2 &h, double *y, double alpha, double beta, const
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = getenv("LEVYH_NO_PDL") ? 0 : 1;
-        if (S.st2 == 2) LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel<2, H2S_SLOTB2>, a2));
-        else LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel<H2S_ST, H2S_SLOTB>, a2));
+        if (S.st2 == 2) LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel<2>, a2));
+        else LH_CUDA(cudaLaunchKernelEx(&cfg, h2s_down_kernel<H2S_ST>, a2));
     }
     if (ev) LH_CUDA(cudaEventRecord(ev[2], s));
     LH_CUDA(cudaGetLastError());

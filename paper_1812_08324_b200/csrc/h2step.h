@@ -26,7 +26,7 @@ namespace lh {
 
 constexpr int H2S_ST = 4;                    // ring stages
 constexpr int H2S_SLOTB = 40960 + 1024;      // bytes per ring slot (a 64 x 64 leaf + x slice)
-constexpr int H2S_SLOTB2 = 32768;            // K2 ring slot when two CTAs share an SM (two stages each)
+constexpr int H2S_SLOTB2 = 32768;            // largest K2 ring slot when two CTAs share an SM (two stages each)
 constexpr int H2S_CONS = 8;                  // consumer warps
 constexpr int H2S_MAXP = 24;                 // path length (as H2_MAXP)
 constexpr int H2S_XG = 512;                  // gathered x_hat entries per coupling chunk
@@ -70,7 +70,8 @@ struct H2SQ {  // rows of a row leaf: y = alpha (yd + Q y_hat) + beta z
 
 struct H2S {
     int G = 0;                        // CTAs (one per SM)
-    int G2 = 0, st2 = H2S_ST;         // K2: CTAs and ring stages (one CTA per row subtree, two per SM, when that fits)
+    int G2 = 0, st2 = H2S_ST, slot2 = H2S_SLOTB;  // K2: CTAs, ring stages and slot bytes (one CTA per row
+                                                  // subtree, two per SM on two-stage rings, when that fits)
     int smem1 = 0, smem2 = 0;         // dynamic shared memory of K1 / K2 (bytes)
     int xsmax = 0, wsmax = 0, ysmax = 0;
     H2SChunk *c1 = nullptr, *c2 = nullptr;

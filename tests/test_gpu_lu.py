@@ -299,9 +299,9 @@ def test_row_walk_one_cta_per_subtree_equals_one_per_sm(P, monkeypatch):
             monkeypatch.setenv("LEVYH_H2S_ONE_PER_SM", "1")
         else:
             monkeypatch.delenv("LEVYH_H2S_ONE_PER_SM", raising=False)
-        s = P.FracCNSystem(P.power_measure(1, 0.5), 0.05, 0.1, -0.05, n, 4 * h)
-        s.prepare(P.HConfig(n_min=64, eps1=1e-9), 1e-10)
-        assert s.factor.propagator_stats()[6] == 2.0
+        s = P.FracCNSystem(P.power_measure(1, 0.25), 0.5, 1.0, -1.0, n, h)   # cfg2 at N = 2^16 - 1
+        s.prepare(P.HConfig(n_min=64, eps1=1e-10), 1e-10)
+        assert s.factor.propagator_stats()[6] == 2.0                           # 256 row subtrees
         u0 = np.maximum(1.0 - s.x ** 2, 0.0) ** 3
         outs.append(P.run_cn(s, u0, 25))
         assert int(P._lib.lib().lh_step_graph_kernels(s.factor.h.handle)) == 2
