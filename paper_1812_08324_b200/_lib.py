@@ -229,12 +229,14 @@ class Context:
             return
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         uid = (C.c_char * 128)()
-        if rank == 0:
-            check(lib().lh_nccl_unique_id(C.cast(uid, C.c_void_p)))
-        obj = [bytes(uid.raw) if rank == 0 else None]
+        rc0 = lib().lh_nccl_unique_id(C.cast(uid, C.c_void_p)) if rank == 0 else 0
+        # a failure on rank 0 (libnccl not loadable) is broadcast too, so that no rank waits for an id
+        obj = [(rc0, bytes(uid.raw)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
                                    group=group)
-        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        if obj[0][0] != 0:
+            raise NativeError(f"[{obj[0][0]}] rank 0 could not create the NCCL unique id (libnccl not loadable?)")
+        uid = (C.c_char * 128).from_buffer_copy(obj[0][1])
         check(lib().lh_nccl_init(self.h, rank, world, C.cast(uid, C.c_void_p)), self.h)
 
     def torch_stream(self):

@@ -211,9 +211,23 @@ def build_toeplitz(t, row_ct, col_ct, cfg=None, distributed=False):
 
         rank = dist.get_rank(group)
         if t.is_cuda and dist.get_backend(group) == "nccl":
-            # the library's own communicator: staged ACA with the exchange overlapped (C ABI)
-            ctx.init_nccl(group)
-            return build_toeplitz_nccl(t, row_ct, col_ct, cfg)
+            # the library's own communicator: staged ACA with the exchange overlapped (C ABI).
+            # Its set-up (libnccl opened at run time, ncclCommInitRank) can fail where torch's
+            # bundled NCCL works; the ranks agree on the outcome, and if any of them failed all
+            # take the exchange through torch.distributed instead (same result, no overlap)
+            import torch
+
+            ok = 1
+            try:
+                ctx.init_nccl(group)
+            except Exception as exc:  # noqa: BLE001
+                ok = 0
+                import warnings
+                warnings.warn(f"library NCCL communicator unavailable ({exc}); exchanging through torch.distributed")
+            flag = torch.tensor([ok], dtype=torch.int32, device=t.device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if int(flag.item()) == 1:
+                return build_toeplitz_nccl(t, row_ct, col_ct, cfg)
         return build_toeplitz_sharded(t, row_ct, col_ct, cfg, rank, world,
                                       lambda buf: allgather_varlen(buf, group))
     h = C.c_void_p()
