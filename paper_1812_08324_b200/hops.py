@@ -81,6 +81,8 @@ class HFactorization:
     eps2: float
     inverse_ready: bool = False
     propagator_ready: bool = False
+    auto_prepare: bool = True   # default-method solves build the propagator after a few calls
+    default_calls: int = 0
 
     def solve(self, b, method=None):
         return solve(self, b, method)
@@ -128,17 +130,34 @@ def hlu(H: HMatrix, eps2=1e-10):
     return HFactorization(H, eps2)
 
 
+AUTO_PROPAGATOR_AFTER = 4
+
+
 def solve(F: HFactorization, b, method=None):
     """hops.py:424-432: x = (LU)^-1 b.  ``method`` None uses the fastest method already
     prepared on F (F.default_method: one H-matvec of the propagator after
     prepare_propagator / CNSystem.prepare, else the triangular-inverse factors, else the
-    reference's forward (unit L with leaf pivots) then backward (U) substitution)."""
+    reference's forward (unit L with leaf pivots) then backward (U) substitution; the fifth such
+    default substitution solve on a 1D factor builds the propagator first, F.auto_prepare = False
+    turns that off)."""
     ctx = F.h.ctx
     bt, was_torch = _to_device(b, ctx)
     if bt.shape[0] != F.h.n_rows:
         raise ValueError("right-hand side length mismatch")
     if method is None:
         method = F.default_method
+        if method == "substitution" and F.auto_prepare and getattr(F.h.row_tree, "dim", 1) == 1:
+            # repeated default solves on one factor (time stepping, preconditioning): after
+            # AUTO_PROPAGATOR_AFTER substitution solves the propagator is built once (about ten
+            # substitution solves' worth of time at N = 2^20) and every later solve is one
+            # streaming H-matvec of Z; pass method="substitution" to keep the reference's solve
+            F.default_calls += 1
+            if F.default_calls > AUTO_PROPAGATOR_AFTER:
+                try:
+                    F.prepare_propagator()
+                    method = "propagator"
+                except (NotImplementedError, MemoryError, _lib.NativeError):
+                    F.auto_prepare = False
     if method not in SOLVE_METHODS:
         raise ValueError(f"unknown solve method {method!r}; expected one of {sorted(SOLVE_METHODS)}")
     m = SOLVE_METHODS[method]

@@ -69,8 +69,11 @@ class _DevVec:
 class Operator:
     """A Krylov operator bound to its native descriptor (keeps every referenced object alive)."""
 
-    def __init__(self, op, n, ctx, method="substitution"):
+    def __init__(self, op, n, ctx, method=None):
         import torch
+
+        if method is None:  # the fastest method already prepared on a factor
+            method = op.default_method if isinstance(op, HFactorization) else "substitution"
 
         self.keep = []
         self.error = None
@@ -130,9 +133,12 @@ class Operator:
         self.c = c
 
 
-def operator(op, method="substitution", n=None):
-    """Wrap an HFactorization with a chosen solve method (or any operator) for pcg / gmres."""
+def operator(op, method=None, n=None):
+    """Wrap an HFactorization with a chosen solve method (or any operator) for pcg / gmres;
+    method None: the fastest method already prepared on the factor (substitution if none)."""
     ctx = _lib.Context.get()
+    if method is None:
+        method = op.default_method if isinstance(op, HFactorization) else "substitution"
     if n is None:
         n = op.h.n_rows if isinstance(op, HFactorization) else op.shape[0]
     return Operator(op, n, ctx, method)

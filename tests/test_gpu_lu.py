@@ -312,3 +312,25 @@ def test_row_walk_one_cta_per_subtree_equals_one_per_sm(P, monkeypatch):
                 ref = perm.from_tree(P.solve(s.factor, P.matvec(s.h_minus, perm.to_tree(ref)), method="substitution"))
             assert _rel(P.run_cn(s, u0, 3), ref) <= 1e-9
     assert _rel(outs[0], outs[1]) <= 1e-13
+
+
+def test_default_solve_builds_the_propagator_after_a_few_calls(P):
+    """hops.solve(F, b) with default arguments: the reference's substitution for the first calls,
+    then (fifth call on the same factor) the propagator is built once and used from there on;
+    every answer stays within 1e-9 of the substitution solve; auto_prepare = False keeps
+    substitution."""
+    g = cases.load("cfg1")
+    s, F, Hm = _factor(P, "cfg1", g)
+    ref = P.solve(F, g["probe"], method="substitution")
+    for k in range(6):
+        x = P.solve(F, g["probe"])
+        assert _rel(x, ref) <= 1e-9
+        assert F.propagator_ready == (k >= P.hops.AUTO_PROPAGATOR_AFTER)
+    x, log = P.gmres_restarted(s.hmatrix("plus", P.HConfig(n_min=int(g["leaf"]), eps1=float(g["eps1"]))), F,
+                               g["probe"][:, 0], tol=1e-10, restart=20, max_iter=40)
+    assert log.converged and log.iterations <= 3      # preconditioned by the prepared propagator
+    s2, F2, _ = _factor(P, "cfg1", g)
+    F2.auto_prepare = False
+    for k in range(6):
+        assert _rel(P.solve(F2, g["probe"]), ref) <= 1e-12
+    assert not F2.propagator_ready
